@@ -45,6 +45,272 @@ GMI_API const char* gmi_last_error(void);
 GMI_API int gmi_exit_code(int err);
 GMI_API int gmi_version(void);
 
+/* ------------------------------------------------------------------ layouts
+ * A GMI layout (the reference's mapping list, reduction.hpp:39-68) is passed
+ * flattened: num_gpus per-GPU lists, counts[g] ids on GPU g, ids GPU-major. */
+enum { GMI_MPR = 0, GMI_MRR = 1, GMI_HAR = 2 };
+enum { GMI_LINK_INTRA = 0, GMI_LINK_HOST_BOUNCE = 1, GMI_LINK_RING = 2, GMI_LINK_LOCAL_REDUCE = 3 };
+
+/* select_strategy (reduction.hpp:98-106), Alg. 1. */
+GMI_API int gmi_select_strategy(int num_gpus, const int* counts, const int* ids, int* strategy);
+/* leader_gmis (reduction.hpp:110-122); leaders[num_gpus]. */
+GMI_API int gmi_leader_gmis(int num_gpus, const int* counts, const int* ids, int* leaders);
+/* mrr_rings (reduction.hpp:127-139); rings[t*g] row-major, *num_rings = t.
+ * GMI_ERR_MULTISTREAM on ragged layouts or t > g. */
+GMI_API int gmi_mrr_rings(int num_gpus, const int* counts, const int* ids, int* rings, int* num_rings);
+/* predict_latency (reduction.hpp:142-152), Table 3. */
+GMI_API int gmi_predict_latency(int strategy, int g, int t, double m_p, double b1, double b2,
+                                double* latency);
+
+typedef struct {
+  int step, src, dst, kind; /* kind: GMI_LINK_* */
+  double bytes;
+} gmi_trace_event_t;
+
+typedef struct {
+  int strategy;
+  int result_holder;
+  double latency;           /* reduction phases only (== predict_latency on uniform layouts) */
+  double broadcast_latency; /* final flush to every GMI */
+  size_t trace_len;
+} gmi_reduction_info_t;
+
+/* Communication schedule of execute() (reduction.hpp:225-334) for len elements of
+ * elem_bytes (8 = the reference's fp64 buffers): trace + ideal-link latencies.
+ * Call with trace == NULL to size, then again with trace_cap >= info->trace_len. */
+GMI_API int gmi_reduction_schedule(int strategy, int num_gpus, const int* counts, const int* ids,
+                                   size_t len, double elem_bytes, double b1, double b2,
+                                   gmi_trace_event_t* trace, size_t trace_cap,
+                                   gmi_reduction_info_t* info);
+
+enum { GMI_F32 = 0, GMI_F64 = 1 };
+/* Device-backed execute(): elementwise sum of the GMIs' device buffers in exactly the
+ * reference's ring fold order (bit-identical for fp64), written to `out` (len elements)
+ * and, when broadcast != 0, to every input buffer. bufs[i] belongs to the i-th id of the
+ * flattened layout. HBM-bound kernel on `stream` (cudaStream_t). */
+GMI_API int gmi_reduce_device(int strategy, int num_gpus, const int* counts, const int* ids,
+                              void* const* bufs, void* out, size_t len, int dtype, int broadcast,
+                              void* stream);
+
+/* ------------------------------------------------------------------ topology
+ * topology.hpp:60-252. arch: 70, 80 or 100 (sm100 is a B200 extension).
+ * backend: 0 = MPS share (realised as an SM-partitioned green context), 1 = MIG. */
+typedef struct {
+  int id, arch, sm_units;
+  double mem_gb;
+} gmi_gpu_t;
+
+typedef struct {
+  int gmi_id, gpu_id, backend;
+  double sm_share, mem_gb;
+} gmi_partition_t;
+
+typedef struct {
+  const gmi_gpu_t* gpus;
+  int num_gpus;
+  const gmi_partition_t* parts;
+  int num_parts;
+  double b1, b2;
+} gmi_topology_t;
+
+typedef struct {
+  int gpu_id; /* -1 for topology-wide rules */
+  char rule[160];
+} gmi_violation_t;
+
+/* validate_layout (topology.hpp:134-212): violations are data, not failures. */
+GMI_API int gmi_validate_layout(const gmi_topology_t* topo, gmi_violation_t* out, int cap,
+                                int* count);
+/* select_backend (topology.hpp:216-222). */
+GMI_API int gmi_select_backend(int arch, int training, int* backend);
+/* path_bandwidth (topology.hpp:243-252); *bw is +inf for GMI_LINK_INTRA. */
+GMI_API int gmi_path_bandwidth(const gmi_topology_t* topo, int src_gmi, int dst_gmi, int* kind,
+                               double* bw);
+
+/* ------------------------------------------------------------------ workload
+ * workload.hpp:26-134. */
+#define GMI_MAX_DIMS 16
+typedef struct {
+  double r_sm, r_mem, t_iter;
+} gmi_role_profile_t;
+
+typedef struct {
+  char name[32];
+  double state_bytes, action_bytes, reward_bytes, model_bytes;
+  int steps_per_train;
+  double alpha, beta;
+  int num_dims;
+  int policy_dims[GMI_MAX_DIMS];
+  gmi_role_profile_t simulator, agent, trainer;
+} gmi_workload_t;
+
+GMI_API int gmi_load_benchmark(const char* name, gmi_workload_t* out);
+GMI_API int gmi_validate_workload(const gmi_workload_t* w);
+GMI_API int gmi_dense_param_count(const int* dims, int n, size_t* out);
+GMI_API int gmi_policy_value_param_count(const int* dims, int n, size_t* out);
+
+/* ------------------------------------------------------------------ placement + costs
+ * mapping.hpp:95-279. template_kind: 0 TDG, 1 TCG, 2 TDG_EX, 3 TCG_EX, 4 async_decoupled.
+ * Role masks: 1 simulator, 2 agent, 4 trainer. */
+enum { GMI_TDG = 0, GMI_TCG = 1, GMI_TDG_EX = 2, GMI_TCG_EX = 3, GMI_ASYNC = 4 };
+enum { GMI_ROLE_SIM = 1, GMI_ROLE_AGENT = 2, GMI_ROLE_TRAINER = 4 };
+
+GMI_API int gmi_serving_cost(int tpl, const gmi_workload_t* w, double* resource, double* comm);
+GMI_API int gmi_training_cost(int tpl, const gmi_workload_t* w, int n_gmis, double* resource,
+                              double* comm);
+GMI_API int gmi_allreduce_bytes(int n_gmis, double model_bytes, double* out);
+/* training != 0: training_throughput (Eq. 3), else serving_throughput (Eq. 2). */
+GMI_API int gmi_throughput(int training, double resource, double comm, const gmi_workload_t* w,
+                           double r_all, double bandwidth, double* out);
+GMI_API int gmi_throughput_ratio(int training, const gmi_workload_t* w, double combw_factor,
+                                 double* out);
+GMI_API int gmi_colocation_penalty(int training, const gmi_workload_t* w, double* out);
+
+/* build_plan (mapping.hpp:216-279). GMI ids are sequential GPU-major, so outputs are:
+ * gpu_ids[num_gpus] sorted, gmi_ids[num_gpus * gmis_per_gpu] GPU-major, role_masks
+ * indexed by gmi id, serving[num_gpus] = 1 serving / 0 training / -1 not async. */
+GMI_API int gmi_build_plan(int tpl, const gmi_topology_t* topo, int gmis_per_gpu, int* gpu_ids,
+                           int* gmi_ids, int* role_masks, int* serving);
+
+/* ------------------------------------------------------------------ adaptive GMI manager
+ * search.hpp:26-249 (Alg. 2). The probe callback is the reference's Profiler::profile
+ * (search.hpp:32-37); it returns 0 or an error code that aborts the search. */
+typedef int (*gmi_probe_fn)(void* user, const char* bench, int gmis_per_gpu, int num_env,
+                            int* runnable, double* top, double* mem);
+
+typedef struct {
+  const int* num_env_grid;
+  int grid_len;
+  int max_gmis_per_gpu;
+  double sat_threshold;
+} gmi_search_config_t;
+
+typedef struct {
+  gmi_workload_t workload;
+  double b1, b2, latency_scale;
+} gmi_estimator_t;
+
+typedef struct {
+  int gmis_per_gpu, num_env, runnable;
+  double top, mem;
+  int has_sat;
+  double sat;
+  int has_acc_top;
+  double acc_top;
+  int pruned_here;
+} gmi_visit_t;
+
+typedef struct {
+  int feasible;
+  char reason[96];
+  int num_env, gmis_per_gpu;
+  double est_throughput;
+  size_t num_visited;
+} gmi_search_result_t;
+
+GMI_API int gmi_saturation(double top, double pre_top, double mem, double pre_mem, double* out);
+GMI_API int gmi_comm_discount(const gmi_estimator_t* est, int gmis_per_gpu, int num_gpu, double* out);
+GMI_API int gmi_estimate(const gmi_estimator_t* est, int gmis_per_gpu, int num_gpu,
+                         double per_gmi_top, double* out);
+/* explore(): visits must hold max_gmis_per_gpu * grid_len entries. */
+GMI_API int gmi_explore(gmi_probe_fn probe, void* user, const gmi_estimator_t* est,
+                        const char* bench, int num_gpu, const gmi_search_config_t* cfg,
+                        gmi_search_result_t* out, gmi_visit_t* visits, size_t visits_cap);
+
+/* SyntheticCostModel (search.hpp:100-132); override tables as (key, value) pairs. */
+typedef struct {
+  double peak_top, mem_base, mem_per_env, mem_capacity, min_runnable_share;
+  int knee_base;
+  int num_knee;
+  const int* knee_keys;
+  const int* knee_values;
+  int num_cap;
+  const int* cap_keys;
+  const double* cap_values;
+} gmi_synthetic_model_t;
+GMI_API void gmi_synthetic_model_defaults(gmi_synthetic_model_t* m);
+GMI_API int gmi_synthetic_profile(const gmi_synthetic_model_t* m, const char* bench,
+                                  int gmis_per_gpu, int num_env, int* runnable, double* top,
+                                  double* mem);
+/* RecordedTraceProfiler (search.hpp:136-171). */
+GMI_API int gmi_trace_profiler_load(const char* path, void** handle);
+GMI_API int gmi_trace_profiler_profile(void* handle, const char* bench, int gmis_per_gpu,
+                                       int num_env, int* runnable, double* top, double* mem);
+GMI_API void gmi_trace_profiler_free(void* handle);
+
+/* ------------------------------------------------------------------ experience channels
+ * channels.hpp:85-397 (decoupled mode accounting). */
+typedef struct {
+  int compress_threshold;
+  int batch_mode; /* 0 slice, 1 stack */
+  int target_batch;
+  double per_message_overhead;
+  unsigned seed;
+} gmi_pipeline_config_t;
+
+typedef struct {
+  double pps, ttop;
+  long records_produced, records_delivered, units_sent, batches_emitted;
+  double bytes_moved, transfer_busy_time, delivery_makespan, training_makespan;
+  size_t num_trainers;
+} gmi_pipeline_metrics_t;
+
+/* An explicit plan: per-GPU lists (gpu_ids[num_gpus], counts, gmi_ids GPU-major) and one
+ * role mask per listed gmi id (parallel to gmi_ids). */
+typedef struct {
+  int template_kind;
+  int num_gpus;
+  const int* gpu_ids;
+  const int* counts;
+  const int* gmi_ids;
+  const int* role_masks;
+} gmi_plan_t;
+
+GMI_API void gmi_pipeline_config_defaults(gmi_pipeline_config_t* c);
+GMI_API int gmi_simulate_pipeline(const gmi_workload_t* w, const gmi_plan_t* plan,
+                                  const gmi_topology_t* topo, const gmi_pipeline_config_t* cfg,
+                                  double duration, void** handle, gmi_pipeline_metrics_t* out);
+GMI_API int gmi_pipeline_trainer_records(void* handle, int* trainers, long* records);
+GMI_API size_t gmi_pipeline_num_batches(void* handle);
+GMI_API int gmi_pipeline_batch(void* handle, size_t i, int* trainer, double* emit_time,
+                               size_t* num_records);
+GMI_API int gmi_pipeline_batch_records(void* handle, size_t i, int* agent_gmis, long* seqs);
+GMI_API void gmi_pipeline_free(void* handle);
+
+/* ------------------------------------------------------------------ config schema
+ * config.hpp:125-301; sections are evaluated lazily like the reference loaders. */
+typedef struct {
+  double serving_combw_factor, training_combw_factor;
+  int gmis_per_gpu;
+  double latency_scale;
+  gmi_pipeline_config_t pipeline;
+} gmi_model_params_t;
+
+#define GMI_MAX_GRID 32
+typedef struct {
+  int grid[GMI_MAX_GRID];
+  int grid_len;
+  int max_gmis_per_gpu;
+  double sat_threshold;
+  int has_profile_trace;
+  char profile_trace[512];
+} gmi_search_settings_t;
+
+GMI_API int gmi_config_parse(const char* text, const char* origin, void** handle);
+GMI_API int gmi_config_load(const char* path, void** handle);
+GMI_API int gmi_config_has(void* handle, const char* section, int* out);
+/* Sizes first: call with caps of 0 to read *num_gpus / *num_parts. */
+GMI_API int gmi_config_topology(void* handle, gmi_gpu_t* gpus, int gpu_cap, int* num_gpus,
+                                gmi_partition_t* parts, int part_cap, int* num_parts, double* b1,
+                                double* b2);
+GMI_API int gmi_config_workload(void* handle, const char* fallback, gmi_workload_t* out);
+GMI_API int gmi_config_model(void* handle, gmi_model_params_t* out);
+GMI_API int gmi_config_search(void* handle, gmi_search_settings_t* out);
+/* Raw value lookup (any section, incl. B200 extensions such as [ppo]); *found = 0/1. */
+GMI_API int gmi_config_get(void* handle, const char* section, const char* key, char* value,
+                           size_t cap, int* found);
+GMI_API void gmi_config_free(void* handle);
+
 /* ------------------------------------------------------------------ diagnostics
  * Single tcgen05 GEMM launch, D[m][n] = sum_k A(m,k) B(n,k), bf16 in, fp32 accumulate.
  * a_mn/b_mn: 0 = operand stored [rows x K], 1 = stored [K x rows].
