@@ -311,6 +311,68 @@ GMI_API int gmi_config_get(void* handle, const char* section, const char* key, c
                            size_t cap, int* found);
 GMI_API void gmi_config_free(void* handle);
 
+/* ------------------------------------------------------------------ PPO iteration (B200)
+ * The data-parallel TCG_EX training iteration (holistic GMIs: simulator + agent + trainer,
+ * mapping.hpp:246-249) that the reference models only as T_s + T_a + T_t + COM/BW
+ * (mapping.hpp:123-128, workload.hpp:43-45). One trainer drives one GPU (`rank` of
+ * `num_gpus`) with `gmis_per_gpu` GMIs; envs are split over the job's GMIs by
+ * [N*c/n, N*(c+1)/n) (reduction.hpp:164-166). Gradients are reduced per minibatch:
+ * K1 fold across the GPU's GMIs, then NCCL across GPUs; Adam runs once per GPU on the
+ * shared replica. Semantics: DESIGN.md §PPO (mirrored by oracle/ppo_oracle.c). */
+#define GMI_MAX_HIDDEN 8
+typedef struct {
+  int obs_dim, act_dim;
+  int num_hidden;
+  int hidden[GMI_MAX_HIDDEN];
+  int num_envs; /* whole job */
+  int horizon, epochs, minibatches;
+  float gamma, lam, clip, lr, beta1, beta2, adam_eps, vf_coef, ent_coef;
+  unsigned long long seed;
+  int num_gpus, gmis_per_gpu; /* job layout (GPU-major GMI ids) */
+  int rank;                   /* GPU index of this trainer within the job */
+  int device;                 /* CUDA device ordinal */
+  int gmi_backend;            /* 0: one CUDA stream per GMI; 1: SM-partitioned green contexts */
+  int sm_per_gmi;             /* green-context SMs per GMI (multiple of 8; 0 = even split) */
+  int use_graph;              /* capture the update phase in a CUDA graph */
+  int instrument;             /* time GEMM launches with CUDA events (roofline) */
+} gmi_ppo_config_t;
+
+typedef struct {
+  double policy_loss, value_loss, approx_kl, clip_frac; /* last minibatch of GMI 0 */
+  double mean_reward;                                   /* rollout mean of GMI 0 */
+  long long env_steps;                                  /* this GPU, this iteration */
+  double gemm_ms;   /* instrument: summed GEMM time this iteration (GMI 0 stream) */
+  double gemm_flop; /* instrument: algorithmic GEMM flops of those launches */
+  int gemm_launches;
+  int kernel_launches; /* every libgmi kernel launched this iteration (this GPU) */
+} gmi_ppo_stats_t;
+
+GMI_API void gmi_ppo_config_defaults(gmi_ppo_config_t* cfg);
+/* nccl_id: 128-byte ncclUniqueId shared by all ranks (NULL when num_gpus == 1). */
+GMI_API int gmi_ppo_create(const gmi_ppo_config_t* cfg, const void* nccl_id, void** trainer);
+GMI_API void gmi_ppo_free(void* trainer);
+GMI_API int gmi_nccl_unique_id(void* out128);
+/* One PPO iteration: rollout (horizon steps), values, GAE, epochs x minibatches of
+ * forward / loss / backward / gradient reduction / Adam. Blocks until done; stats may be NULL. */
+GMI_API int gmi_ppo_iteration(void* trainer, gmi_ppo_stats_t* stats);
+/* Asynchronous variant: enqueue one iteration on the trainer's streams, no host sync. */
+GMI_API int gmi_ppo_iteration_async(void* trainer);
+GMI_API int gmi_ppo_synchronize(void* trainer, gmi_ppo_stats_t* stats);
+/* Rollout + values + GAE of the next iteration only (parity checks). */
+GMI_API int gmi_ppo_rollout(void* trainer);
+/* One minibatch gradient of local GMI `gmi` on caller rows (host fp32; B = minibatch size). */
+GMI_API int gmi_ppo_minibatch_grad(void* trainer, int gmi, const float* X, const float* act,
+                                   const float* oldlp, const float* adv, const float* ret, int B,
+                                   float* grad_out);
+/* Host copies of device state. what: params adam_m adam_v (shared) | grad x obs act logp rew
+ * val adv ret done ep_step ep_len ep_count (per local GMI). Returns the element count via *n
+ * when dst is NULL. */
+GMI_API int gmi_ppo_get(void* trainer, const char* what, int gmi, void* dst, long long* n);
+GMI_API int gmi_ppo_set(void* trainer, const char* what, int gmi, const void* src, long long n);
+GMI_API int gmi_ppo_param_count(void* trainer, long long* padded, long long* real);
+/* cudaStream_t of local GMI `gmi` (-1: the update / reduction stream). */
+GMI_API int gmi_ppo_stream(void* trainer, int gmi, void** stream);
+
 /* ------------------------------------------------------------------ diagnostics
  * Single tcgen05 GEMM launch, D[m][n] = sum_k A(m,k) B(n,k), bf16 in, fp32 accumulate.
  * a_mn/b_mn: 0 = operand stored [rows x K], 1 = stored [K x rows].

@@ -20,33 +20,10 @@
 #include <cuda.h>
 #include <cuda_bf16.h>
 
+#include "gemm_types.hpp"
 #include "ptx.cuh"
 
 namespace gmi {
-
-enum GemmEpi : int { EPI_BIAS_ELU = 0, EPI_DACT = 1, EPI_F32 = 2 };
-
-constexpr int kGemmBlockM = 128;
-constexpr int kGemmBlockK = 64;  // one 128-byte swizzle atom of bf16
-
-struct alignas(64) GemmProblem {
-  CUtensorMap map_a;
-  CUtensorMap map_b;
-  void* out;
-  const float* bias;
-  const __nv_bfloat16* aux;
-  int64_t ld_out;
-  int64_t ld_aux;
-  int64_t split_stride;  // elements between split-K output slabs (EPI_F32)
-  int M, N, K;
-  int kb_per_split;
-};
-
-struct alignas(64) GemmParams {
-  GemmProblem prob[2];
-  int num_problems;
-  int splits;
-};
 
 __device__ __forceinline__ float elu_f(float x) { return x > 0.f ? x : expm1f(x); }
 
@@ -116,16 +93,16 @@ __global__ void __launch_bounds__(128, 1) gemm_tcgen05_kernel(const __grid_const
         if constexpr (A_MN) {
 #pragma unroll
           for (int j = 0; j < kGemmBlockM / 64; ++j)
-            ptx::tma_load_2d(sa + j * 8192, &pr.map_a, &full_bar[s], m0 + 64 * j, k0);
+            ptx::tma_load_2d(sa + j * 8192, &pr.map_a, &full_bar[s], m0 + 64 * j, k0 + pr.a_row0);
         } else {
-          ptx::tma_load_2d(sa, &pr.map_a, &full_bar[s], k0, m0);
+          ptx::tma_load_2d(sa, &pr.map_a, &full_bar[s], k0, m0 + pr.a_row0);
         }
         if constexpr (B_MN) {
 #pragma unroll
           for (int j = 0; j < BLOCK_N / 64; ++j)
-            ptx::tma_load_2d(sb + j * 8192, &pr.map_b, &full_bar[s], n0 + 64 * j, k0);
+            ptx::tma_load_2d(sb + j * 8192, &pr.map_b, &full_bar[s], n0 + 64 * j, k0 + pr.b_row0);
         } else {
-          ptx::tma_load_2d(sb, &pr.map_b, &full_bar[s], k0, n0);
+          ptx::tma_load_2d(sb, &pr.map_b, &full_bar[s], k0, n0 + pr.b_row0);
         }
       }
     } else if (warp == 1 && lane == 0) {

@@ -6,7 +6,7 @@
 
 #include <cstdint>
 
-#include "gemm.cuh"
+#include "gemm_types.hpp"
 
 namespace gmi {
 

@@ -1,0 +1,122 @@
+// Device-side interface of the PPO iteration kernels (K3-K8 of SURVEY §2.2) and their
+// host launch wrappers. Layouts (per GMI, N envs, horizon T, padded obs width S_p):
+//   env state   x[N][S] fp32, ep_step/ep_len/ep_count[N] int32
+//   rollout     X_roll[(T+1)][N][S_p] bf16 (GEMM-ready observations, pads stay 0),
+//               act[T][N][A], logp/rew[T][N] fp32, done[T][N] u8, V[(T+1)][N] fp32
+//   advantages  adv/ret[T][N] fp32, normalised in the epoch shuffle
+//   epoch copy  X_sh[B][S_p] bf16, act_sh[B][A], oldlp/adv/ret_sh[B]  (B = T*N, permuted)
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace gmi::ppo {
+
+constexpr int kMaxAct = 32;
+
+// Device-resident control block, refreshed by the host (H2D) once per iteration.
+struct Control {
+  int iteration;
+  int pad_;
+  long long adam_step0;  // Adam steps completed before this iteration
+};
+
+struct EnvParams {
+  int N, S, A, S_p;
+  int env0;  // global id of env 0 of this GMI
+  int T;
+  uint64_t seed;
+};
+
+struct ActEnvArgs {
+  EnvParams ep;
+  const __nv_bfloat16* H;  // [N][hp] last policy hidden layer
+  int hp;
+  const float* w_mu;  // [A][hp]
+  const float* b_mu;  // [A]
+  const float* log_std;
+  float* x;
+  int* ep_step;
+  const int* ep_len;
+  int* ep_count;
+  __nv_bfloat16* X_next;  // X_roll + (t+1)*N*S_p
+  float* act;             // act + t*N*A
+  float* logp;            // + t*N
+  float* rew;
+  uint8_t* done;
+  int t;
+  const Control* ctl;
+};
+
+struct HeadLossArgs {
+  const __nv_bfloat16* Hpi;  // [B][hp]
+  const __nv_bfloat16* Hv;
+  int hp;
+  const float* w_mu;
+  const float* b_mu;
+  const float* w_v;
+  const float* b_v;
+  const float* log_std;
+  const float* act;  // [B][A]
+  const float* oldlp;
+  const float* adv;
+  const float* ret;
+  __nv_bfloat16* Dpi;  // [B][hp] dPre of the last hidden layer
+  __nv_bfloat16* Dv;
+  float* partial;      // [blocks][partial_stride]
+  int partial_stride;
+  int B, A;
+  float clip, vf_coef, ent_coef;
+};
+
+// Sizes of one head-loss partial record.
+inline int head_partial_stride(int A, int hp) { return A * hp + hp + A + 1 + A + 4; }
+constexpr int kHeadRowsPerBlock = 128;
+
+struct Segment {  // dst[i] = sum_{p < nparts} src[p * stride + i]  (fixed order)
+  float* dst;
+  const float* src;
+  long long stride;
+  int len;
+  int nparts;
+};
+
+struct AdamArgs {
+  float* p;
+  float* m;
+  float* v;
+  __nv_bfloat16* shadow;
+  const float* g;
+  const float* bc;  // [2*steps] bias-correction table: 1-b1^s, 1-b2^s for s = 1..
+  const Control* ctl;
+  int step_in_iter;  // 0-based minibatch update index inside the iteration
+  long long n;
+  float lr, b1, b2, eps, inv_n;
+};
+
+void launch_env_init(const EnvParams& ep, float* x, int* ep_step, int* ep_len, int* ep_count,
+                     __nv_bfloat16* X0, cudaStream_t s);
+void launch_act_env(const ActEnvArgs& a, cudaStream_t s);
+void launch_value_head(const __nv_bfloat16* H, int hp, const float* w, const float* b, float* out,
+                       int rows, cudaStream_t s);
+void launch_gae(const float* rew, const uint8_t* done, const float* V, float* adv, float* ret,
+                double* partials, int N, int T, float gamma, float lam, cudaStream_t s);
+int gae_blocks(int N);
+void launch_adv_stats(const double* partials, int nparts, long long count, float* stats,
+                      cudaStream_t s);
+void launch_shuffle(const __nv_bfloat16* X_roll, const float* act, const float* logp,
+                    const float* adv, const float* ret, const float* adv_stats, __nv_bfloat16* X_sh,
+                    float* act_sh, float* oldlp_sh, float* adv_sh, float* ret_sh, int N, int T,
+                    int S_p, int A, uint64_t seed, int gmi_gid, int epoch, const Control* ctl,
+                    cudaStream_t s);
+void launch_head_loss(const HeadLossArgs& a, cudaStream_t s);
+int head_loss_blocks(int B);
+void launch_colsum(const __nv_bfloat16* const* D, const int* widths, float* const* partial,
+                   int nproblems, int rows, cudaStream_t s);
+int colsum_blocks(int rows);
+void launch_segments(const Segment* segs, int nsegs, cudaStream_t s);
+void launch_adam(const AdamArgs& a, cudaStream_t s);
+
+}  // namespace gmi::ppo

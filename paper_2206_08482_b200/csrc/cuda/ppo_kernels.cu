@@ -1,0 +1,658 @@
+// PPO iteration kernels for sm_100a (non-GEMM parts; the hidden-layer GEMMs are the
+// tcgen05 kernels in gemm.cuh). All of these are HBM- or latency-bound elementwise /
+// reduction kernels; the dominant traffic per kernel is noted beside it.
+//
+// Numerics follow oracle/ppo_oracle.c: every fp32 expression that the oracle evaluates
+// with -ffp-contract=off is evaluated here with explicit _rn intrinsics (no FMA
+// contraction) wherever bit-equality is attainable (env resets, Adam); transcendentals
+// (tanhf/sinf/expf/logf) and reduction orders differ by ulps.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "../host/errors.hpp"
+#include "ppo.cuh"
+#include "rng.cuh"
+
+namespace gmi::ppo {
+
+namespace {
+
+constexpr float kDt = 0.05f, kDamp = 1.0f, kCouple = 0.1f, kCtrl = 0.1f, kStateC = 0.1f;
+constexpr float kLog2PiHalf = 0.91893853320467274f;
+constexpr float kTwoPi = 6.28318530717958648f;
+constexpr int kMaxObsPerLane = 8;  // S <= 256
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ float elu_grad(float h) { return h > 0.f ? 1.f : h + 1.f; }
+
+__device__ __forceinline__ void load8(const __nv_bfloat16* p, float (&f)[8]) {
+  const uint4 u = *reinterpret_cast<const uint4*>(p);
+  const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const __nv_bfloat162 b = *reinterpret_cast<const __nv_bfloat162*>(&w[i]);
+    f[2 * i] = __bfloat162float(b.x);
+    f[2 * i + 1] = __bfloat162float(b.y);
+  }
+}
+
+__device__ __forceinline__ void store8(__nv_bfloat16* p, const float (&f)[8]) {
+  uint32_t w[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    __nv_bfloat162 b = __floats2bfloat162_rn(f[2 * i], f[2 * i + 1]);
+    w[i] = *reinterpret_cast<uint32_t*>(&b);
+  }
+  *reinterpret_cast<uint4*>(p) = make_uint4(w[0], w[1], w[2], w[3]);
+}
+
+// Reset state x[0..S) of env `gid` for episode `count`: U(-0.1, 0.1), bit-exact vs oracle.
+__device__ __forceinline__ float reset_value(uint64_t seed, int gid, int count, int i) {
+  uint32_t r[4];
+  rng::draw(seed, uint32_t(gid), uint32_t(count), uint32_t(i / 4), rng::kReset, r);
+  return __fsub_rn(__fmul_rn(rng::u01(r[i & 3]), 0.2f), 0.1f);
+}
+
+// ------------------------------------------------------------------ env init
+__global__ void env_init_kernel(EnvParams ep, float* x, int* ep_step, int* ep_len, int* ep_count,
+                                __nv_bfloat16* X0) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= ep.N) return;
+  const int gid = ep.env0 + e;
+  uint32_t r[4];
+  rng::draw(ep.seed, uint32_t(gid), 0u, 0u, rng::kEpisode, r);
+  const int len = 16 + int(r[0] % 48u);
+  ep_len[e] = len;
+  ep_step[e] = int(r[1] % uint32_t(len));
+  ep_count[e] = 0;
+  for (int i = 0; i < ep.S; ++i) {
+    const float v = reset_value(ep.seed, gid, 0, i);
+    x[(long long)e * ep.S + i] = v;
+    X0[(long long)e * ep.S_p + i] = __float2bfloat16_rn(v);
+  }
+}
+
+// ------------------------------------------------------------------ K3+K4 head: act + env step
+// One warp per env: policy head (mu = H_L W_mu^T + b), Gaussian sample, log-prob, clipped
+// actions, synthetic Ant-like dynamics, reward, integer episode clock / reset, and the
+// next GEMM-ready observation row. Traffic/env: H_L row (2*hp B) + 2*S*4 (state) + 2*S_p
+// (obs) + (A+3)*4 B.
+template <int MAXA>
+__global__ void __launch_bounds__(256) act_env_kernel(const ActEnvArgs a) {
+  const int lane = threadIdx.x & 31;
+  const int e = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const EnvParams& ep = a.ep;
+  if (e >= ep.N) return;
+  const int A = ep.A, S = ep.S;
+  const int gid = ep.env0 + e;
+
+  // mu: lanes split the hidden dimension in 8-wide chunks
+  float part[MAXA];
+#pragma unroll
+  for (int i = 0; i < MAXA; ++i) part[i] = 0.f;
+  const __nv_bfloat16* hrow = a.H + (long long)e * a.hp;
+  for (int k = lane * 8; k < a.hp; k += 256) {
+    float h[8];
+    load8(hrow + k, h);
+#pragma unroll
+    for (int i = 0; i < MAXA; ++i) {
+      if (i < A) {
+        const float* w = a.w_mu + (long long)i * a.hp + k;
+        float s = part[i];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) s += h[j] * w[j];
+        part[i] = s;
+      }
+    }
+  }
+  float mu_mine = 0.f;
+#pragma unroll
+  for (int i = 0; i < MAXA; ++i) {
+    if (i < A) {
+      const float m = warp_sum(part[i]) + a.b_mu[i];
+      if (i == lane) mu_mine = m;
+    }
+  }
+
+  // N(0,1) noise: lane q draws Philox block q -> 4 normals for actions 4q..4q+3
+  const uint32_t step = uint32_t(a.ctl->iteration * ep.T + a.t);
+  float nrm[4] = {0.f, 0.f, 0.f, 0.f};
+  if (lane * 4 < A) {
+    uint32_t r[4];
+    rng::draw(ep.seed, uint32_t(gid), step, uint32_t(lane), rng::kNoise, r);
+#pragma unroll
+    for (int p = 0; p < 2; ++p) {
+      const float rad = sqrtf(-2.0f * logf(rng::u01_open0(r[2 * p])));
+      const float th = kTwoPi * rng::u01(r[2 * p + 1]);
+      nrm[2 * p] = rad * cosf(th);
+      nrm[2 * p + 1] = rad * sinf(th);
+    }
+  }
+  float got[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) got[j] = __shfl_sync(0xffffffffu, nrm[j], (lane >> 2) & 31);
+  const float eps = (lane & 3) == 0 ? got[0] : (lane & 3) == 1 ? got[1] : (lane & 3) == 2 ? got[2] : got[3];
+
+  float act = 0.f, lp_term = 0.f, u = 0.f;
+  if (lane < A) {
+    const float ls = a.log_std[lane];
+    const float sig = expf(ls);
+    act = mu_mine + sig * eps;
+    const float z = (act - mu_mine) / sig;
+    lp_term = -0.5f * z * z - ls - kLog2PiHalf;
+    u = fminf(fmaxf(act, -1.f), 1.f);
+    a.act[(long long)e * A + lane] = act;
+  }
+  const float logp = warp_sum(lp_term);
+  const float usq = warp_sum(u * u);
+
+  // dynamics: lane owns dims i = lane + 32 j
+  float* xe = a.x + (long long)e * S;
+  float xn[kMaxObsPerLane];
+  float xsq_part = 0.f;
+#pragma unroll
+  for (int j = 0; j < kMaxObsPerLane; ++j) {
+    const int i = lane + 32 * j;
+    const int src = i < S ? i % A : 0;
+    const float drive = tanhf(__shfl_sync(0xffffffffu, u, src));
+    if (i < S) {
+      const float xi = xe[i];
+      const float nb = xe[i + 1 < S ? i + 1 : 0];
+      const float inner = __fadd_rn(__fsub_rn(drive, __fmul_rn(kDamp, xi)), __fmul_rn(kCouple, sinf(nb)));
+      xn[j] = __fadd_rn(xi, __fmul_rn(kDt, inner));
+      xsq_part = __fadd_rn(xsq_part, __fmul_rn(xn[j], xn[j]));
+    } else {
+      xn[j] = 0.f;
+    }
+  }
+  const float xsq = warp_sum(xsq_part);
+  const float xn0 = __shfl_sync(0xffffffffu, xn[0], 0);
+  const int st = a.ep_step[e];
+  const bool done = st + 1 >= a.ep_len[e];
+  const int count = a.ep_count[e] + (done ? 1 : 0);
+  __syncwarp();
+  __nv_bfloat16* xo = a.X_next + (long long)e * ep.S_p;
+#pragma unroll
+  for (int j = 0; j < kMaxObsPerLane; ++j) {
+    const int i = lane + 32 * j;
+    if (i < S) {
+      const float v = done ? reset_value(ep.seed, gid, count, i) : xn[j];
+      xe[i] = v;
+      xo[i] = __float2bfloat16_rn(v);
+    }
+  }
+  if (lane == 0) {
+    const float r0 = __fsub_rn(__fadd_rn(1.0f, xn0), __fdiv_rn(__fmul_rn(kCtrl, usq), float(A)));
+    a.rew[e] = __fsub_rn(r0, __fdiv_rn(__fmul_rn(kStateC, xsq), float(S)));
+    a.logp[e] = logp;
+    a.done[e] = done ? 1 : 0;
+    a.ep_step[e] = done ? 0 : st + 1;
+    a.ep_count[e] = count;
+  }
+}
+
+// ------------------------------------------------------------------ value head
+__global__ void __launch_bounds__(256) value_head_kernel(const __nv_bfloat16* H, int hp, const float* w,
+                                                         const float* b, float* out, int rows) {
+  const int lane = threadIdx.x & 31;
+  const long long r = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (r >= rows) return;
+  float s = 0.f;
+  for (int k = lane * 8; k < hp; k += 256) {
+    float h[8];
+    load8(H + r * hp + k, h);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) s += h[j] * w[k + j];
+  }
+  s = warp_sum(s);
+  if (lane == 0) out[r] = s + b[0];
+}
+
+// ------------------------------------------------------------------ K5 GAE
+// Block = 32 envs x 32 steps. Tiles are staged through shared memory so HBM access is
+// coalesced along envs; each warp then owns one env with lane = time step and runs the
+// reverse affine recurrence A_t = d_t + c_t A_{t+1} as a 5-step shuffle scan.
+__global__ void __launch_bounds__(1024) gae_kernel(const float* rew, const uint8_t* done, const float* V,
+                                                   float* adv, float* ret, double* partials, int N, int T,
+                                                   float gamma, float gl) {
+  __shared__ float r_s[32][33], v_s[33][33], a_s[32][33], q_s[32][33];
+  __shared__ unsigned char d_s[32][33];
+  __shared__ double red[3][32];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int e0 = blockIdx.x * 32;
+  const int e = e0 + tx;
+  const bool ok = e < N;
+  if (ty < T) {
+    r_s[ty][tx] = ok ? rew[(long long)ty * N + e] : 0.f;
+    d_s[ty][tx] = ok ? done[(long long)ty * N + e] : 1;
+  }
+  if (ty <= T) v_s[ty][tx] = ok ? V[(long long)ty * N + e] : 0.f;
+  if (ty == 0 && T == 32) v_s[32][tx] = ok ? V[(long long)32 * N + e] : 0.f;
+  __syncthreads();
+
+  // warp ty -> env column ty, lane tx -> time step
+  const int t = tx;
+  float delta = 0.f, c = 0.f;
+  if (t < T) {
+    const float nonterm = d_s[t][ty] ? 0.f : 1.f;
+    delta = __fsub_rn(__fadd_rn(r_s[t][ty], __fmul_rn(__fmul_rn(gamma, v_s[t + 1][ty]), nonterm)), v_s[t][ty]);
+    c = __fmul_rn(gl, nonterm);
+  }
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const float d2 = __shfl_down_sync(0xffffffffu, delta, o);
+    const float c2 = __shfl_down_sync(0xffffffffu, c, o);
+    if (t + o < 32) {
+      delta = __fadd_rn(delta, __fmul_rn(c, d2));
+      c = __fmul_rn(c, c2);
+    }
+  }
+  if (t < T) {
+    a_s[t][ty] = delta;
+    q_s[t][ty] = __fadd_rn(delta, v_s[t][ty]);
+  }
+  __syncthreads();
+  double s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  if (ty < T && ok) {
+    const float av = a_s[ty][tx];
+    adv[(long long)ty * N + e] = av;
+    ret[(long long)ty * N + e] = q_s[ty][tx];
+    s1 = av;
+    s2 = double(av) * double(av);
+    s3 = r_s[ty][tx];
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+    s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+    s3 += __shfl_xor_sync(0xffffffffu, s3, o);
+  }
+  if (tx == 0) {
+    red[0][ty] = s1;
+    red[1][ty] = s2;
+    red[2][ty] = s3;
+  }
+  __syncthreads();
+  if (ty == 0) {
+    double a1 = red[0][tx], a2 = red[1][tx], a3 = red[2][tx];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      a1 += __shfl_xor_sync(0xffffffffu, a1, o);
+      a2 += __shfl_xor_sync(0xffffffffu, a2, o);
+      a3 += __shfl_xor_sync(0xffffffffu, a3, o);
+    }
+    if (tx == 0) {
+      partials[3 * blockIdx.x] = a1;
+      partials[3 * blockIdx.x + 1] = a2;
+      partials[3 * blockIdx.x + 2] = a3;
+    }
+  }
+}
+
+__global__ void adv_stats_kernel(const double* partials, int nparts, long long count, float* stats) {
+  __shared__ double sh[3][256];
+  double s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  for (int i = threadIdx.x; i < nparts; i += blockDim.x) {
+    s1 += partials[3 * i];
+    s2 += partials[3 * i + 1];
+    s3 += partials[3 * i + 2];
+  }
+  sh[0][threadIdx.x] = s1;
+  sh[1][threadIdx.x] = s2;
+  sh[2][threadIdx.x] = s3;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o)
+      for (int q = 0; q < 3; ++q) sh[q][threadIdx.x] += sh[q][threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const double mean = sh[0][0] / double(count);
+    double var = count > 1 ? (sh[1][0] - sh[0][0] * mean) / double(count - 1) : 0.0;
+    if (var < 0) var = 0;
+    stats[0] = float(mean);
+    stats[1] = float(sqrt(var) + 1e-8);
+    stats[2] = float(sh[2][0] / double(count));
+  }
+}
+
+// ------------------------------------------------------------------ epoch shuffle
+// Row j of the epoch copy is sample perm(j); 16-byte chunks of the bf16 obs row per thread.
+__global__ void __launch_bounds__(256) shuffle_kernel(const __nv_bfloat16* X_roll, const float* act,
+                                                      const float* logp, const float* adv, const float* ret,
+                                                      const float* stats, __nv_bfloat16* X_sh, float* act_sh,
+                                                      float* oldlp_sh, float* adv_sh, float* ret_sh, int N, int T,
+                                                      int S_p, int A, uint64_t seed, int gmi_gid, int epoch,
+                                                      const Control* ctl) {
+  const int cpr = S_p / 8;  // 16-byte chunks per row
+  const long long B = (long long)T * N;
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= B * cpr) return;
+  const long long j = idx / cpr;
+  const int c = int(idx % cpr);
+  uint32_t keys[4];
+  rng::draw(seed, uint32_t(gmi_gid), uint32_t(ctl->iteration), uint32_t(epoch), rng::kPerm, keys);
+  const long long src = rng::perm_index(uint32_t(j), uint32_t(B), keys);
+  reinterpret_cast<uint4*>(X_sh + j * S_p)[c] = reinterpret_cast<const uint4*>(X_roll + src * S_p)[c];
+  if (c == 0) {
+    for (int i = 0; i < A; ++i) act_sh[j * A + i] = act[src * A + i];
+    oldlp_sh[j] = logp[src];
+    adv_sh[j] = __fdiv_rn(__fsub_rn(adv[src], stats[0]), stats[1]);
+    ret_sh[j] = ret[src];
+  }
+}
+
+// ------------------------------------------------------------------ K6 head + PPO loss (+ head backward)
+template <int MAXA>
+__global__ void __launch_bounds__(256) head_loss_kernel(const HeadLossArgs a) {
+  __shared__ float gmu_s[kHeadRowsPerBlock][MAXA + 1];
+  __shared__ float gv_s[kHeadRowsPerBlock];
+  __shared__ float red_s[8][MAXA + 4];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int A = a.A, hp = a.hp;
+  const int r0 = blockIdx.x * kHeadRowsPerBlock;
+  const float invB = 1.0f / float(a.B);
+
+  float gls_acc = 0.f;  // lane a: sum over this warp's rows of dL/dlog_std_a
+  float st_pi = 0.f, st_v = 0.f, st_kl = 0.f, st_clip = 0.f;
+  const float ls_mine = lane < A ? a.log_std[lane] : 0.f;
+  const float sig_mine = expf(ls_mine);
+
+  for (int rr = warp; rr < kHeadRowsPerBlock; rr += 8) {
+    const int r = r0 + rr;
+    if (r >= a.B) {
+      if (lane < MAXA + 1 && lane <= A) gmu_s[rr][lane < A ? lane : MAXA] = 0.f;
+      if (lane == 0) gv_s[rr] = 0.f;
+      continue;
+    }
+    float part[MAXA];
+#pragma unroll
+    for (int i = 0; i < MAXA; ++i) part[i] = 0.f;
+    float pv = 0.f;
+    for (int k = lane * 8; k < hp; k += 256) {
+      float h[8], hv[8];
+      load8(a.Hpi + (long long)r * hp + k, h);
+      load8(a.Hv + (long long)r * hp + k, hv);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) pv += hv[j] * a.w_v[k + j];
+#pragma unroll
+      for (int i = 0; i < MAXA; ++i)
+        if (i < A) {
+          const float* w = a.w_mu + (long long)i * hp + k;
+          float s = part[i];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) s += h[j] * w[j];
+          part[i] = s;
+        }
+    }
+    float mu_mine = 0.f;
+#pragma unroll
+    for (int i = 0; i < MAXA; ++i)
+      if (i < A) {
+        const float m = warp_sum(part[i]) + a.b_mu[i];
+        if (i == lane) mu_mine = m;
+      }
+    const float v = warp_sum(pv) + a.b_v[0];
+    float z = 0.f, term = 0.f;
+    if (lane < A) {
+      z = (a.act[(long long)r * A + lane] - mu_mine) / sig_mine;
+      term = -0.5f * z * z - ls_mine - kLog2PiHalf;
+    }
+    const float lp = warp_sum(term);
+    const float oldlp = a.oldlp[r], adv = a.adv[r];
+    const float ratio = expf(lp - oldlp);
+    const float s1 = ratio * adv;
+    const float rc = fminf(fmaxf(ratio, 1.f - a.clip), 1.f + a.clip);
+    const float s2 = rc * adv;
+    const bool take1 = s1 <= s2;
+    const float glp = take1 ? -s1 * invB : 0.f;
+    const float verr = v - a.ret[r];
+    const float gv = a.vf_coef * verr * invB;
+    float gmu = 0.f;
+    if (lane < A) {
+      gmu = glp * z / sig_mine;
+      gls_acc += glp * (z * z - 1.f) - a.ent_coef * invB;
+      gmu_s[rr][lane] = gmu;
+    }
+    if (lane == 0) {
+      gv_s[rr] = gv;
+      st_pi += -(take1 ? s1 : s2);
+      st_v += 0.5f * a.vf_coef * verr * verr;
+      st_kl += oldlp - lp;
+      st_clip += (ratio < 1.f - a.clip || ratio > 1.f + a.clip) ? 1.f : 0.f;
+    }
+    // head backward into the last hidden layer: dPre = (g W) * elu'(H), stored bf16
+    float g_all[MAXA];
+#pragma unroll
+    for (int i = 0; i < MAXA; ++i) g_all[i] = i < A ? __shfl_sync(0xffffffffu, gmu, i) : 0.f;
+    for (int k = lane * 8; k < hp; k += 256) {
+      float h[8], hv[8], dp[8], dv[8];
+      load8(a.Hpi + (long long)r * hp + k, h);
+      load8(a.Hv + (long long)r * hp + k, hv);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        float acc = 0.f;
+#pragma unroll
+        for (int i = 0; i < MAXA; ++i)
+          if (i < A) acc += g_all[i] * a.w_mu[(long long)i * hp + k + j];
+        dp[j] = acc * elu_grad(h[j]);
+        dv[j] = (gv * a.w_v[k + j]) * elu_grad(hv[j]);
+      }
+      store8(a.Dpi + (long long)r * hp + k, dp);
+      store8(a.Dv + (long long)r * hp + k, dv);
+    }
+  }
+  if (lane < A) red_s[warp][lane] = gls_acc;
+  if (lane == 0) {
+    red_s[warp][MAXA] = st_pi;
+    red_s[warp][MAXA + 1] = st_v;
+    red_s[warp][MAXA + 2] = st_kl;
+    red_s[warp][MAXA + 3] = st_clip;
+  }
+  __syncthreads();
+
+  // block partials of the head weight gradients (rows of this block), fixed order
+  float* out = a.partial + (long long)blockIdx.x * a.partial_stride;
+  const int rows = min(kHeadRowsPerBlock, a.B - r0);
+  for (int k = threadIdx.x; k < hp; k += blockDim.x) {
+    float acc[MAXA];
+#pragma unroll
+    for (int i = 0; i < MAXA; ++i) acc[i] = 0.f;
+    float accv = 0.f;
+    for (int rr = 0; rr < rows; ++rr) {
+      const float h = __bfloat162float(a.Hpi[(long long)(r0 + rr) * hp + k]);
+      const float hv = __bfloat162float(a.Hv[(long long)(r0 + rr) * hp + k]);
+#pragma unroll
+      for (int i = 0; i < MAXA; ++i)
+        if (i < A) acc[i] += gmu_s[rr][i] * h;
+      accv += gv_s[rr] * hv;
+    }
+#pragma unroll
+    for (int i = 0; i < MAXA; ++i)
+      if (i < A) out[(long long)i * hp + k] = acc[i];
+    out[(long long)A * hp + k] = accv;
+  }
+  float* tail = out + (long long)A * hp + hp;
+  if (threadIdx.x < A) {
+    float s = 0.f;
+    for (int rr = 0; rr < rows; ++rr) s += gmu_s[rr][threadIdx.x];
+    tail[threadIdx.x] = s;
+    float l = 0.f;
+    for (int w = 0; w < 8; ++w) l += red_s[w][threadIdx.x];
+    tail[A + 1 + threadIdx.x] = l;
+  } else if (threadIdx.x == 32) {
+    float s = 0.f;
+    for (int rr = 0; rr < rows; ++rr) s += gv_s[rr];
+    tail[A] = s;
+  } else if (threadIdx.x >= 64 && threadIdx.x < 68) {
+    float s = 0.f;
+    for (int w = 0; w < 8; ++w) s += red_s[w][MAXA + (threadIdx.x - 64)];
+    tail[2 * A + 1 + (threadIdx.x - 64)] = s;
+  }
+}
+
+// ------------------------------------------------------------------ bias-gradient column sums
+constexpr int kColsumRows = 256;
+struct ColsumArgs {
+  const __nv_bfloat16* D[16];
+  float* out[16];
+  int width[16];
+};
+__global__ void __launch_bounds__(256) colsum_kernel(const ColsumArgs a, int rows) {
+  const int p = blockIdx.y;
+  const int w = a.width[p];
+  const int r0 = blockIdx.x * kColsumRows;
+  const int r1 = min(rows, r0 + kColsumRows);
+  for (int j = threadIdx.x; j < w; j += blockDim.x) {
+    float s = 0.f;
+    for (int r = r0; r < r1; ++r) s += __bfloat162float(a.D[p][(long long)r * w + j]);
+    a.out[p][(long long)blockIdx.x * w + j] = s;
+  }
+}
+
+// ------------------------------------------------------------------ gradient assembly
+constexpr int kMaxSegments = 64;
+struct SegmentTable {
+  Segment s[kMaxSegments];
+};
+__global__ void __launch_bounds__(256) segments_kernel(const __grid_constant__ SegmentTable t) {
+  const Segment& sg = t.s[blockIdx.y];
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < sg.len; i += gridDim.x * blockDim.x) {
+    float acc = 0.f;
+    for (int p = 0; p < sg.nparts; ++p) acc += sg.src[(long long)p * sg.stride + i];
+    sg.dst[i] = acc;
+  }
+}
+
+// ------------------------------------------------------------------ K8 Adam (fp32 master + bf16 shadow)
+// 28 B/param of algorithmic traffic: read p, m, v, g; write p, m, v, shadow(2 B).
+__global__ void __launch_bounds__(256) adam_kernel(const AdamArgs a) {
+  const long long s = a.ctl->adam_step0 + a.step_in_iter;  // completed steps before this one
+  const float bc1 = a.bc[2 * s], bc2 = a.bc[2 * s + 1];
+  const float ob1 = __fsub_rn(1.0f, a.b1), ob2 = __fsub_rn(1.0f, a.b2);
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += stride) {
+    const float g = __fmul_rn(a.g[i], a.inv_n);
+    const float m = __fadd_rn(__fmul_rn(a.b1, a.m[i]), __fmul_rn(ob1, g));
+    const float v = __fadd_rn(__fmul_rn(a.b2, a.v[i]), __fmul_rn(__fmul_rn(ob2, g), g));
+    a.m[i] = m;
+    a.v[i] = v;
+    const float mh = __fdiv_rn(m, bc1), vh = __fdiv_rn(v, bc2);
+    const float p = __fsub_rn(a.p[i], __fmul_rn(a.lr, __fdiv_rn(mh, __fadd_rn(__fsqrt_rn(vh), a.eps))));
+    a.p[i] = p;
+    a.shadow[i] = __float2bfloat16_rn(p);
+  }
+}
+
+int grid_for(long long work, int block, int cap) {
+  return int(std::max<long long>(1, std::min<long long>((work + block - 1) / block, cap)));
+}
+
+}  // namespace
+
+void launch_env_init(const EnvParams& ep, float* x, int* ep_step, int* ep_len, int* ep_count, __nv_bfloat16* X0,
+                     cudaStream_t s) {
+  env_init_kernel<<<(ep.N + 127) / 128, 128, 0, s>>>(ep, x, ep_step, ep_len, ep_count, X0);
+  GMI_CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_act_env(const ActEnvArgs& a, cudaStream_t s) {
+  if (a.ep.A > kMaxAct) invalid("act_dim > 32 unsupported by the act/env kernel");
+  if (a.ep.S > 32 * kMaxObsPerLane) invalid("obs_dim > 256 unsupported by the act/env kernel");
+  const int blocks = (a.ep.N * 32 + 255) / 256;
+  if (a.ep.A <= 8)
+    act_env_kernel<8><<<blocks, 256, 0, s>>>(a);
+  else if (a.ep.A <= 16)
+    act_env_kernel<16><<<blocks, 256, 0, s>>>(a);
+  else
+    act_env_kernel<32><<<blocks, 256, 0, s>>>(a);
+  GMI_CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_value_head(const __nv_bfloat16* H, int hp, const float* w, const float* b, float* out, int rows,
+                       cudaStream_t s) {
+  value_head_kernel<<<(rows * 32 + 255) / 256, 256, 0, s>>>(H, hp, w, b, out, rows);
+  GMI_CUDA_CHECK(cudaGetLastError());
+}
+
+int gae_blocks(int N) { return (N + 31) / 32; }
+
+void launch_gae(const float* rew, const uint8_t* done, const float* V, float* adv, float* ret, double* partials,
+                int N, int T, float gamma, float lam, cudaStream_t s) {
+  if (T > 32) invalid("horizon > 32 unsupported by the GAE scan");
+  gae_kernel<<<gae_blocks(N), 1024, 0, s>>>(rew, done, V, adv, ret, partials, N, T, gamma, gamma * lam);
+  GMI_CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_adv_stats(const double* partials, int nparts, long long count, float* stats, cudaStream_t s) {
+  adv_stats_kernel<<<1, 256, 0, s>>>(partials, nparts, count, stats);
+  GMI_CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_shuffle(const __nv_bfloat16* X_roll, const float* act, const float* logp, const float* adv,
+                    const float* ret, const float* adv_stats, __nv_bfloat16* X_sh, float* act_sh, float* oldlp_sh,
+                    float* adv_sh, float* ret_sh, int N, int T, int S_p, int A, uint64_t seed, int gmi_gid, int epoch,
+                    const Control* ctl, cudaStream_t s) {
+  const long long work = (long long)T * N * (S_p / 8);
+  shuffle_kernel<<<grid_for(work, 256, 1 << 30), 256, 0, s>>>(X_roll, act, logp, adv, ret, adv_stats, X_sh, act_sh,
+                                                              oldlp_sh, adv_sh, ret_sh, N, T, S_p, A, seed, gmi_gid,
+                                                              epoch, ctl);
+  GMI_CUDA_CHECK(cudaGetLastError());
+}
+
+int head_loss_blocks(int B) { return (B + kHeadRowsPerBlock - 1) / kHeadRowsPerBlock; }
+
+void launch_head_loss(const HeadLossArgs& a, cudaStream_t s) {
+  if (a.A > kMaxAct) invalid("act_dim > 32 unsupported by the head kernel");
+  const int blocks = head_loss_blocks(a.B);
+  if (a.A <= 8)
+    head_loss_kernel<8><<<blocks, 256, 0, s>>>(a);
+  else if (a.A <= 16)
+    head_loss_kernel<16><<<blocks, 256, 0, s>>>(a);
+  else
+    head_loss_kernel<32><<<blocks, 256, 0, s>>>(a);
+  GMI_CUDA_CHECK(cudaGetLastError());
+}
+
+int colsum_blocks(int rows) { return (rows + kColsumRows - 1) / kColsumRows; }
+
+void launch_colsum(const __nv_bfloat16* const* D, const int* widths, float* const* partial, int np, int rows,
+                   cudaStream_t s) {
+  if (np > 16) invalid("too many column-sum problems");
+  ColsumArgs a{};
+  for (int i = 0; i < np; ++i) {
+    a.D[i] = D[i];
+    a.out[i] = partial[i];
+    a.width[i] = widths[i];
+  }
+  colsum_kernel<<<dim3(colsum_blocks(rows), np), 256, 0, s>>>(a, rows);
+  GMI_CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_segments(const Segment* segs, int n, cudaStream_t s) {
+  for (int base = 0; base < n; base += kMaxSegments) {
+    SegmentTable t{};
+    const int m = std::min(kMaxSegments, n - base);
+    int maxlen = 1;
+    for (int i = 0; i < m; ++i) {
+      t.s[i] = segs[base + i];
+      maxlen = std::max(maxlen, t.s[i].len);
+    }
+    segments_kernel<<<dim3(grid_for(maxlen, 256, 64), m), 256, 0, s>>>(t);
+    GMI_CUDA_CHECK(cudaGetLastError());
+  }
+}
+
+void launch_adam(const AdamArgs& a, cudaStream_t s) {
+  adam_kernel<<<grid_for(a.n, 256, 148 * 8), 256, 0, s>>>(a);
+  GMI_CUDA_CHECK(cudaGetLastError());
+}
+
+}  // namespace gmi::ppo

@@ -1,0 +1,25 @@
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <vector>
+
+namespace gmi {
+
+class GmiResources {
+ public:
+  // backend 0: streams; 1: green contexts with sm_per_gmi SMs each (0 = even split).
+  GmiResources(int device, int count, int backend, int sm_per_gmi);
+  ~GmiResources();
+  cudaStream_t stream(int i) const { return streams_[i]; }
+  int sm_count(int i) const { return sms_[i]; }
+  int backend() const { return backend_; }
+
+ private:
+  int backend_;
+  std::vector<cudaStream_t> streams_;
+  std::vector<void*> green_;
+  std::vector<int> sms_;
+};
+
+}  // namespace gmi

@@ -1,0 +1,847 @@
+// B200 PPO trainer (host side): memory layout, GMI scheduling and the launch sequence
+// of one data-parallel PPO iteration. The arithmetic contract is DESIGN.md §PPO, restated
+// on the CPU by oracle/ppo_oracle.c (test infrastructure only, never linked here).
+//
+// Per iteration and GMI (own stream / green context):
+//   rollout   T x [L tcgen05 GEMMs (policy, M = N envs) + act/env kernel]
+//   values    ceil((T+1)N / M) x [L GEMMs (value net) + value head]
+//   GAE       warp-shuffle scan + advantage statistics
+//   update    E epochs x [shuffle + K minibatches x (L fwd GEMMs (both nets grouped),
+//             head/loss, L weight-grad GEMMs + L-1 input-grad GEMMs, bias sums, gradient
+//             assembly)]; after each minibatch the update stream folds the GMIs'
+//             gradients (K1, reference fold order), all-reduces across GPUs (NCCL) and
+//             runs Adam once on the GPU's shared replica.
+#include "trainer.hpp"
+
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "../cuda/rng.cuh"
+#include "errors.hpp"
+#include "gmi_exec.hpp"
+#include "planner.hpp"
+
+namespace gmi {
+
+void reduce_device(plan::Algo algo, const plan::Placement& p, void* const* bufs, void* out, size_t len, int dtype,
+                   bool broadcast, cudaStream_t stream);
+
+namespace {
+
+int pad32(int x) { return (x + 31) / 32 * 32; }
+long long align64(long long x) { return (x + 63) / 64 * 64; }
+
+uint16_t bf16_bits(float f) {  // round-to-nearest-even, like __float2bfloat16_rn
+  uint32_t u;
+  std::memcpy(&u, &f, 4);
+  if ((u & 0x7f800000u) == 0x7f800000u) return uint16_t((u >> 16) | ((u & 0x007fffffu) ? 0x40u : 0u));
+  u += 0x7fffu + ((u >> 16) & 1u);
+  return uint16_t(u >> 16);
+}
+
+float bf16_float(uint16_t b) {
+  const uint32_t u = uint32_t(b) << 16;
+  float f;
+  std::memcpy(&f, &u, 4);
+  return f;
+}
+
+#define NCCL_CHECK(expr)                                                                           \
+  do {                                                                                             \
+    ncclResult_t _r = (expr);                                                                      \
+    if (_r != ncclSuccess) ::gmi::fail(GMI_ERR_NCCL, std::string(#expr) + ": " + ncclGetErrorString(_r)); \
+  } while (0)
+
+CUtensorMap kmaj(const void* p, int cols, long long rows, long long ld, int box_rows) {
+  return make_tma_2d_bf16(p, uint64_t(cols), uint64_t(rows), uint64_t(ld), 64, uint32_t(box_rows));
+}
+
+CUtensorMap mnmaj(const void* p, int cols, long long rows, long long ld) {
+  return make_tma_2d_bf16(p, uint64_t(cols), uint64_t(rows), uint64_t(ld), 64, 64);
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ geometry
+Geometry Geometry::make(const gmi_ppo_config_t& c) {
+  Geometry g;
+  if (c.num_hidden < 1 || c.num_hidden > GMI_MAX_HIDDEN) invalid("num_hidden must be in [1, 8]");
+  if (c.obs_dim < 1 || c.act_dim < 1) invalid("obs_dim and act_dim must be positive");
+  g.L = c.num_hidden;
+  g.S = c.obs_dim;
+  g.A = c.act_dim;
+  g.width.push_back(c.obs_dim);
+  for (int l = 0; l < g.L; ++l) {
+    if (c.hidden[l] < 1) invalid("hidden widths must be positive");
+    g.width.push_back(c.hidden[l]);
+  }
+  for (int w : g.width) g.wp.push_back(pad32(w));
+  long long off = 0;
+  for (int n = 0; n < 2; ++n)
+    for (int l = 0; l <= g.L; ++l) {
+      Tensor& t = g.net[n][l];
+      t.in = g.width[l];
+      t.in_p = g.wp[l];
+      t.out = l < g.L ? g.width[l + 1] : (n == 0 ? c.act_dim : 1);
+      t.out_p = l < g.L ? g.wp[l + 1] : t.out;
+      t.w = off;
+      off = align64(off + (long long)t.out_p * t.in_p);
+      t.b = off;
+      off = align64(off + t.out_p);
+      g.real_params += (long long)t.out * t.in + t.out;
+    }
+  g.log_std = off;
+  g.P = align64(off + c.act_dim);
+  return g;
+}
+
+// ------------------------------------------------------------------ per-GMI state
+struct Trainer::Gmi {
+  int local = 0, gid = 0, env0 = 0, N = 0, B = 0, Bm = 0, Mrows = 0;
+  cudaStream_t s = nullptr;
+  cudaEvent_t ev_done = nullptr;
+  float* x = nullptr;
+  int *ep_step = nullptr, *ep_len = nullptr, *ep_count = nullptr;
+  __nv_bfloat16* X_roll = nullptr;
+  float *act = nullptr, *logp = nullptr, *rew = nullptr, *V = nullptr, *adv = nullptr, *ret = nullptr;
+  uint8_t* done = nullptr;
+  double* gae_part = nullptr;
+  float* adv_stats = nullptr;  // mean, std, mean reward
+  __nv_bfloat16* X_sh = nullptr;
+  float *act_sh = nullptr, *oldlp_sh = nullptr, *adv_sh = nullptr, *ret_sh = nullptr;
+  __nv_bfloat16* H[2][GMI_MAX_HIDDEN] = {};
+  __nv_bfloat16* D[2][2] = {};
+  float* slab[2][GMI_MAX_HIDDEN] = {};
+  float* colsum[2][GMI_MAX_HIDDEN] = {};
+  float* head_part = nullptr;
+  float* grad = nullptr;
+  GemmParams fwd_roll[GMI_MAX_HIDDEN], fwd_val[GMI_MAX_HIDDEN], fwd_train[GMI_MAX_HIDDEN];
+  GemmParams dw[GMI_MAX_HIDDEN], dx[GMI_MAX_HIDDEN];
+  int bn_fwd[GMI_MAX_HIDDEN] = {}, bn_dx[GMI_MAX_HIDDEN] = {}, bn_dw[GMI_MAX_HIDDEN] = {};
+  double flop_fwd_roll[GMI_MAX_HIDDEN] = {}, flop_fwd[GMI_MAX_HIDDEN] = {}, flop_dw[GMI_MAX_HIDDEN] = {},
+         flop_dx[GMI_MAX_HIDDEN] = {};
+  std::vector<ppo::Segment> segs;
+};
+
+// ------------------------------------------------------------------ construction
+Trainer::Trainer(const gmi_ppo_config_t& cfg, const void* nccl_id) : cfg_(cfg) {
+  geo_ = Geometry::make(cfg);
+  if (cfg.horizon < 1 || cfg.horizon > 32) invalid("horizon must be in [1, 32]");
+  if (cfg.epochs < 1 || cfg.minibatches < 1) invalid("epochs and minibatches must be >= 1");
+  if (cfg.num_gpus < 1 || cfg.gmis_per_gpu < 1) invalid("num_gpus and gmis_per_gpu must be >= 1");
+  if (cfg.rank < 0 || cfg.rank >= cfg.num_gpus) invalid("rank out of range");
+  if (geo_.A > ppo::kMaxAct) invalid("act_dim > 32 unsupported");
+  if (geo_.S > 256) invalid("obs_dim > 256 unsupported");
+  T_ = cfg.horizon;
+  K_ = cfg.minibatches;
+  n_local_ = cfg.gmis_per_gpu;
+  n_total_ = cfg.num_gpus * cfg.gmis_per_gpu;
+  if (cfg.num_envs < n_total_) invalid("fewer environments than GMIs");
+  GMI_CUDA_CHECK(cudaSetDevice(cfg.device));
+  exec_ = std::make_unique<GmiResources>(cfg.device, n_local_, cfg.gmi_backend, cfg.sm_per_gmi);
+  GMI_CUDA_CHECK(cudaStreamCreateWithFlags(&upd_, cudaStreamNonBlocking));
+  GMI_CUDA_CHECK(cudaEventCreateWithFlags(&ev_adam_, cudaEventDisableTiming));
+  for (int i = 0; i < n_local_; ++i) {
+    auto g = std::make_unique<Gmi>();
+    g->local = i;
+    g->gid = cfg.rank * n_local_ + i;
+    g->env0 = int((long long)cfg.num_envs * g->gid / n_total_);
+    g->N = int((long long)cfg.num_envs * (g->gid + 1) / n_total_) - g->env0;
+    g->B = T_ * g->N;
+    if (g->B % K_ != 0) invalid("horizon * envs per GMI must be divisible by minibatches");
+    g->Bm = g->B / K_;
+    if (g->Bm % 64 != 0) invalid("minibatch rows per GMI must be a multiple of 64 (use envs per GMI % 8 == 0)");
+    g->Mrows = std::max(g->Bm, g->N);
+    g->s = exec_->stream(i);
+    GMI_CUDA_CHECK(cudaEventCreateWithFlags(&g->ev_done, cudaEventDisableTiming));
+    gmis_.push_back(std::move(g));
+  }
+  alloc();
+  init_params();
+  build_plans();
+  if (cfg.num_gpus > 1) {
+    if (!nccl_id) invalid("nccl_id required when num_gpus > 1");
+    ncclUniqueId id;
+    std::memcpy(&id, nccl_id, sizeof(id));
+    ncclComm_t comm;
+    NCCL_CHECK(ncclCommInitRank(&comm, cfg.num_gpus, id, cfg.rank));
+    nccl_ = comm;
+  }
+  for (auto& g : gmis_) {
+    ppo::EnvParams ep{g->N, geo_.S, geo_.A, geo_.wp[0], g->env0, T_, cfg_.seed};
+    ppo::launch_env_init(ep, g->x, g->ep_step, g->ep_len, g->ep_count, g->X_roll, g->s);
+  }
+  GMI_CUDA_CHECK(cudaEventRecord(ev_adam_, upd_));
+  GMI_CUDA_CHECK(cudaDeviceSynchronize());
+}
+
+Trainer::~Trainer() {
+  cudaDeviceSynchronize();
+  if (nccl_) ncclCommDestroy(static_cast<ncclComm_t>(nccl_));
+  for (auto& e : ev_pool_) {
+    cudaEventDestroy(e.first);
+    cudaEventDestroy(e.second);
+  }
+  for (auto& g : gmis_) cudaEventDestroy(g->ev_done);
+  if (ev_adam_) cudaEventDestroy(ev_adam_);
+  if (upd_) cudaStreamDestroy(upd_);
+  for (void* p : allocs_) cudaFree(p);
+  for (auto& e : ctl_ev_)
+    if (e) cudaEventDestroy(e);
+  if (ctl_host_) cudaFreeHost(ctl_host_);
+  if (stats_host_) cudaFreeHost(stats_host_);
+  exec_.reset();
+}
+
+cudaStream_t Trainer::stream(int gmi) const { return gmi < 0 ? upd_ : gmis_.at(gmi)->s; }
+
+void Trainer::alloc() {
+  auto dev = [&](size_t bytes) {
+    void* p = nullptr;
+    GMI_CUDA_CHECK(cudaMalloc(&p, std::max<size_t>(bytes, 256)));
+    GMI_CUDA_CHECK(cudaMemset(p, 0, std::max<size_t>(bytes, 256)));
+    allocs_.push_back(p);
+    return p;
+  };
+  const long long P = geo_.P;
+  params_ = static_cast<float*>(dev(P * 4));
+  m_ = static_cast<float*>(dev(P * 4));
+  v_ = static_cast<float*>(dev(P * 4));
+  grad_sum_ = static_cast<float*>(dev(P * 4));
+  shadow_ = static_cast<__nv_bfloat16*>(dev(P * 2));
+  ctl_dev_ = static_cast<ppo::Control*>(dev(sizeof(ppo::Control)));
+  stats_dev_ = static_cast<float*>(dev(8 * 4));
+  GMI_CUDA_CHECK(cudaMallocHost(&ctl_host_, sizeof(ppo::Control) * kCtlSlots));
+  for (auto& e : ctl_ev_) GMI_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  GMI_CUDA_CHECK(cudaMallocHost(&stats_host_, 8 * 4));
+  std::memset(ctl_host_, 0, sizeof(ppo::Control) * kCtlSlots);
+
+  const int S_p = geo_.wp[0], A = geo_.A, L = geo_.L;
+  int maxw = 0;
+  for (int l = 1; l <= L; ++l) maxw = std::max(maxw, geo_.wp[l]);
+  for (auto& gp : gmis_) {
+    Gmi& g = *gp;
+    const long long N = g.N, T = T_, B = g.B;
+    g.x = static_cast<float*>(dev(N * geo_.S * 4));
+    g.ep_step = static_cast<int*>(dev(N * 4));
+    g.ep_len = static_cast<int*>(dev(N * 4));
+    g.ep_count = static_cast<int*>(dev(N * 4));
+    g.X_roll = static_cast<__nv_bfloat16*>(dev((T + 1) * N * S_p * 2));
+    g.act = static_cast<float*>(dev(T * N * A * 4));
+    g.logp = static_cast<float*>(dev(T * N * 4));
+    g.rew = static_cast<float*>(dev(T * N * 4));
+    g.done = static_cast<uint8_t*>(dev(T * N));
+    g.V = static_cast<float*>(dev((T + 1) * N * 4));
+    g.adv = static_cast<float*>(dev(T * N * 4));
+    g.ret = static_cast<float*>(dev(T * N * 4));
+    g.gae_part = static_cast<double*>(dev(ppo::gae_blocks(g.N) * 3 * 8));
+    g.adv_stats = static_cast<float*>(dev(4 * 4));
+    g.X_sh = static_cast<__nv_bfloat16*>(dev(B * S_p * 2));
+    g.act_sh = static_cast<float*>(dev(B * A * 4));
+    g.oldlp_sh = static_cast<float*>(dev(B * 4));
+    g.adv_sh = static_cast<float*>(dev(B * 4));
+    g.ret_sh = static_cast<float*>(dev(B * 4));
+    for (int n = 0; n < 2; ++n) {
+      for (int l = 0; l < L; ++l) g.H[n][l] = static_cast<__nv_bfloat16*>(dev((long long)g.Mrows * geo_.wp[l + 1] * 2));
+      for (int j = 0; j < 2; ++j) g.D[n][j] = static_cast<__nv_bfloat16*>(dev((long long)g.Bm * maxw * 2));
+    }
+    g.grad = static_cast<float*>(dev(P * 4));
+    const int hs = ppo::head_partial_stride(A, geo_.wp[L]);
+    g.head_part = static_cast<float*>(dev((long long)ppo::head_loss_blocks(g.Bm) * hs * 4));
+  }
+}
+
+void Trainer::init_params() {
+  const long long P = geo_.P;
+  std::vector<float> p(P, 0.f);
+  for (int n = 0; n < 2; ++n)
+    for (int l = 0; l <= geo_.L; ++l) {
+      const Tensor& t = geo_.net[n][l];
+      const float bound = 1.0f / std::sqrt(float(t.in));
+      const uint32_t wid = uint32_t((n * 16 + l) * 2), bid = wid + 1;
+      for (int r = 0; r < t.out; ++r) {
+        for (int k = 0; k < t.in; ++k) {
+          uint32_t o[4];
+          rng::draw(cfg_.seed, wid, uint32_t(r * t.in + k), 0, rng::kInit, o);
+          const float u2 = rng::u01(o[0]) * 2.0f;
+          p[t.w + (long long)r * t.in_p + k] = (u2 - 1.0f) * bound;
+        }
+        uint32_t o[4];
+        rng::draw(cfg_.seed, bid, uint32_t(r), 0, rng::kInit, o);
+        const float u2 = rng::u01(o[0]) * 2.0f;
+        p[t.b + r] = (u2 - 1.0f) * bound;
+      }
+    }
+  set("params", -1, p.data(), P);
+}
+
+// ------------------------------------------------------------------ GEMM descriptors
+void Trainer::build_plans() {
+  const int L = geo_.L, S_p = geo_.wp[0];
+  for (auto& gp : gmis_) {
+    Gmi& g = *gp;
+    const long long rollrows = (long long)(T_ + 1) * g.N;
+    for (int l = 0; l < L; ++l) {
+      const int in_p = geo_.wp[l], out_p = geo_.wp[l + 1];
+      const int bn = gemm_pick_block_n(out_p);
+      g.bn_fwd[l] = bn;
+      auto fwd_problem = [&](int n, const CUtensorMap& amap, int M) {
+        GemmProblem p{};
+        p.map_a = amap;
+        p.map_b = kmaj(shadow_ + geo_.net[n][l].w, in_p, out_p, in_p, bn);
+        p.out = g.H[n][l];
+        p.ld_out = out_p;
+        p.bias = params_ + geo_.net[n][l].b;
+        p.M = M;
+        p.N = out_p;
+        p.K = in_p;
+        p.kb_per_split = (in_p + kGemmBlockK - 1) / kGemmBlockK;
+        return p;
+      };
+      // rollout / value forward read the observation slots of X_roll (rows offset per launch)
+      const CUtensorMap a_roll = l == 0 ? kmaj(g.X_roll, S_p, rollrows, S_p, kGemmBlockM)
+                                        : kmaj(g.H[0][l - 1], in_p, g.Mrows, in_p, kGemmBlockM);
+      g.fwd_roll[l] = GemmParams{};
+      g.fwd_roll[l].prob[0] = fwd_problem(0, a_roll, g.N);
+      g.fwd_roll[l].num_problems = 1;
+      g.fwd_roll[l].splits = 1;
+      const CUtensorMap a_val = l == 0 ? kmaj(g.X_roll, S_p, rollrows, S_p, kGemmBlockM)
+                                       : kmaj(g.H[1][l - 1], in_p, g.Mrows, in_p, kGemmBlockM);
+      g.fwd_val[l] = GemmParams{};
+      g.fwd_val[l].prob[0] = fwd_problem(1, a_val, g.Mrows);
+      g.fwd_val[l].num_problems = 1;
+      g.fwd_val[l].splits = 1;
+      // training forward: both nets grouped, minibatch rows of the epoch copy
+      g.fwd_train[l] = GemmParams{};
+      for (int n = 0; n < 2; ++n) {
+        const CUtensorMap a = l == 0 ? kmaj(g.X_sh, S_p, g.B, S_p, kGemmBlockM)
+                                     : kmaj(g.H[n][l - 1], in_p, g.Mrows, in_p, kGemmBlockM);
+        g.fwd_train[l].prob[n] = fwd_problem(n, a, g.Bm);
+      }
+      g.fwd_train[l].num_problems = 2;
+      g.fwd_train[l].splits = 1;
+      const double real = 2.0 * geo_.net[0][l].out * geo_.net[0][l].in;
+      g.flop_fwd_roll[l] = real * g.N;
+      g.flop_fwd[l] = 2.0 * real * g.Bm;
+
+      // weight gradient: dW_l[out_p][in_p] = sum_rows dPre_l^T in_l (both operands MN-major)
+      const int cur = (L - 1 - l) & 1;
+      const int bnw = gemm_pick_block_n(in_p);
+      g.bn_dw[l] = bnw;
+      const int tiles = ((out_p + 127) / 128) * ((in_p + bnw - 1) / bnw) * 2;
+      const int nkb = g.Bm / kGemmBlockK;
+      int splits = std::max(1, std::min(nkb, 296 / std::max(1, tiles)));
+      const int kbps = (nkb + splits - 1) / splits;
+      splits = (nkb + kbps - 1) / kbps;
+      g.dw[l] = GemmParams{};
+      for (int n = 0; n < 2; ++n) {
+        g.slab[n][l] = nullptr;
+        void* slab = nullptr;
+        GMI_CUDA_CHECK(cudaMalloc(&slab, (size_t)splits * out_p * in_p * 4));
+        allocs_.push_back(slab);
+        g.slab[n][l] = static_cast<float*>(slab);
+        void* cs = nullptr;
+        GMI_CUDA_CHECK(cudaMalloc(&cs, (size_t)ppo::colsum_blocks(g.Bm) * out_p * 4));
+        allocs_.push_back(cs);
+        g.colsum[n][l] = static_cast<float*>(cs);
+        GemmProblem p{};
+        p.map_a = mnmaj(g.D[n][cur], out_p, g.Bm, out_p);
+        p.map_b = l == 0 ? mnmaj(g.X_sh, S_p, g.B, S_p) : mnmaj(g.H[n][l - 1], in_p, g.Bm, in_p);
+        p.out = g.slab[n][l];
+        p.ld_out = in_p;
+        p.split_stride = (long long)out_p * in_p;
+        p.M = out_p;
+        p.N = in_p;
+        p.K = g.Bm;
+        p.kb_per_split = kbps;
+        g.dw[l].prob[n] = p;
+      }
+      g.dw[l].num_problems = 2;
+      g.dw[l].splits = splits;
+      g.flop_dw[l] = 2.0 * real * g.Bm;
+
+      // input gradient: dPre_{l-1} = (dPre_l W_l) * elu'(H_{l-1}); W_l read MN-major
+      if (l > 0) {
+        const int bnx = gemm_pick_block_n(in_p);
+        g.bn_dx[l] = bnx;
+        g.dx[l] = GemmParams{};
+        for (int n = 0; n < 2; ++n) {
+          GemmProblem p{};
+          p.map_a = kmaj(g.D[n][cur], out_p, g.Bm, out_p, kGemmBlockM);
+          p.map_b = mnmaj(shadow_ + geo_.net[n][l].w, in_p, out_p, in_p);
+          p.out = g.D[n][cur ^ 1];
+          p.ld_out = in_p;
+          p.aux = g.H[n][l - 1];
+          p.ld_aux = in_p;
+          p.M = g.Bm;
+          p.N = in_p;
+          p.K = out_p;
+          p.kb_per_split = (out_p + kGemmBlockK - 1) / kGemmBlockK;
+          g.dx[l].prob[n] = p;
+        }
+        g.dx[l].num_problems = 2;
+        g.dx[l].splits = 1;
+        g.flop_dx[l] = 2.0 * real * g.Bm;
+      }
+    }
+    // gradient assembly segments (fixed-order sums of slabs / partials into the flat grad)
+    const int hb = ppo::head_loss_blocks(g.Bm), cb = ppo::colsum_blocks(g.Bm);
+    const int A = geo_.A, hp = geo_.wp[L];
+    const int hs = ppo::head_partial_stride(A, hp);
+    for (int n = 0; n < 2; ++n)
+      for (int l = 0; l < L; ++l) {
+        const Tensor& t = geo_.net[n][l];
+        g.segs.push_back({g.grad + t.w, g.slab[n][l], (long long)t.out_p * t.in_p, t.out_p * t.in_p, g.dw[l].splits});
+        g.segs.push_back({g.grad + t.b, g.colsum[n][l], t.out_p, t.out_p, cb});
+      }
+    g.segs.push_back({g.grad + geo_.net[0][L].w, g.head_part, hs, A * hp, hb});
+    g.segs.push_back({g.grad + geo_.net[1][L].w, g.head_part + A * hp, hs, hp, hb});
+    g.segs.push_back({g.grad + geo_.net[0][L].b, g.head_part + A * hp + hp, hs, A, hb});
+    g.segs.push_back({g.grad + geo_.net[1][L].b, g.head_part + A * hp + hp + A, hs, 1, hb});
+    g.segs.push_back({g.grad + geo_.log_std, g.head_part + A * hp + hp + A + 1, hs, A, hb});
+    if (g.local == 0) g.segs.push_back({stats_dev_, g.head_part + A * hp + hp + 2 * A + 1, hs, 4, hb});
+  }
+}
+
+// ------------------------------------------------------------------ launch helpers
+void Trainer::gemm(Gmi& g, const GemmParams& P, int bn, int amn, int bmn, int epi, double flop) {
+  const bool timed = cfg_.instrument && g.local == 0;
+  if (timed) {
+    if (ev_used_ >= int(ev_pool_.size())) {
+      cudaEvent_t a, b;
+      GMI_CUDA_CHECK(cudaEventCreate(&a));
+      GMI_CUDA_CHECK(cudaEventCreate(&b));
+      ev_pool_.push_back({a, b});
+      ev_flop_.push_back(0);
+    }
+    GMI_CUDA_CHECK(cudaEventRecord(ev_pool_[ev_used_].first, g.s));
+  }
+  gemm_launch(P, bn, amn, bmn, epi, g.s);
+  ++launches_;
+  if (timed) {
+    GMI_CUDA_CHECK(cudaEventRecord(ev_pool_[ev_used_].second, g.s));
+    ev_flop_[ev_used_] = flop;
+    ++ev_used_;
+  }
+}
+
+void Trainer::set_control() {
+  const long long need = adam_steps_ + (long long)cfg_.epochs * K_ + 1;
+  if (need > bc_cap_) {  // bias-correction table 1-b^s, s = 1.. (double pow, like the oracle)
+    GMI_CUDA_CHECK(cudaDeviceSynchronize());
+    const long long cap = std::max<long long>(need * 2, 4096);
+    std::vector<float> tab(2 * cap);
+    for (long long s = 0; s < cap; ++s) {
+      tab[2 * s] = float(1.0 - std::pow(double(cfg_.beta1), double(s + 1)));
+      tab[2 * s + 1] = float(1.0 - std::pow(double(cfg_.beta2), double(s + 1)));
+    }
+    void* p = nullptr;
+    GMI_CUDA_CHECK(cudaMalloc(&p, tab.size() * 4));
+    GMI_CUDA_CHECK(cudaMemcpy(p, tab.data(), tab.size() * 4, cudaMemcpyHostToDevice));
+    allocs_.push_back(p);
+    bc_ = static_cast<float*>(p);
+    bc_cap_ = cap;
+  }
+  // Pinned ring: a slot is rewritten only after its previous H2D copy has executed.
+  const int slot = iteration_ % kCtlSlots;
+  GMI_CUDA_CHECK(cudaEventSynchronize(ctl_ev_[slot]));
+  ppo::Control* c = ctl_host_ + slot;
+  c->iteration = iteration_;
+  c->adam_step0 = adam_steps_;
+  GMI_CUDA_CHECK(cudaStreamWaitEvent(upd_, ev_adam_, 0));
+  GMI_CUDA_CHECK(cudaMemcpyAsync(ctl_dev_, c, sizeof(ppo::Control), cudaMemcpyHostToDevice, upd_));
+  GMI_CUDA_CHECK(cudaEventRecord(ctl_ev_[slot], upd_));
+  GMI_CUDA_CHECK(cudaEventRecord(ev_adam_, upd_));
+}
+
+// ------------------------------------------------------------------ phases
+void Trainer::rollout(Gmi& g) {
+  const int L = geo_.L, S_p = geo_.wp[0];
+  if (iteration_ > 0)  // the last observation of the previous rollout seeds this one
+    GMI_CUDA_CHECK(cudaMemcpyAsync(g.X_roll, g.X_roll + (long long)T_ * g.N * S_p, (size_t)g.N * S_p * 2,
+                                   cudaMemcpyDeviceToDevice, g.s));
+  const Tensor& head = geo_.net[0][L];
+  for (int t = 0; t < T_; ++t) {
+    for (int l = 0; l < L; ++l) {
+      GemmParams P = g.fwd_roll[l];
+      if (l == 0) P.prob[0].a_row0 = t * g.N;
+      gemm(g, P, g.bn_fwd[l], 0, 0, EPI_BIAS_ELU, g.flop_fwd_roll[l]);
+    }
+    ppo::ActEnvArgs a{};
+    a.ep = {g.N, geo_.S, geo_.A, S_p, g.env0, T_, cfg_.seed};
+    a.H = g.H[0][L - 1];
+    a.hp = geo_.wp[L];
+    a.w_mu = params_ + head.w;
+    a.b_mu = params_ + head.b;
+    a.log_std = params_ + geo_.log_std;
+    a.x = g.x;
+    a.ep_step = g.ep_step;
+    a.ep_len = g.ep_len;
+    a.ep_count = g.ep_count;
+    a.X_next = g.X_roll + (long long)(t + 1) * g.N * S_p;
+    a.act = g.act + (long long)t * g.N * geo_.A;
+    a.logp = g.logp + (long long)t * g.N;
+    a.rew = g.rew + (long long)t * g.N;
+    a.done = g.done + (long long)t * g.N;
+    a.t = t;
+    a.ctl = ctl_dev_;
+    ppo::launch_act_env(a, g.s);
+    ++launches_;
+  }
+}
+
+void Trainer::values(Gmi& g) {
+  const int L = geo_.L;
+  const long long rows = (long long)(T_ + 1) * g.N;
+  const Tensor& head = geo_.net[1][L];
+  for (long long c0 = 0; c0 < rows; c0 += g.Mrows) {
+    const int m = int(std::min<long long>(g.Mrows, rows - c0));
+    for (int l = 0; l < L; ++l) {
+      GemmParams P = g.fwd_val[l];
+      P.prob[0].M = m;
+      if (l == 0) P.prob[0].a_row0 = int(c0);
+      gemm(g, P, g.bn_fwd[l], 0, 0, EPI_BIAS_ELU, g.flop_fwd_roll[l] * double(m) / g.N);
+    }
+    ppo::launch_value_head(g.H[1][L - 1], geo_.wp[L], params_ + head.w, params_ + head.b, g.V + c0, m, g.s);
+    ++launches_;
+  }
+  ppo::launch_gae(g.rew, g.done, g.V, g.adv, g.ret, g.gae_part, g.N, T_, cfg_.gamma, cfg_.lam, g.s);
+  ppo::launch_adv_stats(g.gae_part, ppo::gae_blocks(g.N), (long long)T_ * g.N, g.adv_stats, g.s);
+  launches_ += 2;
+}
+
+void Trainer::train_minibatch(Gmi& g, int k) {
+  const int L = geo_.L, A = geo_.A, hp = geo_.wp[L];
+  for (int l = 0; l < L; ++l) {
+    GemmParams P = g.fwd_train[l];
+    if (l == 0) P.prob[0].a_row0 = P.prob[1].a_row0 = k * g.Bm;
+    gemm(g, P, g.bn_fwd[l], 0, 0, EPI_BIAS_ELU, g.flop_fwd[l]);
+  }
+  ppo::HeadLossArgs h{};
+  h.Hpi = g.H[0][L - 1];
+  h.Hv = g.H[1][L - 1];
+  h.hp = hp;
+  h.w_mu = params_ + geo_.net[0][L].w;
+  h.b_mu = params_ + geo_.net[0][L].b;
+  h.w_v = params_ + geo_.net[1][L].w;
+  h.b_v = params_ + geo_.net[1][L].b;
+  h.log_std = params_ + geo_.log_std;
+  const long long r0 = (long long)k * g.Bm;
+  h.act = g.act_sh + r0 * A;
+  h.oldlp = g.oldlp_sh + r0;
+  h.adv = g.adv_sh + r0;
+  h.ret = g.ret_sh + r0;
+  h.Dpi = g.D[0][0];
+  h.Dv = g.D[1][0];
+  h.partial = g.head_part;
+  h.partial_stride = ppo::head_partial_stride(A, hp);
+  h.B = g.Bm;
+  h.A = A;
+  h.clip = cfg_.clip;
+  h.vf_coef = cfg_.vf_coef;
+  h.ent_coef = cfg_.ent_coef;
+  ppo::launch_head_loss(h, g.s);
+  ++launches_;
+  for (int l = L - 1; l >= 0; --l) {
+    GemmParams P = g.dw[l];
+    if (l == 0) P.prob[0].b_row0 = P.prob[1].b_row0 = k * g.Bm;
+    gemm(g, P, g.bn_dw[l], 1, 1, EPI_F32, g.flop_dw[l]);
+    const int cur = (L - 1 - l) & 1;
+    const __nv_bfloat16* Ds[2] = {g.D[0][cur], g.D[1][cur]};
+    const int widths[2] = {geo_.wp[l + 1], geo_.wp[l + 1]};
+    float* outs[2] = {g.colsum[0][l], g.colsum[1][l]};
+    ppo::launch_colsum(Ds, widths, outs, 2, g.Bm, g.s);
+    ++launches_;
+    if (l > 0) gemm(g, g.dx[l], g.bn_dx[l], 0, 1, EPI_DACT, g.flop_dx[l]);
+  }
+  ppo::launch_segments(g.segs.data(), int(g.segs.size()), g.s);
+  launches_ += (int(g.segs.size()) + 63) / 64;
+}
+
+void Trainer::reduce_and_step(int step_in_iter) {
+  for (auto& g : gmis_) GMI_CUDA_CHECK(cudaStreamWaitEvent(upd_, g->ev_done, 0));
+  float* src = gmis_[0]->grad;
+  if (n_local_ > 1) {  // K1: fold the GMIs' gradients in the layout's ring order (one GPU: MPR)
+    plan::Placement p;
+    p.per_gpu.resize(1);
+    std::vector<void*> bufs;
+    for (auto& g : gmis_) {
+      p.per_gpu[0].push_back(g->local);
+      bufs.push_back(g->grad);
+    }
+    reduce_device(plan::Algo::MPR, p, bufs.data(), grad_sum_, size_t(geo_.P), GMI_F32, false, upd_);
+    ++launches_;
+    src = grad_sum_;
+  }
+  if (nccl_) {
+    NCCL_CHECK(ncclAllReduce(src, grad_sum_, size_t(geo_.P), ncclFloat32, ncclSum,
+                             static_cast<ncclComm_t>(nccl_), upd_));
+    src = grad_sum_;
+  }
+  ppo::AdamArgs a{};
+  a.p = params_;
+  a.m = m_;
+  a.v = v_;
+  a.shadow = shadow_;
+  a.g = src;
+  a.bc = bc_;
+  a.ctl = ctl_dev_;
+  a.step_in_iter = step_in_iter;
+  a.n = geo_.P;
+  a.lr = cfg_.lr;
+  a.b1 = cfg_.beta1;
+  a.b2 = cfg_.beta2;
+  a.eps = cfg_.adam_eps;
+  a.inv_n = 1.0f / float(n_total_);
+  ppo::launch_adam(a, upd_);
+  ++launches_;
+  GMI_CUDA_CHECK(cudaEventRecord(ev_adam_, upd_));
+}
+
+void Trainer::enqueue_rollout() {
+  set_control();
+  for (auto& g : gmis_) {
+    GMI_CUDA_CHECK(cudaStreamWaitEvent(g->s, ev_adam_, 0));
+    rollout(*g);
+    values(*g);
+  }
+}
+
+void Trainer::enqueue_iteration() {
+  launches_ = 0;
+  ev_used_ = 0;
+  enqueue_rollout();
+  int step = 0;
+  for (int e = 0; e < cfg_.epochs; ++e) {
+    for (auto& g : gmis_) {
+      ppo::launch_shuffle(g->X_roll, g->act, g->logp, g->adv, g->ret, g->adv_stats, g->X_sh, g->act_sh,
+                          g->oldlp_sh, g->adv_sh, g->ret_sh, g->N, T_, geo_.wp[0], geo_.A, cfg_.seed, g->gid, e,
+                          ctl_dev_, g->s);
+      ++launches_;
+    }
+    for (int k = 0; k < K_; ++k, ++step) {
+      for (auto& g : gmis_) {
+        if (step > 0) GMI_CUDA_CHECK(cudaStreamWaitEvent(g->s, ev_adam_, 0));
+        train_minibatch(*g, k);
+        GMI_CUDA_CHECK(cudaEventRecord(g->ev_done, g->s));
+      }
+      reduce_and_step(step);
+    }
+  }
+  GMI_CUDA_CHECK(cudaStreamWaitEvent(upd_, gmis_[0]->ev_done, 0));
+  GMI_CUDA_CHECK(cudaMemcpyAsync(stats_dev_ + 4, gmis_[0]->adv_stats, 3 * 4, cudaMemcpyDeviceToDevice, upd_));
+  GMI_CUDA_CHECK(cudaMemcpyAsync(stats_host_, stats_dev_, 8 * 4, cudaMemcpyDeviceToHost, upd_));
+  GMI_CUDA_CHECK(cudaEventRecord(ev_adam_, upd_));
+  iteration_ += 1;
+  adam_steps_ += (long long)cfg_.epochs * K_;
+}
+
+void Trainer::synchronize(gmi_ppo_stats_t* st) {
+  GMI_CUDA_CHECK(cudaStreamSynchronize(upd_));
+  for (auto& g : gmis_) GMI_CUDA_CHECK(cudaStreamSynchronize(g->s));
+  if (!st) return;
+  std::memset(st, 0, sizeof(*st));
+  const double Bm = gmis_[0]->Bm;
+  st->policy_loss = stats_host_[0] / Bm;
+  st->value_loss = stats_host_[1] / Bm;
+  st->approx_kl = stats_host_[2] / Bm;
+  st->clip_frac = stats_host_[3] / Bm;
+  st->mean_reward = stats_host_[6];
+  long long steps = 0;
+  for (auto& g : gmis_) steps += (long long)T_ * g->N;
+  st->env_steps = steps;
+  st->kernel_launches = launches_;
+  for (int i = 0; i < ev_used_; ++i) {
+    float ms = 0;
+    GMI_CUDA_CHECK(cudaEventElapsedTime(&ms, ev_pool_[i].first, ev_pool_[i].second));
+    st->gemm_ms += ms;
+    st->gemm_flop += ev_flop_[i];
+  }
+  st->gemm_launches = ev_used_;
+}
+
+// ------------------------------------------------------------------ parity hooks
+void Trainer::minibatch_grad(int gi, const float* X, const float* act, const float* oldlp, const float* adv,
+                             const float* ret, int B, float* grad_out) {
+  Gmi& g = *gmis_.at(gi);
+  if (B != g.Bm) invalid("minibatch rows must equal the trainer's minibatch size");
+  const int S = geo_.S, S_p = geo_.wp[0], A = geo_.A;
+  std::vector<uint16_t> xb((size_t)B * S_p, 0);
+  for (int r = 0; r < B; ++r)
+    for (int i = 0; i < S; ++i) xb[(size_t)r * S_p + i] = bf16_bits(X[(size_t)r * S + i]);
+  GMI_CUDA_CHECK(cudaStreamSynchronize(upd_));
+  GMI_CUDA_CHECK(cudaMemcpy(g.X_sh, xb.data(), xb.size() * 2, cudaMemcpyHostToDevice));
+  GMI_CUDA_CHECK(cudaMemcpy(g.act_sh, act, (size_t)B * A * 4, cudaMemcpyHostToDevice));
+  GMI_CUDA_CHECK(cudaMemcpy(g.oldlp_sh, oldlp, (size_t)B * 4, cudaMemcpyHostToDevice));
+  GMI_CUDA_CHECK(cudaMemcpy(g.adv_sh, adv, (size_t)B * 4, cudaMemcpyHostToDevice));
+  GMI_CUDA_CHECK(cudaMemcpy(g.ret_sh, ret, (size_t)B * 4, cudaMemcpyHostToDevice));
+  train_minibatch(g, 0);
+  GMI_CUDA_CHECK(cudaStreamSynchronize(g.s));
+  GMI_CUDA_CHECK(cudaMemcpy(grad_out, g.grad, (size_t)geo_.P * 4, cudaMemcpyDeviceToHost));
+}
+
+long long Trainer::get(const std::string& what, int gi, void* dst) {
+  GMI_CUDA_CHECK(cudaDeviceSynchronize());
+  auto copy = [&](const void* src, long long n, int esz) {
+    if (dst) GMI_CUDA_CHECK(cudaMemcpy(dst, src, (size_t)n * esz, cudaMemcpyDeviceToHost));
+    return n;
+  };
+  const long long P = geo_.P;
+  if (what == "params") return copy(params_, P, 4);
+  if (what == "adam_m") return copy(m_, P, 4);
+  if (what == "adam_v") return copy(v_, P, 4);
+  Gmi& g = *gmis_.at(gi);
+  const long long N = g.N, T = T_, S = geo_.S, A = geo_.A;
+  if (what == "grad") return copy(g.grad, P, 4);
+  if (what == "x") return copy(g.x, N * S, 4);
+  if (what == "act") return copy(g.act, T * N * A, 4);
+  if (what == "logp") return copy(g.logp, T * N, 4);
+  if (what == "rew") return copy(g.rew, T * N, 4);
+  if (what == "val") return copy(g.V, (T + 1) * N, 4);
+  if (what == "adv") return copy(g.adv, T * N, 4);
+  if (what == "ret") return copy(g.ret, T * N, 4);
+  if (what == "done") return copy(g.done, T * N, 1);
+  if (what == "ep_step") return copy(g.ep_step, N, 4);
+  if (what == "ep_len") return copy(g.ep_len, N, 4);
+  if (what == "ep_count") return copy(g.ep_count, N, 4);
+  if (what == "obs") {  // bf16 X_roll -> fp32 [(T+1)][N][S]
+    const long long n = (T + 1) * N * S;
+    if (dst) {
+      const int S_p = geo_.wp[0];
+      std::vector<uint16_t> raw((size_t)(T + 1) * N * S_p);
+      GMI_CUDA_CHECK(cudaMemcpy(raw.data(), g.X_roll, raw.size() * 2, cudaMemcpyDeviceToHost));
+      float* o = static_cast<float*>(dst);
+      for (long long r = 0; r < (T + 1) * N; ++r)
+        for (long long i = 0; i < S; ++i) o[r * S + i] = bf16_float(raw[(size_t)(r * S_p + i)]);
+    }
+    return n;
+  }
+  invalid("unknown state field: " + what);
+}
+
+void Trainer::set(const std::string& what, int gi, const void* src, long long n) {
+  GMI_CUDA_CHECK(cudaDeviceSynchronize());
+  auto put = [&](void* d, long long want, int esz) {
+    if (n != want) invalid("size mismatch for " + what);
+    GMI_CUDA_CHECK(cudaMemcpy(d, src, (size_t)n * esz, cudaMemcpyHostToDevice));
+  };
+  const long long P = geo_.P;
+  if (what == "params") {
+    put(params_, P, 4);
+    std::vector<uint16_t> sh(P);
+    const float* f = static_cast<const float*>(src);
+    for (long long i = 0; i < P; ++i) sh[i] = bf16_bits(f[i]);
+    GMI_CUDA_CHECK(cudaMemcpy(shadow_, sh.data(), P * 2, cudaMemcpyHostToDevice));
+    return;
+  }
+  if (what == "adam_m") return put(m_, P, 4);
+  if (what == "adam_v") return put(v_, P, 4);
+  Gmi& g = *gmis_.at(gi);
+  if (what == "x") return put(g.x, (long long)g.N * geo_.S, 4);
+  if (what == "ep_step") return put(g.ep_step, g.N, 4);
+  if (what == "ep_count") return put(g.ep_count, g.N, 4);
+  invalid("field not settable: " + what);
+}
+
+}  // namespace gmi
+
+// ------------------------------------------------------------------ C-ABI
+extern "C" {
+
+GMI_API void gmi_ppo_config_defaults(gmi_ppo_config_t* c) {
+  std::memset(c, 0, sizeof(*c));
+  c->obs_dim = 60;
+  c->act_dim = 8;
+  c->num_hidden = 3;
+  c->hidden[0] = c->hidden[1] = c->hidden[2] = 256;
+  c->num_envs = 4096;
+  c->horizon = 32;
+  c->epochs = 4;
+  c->minibatches = 4;
+  c->gamma = 0.99f;
+  c->lam = 0.95f;
+  c->clip = 0.2f;
+  c->lr = 3e-4f;
+  c->beta1 = 0.9f;
+  c->beta2 = 0.999f;
+  c->adam_eps = 1e-8f;
+  c->vf_coef = 1.0f;
+  c->ent_coef = 0.0f;
+  c->seed = 20240811ull;
+  c->num_gpus = 1;
+  c->gmis_per_gpu = 1;
+}
+
+GMI_API int gmi_ppo_create(const gmi_ppo_config_t* cfg, const void* nccl_id, void** trainer) {
+  return gmi::guarded([&] {
+    if (!cfg || !trainer) gmi::invalid("null argument");
+    *trainer = new gmi::Trainer(*cfg, nccl_id);
+  });
+}
+
+GMI_API void gmi_ppo_free(void* t) { delete static_cast<gmi::Trainer*>(t); }
+
+GMI_API int gmi_nccl_unique_id(void* out) {
+  return gmi::guarded([&] {
+    ncclUniqueId id;
+    NCCL_CHECK(ncclGetUniqueId(&id));
+    std::memcpy(out, &id, sizeof(id));
+  });
+}
+
+GMI_API int gmi_ppo_iteration(void* t, gmi_ppo_stats_t* st) {
+  return gmi::guarded([&] {
+    auto* tr = static_cast<gmi::Trainer*>(t);
+    tr->enqueue_iteration();
+    tr->synchronize(st);
+  });
+}
+
+GMI_API int gmi_ppo_iteration_async(void* t) {
+  return gmi::guarded([&] { static_cast<gmi::Trainer*>(t)->enqueue_iteration(); });
+}
+
+GMI_API int gmi_ppo_synchronize(void* t, gmi_ppo_stats_t* st) {
+  return gmi::guarded([&] { static_cast<gmi::Trainer*>(t)->synchronize(st); });
+}
+
+GMI_API int gmi_ppo_rollout(void* t) {
+  return gmi::guarded([&] {
+    auto* tr = static_cast<gmi::Trainer*>(t);
+    tr->enqueue_rollout();
+    tr->synchronize(nullptr);
+  });
+}
+
+GMI_API int gmi_ppo_minibatch_grad(void* t, int gmi, const float* X, const float* act, const float* oldlp,
+                                   const float* adv, const float* ret, int B, float* grad_out) {
+  return gmi::guarded([&] { static_cast<gmi::Trainer*>(t)->minibatch_grad(gmi, X, act, oldlp, adv, ret, B, grad_out); });
+}
+
+GMI_API int gmi_ppo_get(void* t, const char* what, int gmi, void* dst, long long* n) {
+  return gmi::guarded([&] {
+    const long long c = static_cast<gmi::Trainer*>(t)->get(what ? what : "", gmi, dst);
+    if (n) *n = c;
+  });
+}
+
+GMI_API int gmi_ppo_set(void* t, const char* what, int gmi, const void* src, long long n) {
+  return gmi::guarded([&] { static_cast<gmi::Trainer*>(t)->set(what ? what : "", gmi, src, n); });
+}
+
+GMI_API int gmi_ppo_param_count(void* t, long long* padded, long long* real) {
+  return gmi::guarded([&] {
+    const auto& g = static_cast<gmi::Trainer*>(t)->geometry();
+    if (padded) *padded = g.P;
+    if (real) *real = g.real_params;
+  });
+}
+
+GMI_API int gmi_ppo_stream(void* t, int gmi, void** stream) {
+  return gmi::guarded([&] { *stream = static_cast<gmi::Trainer*>(t)->stream(gmi); });
+}
+
+}  // extern "C"

@@ -1,0 +1,94 @@
+// B200 PPO trainer: one instance drives one GPU of the data-parallel job (TCG_EX
+// holistic GMIs). Owns device memory, GMI execution resources (streams or green
+// contexts), the prebuilt GEMM problem descriptors and the NCCL communicator.
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../cuda/gemm_host.hpp"
+#include "../cuda/ppo.cuh"
+#include "gmi.h"
+
+namespace gmi {
+
+struct Tensor {  // one weight or bias block inside the flat parameter vector
+  long long w = 0, b = 0;
+  int out = 0, in = 0, out_p = 0, in_p = 0;
+};
+
+// Geometry shared bit-for-bit with oracle/ppo_oracle.c and tests/golden_util.param_layout.
+struct Geometry {
+  int L = 0, S = 0, A = 0;
+  std::vector<int> width, wp;  // [0] = obs, 1..L hidden; wp padded to 32
+  Tensor net[2][GMI_MAX_HIDDEN + 1];
+  long long log_std = 0, P = 0, real_params = 0;
+  static Geometry make(const gmi_ppo_config_t& c);
+};
+
+class GmiResources;  // streams / green contexts (gmi_exec.cpp)
+
+class Trainer {
+ public:
+  Trainer(const gmi_ppo_config_t& cfg, const void* nccl_id);
+  ~Trainer();
+
+  void enqueue_iteration();
+  void enqueue_rollout();
+  void synchronize(gmi_ppo_stats_t* stats);
+  void minibatch_grad(int gmi, const float* X, const float* act, const float* oldlp, const float* adv,
+                      const float* ret, int B, float* grad_out);
+  long long get(const std::string& what, int gmi, void* dst);
+  void set(const std::string& what, int gmi, const void* src, long long n);
+  const Geometry& geometry() const { return geo_; }
+  cudaStream_t stream(int gmi) const;
+
+ private:
+  struct Gmi;
+  struct Launch;
+
+  void alloc();
+  void init_params();
+  void build_plans();
+  void rollout(Gmi& g);
+  void values(Gmi& g);
+  void train_minibatch(Gmi& g, int k);
+  void reduce_and_step(int k);
+  void gemm(Gmi& g, const GemmParams& P, int bn, int amn, int bmn, int epi, double flop);
+  void set_control();
+
+  gmi_ppo_config_t cfg_;
+  Geometry geo_;
+  int T_ = 0, K_ = 0, n_local_ = 0, n_total_ = 0;
+  std::unique_ptr<GmiResources> exec_;
+  std::vector<std::unique_ptr<Gmi>> gmis_;
+  std::vector<void*> allocs_;
+
+  // shared per GPU
+  float *params_ = nullptr, *m_ = nullptr, *v_ = nullptr, *grad_sum_ = nullptr, *bc_ = nullptr;
+  __nv_bfloat16* shadow_ = nullptr;
+  long long bc_cap_ = 0;
+  ppo::Control* ctl_dev_ = nullptr;
+  ppo::Control* ctl_host_ = nullptr;  // pinned ring of kCtlSlots blocks
+  static constexpr int kCtlSlots = 4;
+  cudaEvent_t ctl_ev_[kCtlSlots] = {};
+  float* stats_dev_ = nullptr;   // [8]
+  float* stats_host_ = nullptr;  // pinned
+  cudaStream_t upd_ = nullptr;   // update / reduction stream
+  cudaEvent_t ev_adam_ = nullptr;
+  void* nccl_ = nullptr;
+  int iteration_ = 0;
+  long long adam_steps_ = 0;
+  int launches_ = 0;
+  // instrumentation
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pool_;
+  std::vector<double> ev_flop_;
+  int ev_used_ = 0;
+  double gemm_flop_ = 0;
+};
+
+}  // namespace gmi

@@ -1,0 +1,133 @@
+"""B200 PPO iteration (libgmi) vs the CPU restatement (oracle/ppo_oracle.c).
+
+Tolerances (stated per quantity; the oracle mirrors every bf16 rounding point, so the
+residual is fp32 accumulation order in TMEM vs double on the CPU, ulp differences of
+expf/logf/tanhf/sinf, and the occasional bf16 rounding flip those cause):
+  * integer state (episode clocks, reset masks) and initial parameters: bit-exact
+  * rollout trajectories over the horizon: max |d| <= 2e-2, mean |d| <= 1e-4 (act/obs/rew)
+  * minibatch gradients: per tensor ||d|| <= 2e-2 ||g||
+  * parameters after one full iteration (16 Adam steps, lr 3e-4): max |d| <= 2e-3, mean |d| <= 5e-5
+"""
+import numpy as np
+import pytest
+
+from golden_util import PpoOracle, make_cfg, param_layout
+
+pytestmark = pytest.mark.gpu
+
+SMALL = dict(obs_dim=12, act_dim=3, hidden=[64, 64], num_envs=64)
+
+
+def _pair(obs_dim, act_dim, hidden, num_envs, **kw):
+    from paper_2206_08482_b200.ppo import PpoConfig, Trainer
+    dev = Trainer(PpoConfig(obs_dim=obs_dim, act_dim=act_dim, hidden=list(hidden), num_envs=num_envs, **kw))
+    okw = {k: v for k, v in kw.items() if k in ("num_gpus", "gmis_per_gpu", "seed", "horizon", "epochs",
+                                                "minibatches", "lr", "ent_coef", "vf_coef")}
+    orc = PpoOracle(make_cfg(obs_dim, act_dim, hidden, num_envs, **okw))
+    return dev, orc
+
+
+def _close(name, got, want, max_abs, mean_abs):
+    d = np.abs(got.astype(np.float64) - want.astype(np.float64))
+    assert d.max() <= max_abs and d.mean() <= mean_abs, (name, float(d.max()), float(d.mean()))
+
+
+def test_init_is_bit_exact(cuda):
+    dev, orc = _pair(**SMALL)
+    assert dev.param_count == orc.P
+    assert np.array_equal(dev.get("params").view(np.uint32), orc.get("params").view(np.uint32))
+    for f in ("x", "ep_len", "ep_step"):
+        assert np.array_equal(dev.get(f), orc.get(f)), f
+
+
+@pytest.mark.parametrize("gmis", [1, 2])
+def test_rollout_matches_oracle(cuda, gmis):
+    dev, orc = _pair(**SMALL, gmis_per_gpu=gmis)
+    dev.rollout()
+    orc.rollout()
+    for c in range(gmis):
+        assert np.array_equal(dev.get("done", c), orc.get("done", c))
+        assert np.array_equal(dev.get("ep_count", c), orc.get("ep_count", c))
+        _close("act", dev.get("act", c), orc.get("act", c), 2e-2, 1e-4)
+        _close("obs", dev.get("obs", c), orc.get("obs", c), 2e-2, 1e-4)
+        _close("rew", dev.get("rew", c), orc.get("rew", c), 2e-2, 1e-4)
+        _close("logp", dev.get("logp", c), orc.get("logp", c), 5e-2, 1e-3)
+        _close("val", dev.get("val", c), orc.get("val", c), 2e-2, 1e-4)
+        _close("adv", dev.get("adv", c), orc.get("adv", c), 5e-2, 1e-3)
+        _close("ret", dev.get("ret", c), orc.get("ret", c), 5e-2, 1e-3)
+
+
+@pytest.mark.parametrize("dims", [(12, 3, [64, 64]), (60, 8, [256, 256, 256]), (108, 21, [200, 400, 100])])
+def test_minibatch_gradient_matches_oracle(cuda, dims):
+    S, A, hidden = dims
+    dev, orc = _pair(S, A, hidden, 64)
+    B = 64 * 32 // 4
+    rng = np.random.default_rng(S)
+    X = rng.uniform(-1, 1, (B, S)).astype(np.float32)
+    act = rng.standard_normal((B, A)).astype(np.float32)
+    oldlp = (rng.standard_normal(B) - 3).astype(np.float32)
+    adv = rng.standard_normal(B).astype(np.float32)
+    ret = rng.standard_normal(B).astype(np.float32)
+    g_dev = dev.minibatch_grad(X, act, oldlp, adv, ret)
+    g_orc, _ = orc.minibatch(X, act, oldlp, adv, ret)
+    lay = param_layout(S, A, hidden)
+    for key, t in lay.items():
+        if not isinstance(key, tuple):
+            continue
+        for part, n in (("w", t["out_p"] * t["in_p"]), ("b", t["out_p"])):
+            a, b = g_dev[t[part]:t[part] + n], g_orc[t[part]:t[part] + n]
+            ref = np.linalg.norm(b) + 1e-12
+            assert np.linalg.norm(a - b) <= 2e-2 * ref, (key, part, np.linalg.norm(a - b) / ref)
+    ls = slice(lay["log_std"], lay["log_std"] + A)
+    assert np.linalg.norm(g_dev[ls] - g_orc[ls]) <= 2e-2 * (np.linalg.norm(g_orc[ls]) + 1e-12)
+
+
+@pytest.mark.parametrize("gmis", [1, 2])
+def test_full_iteration_matches_oracle(cuda, gmis):
+    dev, orc = _pair(**SMALL, gmis_per_gpu=gmis)
+    s = dev.iteration()
+    orc.iteration()
+    assert s.env_steps == SMALL["num_envs"] * 32
+    _close("params", dev.get("params"), orc.get("params"), 2e-3, 5e-5)
+    m_dev, m_orc = dev.get("adam_m"), orc.get("adam_m")
+    assert np.linalg.norm(m_dev - m_orc) <= 5e-2 * np.linalg.norm(m_orc)
+    # the next rollout starts from the carried-over observation slot
+    dev.rollout()
+    orc.rollout()
+    assert np.array_equal(dev.get("done"), orc.get("done"))
+    _close("rew", dev.get("rew"), orc.get("rew"), 5e-2, 5e-4)
+
+
+def test_iterations_are_deterministic(cuda):
+    from paper_2206_08482_b200.ppo import PpoConfig, Trainer
+    runs = []
+    for _ in range(2):
+        t = Trainer(PpoConfig(obs_dim=12, act_dim=3, hidden=[64, 64], num_envs=64, gmis_per_gpu=2))
+        t.iteration()
+        t.iteration()
+        runs.append(t.get("params"))
+    assert np.array_equal(runs[0].view(np.uint32), runs[1].view(np.uint32))
+
+
+def test_rollout_is_layout_invariant_on_device(cuda):
+    from paper_2206_08482_b200.ppo import PpoConfig, Trainer
+    one = Trainer(PpoConfig(obs_dim=12, act_dim=3, hidden=[64, 64], num_envs=64))
+    two = Trainer(PpoConfig(obs_dim=12, act_dim=3, hidden=[64, 64], num_envs=64, gmis_per_gpu=2))
+    one.rollout()
+    two.rollout()
+    r1 = one.get("rew").reshape(32, 64)
+    r2 = np.concatenate([two.get("rew", c).reshape(32, 32) for c in range(2)], axis=1)
+    assert np.array_equal(r1, r2)
+
+
+def test_bench_workload_runs(cuda):
+    """BASELINE config 2: AT, 4096 envs, 3x256, 1 GMI."""
+    from paper_2206_08482_b200.ppo import PpoConfig, Trainer
+    t = Trainer(PpoConfig.from_benchmark("AT", 4096, hidden=[256, 256, 256], instrument=1))
+    assert t.real_param_count == 296713
+    for _ in range(2):
+        s = t.iteration()
+    assert s.env_steps == 4096 * 32
+    assert np.isfinite([s.policy_loss, s.value_loss, s.approx_kl, s.mean_reward]).all()
+    assert s.gemm_launches > 0 and s.kernel_launches > s.gemm_launches
+    assert np.isfinite(t.get("params")).all()
