@@ -1,0 +1,271 @@
+#!/usr/bin/env python3
+"""Benchmark: whole-box PPO training env-steps/s on B200 (BASELINE.json `metric`).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config configs/at_4096env_3x256.cfg]
+    torchrun --nproc-per-node N bench.py --gpus N ...          (N > 1, one rank per GPU)
+    python bench.py --impl reference ...                        (CPU reference arm)
+
+A step is one PPO iteration of the data-parallel TCG_EX job: every env of every GMI
+advances `horizon` steps (rollout), then `epochs` x `minibatches` PPO updates with the
+cross-GMI / cross-GPU gradient reduction.  Default workload = BASELINE configs[1]
+(AT-like, 4096 envs per GPU, 3x256 MLP, 1 GMI per B200).  Envs shard across ranks
+([N*c/n, N*(c+1)/n)); the only data-path collective is the per-minibatch gradient
+all-reduce.  Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "PPO training env-steps/sec (whole box)"
+UNIT = "env-steps/s"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--config", default=os.path.join(ROOT, "configs", "at_4096env_3x256.cfg"))
+    p.add_argument("--gmis", type=int, default=0, help="override GMIs per GPU")
+    p.add_argument("--envs", type=int, default=0, help="override envs per GPU")
+    p.add_argument("--backend", type=int, default=0, help="0 streams, 1 green contexts")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-sample-envs", type=int, default=64)
+    return p.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# ------------------------------------------------------------------ clocks during the timed region
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self):
+        self.proc = None
+        self.path = os.path.join(tempfile.gettempdir(), f"gmi_clocks_{os.getpid()}.csv")
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                                          "-lms", "200"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        self.proc.wait(timeout=10)
+        rows = []
+        with open(self.path) as f:
+            for line in f:
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) >= 9 and parts[1].replace(".", "").isdigit():
+                    rows.append(parts)
+        os.unlink(self.path)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[1]) for r in rows]
+        mx = max(float(r[2]) for r in rows)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower().startswith("active")})
+        loaded = [s for s in sm if s > 0.5 * mx] or sm
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": mx, "reasons": reasons,
+                "samples": len(rows)}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            j = json.load(f)
+        return j["bf16_tflops_sustained"], j["hbm_gbs"], "measured (MEASURED_PEAKS.json, sustained bf16)"
+    except (OSError, KeyError, ValueError):
+        return 1400.0, 6650.0, "fallback (B200_PROFILING.md)"
+
+
+# ------------------------------------------------------------------ CPU leg (oracle port)
+def cpu_iteration_sample(cfg, envs: int, iters: int, warmup: int):
+    """Times the CPU restatement (oracle/ppo_oracle.c, OpenMP, all host threads) on a bounded
+    sample of the same workload: `envs` environments, same MLP / horizon / epochs / minibatches."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from golden_util import PpoOracle, make_cfg  # test infrastructure: baseline leg only
+
+    threads = os.cpu_count() or 1
+    o = PpoOracle(make_cfg(cfg.obs_dim, cfg.act_dim, cfg.hidden, envs, threads=threads,
+                           horizon=cfg.horizon, epochs=cfg.epochs, minibatches=cfg.minibatches))
+    for _ in range(warmup):
+        o.iteration()
+    t0 = time.perf_counter()
+    steps = 0
+    for _ in range(iters):
+        steps += o.iteration().env_steps
+    dt = time.perf_counter() - t0
+    sample = (f"{iters} PPO iteration(s) of the same workload at {envs} envs "
+              f"({steps // max(iters, 1)} env-steps each, {cfg.epochs}x{cfg.minibatches} updates), "
+              f"oracle/ppo_oracle.c with {threads} OpenMP threads")
+    return steps / dt, threads, sample
+
+
+def run_reference(args, cfg):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    value, threads, sample = cpu_iteration_sample(cfg, args.cpu_sample_envs, args.steps, args.warmup)
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": "AT-like locomotion, 3x256 actor-critic MLP (BASELINE configs[1] shapes)",
+                       "num_envs": args.cpu_sample_envs, "note": "reference has no PPO code; oracle port timed"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ our arm
+def main():
+    args = parse()
+    from paper_2206_08482_b200.ppo import PpoConfig, Trainer, nccl_unique_id
+
+    world, rank, local = dist_env()
+    cfg = PpoConfig.from_config_file(args.config)
+    if args.gmis:
+        cfg.gmis_per_gpu = args.gmis
+    envs_per_gpu = args.envs or cfg.num_envs // max(1, cfg.num_gpus)
+    if args.impl == "reference":
+        run_reference(args, cfg)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg.num_gpus, cfg.rank, cfg.device = world, rank, local
+    cfg.num_envs = envs_per_gpu * world
+    cfg.gmi_backend = args.backend
+    cfg.instrument = 1
+    nid = None
+    if world > 1:
+        obj = [nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nid = obj[0]
+    trainer = Trainer(cfg, nid)
+    upd = torch.cuda.ExternalStream(trainer.stream(-1))
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+            torch.cuda.synchronize()
+
+    for _ in range(max(3, args.warmup)):
+        trainer.iteration()
+
+    # ---- device-timed throughput: K iterations enqueued back to back, inputs resident in HBM
+    clocks = ClockSampler()
+    if rank == 0:
+        clocks.start()
+    barrier()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record(upd)
+    launches = 0
+    gemm_ms = gemm_flop = 0.0
+    for _ in range(args.steps):
+        trainer.iteration_async()
+    t1.record(upd)
+    st = trainer.synchronize()
+    barrier()
+    clk = clocks.stop() if rank == 0 else None
+    ms = t0.elapsed_time(t1)
+    launches = st.kernel_launches * args.steps
+    gemm_ms, gemm_flop = st.gemm_ms, st.gemm_flop  # last iteration's GEMM launches (GMI 0)
+    ms_t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms_max = ms_t.item()
+    steps_total = st.env_steps * world * args.steps
+    value = steps_total / (ms_max / 1e3)
+
+    # ---- end to end through the public API: synchronous gmi_ppo_iteration per step, including
+    # the H2D of the iteration control block and the D2H read of the iteration's loss statistics.
+    barrier()
+    w0 = time.perf_counter()
+    for _ in range(args.steps):
+        trainer.iteration()
+    barrier()
+    wall = time.perf_counter() - w0
+    wall_t = torch.tensor([wall], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(wall_t, op=dist.ReduceOp.MAX)
+    e2e = steps_total / wall_t.item()
+
+    if rank == 0:
+        peak_tf, _, peak_src = measured_peaks()
+        achieved = gemm_flop / (gemm_ms / 1e3) / 1e12 if gemm_ms > 0 else 0.0
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            cv, cores, sample = cpu_iteration_sample(cfg, args.cpu_sample_envs, 1, 0)
+            cpu = {"value": cv, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample}
+        ws = working_set_mb(cfg, envs_per_gpu)
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": max(3, args.warmup), "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": f"AT-like locomotion, {envs_per_gpu} envs/GPU, "
+                                   f"{'x'.join(map(str, cfg.hidden))} actor-critic MLP, "
+                                   f"{cfg.gmis_per_gpu} GMI(s) per B200 (BASELINE configs[1])",
+                       "config_file": os.path.relpath(args.config, ROOT), "envs_per_gpu": envs_per_gpu,
+                       "obs_dim": cfg.obs_dim, "act_dim": cfg.act_dim, "hidden": cfg.hidden,
+                       "horizon": cfg.horizon, "epochs": cfg.epochs, "minibatches": cfg.minibatches,
+                       "gmis_per_gpu": cfg.gmis_per_gpu, "gmi_backend": ["streams", "green_ctx"][args.backend],
+                       "parallelism": f"dp{world * cfg.gmis_per_gpu} ({world} GPU x {cfg.gmis_per_gpu} GMI)",
+                       "env_steps_per_step": steps_total // args.steps,
+                       "l2": f"no flush: per-iteration working set ~{ws:.0f} MB > 126 MB L2"},
+            "roofline": {"bound": "tensor", "kernel": "tcgen05 bf16 GEMM (all MLP layers, GMI 0)",
+                         "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
+                         "frac": achieved / peak_tf, "traffic": None, "peak_source": peak_src,
+                         "gemm_share_of_step": (gemm_ms / (ms_max / args.steps)) if ms_max else None},
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": 16, "d2h_bytes_per_step": 32,
+                    "api": "gmi_ppo_iteration (synchronous C-ABI call per step)"},
+            "gpu_launches": launches,
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    trainer.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def working_set_mb(cfg, envs):
+    S_p = (cfg.obs_dim + 31) // 32 * 32
+    T = cfg.horizon
+    B = T * envs
+    hid = sum((h + 31) // 32 * 32 for h in cfg.hidden)
+    byt = (T + 1) * envs * S_p * 2 + B * S_p * 2  # rollout obs + epoch copy
+    byt += 2 * (B // cfg.minibatches) * hid * 2 * 2  # activations + grads, both nets
+    byt += B * (cfg.act_dim + 6) * 4
+    return byt / 1e6
+
+
+if __name__ == "__main__":
+    main()
