@@ -92,6 +92,13 @@ GMI_API int gmi_reduce_device(int strategy, int num_gpus, const int* counts, con
                               void* const* bufs, void* out, size_t len, int dtype, int broadcast,
                               void* stream);
 
+/* execute() with HOST buffers (the reference's calling convention, reduction.hpp:225):
+ * bufs[i] (len elements of dtype) belongs to the i-th id of the flattened layout; the call
+ * stages them into device memory, runs gmi_reduce_device and copies the result back to
+ * `result` (len elements). Synchronous. */
+GMI_API int gmi_execute_host(int strategy, int num_gpus, const int* counts, const int* ids,
+                             const void* const* bufs, size_t len, int dtype, void* result);
+
 /* ------------------------------------------------------------------ topology
  * topology.hpp:60-252. arch: 70, 80 or 100 (sm100 is a B200 extension).
  * backend: 0 = MPS share (realised as an SM-partitioned green context), 1 = MIG. */

@@ -132,6 +132,46 @@ void reduce_device(plan::Algo algo, const plan::Placement& p, void* const* bufs,
 
 }  // namespace gmi
 
+extern "C" GMI_API int gmi_execute_host(int strategy, int num_gpus, const int* counts, const int* ids,
+                                        const void* const* bufs, size_t len, int dtype, void* result) {
+  return gmi::guarded([&] {
+    if (strategy < 0 || strategy > 2) gmi::invalid("unknown strategy");
+    if (dtype != GMI_F32 && dtype != GMI_F64) gmi::invalid("dtype must be GMI_F32 or GMI_F64");
+    gmi::plan::Placement p;
+    if (num_gpus < 0) gmi::invalid("num_gpus must be >= 0");
+    p.per_gpu.resize(num_gpus);
+    int k = 0;
+    for (int g = 0; g < num_gpus; ++g) {
+      p.per_gpu[g].assign(ids + k, ids + k + counts[g]);
+      k += counts[g];
+    }
+    p.check();
+    const size_t esz = dtype == GMI_F64 ? 8 : 4;
+    const size_t n = p.flat().size();
+    const size_t bytes = std::max<size_t>(len * esz, 16);
+    char* arena = nullptr;
+    GMI_CUDA_CHECK(cudaMalloc(&arena, bytes * (n + 1)));
+    std::vector<void*> dev(n);
+    cudaStream_t s = nullptr;
+    try {
+      GMI_CUDA_CHECK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+      for (size_t i = 0; i < n; ++i) {
+        dev[i] = arena + i * bytes;
+        GMI_CUDA_CHECK(cudaMemcpyAsync(dev[i], bufs[i], len * esz, cudaMemcpyHostToDevice, s));
+      }
+      gmi::reduce_device(gmi::plan::Algo(strategy), p, dev.data(), arena + n * bytes, len, dtype, false, s);
+      GMI_CUDA_CHECK(cudaMemcpyAsync(result, arena + n * bytes, len * esz, cudaMemcpyDeviceToHost, s));
+      GMI_CUDA_CHECK(cudaStreamSynchronize(s));
+    } catch (...) {
+      if (s) cudaStreamDestroy(s);
+      cudaFree(arena);
+      throw;
+    }
+    cudaStreamDestroy(s);
+    cudaFree(arena);
+  });
+}
+
 extern "C" GMI_API int gmi_reduce_device(int strategy, int num_gpus, const int* counts, const int* ids,
                                          void* const* bufs, void* out, size_t len, int dtype, int broadcast,
                                          void* stream) {
