@@ -659,7 +659,7 @@ class RecordedTraceProfiler(Profiler):
         return ProfileResult(bool(ok.value), top.value, mem.value)
 
     def __del__(self):
-        if getattr(self, "_h", None):
+        if getattr(self, "_h", None) and L is not None:
             L.lib().gmi_trace_profiler_free(self._h)
             self._h = None
 
@@ -820,7 +820,7 @@ class ConfigFile:
         self._h = handle
 
     def __del__(self):
-        if getattr(self, "_h", None):
+        if getattr(self, "_h", None) and L is not None:
             L.lib().gmi_config_free(self._h)
             self._h = None
 

@@ -165,7 +165,7 @@ class Trainer:
         self.param_count, self.real_param_count = p.value, r.value
 
     def close(self):
-        if getattr(self, "_h", None):
+        if getattr(self, "_h", None) and L is not None:
             L.lib().gmi_ppo_free(self._h)
             self._h = None
 

@@ -67,11 +67,10 @@ def test_broadcast_writes_every_gmi_buffer(cuda):
 
 
 def test_mrr_rejects_oversubscribed_layout(cuda):
-    from paper_2206_08482_b200 import _lib
+    from paper_2206_08482_b200 import gmux
     bufs = [buffer_values("hash", 5, i, 8) for i in range(6)]
-    with pytest.raises(_lib.GmiError) as ei:
+    with pytest.raises(gmux.MultiStreamError, match="multiple streams per GPU: 3 rings over 2 GPUs"):
         _device_reduce(1, [[0, 1, 2], [3, 4, 5]], bufs)
-    assert ei.value.code == _lib.GMI_ERR_MULTISTREAM
 
 
 def test_execute_dropin_matches_reference_cli_example(cuda):
