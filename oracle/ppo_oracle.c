@@ -476,7 +476,8 @@ static void minibatch_grad(oracle_t* o, int gi, mb_t* mb, int Bm, const float* w
       for (int k = 0; k < th->in; ++k) {
         double acc = 0.0;
         for (int r = 0; r < Bm; ++r)
-          acc += (double)(n == 0 ? mb->gmu[(long long)r * A + a] : mb->gv[r]) * (double)hl[(long long)r * hw + k];
+          /* head weight gradients run on the tensor cores with bf16 dL/dmu, dL/dv operands */
+          acc += (double)R(n == 0 ? mb->gmu[(long long)r * A + a] : mb->gv[r]) * (double)hl[(long long)r * hw + k];
         grad[th->w + (long long)a * th->in_p + k] = (float)acc;
       }
     }

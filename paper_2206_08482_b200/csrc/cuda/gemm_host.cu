@@ -1,8 +1,9 @@
-// Host side of the tcgen05 GEMM: TMA tensor-map encoding, template dispatch and a
-// C-ABI diagnostic entry point used by the GPU parity tests.
+// Host side of the tcgen05 GEMM: TMA tensor-map encoding, tile-count based block-N choice,
+// template dispatch, and a C-ABI diagnostic entry point used by the GPU parity tests.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <mutex>
 #include <string>
 
@@ -14,10 +15,9 @@ namespace gmi {
 
 namespace {
 
-using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
-                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
-                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
-                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
 EncodeTiledFn encode_fn() {
   static EncodeTiledFn fn = nullptr;
@@ -25,8 +25,7 @@ EncodeTiledFn encode_fn() {
   std::call_once(once, [] {
     void* p = nullptr;
     cudaDriverEntryPointQueryResult q{};
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
-            cudaSuccess &&
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
         q == cudaDriverEntryPointSuccess)
       fn = reinterpret_cast<EncodeTiledFn>(p);
   });
@@ -34,118 +33,145 @@ EncodeTiledFn encode_fn() {
   return fn;
 }
 
-}  // namespace
-
-CUtensorMap make_tma_2d_bf16(const void* base, uint64_t inner, uint64_t outer, uint64_t ld_elems,
-                             uint32_t box_inner, uint32_t box_outer) {
+CUtensorMap encode(CUtensorMapDataType dt, int rank, const void* base, const cuuint64_t* dims,
+                   const cuuint64_t* strides_bytes, const cuuint32_t* box, CUtensorMapSwizzle sw) {
   if (reinterpret_cast<uintptr_t>(base) % 16 != 0) invalid("TMA base address must be 16-byte aligned");
-  if ((ld_elems * 2) % 16 != 0) invalid("TMA row pitch must be a multiple of 16 bytes");
+  for (int i = 0; i < rank - 1; ++i)
+    if (strides_bytes[i] % 16 != 0) invalid("TMA row pitch must be a multiple of 16 bytes");
   CUtensorMap map;
-  const cuuint64_t dims[2] = {inner, outer};
-  const cuuint64_t strides[1] = {ld_elems * 2};
-  const cuuint32_t box[2] = {box_inner, box_outer};
-  const cuuint32_t estride[2] = {1, 1};
-  CUresult r = encode_fn()(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims,
-                           strides, box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS)
-    fail(GMI_ERR_CUDA, "cuTensorMapEncodeTiled failed with code " + std::to_string(int(r)));
+  const cuuint32_t es[3] = {1, 1, 1};
+  const CUresult r = encode_fn()(&map, dt, cuuint32_t(rank), const_cast<void*>(base), dims, strides_bytes, box, es,
+                                 CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) fail(GMI_ERR_CUDA, "cuTensorMapEncodeTiled failed with code " + std::to_string(int(r)));
   return map;
 }
 
-void gemm_set_problem(GemmProblem& p, const GemmOperandDesc& a, const GemmOperandDesc& b, int M,
-                      int N, int K, int block_n) {
-  // A(m,k): K-major -> row-major [M x K]; MN-major -> row-major [K x M].
-  if (a.mn_major)
-    p.map_a = make_tma_2d_bf16(a.ptr, M, K, a.ld, 64, kGemmBlockK);
-  else
-    p.map_a = make_tma_2d_bf16(a.ptr, K, M, a.ld, kGemmBlockK, kGemmBlockM);
-  if (b.mn_major)
-    p.map_b = make_tma_2d_bf16(b.ptr, N, K, b.ld, 64, kGemmBlockK);
-  else
-    p.map_b = make_tma_2d_bf16(b.ptr, K, N, b.ld, kGemmBlockK, block_n);
-  p.M = M;
-  p.N = N;
-  p.K = K;
-  p.kb_per_split = (K + kGemmBlockK - 1) / kGemmBlockK;
+}  // namespace
+
+CUtensorMap make_tma_2d_bf16(const void* base, uint64_t inner, uint64_t outer, uint64_t ld, uint32_t box_inner,
+                             uint32_t box_outer) {
+  const cuuint64_t dims[2] = {inner, outer};
+  const cuuint64_t strides[1] = {ld * 2};
+  const cuuint32_t box[2] = {box_inner, box_outer};
+  return encode(CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, base, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B);
+}
+
+CUtensorMap make_tma_out_bf16(const void* base, uint64_t cols, uint64_t rows, uint64_t ld) {
+  const cuuint64_t dims[2] = {cols, rows};
+  const cuuint64_t strides[1] = {ld * 2};
+  const cuuint32_t box[2] = {32, 32};
+  return encode(CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, base, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_64B);
+}
+
+CUtensorMap make_tma_out_f32(const void* base, uint64_t cols, uint64_t rows, uint64_t splits, uint64_t ld,
+                             uint64_t split_stride) {
+  const cuuint64_t dims[3] = {cols, rows, splits};
+  const cuuint64_t strides[2] = {ld * 4, split_stride * 4};
+  const cuuint32_t box[3] = {32, 32, 1};
+  return encode(CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, base, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B);
+}
+
+CUtensorMap tma_kmajor(const void* p, int cols, long long rows, long long ld, int box_rows) {
+  return make_tma_2d_bf16(p, uint64_t(cols), uint64_t(rows), uint64_t(ld), kGemmBlockK, uint32_t(box_rows));
+}
+
+CUtensorMap tma_mnmajor(const void* p, int cols, long long rows, long long ld) {
+  return make_tma_2d_bf16(p, uint64_t(cols), uint64_t(rows), uint64_t(ld), 64, 64);
+}
+
+int device_sm_count() {
+  int dev = 0, n = 0;
+  GMI_CUDA_CHECK(cudaGetDevice(&dev));
+  GMI_CUDA_CHECK(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
+  return n;
+}
+
+int gemm_tiles(int M, int N, int bn, int problems, int splits) {
+  return ((M + kGemmBlockM - 1) / kGemmBlockM) * ((N + bn - 1) / bn) * problems * splits;
+}
+
+int gemm_choose_bn(int M, int N, int problems, int splits, int sms) {
+  const int cands[3] = {256, 128, 64};
+  for (int bn : cands) {
+    if (bn > ((N + 63) / 64) * 64) continue;
+    if (gemm_tiles(M, N, bn, problems, splits) >= 4 * sms) return bn;
+  }
+  return 64;
 }
 
 namespace {
 
-template <int BN, int ST, int AMN, int BMN, int EPI>
-void launch_t(const GemmParams& P, dim3 grid, cudaStream_t s) {
-  constexpr int smem = gemm_smem_bytes<BN, ST>();
-  auto kern = gemm_tcgen05_kernel<BN, ST, AMN, BMN, EPI>;
+template <int BN, int AMN, int BMN, int EPI>
+void launch_t(const GemmParams& P, int ctas, cudaStream_t s) {
+  constexpr int smem = GemmSmem<BN>::kBytes;
+  auto kern = gemm_tcgen05_kernel<BN, AMN, BMN, EPI>;
   static bool configured = false;  // per instantiation
   if (!configured) {
     GMI_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     configured = true;
   }
-  kern<<<grid, 128, smem, s>>>(P);
+  kern<<<ctas, kGemmThreads, smem, s>>>(P);
   GMI_CUDA_CHECK(cudaGetLastError());
 }
 
-template <int BN, int ST>
-void launch_bn(const GemmParams& P, int a_mn, int b_mn, int epi, dim3 grid, cudaStream_t s) {
+template <int BN>
+void launch_bn(const GemmParams& P, int a_mn, int b_mn, int epi, int ctas, cudaStream_t s) {
   const int key = a_mn * 100 + b_mn * 10 + epi;
   switch (key) {
-    case 0 * 100 + 0 * 10 + EPI_BIAS_ELU: return launch_t<BN, ST, 0, 0, EPI_BIAS_ELU>(P, grid, s);
-    case 0 * 100 + 0 * 10 + EPI_F32: return launch_t<BN, ST, 0, 0, EPI_F32>(P, grid, s);
-    case 0 * 100 + 0 * 10 + EPI_DACT: return launch_t<BN, ST, 0, 0, EPI_DACT>(P, grid, s);
-    case 0 * 100 + 1 * 10 + EPI_DACT: return launch_t<BN, ST, 0, 1, EPI_DACT>(P, grid, s);
-    case 0 * 100 + 1 * 10 + EPI_F32: return launch_t<BN, ST, 0, 1, EPI_F32>(P, grid, s);
-    case 1 * 100 + 1 * 10 + EPI_F32: return launch_t<BN, ST, 1, 1, EPI_F32>(P, grid, s);
-    case 1 * 100 + 0 * 10 + EPI_F32: return launch_t<BN, ST, 1, 0, EPI_F32>(P, grid, s);
+    case 0 * 100 + 0 * 10 + EPI_BIAS_ELU: return launch_t<BN, 0, 0, EPI_BIAS_ELU>(P, ctas, s);
+    case 0 * 100 + 0 * 10 + EPI_F32: return launch_t<BN, 0, 0, EPI_F32>(P, ctas, s);
+    case 0 * 100 + 0 * 10 + EPI_DACT: return launch_t<BN, 0, 0, EPI_DACT>(P, ctas, s);
+    case 0 * 100 + 1 * 10 + EPI_DACT: return launch_t<BN, 0, 1, EPI_DACT>(P, ctas, s);
+    case 0 * 100 + 1 * 10 + EPI_F32: return launch_t<BN, 0, 1, EPI_F32>(P, ctas, s);
+    case 1 * 100 + 1 * 10 + EPI_F32: return launch_t<BN, 1, 1, EPI_F32>(P, ctas, s);
+    case 1 * 100 + 0 * 10 + EPI_F32: return launch_t<BN, 1, 0, EPI_F32>(P, ctas, s);
     default: invalid("unsupported GEMM operand-major / epilogue combination");
   }
 }
 
 }  // namespace
 
-void gemm_launch(const GemmParams& P, int block_n, int a_mn, int b_mn, int epi, cudaStream_t s) {
-  int max_m = 0, max_n = 0;
-  for (int i = 0; i < P.num_problems; ++i) {
-    max_m = P.prob[i].M > max_m ? P.prob[i].M : max_m;
-    max_n = P.prob[i].N > max_n ? P.prob[i].N : max_n;
-  }
-  dim3 grid((max_m + kGemmBlockM - 1) / kGemmBlockM, (max_n + block_n - 1) / block_n,
-            P.num_problems * P.splits);
-  switch (block_n) {
-    case 64: return launch_bn<64, 4>(P, a_mn, b_mn, epi, grid, s);
-    case 128: return launch_bn<128, 4>(P, a_mn, b_mn, epi, grid, s);
-    case 256: return launch_bn<256, 4>(P, a_mn, b_mn, epi, grid, s);
+void gemm_launch(const GemmParams& P, int bn, int a_mn, int b_mn, int epi, cudaStream_t s, int max_ctas) {
+  static int sms = 0;
+  if (!sms) sms = device_sm_count();
+  for (int i = 1; i < P.num_problems; ++i)
+    if (P.prob[i].M != P.prob[0].M || P.prob[i].N != P.prob[0].N || P.prob[i].K != P.prob[0].K)
+      invalid("grouped GEMM problems must share M, N, K");
+  const int tiles = gemm_tiles(P.prob[0].M, P.prob[0].N, bn, P.num_problems, P.splits);
+  const int ctas = std::max(1, std::min(tiles, max_ctas > 0 ? max_ctas : sms));
+  switch (bn) {
+    case 64: return launch_bn<64>(P, a_mn, b_mn, epi, ctas, s);
+    case 128: return launch_bn<128>(P, a_mn, b_mn, epi, ctas, s);
+    case 256: return launch_bn<256>(P, a_mn, b_mn, epi, ctas, s);
     default: invalid("GEMM block_n must be 64, 128 or 256");
   }
 }
 
-int gemm_pick_block_n(int N) {
-  if (N <= 64) return 64;
-  if (N <= 128) return 128;
-  return 256;
-}
-
 }  // namespace gmi
 
-extern "C" int gmi_dev_gemm(int a_mn, int b_mn, int epi, int M, int N, int K, const void* A,
-                            long long lda, const void* B, long long ldb, void* out, long long ldo,
-                            const float* bias, const void* aux, long long ld_aux, int splits,
-                            void* stream) {
+extern "C" GMI_API int gmi_dev_gemm(int a_mn, int b_mn, int epi, int M, int N, int K, const void* A, long long lda,
+                                    const void* B, long long ldb, void* out, long long ldo, const float* bias,
+                                    const void* aux, long long ld_aux, int splits, void* stream) {
   return gmi::guarded([&] {
     if (M <= 0 || N <= 0 || K <= 0) gmi::invalid("gemm dims must be positive");
     if (N % 32 != 0) gmi::invalid("gemm N must be a multiple of 32");
     if (splits < 1) gmi::invalid("splits must be >= 1");
+    const int bn = gmi::gemm_choose_bn(M, N, 1, splits, gmi::device_sm_count());
     gmi::GemmParams P{};
-    const int bn = gmi::gemm_pick_block_n(N);
-    gmi::gemm_set_problem(P.prob[0], {A, lda, a_mn != 0}, {B, ldb, b_mn != 0}, M, N, K, bn);
+    gmi::GemmProblem& p = P.prob[0];
+    p.map_a = a_mn ? gmi::tma_mnmajor(A, M, K, lda) : gmi::tma_kmajor(A, K, M, lda, gmi::kGemmBlockM);
+    p.map_b = b_mn ? gmi::tma_mnmajor(B, N, K, ldb) : gmi::tma_kmajor(B, K, N, ldb, bn);
+    p.map_out = epi == gmi::EPI_F32 ? gmi::make_tma_out_f32(out, N, M, splits, ldo, (uint64_t)M * ldo)
+                                    : gmi::make_tma_out_bf16(out, N, M, ldo);
+    p.M = M;
+    p.N = N;
+    p.K = K;
     const int nkb = (K + gmi::kGemmBlockK - 1) / gmi::kGemmBlockK;
-    P.prob[0].kb_per_split = (nkb + splits - 1) / splits;
-    P.prob[0].out = out;
-    P.prob[0].ld_out = ldo;
-    P.prob[0].bias = bias;
-    P.prob[0].aux = static_cast<const __nv_bfloat16*>(aux);
-    P.prob[0].ld_aux = ld_aux;
-    P.prob[0].split_stride = static_cast<int64_t>(M) * ldo;
+    p.kb_per_split = (nkb + splits - 1) / splits;
+    p.bias = bias;
+    p.aux = static_cast<const __nv_bfloat16*>(aux);
+    p.ld_aux = ld_aux;
     P.num_problems = 1;
     P.splits = splits;
     gmi::gemm_launch(P, bn, a_mn, b_mn, epi, static_cast<cudaStream_t>(stream));

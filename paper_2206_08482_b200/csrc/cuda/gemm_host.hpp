@@ -10,21 +10,26 @@
 
 namespace gmi {
 
-struct GemmOperandDesc {
-  const void* ptr;
-  long long ld;   // elements between consecutive rows of the stored matrix
-  bool mn_major;  // false: stored [rows x K]; true: stored [K x rows]
-};
-
+// Operand map: bf16 [outer rows x inner cols] with row pitch ld (elements), 128B swizzle.
 CUtensorMap make_tma_2d_bf16(const void* base, uint64_t inner, uint64_t outer, uint64_t ld_elems,
                              uint32_t box_inner, uint32_t box_outer);
+// bf16 output map [rows x cols], box 32 x 32, 64B swizzle (epilogue staging layout).
+CUtensorMap make_tma_out_bf16(const void* base, uint64_t cols, uint64_t rows, uint64_t ld_elems);
+// fp32 split-K output map [splits][M][N] (split stride in elements), box 32 x 32 x 1, 128B swizzle.
+CUtensorMap make_tma_out_f32(const void* base, uint64_t cols, uint64_t rows, uint64_t splits, uint64_t ld_elems,
+                             uint64_t split_stride);
 
-// Fills the tensor maps and shape of one problem (kb_per_split = all k-blocks).
-void gemm_set_problem(GemmProblem& p, const GemmOperandDesc& a, const GemmOperandDesc& b, int M,
-                      int N, int K, int block_n);
+// K-major operand map for A (box rows = 128) or B (box rows = bn); MN-major map (box 64 x 64).
+CUtensorMap tma_kmajor(const void* p, int cols, long long rows, long long ld, int box_rows);
+CUtensorMap tma_mnmajor(const void* p, int cols, long long rows, long long ld);
 
-void gemm_launch(const GemmParams& P, int block_n, int a_mn, int b_mn, int epi, cudaStream_t s);
+// Launches the persistent kernel with min(tiles, max_ctas) CTAs (max_ctas 0 = SM count).
+void gemm_launch(const GemmParams& P, int bn, int a_mn, int b_mn, int epi, cudaStream_t s, int max_ctas = 0);
 
-int gemm_pick_block_n(int N);
+// Block N for a launch: the largest of {256,128,64} (<= padded N) that still gives at
+// least 4 tiles per SM, else the smallest.
+int gemm_choose_bn(int M, int N, int problems, int splits, int sms);
+int gemm_tiles(int M, int N, int bn, int problems, int splits);
+int device_sm_count();
 
 }  // namespace gmi

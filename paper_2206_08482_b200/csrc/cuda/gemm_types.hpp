@@ -12,22 +12,24 @@ enum GemmEpi : int { EPI_BIAS_ELU = 0, EPI_DACT = 1, EPI_F32 = 2 };
 
 constexpr int kGemmBlockM = 128;
 constexpr int kGemmBlockK = 64;  // one 128-byte swizzle atom of bf16
+constexpr int kGemmEpiWarps = 8;
+constexpr int kGemmThreads = 64 + 32 * kGemmEpiWarps;  // TMA warp, MMA warp, epilogue warps
 
 struct alignas(64) GemmProblem {
   CUtensorMap map_a;
   CUtensorMap map_b;
-  void* out;
+  CUtensorMap map_out;  // bf16 2-D {N, rows} box {32,32} SW64, or fp32 3-D {N, M, splits} box {32,32,1} SW128
   const float* bias;
   const __nv_bfloat16* aux;
-  int64_t ld_out;
   int64_t ld_aux;
-  int64_t split_stride;  // elements between split-K output slabs (EPI_F32)
   int M, N, K;
   int kb_per_split;
-  int a_row0;  // offset added to A's stored-row coordinate (M for K-major, K for MN-major)
-  int b_row0;  // offset added to B's stored-row coordinate (N for K-major, K for MN-major)
+  int a_row0;    // offset added to A's stored-row coordinate (M for K-major, K for MN-major)
+  int b_row0;    // offset added to B's stored-row coordinate (N for K-major, K for MN-major)
+  int out_row0;  // offset added to the output row coordinate (bf16 outputs)
 };
 
+// All problems of one launch share M, N, K and the split count (grouped GEMM).
 struct alignas(64) GemmParams {
   GemmProblem prob[2];
   int num_problems;

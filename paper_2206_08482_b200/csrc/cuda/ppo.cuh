@@ -5,6 +5,8 @@
 //               act[T][N][A], logp/rew[T][N] fp32, done[T][N] u8, V[(T+1)][N] fp32
 //   advantages  adv/ret[T][N] fp32, normalised in the epoch shuffle
 //   epoch copy  X_sh[B][S_p] bf16, act_sh[B][A], oldlp/adv/ret_sh[B]  (B = T*N, permuted)
+//   head grads  G_pi[Bm][64] / G_v[Bm][64] bf16 (dL/dmu, dL/dv; zero pads) for the
+//               tensor-core head weight-gradient GEMM
 #pragma once
 
 #include <cuda_bf16.h>
@@ -12,9 +14,13 @@
 
 #include <cstdint>
 
+#include "rng.cuh"  // GMI_HD
+
 namespace gmi::ppo {
 
-constexpr int kMaxAct = 32;
+constexpr int kMaxAct = 31;  // lane 31 carries the value head in the head kernel
+constexpr int kMaxHeadIn = 512;
+constexpr int kHeadG = 64;  // padded width of the G_pi / G_v buffers
 
 // Device-resident control block, refreshed by the host (H2D) once per iteration.
 struct Control {
@@ -65,15 +71,16 @@ struct HeadLossArgs {
   const float* ret;
   __nv_bfloat16* Dpi;  // [B][hp] dPre of the last hidden layer
   __nv_bfloat16* Dv;
-  float* partial;      // [blocks][partial_stride]
-  int partial_stride;
+  __nv_bfloat16* Gpi;  // [B][64] dL/dmu (bf16), input of the head weight-gradient GEMM
+  __nv_bfloat16* Gv;   // [B][64] dL/dv in column 0
+  float* partial;      // [blocks][head_partial_stride(A)]
   int B, A;
   float clip, vf_coef, ent_coef;
 };
 
-// Sizes of one head-loss partial record.
-inline int head_partial_stride(int A, int hp) { return A * hp + hp + A + 1 + A + 4; }
-constexpr int kHeadRowsPerBlock = 128;
+// One head-loss partial record: db_mu[A], db_v, dlog_std[A], 4 loss statistics.
+GMI_HD constexpr int head_partial_stride(int A) { return 2 * A + 5; }
+constexpr int kHeadRowsPerBlock = 64;
 
 struct Segment {  // dst[i] = sum_{p < nparts} src[p * stride + i]  (fixed order)
   float* dst;

@@ -13,6 +13,7 @@
 
 #include "../host/errors.hpp"
 #include "ppo.cuh"
+#include "ppo_common.cuh"
 #include "rng.cuh"
 
 namespace gmi::ppo {
@@ -20,38 +21,9 @@ namespace gmi::ppo {
 namespace {
 
 constexpr float kDt = 0.05f, kDamp = 1.0f, kCouple = 0.1f, kCtrl = 0.1f, kStateC = 0.1f;
-constexpr float kLog2PiHalf = 0.91893853320467274f;
 constexpr float kTwoPi = 6.28318530717958648f;
 constexpr int kMaxObsPerLane = 8;  // S <= 256
 
-__device__ __forceinline__ float warp_sum(float v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
-}
-
-__device__ __forceinline__ float elu_grad(float h) { return h > 0.f ? 1.f : h + 1.f; }
-
-__device__ __forceinline__ void load8(const __nv_bfloat16* p, float (&f)[8]) {
-  const uint4 u = *reinterpret_cast<const uint4*>(p);
-  const uint32_t w[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const __nv_bfloat162 b = *reinterpret_cast<const __nv_bfloat162*>(&w[i]);
-    f[2 * i] = __bfloat162float(b.x);
-    f[2 * i + 1] = __bfloat162float(b.y);
-  }
-}
-
-__device__ __forceinline__ void store8(__nv_bfloat16* p, const float (&f)[8]) {
-  uint32_t w[4];
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    __nv_bfloat162 b = __floats2bfloat162_rn(f[2 * i], f[2 * i + 1]);
-    w[i] = *reinterpret_cast<uint32_t*>(&b);
-  }
-  *reinterpret_cast<uint4*>(p) = make_uint4(w[0], w[1], w[2], w[3]);
-}
 
 // Reset state x[0..S) of env `gid` for episode `count`: U(-0.1, 0.1), bit-exact vs oracle.
 __device__ __forceinline__ float reset_value(uint64_t seed, int gid, int count, int i) {
@@ -84,42 +56,34 @@ __global__ void env_init_kernel(EnvParams ep, float* x, int* ep_step, int* ep_le
 // actions, synthetic Ant-like dynamics, reward, integer episode clock / reset, and the
 // next GEMM-ready observation row. Traffic/env: H_L row (2*hp B) + 2*S*4 (state) + 2*S_p
 // (obs) + (A+3)*4 B.
-template <int MAXA>
+template <int NV>
 __global__ void __launch_bounds__(256) act_env_kernel(const ActEnvArgs a) {
+  extern __shared__ float w_s[];  // [A][hp] policy head weights, staged once per block
   const int lane = threadIdx.x & 31;
-  const int e = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const EnvParams& ep = a.ep;
+  const int A = ep.A, S = ep.S, hp = a.hp;
+  for (int i = threadIdx.x; i < A * hp; i += blockDim.x) w_s[i] = a.w_mu[i];
+  __syncthreads();
+  const int e = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (e >= ep.N) return;
-  const int A = ep.A, S = ep.S;
   const int gid = ep.env0 + e;
 
-  // mu: lanes split the hidden dimension in 8-wide chunks
-  float part[MAXA];
+  // mu: lane owns hidden units k = 2*lane + 64 j (+1); transpose-reduce across the warp
+  float part[NV];
 #pragma unroll
-  for (int i = 0; i < MAXA; ++i) part[i] = 0.f;
-  const __nv_bfloat16* hrow = a.H + (long long)e * a.hp;
-  for (int k = lane * 8; k < a.hp; k += 256) {
-    float h[8];
-    load8(hrow + k, h);
+  for (int i = 0; i < NV; ++i) part[i] = 0.f;
+  const __nv_bfloat16* hrow = a.H + (long long)e * hp;
+  for (int k = 2 * lane; k < hp; k += 64) {
+    const float2 h = ld_bf16x2(hrow + k);
 #pragma unroll
-    for (int i = 0; i < MAXA; ++i) {
+    for (int i = 0; i < NV; ++i)
       if (i < A) {
-        const float* w = a.w_mu + (long long)i * a.hp + k;
-        float s = part[i];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) s += h[j] * w[j];
-        part[i] = s;
+        const float2 w = *reinterpret_cast<const float2*>(w_s + i * hp + k);
+        part[i] += h.x * w.x + h.y * w.y;
       }
-    }
   }
-  float mu_mine = 0.f;
-#pragma unroll
-  for (int i = 0; i < MAXA; ++i) {
-    if (i < A) {
-      const float m = warp_sum(part[i]) + a.b_mu[i];
-      if (i == lane) mu_mine = m;
-    }
-  }
+  const float red = warp_reduce_transpose<NV>(part);
+  const float mu_mine = lane < A ? red + a.b_mu[lane] : 0.f;
 
   // N(0,1) noise: lane q draws Philox block q -> 4 normals for actions 4q..4q+3
   const uint32_t step = uint32_t(a.ctl->iteration * ep.T + a.t);
@@ -349,188 +313,6 @@ __global__ void __launch_bounds__(256) shuffle_kernel(const __nv_bfloat16* X_rol
   }
 }
 
-// ------------------------------------------------------------------ K6 head + PPO loss (+ head backward)
-template <int MAXA>
-__global__ void __launch_bounds__(256) head_loss_kernel(const HeadLossArgs a) {
-  __shared__ float gmu_s[kHeadRowsPerBlock][MAXA + 1];
-  __shared__ float gv_s[kHeadRowsPerBlock];
-  __shared__ float red_s[8][MAXA + 4];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int A = a.A, hp = a.hp;
-  const int r0 = blockIdx.x * kHeadRowsPerBlock;
-  const float invB = 1.0f / float(a.B);
-
-  float gls_acc = 0.f;  // lane a: sum over this warp's rows of dL/dlog_std_a
-  float st_pi = 0.f, st_v = 0.f, st_kl = 0.f, st_clip = 0.f;
-  const float ls_mine = lane < A ? a.log_std[lane] : 0.f;
-  const float sig_mine = expf(ls_mine);
-
-  for (int rr = warp; rr < kHeadRowsPerBlock; rr += 8) {
-    const int r = r0 + rr;
-    if (r >= a.B) {
-      if (lane < MAXA + 1 && lane <= A) gmu_s[rr][lane < A ? lane : MAXA] = 0.f;
-      if (lane == 0) gv_s[rr] = 0.f;
-      continue;
-    }
-    float part[MAXA];
-#pragma unroll
-    for (int i = 0; i < MAXA; ++i) part[i] = 0.f;
-    float pv = 0.f;
-    for (int k = lane * 8; k < hp; k += 256) {
-      float h[8], hv[8];
-      load8(a.Hpi + (long long)r * hp + k, h);
-      load8(a.Hv + (long long)r * hp + k, hv);
-#pragma unroll
-      for (int j = 0; j < 8; ++j) pv += hv[j] * a.w_v[k + j];
-#pragma unroll
-      for (int i = 0; i < MAXA; ++i)
-        if (i < A) {
-          const float* w = a.w_mu + (long long)i * hp + k;
-          float s = part[i];
-#pragma unroll
-          for (int j = 0; j < 8; ++j) s += h[j] * w[j];
-          part[i] = s;
-        }
-    }
-    float mu_mine = 0.f;
-#pragma unroll
-    for (int i = 0; i < MAXA; ++i)
-      if (i < A) {
-        const float m = warp_sum(part[i]) + a.b_mu[i];
-        if (i == lane) mu_mine = m;
-      }
-    const float v = warp_sum(pv) + a.b_v[0];
-    float z = 0.f, term = 0.f;
-    if (lane < A) {
-      z = (a.act[(long long)r * A + lane] - mu_mine) / sig_mine;
-      term = -0.5f * z * z - ls_mine - kLog2PiHalf;
-    }
-    const float lp = warp_sum(term);
-    const float oldlp = a.oldlp[r], adv = a.adv[r];
-    const float ratio = expf(lp - oldlp);
-    const float s1 = ratio * adv;
-    const float rc = fminf(fmaxf(ratio, 1.f - a.clip), 1.f + a.clip);
-    const float s2 = rc * adv;
-    const bool take1 = s1 <= s2;
-    const float glp = take1 ? -s1 * invB : 0.f;
-    const float verr = v - a.ret[r];
-    const float gv = a.vf_coef * verr * invB;
-    float gmu = 0.f;
-    if (lane < A) {
-      gmu = glp * z / sig_mine;
-      gls_acc += glp * (z * z - 1.f) - a.ent_coef * invB;
-      gmu_s[rr][lane] = gmu;
-    }
-    if (lane == 0) {
-      gv_s[rr] = gv;
-      st_pi += -(take1 ? s1 : s2);
-      st_v += 0.5f * a.vf_coef * verr * verr;
-      st_kl += oldlp - lp;
-      st_clip += (ratio < 1.f - a.clip || ratio > 1.f + a.clip) ? 1.f : 0.f;
-    }
-    // head backward into the last hidden layer: dPre = (g W) * elu'(H), stored bf16
-    float g_all[MAXA];
-#pragma unroll
-    for (int i = 0; i < MAXA; ++i) g_all[i] = i < A ? __shfl_sync(0xffffffffu, gmu, i) : 0.f;
-    for (int k = lane * 8; k < hp; k += 256) {
-      float h[8], hv[8], dp[8], dv[8];
-      load8(a.Hpi + (long long)r * hp + k, h);
-      load8(a.Hv + (long long)r * hp + k, hv);
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        float acc = 0.f;
-#pragma unroll
-        for (int i = 0; i < MAXA; ++i)
-          if (i < A) acc += g_all[i] * a.w_mu[(long long)i * hp + k + j];
-        dp[j] = acc * elu_grad(h[j]);
-        dv[j] = (gv * a.w_v[k + j]) * elu_grad(hv[j]);
-      }
-      store8(a.Dpi + (long long)r * hp + k, dp);
-      store8(a.Dv + (long long)r * hp + k, dv);
-    }
-  }
-  if (lane < A) red_s[warp][lane] = gls_acc;
-  if (lane == 0) {
-    red_s[warp][MAXA] = st_pi;
-    red_s[warp][MAXA + 1] = st_v;
-    red_s[warp][MAXA + 2] = st_kl;
-    red_s[warp][MAXA + 3] = st_clip;
-  }
-  __syncthreads();
-
-  // block partials of the head weight gradients (rows of this block), fixed order
-  float* out = a.partial + (long long)blockIdx.x * a.partial_stride;
-  const int rows = min(kHeadRowsPerBlock, a.B - r0);
-  for (int k = threadIdx.x; k < hp; k += blockDim.x) {
-    float acc[MAXA];
-#pragma unroll
-    for (int i = 0; i < MAXA; ++i) acc[i] = 0.f;
-    float accv = 0.f;
-    for (int rr = 0; rr < rows; ++rr) {
-      const float h = __bfloat162float(a.Hpi[(long long)(r0 + rr) * hp + k]);
-      const float hv = __bfloat162float(a.Hv[(long long)(r0 + rr) * hp + k]);
-#pragma unroll
-      for (int i = 0; i < MAXA; ++i)
-        if (i < A) acc[i] += gmu_s[rr][i] * h;
-      accv += gv_s[rr] * hv;
-    }
-#pragma unroll
-    for (int i = 0; i < MAXA; ++i)
-      if (i < A) out[(long long)i * hp + k] = acc[i];
-    out[(long long)A * hp + k] = accv;
-  }
-  float* tail = out + (long long)A * hp + hp;
-  if (threadIdx.x < A) {
-    float s = 0.f;
-    for (int rr = 0; rr < rows; ++rr) s += gmu_s[rr][threadIdx.x];
-    tail[threadIdx.x] = s;
-    float l = 0.f;
-    for (int w = 0; w < 8; ++w) l += red_s[w][threadIdx.x];
-    tail[A + 1 + threadIdx.x] = l;
-  } else if (threadIdx.x == 32) {
-    float s = 0.f;
-    for (int rr = 0; rr < rows; ++rr) s += gv_s[rr];
-    tail[A] = s;
-  } else if (threadIdx.x >= 64 && threadIdx.x < 68) {
-    float s = 0.f;
-    for (int w = 0; w < 8; ++w) s += red_s[w][MAXA + (threadIdx.x - 64)];
-    tail[2 * A + 1 + (threadIdx.x - 64)] = s;
-  }
-}
-
-// ------------------------------------------------------------------ bias-gradient column sums
-constexpr int kColsumRows = 256;
-struct ColsumArgs {
-  const __nv_bfloat16* D[16];
-  float* out[16];
-  int width[16];
-};
-__global__ void __launch_bounds__(256) colsum_kernel(const ColsumArgs a, int rows) {
-  const int p = blockIdx.y;
-  const int w = a.width[p];
-  const int r0 = blockIdx.x * kColsumRows;
-  const int r1 = min(rows, r0 + kColsumRows);
-  for (int j = threadIdx.x; j < w; j += blockDim.x) {
-    float s = 0.f;
-    for (int r = r0; r < r1; ++r) s += __bfloat162float(a.D[p][(long long)r * w + j]);
-    a.out[p][(long long)blockIdx.x * w + j] = s;
-  }
-}
-
-// ------------------------------------------------------------------ gradient assembly
-constexpr int kMaxSegments = 64;
-struct SegmentTable {
-  Segment s[kMaxSegments];
-};
-__global__ void __launch_bounds__(256) segments_kernel(const __grid_constant__ SegmentTable t) {
-  const Segment& sg = t.s[blockIdx.y];
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < sg.len; i += gridDim.x * blockDim.x) {
-    float acc = 0.f;
-    for (int p = 0; p < sg.nparts; ++p) acc += sg.src[(long long)p * sg.stride + i];
-    sg.dst[i] = acc;
-  }
-}
-
 // ------------------------------------------------------------------ K8 Adam (fp32 master + bf16 shadow)
 // 28 B/param of algorithmic traffic: read p, m, v, g; write p, m, v, shadow(2 B).
 __global__ void __launch_bounds__(256) adam_kernel(const AdamArgs a) {
@@ -551,10 +333,6 @@ __global__ void __launch_bounds__(256) adam_kernel(const AdamArgs a) {
   }
 }
 
-int grid_for(long long work, int block, int cap) {
-  return int(std::max<long long>(1, std::min<long long>((work + block - 1) / block, cap)));
-}
-
 }  // namespace
 
 void launch_env_init(const EnvParams& ep, float* x, int* ep_step, int* ep_len, int* ep_count, __nv_bfloat16* X0,
@@ -564,15 +342,22 @@ void launch_env_init(const EnvParams& ep, float* x, int* ep_step, int* ep_len, i
 }
 
 void launch_act_env(const ActEnvArgs& a, cudaStream_t s) {
-  if (a.ep.A > kMaxAct) invalid("act_dim > 32 unsupported by the act/env kernel");
+  if (a.ep.A > kMaxAct) invalid("act_dim > 31 unsupported by the act/env kernel");
   if (a.ep.S > 32 * kMaxObsPerLane) invalid("obs_dim > 256 unsupported by the act/env kernel");
+  if (a.hp > kMaxHeadIn) invalid("last hidden width > 512 unsupported by the act/env kernel");
   const int blocks = (a.ep.N * 32 + 255) / 256;
+  const size_t smem = size_t(a.ep.A) * a.hp * 4;
+  auto go = [&](auto kern) {
+    if (smem > 48 * 1024)
+      GMI_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    kern<<<blocks, 256, smem, s>>>(a);
+  };
   if (a.ep.A <= 8)
-    act_env_kernel<8><<<blocks, 256, 0, s>>>(a);
+    go(act_env_kernel<8>);
   else if (a.ep.A <= 16)
-    act_env_kernel<16><<<blocks, 256, 0, s>>>(a);
+    go(act_env_kernel<16>);
   else
-    act_env_kernel<32><<<blocks, 256, 0, s>>>(a);
+    go(act_env_kernel<32>);
   GMI_CUDA_CHECK(cudaGetLastError());
 }
 
@@ -607,47 +392,17 @@ void launch_shuffle(const __nv_bfloat16* X_roll, const float* act, const float* 
   GMI_CUDA_CHECK(cudaGetLastError());
 }
 
-int head_loss_blocks(int B) { return (B + kHeadRowsPerBlock - 1) / kHeadRowsPerBlock; }
-
-void launch_head_loss(const HeadLossArgs& a, cudaStream_t s) {
-  if (a.A > kMaxAct) invalid("act_dim > 32 unsupported by the head kernel");
-  const int blocks = head_loss_blocks(a.B);
-  if (a.A <= 8)
-    head_loss_kernel<8><<<blocks, 256, 0, s>>>(a);
-  else if (a.A <= 16)
-    head_loss_kernel<16><<<blocks, 256, 0, s>>>(a);
-  else
-    head_loss_kernel<32><<<blocks, 256, 0, s>>>(a);
-  GMI_CUDA_CHECK(cudaGetLastError());
+namespace {
+__global__ void control_advance_kernel(Control* c, int dsteps) {
+  c->iteration += 1;
+  c->adam_step0 += dsteps;
 }
+}  // namespace
 
-int colsum_blocks(int rows) { return (rows + kColsumRows - 1) / kColsumRows; }
-
-void launch_colsum(const __nv_bfloat16* const* D, const int* widths, float* const* partial, int np, int rows,
-                   cudaStream_t s) {
-  if (np > 16) invalid("too many column-sum problems");
-  ColsumArgs a{};
-  for (int i = 0; i < np; ++i) {
-    a.D[i] = D[i];
-    a.out[i] = partial[i];
-    a.width[i] = widths[i];
-  }
-  colsum_kernel<<<dim3(colsum_blocks(rows), np), 256, 0, s>>>(a, rows);
+// Device-side end-of-iteration bookkeeping, so a captured iteration graph can be replayed.
+void launch_control_advance(Control* c, int dsteps, cudaStream_t s) {
+  control_advance_kernel<<<1, 1, 0, s>>>(c, dsteps);
   GMI_CUDA_CHECK(cudaGetLastError());
-}
-
-void launch_segments(const Segment* segs, int n, cudaStream_t s) {
-  for (int base = 0; base < n; base += kMaxSegments) {
-    SegmentTable t{};
-    const int m = std::min(kMaxSegments, n - base);
-    int maxlen = 1;
-    for (int i = 0; i < m; ++i) {
-      t.s[i] = segs[base + i];
-      maxlen = std::max(maxlen, t.s[i].len);
-    }
-    segments_kernel<<<dim3(grid_for(maxlen, 256, 64), m), 256, 0, s>>>(t);
-    GMI_CUDA_CHECK(cudaGetLastError());
-  }
 }
 
 void launch_adam(const AdamArgs& a, cudaStream_t s) {

@@ -7,10 +7,13 @@
 //   values    ceil((T+1)N / M) x [L GEMMs (value net) + value head]
 //   GAE       warp-shuffle scan + advantage statistics
 //   update    E epochs x [shuffle + K minibatches x (L fwd GEMMs (both nets grouped),
-//             head/loss, L weight-grad GEMMs + L-1 input-grad GEMMs, bias sums, gradient
-//             assembly)]; after each minibatch the update stream folds the GMIs'
-//             gradients (K1, reference fold order), all-reduces across GPUs (NCCL) and
-//             runs Adam once on the GPU's shared replica.
+//             head/loss, head weight-grad GEMM, L weight-grad GEMMs + L-1 input-grad GEMMs,
+//             bias sums, gradient assembly)]; after each minibatch the update stream folds
+//             the GMIs' gradients (K1, reference fold order), all-reduces across GPUs (NCCL)
+//             and runs Adam once on the GPU's shared replica.
+// From the second iteration on, the whole sequence (all GMI streams, events, NCCL) is
+// replayed from one captured CUDA graph; a device-side control block carries the
+// iteration counter so the graph is iteration-agnostic.
 #include "trainer.hpp"
 
 #include <nccl.h>
@@ -28,6 +31,9 @@ namespace gmi {
 
 void reduce_device(plan::Algo algo, const plan::Placement& p, void* const* bufs, void* out, size_t len, int dtype,
                    bool broadcast, cudaStream_t stream);
+namespace ppo {
+void launch_control_advance(Control* c, int dsteps, cudaStream_t s);
+}
 
 namespace {
 
@@ -49,18 +55,20 @@ float bf16_float(uint16_t b) {
   return f;
 }
 
-#define NCCL_CHECK(expr)                                                                           \
-  do {                                                                                             \
-    ncclResult_t _r = (expr);                                                                      \
+#define NCCL_CHECK(expr)                                                                                  \
+  do {                                                                                                    \
+    ncclResult_t _r = (expr);                                                                             \
     if (_r != ncclSuccess) ::gmi::fail(GMI_ERR_NCCL, std::string(#expr) + ": " + ncclGetErrorString(_r)); \
   } while (0)
 
-CUtensorMap kmaj(const void* p, int cols, long long rows, long long ld, int box_rows) {
-  return make_tma_2d_bf16(p, uint64_t(cols), uint64_t(rows), uint64_t(ld), 64, uint32_t(box_rows));
-}
-
-CUtensorMap mnmaj(const void* p, int cols, long long rows, long long ld) {
-  return make_tma_2d_bf16(p, uint64_t(cols), uint64_t(rows), uint64_t(ld), 64, 64);
+// Splits of the weight-gradient GEMM: enough k-slabs to give ~one tile per SM.
+void pick_splits(int M, int N, int bn, int problems, int rows, int sms, int* splits, int* kbps) {
+  const int base = gemm_tiles(M, N, bn, problems, 1);
+  const int nkb = (rows + kGemmBlockK - 1) / kGemmBlockK;
+  const int s = std::max(1, std::min(nkb, sms / std::max(1, base)));
+  const int per = (nkb + s - 1) / s;
+  *kbps = per;
+  *splits = (nkb + per - 1) / per;
 }
 
 }  // namespace
@@ -100,7 +108,7 @@ Geometry Geometry::make(const gmi_ppo_config_t& c) {
 
 // ------------------------------------------------------------------ per-GMI state
 struct Trainer::Gmi {
-  int local = 0, gid = 0, env0 = 0, N = 0, B = 0, Bm = 0, Mrows = 0;
+  int local = 0, gid = 0, env0 = 0, N = 0, B = 0, Bm = 0, Mrows = 0, ctas = 0;
   cudaStream_t s = nullptr;
   cudaEvent_t ev_done = nullptr;
   float* x = nullptr;
@@ -114,15 +122,18 @@ struct Trainer::Gmi {
   float *act_sh = nullptr, *oldlp_sh = nullptr, *adv_sh = nullptr, *ret_sh = nullptr;
   __nv_bfloat16* H[2][GMI_MAX_HIDDEN] = {};
   __nv_bfloat16* D[2][2] = {};
+  __nv_bfloat16 *Gpi = nullptr, *Gv = nullptr;
   float* slab[2][GMI_MAX_HIDDEN] = {};
   float* colsum[2][GMI_MAX_HIDDEN] = {};
+  float* head_slab[2] = {};
   float* head_part = nullptr;
   float* grad = nullptr;
   GemmParams fwd_roll[GMI_MAX_HIDDEN], fwd_val[GMI_MAX_HIDDEN], fwd_train[GMI_MAX_HIDDEN];
-  GemmParams dw[GMI_MAX_HIDDEN], dx[GMI_MAX_HIDDEN];
-  int bn_fwd[GMI_MAX_HIDDEN] = {}, bn_dx[GMI_MAX_HIDDEN] = {}, bn_dw[GMI_MAX_HIDDEN] = {};
-  double flop_fwd_roll[GMI_MAX_HIDDEN] = {}, flop_fwd[GMI_MAX_HIDDEN] = {}, flop_dw[GMI_MAX_HIDDEN] = {},
-         flop_dx[GMI_MAX_HIDDEN] = {};
+  GemmParams dw[GMI_MAX_HIDDEN], dx[GMI_MAX_HIDDEN], dhead;
+  int bn_roll[GMI_MAX_HIDDEN] = {}, bn_val[GMI_MAX_HIDDEN] = {}, bn_fwd[GMI_MAX_HIDDEN] = {};
+  int bn_dx[GMI_MAX_HIDDEN] = {}, bn_dw[GMI_MAX_HIDDEN] = {}, bn_head = 0;
+  double flop_roll[GMI_MAX_HIDDEN] = {}, flop_fwd[GMI_MAX_HIDDEN] = {}, flop_dw[GMI_MAX_HIDDEN] = {},
+         flop_dx[GMI_MAX_HIDDEN] = {}, flop_head = 0;
   std::vector<ppo::Segment> segs;
 };
 
@@ -133,8 +144,9 @@ Trainer::Trainer(const gmi_ppo_config_t& cfg, const void* nccl_id) : cfg_(cfg) {
   if (cfg.epochs < 1 || cfg.minibatches < 1) invalid("epochs and minibatches must be >= 1");
   if (cfg.num_gpus < 1 || cfg.gmis_per_gpu < 1) invalid("num_gpus and gmis_per_gpu must be >= 1");
   if (cfg.rank < 0 || cfg.rank >= cfg.num_gpus) invalid("rank out of range");
-  if (geo_.A > ppo::kMaxAct) invalid("act_dim > 32 unsupported");
+  if (geo_.A > ppo::kMaxAct) invalid("act_dim > 31 unsupported");
   if (geo_.S > 256) invalid("obs_dim > 256 unsupported");
+  if (geo_.wp[geo_.L] > ppo::kMaxHeadIn) invalid("last hidden width > 512 unsupported");
   T_ = cfg.horizon;
   K_ = cfg.minibatches;
   n_local_ = cfg.gmis_per_gpu;
@@ -144,6 +156,8 @@ Trainer::Trainer(const gmi_ppo_config_t& cfg, const void* nccl_id) : cfg_(cfg) {
   exec_ = std::make_unique<GmiResources>(cfg.device, n_local_, cfg.gmi_backend, cfg.sm_per_gmi);
   GMI_CUDA_CHECK(cudaStreamCreateWithFlags(&upd_, cudaStreamNonBlocking));
   GMI_CUDA_CHECK(cudaEventCreateWithFlags(&ev_adam_, cudaEventDisableTiming));
+  GMI_CUDA_CHECK(cudaEventCreateWithFlags(&ev_start_, cudaEventDisableTiming));
+  const int sms = device_sm_count();
   for (int i = 0; i < n_local_; ++i) {
     auto g = std::make_unique<Gmi>();
     g->local = i;
@@ -156,12 +170,14 @@ Trainer::Trainer(const gmi_ppo_config_t& cfg, const void* nccl_id) : cfg_(cfg) {
     if (g->Bm % 64 != 0) invalid("minibatch rows per GMI must be a multiple of 64 (use envs per GMI % 8 == 0)");
     g->Mrows = std::max(g->Bm, g->N);
     g->s = exec_->stream(i);
+    g->ctas = exec_->sm_count(i) > 0 ? exec_->sm_count(i) : sms;
     GMI_CUDA_CHECK(cudaEventCreateWithFlags(&g->ev_done, cudaEventDisableTiming));
     gmis_.push_back(std::move(g));
   }
   alloc();
   init_params();
   build_plans();
+  ensure_bias_table(1 << 20);
   if (cfg.num_gpus > 1) {
     if (!nccl_id) invalid("nccl_id required when num_gpus > 1");
     ncclUniqueId id;
@@ -180,6 +196,7 @@ Trainer::Trainer(const gmi_ppo_config_t& cfg, const void* nccl_id) : cfg_(cfg) {
 
 Trainer::~Trainer() {
   cudaDeviceSynchronize();
+  if (graph_) cudaGraphExecDestroy(graph_);
   if (nccl_) ncclCommDestroy(static_cast<ncclComm_t>(nccl_));
   for (auto& e : ev_pool_) {
     cudaEventDestroy(e.first);
@@ -187,10 +204,9 @@ Trainer::~Trainer() {
   }
   for (auto& g : gmis_) cudaEventDestroy(g->ev_done);
   if (ev_adam_) cudaEventDestroy(ev_adam_);
+  if (ev_start_) cudaEventDestroy(ev_start_);
   if (upd_) cudaStreamDestroy(upd_);
   for (void* p : allocs_) cudaFree(p);
-  for (auto& e : ctl_ev_)
-    if (e) cudaEventDestroy(e);
   if (ctl_host_) cudaFreeHost(ctl_host_);
   if (stats_host_) cudaFreeHost(stats_host_);
   exec_.reset();
@@ -214,10 +230,10 @@ void Trainer::alloc() {
   shadow_ = static_cast<__nv_bfloat16*>(dev(P * 2));
   ctl_dev_ = static_cast<ppo::Control*>(dev(sizeof(ppo::Control)));
   stats_dev_ = static_cast<float*>(dev(8 * 4));
-  GMI_CUDA_CHECK(cudaMallocHost(&ctl_host_, sizeof(ppo::Control) * kCtlSlots));
-  for (auto& e : ctl_ev_) GMI_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  GMI_CUDA_CHECK(cudaMallocHost(&ctl_host_, sizeof(ppo::Control)));
   GMI_CUDA_CHECK(cudaMallocHost(&stats_host_, 8 * 4));
-  std::memset(ctl_host_, 0, sizeof(ppo::Control) * kCtlSlots);
+  std::memset(ctl_host_, 0, sizeof(ppo::Control));
+  std::memset(stats_host_, 0, 8 * 4);
 
   const int S_p = geo_.wp[0], A = geo_.A, L = geo_.L;
   int maxw = 0;
@@ -248,9 +264,10 @@ void Trainer::alloc() {
       for (int l = 0; l < L; ++l) g.H[n][l] = static_cast<__nv_bfloat16*>(dev((long long)g.Mrows * geo_.wp[l + 1] * 2));
       for (int j = 0; j < 2; ++j) g.D[n][j] = static_cast<__nv_bfloat16*>(dev((long long)g.Bm * maxw * 2));
     }
+    g.Gpi = static_cast<__nv_bfloat16*>(dev((long long)g.Bm * ppo::kHeadG * 2));
+    g.Gv = static_cast<__nv_bfloat16*>(dev((long long)g.Bm * ppo::kHeadG * 2));
     g.grad = static_cast<float*>(dev(P * 4));
-    const int hs = ppo::head_partial_stride(A, geo_.wp[L]);
-    g.head_part = static_cast<float*>(dev((long long)ppo::head_loss_blocks(g.Bm) * hs * 4));
+    g.head_part = static_cast<float*>(dev((long long)ppo::head_loss_blocks(g.Bm) * ppo::head_partial_stride(A) * 4));
   }
 }
 
@@ -280,20 +297,24 @@ void Trainer::init_params() {
 
 // ------------------------------------------------------------------ GEMM descriptors
 void Trainer::build_plans() {
-  const int L = geo_.L, S_p = geo_.wp[0];
+  const int L = geo_.L, S_p = geo_.wp[0], A = geo_.A, hp = geo_.wp[L];
+  auto dev = [&](size_t bytes) {
+    void* p = nullptr;
+    GMI_CUDA_CHECK(cudaMalloc(&p, std::max<size_t>(bytes, 256)));
+    allocs_.push_back(p);
+    return static_cast<float*>(p);
+  };
   for (auto& gp : gmis_) {
     Gmi& g = *gp;
     const long long rollrows = (long long)(T_ + 1) * g.N;
     for (int l = 0; l < L; ++l) {
       const int in_p = geo_.wp[l], out_p = geo_.wp[l + 1];
-      const int bn = gemm_pick_block_n(out_p);
-      g.bn_fwd[l] = bn;
-      auto fwd_problem = [&](int n, const CUtensorMap& amap, int M) {
+      const double real = 2.0 * geo_.net[0][l].out * geo_.net[0][l].in;
+      auto fwd_problem = [&](int n, const CUtensorMap& amap, int M, int bn) {
         GemmProblem p{};
         p.map_a = amap;
-        p.map_b = kmaj(shadow_ + geo_.net[n][l].w, in_p, out_p, in_p, bn);
-        p.out = g.H[n][l];
-        p.ld_out = out_p;
+        p.map_b = tma_kmajor(shadow_ + geo_.net[n][l].w, in_p, out_p, in_p, bn);
+        p.map_out = make_tma_out_bf16(g.H[n][l], out_p, g.Mrows, out_p);
         p.bias = params_ + geo_.net[n][l].b;
         p.M = M;
         p.N = out_p;
@@ -301,58 +322,49 @@ void Trainer::build_plans() {
         p.kb_per_split = (in_p + kGemmBlockK - 1) / kGemmBlockK;
         return p;
       };
-      // rollout / value forward read the observation slots of X_roll (rows offset per launch)
-      const CUtensorMap a_roll = l == 0 ? kmaj(g.X_roll, S_p, rollrows, S_p, kGemmBlockM)
-                                        : kmaj(g.H[0][l - 1], in_p, g.Mrows, in_p, kGemmBlockM);
+      // rollout (policy, M = N envs) and value forward (value net, chunks of Mrows rows)
+      // read observation slots of X_roll through a row offset per launch.
+      g.bn_roll[l] = gemm_choose_bn(g.N, out_p, 1, 1, g.ctas);
+      const CUtensorMap a_roll = l == 0 ? tma_kmajor(g.X_roll, S_p, rollrows, S_p, kGemmBlockM)
+                                        : tma_kmajor(g.H[0][l - 1], in_p, g.Mrows, in_p, kGemmBlockM);
       g.fwd_roll[l] = GemmParams{};
-      g.fwd_roll[l].prob[0] = fwd_problem(0, a_roll, g.N);
+      g.fwd_roll[l].prob[0] = fwd_problem(0, a_roll, g.N, g.bn_roll[l]);
       g.fwd_roll[l].num_problems = 1;
       g.fwd_roll[l].splits = 1;
-      const CUtensorMap a_val = l == 0 ? kmaj(g.X_roll, S_p, rollrows, S_p, kGemmBlockM)
-                                       : kmaj(g.H[1][l - 1], in_p, g.Mrows, in_p, kGemmBlockM);
+      g.bn_val[l] = gemm_choose_bn(g.Mrows, out_p, 1, 1, g.ctas);
+      const CUtensorMap a_val = l == 0 ? tma_kmajor(g.X_roll, S_p, rollrows, S_p, kGemmBlockM)
+                                       : tma_kmajor(g.H[1][l - 1], in_p, g.Mrows, in_p, kGemmBlockM);
       g.fwd_val[l] = GemmParams{};
-      g.fwd_val[l].prob[0] = fwd_problem(1, a_val, g.Mrows);
+      g.fwd_val[l].prob[0] = fwd_problem(1, a_val, g.Mrows, g.bn_val[l]);
       g.fwd_val[l].num_problems = 1;
       g.fwd_val[l].splits = 1;
-      // training forward: both nets grouped, minibatch rows of the epoch copy
+      // training forward: both nets grouped over the minibatch rows of the epoch copy
+      g.bn_fwd[l] = gemm_choose_bn(g.Bm, out_p, 2, 1, g.ctas);
       g.fwd_train[l] = GemmParams{};
       for (int n = 0; n < 2; ++n) {
-        const CUtensorMap a = l == 0 ? kmaj(g.X_sh, S_p, g.B, S_p, kGemmBlockM)
-                                     : kmaj(g.H[n][l - 1], in_p, g.Mrows, in_p, kGemmBlockM);
-        g.fwd_train[l].prob[n] = fwd_problem(n, a, g.Bm);
+        const CUtensorMap a = l == 0 ? tma_kmajor(g.X_sh, S_p, g.B, S_p, kGemmBlockM)
+                                     : tma_kmajor(g.H[n][l - 1], in_p, g.Mrows, in_p, kGemmBlockM);
+        g.fwd_train[l].prob[n] = fwd_problem(n, a, g.Bm, g.bn_fwd[l]);
       }
       g.fwd_train[l].num_problems = 2;
       g.fwd_train[l].splits = 1;
-      const double real = 2.0 * geo_.net[0][l].out * geo_.net[0][l].in;
-      g.flop_fwd_roll[l] = real * g.N;
+      g.flop_roll[l] = real * g.N;
       g.flop_fwd[l] = 2.0 * real * g.Bm;
 
-      // weight gradient: dW_l[out_p][in_p] = sum_rows dPre_l^T in_l (both operands MN-major)
+      // weight gradient dW_l[out_p][in_p] = sum_rows dPre_l^T in_l (both operands MN-major)
       const int cur = (L - 1 - l) & 1;
-      const int bnw = gemm_pick_block_n(in_p);
+      const int bnw = std::min(256, ((in_p + 63) / 64) * 64);
       g.bn_dw[l] = bnw;
-      const int tiles = ((out_p + 127) / 128) * ((in_p + bnw - 1) / bnw) * 2;
-      const int nkb = g.Bm / kGemmBlockK;
-      int splits = std::max(1, std::min(nkb, 296 / std::max(1, tiles)));
-      const int kbps = (nkb + splits - 1) / splits;
-      splits = (nkb + kbps - 1) / kbps;
+      int splits = 1, kbps = 1;
+      pick_splits(out_p, in_p, bnw, 2, g.Bm, g.ctas, &splits, &kbps);
       g.dw[l] = GemmParams{};
       for (int n = 0; n < 2; ++n) {
-        g.slab[n][l] = nullptr;
-        void* slab = nullptr;
-        GMI_CUDA_CHECK(cudaMalloc(&slab, (size_t)splits * out_p * in_p * 4));
-        allocs_.push_back(slab);
-        g.slab[n][l] = static_cast<float*>(slab);
-        void* cs = nullptr;
-        GMI_CUDA_CHECK(cudaMalloc(&cs, (size_t)ppo::colsum_blocks(g.Bm) * out_p * 4));
-        allocs_.push_back(cs);
-        g.colsum[n][l] = static_cast<float*>(cs);
+        g.slab[n][l] = dev((size_t)splits * out_p * in_p * 4);
+        g.colsum[n][l] = dev((size_t)ppo::colsum_blocks(g.Bm) * out_p * 4);
         GemmProblem p{};
-        p.map_a = mnmaj(g.D[n][cur], out_p, g.Bm, out_p);
-        p.map_b = l == 0 ? mnmaj(g.X_sh, S_p, g.B, S_p) : mnmaj(g.H[n][l - 1], in_p, g.Bm, in_p);
-        p.out = g.slab[n][l];
-        p.ld_out = in_p;
-        p.split_stride = (long long)out_p * in_p;
+        p.map_a = tma_mnmajor(g.D[n][cur], out_p, g.Bm, out_p);
+        p.map_b = l == 0 ? tma_mnmajor(g.X_sh, S_p, g.B, S_p) : tma_mnmajor(g.H[n][l - 1], in_p, g.Bm, in_p);
+        p.map_out = make_tma_out_f32(g.slab[n][l], in_p, out_p, splits, in_p, (uint64_t)out_p * in_p);
         p.M = out_p;
         p.N = in_p;
         p.K = g.Bm;
@@ -363,17 +375,15 @@ void Trainer::build_plans() {
       g.dw[l].splits = splits;
       g.flop_dw[l] = 2.0 * real * g.Bm;
 
-      // input gradient: dPre_{l-1} = (dPre_l W_l) * elu'(H_{l-1}); W_l read MN-major
+      // input gradient dPre_{l-1} = (dPre_l W_l) * elu'(H_{l-1}); W_l read MN-major
       if (l > 0) {
-        const int bnx = gemm_pick_block_n(in_p);
-        g.bn_dx[l] = bnx;
+        g.bn_dx[l] = gemm_choose_bn(g.Bm, in_p, 2, 1, g.ctas);
         g.dx[l] = GemmParams{};
         for (int n = 0; n < 2; ++n) {
           GemmProblem p{};
-          p.map_a = kmaj(g.D[n][cur], out_p, g.Bm, out_p, kGemmBlockM);
-          p.map_b = mnmaj(shadow_ + geo_.net[n][l].w, in_p, out_p, in_p);
-          p.out = g.D[n][cur ^ 1];
-          p.ld_out = in_p;
+          p.map_a = tma_kmajor(g.D[n][cur], out_p, g.Bm, out_p, kGemmBlockM);
+          p.map_b = tma_mnmajor(shadow_ + geo_.net[n][l].w, in_p, out_p, in_p);
+          p.map_out = make_tma_out_bf16(g.D[n][cur ^ 1], in_p, g.Bm, in_p);
           p.aux = g.H[n][l - 1];
           p.ld_aux = in_p;
           p.M = g.Bm;
@@ -387,22 +397,45 @@ void Trainer::build_plans() {
         g.flop_dx[l] = 2.0 * real * g.Bm;
       }
     }
+    // head weight gradients on the tensor cores: dW_mu = G_pi^T H_L, dw_v = G_v^T H^v_L
+    const int bnh = std::min(256, ((hp + 63) / 64) * 64);
+    g.bn_head = bnh;
+    int hsplits = 1, hkbps = 1;
+    pick_splits(A, hp, bnh, 2, g.Bm, g.ctas, &hsplits, &hkbps);
+    g.head_slab[0] = dev((size_t)hsplits * A * hp * 4);
+    g.head_slab[1] = dev((size_t)hsplits * hp * 4);
+    g.dhead = GemmParams{};
+    const __nv_bfloat16* G[2] = {g.Gpi, g.Gv};
+    for (int n = 0; n < 2; ++n) {
+      GemmProblem p{};
+      p.map_a = tma_mnmajor(G[n], ppo::kHeadG, g.Bm, ppo::kHeadG);
+      p.map_b = tma_mnmajor(g.H[n][L - 1], hp, g.Bm, hp);
+      const int rows = n == 0 ? A : 1;
+      p.map_out = make_tma_out_f32(g.head_slab[n], hp, rows, hsplits, hp, (uint64_t)rows * hp);
+      p.M = A;  // both problems share the tile grid; the value map clips to one row
+      p.N = hp;
+      p.K = g.Bm;
+      p.kb_per_split = hkbps;
+      g.dhead.prob[n] = p;
+    }
+    g.dhead.num_problems = 2;
+    g.dhead.splits = hsplits;
+    g.flop_head = 2.0 * (A + 1) * double(geo_.width[L]) * g.Bm;
     // gradient assembly segments (fixed-order sums of slabs / partials into the flat grad)
     const int hb = ppo::head_loss_blocks(g.Bm), cb = ppo::colsum_blocks(g.Bm);
-    const int A = geo_.A, hp = geo_.wp[L];
-    const int hs = ppo::head_partial_stride(A, hp);
+    const int hs = ppo::head_partial_stride(A);
     for (int n = 0; n < 2; ++n)
       for (int l = 0; l < L; ++l) {
         const Tensor& t = geo_.net[n][l];
         g.segs.push_back({g.grad + t.w, g.slab[n][l], (long long)t.out_p * t.in_p, t.out_p * t.in_p, g.dw[l].splits});
         g.segs.push_back({g.grad + t.b, g.colsum[n][l], t.out_p, t.out_p, cb});
       }
-    g.segs.push_back({g.grad + geo_.net[0][L].w, g.head_part, hs, A * hp, hb});
-    g.segs.push_back({g.grad + geo_.net[1][L].w, g.head_part + A * hp, hs, hp, hb});
-    g.segs.push_back({g.grad + geo_.net[0][L].b, g.head_part + A * hp + hp, hs, A, hb});
-    g.segs.push_back({g.grad + geo_.net[1][L].b, g.head_part + A * hp + hp + A, hs, 1, hb});
-    g.segs.push_back({g.grad + geo_.log_std, g.head_part + A * hp + hp + A + 1, hs, A, hb});
-    if (g.local == 0) g.segs.push_back({stats_dev_, g.head_part + A * hp + hp + 2 * A + 1, hs, 4, hb});
+    g.segs.push_back({g.grad + geo_.net[0][L].w, g.head_slab[0], (long long)A * hp, A * hp, hsplits});
+    g.segs.push_back({g.grad + geo_.net[1][L].w, g.head_slab[1], hp, hp, hsplits});
+    g.segs.push_back({g.grad + geo_.net[0][L].b, g.head_part, hs, A, hb});
+    g.segs.push_back({g.grad + geo_.net[1][L].b, g.head_part + A, hs, 1, hb});
+    g.segs.push_back({g.grad + geo_.log_std, g.head_part + A + 1, hs, A, hb});
+    if (g.local == 0) g.segs.push_back({stats_dev_, g.head_part + 2 * A + 1, hs, 4, hb});
   }
 }
 
@@ -419,7 +452,7 @@ void Trainer::gemm(Gmi& g, const GemmParams& P, int bn, int amn, int bmn, int ep
     }
     GMI_CUDA_CHECK(cudaEventRecord(ev_pool_[ev_used_].first, g.s));
   }
-  gemm_launch(P, bn, amn, bmn, epi, g.s);
+  gemm_launch(P, bn, amn, bmn, epi, g.s, g.ctas);
   ++launches_;
   if (timed) {
     GMI_CUDA_CHECK(cudaEventRecord(ev_pool_[ev_used_].second, g.s));
@@ -428,33 +461,35 @@ void Trainer::gemm(Gmi& g, const GemmParams& P, int bn, int amn, int bmn, int ep
   }
 }
 
-void Trainer::set_control() {
-  const long long need = adam_steps_ + (long long)cfg_.epochs * K_ + 1;
-  if (need > bc_cap_) {  // bias-correction table 1-b^s, s = 1.. (double pow, like the oracle)
-    GMI_CUDA_CHECK(cudaDeviceSynchronize());
-    const long long cap = std::max<long long>(need * 2, 4096);
-    std::vector<float> tab(2 * cap);
-    for (long long s = 0; s < cap; ++s) {
-      tab[2 * s] = float(1.0 - std::pow(double(cfg_.beta1), double(s + 1)));
-      tab[2 * s + 1] = float(1.0 - std::pow(double(cfg_.beta2), double(s + 1)));
-    }
-    void* p = nullptr;
-    GMI_CUDA_CHECK(cudaMalloc(&p, tab.size() * 4));
-    GMI_CUDA_CHECK(cudaMemcpy(p, tab.data(), tab.size() * 4, cudaMemcpyHostToDevice));
-    allocs_.push_back(p);
-    bc_ = static_cast<float*>(p);
-    bc_cap_ = cap;
+void Trainer::ensure_bias_table(long long steps) {
+  if (steps <= bc_cap_) return;
+  // Adam bias corrections 1-b^s for s = 1..cap in double, rounded to fp32 (as the oracle)
+  GMI_CUDA_CHECK(cudaDeviceSynchronize());
+  const long long cap = std::max<long long>(steps, 2 * bc_cap_);
+  std::vector<float> tab(2 * cap);
+  for (long long s = 0; s < cap; ++s) {
+    tab[2 * s] = float(1.0 - std::pow(double(cfg_.beta1), double(s + 1)));
+    tab[2 * s + 1] = float(1.0 - std::pow(double(cfg_.beta2), double(s + 1)));
   }
-  // Pinned ring: a slot is rewritten only after its previous H2D copy has executed.
-  const int slot = iteration_ % kCtlSlots;
-  GMI_CUDA_CHECK(cudaEventSynchronize(ctl_ev_[slot]));
-  ppo::Control* c = ctl_host_ + slot;
-  c->iteration = iteration_;
-  c->adam_step0 = adam_steps_;
-  GMI_CUDA_CHECK(cudaStreamWaitEvent(upd_, ev_adam_, 0));
-  GMI_CUDA_CHECK(cudaMemcpyAsync(ctl_dev_, c, sizeof(ppo::Control), cudaMemcpyHostToDevice, upd_));
-  GMI_CUDA_CHECK(cudaEventRecord(ctl_ev_[slot], upd_));
-  GMI_CUDA_CHECK(cudaEventRecord(ev_adam_, upd_));
+  void* p = nullptr;
+  GMI_CUDA_CHECK(cudaMalloc(&p, tab.size() * 4));
+  GMI_CUDA_CHECK(cudaMemcpy(p, tab.data(), tab.size() * 4, cudaMemcpyHostToDevice));
+  allocs_.push_back(p);
+  bc_ = static_cast<float*>(p);
+  bc_cap_ = cap;
+  if (graph_) {  // the captured Adam launches point at the old table
+    GMI_CUDA_CHECK(cudaGraphExecDestroy(graph_));
+    graph_ = nullptr;
+  }
+}
+
+// Host -> device control block (the iteration's only host input): used on the first
+// iteration, by the rollout parity hook, and on the synchronous public path.
+void Trainer::write_control() {
+  GMI_CUDA_CHECK(cudaStreamSynchronize(upd_));
+  ctl_host_->iteration = iteration_;
+  ctl_host_->adam_step0 = adam_steps_;
+  GMI_CUDA_CHECK(cudaMemcpyAsync(ctl_dev_, ctl_host_, sizeof(ppo::Control), cudaMemcpyHostToDevice, upd_));
 }
 
 // ------------------------------------------------------------------ phases
@@ -468,7 +503,7 @@ void Trainer::rollout(Gmi& g) {
     for (int l = 0; l < L; ++l) {
       GemmParams P = g.fwd_roll[l];
       if (l == 0) P.prob[0].a_row0 = t * g.N;
-      gemm(g, P, g.bn_fwd[l], 0, 0, EPI_BIAS_ELU, g.flop_fwd_roll[l]);
+      gemm(g, P, g.bn_roll[l], 0, 0, EPI_BIAS_ELU, g.flop_roll[l]);
     }
     ppo::ActEnvArgs a{};
     a.ep = {g.N, geo_.S, geo_.A, S_p, g.env0, T_, cfg_.seed};
@@ -503,7 +538,7 @@ void Trainer::values(Gmi& g) {
       GemmParams P = g.fwd_val[l];
       P.prob[0].M = m;
       if (l == 0) P.prob[0].a_row0 = int(c0);
-      gemm(g, P, g.bn_fwd[l], 0, 0, EPI_BIAS_ELU, g.flop_fwd_roll[l] * double(m) / g.N);
+      gemm(g, P, g.bn_val[l], 0, 0, EPI_BIAS_ELU, g.flop_roll[l] * double(m) / g.N);
     }
     ppo::launch_value_head(g.H[1][L - 1], geo_.wp[L], params_ + head.w, params_ + head.b, g.V + c0, m, g.s);
     ++launches_;
@@ -536,8 +571,9 @@ void Trainer::train_minibatch(Gmi& g, int k) {
   h.ret = g.ret_sh + r0;
   h.Dpi = g.D[0][0];
   h.Dv = g.D[1][0];
+  h.Gpi = g.Gpi;
+  h.Gv = g.Gv;
   h.partial = g.head_part;
-  h.partial_stride = ppo::head_partial_stride(A, hp);
   h.B = g.Bm;
   h.A = A;
   h.clip = cfg_.clip;
@@ -545,6 +581,7 @@ void Trainer::train_minibatch(Gmi& g, int k) {
   h.ent_coef = cfg_.ent_coef;
   ppo::launch_head_loss(h, g.s);
   ++launches_;
+  gemm(g, g.dhead, g.bn_head, 1, 1, EPI_F32, g.flop_head);
   for (int l = L - 1; l >= 0; --l) {
     GemmParams P = g.dw[l];
     if (l == 0) P.prob[0].b_row0 = P.prob[1].b_row0 = k * g.Bm;
@@ -577,8 +614,8 @@ void Trainer::reduce_and_step(int step_in_iter) {
     src = grad_sum_;
   }
   if (nccl_) {
-    NCCL_CHECK(ncclAllReduce(src, grad_sum_, size_t(geo_.P), ncclFloat32, ncclSum,
-                             static_cast<ncclComm_t>(nccl_), upd_));
+    NCCL_CHECK(ncclAllReduce(src, grad_sum_, size_t(geo_.P), ncclFloat32, ncclSum, static_cast<ncclComm_t>(nccl_),
+                             upd_));
     src = grad_sum_;
   }
   ppo::AdamArgs a{};
@@ -602,24 +639,33 @@ void Trainer::reduce_and_step(int step_in_iter) {
 }
 
 void Trainer::enqueue_rollout() {
-  set_control();
+  write_control();
+  GMI_CUDA_CHECK(cudaEventRecord(ev_start_, upd_));
   for (auto& g : gmis_) {
-    GMI_CUDA_CHECK(cudaStreamWaitEvent(g->s, ev_adam_, 0));
+    GMI_CUDA_CHECK(cudaStreamWaitEvent(g->s, ev_start_, 0));
     rollout(*g);
     values(*g);
+    GMI_CUDA_CHECK(cudaEventRecord(g->ev_done, g->s));
+    GMI_CUDA_CHECK(cudaStreamWaitEvent(upd_, g->ev_done, 0));
   }
 }
 
-void Trainer::enqueue_iteration() {
+// Every kernel / copy / collective of one iteration, on the GMI streams and upd_.
+void Trainer::record_iteration() {
   launches_ = 0;
   ev_used_ = 0;
-  enqueue_rollout();
+  GMI_CUDA_CHECK(cudaEventRecord(ev_start_, upd_));
+  for (auto& g : gmis_) {
+    GMI_CUDA_CHECK(cudaStreamWaitEvent(g->s, ev_start_, 0));
+    rollout(*g);
+    values(*g);
+  }
   int step = 0;
   for (int e = 0; e < cfg_.epochs; ++e) {
     for (auto& g : gmis_) {
-      ppo::launch_shuffle(g->X_roll, g->act, g->logp, g->adv, g->ret, g->adv_stats, g->X_sh, g->act_sh,
-                          g->oldlp_sh, g->adv_sh, g->ret_sh, g->N, T_, geo_.wp[0], geo_.A, cfg_.seed, g->gid, e,
-                          ctl_dev_, g->s);
+      if (step > 0) GMI_CUDA_CHECK(cudaStreamWaitEvent(g->s, ev_adam_, 0));
+      ppo::launch_shuffle(g->X_roll, g->act, g->logp, g->adv, g->ret, g->adv_stats, g->X_sh, g->act_sh, g->oldlp_sh,
+                          g->adv_sh, g->ret_sh, g->N, T_, geo_.wp[0], geo_.A, cfg_.seed, g->gid, e, ctl_dev_, g->s);
       ++launches_;
     }
     for (int k = 0; k < K_; ++k, ++step) {
@@ -631,10 +677,38 @@ void Trainer::enqueue_iteration() {
       reduce_and_step(step);
     }
   }
-  GMI_CUDA_CHECK(cudaStreamWaitEvent(upd_, gmis_[0]->ev_done, 0));
+  for (auto& g : gmis_) GMI_CUDA_CHECK(cudaStreamWaitEvent(upd_, g->ev_done, 0));
   GMI_CUDA_CHECK(cudaMemcpyAsync(stats_dev_ + 4, gmis_[0]->adv_stats, 3 * 4, cudaMemcpyDeviceToDevice, upd_));
   GMI_CUDA_CHECK(cudaMemcpyAsync(stats_host_, stats_dev_, 8 * 4, cudaMemcpyDeviceToHost, upd_));
-  GMI_CUDA_CHECK(cudaEventRecord(ev_adam_, upd_));
+  ppo::launch_control_advance(ctl_dev_, cfg_.epochs * K_, upd_);
+  ++launches_;
+}
+
+void Trainer::enqueue_iteration(bool host_control) {
+  ensure_bias_table(adam_steps_ + (long long)cfg_.epochs * K_ + 1);
+  if (host_control || iteration_ == 0) write_control();
+  if (cfg_.use_graph && iteration_ > 0) {
+    if (!graph_) {
+      GMI_CUDA_CHECK(cudaStreamSynchronize(upd_));
+      cudaGraph_t gr;
+      GMI_CUDA_CHECK(cudaStreamBeginCapture(upd_, cudaStreamCaptureModeThreadLocal));
+      capturing_ = true;
+      try {
+        record_iteration();
+      } catch (...) {
+        cudaStreamEndCapture(upd_, &gr);
+        capturing_ = false;
+        throw;
+      }
+      capturing_ = false;
+      GMI_CUDA_CHECK(cudaStreamEndCapture(upd_, &gr));
+      GMI_CUDA_CHECK(cudaGraphInstantiate(&graph_, gr, 0));
+      GMI_CUDA_CHECK(cudaGraphDestroy(gr));
+    }
+    GMI_CUDA_CHECK(cudaGraphLaunch(graph_, upd_));
+  } else {
+    record_iteration();
+  }
   iteration_ += 1;
   adam_steps_ += (long long)cfg_.epochs * K_;
 }
@@ -672,7 +746,7 @@ void Trainer::minibatch_grad(int gi, const float* X, const float* act, const flo
   std::vector<uint16_t> xb((size_t)B * S_p, 0);
   for (int r = 0; r < B; ++r)
     for (int i = 0; i < S; ++i) xb[(size_t)r * S_p + i] = bf16_bits(X[(size_t)r * S + i]);
-  GMI_CUDA_CHECK(cudaStreamSynchronize(upd_));
+  GMI_CUDA_CHECK(cudaDeviceSynchronize());
   GMI_CUDA_CHECK(cudaMemcpy(g.X_sh, xb.data(), xb.size() * 2, cudaMemcpyHostToDevice));
   GMI_CUDA_CHECK(cudaMemcpy(g.act_sh, act, (size_t)B * A * 4, cudaMemcpyHostToDevice));
   GMI_CUDA_CHECK(cudaMemcpy(g.oldlp_sh, oldlp, (size_t)B * 4, cudaMemcpyHostToDevice));
@@ -773,6 +847,7 @@ GMI_API void gmi_ppo_config_defaults(gmi_ppo_config_t* c) {
   c->seed = 20240811ull;
   c->num_gpus = 1;
   c->gmis_per_gpu = 1;
+  c->use_graph = 1;
 }
 
 GMI_API int gmi_ppo_create(const gmi_ppo_config_t* cfg, const void* nccl_id, void** trainer) {
@@ -795,13 +870,13 @@ GMI_API int gmi_nccl_unique_id(void* out) {
 GMI_API int gmi_ppo_iteration(void* t, gmi_ppo_stats_t* st) {
   return gmi::guarded([&] {
     auto* tr = static_cast<gmi::Trainer*>(t);
-    tr->enqueue_iteration();
+    tr->enqueue_iteration(true);
     tr->synchronize(st);
   });
 }
 
 GMI_API int gmi_ppo_iteration_async(void* t) {
-  return gmi::guarded([&] { static_cast<gmi::Trainer*>(t)->enqueue_iteration(); });
+  return gmi::guarded([&] { static_cast<gmi::Trainer*>(t)->enqueue_iteration(false); });
 }
 
 GMI_API int gmi_ppo_synchronize(void* t, gmi_ppo_stats_t* st) {

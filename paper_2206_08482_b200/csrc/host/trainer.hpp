@@ -1,6 +1,7 @@
 // B200 PPO trainer: one instance drives one GPU of the data-parallel job (TCG_EX
 // holistic GMIs). Owns device memory, GMI execution resources (streams or green
-// contexts), the prebuilt GEMM problem descriptors and the NCCL communicator.
+// contexts), the prebuilt GEMM problem descriptors, the NCCL communicator and the CUDA
+// graph that replays one whole iteration.
 #pragma once
 
 #include <cuda_bf16.h>
@@ -37,7 +38,7 @@ class Trainer {
   Trainer(const gmi_ppo_config_t& cfg, const void* nccl_id);
   ~Trainer();
 
-  void enqueue_iteration();
+  void enqueue_iteration(bool host_control);
   void enqueue_rollout();
   void synchronize(gmi_ppo_stats_t* stats);
   void minibatch_grad(int gmi, const float* X, const float* act, const float* oldlp, const float* adv,
@@ -49,17 +50,18 @@ class Trainer {
 
  private:
   struct Gmi;
-  struct Launch;
 
   void alloc();
   void init_params();
   void build_plans();
+  void ensure_bias_table(long long steps);
+  void write_control();
+  void record_iteration();  // the launch sequence of one iteration (eager or under capture)
   void rollout(Gmi& g);
   void values(Gmi& g);
   void train_minibatch(Gmi& g, int k);
   void reduce_and_step(int k);
   void gemm(Gmi& g, const GemmParams& P, int bn, int amn, int bmn, int epi, double flop);
-  void set_control();
 
   gmi_ppo_config_t cfg_;
   Geometry geo_;
@@ -73,22 +75,22 @@ class Trainer {
   __nv_bfloat16* shadow_ = nullptr;
   long long bc_cap_ = 0;
   ppo::Control* ctl_dev_ = nullptr;
-  ppo::Control* ctl_host_ = nullptr;  // pinned ring of kCtlSlots blocks
-  static constexpr int kCtlSlots = 4;
-  cudaEvent_t ctl_ev_[kCtlSlots] = {};
-  float* stats_dev_ = nullptr;   // [8]
-  float* stats_host_ = nullptr;  // pinned
-  cudaStream_t upd_ = nullptr;   // update / reduction stream
+  ppo::Control* ctl_host_ = nullptr;  // pinned
+  float* stats_dev_ = nullptr;        // [8]
+  float* stats_host_ = nullptr;       // pinned
+  cudaStream_t upd_ = nullptr;        // update / reduction stream
   cudaEvent_t ev_adam_ = nullptr;
+  cudaEvent_t ev_start_ = nullptr;
   void* nccl_ = nullptr;
-  int iteration_ = 0;
+  int iteration_ = 0;      // iterations enqueued so far
   long long adam_steps_ = 0;
-  int launches_ = 0;
-  // instrumentation
+  int launches_ = 0;       // kernels in one iteration
+  bool capturing_ = false;
+  cudaGraphExec_t graph_ = nullptr;
+  // instrumentation (GEMM launches of GMI 0)
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pool_;
   std::vector<double> ev_flop_;
   int ev_used_ = 0;
-  double gemm_flop_ = 0;
 };
 
 }  // namespace gmi
