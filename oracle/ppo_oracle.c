@@ -220,7 +220,8 @@ static void mlp_hidden(const oracle_t* o, const float* wbf, int n, const float* 
 static float head_out(const oracle_t* o, int n, int a, const float* hl) {
   const tensor_t* t = &o->net[n][o->L];
   double acc = 0.0;
-  for (int k = 0; k < t->in; ++k) acc += (double)hl[k] * (double)o->params[t->w + (long long)a * t->in_p + k];
+  /* heads run on the tensor cores: bf16 head weights, fp32 bias added after the GEMM */
+  for (int k = 0; k < t->in; ++k) acc += (double)hl[k] * (double)R(o->params[t->w + (long long)a * t->in_p + k]);
   return (float)acc + o->params[t->b + a];
 }
 
@@ -417,9 +418,10 @@ static void minibatch_grad(oracle_t* o, int gi, mb_t* mb, int Bm, const float* w
       for (int k = 0; k < th->in; ++k) {
         double acc = 0.0;
         if (n == 0)
-          for (int a = 0; a < A; ++a) acc += (double)mb->gmu[(long long)r * A + a] * (double)o->params[th->w + (long long)a * th->in_p + k];
+          for (int a = 0; a < A; ++a)
+            acc += (double)R(mb->gmu[(long long)r * A + a]) * (double)R(o->params[th->w + (long long)a * th->in_p + k]);
         else
-          acc = (double)mb->gv[r] * (double)o->params[th->w + k];
+          acc = (double)R(mb->gv[r]) * (double)R(o->params[th->w + k]);
         d[k] = R((float)acc * elu_grad_from_out(hl[k]));
       }
       /* hidden backward: dPre_{l-1} = (dPre_l W_l) * elu'(H_{l-1}) */

@@ -5,7 +5,7 @@
 // One CTA per SM walks a static tile schedule (grouped problems x split-K slabs x M x N
 // tiles). Warp 0 streams operands with TMA (128B swizzle) through a STAGES-deep
 // shared-memory ring; warp 1 issues tcgen05.mma (M = 128, N = BN, K = 16) into one of two
-// TMEM accumulators; eight epilogue warps drain the other accumulator concurrently
+// TMEM accumulators; the epilogue warps drain the other accumulator concurrently
 // (tcgen05.ld -> fused epilogue -> swizzled smem staging -> TMA store), so the epilogue
 // of tile i overlaps the MMAs of tile i+1. Either operand may be K-major (row-major
 // [rows x K]) or MN-major (row-major [K x rows]); MN-major lets the weight-gradient GEMM
@@ -14,7 +14,7 @@
 // Epilogues:
 //   EPI_BIAS_ELU  hidden-layer forward: bf16 out = elu(acc + bias[n])
 //   EPI_DACT      hidden-layer backward: bf16 out = acc * elu'(H[m][n]), elu' = H > 0 ? 1 : H + 1
-//   EPI_F32       fp32 split-K slab [split][m][n] (reduced in a fixed order afterwards)
+//   EPI_F32       fp32 [split][m][n] (split-K weight-gradient slabs, head outputs)
 #pragma once
 
 #include <cstdint>
@@ -26,19 +26,18 @@
 
 namespace gmi {
 
-// elu(x) = x > 0 ? x : expm1(x); expm1 via a degree-6 Taylor polynomial near 0 and the
-// SFU exp elsewhere (|rel err| < 2e-6, far below the bf16 output rounding).
+// elu(x) = x > 0 ? x : expm1(x), branch-free: degree-6 Taylor polynomial on (-0.25, 0],
+// SFU exp below (|rel err| < 2e-6, far below the bf16 output rounding).
 __device__ __forceinline__ float elu_fast(float x) {
-  if (x > 0.f) return x;
-  if (x > -0.25f) {
-    float p = fmaf(x, 1.f / 720.f, 1.f / 120.f);
-    p = fmaf(p, x, 1.f / 24.f);
-    p = fmaf(p, x, 1.f / 6.f);
-    p = fmaf(p, x, 0.5f);
-    p = fmaf(p, x, 1.f);
-    return p * x;
-  }
-  return __expf(x) - 1.f;
+  float p = fmaf(x, 1.f / 720.f, 1.f / 120.f);
+  p = fmaf(p, x, 1.f / 24.f);
+  p = fmaf(p, x, 1.f / 6.f);
+  p = fmaf(p, x, 0.5f);
+  p = fmaf(p, x, 1.f);
+  p *= x;
+  const float e = __expf(x) - 1.f;
+  const float neg = x > -0.25f ? p : e;
+  return x > 0.f ? x : neg;
 }
 
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
@@ -46,22 +45,24 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
-template <int BN>
+template <int BN, int EPI>
 struct GemmSmem {
+  static constexpr int kEpiWarps = gemm_epi_warps(EPI);
   static constexpr int kStages = BN == 256 ? 3 : 4;
   static constexpr uint32_t kA = kGemmBlockM * kGemmBlockK * 2;  // 16 KB
   static constexpr uint32_t kB = BN * kGemmBlockK * 2;
   static constexpr uint32_t kStage = kA + kB;
-  static constexpr uint32_t kStaging = 4096;  // one 32x32 fp32 (or bf16) chunk, per warp, x2
-  static constexpr uint32_t kBarOff = kStages * kStage + kGemmEpiWarps * 2 * kStaging;
+  static constexpr uint32_t kStaging = EPI == 2 ? 4096 : 2048;  // one 32x32 chunk per warp, x2
+  static constexpr uint32_t kBarOff = kStages * kStage + kEpiWarps * 2 * kStaging;
   static constexpr uint32_t kBytes = kBarOff + 256 + 1024;  // + barriers + alignment slack
   static constexpr uint32_t kTmemCols = 2 * BN < 32 ? 32 : 2 * BN;
 };
 
 template <int BN, int A_MN, int B_MN, int EPI>
-__global__ void __launch_bounds__(kGemmThreads, 1) gemm_tcgen05_kernel(const __grid_constant__ GemmParams P) {
-  using L = GemmSmem<BN>;
+__global__ void __launch_bounds__(gemm_threads(EPI), 1) gemm_tcgen05_kernel(const __grid_constant__ GemmParams P) {
+  using L = GemmSmem<BN, EPI>;
   constexpr int S = L::kStages;
+  constexpr int kEpiWarps = L::kEpiWarps;
   constexpr uint32_t kIdesc = ptx::umma_idesc_bf16(kGemmBlockM, BN, A_MN, B_MN);
   static_assert(BN % 64 == 0 && BN <= 256, "BN must be 64, 128 or 256");
 
@@ -90,7 +91,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_tcgen05_kernel(const __g
     }
     for (int b = 0; b < 2; ++b) {
       ptx::mbar_init(&tfull_bar[b], 1);
-      ptx::mbar_init(&tempty_bar[b], kGemmEpiWarps);
+      ptx::mbar_init(&tempty_bar[b], kEpiWarps);
     }
     ptx::fence_mbar_init();
     for (int i = 0; i < P.num_problems; ++i) {
@@ -182,12 +183,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_tcgen05_kernel(const __g
       }
     }
   } else {
-    // ---------------- epilogue warps: quarter q of the TMEM lanes, half h of the columns
+    // ---------------- epilogue warps: TMEM lane quarter q, every W-th 32-column chunk
+    constexpr int W = kEpiWarps / 4;  // warps per lane quarter
     const int e = warp - 2;
     const int q = warp & 3;
     const int h = e >> 2;
     constexpr int kChunks = BN / 32;
-    constexpr int kMine = kChunks / 2;
     uint8_t* stage_base = staging + e * 2 * L::kStaging;
     int sbuf = 0;
     int lt = 0;
@@ -201,9 +202,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_tcgen05_kernel(const __g
       const int rbase = m0 + q * 32;
       const int row = rbase + lane;
 #pragma unroll 1
-      for (int cc = 0; cc < kMine; ++cc) {
-        const int c = h * kMine + cc;
+      for (int c = h; c < kChunks; c += W) {
         const int col0 = n0 + c * 32;
+        if (col0 >= pr.N) break;  // warp-uniform
         uint32_t r[32];
         ptx::tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + buf * BN + c * 32, r);
         ptx::tmem_ld_wait();
@@ -211,7 +212,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_tcgen05_kernel(const __g
 #pragma unroll
           for (int j = 0; j < 32; ++j) r[j] = 0u;
         }
-        if (col0 >= pr.N) continue;  // warp-uniform
         uint8_t* st = stage_base + sbuf * L::kStaging;
         if (lane == 0) ptx::bulk_wait_read<1>();  // the staging buffer used two stores ago is free
         __syncwarp();

@@ -104,14 +104,14 @@ namespace {
 
 template <int BN, int AMN, int BMN, int EPI>
 void launch_t(const GemmParams& P, int ctas, cudaStream_t s) {
-  constexpr int smem = GemmSmem<BN>::kBytes;
+  constexpr int smem = GemmSmem<BN, EPI>::kBytes;
   auto kern = gemm_tcgen05_kernel<BN, AMN, BMN, EPI>;
   static bool configured = false;  // per instantiation
   if (!configured) {
     GMI_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     configured = true;
   }
-  kern<<<ctas, kGemmThreads, smem, s>>>(P);
+  kern<<<ctas, gemm_threads(EPI), smem, s>>>(P);
   GMI_CUDA_CHECK(cudaGetLastError());
 }
 

@@ -38,9 +38,7 @@ struct EnvParams {
 
 struct ActEnvArgs {
   EnvParams ep;
-  const __nv_bfloat16* H;  // [N][hp] last policy hidden layer
-  int hp;
-  const float* w_mu;  // [A][hp]
+  const float* mu;    // [N][64] policy-head GEMM output (bias not yet added)
   const float* b_mu;  // [A]
   const float* log_std;
   float* x;
@@ -57,21 +55,16 @@ struct ActEnvArgs {
 };
 
 struct HeadLossArgs {
-  const __nv_bfloat16* Hpi;  // [B][hp]
-  const __nv_bfloat16* Hv;
-  int hp;
-  const float* w_mu;
+  const float* mu;  // [B][64] policy-head GEMM output (no bias)
+  const float* v;   // [B][64] value-head GEMM output, column 0 (no bias)
   const float* b_mu;
-  const float* w_v;
   const float* b_v;
   const float* log_std;
   const float* act;  // [B][A]
   const float* oldlp;
   const float* adv;
   const float* ret;
-  __nv_bfloat16* Dpi;  // [B][hp] dPre of the last hidden layer
-  __nv_bfloat16* Dv;
-  __nv_bfloat16* Gpi;  // [B][64] dL/dmu (bf16), input of the head weight-gradient GEMM
+  __nv_bfloat16* Gpi;  // [B][64] dL/dmu (bf16), input of the head input/weight-gradient GEMMs
   __nv_bfloat16* Gv;   // [B][64] dL/dv in column 0
   float* partial;      // [blocks][head_partial_stride(A)]
   int B, A;
@@ -106,8 +99,7 @@ struct AdamArgs {
 void launch_env_init(const EnvParams& ep, float* x, int* ep_step, int* ep_len, int* ep_count,
                      __nv_bfloat16* X0, cudaStream_t s);
 void launch_act_env(const ActEnvArgs& a, cudaStream_t s);
-void launch_value_head(const __nv_bfloat16* H, int hp, const float* w, const float* b, float* out,
-                       int rows, cudaStream_t s);
+void launch_value_head(const float* vraw, const float* b, float* out, int rows, cudaStream_t s);
 void launch_gae(const float* rew, const uint8_t* done, const float* V, float* adv, float* ret,
                 double* partials, int N, int T, float gamma, float lam, cudaStream_t s);
 int gae_blocks(int N);

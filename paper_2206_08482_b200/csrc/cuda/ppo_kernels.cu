@@ -56,34 +56,16 @@ __global__ void env_init_kernel(EnvParams ep, float* x, int* ep_step, int* ep_le
 // actions, synthetic Ant-like dynamics, reward, integer episode clock / reset, and the
 // next GEMM-ready observation row. Traffic/env: H_L row (2*hp B) + 2*S*4 (state) + 2*S_p
 // (obs) + (A+3)*4 B.
-template <int NV>
 __global__ void __launch_bounds__(256) act_env_kernel(const ActEnvArgs a) {
-  extern __shared__ float w_s[];  // [A][hp] policy head weights, staged once per block
   const int lane = threadIdx.x & 31;
   const EnvParams& ep = a.ep;
-  const int A = ep.A, S = ep.S, hp = a.hp;
-  for (int i = threadIdx.x; i < A * hp; i += blockDim.x) w_s[i] = a.w_mu[i];
-  __syncthreads();
+  const int A = ep.A, S = ep.S;
   const int e = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (e >= ep.N) return;
   const int gid = ep.env0 + e;
 
-  // mu: lane owns hidden units k = 2*lane + 64 j (+1); transpose-reduce across the warp
-  float part[NV];
-#pragma unroll
-  for (int i = 0; i < NV; ++i) part[i] = 0.f;
-  const __nv_bfloat16* hrow = a.H + (long long)e * hp;
-  for (int k = 2 * lane; k < hp; k += 64) {
-    const float2 h = ld_bf16x2(hrow + k);
-#pragma unroll
-    for (int i = 0; i < NV; ++i)
-      if (i < A) {
-        const float2 w = *reinterpret_cast<const float2*>(w_s + i * hp + k);
-        part[i] += h.x * w.x + h.y * w.y;
-      }
-  }
-  const float red = warp_reduce_transpose<NV>(part);
-  const float mu_mine = lane < A ? red + a.b_mu[lane] : 0.f;
+  // mu: policy-head GEMM output (tensor cores) + bias
+  const float mu_mine = lane < A ? a.mu[(long long)e * kHeadG + lane] + a.b_mu[lane] : 0.f;
 
   // N(0,1) noise: lane q draws Philox block q -> 4 normals for actions 4q..4q+3
   const uint32_t step = uint32_t(a.ctl->iteration * ep.T + a.t);
@@ -163,20 +145,10 @@ __global__ void __launch_bounds__(256) act_env_kernel(const ActEnvArgs a) {
 }
 
 // ------------------------------------------------------------------ value head
-__global__ void __launch_bounds__(256) value_head_kernel(const __nv_bfloat16* H, int hp, const float* w,
-                                                         const float* b, float* out, int rows) {
-  const int lane = threadIdx.x & 31;
-  const long long r = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (r >= rows) return;
-  float s = 0.f;
-  for (int k = lane * 8; k < hp; k += 256) {
-    float h[8];
-    load8(H + r * hp + k, h);
-#pragma unroll
-    for (int j = 0; j < 8; ++j) s += h[j] * w[k + j];
-  }
-  s = warp_sum(s);
-  if (lane == 0) out[r] = s + b[0];
+// V[r] = value-head GEMM output (column 0) + bias.
+__global__ void __launch_bounds__(256) value_head_kernel(const float* vraw, const float* b, float* out, int rows) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < rows) out[r] = vraw[(long long)r * kHeadG] + b[0];
 }
 
 // ------------------------------------------------------------------ K5 GAE
@@ -344,26 +316,13 @@ void launch_env_init(const EnvParams& ep, float* x, int* ep_step, int* ep_len, i
 void launch_act_env(const ActEnvArgs& a, cudaStream_t s) {
   if (a.ep.A > kMaxAct) invalid("act_dim > 31 unsupported by the act/env kernel");
   if (a.ep.S > 32 * kMaxObsPerLane) invalid("obs_dim > 256 unsupported by the act/env kernel");
-  if (a.hp > kMaxHeadIn) invalid("last hidden width > 512 unsupported by the act/env kernel");
   const int blocks = (a.ep.N * 32 + 255) / 256;
-  const size_t smem = size_t(a.ep.A) * a.hp * 4;
-  auto go = [&](auto kern) {
-    if (smem > 48 * 1024)
-      GMI_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    kern<<<blocks, 256, smem, s>>>(a);
-  };
-  if (a.ep.A <= 8)
-    go(act_env_kernel<8>);
-  else if (a.ep.A <= 16)
-    go(act_env_kernel<16>);
-  else
-    go(act_env_kernel<32>);
+  act_env_kernel<<<blocks, 256, 0, s>>>(a);
   GMI_CUDA_CHECK(cudaGetLastError());
 }
 
-void launch_value_head(const __nv_bfloat16* H, int hp, const float* w, const float* b, float* out, int rows,
-                       cudaStream_t s) {
-  value_head_kernel<<<(rows * 32 + 255) / 256, 256, 0, s>>>(H, hp, w, b, out, rows);
+void launch_value_head(const float* vraw, const float* b, float* out, int rows, cudaStream_t s) {
+  value_head_kernel<<<(rows + 255) / 256, 256, 0, s>>>(vraw, b, out, rows);
   GMI_CUDA_CHECK(cudaGetLastError());
 }
 

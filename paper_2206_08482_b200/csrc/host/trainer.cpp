@@ -123,6 +123,7 @@ struct Trainer::Gmi {
   __nv_bfloat16* H[2][GMI_MAX_HIDDEN] = {};
   __nv_bfloat16* D[2][2] = {};
   __nv_bfloat16 *Gpi = nullptr, *Gv = nullptr;
+  float* outh[2] = {};  // [Mrows][64] fp32 head outputs: mu (policy), v in column 0 (value)
   float* slab[2][GMI_MAX_HIDDEN] = {};
   float* colsum[2][GMI_MAX_HIDDEN] = {};
   float* head_slab[2] = {};
@@ -130,6 +131,7 @@ struct Trainer::Gmi {
   float* grad = nullptr;
   GemmParams fwd_roll[GMI_MAX_HIDDEN], fwd_val[GMI_MAX_HIDDEN], fwd_train[GMI_MAX_HIDDEN];
   GemmParams dw[GMI_MAX_HIDDEN], dx[GMI_MAX_HIDDEN], dhead;
+  GemmParams head_roll, head_val, head_train, head_dx;  // head forward / input-grad GEMMs
   int bn_roll[GMI_MAX_HIDDEN] = {}, bn_val[GMI_MAX_HIDDEN] = {}, bn_fwd[GMI_MAX_HIDDEN] = {};
   int bn_dx[GMI_MAX_HIDDEN] = {}, bn_dw[GMI_MAX_HIDDEN] = {}, bn_head = 0;
   double flop_roll[GMI_MAX_HIDDEN] = {}, flop_fwd[GMI_MAX_HIDDEN] = {}, flop_dw[GMI_MAX_HIDDEN] = {},
@@ -266,6 +268,7 @@ void Trainer::alloc() {
     }
     g.Gpi = static_cast<__nv_bfloat16*>(dev((long long)g.Bm * ppo::kHeadG * 2));
     g.Gv = static_cast<__nv_bfloat16*>(dev((long long)g.Bm * ppo::kHeadG * 2));
+    for (int n = 0; n < 2; ++n) g.outh[n] = static_cast<float*>(dev((long long)g.Mrows * ppo::kHeadG * 4));
     g.grad = static_cast<float*>(dev(P * 4));
     g.head_part = static_cast<float*>(dev((long long)ppo::head_loss_blocks(g.Bm) * ppo::head_partial_stride(A) * 4));
   }
@@ -397,6 +400,53 @@ void Trainer::build_plans() {
         g.flop_dx[l] = 2.0 * real * g.Bm;
       }
     }
+    // heads on the tensor cores. Forward: mu = H_L W_mu^T (N padded to 64, rows >= A read as
+    // zero by TMA), v = H^v_L w_v^T; fp32 outputs, bias added by the consumer kernels.
+    const int head_rows[2] = {A, 1};
+    auto head_fwd = [&](int n, int M, const CUtensorMap& amap) {
+      GemmProblem p{};
+      p.map_a = amap;
+      p.map_b = tma_kmajor(shadow_ + geo_.net[n][L].w, hp, head_rows[n], hp, 64);
+      p.map_out = make_tma_out_f32(g.outh[n], ppo::kHeadG, g.Mrows, 1, ppo::kHeadG, (uint64_t)g.Mrows * ppo::kHeadG);
+      p.M = M;
+      p.N = ppo::kHeadG;
+      p.K = hp;
+      p.kb_per_split = (hp + kGemmBlockK - 1) / kGemmBlockK;
+      return p;
+    };
+    g.head_roll = GemmParams{};
+    g.head_roll.prob[0] = head_fwd(0, g.N, tma_kmajor(g.H[0][L - 1], hp, g.Mrows, hp, kGemmBlockM));
+    g.head_roll.num_problems = 1;
+    g.head_roll.splits = 1;
+    g.head_val = GemmParams{};
+    g.head_val.prob[0] = head_fwd(1, g.Mrows, tma_kmajor(g.H[1][L - 1], hp, g.Mrows, hp, kGemmBlockM));
+    g.head_val.num_problems = 1;
+    g.head_val.splits = 1;
+    g.head_train = GemmParams{};
+    for (int n = 0; n < 2; ++n)
+      g.head_train.prob[n] = head_fwd(n, g.Bm, tma_kmajor(g.H[n][L - 1], hp, g.Mrows, hp, kGemmBlockM));
+    g.head_train.num_problems = 2;
+    g.head_train.splits = 1;
+    // Head input gradient: dPre_{L-1} = (G W_head) * elu'(H_L), K = 64 (zero-padded G).
+    g.head_dx = GemmParams{};
+    {
+      const __nv_bfloat16* G[2] = {g.Gpi, g.Gv};
+      for (int n = 0; n < 2; ++n) {
+        GemmProblem p{};
+        p.map_a = tma_kmajor(G[n], ppo::kHeadG, g.Bm, ppo::kHeadG, kGemmBlockM);
+        p.map_b = tma_mnmajor(shadow_ + geo_.net[n][L].w, hp, head_rows[n], hp);
+        p.map_out = make_tma_out_bf16(g.D[n][0], hp, g.Bm, hp);
+        p.aux = g.H[n][L - 1];
+        p.ld_aux = hp;
+        p.M = g.Bm;
+        p.N = hp;
+        p.K = ppo::kHeadG;
+        p.kb_per_split = 1;
+        g.head_dx.prob[n] = p;
+      }
+      g.head_dx.num_problems = 2;
+      g.head_dx.splits = 1;
+    }
     // head weight gradients on the tensor cores: dW_mu = G_pi^T H_L, dw_v = G_v^T H^v_L
     const int bnh = std::min(256, ((hp + 63) / 64) * 64);
     g.bn_head = bnh;
@@ -505,11 +555,10 @@ void Trainer::rollout(Gmi& g) {
       if (l == 0) P.prob[0].a_row0 = t * g.N;
       gemm(g, P, g.bn_roll[l], 0, 0, EPI_BIAS_ELU, g.flop_roll[l]);
     }
+    gemm(g, g.head_roll, 64, 0, 0, EPI_F32, 2.0 * geo_.A * geo_.width[L] * g.N);
     ppo::ActEnvArgs a{};
     a.ep = {g.N, geo_.S, geo_.A, S_p, g.env0, T_, cfg_.seed};
-    a.H = g.H[0][L - 1];
-    a.hp = geo_.wp[L];
-    a.w_mu = params_ + head.w;
+    a.mu = g.outh[0];
     a.b_mu = params_ + head.b;
     a.log_std = params_ + geo_.log_std;
     a.x = g.x;
@@ -540,7 +589,10 @@ void Trainer::values(Gmi& g) {
       if (l == 0) P.prob[0].a_row0 = int(c0);
       gemm(g, P, g.bn_val[l], 0, 0, EPI_BIAS_ELU, g.flop_roll[l] * double(m) / g.N);
     }
-    ppo::launch_value_head(g.H[1][L - 1], geo_.wp[L], params_ + head.w, params_ + head.b, g.V + c0, m, g.s);
+    GemmParams Ph = g.head_val;
+    Ph.prob[0].M = m;
+    gemm(g, Ph, 64, 0, 0, EPI_F32, 2.0 * geo_.width[L] * m);
+    ppo::launch_value_head(g.outh[1], params_ + head.b, g.V + c0, m, g.s);
     ++launches_;
   }
   ppo::launch_gae(g.rew, g.done, g.V, g.adv, g.ret, g.gae_part, g.N, T_, cfg_.gamma, cfg_.lam, g.s);
@@ -555,13 +607,12 @@ void Trainer::train_minibatch(Gmi& g, int k) {
     if (l == 0) P.prob[0].a_row0 = P.prob[1].a_row0 = k * g.Bm;
     gemm(g, P, g.bn_fwd[l], 0, 0, EPI_BIAS_ELU, g.flop_fwd[l]);
   }
+  const double hflop = 2.0 * (A + 1) * geo_.width[L] * g.Bm;
+  gemm(g, g.head_train, 64, 0, 0, EPI_F32, hflop);
   ppo::HeadLossArgs h{};
-  h.Hpi = g.H[0][L - 1];
-  h.Hv = g.H[1][L - 1];
-  h.hp = hp;
-  h.w_mu = params_ + geo_.net[0][L].w;
+  h.mu = g.outh[0];
+  h.v = g.outh[1];
   h.b_mu = params_ + geo_.net[0][L].b;
-  h.w_v = params_ + geo_.net[1][L].w;
   h.b_v = params_ + geo_.net[1][L].b;
   h.log_std = params_ + geo_.log_std;
   const long long r0 = (long long)k * g.Bm;
@@ -569,8 +620,6 @@ void Trainer::train_minibatch(Gmi& g, int k) {
   h.oldlp = g.oldlp_sh + r0;
   h.adv = g.adv_sh + r0;
   h.ret = g.ret_sh + r0;
-  h.Dpi = g.D[0][0];
-  h.Dv = g.D[1][0];
   h.Gpi = g.Gpi;
   h.Gv = g.Gv;
   h.partial = g.head_part;
@@ -581,6 +630,7 @@ void Trainer::train_minibatch(Gmi& g, int k) {
   h.ent_coef = cfg_.ent_coef;
   ppo::launch_head_loss(h, g.s);
   ++launches_;
+  gemm(g, g.head_dx, gemm_choose_bn(g.Bm, hp, 2, 1, g.ctas), 0, 1, EPI_DACT, hflop);
   gemm(g, g.dhead, g.bn_head, 1, 1, EPI_F32, g.flop_head);
   for (int l = L - 1; l >= 0; --l) {
     GemmParams P = g.dw[l];
