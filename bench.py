@@ -33,7 +33,7 @@ UNIT = "env-steps/s"
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--steps", type=int, default=30)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--config", default=os.path.join(ROOT, "configs", "at_4096env_3x256.cfg"))
@@ -54,51 +54,88 @@ def dist_env():
 
 # ------------------------------------------------------------------ clocks during the timed region
 class ClockSampler:
-    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    """Samples SM clock and throttle reasons every `period` s on a thread (NVML), falling
+    back to `nvidia-smi -lms` when NVML is unavailable."""
 
-    def __init__(self):
-        self.proc = None
-        self.path = os.path.join(tempfile.gettempdir(), f"gmi_clocks_{os.getpid()}.csv")
+    REASONS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+               ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+               ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"))
+
+    def __init__(self, device: int = 0, period: float = 0.01):
+        import threading
+        self.device, self.period = device, period
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        self._thread = None
+        self._nvml = None
+
+    def _run(self):
+        nv = self._nvml
+        h = nv.nvmlDeviceGetHandleByIndex(self.device)
+        self.max_mhz = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        while not self._stop.is_set():
+            self.samples.append(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
+            mask = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+            for name, attr in self.REASONS:
+                if mask & getattr(nv, attr, 0):
+                    self.reasons.add(name)
+            time.sleep(self.period)
 
     def start(self):
+        import threading
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                                          "-lms", "200"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
-        except OSError:
-            self.proc = None
+            import pynvml
+            pynvml.nvmlInit()
+            self._nvml = pynvml
+        except Exception:  # noqa: BLE001 - no NVML: clocks reported as unavailable
+            return
+        self._thread = threading.Thread(target=self._run, daemon=True)
+        self._thread.start()
 
     def stop(self):
-        if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.proc.terminate()
-        self.proc.wait(timeout=10)
-        rows = []
-        with open(self.path) as f:
-            for line in f:
-                parts = [x.strip() for x in line.split(",")]
-                if len(parts) >= 9 and parts[1].replace(".", "").isdigit():
-                    rows.append(parts)
-        os.unlink(self.path)
-        if not rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
-        sm = [float(r[1]) for r in rows]
-        mx = max(float(r[2]) for r in rows)
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower().startswith("active")})
-        loaded = [s for s in sm if s > 0.5 * mx] or sm
-        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": mx, "reasons": reasons,
-                "samples": len(rows)}
+        if self._thread is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"], "samples": 0}
+        self._stop.set()
+        self._thread.join(timeout=5)
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["no samples"], "samples": 0}
+        loaded = [x for x in self.samples if x > 0.5 * (self.max_mhz or max(self.samples))] or self.samples
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples), "source": "nvml"}
 
 
 def measured_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             j = json.load(f)
-        return j["bf16_tflops_sustained"], j["hbm_gbs"], "measured (MEASURED_PEAKS.json, sustained bf16)"
+        return j["bf16_tflops_sustained"], j["hbm_gbs"], "measured (MEASURED_PEAKS.json: sustained bf16, HBM copy)"
     except (OSError, KeyError, ValueError):
         return 1400.0, 6650.0, "fallback (B200_PROFILING.md)"
+
+
+GEMM_PHASES = ("roll_gemm", "roll_head", "val_gemm", "val_head", "fwd_gemm", "head_fwd", "head_dx", "head_dw",
+               "dw_gemm", "dx_gemm")
+
+
+def phase_table(prof: dict, iter_ms: float, peak_tf: float, peak_gbs: float) -> dict:
+    """Per-phase device time per iteration (GMI 0 + update stream, CUDA events around every
+    launch) with the roofline each phase is bound by: tensor (algorithmic flops / time) or
+    HBM (algorithmic bytes / time)."""
+    out = {}
+    for name, p in prof.items():
+        if p["launches"] == 0:
+            continue
+        row = {"ms": round(p["ms"], 4), "share": round(p["ms"] / iter_ms, 4) if iter_ms else None,
+               "launches": p["launches"]}
+        if p["flop"] > 0 and p["ms"] > 0:
+            tf = p["flop"] / (p["ms"] / 1e3) / 1e12
+            row.update(bound="tensor", achieved_tflops=round(tf, 1), frac=round(tf / peak_tf, 4))
+        elif p["bytes"] > 0 and p["ms"] > 0:
+            gbs = p["bytes"] / (p["ms"] / 1e3) / 1e9
+            row.update(bound="hbm", achieved_gbs=round(gbs, 1), frac=round(gbs / peak_gbs, 4))
+        out[name] = row
+    return out
 
 
 # ------------------------------------------------------------------ CPU leg (oracle port)
@@ -162,7 +199,7 @@ def main():
     cfg.num_gpus, cfg.rank, cfg.device = world, rank, local
     cfg.num_envs = envs_per_gpu * world
     cfg.gmi_backend = args.backend
-    cfg.instrument = 1
+    cfg.instrument = 0  # timed loop runs the plain graph; a separate pass below is instrumented
     nid = None
     if world > 1:
         obj = [nccl_unique_id() if rank == 0 else None]
@@ -181,14 +218,12 @@ def main():
         trainer.iteration()
 
     # ---- device-timed throughput: K iterations enqueued back to back, inputs resident in HBM
-    clocks = ClockSampler()
+    clocks = ClockSampler(local)
     if rank == 0:
         clocks.start()
     barrier()
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t0.record(upd)
-    launches = 0
-    gemm_ms = gemm_flop = 0.0
     for _ in range(args.steps):
         trainer.iteration_async()
     t1.record(upd)
@@ -197,7 +232,6 @@ def main():
     clk = clocks.stop() if rank == 0 else None
     ms = t0.elapsed_time(t1)
     launches = st.kernel_launches * args.steps
-    gemm_ms, gemm_flop = st.gemm_ms, st.gemm_flop  # last iteration's GEMM launches (GMI 0)
     ms_t = torch.tensor([ms], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
@@ -218,8 +252,23 @@ def main():
         dist.all_reduce(wall_t, op=dist.ReduceOp.MAX)
     e2e = steps_total / wall_t.item()
 
+    # ---- instrumented pass (not part of the timed numbers): CUDA events around every launch
+    # of GMI 0 and the update stream -> per-phase time, flops and bytes for the rooflines.
+    trainer.set_instrument(True)
+    trainer.iteration()
+    t2, t3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    t2.record(upd)
+    trainer.iteration_async()
+    t3.record(upd)
+    ist = trainer.synchronize()
+    prof = trainer.profile()
+    iter_ms_instr = t2.elapsed_time(t3)
+    trainer.set_instrument(False)
+
     if rank == 0:
-        peak_tf, _, peak_src = measured_peaks()
+        peak_tf, peak_gbs, peak_src = measured_peaks()
+        gemm_ms, gemm_flop = ist.gemm_ms, ist.gemm_flop
         achieved = gemm_flop / (gemm_ms / 1e3) / 1e12 if gemm_ms > 0 else 0.0
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
@@ -239,11 +288,14 @@ def main():
                        "gmis_per_gpu": cfg.gmis_per_gpu, "gmi_backend": ["streams", "green_ctx"][args.backend],
                        "parallelism": f"dp{world * cfg.gmis_per_gpu} ({world} GPU x {cfg.gmis_per_gpu} GMI)",
                        "env_steps_per_step": steps_total // args.steps,
-                       "l2": f"no flush: per-iteration working set ~{ws:.0f} MB > 126 MB L2"},
-            "roofline": {"bound": "tensor", "kernel": "tcgen05 bf16 GEMM (all MLP layers, GMI 0)",
+                       "l2": f"no flush: per-iteration working set ~{ws:.0f} MB > 126 MB L2",
+                       "cuda_graph": bool(cfg.use_graph)},
+            "roofline": {"bound": "tensor", "kernel": "gemm_tcgen05_kernel (every MLP GEMM of GMI 0, all phases)",
                          "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
                          "frac": achieved / peak_tf, "traffic": None, "peak_source": peak_src,
-                         "gemm_share_of_step": (gemm_ms / (ms_max / args.steps)) if ms_max else None},
+                         "gemm_share_of_step": gemm_ms / iter_ms_instr if iter_ms_instr else None,
+                         "instrumented_ms_per_step": iter_ms_instr},
+            "phases": phase_table(prof, iter_ms_instr, peak_tf, peak_gbs),
             "cpu_baseline": cpu,
             "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": 16, "d2h_bytes_per_step": 32,
                     "api": "gmi_ppo_iteration (synchronous C-ABI call per step)"},

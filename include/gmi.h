@@ -380,6 +380,44 @@ GMI_API int gmi_ppo_param_count(void* trainer, long long* padded, long long* rea
 /* cudaStream_t of local GMI `gmi` (-1: the update / reduction stream). */
 GMI_API int gmi_ppo_stream(void* trainer, int gmi, void** stream);
 
+/* Per-phase device time of the last completed iteration when cfg.instrument = 1: CUDA
+ * events around every launch on GMI 0's stream and the update stream, plus the
+ * algorithmic flops (tensor-core phases) or HBM bytes (memory-bound phases) of those
+ * launches, for the per-kernel roofline. */
+enum {
+  GMI_PH_ROLL_GEMM, /* rollout: policy hidden layers, M = envs per GMI */
+  GMI_PH_ROLL_HEAD, /* rollout: policy head GEMM */
+  GMI_PH_ACT_ENV,   /* rollout: Gaussian action + env step + reset + next obs */
+  GMI_PH_VAL_GEMM,  /* values: value-net hidden layers over (T+1) x envs rows */
+  GMI_PH_VAL_HEAD,  /* values: value head GEMM + bias */
+  GMI_PH_GAE,       /* GAE scan + advantage statistics */
+  GMI_PH_SHUFFLE,   /* epoch permutation gather */
+  GMI_PH_FWD_GEMM,  /* update: hidden forward (both nets) */
+  GMI_PH_HEAD_FWD,  /* update: head forward GEMMs */
+  GMI_PH_HEAD_LOSS, /* update: clipped surrogate / value loss + head output grads */
+  GMI_PH_HEAD_DX,   /* update: head input-gradient GEMM */
+  GMI_PH_HEAD_DW,   /* update: head weight-gradient GEMM */
+  GMI_PH_DW_GEMM,   /* update: hidden weight-gradient GEMMs (split-K slabs) */
+  GMI_PH_COLSUM,    /* update: bias-gradient column sums */
+  GMI_PH_DX_GEMM,   /* update: hidden input-gradient GEMMs */
+  GMI_PH_SEGMENTS,  /* update: fixed-order gradient assembly */
+  GMI_PH_REDUCE,    /* K1 intra-GPU GMI gradient fold */
+  GMI_PH_ALLREDUCE, /* NCCL cross-GPU gradient all-reduce */
+  GMI_PH_ADAM,      /* Adam on the shared replica */
+  GMI_PH_OTHER,     /* copies, control block */
+  GMI_PPO_PHASES
+};
+typedef struct {
+  double ms;    /* summed event time of the phase's launches */
+  double flop;  /* algorithmic flops (GEMM phases) */
+  double bytes; /* algorithmic HBM bytes (memory-bound phases) */
+  int launches;
+} gmi_ppo_phase_t;
+GMI_API const char* gmi_ppo_phase_name(int phase);
+GMI_API int gmi_ppo_profile(void* trainer, gmi_ppo_phase_t* out /* [GMI_PPO_PHASES] */);
+/* Toggle cfg.instrument on a live trainer (re-captures the iteration graph). */
+GMI_API int gmi_ppo_set_instrument(void* trainer, int on);
+
 /* ------------------------------------------------------------------ diagnostics
  * Single tcgen05 GEMM launch, D[m][n] = sum_k A(m,k) B(n,k), bf16 in, fp32 accumulate.
  * a_mn/b_mn: 0 = operand stored [rows x K], 1 = stored [K x rows].

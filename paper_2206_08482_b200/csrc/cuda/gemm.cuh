@@ -26,18 +26,33 @@
 
 namespace gmi {
 
-// elu(x) = x > 0 ? x : expm1(x), branch-free: degree-6 Taylor polynomial on (-0.25, 0],
-// SFU exp below (|rel err| < 2e-6, far below the bf16 output rounding).
-__device__ __forceinline__ float elu_fast(float x) {
-  float p = fmaf(x, 1.f / 720.f, 1.f / 120.f);
-  p = fmaf(p, x, 1.f / 24.f);
-  p = fmaf(p, x, 1.f / 6.f);
-  p = fmaf(p, x, 0.5f);
-  p = fmaf(p, x, 1.f);
-  p *= x;
-  const float e = __expf(x) - 1.f;
-  const float neg = x > -0.25f ? p : e;
-  return x > 0.f ? x : neg;
+// elu on a pair, (acc + bias) -> x > 0 ? x : expm1(x), in 1.5 FMA-pipe instructions, one
+// SFU exp and two min/max per element (the epilogue is issue-bound, so this is what sets
+// the GEMM's speed at K <= 256). n = 2^(x log2 e) - 1 has absolute error ~1e-7
+// (ex2.approx), i.e. well below bf16 output rounding except at |x| < ~1e-3, where
+// max(min(n, 0), x) picks whichever of n and x is closer to expm1(x) (expm1(x) >= x).
+__device__ __forceinline__ float2 bias_elu2(float2 acc, float2 bias) {
+  const float2 x = ptx::add2(acc, bias);
+  const float2 t = ptx::mul2(x, make_float2(1.4426950408889634f, 1.4426950408889634f));
+  const float2 n = ptx::add2(make_float2(ptx::ex2_approx(t.x), ptx::ex2_approx(t.y)), make_float2(-1.f, -1.f));
+  return make_float2(fmaxf(fminf(n.x, 0.f), x.x), fmaxf(fminf(n.y, 0.f), x.y));
+}
+
+// dPre = dH * elu'(H), elu'(H) = H > 0 ? 1 : H + 1 (H = elu output). acc * (min(H,0) + 1)
+// equals fma(acc, min(H,0), acc) exactly (min(H,0) + 1 is exact for bf16 H >= -1), so the
+// packed FFMA2 form is bit-identical to the scalar definition.
+__device__ __forceinline__ float2 dact2(float2 acc, uint32_t h2) {
+  const float2 h = make_float2(__uint_as_float(h2 << 16), __uint_as_float(h2 & 0xFFFF0000u));
+  return ptx::fma2(acc, make_float2(fminf(h.x, 0.f), fminf(h.y, 0.f)), acc);
+}
+
+// n / d for 0 <= n < 2^24, d >= 1 via an fp32 reciprocal (exact after one correction step);
+// the tile decode runs on every warp once per tile, so integer division is worth avoiding.
+__device__ __forceinline__ int fdiv(int n, int d, float rd) {
+  int q = __float2int_rz(__int2float_rn(n) * rd);
+  const int r = n - q * d;
+  q += (r >= d) - (r < 0);
+  return q;
 }
 
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
@@ -106,13 +121,16 @@ __global__ void __launch_bounds__(gemm_threads(EPI), 1) gemm_tcgen05_kernel(cons
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
+  const int mn_tiles = mtiles * ntiles;
+  const float r_per_prob = 1.f / float(per_prob), r_mn = 1.f / float(mn_tiles), r_n = 1.f / float(ntiles);
   auto decode = [&](int tile, int& prob, int& split, int& m0, int& n0, int& kb0, int& nkb) {
-    prob = tile / per_prob;
+    prob = fdiv(tile, per_prob, r_per_prob);
     int r = tile - prob * per_prob;
-    split = r / (mtiles * ntiles);
-    r -= split * (mtiles * ntiles);
-    m0 = (r / ntiles) * kGemmBlockM;
-    n0 = (r % ntiles) * BN;
+    split = fdiv(r, mn_tiles, r_mn);
+    r -= split * mn_tiles;
+    const int mt = fdiv(r, ntiles, r_n);
+    m0 = mt * kGemmBlockM;
+    n0 = (r - mt * ntiles) * BN;
     kb0 = split * P.prob[prob].kb_per_split;
     const int kb1 = min(nkb_total, kb0 + P.prob[prob].kb_per_split);
     nkb = kb1 > kb0 ? kb1 - kb0 : 0;
@@ -228,10 +246,12 @@ __global__ void __launch_bounds__(gemm_threads(EPI), 1) gemm_tcgen05_kernel(cons
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
               const float4 b = __ldg(b4 + j);
-              packed[2 * j] = pack_bf16(elu_fast(__uint_as_float(r[4 * j]) + b.x),
-                                        elu_fast(__uint_as_float(r[4 * j + 1]) + b.y));
-              packed[2 * j + 1] = pack_bf16(elu_fast(__uint_as_float(r[4 * j + 2]) + b.z),
-                                            elu_fast(__uint_as_float(r[4 * j + 3]) + b.w));
+              const float2 y0 = bias_elu2(make_float2(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1])),
+                                          make_float2(b.x, b.y));
+              const float2 y1 = bias_elu2(make_float2(__uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3])),
+                                          make_float2(b.z, b.w));
+              packed[2 * j] = pack_bf16(y0.x, y0.y);
+              packed[2 * j + 1] = pack_bf16(y1.x, y1.y);
             }
           } else {  // EPI_DACT
             uint4 hv[4] = {};
@@ -245,11 +265,9 @@ __global__ void __launch_bounds__(gemm_threads(EPI), 1) gemm_tcgen05_kernel(cons
               const uint32_t hw[4] = {hv[qd].x, hv[qd].y, hv[qd].z, hv[qd].w};
 #pragma unroll
               for (int x = 0; x < 4; ++x) {
-                const __nv_bfloat162 h2 = *reinterpret_cast<const __nv_bfloat162*>(&hw[x]);
-                const float h0 = __bfloat162float(h2.x), h1 = __bfloat162float(h2.y);
                 const int j = qd * 8 + x * 2;
-                packed[j / 2] = pack_bf16(__uint_as_float(r[j]) * (h0 > 0.f ? 1.f : h0 + 1.f),
-                                          __uint_as_float(r[j + 1]) * (h1 > 0.f ? 1.f : h1 + 1.f));
+                const float2 d = dact2(make_float2(__uint_as_float(r[j]), __uint_as_float(r[j + 1])), hw[x]);
+                packed[j / 2] = pack_bf16(d.x, d.y);
               }
             }
           }

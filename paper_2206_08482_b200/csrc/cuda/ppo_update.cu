@@ -133,29 +133,79 @@ __global__ void __launch_bounds__(256) colsum_kernel(const ColsumArgs a, int row
 }
 
 // ------------------------------------------------------------------ gradient assembly
-// dst[i] = sum_p src[p*stride + i]. Block = 32 consecutive elements x 8 warps; warp g sums
-// parts g, g+8, ... into 4 accumulators; warps combined in order (deterministic).
+// dst[i] = sum_p src[p*stride + i]. Block = 128 consecutive elements (one float4 per lane) x
+// 8 warps; warp w sums the contiguous part range [w*np/8, (w+1)*np/8) in part order with 4
+// loads in flight, then the 8 warp sums are added in warp order (deterministic, and the same
+// fixed order for every launch). Segments whose length / stride / pointers are not 16-byte
+// multiples take the scalar lane path with the same order.
 constexpr int kMaxSegments = 64;
+constexpr int kSegElems = 128;
 struct SegmentTable {
   Segment s[kMaxSegments];
+  int first_block[kMaxSegments + 1];  // prefix of blocks per segment
+  int nseg;
 };
 __global__ void __launch_bounds__(256) segments_kernel(const __grid_constant__ SegmentTable t) {
-  __shared__ float acc_s[8][33];
-  const Segment& sg = t.s[blockIdx.y];
+  __shared__ float4 acc_s[8][32];
+  int si = 0;
+  while (si + 1 < t.nseg && (int)blockIdx.x >= t.first_block[si + 1]) ++si;
+  const Segment& sg = t.s[si];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int i = blockIdx.x * 32 + lane;
-  if (blockIdx.x * 32 >= sg.len) return;  // block-uniform
-  float acc[4] = {0.f, 0.f, 0.f, 0.f};
-  if (i < sg.len) {
-    int k = 0;
-    for (int p = warp; p < sg.nparts; p += 8, ++k) acc[k & 3] += sg.src[(long long)p * sg.stride + i];
+  const int i0 = (blockIdx.x - t.first_block[si]) * kSegElems + lane * 4;
+  const int p0 = warp * sg.nparts / 8, p1 = (warp + 1) * sg.nparts / 8;
+  const bool vec = ((sg.len | (int)(sg.stride & 3)) & 3) == 0 &&
+                   ((reinterpret_cast<uintptr_t>(sg.src) | reinterpret_cast<uintptr_t>(sg.dst)) & 15) == 0;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (vec) {
+    if (i0 < sg.len) {
+      const float* base = sg.src + i0;
+      int p = p0;
+      for (; p + 4 <= p1; p += 4) {
+        float4 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[u] = __ldcs(reinterpret_cast<const float4*>(base + (long long)(p + u) * sg.stride));
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          acc.x += v[u].x;
+          acc.y += v[u].y;
+          acc.z += v[u].z;
+          acc.w += v[u].w;
+        }
+      }
+      for (; p < p1; ++p) {
+        const float4 v = __ldcs(reinterpret_cast<const float4*>(base + (long long)p * sg.stride));
+        acc.x += v.x;
+        acc.y += v.y;
+        acc.z += v.z;
+        acc.w += v.w;
+      }
+    }
+  } else {
+    float a[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+      if (i0 + c < sg.len)
+        for (int p = p0; p < p1; ++p) a[c] += sg.src[(long long)p * sg.stride + i0 + c];
+    acc = make_float4(a[0], a[1], a[2], a[3]);
   }
-  acc_s[warp][lane] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+  acc_s[warp][lane] = acc;
   __syncthreads();
-  if (warp == 0 && i < sg.len) {
-    float s = 0.f;
-    for (int w = 0; w < 8; ++w) s += acc_s[w][lane];
-    sg.dst[i] = s;
+  if (warp == 0 && i0 < sg.len) {
+    float4 s = acc_s[0][lane];
+#pragma unroll
+    for (int w = 1; w < 8; ++w) {
+      const float4 v = acc_s[w][lane];
+      s.x += v.x;
+      s.y += v.y;
+      s.z += v.z;
+      s.w += v.w;
+    }
+    if (vec) {
+      *reinterpret_cast<float4*>(sg.dst + i0) = s;
+    } else {
+      const float o[4] = {s.x, s.y, s.z, s.w};
+      for (int c = 0; c < 4 && i0 + c < sg.len; ++c) sg.dst[i0 + c] = o[c];
+    }
   }
 }
 
@@ -197,12 +247,13 @@ void launch_segments(const Segment* segs, int n, cudaStream_t s) {
   for (int base = 0; base < n; base += kMaxSegments) {
     SegmentTable t{};
     const int m = std::min(kMaxSegments, n - base);
-    int maxlen = 1;
+    t.nseg = m;
+    t.first_block[0] = 0;
     for (int i = 0; i < m; ++i) {
       t.s[i] = segs[base + i];
-      maxlen = std::max(maxlen, t.s[i].len);
+      t.first_block[i + 1] = t.first_block[i] + (std::max(1, t.s[i].len) + kSegElems - 1) / kSegElems;
     }
-    segments_kernel<<<dim3((maxlen + 31) / 32, m), 256, 0, s>>>(t);
+    segments_kernel<<<t.first_block[m], 256, 0, s>>>(t);
     GMI_CUDA_CHECK(cudaGetLastError());
   }
 }

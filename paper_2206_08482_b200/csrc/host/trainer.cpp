@@ -200,9 +200,9 @@ Trainer::~Trainer() {
   cudaDeviceSynchronize();
   if (graph_) cudaGraphExecDestroy(graph_);
   if (nccl_) ncclCommDestroy(static_cast<ncclComm_t>(nccl_));
-  for (auto& e : ev_pool_) {
-    cudaEventDestroy(e.first);
-    cudaEventDestroy(e.second);
+  for (auto& m : marks_) {
+    cudaEventDestroy(m.a);
+    cudaEventDestroy(m.b);
   }
   for (auto& g : gmis_) cudaEventDestroy(g->ev_done);
   if (ev_adam_) cudaEventDestroy(ev_adam_);
@@ -490,24 +490,42 @@ void Trainer::build_plans() {
 }
 
 // ------------------------------------------------------------------ launch helpers
-void Trainer::gemm(Gmi& g, const GemmParams& P, int bn, int amn, int bmn, int epi, double flop) {
-  const bool timed = cfg_.instrument && g.local == 0;
-  if (timed) {
-    if (ev_used_ >= int(ev_pool_.size())) {
-      cudaEvent_t a, b;
-      GMI_CUDA_CHECK(cudaEventCreate(&a));
-      GMI_CUDA_CHECK(cudaEventCreate(&b));
-      ev_pool_.push_back({a, b});
-      ev_flop_.push_back(0);
-    }
-    GMI_CUDA_CHECK(cudaEventRecord(ev_pool_[ev_used_].first, g.s));
+template <class F>
+void Trainer::timed(cudaStream_t s, int phase, double flop, double bytes, F&& f) {
+  const bool on = cfg_.instrument && (s == upd_ || s == gmis_[0]->s);
+  if (!on) {
+    f();
+    return;
   }
-  gemm_launch(P, bn, amn, bmn, epi, g.s, g.ctas);
+  if (marks_used_ >= int(marks_.size())) {
+    Mark m;
+    GMI_CUDA_CHECK(cudaEventCreate(&m.a));
+    GMI_CUDA_CHECK(cudaEventCreate(&m.b));
+    marks_.push_back(m);
+  }
+  Mark& m = marks_[marks_used_++];
+  // under stream capture a plain record only forms a dependency; the external flag makes it
+  // a real event-record node of the graph, so the replay timestamps it
+  const unsigned flags = capturing_ ? cudaEventRecordExternal : cudaEventRecordDefault;
+  GMI_CUDA_CHECK(cudaEventRecordWithFlags(m.a, s, flags));
+  f();
+  GMI_CUDA_CHECK(cudaEventRecordWithFlags(m.b, s, flags));
+  m.phase = phase;
+  m.flop = flop;
+  m.bytes = bytes;
+}
+
+void Trainer::gemm(Gmi& g, int phase, const GemmParams& P, int bn, int amn, int bmn, int epi, double flop) {
+  timed(g.s, phase, flop, 0.0, [&] { gemm_launch(P, bn, amn, bmn, epi, g.s, g.ctas); });
   ++launches_;
-  if (timed) {
-    GMI_CUDA_CHECK(cudaEventRecord(ev_pool_[ev_used_].second, g.s));
-    ev_flop_[ev_used_] = flop;
-    ++ev_used_;
+}
+
+void Trainer::set_instrument(int on) {
+  GMI_CUDA_CHECK(cudaDeviceSynchronize());
+  cfg_.instrument = on ? 1 : 0;
+  if (graph_) {  // the captured sequence has (or lacks) the event records
+    GMI_CUDA_CHECK(cudaGraphExecDestroy(graph_));
+    graph_ = nullptr;
   }
 }
 
@@ -544,18 +562,21 @@ void Trainer::write_control() {
 
 // ------------------------------------------------------------------ phases
 void Trainer::rollout(Gmi& g) {
-  const int L = geo_.L, S_p = geo_.wp[0];
+  const int L = geo_.L, S_p = geo_.wp[0], S = geo_.S, A = geo_.A;
   if (iteration_ > 0)  // the last observation of the previous rollout seeds this one
-    GMI_CUDA_CHECK(cudaMemcpyAsync(g.X_roll, g.X_roll + (long long)T_ * g.N * S_p, (size_t)g.N * S_p * 2,
-                                   cudaMemcpyDeviceToDevice, g.s));
+    timed(g.s, GMI_PH_OTHER, 0.0, 4.0 * g.N * S_p, [&] {
+      GMI_CUDA_CHECK(cudaMemcpyAsync(g.X_roll, g.X_roll + (long long)T_ * g.N * S_p, (size_t)g.N * S_p * 2,
+                                     cudaMemcpyDeviceToDevice, g.s));
+    });
   const Tensor& head = geo_.net[0][L];
+  const double env_bytes = double(g.N) * (8.0 * A + 8.0 * S + 2.0 * S_p + 29.0);
   for (int t = 0; t < T_; ++t) {
     for (int l = 0; l < L; ++l) {
       GemmParams P = g.fwd_roll[l];
       if (l == 0) P.prob[0].a_row0 = t * g.N;
-      gemm(g, P, g.bn_roll[l], 0, 0, EPI_BIAS_ELU, g.flop_roll[l]);
+      gemm(g, GMI_PH_ROLL_GEMM, P, g.bn_roll[l], 0, 0, EPI_BIAS_ELU, g.flop_roll[l]);
     }
-    gemm(g, g.head_roll, 64, 0, 0, EPI_F32, 2.0 * geo_.A * geo_.width[L] * g.N);
+    gemm(g, GMI_PH_ROLL_HEAD, g.head_roll, 64, 0, 0, EPI_F32, 2.0 * geo_.A * geo_.width[L] * g.N);
     ppo::ActEnvArgs a{};
     a.ep = {g.N, geo_.S, geo_.A, S_p, g.env0, T_, cfg_.seed};
     a.mu = g.outh[0];
@@ -572,7 +593,7 @@ void Trainer::rollout(Gmi& g) {
     a.done = g.done + (long long)t * g.N;
     a.t = t;
     a.ctl = ctl_dev_;
-    ppo::launch_act_env(a, g.s);
+    timed(g.s, GMI_PH_ACT_ENV, 0.0, env_bytes, [&] { ppo::launch_act_env(a, g.s); });
     ++launches_;
   }
 }
@@ -587,16 +608,20 @@ void Trainer::values(Gmi& g) {
       GemmParams P = g.fwd_val[l];
       P.prob[0].M = m;
       if (l == 0) P.prob[0].a_row0 = int(c0);
-      gemm(g, P, g.bn_val[l], 0, 0, EPI_BIAS_ELU, g.flop_roll[l] * double(m) / g.N);
+      gemm(g, GMI_PH_VAL_GEMM, P, g.bn_val[l], 0, 0, EPI_BIAS_ELU, g.flop_roll[l] * double(m) / g.N);
     }
     GemmParams Ph = g.head_val;
     Ph.prob[0].M = m;
-    gemm(g, Ph, 64, 0, 0, EPI_F32, 2.0 * geo_.width[L] * m);
-    ppo::launch_value_head(g.outh[1], params_ + head.b, g.V + c0, m, g.s);
+    gemm(g, GMI_PH_VAL_HEAD, Ph, 64, 0, 0, EPI_F32, 2.0 * geo_.width[L] * m);
+    timed(g.s, GMI_PH_VAL_HEAD, 0.0, 8.0 * m,
+          [&] { ppo::launch_value_head(g.outh[1], params_ + head.b, g.V + c0, m, g.s); });
     ++launches_;
   }
-  ppo::launch_gae(g.rew, g.done, g.V, g.adv, g.ret, g.gae_part, g.N, T_, cfg_.gamma, cfg_.lam, g.s);
-  ppo::launch_adv_stats(g.gae_part, ppo::gae_blocks(g.N), (long long)T_ * g.N, g.adv_stats, g.s);
+  const double TN = double(T_) * g.N;
+  timed(g.s, GMI_PH_GAE, 0.0, 17.0 * TN + 4.0 * g.N, [&] {
+    ppo::launch_gae(g.rew, g.done, g.V, g.adv, g.ret, g.gae_part, g.N, T_, cfg_.gamma, cfg_.lam, g.s);
+    ppo::launch_adv_stats(g.gae_part, ppo::gae_blocks(g.N), (long long)T_ * g.N, g.adv_stats, g.s);
+  });
   launches_ += 2;
 }
 
@@ -605,10 +630,10 @@ void Trainer::train_minibatch(Gmi& g, int k) {
   for (int l = 0; l < L; ++l) {
     GemmParams P = g.fwd_train[l];
     if (l == 0) P.prob[0].a_row0 = P.prob[1].a_row0 = k * g.Bm;
-    gemm(g, P, g.bn_fwd[l], 0, 0, EPI_BIAS_ELU, g.flop_fwd[l]);
+    gemm(g, GMI_PH_FWD_GEMM, P, g.bn_fwd[l], 0, 0, EPI_BIAS_ELU, g.flop_fwd[l]);
   }
   const double hflop = 2.0 * (A + 1) * geo_.width[L] * g.Bm;
-  gemm(g, g.head_train, 64, 0, 0, EPI_F32, hflop);
+  gemm(g, GMI_PH_HEAD_FWD, g.head_train, 64, 0, 0, EPI_F32, hflop);
   ppo::HeadLossArgs h{};
   h.mu = g.outh[0];
   h.v = g.outh[1];
@@ -628,23 +653,26 @@ void Trainer::train_minibatch(Gmi& g, int k) {
   h.clip = cfg_.clip;
   h.vf_coef = cfg_.vf_coef;
   h.ent_coef = cfg_.ent_coef;
-  ppo::launch_head_loss(h, g.s);
+  timed(g.s, GMI_PH_HEAD_LOSS, 0.0, double(g.Bm) * (10.0 * A + 18.0), [&] { ppo::launch_head_loss(h, g.s); });
   ++launches_;
-  gemm(g, g.head_dx, gemm_choose_bn(g.Bm, hp, 2, 1, g.ctas), 0, 1, EPI_DACT, hflop);
-  gemm(g, g.dhead, g.bn_head, 1, 1, EPI_F32, g.flop_head);
+  gemm(g, GMI_PH_HEAD_DX, g.head_dx, gemm_choose_bn(g.Bm, hp, 2, 1, g.ctas), 0, 1, EPI_DACT, hflop);
+  gemm(g, GMI_PH_HEAD_DW, g.dhead, g.bn_head, 1, 1, EPI_F32, g.flop_head);
   for (int l = L - 1; l >= 0; --l) {
     GemmParams P = g.dw[l];
     if (l == 0) P.prob[0].b_row0 = P.prob[1].b_row0 = k * g.Bm;
-    gemm(g, P, g.bn_dw[l], 1, 1, EPI_F32, g.flop_dw[l]);
+    gemm(g, GMI_PH_DW_GEMM, P, g.bn_dw[l], 1, 1, EPI_F32, g.flop_dw[l]);
     const int cur = (L - 1 - l) & 1;
     const __nv_bfloat16* Ds[2] = {g.D[0][cur], g.D[1][cur]};
     const int widths[2] = {geo_.wp[l + 1], geo_.wp[l + 1]};
     float* outs[2] = {g.colsum[0][l], g.colsum[1][l]};
-    ppo::launch_colsum(Ds, widths, outs, 2, g.Bm, g.s);
+    timed(g.s, GMI_PH_COLSUM, 0.0, 2.0 * 2.0 * g.Bm * geo_.wp[l + 1],
+          [&] { ppo::launch_colsum(Ds, widths, outs, 2, g.Bm, g.s); });
     ++launches_;
-    if (l > 0) gemm(g, g.dx[l], g.bn_dx[l], 0, 1, EPI_DACT, g.flop_dx[l]);
+    if (l > 0) gemm(g, GMI_PH_DX_GEMM, g.dx[l], g.bn_dx[l], 0, 1, EPI_DACT, g.flop_dx[l]);
   }
-  ppo::launch_segments(g.segs.data(), int(g.segs.size()), g.s);
+  double seg_bytes = 0;
+  for (const auto& sg : g.segs) seg_bytes += 4.0 * sg.len * (sg.nparts + 1.0);
+  timed(g.s, GMI_PH_SEGMENTS, 0.0, seg_bytes, [&] { ppo::launch_segments(g.segs.data(), int(g.segs.size()), g.s); });
   launches_ += (int(g.segs.size()) + 63) / 64;
 }
 
@@ -659,13 +687,18 @@ void Trainer::reduce_and_step(int step_in_iter) {
       p.per_gpu[0].push_back(g->local);
       bufs.push_back(g->grad);
     }
-    reduce_device(plan::Algo::MPR, p, bufs.data(), grad_sum_, size_t(geo_.P), GMI_F32, false, upd_);
+    timed(upd_, GMI_PH_REDUCE, 0.0, 4.0 * geo_.P * (n_local_ + 1), [&] {
+      reduce_device(plan::Algo::MPR, p, bufs.data(), grad_sum_, size_t(geo_.P), GMI_F32, false, upd_);
+    });
     ++launches_;
     src = grad_sum_;
   }
   if (nccl_) {
-    NCCL_CHECK(ncclAllReduce(src, grad_sum_, size_t(geo_.P), ncclFloat32, ncclSum, static_cast<ncclComm_t>(nccl_),
-                             upd_));
+    const double bus = 2.0 * (cfg_.num_gpus - 1) / cfg_.num_gpus * 4.0 * geo_.P;
+    timed(upd_, GMI_PH_ALLREDUCE, 0.0, bus, [&] {
+      NCCL_CHECK(ncclAllReduce(src, grad_sum_, size_t(geo_.P), ncclFloat32, ncclSum,
+                               static_cast<ncclComm_t>(nccl_), upd_));
+    });
     src = grad_sum_;
   }
   ppo::AdamArgs a{};
@@ -683,7 +716,7 @@ void Trainer::reduce_and_step(int step_in_iter) {
   a.b2 = cfg_.beta2;
   a.eps = cfg_.adam_eps;
   a.inv_n = 1.0f / float(n_total_);
-  ppo::launch_adam(a, upd_);
+  timed(upd_, GMI_PH_ADAM, 0.0, 30.0 * geo_.P, [&] { ppo::launch_adam(a, upd_); });
   ++launches_;
   GMI_CUDA_CHECK(cudaEventRecord(ev_adam_, upd_));
 }
@@ -703,7 +736,7 @@ void Trainer::enqueue_rollout() {
 // Every kernel / copy / collective of one iteration, on the GMI streams and upd_.
 void Trainer::record_iteration() {
   launches_ = 0;
-  ev_used_ = 0;
+  marks_used_ = 0;
   GMI_CUDA_CHECK(cudaEventRecord(ev_start_, upd_));
   for (auto& g : gmis_) {
     GMI_CUDA_CHECK(cudaStreamWaitEvent(g->s, ev_start_, 0));
@@ -714,8 +747,11 @@ void Trainer::record_iteration() {
   for (int e = 0; e < cfg_.epochs; ++e) {
     for (auto& g : gmis_) {
       if (step > 0) GMI_CUDA_CHECK(cudaStreamWaitEvent(g->s, ev_adam_, 0));
-      ppo::launch_shuffle(g->X_roll, g->act, g->logp, g->adv, g->ret, g->adv_stats, g->X_sh, g->act_sh, g->oldlp_sh,
-                          g->adv_sh, g->ret_sh, g->N, T_, geo_.wp[0], geo_.A, cfg_.seed, g->gid, e, ctl_dev_, g->s);
+      timed(g->s, GMI_PH_SHUFFLE, 0.0, 2.0 * g->B * (2.0 * geo_.wp[0] + 4.0 * geo_.A + 12.0), [&] {
+        ppo::launch_shuffle(g->X_roll, g->act, g->logp, g->adv, g->ret, g->adv_stats, g->X_sh, g->act_sh,
+                            g->oldlp_sh, g->adv_sh, g->ret_sh, g->N, T_, geo_.wp[0], geo_.A, cfg_.seed, g->gid, e,
+                            ctl_dev_, g->s);
+      });
       ++launches_;
     }
     for (int k = 0; k < K_; ++k, ++step) {
@@ -728,9 +764,11 @@ void Trainer::record_iteration() {
     }
   }
   for (auto& g : gmis_) GMI_CUDA_CHECK(cudaStreamWaitEvent(upd_, g->ev_done, 0));
-  GMI_CUDA_CHECK(cudaMemcpyAsync(stats_dev_ + 4, gmis_[0]->adv_stats, 3 * 4, cudaMemcpyDeviceToDevice, upd_));
-  GMI_CUDA_CHECK(cudaMemcpyAsync(stats_host_, stats_dev_, 8 * 4, cudaMemcpyDeviceToHost, upd_));
-  ppo::launch_control_advance(ctl_dev_, cfg_.epochs * K_, upd_);
+  timed(upd_, GMI_PH_OTHER, 0.0, 0.0, [&] {
+    GMI_CUDA_CHECK(cudaMemcpyAsync(stats_dev_ + 4, gmis_[0]->adv_stats, 3 * 4, cudaMemcpyDeviceToDevice, upd_));
+    GMI_CUDA_CHECK(cudaMemcpyAsync(stats_host_, stats_dev_, 8 * 4, cudaMemcpyDeviceToHost, upd_));
+    ppo::launch_control_advance(ctl_dev_, cfg_.epochs * K_, upd_);
+  });
   ++launches_;
 }
 
@@ -766,6 +804,24 @@ void Trainer::enqueue_iteration(bool host_control) {
 void Trainer::synchronize(gmi_ppo_stats_t* st) {
   GMI_CUDA_CHECK(cudaStreamSynchronize(upd_));
   for (auto& g : gmis_) GMI_CUDA_CHECK(cudaStreamSynchronize(g->s));
+  gmi_ppo_phase_t gemm{};
+  if (cfg_.instrument) {
+    std::memset(phases_, 0, sizeof(phases_));
+    for (int i = 0; i < marks_used_; ++i) {
+      float ms = 0;
+      GMI_CUDA_CHECK(cudaEventElapsedTime(&ms, marks_[i].a, marks_[i].b));
+      gmi_ppo_phase_t& ph = phases_[marks_[i].phase];
+      ph.ms += ms;
+      ph.flop += marks_[i].flop;
+      ph.bytes += marks_[i].bytes;
+      ph.launches += 1;
+      if (marks_[i].flop > 0) {
+        gemm.ms += ms;
+        gemm.flop += marks_[i].flop;
+        gemm.launches += 1;
+      }
+    }
+  }
   if (!st) return;
   std::memset(st, 0, sizeof(*st));
   const double Bm = gmis_[0]->Bm;
@@ -778,13 +834,9 @@ void Trainer::synchronize(gmi_ppo_stats_t* st) {
   for (auto& g : gmis_) steps += (long long)T_ * g->N;
   st->env_steps = steps;
   st->kernel_launches = launches_;
-  for (int i = 0; i < ev_used_; ++i) {
-    float ms = 0;
-    GMI_CUDA_CHECK(cudaEventElapsedTime(&ms, ev_pool_[i].first, ev_pool_[i].second));
-    st->gemm_ms += ms;
-    st->gemm_flop += ev_flop_[i];
-  }
-  st->gemm_launches = ev_used_;
+  st->gemm_ms = gemm.ms;
+  st->gemm_flop = gemm.flop;
+  st->gemm_launches = gemm.launches;
 }
 
 // ------------------------------------------------------------------ parity hooks
@@ -967,6 +1019,25 @@ GMI_API int gmi_ppo_param_count(void* t, long long* padded, long long* real) {
 
 GMI_API int gmi_ppo_stream(void* t, int gmi, void** stream) {
   return gmi::guarded([&] { *stream = static_cast<gmi::Trainer*>(t)->stream(gmi); });
+}
+
+GMI_API const char* gmi_ppo_phase_name(int phase) {
+  static const char* const names[GMI_PPO_PHASES] = {
+      "roll_gemm", "roll_head", "act_env", "val_gemm", "val_head", "gae",      "shuffle",
+      "fwd_gemm",  "head_fwd",  "head_loss", "head_dx", "head_dw", "dw_gemm", "colsum",
+      "dx_gemm",   "segments",  "reduce",  "allreduce", "adam",   "other"};
+  return phase >= 0 && phase < GMI_PPO_PHASES ? names[phase] : nullptr;
+}
+
+GMI_API int gmi_ppo_profile(void* t, gmi_ppo_phase_t* out) {
+  return gmi::guarded([&] {
+    if (!out) gmi::invalid("null output");
+    std::memcpy(out, static_cast<gmi::Trainer*>(t)->phases(), sizeof(gmi_ppo_phase_t) * GMI_PPO_PHASES);
+  });
+}
+
+GMI_API int gmi_ppo_set_instrument(void* t, int on) {
+  return gmi::guarded([&] { static_cast<gmi::Trainer*>(t)->set_instrument(on); });
 }
 
 }  // extern "C"

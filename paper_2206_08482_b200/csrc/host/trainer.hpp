@@ -61,7 +61,11 @@ class Trainer {
   void values(Gmi& g);
   void train_minibatch(Gmi& g, int k);
   void reduce_and_step(int k);
-  void gemm(Gmi& g, const GemmParams& P, int bn, int amn, int bmn, int epi, double flop);
+  void gemm(Gmi& g, int phase, const GemmParams& P, int bn, int amn, int bmn, int epi, double flop);
+  // Runs f (which enqueues work on s); with cfg.instrument and s = GMI 0's stream or the
+  // update stream, brackets it with CUDA events booked to `phase` (+ algorithmic flop/bytes).
+  template <class F>
+  void timed(cudaStream_t s, int phase, double flop, double bytes, F&& f);
 
   gmi_ppo_config_t cfg_;
   Geometry geo_;
@@ -87,10 +91,19 @@ class Trainer {
   int launches_ = 0;       // kernels in one iteration
   bool capturing_ = false;
   cudaGraphExec_t graph_ = nullptr;
-  // instrumentation (GEMM launches of GMI 0)
-  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pool_;
-  std::vector<double> ev_flop_;
-  int ev_used_ = 0;
+  // instrumentation: one event pair per launch of GMI 0 / the update stream
+  struct Mark {
+    cudaEvent_t a = nullptr, b = nullptr;
+    int phase = 0;
+    double flop = 0, bytes = 0;
+  };
+  std::vector<Mark> marks_;
+  int marks_used_ = 0;
+  gmi_ppo_phase_t phases_[GMI_PPO_PHASES] = {};
+
+ public:
+  const gmi_ppo_phase_t* phases() const { return phases_; }
+  void set_instrument(int on);
 };
 
 }  // namespace gmi

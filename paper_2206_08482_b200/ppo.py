@@ -29,6 +29,13 @@ class PpoConfigT(C.Structure):
                 ("instrument", C.c_int)]
 
 
+PPO_PHASES = 20  # GMI_PPO_PHASES
+
+
+class PhaseT(C.Structure):
+    _fields_ = [("ms", C.c_double), ("flop", C.c_double), ("bytes", C.c_double), ("launches", C.c_int)]
+
+
 class PpoStatsT(C.Structure):
     _fields_ = [("policy_loss", C.c_double), ("value_loss", C.c_double), ("approx_kl", C.c_double),
                 ("clip_frac", C.c_double), ("mean_reward", C.c_double), ("env_steps", C.c_longlong),
@@ -51,6 +58,9 @@ _PROTOS = {
     "gmi_ppo_set": (C.c_int, [C.c_void_p, C.c_char_p, C.c_int, C.c_void_p, C.c_longlong]),
     "gmi_ppo_param_count": (C.c_int, [C.c_void_p, C.POINTER(C.c_longlong), C.POINTER(C.c_longlong)]),
     "gmi_ppo_stream": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_void_p)]),
+    "gmi_ppo_phase_name": (C.c_char_p, [C.c_int]),
+    "gmi_ppo_profile": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "gmi_ppo_set_instrument": (C.c_int, [C.c_void_p, C.c_int]),
 }
 L.PROTOTYPES.update(_PROTOS)
 if L._lib is not None:  # library already loaded: bind the late prototypes
@@ -83,7 +93,7 @@ class PpoConfig:
     device: int = 0
     gmi_backend: int = 0
     sm_per_gmi: int = 0
-    use_graph: int = 0
+    use_graph: int = 1
     instrument: int = 0
 
     def to_c(self) -> PpoConfigT:
@@ -196,6 +206,18 @@ class Trainer:
         s = C.c_void_p()
         L.check(L.lib().gmi_ppo_stream(self._h, gmi, C.byref(s)))
         return s.value or 0
+
+    def set_instrument(self, on: bool) -> None:
+        L.check(L.lib().gmi_ppo_set_instrument(self._h, int(bool(on))))
+
+    def profile(self) -> dict:
+        """Per-phase device time of the last iteration run with instrumentation on:
+        {phase: {"ms", "flop", "bytes", "launches"}} (GMI 0 stream + update stream)."""
+        arr = (PhaseT * PPO_PHASES)()
+        L.check(L.lib().gmi_ppo_profile(self._h, arr))
+        return {L.lib().gmi_ppo_phase_name(i).decode(): {"ms": a.ms, "flop": a.flop, "bytes": a.bytes,
+                                                        "launches": a.launches}
+                for i, a in enumerate(arr)}
 
     def get(self, what: str, gmi: int = 0) -> np.ndarray:
         n = C.c_longlong()
