@@ -421,10 +421,11 @@ GMI_API int gmi_ppo_set_instrument(void* trainer, int on);
 /* ------------------------------------------------------------------ diagnostics
  * Single tcgen05 GEMM launch, D[m][n] = sum_k A(m,k) B(n,k), bf16 in, fp32 accumulate.
  * a_mn/b_mn: 0 = operand stored [rows x K], 1 = stored [K x rows].
- * epi: 0 = bf16 elu(acc + bias), 1 = bf16 acc * elu'(aux), 2 = fp32 (split-K slabs). */
+ * epi: 0 = bf16 elu(acc + bias), 1 = bf16 acc * elu'(aux), 2 = fp32 (split-K slabs).
+ * weight_stationary: 1 = B resident in shared memory (N <= 256, K <= 256, splits == 1). */
 GMI_API int gmi_dev_gemm(int a_mn, int b_mn, int epi, int M, int N, int K, const void* A, long long lda,
                  const void* B, long long ldb, void* out, long long ldo, const float* bias,
-                 const void* aux, long long ld_aux, int splits, void* stream);
+                 const void* aux, long long ld_aux, int splits, int weight_stationary, void* stream);
 
 #ifdef __cplusplus
 }

@@ -187,7 +187,7 @@ PROTOTYPES: dict[str, tuple] = {
     "gmi_config_search": (ci, [vp, P(SearchSettingsT)]),
     "gmi_config_get": (ci, [vp, C.c_char_p, C.c_char_p, C.c_char_p, csz, c_int_p]),
     "gmi_config_free": (None, [vp]),
-    "gmi_dev_gemm": (ci, [ci, ci, ci, ci, ci, ci, vp, cll, vp, cll, vp, cll, vp, vp, cll, ci, vp]),
+    "gmi_dev_gemm": (ci, [ci, ci, ci, ci, ci, ci, vp, cll, vp, cll, vp, cll, vp, vp, cll, ci, ci, vp]),
 }
 
 # Error codes (gmi.h)

@@ -11,6 +11,12 @@
 // [rows x K]) or MN-major (row-major [K x rows]); MN-major lets the weight-gradient GEMM
 // (dW = dPre^T H, reduction over minibatch rows) read activations in place.
 //
+// Weight-stationary mode (WS = 1; N <= BN, K <= 256, no split-K): each CTA serves one
+// problem (CTA index mod problems), loads that problem's whole B operand (the layer's
+// weights, <= 128 KB) into shared memory once and then streams only the A tiles
+// (activations / dPre rows). This removes the per-tile weight re-reads that made the
+// training-forward and input-gradient GEMMs L2-bandwidth-bound.
+//
 // Epilogues:
 //   EPI_BIAS_ELU  hidden-layer forward: bf16 out = elu(acc + bias[n])
 //   EPI_DACT      hidden-layer backward: bf16 out = acc * elu'(H[m][n]), elu' = H > 0 ? 1 : H + 1
@@ -22,6 +28,7 @@
 #include <cuda_bf16.h>
 
 #include "gemm_types.hpp"
+#include "launch.cuh"
 #include "ptx.cuh"
 
 namespace gmi {
@@ -60,22 +67,25 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
-template <int BN, int EPI>
+template <int BN, int EPI, int WS>
 struct GemmSmem {
   static constexpr int kEpiWarps = gemm_epi_warps(EPI);
-  static constexpr int kStages = BN == 256 ? 3 : 4;
+  static constexpr int kStages = WS ? 3 : (BN == 256 ? 3 : 4);
   static constexpr uint32_t kA = kGemmBlockM * kGemmBlockK * 2;  // 16 KB
-  static constexpr uint32_t kB = BN * kGemmBlockK * 2;
-  static constexpr uint32_t kStage = kA + kB;
-  static constexpr uint32_t kStaging = EPI == 2 ? 4096 : 2048;  // one 32x32 chunk per warp, x2
-  static constexpr uint32_t kBarOff = kStages * kStage + kEpiWarps * 2 * kStaging;
+  static constexpr uint32_t kB = BN * kGemmBlockK * 2;           // one k-block of B
+  static constexpr uint32_t kStage = WS ? kA : kA + kB;
+  static constexpr uint32_t kBRes = WS ? kGemmMaxKbWS * kB : 0;  // resident B (WS)
+  static constexpr int kStagingBufs = WS ? 1 : 2;
+  static constexpr uint32_t kStaging = EPI == 2 ? 4096 : 2048;  // one 32x32 chunk per warp
+  static constexpr uint32_t kBarOff = kStages * kStage + kBRes + kEpiWarps * kStagingBufs * kStaging;
   static constexpr uint32_t kBytes = kBarOff + 256 + 1024;  // + barriers + alignment slack
   static constexpr uint32_t kTmemCols = 2 * BN < 32 ? 32 : 2 * BN;
+  static_assert(kBytes <= 232448, "shared memory budget");
 };
 
-template <int BN, int A_MN, int B_MN, int EPI>
+template <int BN, int A_MN, int B_MN, int EPI, int WS>
 __global__ void __launch_bounds__(gemm_threads(EPI), 1) gemm_tcgen05_kernel(const __grid_constant__ GemmParams P) {
-  using L = GemmSmem<BN, EPI>;
+  using L = GemmSmem<BN, EPI, WS>;
   constexpr int S = L::kStages;
   constexpr int kEpiWarps = L::kEpiWarps;
   constexpr uint32_t kIdesc = ptx::umma_idesc_bf16(kGemmBlockM, BN, A_MN, B_MN);
@@ -83,12 +93,14 @@ __global__ void __launch_bounds__(gemm_threads(EPI), 1) gemm_tcgen05_kernel(cons
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* staging = smem + S * L::kStage;
+  uint8_t* b_res = smem + S * L::kStage;  // WS: resident B, k-block j at j * kB
+  uint8_t* staging = b_res + L::kBRes;
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + L::kBarOff);
   uint64_t* empty_bar = full_bar + S;
   uint64_t* tfull_bar = empty_bar + S;   // [2] accumulator ready
   uint64_t* tempty_bar = tfull_bar + 2;  // [2] accumulator drained
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+  uint64_t* bres_bar = tempty_bar + 2;   // WS: resident B landed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bres_bar + 1);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -108,6 +120,7 @@ __global__ void __launch_bounds__(gemm_threads(EPI), 1) gemm_tcgen05_kernel(cons
       ptx::mbar_init(&tfull_bar[b], 1);
       ptx::mbar_init(&tempty_bar[b], kEpiWarps);
     }
+    ptx::mbar_init(bres_bar, 1);
     ptx::fence_mbar_init();
     for (int i = 0; i < P.num_problems; ++i) {
       ptx::tma_prefetch_desc(&P.prob[i].map_a);
@@ -116,14 +129,27 @@ __global__ void __launch_bounds__(gemm_threads(EPI), 1) gemm_tcgen05_kernel(cons
     }
   }
   if (warp == 1) ptx::tmem_alloc(tmem_slot, L::kTmemCols);
+  pdl_trigger();
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_wait();  // operands / bias / aux come from the preceding kernels in the stream
 
   const int mn_tiles = mtiles * ntiles;
   const float r_per_prob = 1.f / float(per_prob), r_mn = 1.f / float(mn_tiles), r_n = 1.f / float(ntiles);
+  const float r_np = 1.f / float(P.num_problems);
   auto decode = [&](int tile, int& prob, int& split, int& m0, int& n0, int& kb0, int& nkb) {
+    if constexpr (WS) {  // tile = m_tile * problems + prob; gridDim.x % problems == 0
+      const int mt = fdiv(tile, P.num_problems, r_np);
+      prob = tile - mt * P.num_problems;
+      split = 0;
+      m0 = mt * kGemmBlockM;
+      n0 = 0;
+      kb0 = 0;
+      nkb = nkb_total;
+      return;
+    }
     prob = fdiv(tile, per_prob, r_per_prob);
     int r = tile - prob * per_prob;
     split = fdiv(r, mn_tiles, r_mn);
@@ -139,6 +165,19 @@ __global__ void __launch_bounds__(gemm_threads(EPI), 1) gemm_tcgen05_kernel(cons
   if (warp == 0) {
     // ---------------- TMA producer (one lane)
     if (lane == 0) {
+      auto load_b = [&](const GemmProblem& pr, uint8_t* sb, uint64_t* bar, int n0, int k0) {
+        if constexpr (B_MN) {
+#pragma unroll
+          for (int j = 0; j < BN / 64; ++j) ptx::tma_load_2d(sb + j * 8192, &pr.map_b, bar, n0 + 64 * j, k0 + pr.b_row0);
+        } else {
+          ptx::tma_load_2d(sb, &pr.map_b, bar, k0, n0 + pr.b_row0);
+        }
+      };
+      if constexpr (WS) {  // this CTA's problem: whole B once
+        const GemmProblem& pr = P.prob[blockIdx.x % P.num_problems];
+        ptx::mbar_arrive_expect_tx(bres_bar, nkb_total * L::kB);
+        for (int j = 0; j < nkb_total; ++j) load_b(pr, b_res + j * L::kB, bres_bar, 0, j * kGemmBlockK);
+      }
       int it = 0;
       for (int tile = blockIdx.x; tile < ntile_total; tile += gridDim.x) {
         int prob, split, m0, n0, kb0, nkb;
@@ -148,7 +187,6 @@ __global__ void __launch_bounds__(gemm_threads(EPI), 1) gemm_tcgen05_kernel(cons
           const int s = it % S;
           if (it >= S) ptx::mbar_wait(&empty_bar[s], ((it / S) - 1) & 1);
           uint8_t* sa = smem + s * L::kStage;
-          uint8_t* sb = sa + L::kA;
           const int k0 = (kb0 + i) * kGemmBlockK;
           ptx::mbar_arrive_expect_tx(&full_bar[s], L::kStage);
           if constexpr (A_MN) {
@@ -158,13 +196,7 @@ __global__ void __launch_bounds__(gemm_threads(EPI), 1) gemm_tcgen05_kernel(cons
           } else {
             ptx::tma_load_2d(sa, &pr.map_a, &full_bar[s], k0, m0 + pr.a_row0);
           }
-          if constexpr (B_MN) {
-#pragma unroll
-            for (int j = 0; j < BN / 64; ++j)
-              ptx::tma_load_2d(sb + j * 8192, &pr.map_b, &full_bar[s], n0 + 64 * j, k0 + pr.b_row0);
-          } else {
-            ptx::tma_load_2d(sb, &pr.map_b, &full_bar[s], k0, n0 + pr.b_row0);
-          }
+          if constexpr (!WS) load_b(pr, sa + L::kA, &full_bar[s], n0, k0);
         }
       }
     }
@@ -172,6 +204,7 @@ __global__ void __launch_bounds__(gemm_threads(EPI), 1) gemm_tcgen05_kernel(cons
     // ---------------- MMA issuer (one lane), double-buffered TMEM accumulators
     if (lane == 0) {
       int it = 0, lt = 0;
+      if constexpr (WS) ptx::mbar_wait(bres_bar, 0);
       for (int tile = blockIdx.x; tile < ntile_total; tile += gridDim.x, ++lt) {
         int prob, split, m0, n0, kb0, nkb;
         decode(tile, prob, split, m0, n0, kb0, nkb);
@@ -184,7 +217,7 @@ __global__ void __launch_bounds__(gemm_threads(EPI), 1) gemm_tcgen05_kernel(cons
           ptx::mbar_wait(&full_bar[s], (it / S) & 1);
           ptx::tc_fence_after();
           const uint32_t sa = ptx::smem_u32(smem + s * L::kStage);
-          const uint32_t sb = sa + L::kA;
+          const uint32_t sb = WS ? ptx::smem_u32(b_res + i * L::kB) : sa + L::kA;
 #pragma unroll
           for (int k = 0; k < kGemmBlockK / 16; ++k) {
             // K-major: step 16 elements (32 B) inside the swizzle atom.
@@ -207,7 +240,7 @@ __global__ void __launch_bounds__(gemm_threads(EPI), 1) gemm_tcgen05_kernel(cons
     const int q = warp & 3;
     const int h = e >> 2;
     constexpr int kChunks = BN / 32;
-    uint8_t* stage_base = staging + e * 2 * L::kStaging;
+    uint8_t* stage_base = staging + e * L::kStagingBufs * L::kStaging;
     int sbuf = 0;
     int lt = 0;
     for (int tile = blockIdx.x; tile < ntile_total; tile += gridDim.x, ++lt) {
@@ -231,7 +264,7 @@ __global__ void __launch_bounds__(gemm_threads(EPI), 1) gemm_tcgen05_kernel(cons
           for (int j = 0; j < 32; ++j) r[j] = 0u;
         }
         uint8_t* st = stage_base + sbuf * L::kStaging;
-        if (lane == 0) ptx::bulk_wait_read<1>();  // the staging buffer used two stores ago is free
+        if (lane == 0) ptx::bulk_wait_read<L::kStagingBufs - 1>();  // this staging buffer's last store has read it
         __syncwarp();
         if constexpr (EPI == EPI_F32) {
           // 32 fp32 = 8 x 16 B per row; SWIZZLE_128B: chunk ^= row & 7
@@ -286,7 +319,7 @@ __global__ void __launch_bounds__(gemm_threads(EPI), 1) gemm_tcgen05_kernel(cons
             ptx::tma_store_2d(&pr.map_out, st, col0, rbase + pr.out_row0);
           ptx::bulk_commit();
         }
-        sbuf ^= 1;
+        sbuf = (sbuf + 1) % L::kStagingBufs;
       }
       ptx::tc_fence_before();
       __syncwarp();

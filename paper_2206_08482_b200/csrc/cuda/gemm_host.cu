@@ -102,22 +102,28 @@ int gemm_choose_bn(int M, int N, int problems, int splits, int sms) {
 
 namespace {
 
-template <int BN, int AMN, int BMN, int EPI>
+template <int BN, int AMN, int BMN, int EPI, int WS = 0>
 void launch_t(const GemmParams& P, int ctas, cudaStream_t s) {
-  constexpr int smem = GemmSmem<BN, EPI>::kBytes;
-  auto kern = gemm_tcgen05_kernel<BN, AMN, BMN, EPI>;
+  constexpr int smem = GemmSmem<BN, EPI, WS>::kBytes;
+  auto kern = gemm_tcgen05_kernel<BN, AMN, BMN, EPI, WS>;
   static bool configured = false;  // per instantiation
   if (!configured) {
     GMI_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     configured = true;
   }
-  kern<<<ctas, gemm_threads(EPI), smem, s>>>(P);
-  GMI_CUDA_CHECK(cudaGetLastError());
+  launch_pdl(kern, dim3(ctas), dim3(gemm_threads(EPI)), smem, s, P);
 }
 
 template <int BN>
-void launch_bn(const GemmParams& P, int a_mn, int b_mn, int epi, int ctas, cudaStream_t s) {
+void launch_bn(const GemmParams& P, int a_mn, int b_mn, int epi, int ctas, cudaStream_t s, int ws) {
   const int key = a_mn * 100 + b_mn * 10 + epi;
+  if (ws) {
+    switch (key) {
+      case 0 * 100 + 0 * 10 + EPI_BIAS_ELU: return launch_t<BN, 0, 0, EPI_BIAS_ELU, 1>(P, ctas, s);
+      case 0 * 100 + 1 * 10 + EPI_DACT: return launch_t<BN, 0, 1, EPI_DACT, 1>(P, ctas, s);
+      default: invalid("weight-stationary GEMM supports the forward and input-gradient epilogues only");
+    }
+  }
   switch (key) {
     case 0 * 100 + 0 * 10 + EPI_BIAS_ELU: return launch_t<BN, 0, 0, EPI_BIAS_ELU>(P, ctas, s);
     case 0 * 100 + 0 * 10 + EPI_F32: return launch_t<BN, 0, 0, EPI_F32>(P, ctas, s);
@@ -132,18 +138,30 @@ void launch_bn(const GemmParams& P, int a_mn, int b_mn, int epi, int ctas, cudaS
 
 }  // namespace
 
-void gemm_launch(const GemmParams& P, int bn, int a_mn, int b_mn, int epi, cudaStream_t s, int max_ctas) {
+int gemm_ws_bn(int M, int N, int K, int problems, int sms) {
+  const int bn = ((N + 63) / 64) * 64;
+  if (bn > 256 || K > kGemmMaxKbWS * kGemmBlockK) return 0;
+  if (((M + kGemmBlockM - 1) / kGemmBlockM) * problems < sms) return 0;
+  return bn;
+}
+
+void gemm_launch(const GemmParams& P, int bn, int a_mn, int b_mn, int epi, cudaStream_t s, int max_ctas, int ws) {
   static int sms = 0;
   if (!sms) sms = device_sm_count();
   for (int i = 1; i < P.num_problems; ++i)
     if (P.prob[i].M != P.prob[0].M || P.prob[i].N != P.prob[0].N || P.prob[i].K != P.prob[0].K)
       invalid("grouped GEMM problems must share M, N, K");
   const int tiles = gemm_tiles(P.prob[0].M, P.prob[0].N, bn, P.num_problems, P.splits);
-  const int ctas = std::max(1, std::min(tiles, max_ctas > 0 ? max_ctas : sms));
+  int ctas = std::max(1, std::min(tiles, max_ctas > 0 ? max_ctas : sms));
+  if (ws) {
+    if (P.splits != 1 || P.prob[0].N > bn || P.prob[0].K > kGemmMaxKbWS * kGemmBlockK)
+      invalid("weight-stationary GEMM needs splits == 1, N <= block_n, K <= 256");
+    ctas = std::max(P.num_problems, ctas / P.num_problems * P.num_problems);  // one problem per CTA
+  }
   switch (bn) {
-    case 64: return launch_bn<64>(P, a_mn, b_mn, epi, ctas, s);
-    case 128: return launch_bn<128>(P, a_mn, b_mn, epi, ctas, s);
-    case 256: return launch_bn<256>(P, a_mn, b_mn, epi, ctas, s);
+    case 64: return launch_bn<64>(P, a_mn, b_mn, epi, ctas, s, ws);
+    case 128: return launch_bn<128>(P, a_mn, b_mn, epi, ctas, s, ws);
+    case 256: return launch_bn<256>(P, a_mn, b_mn, epi, ctas, s, ws);
     default: invalid("GEMM block_n must be 64, 128 or 256");
   }
 }
@@ -152,12 +170,13 @@ void gemm_launch(const GemmParams& P, int bn, int a_mn, int b_mn, int epi, cudaS
 
 extern "C" GMI_API int gmi_dev_gemm(int a_mn, int b_mn, int epi, int M, int N, int K, const void* A, long long lda,
                                     const void* B, long long ldb, void* out, long long ldo, const float* bias,
-                                    const void* aux, long long ld_aux, int splits, void* stream) {
+                                    const void* aux, long long ld_aux, int splits, int weight_stationary,
+                                    void* stream) {
   return gmi::guarded([&] {
     if (M <= 0 || N <= 0 || K <= 0) gmi::invalid("gemm dims must be positive");
     if (N % 32 != 0) gmi::invalid("gemm N must be a multiple of 32");
     if (splits < 1) gmi::invalid("splits must be >= 1");
-    const int bn = gmi::gemm_choose_bn(M, N, 1, splits, gmi::device_sm_count());
+    const int bn = weight_stationary ? ((N + 63) / 64) * 64 : gmi::gemm_choose_bn(M, N, 1, splits, gmi::device_sm_count());
     gmi::GemmParams P{};
     gmi::GemmProblem& p = P.prob[0];
     p.map_a = a_mn ? gmi::tma_mnmajor(A, M, K, lda) : gmi::tma_kmajor(A, K, M, lda, gmi::kGemmBlockM);
@@ -174,6 +193,6 @@ extern "C" GMI_API int gmi_dev_gemm(int a_mn, int b_mn, int epi, int M, int N, i
     p.ld_aux = ld_aux;
     P.num_problems = 1;
     P.splits = splits;
-    gmi::gemm_launch(P, bn, a_mn, b_mn, epi, static_cast<cudaStream_t>(stream));
+    gmi::gemm_launch(P, bn, a_mn, b_mn, epi, static_cast<cudaStream_t>(stream), 0, weight_stationary);
   });
 }

@@ -24,7 +24,12 @@ CUtensorMap tma_kmajor(const void* p, int cols, long long rows, long long ld, in
 CUtensorMap tma_mnmajor(const void* p, int cols, long long rows, long long ld);
 
 // Launches the persistent kernel with min(tiles, max_ctas) CTAs (max_ctas 0 = SM count).
-void gemm_launch(const GemmParams& P, int bn, int a_mn, int b_mn, int epi, cudaStream_t s, int max_ctas = 0);
+// ws = 1: weight-stationary mode (requires N <= bn, K <= 256, splits == 1).
+void gemm_launch(const GemmParams& P, int bn, int a_mn, int b_mn, int epi, cudaStream_t s, int max_ctas = 0,
+                 int ws = 0);
+// Weight-stationary choice for a launch: returns the block N (N padded to 64) when every
+// CTA gets at least one tile and the weights fit, else 0 (use the streaming kernel).
+int gemm_ws_bn(int M, int N, int K, int problems, int sms);
 
 // Block N for a launch: the largest of {256,128,64} (<= padded N) that still gives at
 // least 4 tiles per SM, else the smallest.

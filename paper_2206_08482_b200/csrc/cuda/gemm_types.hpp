@@ -12,6 +12,7 @@ enum GemmEpi : int { EPI_BIAS_ELU = 0, EPI_DACT = 1, EPI_F32 = 2 };
 
 constexpr int kGemmBlockM = 128;
 constexpr int kGemmBlockK = 64;  // one 128-byte swizzle atom of bf16
+constexpr int kGemmMaxKbWS = 4;  // weight-stationary mode: K <= 256
 // Epilogue warps: 16 for the bf16 (elementwise-heavy) epilogues, 8 for fp32 slabs.
 constexpr int gemm_epi_warps(int epi) { return epi == 2 ? 8 : 16; }
 constexpr int gemm_threads(int epi) { return 64 + 32 * gemm_epi_warps(epi); }  // TMA, MMA, epilogue

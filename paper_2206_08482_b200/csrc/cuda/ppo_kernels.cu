@@ -12,6 +12,7 @@
 #include <algorithm>
 
 #include "../host/errors.hpp"
+#include "launch.cuh"
 #include "ppo.cuh"
 #include "ppo_common.cuh"
 #include "rng.cuh"
@@ -35,6 +36,8 @@ __device__ __forceinline__ float reset_value(uint64_t seed, int gid, int count, 
 // ------------------------------------------------------------------ env init
 __global__ void env_init_kernel(EnvParams ep, float* x, int* ep_step, int* ep_len, int* ep_count,
                                 __nv_bfloat16* X0) {
+  pdl_trigger();
+  pdl_wait();
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= ep.N) return;
   const int gid = ep.env0 + e;
@@ -57,6 +60,8 @@ __global__ void env_init_kernel(EnvParams ep, float* x, int* ep_step, int* ep_le
 // next GEMM-ready observation row. Traffic/env: H_L row (2*hp B) + 2*S*4 (state) + 2*S_p
 // (obs) + (A+3)*4 B.
 __global__ void __launch_bounds__(256) act_env_kernel(const ActEnvArgs a) {
+  pdl_trigger();
+  pdl_wait();
   const int lane = threadIdx.x & 31;
   const EnvParams& ep = a.ep;
   const int A = ep.A, S = ep.S;
@@ -147,6 +152,8 @@ __global__ void __launch_bounds__(256) act_env_kernel(const ActEnvArgs a) {
 // ------------------------------------------------------------------ value head
 // V[r] = value-head GEMM output (column 0) + bias.
 __global__ void __launch_bounds__(256) value_head_kernel(const float* vraw, const float* b, float* out, int rows) {
+  pdl_trigger();
+  pdl_wait();
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r < rows) out[r] = vraw[(long long)r * kHeadG] + b[0];
 }
@@ -161,6 +168,8 @@ __global__ void __launch_bounds__(1024) gae_kernel(const float* rew, const uint8
   __shared__ float r_s[32][33], v_s[33][33], a_s[32][33], q_s[32][33];
   __shared__ unsigned char d_s[32][33];
   __shared__ double red[3][32];
+  pdl_trigger();
+  pdl_wait();
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const int e0 = blockIdx.x * 32;
   const int e = e0 + tx;
@@ -234,6 +243,8 @@ __global__ void __launch_bounds__(1024) gae_kernel(const float* rew, const uint8
 
 __global__ void adv_stats_kernel(const double* partials, int nparts, long long count, float* stats) {
   __shared__ double sh[3][256];
+  pdl_trigger();
+  pdl_wait();
   double s1 = 0.0, s2 = 0.0, s3 = 0.0;
   for (int i = threadIdx.x; i < nparts; i += blockDim.x) {
     s1 += partials[3 * i];
@@ -267,6 +278,8 @@ __global__ void __launch_bounds__(256) shuffle_kernel(const __nv_bfloat16* X_rol
                                                       float* oldlp_sh, float* adv_sh, float* ret_sh, int N, int T,
                                                       int S_p, int A, uint64_t seed, int gmi_gid, int epoch,
                                                       const Control* ctl) {
+  pdl_trigger();
+  pdl_wait();
   const int cpr = S_p / 8;  // 16-byte chunks per row
   const long long B = (long long)T * N;
   const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -288,6 +301,8 @@ __global__ void __launch_bounds__(256) shuffle_kernel(const __nv_bfloat16* X_rol
 // ------------------------------------------------------------------ K8 Adam (fp32 master + bf16 shadow)
 // 28 B/param of algorithmic traffic: read p, m, v, g; write p, m, v, shadow(2 B).
 __global__ void __launch_bounds__(256) adam_kernel(const AdamArgs a) {
+  pdl_trigger();
+  pdl_wait();
   const long long s = a.ctl->adam_step0 + a.step_in_iter;  // completed steps before this one
   const float bc1 = a.bc[2 * s], bc2 = a.bc[2 * s + 1];
   const float ob1 = __fsub_rn(1.0f, a.b1), ob2 = __fsub_rn(1.0f, a.b2);
@@ -309,21 +324,18 @@ __global__ void __launch_bounds__(256) adam_kernel(const AdamArgs a) {
 
 void launch_env_init(const EnvParams& ep, float* x, int* ep_step, int* ep_len, int* ep_count, __nv_bfloat16* X0,
                      cudaStream_t s) {
-  env_init_kernel<<<(ep.N + 127) / 128, 128, 0, s>>>(ep, x, ep_step, ep_len, ep_count, X0);
-  GMI_CUDA_CHECK(cudaGetLastError());
+  launch_pdl(env_init_kernel, dim3((ep.N + 127) / 128), dim3(128), 0, s, ep, x, ep_step, ep_len, ep_count, X0);
 }
 
 void launch_act_env(const ActEnvArgs& a, cudaStream_t s) {
   if (a.ep.A > kMaxAct) invalid("act_dim > 31 unsupported by the act/env kernel");
   if (a.ep.S > 32 * kMaxObsPerLane) invalid("obs_dim > 256 unsupported by the act/env kernel");
   const int blocks = (a.ep.N * 32 + 255) / 256;
-  act_env_kernel<<<blocks, 256, 0, s>>>(a);
-  GMI_CUDA_CHECK(cudaGetLastError());
+  launch_pdl(act_env_kernel, dim3(blocks), dim3(256), 0, s, a);
 }
 
 void launch_value_head(const float* vraw, const float* b, float* out, int rows, cudaStream_t s) {
-  value_head_kernel<<<(rows + 255) / 256, 256, 0, s>>>(vraw, b, out, rows);
-  GMI_CUDA_CHECK(cudaGetLastError());
+  launch_pdl(value_head_kernel, dim3((rows + 255) / 256), dim3(256), 0, s, vraw, b, out, rows);
 }
 
 int gae_blocks(int N) { return (N + 31) / 32; }
@@ -331,13 +343,12 @@ int gae_blocks(int N) { return (N + 31) / 32; }
 void launch_gae(const float* rew, const uint8_t* done, const float* V, float* adv, float* ret, double* partials,
                 int N, int T, float gamma, float lam, cudaStream_t s) {
   if (T > 32) invalid("horizon > 32 unsupported by the GAE scan");
-  gae_kernel<<<gae_blocks(N), 1024, 0, s>>>(rew, done, V, adv, ret, partials, N, T, gamma, gamma * lam);
-  GMI_CUDA_CHECK(cudaGetLastError());
+  launch_pdl(gae_kernel, dim3(gae_blocks(N)), dim3(1024), 0, s, rew, done, V, adv, ret, partials, N, T, gamma,
+             gamma * lam);
 }
 
 void launch_adv_stats(const double* partials, int nparts, long long count, float* stats, cudaStream_t s) {
-  adv_stats_kernel<<<1, 256, 0, s>>>(partials, nparts, count, stats);
-  GMI_CUDA_CHECK(cudaGetLastError());
+  launch_pdl(adv_stats_kernel, dim3(1), dim3(256), 0, s, partials, nparts, count, stats);
 }
 
 void launch_shuffle(const __nv_bfloat16* X_roll, const float* act, const float* logp, const float* adv,
@@ -345,14 +356,14 @@ void launch_shuffle(const __nv_bfloat16* X_roll, const float* act, const float* 
                     float* adv_sh, float* ret_sh, int N, int T, int S_p, int A, uint64_t seed, int gmi_gid, int epoch,
                     const Control* ctl, cudaStream_t s) {
   const long long work = (long long)T * N * (S_p / 8);
-  shuffle_kernel<<<grid_for(work, 256, 1 << 30), 256, 0, s>>>(X_roll, act, logp, adv, ret, adv_stats, X_sh, act_sh,
-                                                              oldlp_sh, adv_sh, ret_sh, N, T, S_p, A, seed, gmi_gid,
-                                                              epoch, ctl);
-  GMI_CUDA_CHECK(cudaGetLastError());
+  launch_pdl(shuffle_kernel, dim3(grid_for(work, 256, 1 << 30)), dim3(256), 0, s, X_roll, act, logp, adv, ret,
+             adv_stats, X_sh, act_sh, oldlp_sh, adv_sh, ret_sh, N, T, S_p, A, seed, gmi_gid, epoch, ctl);
 }
 
 namespace {
 __global__ void control_advance_kernel(Control* c, int dsteps) {
+  pdl_trigger();
+  pdl_wait();
   c->iteration += 1;
   c->adam_step0 += dsteps;
 }
@@ -360,13 +371,11 @@ __global__ void control_advance_kernel(Control* c, int dsteps) {
 
 // Device-side end-of-iteration bookkeeping, so a captured iteration graph can be replayed.
 void launch_control_advance(Control* c, int dsteps, cudaStream_t s) {
-  control_advance_kernel<<<1, 1, 0, s>>>(c, dsteps);
-  GMI_CUDA_CHECK(cudaGetLastError());
+  launch_pdl(control_advance_kernel, dim3(1), dim3(1), 0, s, c, dsteps);
 }
 
 void launch_adam(const AdamArgs& a, cudaStream_t s) {
-  adam_kernel<<<grid_for(a.n, 256, 148 * 8), 256, 0, s>>>(a);
-  GMI_CUDA_CHECK(cudaGetLastError());
+  launch_pdl(adam_kernel, dim3(grid_for(a.n, 256, 148 * 8)), dim3(256), 0, s, a);
 }
 
 }  // namespace gmi::ppo

@@ -8,6 +8,7 @@
 #include <algorithm>
 
 #include "../host/errors.hpp"
+#include "launch.cuh"
 #include "ppo.cuh"
 #include "ppo_common.cuh"
 
@@ -24,6 +25,8 @@ namespace {
 template <int MAXA>
 __global__ void __launch_bounds__(256) head_loss_kernel(const HeadLossArgs a) {
   __shared__ float red_s[8][2 * kMaxAct + 5];
+  pdl_trigger();
+  pdl_wait();
   const int A = a.A;
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -104,6 +107,8 @@ struct ColsumArgs {
 };
 __global__ void __launch_bounds__(256) colsum_kernel(const ColsumArgs a, int rows) {
   __shared__ float part_s[2048];  // [row lanes][w]; row lanes * w <= 2048
+  pdl_trigger();
+  pdl_wait();
   const int p = blockIdx.y;
   const int w = a.width[p];
   const int tpr = w / 8;
@@ -147,6 +152,8 @@ struct SegmentTable {
 };
 __global__ void __launch_bounds__(256) segments_kernel(const __grid_constant__ SegmentTable t) {
   __shared__ float4 acc_s[8][32];
+  pdl_trigger();
+  pdl_wait();
   int si = 0;
   while (si + 1 < t.nseg && (int)blockIdx.x >= t.first_block[si + 1]) ++si;
   const Segment& sg = t.s[si];
@@ -217,14 +224,13 @@ void launch_head_loss(const HeadLossArgs& a, cudaStream_t s) {
   if (a.A > kMaxAct) invalid("act_dim > 31 unsupported by the loss kernel");
   const int blocks = head_loss_blocks(a.B);
   if (a.A <= 8)
-    head_loss_kernel<8><<<blocks, 256, 0, s>>>(a);
+    launch_pdl(head_loss_kernel<8>, dim3(blocks), dim3(256), 0, s, a);
   else if (a.A <= 16)
-    head_loss_kernel<16><<<blocks, 256, 0, s>>>(a);
+    launch_pdl(head_loss_kernel<16>, dim3(blocks), dim3(256), 0, s, a);
   else if (a.A <= 24)
-    head_loss_kernel<24><<<blocks, 256, 0, s>>>(a);
+    launch_pdl(head_loss_kernel<24>, dim3(blocks), dim3(256), 0, s, a);
   else
-    head_loss_kernel<31><<<blocks, 256, 0, s>>>(a);
-  GMI_CUDA_CHECK(cudaGetLastError());
+    launch_pdl(head_loss_kernel<31>, dim3(blocks), dim3(256), 0, s, a);
 }
 
 int colsum_blocks(int rows) { return (rows + kColsumRows - 1) / kColsumRows; }
@@ -239,8 +245,7 @@ void launch_colsum(const __nv_bfloat16* const* D, const int* widths, float* cons
     a.out[i] = partial[i];
     a.width[i] = widths[i];
   }
-  colsum_kernel<<<dim3(colsum_blocks(rows), np), 256, 0, s>>>(a, rows);
-  GMI_CUDA_CHECK(cudaGetLastError());
+  launch_pdl(colsum_kernel, dim3(colsum_blocks(rows), np), dim3(256), 0, s, a, rows);
 }
 
 void launch_segments(const Segment* segs, int n, cudaStream_t s) {
@@ -253,8 +258,7 @@ void launch_segments(const Segment* segs, int n, cudaStream_t s) {
       t.s[i] = segs[base + i];
       t.first_block[i + 1] = t.first_block[i] + (std::max(1, t.s[i].len) + kSegElems - 1) / kSegElems;
     }
-    segments_kernel<<<t.first_block[m], 256, 0, s>>>(t);
-    GMI_CUDA_CHECK(cudaGetLastError());
+    launch_pdl(segments_kernel, dim3(t.first_block[m]), dim3(256), 0, s, t);
   }
 }
 

@@ -17,6 +17,7 @@
 
 #include "../host/errors.hpp"
 #include "../host/planner.hpp"
+#include "launch.cuh"
 
 namespace gmi {
 
@@ -56,6 +57,8 @@ __device__ __forceinline__ T ring_fold(const ReduceArgs& a, const unsigned char*
 
 template <typename T>
 __global__ void __launch_bounds__(256) gmi_reduce_kernel(const __grid_constant__ ReduceArgs a) {
+  pdl_trigger();
+  pdl_wait();
   const u64 stride = u64(gridDim.x) * blockDim.x;
   for (u64 e = u64(blockIdx.x) * blockDim.x + threadIdx.x; e < a.len; e += stride) {
     T acc;
@@ -122,12 +125,11 @@ void reduce_device(plan::Algo algo, const plan::Placement& p, void* const* bufs,
   const u64 want = (len + threads - 1) / threads;
   const int blocks = int(std::min<u64>(want, 148ull * 16));
   if (dtype == GMI_F64)
-    gmi_reduce_kernel<double><<<blocks, threads, 0, stream>>>(a);
+    launch_pdl(gmi_reduce_kernel<double>, dim3(blocks), dim3(threads), 0, stream, a);
   else if (dtype == GMI_F32)
-    gmi_reduce_kernel<float><<<blocks, threads, 0, stream>>>(a);
+    launch_pdl(gmi_reduce_kernel<float>, dim3(blocks), dim3(threads), 0, stream, a);
   else
     invalid("dtype must be GMI_F32 or GMI_F64");
-  GMI_CUDA_CHECK(cudaGetLastError());
 }
 
 }  // namespace gmi

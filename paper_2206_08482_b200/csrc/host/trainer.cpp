@@ -133,7 +133,8 @@ struct Trainer::Gmi {
   GemmParams dw[GMI_MAX_HIDDEN], dx[GMI_MAX_HIDDEN], dhead;
   GemmParams head_roll, head_val, head_train, head_dx;  // head forward / input-grad GEMMs
   int bn_roll[GMI_MAX_HIDDEN] = {}, bn_val[GMI_MAX_HIDDEN] = {}, bn_fwd[GMI_MAX_HIDDEN] = {};
-  int bn_dx[GMI_MAX_HIDDEN] = {}, bn_dw[GMI_MAX_HIDDEN] = {}, bn_head = 0;
+  int bn_dx[GMI_MAX_HIDDEN] = {}, bn_dw[GMI_MAX_HIDDEN] = {}, bn_head = 0, bn_hdx = 0;
+  int ws_val[GMI_MAX_HIDDEN] = {}, ws_fwd[GMI_MAX_HIDDEN] = {}, ws_dx[GMI_MAX_HIDDEN] = {}, ws_hdx = 0;
   double flop_roll[GMI_MAX_HIDDEN] = {}, flop_fwd[GMI_MAX_HIDDEN] = {}, flop_dw[GMI_MAX_HIDDEN] = {},
          flop_dx[GMI_MAX_HIDDEN] = {}, flop_head = 0;
   std::vector<ppo::Segment> segs;
@@ -334,7 +335,10 @@ void Trainer::build_plans() {
       g.fwd_roll[l].prob[0] = fwd_problem(0, a_roll, g.N, g.bn_roll[l]);
       g.fwd_roll[l].num_problems = 1;
       g.fwd_roll[l].splits = 1;
-      g.bn_val[l] = gemm_choose_bn(g.Mrows, out_p, 1, 1, g.ctas);
+      // weight-stationary where every CTA gets a tile (weights loaded once per CTA)
+      const int ws_val = gemm_ws_bn(g.Mrows, out_p, in_p, 1, g.ctas);
+      g.ws_val[l] = ws_val > 0;
+      g.bn_val[l] = ws_val > 0 ? ws_val : gemm_choose_bn(g.Mrows, out_p, 1, 1, g.ctas);
       const CUtensorMap a_val = l == 0 ? tma_kmajor(g.X_roll, S_p, rollrows, S_p, kGemmBlockM)
                                        : tma_kmajor(g.H[1][l - 1], in_p, g.Mrows, in_p, kGemmBlockM);
       g.fwd_val[l] = GemmParams{};
@@ -342,7 +346,9 @@ void Trainer::build_plans() {
       g.fwd_val[l].num_problems = 1;
       g.fwd_val[l].splits = 1;
       // training forward: both nets grouped over the minibatch rows of the epoch copy
-      g.bn_fwd[l] = gemm_choose_bn(g.Bm, out_p, 2, 1, g.ctas);
+      const int ws_fwd = gemm_ws_bn(g.Bm, out_p, in_p, 2, g.ctas);
+      g.ws_fwd[l] = ws_fwd > 0;
+      g.bn_fwd[l] = ws_fwd > 0 ? ws_fwd : gemm_choose_bn(g.Bm, out_p, 2, 1, g.ctas);
       g.fwd_train[l] = GemmParams{};
       for (int n = 0; n < 2; ++n) {
         const CUtensorMap a = l == 0 ? tma_kmajor(g.X_sh, S_p, g.B, S_p, kGemmBlockM)
@@ -380,7 +386,9 @@ void Trainer::build_plans() {
 
       // input gradient dPre_{l-1} = (dPre_l W_l) * elu'(H_{l-1}); W_l read MN-major
       if (l > 0) {
-        g.bn_dx[l] = gemm_choose_bn(g.Bm, in_p, 2, 1, g.ctas);
+        const int ws_dx = gemm_ws_bn(g.Bm, in_p, out_p, 2, g.ctas);
+        g.ws_dx[l] = ws_dx > 0;
+        g.bn_dx[l] = ws_dx > 0 ? ws_dx : gemm_choose_bn(g.Bm, in_p, 2, 1, g.ctas);
         g.dx[l] = GemmParams{};
         for (int n = 0; n < 2; ++n) {
           GemmProblem p{};
@@ -428,6 +436,9 @@ void Trainer::build_plans() {
     g.head_train.num_problems = 2;
     g.head_train.splits = 1;
     // Head input gradient: dPre_{L-1} = (G W_head) * elu'(H_L), K = 64 (zero-padded G).
+    const int ws_hdx = gemm_ws_bn(g.Bm, hp, ppo::kHeadG, 2, g.ctas);
+    g.ws_hdx = ws_hdx > 0;
+    g.bn_hdx = ws_hdx > 0 ? ws_hdx : gemm_choose_bn(g.Bm, hp, 2, 1, g.ctas);
     g.head_dx = GemmParams{};
     {
       const __nv_bfloat16* G[2] = {g.Gpi, g.Gv};
@@ -515,8 +526,8 @@ void Trainer::timed(cudaStream_t s, int phase, double flop, double bytes, F&& f)
   m.bytes = bytes;
 }
 
-void Trainer::gemm(Gmi& g, int phase, const GemmParams& P, int bn, int amn, int bmn, int epi, double flop) {
-  timed(g.s, phase, flop, 0.0, [&] { gemm_launch(P, bn, amn, bmn, epi, g.s, g.ctas); });
+void Trainer::gemm(Gmi& g, int phase, const GemmParams& P, int bn, int amn, int bmn, int epi, double flop, int ws) {
+  timed(g.s, phase, flop, 0.0, [&] { gemm_launch(P, bn, amn, bmn, epi, g.s, g.ctas, ws); });
   ++launches_;
 }
 
@@ -608,7 +619,7 @@ void Trainer::values(Gmi& g) {
       GemmParams P = g.fwd_val[l];
       P.prob[0].M = m;
       if (l == 0) P.prob[0].a_row0 = int(c0);
-      gemm(g, GMI_PH_VAL_GEMM, P, g.bn_val[l], 0, 0, EPI_BIAS_ELU, g.flop_roll[l] * double(m) / g.N);
+      gemm(g, GMI_PH_VAL_GEMM, P, g.bn_val[l], 0, 0, EPI_BIAS_ELU, g.flop_roll[l] * double(m) / g.N, g.ws_val[l]);
     }
     GemmParams Ph = g.head_val;
     Ph.prob[0].M = m;
@@ -626,11 +637,11 @@ void Trainer::values(Gmi& g) {
 }
 
 void Trainer::train_minibatch(Gmi& g, int k) {
-  const int L = geo_.L, A = geo_.A, hp = geo_.wp[L];
+  const int L = geo_.L, A = geo_.A;
   for (int l = 0; l < L; ++l) {
     GemmParams P = g.fwd_train[l];
     if (l == 0) P.prob[0].a_row0 = P.prob[1].a_row0 = k * g.Bm;
-    gemm(g, GMI_PH_FWD_GEMM, P, g.bn_fwd[l], 0, 0, EPI_BIAS_ELU, g.flop_fwd[l]);
+    gemm(g, GMI_PH_FWD_GEMM, P, g.bn_fwd[l], 0, 0, EPI_BIAS_ELU, g.flop_fwd[l], g.ws_fwd[l]);
   }
   const double hflop = 2.0 * (A + 1) * geo_.width[L] * g.Bm;
   gemm(g, GMI_PH_HEAD_FWD, g.head_train, 64, 0, 0, EPI_F32, hflop);
@@ -655,7 +666,7 @@ void Trainer::train_minibatch(Gmi& g, int k) {
   h.ent_coef = cfg_.ent_coef;
   timed(g.s, GMI_PH_HEAD_LOSS, 0.0, double(g.Bm) * (10.0 * A + 18.0), [&] { ppo::launch_head_loss(h, g.s); });
   ++launches_;
-  gemm(g, GMI_PH_HEAD_DX, g.head_dx, gemm_choose_bn(g.Bm, hp, 2, 1, g.ctas), 0, 1, EPI_DACT, hflop);
+  gemm(g, GMI_PH_HEAD_DX, g.head_dx, g.bn_hdx, 0, 1, EPI_DACT, hflop, g.ws_hdx);
   gemm(g, GMI_PH_HEAD_DW, g.dhead, g.bn_head, 1, 1, EPI_F32, g.flop_head);
   for (int l = L - 1; l >= 0; --l) {
     GemmParams P = g.dw[l];
@@ -668,7 +679,7 @@ void Trainer::train_minibatch(Gmi& g, int k) {
     timed(g.s, GMI_PH_COLSUM, 0.0, 2.0 * 2.0 * g.Bm * geo_.wp[l + 1],
           [&] { ppo::launch_colsum(Ds, widths, outs, 2, g.Bm, g.s); });
     ++launches_;
-    if (l > 0) gemm(g, GMI_PH_DX_GEMM, g.dx[l], g.bn_dx[l], 0, 1, EPI_DACT, g.flop_dx[l]);
+    if (l > 0) gemm(g, GMI_PH_DX_GEMM, g.dx[l], g.bn_dx[l], 0, 1, EPI_DACT, g.flop_dx[l], g.ws_dx[l]);
   }
   double seg_bytes = 0;
   for (const auto& sg : g.segs) seg_bytes += 4.0 * sg.len * (sg.nparts + 1.0);

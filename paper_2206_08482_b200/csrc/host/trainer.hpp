@@ -61,7 +61,7 @@ class Trainer {
   void values(Gmi& g);
   void train_minibatch(Gmi& g, int k);
   void reduce_and_step(int k);
-  void gemm(Gmi& g, int phase, const GemmParams& P, int bn, int amn, int bmn, int epi, double flop);
+  void gemm(Gmi& g, int phase, const GemmParams& P, int bn, int amn, int bmn, int epi, double flop, int ws = 0);
   // Runs f (which enqueues work on s); with cfg.instrument and s = GMI 0's stream or the
   // update stream, brackets it with CUDA events booked to `phase` (+ algorithmic flop/bytes).
   template <class F>

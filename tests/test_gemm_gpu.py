@@ -11,7 +11,7 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 
-def _gemm(a_mn, b_mn, epi, M, N, K, A, B, out, bias=None, aux=None, splits=1):
+def _gemm(a_mn, b_mn, epi, M, N, K, A, B, out, bias=None, aux=None, splits=1, ws=0):
     import torch
     from paper_2206_08482_b200 import _lib
 
@@ -21,7 +21,7 @@ def _gemm(a_mn, b_mn, epi, M, N, K, A, B, out, bias=None, aux=None, splits=1):
               C.c_void_p(out.data_ptr()), out.stride(0) if out.dim() == 2 else out.stride(1),
               C.c_void_p(bias.data_ptr() if bias is not None else 0),
               C.c_void_p(aux.data_ptr() if aux is not None else 0),
-              aux.stride(0) if aux is not None else 0, splits, C.c_void_p(stream))
+              aux.stride(0) if aux is not None else 0, splits, ws, C.c_void_p(stream))
     torch.cuda.synchronize()
 
 
@@ -30,9 +30,10 @@ def _elu(x):
     return torch.where(x > 0, x, torch.expm1(x))
 
 
-@pytest.mark.parametrize("M,N,K,ldk", [(128, 64, 64, 64), (300, 256, 60, 64), (1024, 128, 256, 256),
-                                       (4096, 256, 192, 192), (384, 512, 128, 128)])
-def test_forward_bias_elu(cuda, M, N, K, ldk):
+@pytest.mark.parametrize("M,N,K,ldk,ws", [(128, 64, 64, 64, 0), (300, 256, 60, 64, 0), (1024, 128, 256, 256, 0),
+                                          (4096, 256, 192, 192, 0), (384, 512, 128, 128, 0),
+                                          (40000, 256, 256, 256, 1), (20000, 224, 64, 64, 1), (300, 128, 192, 192, 1)])
+def test_forward_bias_elu(cuda, M, N, K, ldk, ws):
     import torch
     g = torch.Generator(device="cpu").manual_seed(M * 7 + N)
     A = torch.zeros(M, ldk, dtype=torch.bfloat16)
@@ -42,7 +43,7 @@ def test_forward_bias_elu(cuda, M, N, K, ldk):
     bias = (torch.rand(N, generator=g) - 0.5).float()
     A, W, bias = A.to(cuda), W.to(cuda), bias.to(cuda)
     out = torch.full((M, N), float("nan"), dtype=torch.bfloat16, device=cuda)
-    _gemm(0, 0, 0, M, N, K, A, W, out, bias=bias)
+    _gemm(0, 0, 0, M, N, K, A, W, out, bias=bias, ws=ws)
     ref = _elu(A[:, :K].float() @ W[:, :K].float().T + bias)
     err = (out.float() - ref).abs().max().item()
     assert err <= 1e-2 * max(1.0, ref.abs().max().item()), err
@@ -62,17 +63,17 @@ def test_f32_split_k(cuda, splits):
     assert torch.allclose(got, ref, rtol=1e-4, atol=1e-4), (got - ref).abs().max().item()
 
 
-def test_dgrad_mn_major_weights(cuda):
+@pytest.mark.parametrize("M,Nl,Kl,ws", [(512, 256, 192, 0), (33000, 256, 256, 1), (20000, 64, 224, 1)])
+def test_dgrad_mn_major_weights(cuda, M, Nl, Kl, ws):
     """dH = (dPre @ W) * elu'(H): B operand is the [N_l x K_l] weight read MN-major."""
     import torch
-    M, Nl, Kl = 512, 256, 192
     g = torch.Generator(device="cpu").manual_seed(11)
     dpre = (torch.rand(M, Nl, generator=g) - 0.5).bfloat16().to(cuda)
     W = ((torch.rand(Nl, Kl, generator=g) - 0.5) / 8).bfloat16().to(cuda)
     H = _elu(torch.randn(M, Kl, generator=g)).bfloat16().to(cuda)
     out = torch.zeros(M, Kl, dtype=torch.bfloat16, device=cuda)
     # D[m][n] = sum_k dpre[m][k] * W[k][n]  -> B(n,k) = W[k][n], stored [K x rows]
-    _gemm(0, 1, 1, M, Kl, Nl, dpre, W, out, aux=H)
+    _gemm(0, 1, 1, M, Kl, Nl, dpre, W, out, aux=H, ws=ws)
     Hf = H.float()
     ref = (dpre.float() @ W.float()) * torch.where(Hf > 0, torch.ones_like(Hf), Hf + 1)
     err = (out.float() - ref).abs().max().item()
