@@ -243,19 +243,39 @@ __global__ void __launch_bounds__(gemm_threads(EPI), 1) gemm_tcgen05_kernel(cons
     uint8_t* stage_base = staging + e * L::kStagingBufs * L::kStaging;
     int sbuf = 0;
     int lt = 0;
+    // Fused bias gradient (EPI_DACT, weight-stationary: this CTA always sees the same problem
+    // and columns): per-lane running column sums of the bf16 output over all of its tiles.
+    constexpr bool kColsum = EPI == EPI_DACT && WS;
+    constexpr int kMyChunks = (kChunks + W - 1) / W;
+    float csum[kMyChunks];
+#pragma unroll
+    for (int i = 0; i < kMyChunks; ++i) csum[i] = 0.f;
     for (int tile = blockIdx.x; tile < ntile_total; tile += gridDim.x, ++lt) {
       int prob, split, m0, n0, kb0, nkb;
       decode(tile, prob, split, m0, n0, kb0, nkb);
       const GemmProblem& pr = P.prob[prob];
       const int buf = lt & 1;
-      ptx::mbar_wait(&tfull_bar[buf], (lt >> 1) & 1);
-      ptx::tc_fence_after();
       const int rbase = m0 + q * 32;
       const int row = rbase + lane;
+      // EPI_DACT: the elu' operand (H rows, bf16) is fetched one chunk ahead so its HBM/L2
+      // latency overlaps the accumulator wait and the previous chunk's math.
+      uint4 hv[4] = {}, hn[4] = {};
+      auto load_aux = [&](int c, uint4(&dst)[4]) {
+        const int col0 = n0 + c * 32;
+        if (c < kChunks && col0 < pr.N && row < pr.M) {
+          const uint4* hp = reinterpret_cast<const uint4*>(pr.aux + (long long)row * pr.ld_aux + col0);
+#pragma unroll
+          for (int qd = 0; qd < 4; ++qd) dst[qd] = hp[qd];
+        }
+      };
+      if constexpr (EPI == EPI_DACT) load_aux(h, hv);
+      ptx::mbar_wait(&tfull_bar[buf], (lt >> 1) & 1);
+      ptx::tc_fence_after();
 #pragma unroll 1
       for (int c = h; c < kChunks; c += W) {
         const int col0 = n0 + c * 32;
         if (col0 >= pr.N) break;  // warp-uniform
+        if constexpr (EPI == EPI_DACT) load_aux(c + W, hn);
         uint32_t r[32];
         ptx::tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + buf * BN + c * 32, r);
         ptx::tmem_ld_wait();
@@ -287,12 +307,6 @@ __global__ void __launch_bounds__(gemm_threads(EPI), 1) gemm_tcgen05_kernel(cons
               packed[2 * j + 1] = pack_bf16(y1.x, y1.y);
             }
           } else {  // EPI_DACT
-            uint4 hv[4] = {};
-            if (row < pr.M) {
-              const uint4* hp = reinterpret_cast<const uint4*>(pr.aux + (long long)row * pr.ld_aux + col0);
-#pragma unroll
-              for (int qd = 0; qd < 4; ++qd) hv[qd] = hp[qd];
-            }
 #pragma unroll
             for (int qd = 0; qd < 4; ++qd) {
               const uint32_t hw[4] = {hv[qd].x, hv[qd].y, hv[qd].z, hv[qd].w};
@@ -303,12 +317,29 @@ __global__ void __launch_bounds__(gemm_threads(EPI), 1) gemm_tcgen05_kernel(cons
                 packed[j / 2] = pack_bf16(d.x, d.y);
               }
             }
+#pragma unroll
+            for (int qd = 0; qd < 4; ++qd) hv[qd] = hn[qd];
           }
           // 32 bf16 = 4 x 16 B per row; SWIZZLE_64B: chunk ^= (row >> 1) & 3
 #pragma unroll
           for (int j = 0; j < 4; ++j)
             *reinterpret_cast<uint4*>(st + lane * 64 + ((j ^ ((lane >> 1) & 3)) << 4)) =
                 make_uint4(packed[4 * j], packed[4 * j + 1], packed[4 * j + 2], packed[4 * j + 3]);
+          if constexpr (kColsum) {
+            if (pr.colsum) {  // lane = column: sum the staged 32 rows in row order
+              __syncwarp();
+              float s = 0.f;
+#pragma unroll
+              for (int rr = 0; rr < 32; ++rr) {
+                const uint16_t v = *reinterpret_cast<const uint16_t*>(
+                    st + rr * 64 + ((((lane >> 3) ^ ((rr >> 1) & 3))) << 4) + (lane & 7) * 2);
+                s += __uint_as_float(uint32_t(v) << 16);
+              }
+#pragma unroll
+              for (int i = 0; i < kMyChunks; ++i)
+                if (i == (c - h) / W) csum[i] += s;
+            }
+          }
         }
         ptx::fence_proxy_async_smem();
         __syncwarp();
@@ -324,6 +355,27 @@ __global__ void __launch_bounds__(gemm_threads(EPI), 1) gemm_tcgen05_kernel(cons
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(&tempty_bar[buf]);
+    }
+    if constexpr (kColsum) {
+      const GemmProblem& pr = P.prob[blockIdx.x % P.num_problems];
+      if (pr.colsum) {  // combine the 4 lane quarters in order; one row per CTA
+        float* red = reinterpret_cast<float*>(smem);  // operand stages are idle by now
+#pragma unroll
+        for (int i = 0; i < kMyChunks; ++i) {
+          const int c = h + i * W;
+          if (c < kChunks) red[q * BN + c * 32 + lane] = csum[i];
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");
+        if (q == 0) {
+          float* dst = pr.colsum + (long long)(blockIdx.x / P.num_problems) * pr.N;
+#pragma unroll
+          for (int i = 0; i < kMyChunks; ++i) {
+            const int col = (h + i * W) * 32 + lane;
+            if (col < pr.N && col < BN)
+              dst[col] = ((red[col] + red[BN + col]) + red[2 * BN + col]) + red[3 * BN + col];
+          }
+        }
+      }
     }
     if (lane == 0) ptx::bulk_wait<0>();
   }

@@ -145,6 +145,12 @@ int gemm_ws_bn(int M, int N, int K, int problems, int sms) {
   return bn;
 }
 
+int gemm_ws_grid(int M, int problems, int max_ctas) {
+  const int tiles = ((M + kGemmBlockM - 1) / kGemmBlockM) * problems;
+  const int ctas = std::max(1, std::min(tiles, max_ctas > 0 ? max_ctas : device_sm_count()));
+  return std::max(problems, ctas / problems * problems);  // one problem per CTA
+}
+
 void gemm_launch(const GemmParams& P, int bn, int a_mn, int b_mn, int epi, cudaStream_t s, int max_ctas, int ws) {
   static int sms = 0;
   if (!sms) sms = device_sm_count();
@@ -156,7 +162,10 @@ void gemm_launch(const GemmParams& P, int bn, int a_mn, int b_mn, int epi, cudaS
   if (ws) {
     if (P.splits != 1 || P.prob[0].N > bn || P.prob[0].K > kGemmMaxKbWS * kGemmBlockK)
       invalid("weight-stationary GEMM needs splits == 1, N <= block_n, K <= 256");
-    ctas = std::max(P.num_problems, ctas / P.num_problems * P.num_problems);  // one problem per CTA
+    ctas = gemm_ws_grid(P.prob[0].M, P.num_problems, max_ctas > 0 ? max_ctas : sms);
+  } else {
+    for (int i = 0; i < P.num_problems; ++i)
+      if (P.prob[i].colsum) invalid("fused column sums need the weight-stationary GEMM");
   }
   switch (bn) {
     case 64: return launch_bn<64>(P, a_mn, b_mn, epi, ctas, s, ws);

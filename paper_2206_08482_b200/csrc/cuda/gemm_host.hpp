@@ -30,6 +30,9 @@ void gemm_launch(const GemmParams& P, int bn, int a_mn, int b_mn, int epi, cudaS
 // Weight-stationary choice for a launch: returns the block N (N padded to 64) when every
 // CTA gets at least one tile and the weights fit, else 0 (use the streaming kernel).
 int gemm_ws_bn(int M, int N, int K, int problems, int sms);
+// Grid of a weight-stationary launch (a multiple of `problems`); the fused column-sum
+// output has grid / problems rows per problem.
+int gemm_ws_grid(int M, int problems, int max_ctas);
 
 // Block N for a launch: the largest of {256,128,64} (<= padded N) that still gives at
 // least 4 tiles per SM, else the smallest.

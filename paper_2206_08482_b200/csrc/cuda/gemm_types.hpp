@@ -24,6 +24,9 @@ struct alignas(64) GemmProblem {
   const float* bias;
   const __nv_bfloat16* aux;
   int64_t ld_aux;
+  // EPI_DACT + weight-stationary: per-CTA column sums of the bf16 output (the bias gradient
+  // of the layer), one fp32 row of N per CTA serving this problem (CTA order), or null.
+  float* colsum;
   int M, N, K;
   int kb_per_split;
   int a_row0;    // offset added to A's stored-row coordinate (M for K-major, K for MN-major)

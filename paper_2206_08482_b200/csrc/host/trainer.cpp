@@ -20,9 +20,11 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 #include "../cuda/rng.cuh"
+#include "../cuda/rollout.cuh"
 #include "errors.hpp"
 #include "gmi_exec.hpp"
 #include "planner.hpp"
@@ -138,6 +140,9 @@ struct Trainer::Gmi {
   double flop_roll[GMI_MAX_HIDDEN] = {}, flop_fwd[GMI_MAX_HIDDEN] = {}, flop_dw[GMI_MAX_HIDDEN] = {},
          flop_dx[GMI_MAX_HIDDEN] = {}, flop_head = 0;
   std::vector<ppo::Segment> segs;
+  bool fused_roll = false;
+  ppo::RolloutArgs roll_args{};
+  bool fused_bias[GMI_MAX_HIDDEN] = {};  // bias gradient summed in the producing DACT GEMM
 };
 
 // ------------------------------------------------------------------ construction
@@ -397,6 +402,7 @@ void Trainer::build_plans() {
           p.map_out = make_tma_out_bf16(g.D[n][cur ^ 1], in_p, g.Bm, in_p);
           p.aux = g.H[n][l - 1];
           p.ld_aux = in_p;
+          p.colsum = g.ws_dx[l] ? g.colsum[n][l - 1] : nullptr;  // bias gradient of layer l-1
           p.M = g.Bm;
           p.N = in_p;
           p.K = out_p;
@@ -405,6 +411,7 @@ void Trainer::build_plans() {
         }
         g.dx[l].num_problems = 2;
         g.dx[l].splits = 1;
+        g.fused_bias[l - 1] = g.ws_dx[l];
         g.flop_dx[l] = 2.0 * real * g.Bm;
       }
     }
@@ -449,6 +456,7 @@ void Trainer::build_plans() {
         p.map_out = make_tma_out_bf16(g.D[n][0], hp, g.Bm, hp);
         p.aux = g.H[n][L - 1];
         p.ld_aux = hp;
+        p.colsum = g.ws_hdx ? g.colsum[n][L - 1] : nullptr;  // bias gradient of layer L-1
         p.M = g.Bm;
         p.N = hp;
         p.K = ppo::kHeadG;
@@ -457,6 +465,7 @@ void Trainer::build_plans() {
       }
       g.head_dx.num_problems = 2;
       g.head_dx.splits = 1;
+      g.fused_bias[L - 1] = g.ws_hdx;
     }
     // head weight gradients on the tensor cores: dW_mu = G_pi^T H_L, dw_v = G_v^T H^v_L
     const int bnh = std::min(256, ((hp + 63) / 64) * 64);
@@ -489,7 +498,8 @@ void Trainer::build_plans() {
       for (int l = 0; l < L; ++l) {
         const Tensor& t = geo_.net[n][l];
         g.segs.push_back({g.grad + t.w, g.slab[n][l], (long long)t.out_p * t.in_p, t.out_p * t.in_p, g.dw[l].splits});
-        g.segs.push_back({g.grad + t.b, g.colsum[n][l], t.out_p, t.out_p, cb});
+        const int parts = g.fused_bias[l] ? gemm_ws_grid(g.Bm, 2, g.ctas) / 2 : cb;
+        g.segs.push_back({g.grad + t.b, g.colsum[n][l], t.out_p, t.out_p, parts});
       }
     g.segs.push_back({g.grad + geo_.net[0][L].w, g.head_slab[0], (long long)A * hp, A * hp, hsplits});
     g.segs.push_back({g.grad + geo_.net[1][L].w, g.head_slab[1], hp, hp, hsplits});
@@ -497,6 +507,45 @@ void Trainer::build_plans() {
     g.segs.push_back({g.grad + geo_.net[1][L].b, g.head_part + A, hs, 1, hb});
     g.segs.push_back({g.grad + geo_.log_std, g.head_part + A + 1, hs, A, hb});
     if (g.local == 0) g.segs.push_back({stats_dev_, g.head_part + 2 * A + 1, hs, 4, hb});
+
+    // fused rollout (one persistent kernel per rollout) when the policy MLP fits on chip
+    const char* unfused = std::getenv("GMI_ROLLOUT_UNFUSED");
+    g.fused_roll = ppo::rollout_fusable(L, geo_.wp.data(), S_p, A) && !(unfused && unfused[0] == '1');
+    if (g.fused_roll) {
+      ppo::RolloutArgs& r = g.roll_args;
+      r.map_obs = tma_kmajor(g.X_roll, S_p, g.N, S_p, kGemmBlockM);
+      for (int l = 0; l < L; ++l) {
+        const Tensor& t = geo_.net[0][l];
+        r.map_w[l] = tma_kmajor(shadow_ + t.w, t.in_p, t.out_p, t.in_p, t.out_p);
+        r.bias[l] = params_ + t.b;
+        r.in_p[l] = t.in_p;
+        r.out_n[l] = t.out_p;
+      }
+      const int head_n = A <= 16 ? 16 : 32;
+      r.map_w[L] = tma_kmajor(shadow_ + geo_.net[0][L].w, hp, A, hp, head_n);
+      r.bias[L] = params_ + geo_.net[0][L].b;
+      r.in_p[L] = hp;
+      r.out_n[L] = head_n;
+      r.log_std = params_ + geo_.log_std;
+      r.L = L;
+      r.A = A;
+      r.S = geo_.S;
+      r.S_p = S_p;
+      r.N = g.N;
+      r.T = T_;
+      r.env0 = g.env0;
+      r.seed = cfg_.seed;
+      r.x = g.x;
+      r.ep_step = g.ep_step;
+      r.ep_len = g.ep_len;
+      r.ep_count = g.ep_count;
+      r.X_roll = g.X_roll;
+      r.act = g.act;
+      r.logp = g.logp;
+      r.rew = g.rew;
+      r.done = g.done;
+      r.ctl = ctl_dev_;
+    }
   }
 }
 
@@ -581,6 +630,13 @@ void Trainer::rollout(Gmi& g) {
     });
   const Tensor& head = geo_.net[0][L];
   const double env_bytes = double(g.N) * (8.0 * A + 8.0 * S + 2.0 * S_p + 29.0);
+  if (g.fused_roll) {  // whole rollout in one persistent kernel (cuda/rollout.cu)
+    double flop = 2.0 * geo_.A * geo_.width[L] * g.N;
+    for (int l = 0; l < L; ++l) flop += g.flop_roll[l];
+    timed(g.s, GMI_PH_ROLL_GEMM, flop * T_, 0.0, [&] { ppo::launch_rollout(g.roll_args, g.s); });
+    ++launches_;
+    return;
+  }
   for (int t = 0; t < T_; ++t) {
     for (int l = 0; l < L; ++l) {
       GemmParams P = g.fwd_roll[l];
@@ -672,13 +728,15 @@ void Trainer::train_minibatch(Gmi& g, int k) {
     GemmParams P = g.dw[l];
     if (l == 0) P.prob[0].b_row0 = P.prob[1].b_row0 = k * g.Bm;
     gemm(g, GMI_PH_DW_GEMM, P, g.bn_dw[l], 1, 1, EPI_F32, g.flop_dw[l]);
-    const int cur = (L - 1 - l) & 1;
-    const __nv_bfloat16* Ds[2] = {g.D[0][cur], g.D[1][cur]};
-    const int widths[2] = {geo_.wp[l + 1], geo_.wp[l + 1]};
-    float* outs[2] = {g.colsum[0][l], g.colsum[1][l]};
-    timed(g.s, GMI_PH_COLSUM, 0.0, 2.0 * 2.0 * g.Bm * geo_.wp[l + 1],
-          [&] { ppo::launch_colsum(Ds, widths, outs, 2, g.Bm, g.s); });
-    ++launches_;
+    if (!g.fused_bias[l]) {  // else summed by the DACT GEMM that produced dPre_l
+      const int cur = (L - 1 - l) & 1;
+      const __nv_bfloat16* Ds[2] = {g.D[0][cur], g.D[1][cur]};
+      const int widths[2] = {geo_.wp[l + 1], geo_.wp[l + 1]};
+      float* outs[2] = {g.colsum[0][l], g.colsum[1][l]};
+      timed(g.s, GMI_PH_COLSUM, 0.0, 2.0 * 2.0 * g.Bm * geo_.wp[l + 1],
+            [&] { ppo::launch_colsum(Ds, widths, outs, 2, g.Bm, g.s); });
+      ++launches_;
+    }
     if (l > 0) gemm(g, GMI_PH_DX_GEMM, g.dx[l], g.bn_dx[l], 0, 1, EPI_DACT, g.flop_dx[l], g.ws_dx[l]);
   }
   double seg_bytes = 0;

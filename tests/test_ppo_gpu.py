@@ -120,6 +120,26 @@ def test_rollout_is_layout_invariant_on_device(cuda):
     assert np.array_equal(r1, r2)
 
 
+@pytest.mark.parametrize("dims", [(12, 3, [64, 64]), (60, 8, [256, 256, 256]), (40, 20, [96, 160])])
+def test_fused_rollout_matches_per_layer_path(cuda, monkeypatch, dims):
+    """cuda/rollout.cu (one persistent kernel) vs the per-layer GEMM + act/env path: the MLP
+    arithmetic is identical, so integer state, actions and observations agree bit-for-bit;
+    rewards / log-probs differ only in the order of their small reductions."""
+    from paper_2206_08482_b200.ppo import PpoConfig, Trainer
+    S, A, hidden = dims
+    cfg = dict(obs_dim=S, act_dim=A, hidden=hidden, num_envs=200)
+    fused = Trainer(PpoConfig(**cfg))
+    monkeypatch.setenv("GMI_ROLLOUT_UNFUSED", "1")
+    plain = Trainer(PpoConfig(**cfg))
+    for _ in range(2):  # second rollout starts from carried-over state (done resets inside)
+        fused.rollout()
+        plain.rollout()
+        for f in ("done", "ep_count", "ep_step", "act", "obs", "x"):
+            assert np.array_equal(fused.get(f), plain.get(f)), f
+        for f in ("rew", "logp"):
+            np.testing.assert_allclose(fused.get(f), plain.get(f), rtol=1e-5, atol=1e-5)
+
+
 def test_bench_workload_runs(cuda):
     """BASELINE config 2: AT, 4096 envs, 3x256, 1 GMI."""
     from paper_2206_08482_b200.ppo import PpoConfig, Trainer
