@@ -116,7 +116,7 @@ __global__ void __launch_bounds__(256) act_env_kernel(const ActEnvArgs a) {
     if (i < S) {
       const float xi = xe[i];
       const float nb = xe[i + 1 < S ? i + 1 : 0];
-      const float inner = __fadd_rn(__fsub_rn(drive, __fmul_rn(kDamp, xi)), __fmul_rn(kCouple, sinf(nb)));
+      const float inner = __fadd_rn(__fsub_rn(drive, __fmul_rn(kDamp, xi)), __fmul_rn(kCouple, env_sin(nb)));
       xn[j] = __fadd_rn(xi, __fmul_rn(kDt, inner));
       xsq_part = __fadd_rn(xsq_part, __fmul_rn(xn[j], xn[j]));
     } else {

@@ -45,9 +45,18 @@ constexpr uint32_t kChunk = kRows * 128;        // one 64-column K-chunk of a 12
 constexpr uint32_t kActBytes = 4 * kChunk;       // 128 x 256 bf16
 constexpr uint32_t kWStage = 256 * 128;          // <= 256 weight rows x 64 K bf16
 constexpr int kMuLd = 33;                        // fp32 row pitch of the mu / action staging
-constexpr uint32_t kSmemBytes = 2 * kActBytes + kStages * kWStage + 128 + 1024;
+constexpr uint32_t kSmemBytes = 2 * kActBytes + kStages * kWStage + 512 + 1024;  // + barriers, std table
 
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory"); }
+
+// Development trace: globaltimer stamps of one epilogue thread of CTA 0 (a.trace[t * 16 + k]).
+__device__ __forceinline__ void trace_at(const RolloutArgs& a, int idx) {
+  if (a.trace != nullptr && blockIdx.x == 0 && threadIdx.x == 64) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    a.trace[idx] = t;
+  }
+}
 
 __device__ __forceinline__ uint32_t sw128(int row, int col_bf16) {  // byte offset inside a K-chunk
   const int u = (col_bf16 & 63) >> 3;
@@ -67,8 +76,11 @@ __global__ void __launch_bounds__(kThreads, 1) rollout_kernel(const __grid_const
   uint64_t* wempty = bars + kStages;
   uint64_t* obs_bar = bars + 2 * kStages;
   uint64_t* acc_full = obs_bar + 1;
-  uint64_t* act_ready = acc_full + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(act_ready + 1);
+  uint64_t* act_lo = acc_full + 1;  // next operand tile, K-chunks 0-1 (columns 0..127) written
+  uint64_t* act_hi = act_lo + 1;    // K-chunks 2-3 written
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(act_hi + 1);
+  float* ls_s = reinterpret_cast<float*>(bars + 16);  // log_std[32], exp(log_std)[32]
+  float* sig_s = ls_s + 32;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int L = a.L, T = a.T;
@@ -81,12 +93,14 @@ __global__ void __launch_bounds__(kThreads, 1) rollout_kernel(const __grid_const
     }
     ptx::mbar_init(obs_bar, 1);
     ptx::mbar_init(acc_full, 1);
-    ptx::mbar_init(act_ready, kEpiWarps);
+    ptx::mbar_init(act_lo, kEpiWarps);
+    ptx::mbar_init(act_hi, kEpiWarps);
     ptx::fence_mbar_init();
     ptx::tma_prefetch_desc(&a.map_obs);
     for (int l = 0; l <= L; ++l) ptx::tma_prefetch_desc(&a.map_w[l]);
   }
-  if (warp == 1) ptx::tmem_alloc(tmem_slot, 256);
+  // two 256-column accumulators: layer l+1's MMAs run while layer l's epilogue drains
+  if (warp == 1) ptx::tmem_alloc(tmem_slot, 512);
   pdl_trigger();
   ptx::tc_fence_before();
   __syncthreads();
@@ -117,31 +131,31 @@ __global__ void __launch_bounds__(kThreads, 1) rollout_kernel(const __grid_const
     // ------------------------------------------------ MMA issuer
     if (lane == 0) {
       ptx::mbar_wait_sleep(obs_bar, 0);
-      int it = 0, ph = 0;
+      int it = 0, ph_lo = 0, ph_hi = 0, acc_ph = 0;
       for (int t = 0; t < T; ++t)
-        for (int l = 0; l <= L; ++l) {
-          if (t > 0 || l > 0) {
-            ptx::mbar_wait_sleep(act_ready, ph & 1);
-            ++ph;
-          }
-          ptx::tc_fence_after();
+        for (int l = 0; l <= L; ++l, ++acc_ph) {
+          const bool first = t == 0 && l == 0;
+          const uint32_t acc = tmem + (acc_ph & 1) * 256;
           const uint32_t idesc = ptx::umma_idesc_bf16(kRows, uint32_t(a.out_n[l]), 0, 0);
           const uint32_t in = ptx::smem_u32((l & 1) ? act_buf1 : act_buf0);
           const int K = a.in_p[l];
           const int nk = (K + 63) / 64;
           for (int kc = 0; kc < nk; ++kc, ++it) {
+            if (!first && kc == 0) ptx::mbar_wait(act_lo, (ph_lo++) & 1);
+            if (!first && kc == 2) ptx::mbar_wait(act_hi, (ph_hi++) & 1);
             const int s = it % kStages;
-            ptx::mbar_wait_sleep(&wfull[s], (it / kStages) & 1);
+            ptx::mbar_wait(&wfull[s], (it / kStages) & 1);
             ptx::tc_fence_after();
             const uint32_t wb = ptx::smem_u32(wring + s * kWStage);
             const int ks = min(4, (K - kc * 64 + 15) / 16);
             for (int k = 0; k < ks; ++k) {
               const uint64_t ad = ptx::umma_desc_sw128(in + kc * kChunk + k * 32, 16, 1024);
               const uint64_t bd = ptx::umma_desc_sw128(wb + k * 32, 16, 1024);
-              ptx::mma_bf16(tmem, ad, bd, idesc, (kc > 0 || k > 0) ? 1u : 0u);
+              ptx::mma_bf16(acc, ad, bd, idesc, (kc > 0 || k > 0) ? 1u : 0u);
             }
             ptx::mma_commit(&wempty[s]);
           }
+          if (!first && nk <= 2) ptx::mbar_wait(act_hi, (ph_hi++) & 1);  // keep the phases paired
           ptx::mma_commit(acc_full);
         }
     }
@@ -171,19 +185,31 @@ __global__ void __launch_bounds__(kThreads, 1) rollout_kernel(const __grid_const
       cnt = a.ep_count[env];
     }
     const uint32_t it0 = uint32_t(a.ctl->iteration) * uint32_t(T);
+    if (tid < A) {  // first read after the first epi_bar (head phase of step 0)
+      const float ls = a.log_std[tid];
+      ls_s[tid] = ls;
+      sig_s[tid] = expf(ls);
+    }
     int accph = 0;
     for (int t = 0; t < T; ++t) {
       // ---- hidden layers: bias + ELU -> bf16 operand tile of the next layer
       for (int l = 0; l < L; ++l) {
+        const uint32_t acc = tmem + (accph & 1) * 256;
         ptx::mbar_wait_sleep(acc_full, accph & 1);
         ++accph;
         ptx::tc_fence_after();
+        trace_at(a, t * 16 + 2 * l);
         uint8_t* out = (l & 1) ? act_buf0 : act_buf1;
         const float* bias = a.bias[l];
         const int nchunks = a.out_n[l] / 32;
-        for (int c = h; c < nchunks; c += 4) {
+        // pass 0: columns 0..127 (chunks h), then release K-chunks 0-1 to the next layer's MMA;
+        // pass 1: columns 128..255 (chunks h + 4), then release K-chunks 2-3.
+#pragma unroll 1
+        for (int pass = 0; pass < 2; ++pass) {
+          const int c = h + 4 * pass;
+          if (c < nchunks) {
           uint32_t r[32];
-          ptx::tmem_ld_32x32b_x32(tmem + (static_cast<uint32_t>(q * 32) << 16) + c * 32, r);
+          ptx::tmem_ld_32x32b_x32(acc + (static_cast<uint32_t>(q * 32) << 16) + c * 32, r);
           ptx::tmem_ld_wait();
           const float4* b4 = reinterpret_cast<const float4*>(bias + c * 32);
           uint32_t packed[16];
@@ -203,56 +229,60 @@ __global__ void __launch_bounds__(kThreads, 1) rollout_kernel(const __grid_const
           for (int j = 0; j < 4; ++j)
             *reinterpret_cast<uint4*>(chunk + (((u0 + j) ^ (row & 7)) << 4)) =
                 make_uint4(packed[4 * j], packed[4 * j + 1], packed[4 * j + 2], packed[4 * j + 3]);
+          }
+          ptx::fence_proxy_async_smem();
+          ptx::tc_fence_before();
+          __syncwarp();
+          if (pass == 1) trace_at(a, t * 16 + 2 * l + 1);
+          if (lane == 0) ptx::mbar_arrive(pass == 0 ? act_lo : act_hi);
         }
-        ptx::fence_proxy_async_smem();
-        ptx::tc_fence_before();
-        __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(act_ready);
       }
 
       // ---- policy head: mu = acc + b_mu into smem (aliases the head's input tile)
+      const uint32_t hacc = tmem + (accph & 1) * 256;
       ptx::mbar_wait_sleep(acc_full, accph & 1);
       ++accph;
       ptx::tc_fence_after();
+      trace_at(a, t * 16 + 10);
       float* mu_s = reinterpret_cast<float*>((L & 1) ? act_buf1 : act_buf0);
       float* u_s = mu_s + kRows * kMuLd;
       if (h == 0) {
         uint32_t r[32];
-        ptx::tmem_ld_32x32b_x32(tmem + (static_cast<uint32_t>(q * 32) << 16), r);
+        ptx::tmem_ld_32x32b_x32(hacc + (static_cast<uint32_t>(q * 32) << 16), r);
         ptx::tmem_ld_wait();
         for (int i = 0; i < A; ++i) mu_s[row * kMuLd + i] = __uint_as_float(r[i]) + a.bias[L][i];
       }
       ptx::tc_fence_before();
       epi_bar();
 
-      // ---- actions: thread `sub` of env `el` samples Philox blocks sub, sub + 4 (4 actions each)
+      // ---- actions: work item w = (Philox block w / 2, Box-Muller pair w % 2) -> actions
+      // 4 (w / 2) + 2 (w % 2) + {0, 1}; thread `sub` of env `el` takes items sub, sub + 4, ...
+      // The dynamics only need tanh(clip(a)), so it is computed once per action here.
       const uint32_t step = it0 + uint32_t(t);
       float lp_part = 0.f, usq_part = 0.f;
       if (valid) {
-        for (int blk = sub; blk * 4 < A; blk += 4) {
+        for (int w = sub; w < 2 * ((A + 3) / 4); w += 4) {
+          const int blk = w >> 1, p = w & 1;
           uint32_t rr[4];
           rng::draw(a.seed, uint32_t(gid), step, uint32_t(blk), rng::kNoise, rr);
-          float nrm[4];
+          const uint32_t r0 = p ? rr[2] : rr[0], r1 = p ? rr[3] : rr[1];  // no dynamic indexing
+          const float rad = sqrtf(-2.0f * logf(rng::u01_open0(r0)));
+          const float th = kTwoPi * rng::u01(r1);
+          float sn, cs;
+          sincosf(th, &sn, &cs);
+          const float nrm[2] = {rad * cs, rad * sn};
 #pragma unroll
-          for (int p = 0; p < 2; ++p) {
-            const float rad = sqrtf(-2.0f * logf(rng::u01_open0(rr[2 * p])));
-            const float th = kTwoPi * rng::u01(rr[2 * p + 1]);
-            nrm[2 * p] = rad * cosf(th);
-            nrm[2 * p + 1] = rad * sinf(th);
-          }
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const int ai = blk * 4 + j;
+          for (int j = 0; j < 2; ++j) {
+            const int ai = blk * 4 + 2 * p + j;
             if (ai < A) {
               const float mu = mu_s[el * kMuLd + ai];
-              const float ls = a.log_std[ai];
-              const float sig = expf(ls);
+              const float ls = ls_s[ai], sig = sig_s[ai];
               const float act = mu + sig * nrm[j];
               const float z = (act - mu) / sig;
               lp_part += -0.5f * z * z - ls - kLog2PiHalf;
               const float u = fminf(fmaxf(act, -1.f), 1.f);
               usq_part += u * u;
-              u_s[el * kMuLd + ai] = u;
+              u_s[el * kMuLd + ai] = tanhf(u);
               a.act[((long long)t * a.N + env) * A + ai] = act;
             }
           }
@@ -263,6 +293,7 @@ __global__ void __launch_bounds__(kThreads, 1) rollout_kernel(const __grid_const
       usq_part += __shfl_xor_sync(0xffffffffu, usq_part, 1);
       usq_part += __shfl_xor_sync(0xffffffffu, usq_part, 2);
       __syncwarp();
+      trace_at(a, t * 16 + 11);
 
       // ---- dynamics on the register-resident state: thread `sub` owns dim blocks
       // k = sub + 4 bi (4 dims each); the right neighbour of a block's last dim is the
@@ -282,9 +313,9 @@ __global__ void __launch_bounds__(kThreads, 1) rollout_kernel(const __grid_const
           xn[bi][j] = 0.f;
           if (valid && i < S) {
             const float nb = i + 1 >= S ? x0 : j < 3 ? xs[bi][j + 1] : (sub == 3 ? nB : nA);
-            const float drive = tanhf(u_s[el * kMuLd + i % A]);
+            const float drive = u_s[el * kMuLd + i % A];  // tanh(clip(a)), see above
             const float xi = xs[bi][j];
-            const float inner = __fadd_rn(__fsub_rn(drive, __fmul_rn(kDamp, xi)), __fmul_rn(kCouple, sinf(nb)));
+            const float inner = __fadd_rn(__fsub_rn(drive, __fmul_rn(kDamp, xi)), __fmul_rn(kCouple, env_sin(nb)));
             xn[bi][j] = __fadd_rn(xi, __fmul_rn(kDt, inner));
             xsq_part = __fadd_rn(xsq_part, __fmul_rn(xn[bi][j], xn[bi][j]));
           }
@@ -325,6 +356,7 @@ __global__ void __launch_bounds__(kThreads, 1) rollout_kernel(const __grid_const
       }
 
       // ---- next observation into the layer-0 operand tile (pads written as zero)
+      trace_at(a, t * 16 + 12);
       epi_bar();  // mu / u staging may alias the obs tile
       if (t + 1 < T) {
         if (valid) {
@@ -339,7 +371,11 @@ __global__ void __launch_bounds__(kThreads, 1) rollout_kernel(const __grid_const
         }
         ptx::fence_proxy_async_smem();
         __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(act_ready);
+        trace_at(a, t * 16 + 13);
+        if (lane == 0) {
+          ptx::mbar_arrive(act_lo);
+          ptx::mbar_arrive(act_hi);
+        }
       }
     }
     if (valid) {
@@ -359,7 +395,7 @@ __global__ void __launch_bounds__(kThreads, 1) rollout_kernel(const __grid_const
 
   ptx::tc_fence_before();
   __syncthreads();
-  if (warp == 1) ptx::tmem_dealloc(tmem, 256);
+  if (warp == 1) ptx::tmem_dealloc(tmem, 512);
 }
 
 }  // namespace

@@ -32,6 +32,7 @@ struct RolloutArgs {
   float* rew;
   uint8_t* done;
   const Control* ctl;
+  unsigned long long* trace;  // optional [T][16] globaltimer stamps of CTA 0 (development aid)
 };
 
 // Whether the fused rollout supports this MLP (hidden widths <= 256, <= 4 layers, S_p <= 256, A <= 31).

@@ -545,6 +545,8 @@ void Trainer::build_plans() {
       r.rew = g.rew;
       r.done = g.done;
       r.ctl = ctl_dev_;
+      const char* trace = std::getenv("GMI_ROLLOUT_TRACE");
+      if (trace && trace[0] == '1') r.trace = reinterpret_cast<unsigned long long*>(dev((size_t)T_ * 16 * 8));
     }
   }
 }
@@ -952,6 +954,10 @@ long long Trainer::get(const std::string& what, int gi, void* dst) {
   if (what == "ep_step") return copy(g.ep_step, N, 4);
   if (what == "ep_len") return copy(g.ep_len, N, 4);
   if (what == "ep_count") return copy(g.ep_count, N, 4);
+  if (what == "rollout_trace") {  // GMI_ROLLOUT_TRACE=1: globaltimer stamps of CTA 0 (int64)
+    if (!g.roll_args.trace) invalid("rollout trace not enabled (GMI_ROLLOUT_TRACE=1)");
+    return copy(g.roll_args.trace, T * 16, 8);
+  }
   if (what == "obs") {  // bf16 X_roll -> fp32 [(T+1)][N][S]
     const long long n = (T + 1) * N * S;
     if (dst) {

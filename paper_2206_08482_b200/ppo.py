@@ -159,7 +159,8 @@ class IterationStats:
     kernel_launches: int
 
 
-_DT = {"done": np.uint8, "ep_step": np.int32, "ep_len": np.int32, "ep_count": np.int32}
+_DT = {"done": np.uint8, "ep_step": np.int32, "ep_len": np.int32, "ep_count": np.int32,
+       "rollout_trace": np.int64}
 
 
 class Trainer:
