@@ -139,8 +139,8 @@ void launch_bn(const GemmParams& P, int a_mn, int b_mn, int epi, int ctas, cudaS
 }  // namespace
 
 int gemm_ws_bn(int M, int N, int K, int problems, int sms) {
-  const int bn = ((N + 63) / 64) * 64;
-  if (bn > 256 || K > kGemmMaxKbWS * kGemmBlockK) return 0;
+  const int bn = N <= 64 ? 64 : N <= 128 ? 128 : 256;  // instantiated block widths
+  if (N > 256 || K > kGemmMaxKbWS * kGemmBlockK) return 0;
   if (((M + kGemmBlockM - 1) / kGemmBlockM) * problems < sms) return 0;
   return bn;
 }

@@ -1,0 +1,386 @@
+// Fused PPO head step of one minibatch (K6 + the head parts of K4/K7): for each
+// 128-row tile of the last hidden activations H_L of one net,
+//   MMA1  head forward        mu | v  = H_L W_head^T           (N = 16 / 32, fp32 in TMEM)
+//   loss  clipped surrogate / value loss per row -> G = dL/dmu | dL/dv (bf16, smem operand)
+//   MMA2  head input grad     acc    = G W_head                (N = hp)
+//   epi   dPre_{L-1} = acc * elu'(H_L) (H_L read from the smem tile) -> bf16 -> TMA store,
+//         plus the column sums of dPre_{L-1} (bias gradient of layer L-1)
+//   MMA3  head weight grad    dW^T  += H_L^T G                 (accumulated in TMEM over all
+//         tiles of the CTA; one fp32 slab per CTA)
+// so the head forward, the loss, the head input- and weight-gradient GEMMs and a column-sum
+// pass become one launch, and mu / v / G never touch HBM.
+//
+// CTA b serves net b % 2 (0 = policy, 1 = value) and its tiles b/2, b/2 + grid/2, ...
+// Warp 0: TMA (head weights once, H tiles), warp 1: tcgen05.mma issuer, warps 2..17:
+// epilogue (warps with column group 0 also run the per-row loss). Per-CTA partial outputs
+// (weight-grad slab, bias-grad row, head-bias / log-std grads and loss statistics) are summed
+// in a fixed order by the gradient-assembly kernel, so results are deterministic.
+// Numerics follow head_loss_kernel / oracle/ppo_oracle.c.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "../host/errors.hpp"
+#include "gemm.cuh"
+#include "head_fused.cuh"
+#include "launch.cuh"
+#include "ppo_common.cuh"
+
+namespace gmi::ppo {
+
+namespace {
+
+constexpr int kRows = 128;
+constexpr int kEpiWarps = 16;
+constexpr int kThreads = 64 + 32 * kEpiWarps;
+constexpr uint32_t kChunk = kRows * 128;  // [128 rows][64 bf16], SW128
+constexpr uint32_t kOffH = 0;              // H_L tile, 4 K-chunks
+constexpr uint32_t kOffG = 4 * kChunk;     // G tile [128][64] bf16 (cols >= n_out stay 0)
+constexpr uint32_t kOffWK = kOffG + kChunk;  // W_head K-major, per K-chunk [32 rows][128 B]
+constexpr uint32_t kOffWM = kOffWK + 4 * 4096;  // W_head MN-major, 64x64 boxes
+constexpr uint32_t kOffStg = kOffWM + 4 * 8192;  // epilogue staging, 2 KB per warp
+constexpr uint32_t kOffRed = kOffStg + kEpiWarps * 2048;  // 4 x 256 fp32
+constexpr uint32_t kOffBar = kOffRed + 4 * 256 * 4;
+constexpr uint32_t kSmem = kOffBar + 256 + 1024;
+constexpr uint32_t kTmemAcc1 = 0, kTmemAcc3 = 64, kTmemAcc2 = 256;
+
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory"); }
+
+template <int MAXA>
+__global__ void __launch_bounds__(kThreads, 1) head_fused_kernel(const __grid_constant__ HeadFusedArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sH = smem + kOffH;
+  uint8_t* sG = smem + kOffG;
+  uint8_t* sWK = smem + kOffWK;
+  uint8_t* sWM = smem + kOffWM;
+  float* red = reinterpret_cast<float*>(smem + kOffRed);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kOffBar);
+  uint64_t* wbar = bars;
+  uint64_t* hfull = bars + 1;
+  uint64_t* hfree = bars + 2;
+  uint64_t* acc1_full = bars + 3;
+  uint64_t* g_ready = bars + 4;
+  uint64_t* acc2_full = bars + 5;
+  uint64_t* fin = bars + 6;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 7);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int net = blockIdx.x & 1;
+  const int cta = blockIdx.x >> 1, ctas = gridDim.x >> 1;
+  const HeadNet& hn = a.net[net];
+  const int hp = a.hp, nk = (hp + 63) / 64, NH = hn.nh, nout = hn.n_out;
+  const int mtiles = (a.Bm + kRows - 1) / kRows;
+
+  if (threadIdx.x == 0) {
+    ptx::mbar_init(wbar, 1);
+    ptx::mbar_init(hfull, 1);
+    ptx::mbar_init(hfree, kEpiWarps + 1);
+    ptx::mbar_init(acc1_full, 1);
+    ptx::mbar_init(g_ready, 4);
+    ptx::mbar_init(acc2_full, 1);
+    ptx::mbar_init(fin, 1);
+    ptx::fence_mbar_init();
+    ptx::tma_prefetch_desc(&hn.map_h);
+    ptx::tma_prefetch_desc(&hn.map_wk);
+    ptx::tma_prefetch_desc(&hn.map_wm);
+    ptx::tma_prefetch_desc(&hn.map_d);
+  }
+  if (warp == 1) ptx::tmem_alloc(tmem_slot, 512);
+  // G tile: columns >= n_out must be zero (they are the K padding of MMA2 / N padding of MMA3)
+  for (int i = threadIdx.x; i < int(kChunk / 16); i += blockDim.x)
+    reinterpret_cast<uint4*>(sG)[i] = make_uint4(0u, 0u, 0u, 0u);
+  ptx::fence_proxy_async_smem();
+  pdl_trigger();
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  pdl_wait();
+
+  if (warp == 0) {
+    // ------------------------------------------------ TMA producer
+    if (lane == 0) {
+      ptx::mbar_arrive_expect_tx(wbar, uint32_t(nk) * (uint32_t(NH) * 128u + 8192u));
+      for (int kc = 0; kc < nk; ++kc) {
+        ptx::tma_load_2d(sWK + kc * 4096, &hn.map_wk, wbar, kc * 64, 0);
+        ptx::tma_load_2d(sWM + kc * 8192, &hn.map_wm, wbar, kc * 64, 0);
+      }
+      int it = 0;
+      for (int j = cta; j < mtiles; j += ctas, ++it) {
+        if (it > 0) ptx::mbar_wait_sleep(hfree, (it - 1) & 1);
+        ptx::mbar_arrive_expect_tx(hfull, uint32_t(nk) * kChunk);
+        for (int kc = 0; kc < nk; ++kc) ptx::tma_load_2d(sH + kc * kChunk, &hn.map_h, hfull, kc * 64, j * kRows);
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      ptx::mbar_wait_sleep(wbar, 0);
+      const uint32_t idesc1 = ptx::umma_idesc_bf16(kRows, uint32_t(NH), 0, 0);
+      const uint32_t idesc2 = ptx::umma_idesc_bf16(kRows, uint32_t((hp + 15) / 16 * 16), 0, 1);
+      const uint32_t idesc3 = ptx::umma_idesc_bf16(kRows, uint32_t(NH), 1, 1);
+      const uint32_t h0 = ptx::smem_u32(sH), g0 = ptx::smem_u32(sG);
+      const uint32_t wk0 = ptx::smem_u32(sWK), wm0 = ptx::smem_u32(sWM);
+      int it = 0;
+      for (int j = cta; j < mtiles; j += ctas, ++it) {
+        ptx::mbar_wait(hfull, it & 1);
+        ptx::tc_fence_after();
+        // MMA1: [128 x NH] = H . W_head^T (K = hp)
+        for (int kc = 0; kc < nk; ++kc) {
+          const int ks = min(4, (hp - kc * 64 + 15) / 16);
+          for (int k = 0; k < ks; ++k)
+            ptx::mma_bf16(tmem + kTmemAcc1, ptx::umma_desc_sw128(h0 + kc * kChunk + k * 32, 16, 1024),
+                          ptx::umma_desc_sw128(wk0 + kc * 4096 + k * 32, 16, 1024), idesc1,
+                          (kc > 0 || k > 0) ? 1u : 0u);
+        }
+        ptx::mma_commit(acc1_full);
+        ptx::mbar_wait(g_ready, it & 1);
+        ptx::tc_fence_after();
+        // MMA2: [128 x hp] = G . W_head (K = NH; W_head read MN-major)
+        for (int k = 0; k < NH / 16; ++k)
+          ptx::mma_bf16(tmem + kTmemAcc2, ptx::umma_desc_sw128(g0 + k * 32, 16, 1024),
+                        ptx::umma_desc_sw128(wm0 + k * 2048, 8192, 1024), idesc2, k > 0 ? 1u : 0u);
+        ptx::mma_commit(acc2_full);
+        // MMA3: dW_head^T[hp x NH] += H^T . G (K = tile rows; both operands MN-major views)
+        for (int half = 0; half * 128 < hp; ++half)
+          for (int k = 0; k < kRows / 16; ++k)
+            ptx::mma_bf16(tmem + kTmemAcc3 + half * 32,
+                          ptx::umma_desc_sw128(h0 + 2 * half * kChunk + k * 2048, kChunk, 1024),
+                          ptx::umma_desc_sw128(g0 + k * 2048, 8192, 1024), idesc3,
+                          (it > 0 || k > 0) ? 1u : 0u);
+        ptx::mma_commit(hfree);
+      }
+      ptx::mma_commit(fin);
+    }
+  } else {
+    // ------------------------------------------------ epilogue warps
+    const int q = warp & 3;
+    const int h = (warp - 2) >> 2;
+    const int row = q * 32 + lane;
+    const float invB = 1.0f / float(a.Bm);
+    uint8_t* stg = smem + kOffStg + (warp - 2) * 2048;
+    float sg[MAXA], sl[MAXA];  // running db_head / dlog_std of this thread's rows
+#pragma unroll
+    for (int i = 0; i < MAXA; ++i) sg[i] = sl[i] = 0.f;
+    float st[4] = {0.f, 0.f, 0.f, 0.f};
+    float csum[2] = {0.f, 0.f};
+    int it = 0;
+    for (int j = cta; j < mtiles; j += ctas, ++it) {
+      const int grow = j * kRows + row;
+      const bool valid = grow < a.Bm;
+      if (h == 0) {
+        // ---- per-row loss (thread = row): TMEM lane quarter q
+        ptx::mbar_wait_sleep(acc1_full, it & 1);
+        ptx::tc_fence_after();
+        uint32_t r[32];
+        ptx::tmem_ld_32x32b_x32(tmem + kTmemAcc1 + (static_cast<uint32_t>(q * 32) << 16), r);
+        ptx::tmem_ld_wait();
+        uint8_t* grow_s = sG + row * 128;
+        auto put_g = [&](int col, float v) {  // bf16 into the SW128 G tile
+          *reinterpret_cast<__nv_bfloat16*>(grow_s + ((((col >> 3) ^ (row & 7))) << 4) + (col & 7) * 2) =
+              __float2bfloat16_rn(v);
+        };
+        if (net == 0) {
+          const int A = nout;
+          float gmu[MAXA];
+#pragma unroll
+          for (int i = 0; i < MAXA; ++i) gmu[i] = 0.f;
+          if (valid) {
+            const long long rr = a.row0 + grow;
+            float mu[MAXA], z[MAXA], sig[MAXA], ls[MAXA];
+            float lp = 0.f;
+#pragma unroll
+            for (int i = 0; i < MAXA; ++i)
+              if (i < A) {
+                mu[i] = __uint_as_float(r[i]) + hn.bias[i];
+                ls[i] = a.log_std[i];
+                sig[i] = expf(ls[i]);
+                z[i] = (a.act[rr * A + i] - mu[i]) / sig[i];
+                lp += -0.5f * z[i] * z[i] - ls[i] - kLog2PiHalf;
+              }
+            const float oldlp = a.oldlp[rr], adv = a.adv[rr];
+            const float ratio = expf(lp - oldlp);
+            const float s1 = ratio * adv;
+            const float rc = fminf(fmaxf(ratio, 1.f - a.clip), 1.f + a.clip);
+            const float s2 = rc * adv;
+            const bool take1 = s1 <= s2;
+            const float glp = take1 ? -s1 * invB : 0.f;
+#pragma unroll
+            for (int i = 0; i < MAXA; ++i)
+              if (i < A) {
+                gmu[i] = glp * z[i] / sig[i];
+                sg[i] += gmu[i];
+                sl[i] += glp * (z[i] * z[i] - 1.f) - a.ent_coef * invB;
+              }
+            st[0] += -(take1 ? s1 : s2);
+            st[2] += oldlp - lp;
+            st[3] += (ratio < 1.f - a.clip || ratio > 1.f + a.clip) ? 1.f : 0.f;
+          }
+#pragma unroll
+          for (int i = 0; i < MAXA; ++i)
+            if (i < A) put_g(i, gmu[i]);
+        } else {
+          float gv = 0.f;
+          if (valid) {
+            const long long rr = a.row0 + grow;
+            const float v = __uint_as_float(r[0]) + hn.bias[0];
+            const float verr = v - a.ret[rr];
+            gv = a.vf_coef * verr * invB;
+            sg[0] += gv;
+            st[1] += 0.5f * a.vf_coef * verr * verr;
+          }
+          put_g(0, gv);
+        }
+        ptx::fence_proxy_async_smem();
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(g_ready);
+      }
+
+      // ---- dPre_{L-1} = (G W_head) * elu'(H_L): 32-column chunks c = h, h + 4
+      ptx::mbar_wait_sleep(acc2_full, it & 1);
+      ptx::tc_fence_after();
+#pragma unroll 1
+      for (int pass = 0; pass < 2; ++pass) {
+        const int c = h + 4 * pass;
+        if (c * 32 >= hp) break;
+        uint32_t r[32];
+        ptx::tmem_ld_32x32b_x32(tmem + kTmemAcc2 + (static_cast<uint32_t>(q * 32) << 16) + c * 32, r);
+        // H_L row `row`, columns 32c..32c+31: 4 x 16 B from the swizzled operand tile
+        const uint8_t* hrow = sH + (c >> 1) * kChunk + row * 128;
+        uint4 hv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          hv[u] = *reinterpret_cast<const uint4*>(hrow + ((((c & 1) * 4 + u) ^ (row & 7)) << 4));
+        ptx::tmem_ld_wait();
+        uint32_t packed[16];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const uint32_t hw[4] = {hv[u].x, hv[u].y, hv[u].z, hv[u].w};
+#pragma unroll
+          for (int x = 0; x < 4; ++x) {
+            const int jj = u * 8 + x * 2;
+            const float2 d = dact2(make_float2(__uint_as_float(r[jj]), __uint_as_float(r[jj + 1])), hw[x]);
+            packed[jj / 2] = pack_bf16(d.x, d.y);
+          }
+        }
+        if (lane == 0) ptx::bulk_wait_read<0>();  // the staging buffer's previous store has read it
+        __syncwarp();
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          *reinterpret_cast<uint4*>(stg + lane * 64 + ((u ^ ((lane >> 1) & 3)) << 4)) =
+              make_uint4(packed[4 * u], packed[4 * u + 1], packed[4 * u + 2], packed[4 * u + 3]);
+        __syncwarp();
+        float s = 0.f;  // lane = column: the 32 staged rows in row order
+#pragma unroll
+        for (int rr = 0; rr < 32; ++rr) {
+          const uint16_t v =
+              *reinterpret_cast<const uint16_t*>(stg + rr * 64 + (((lane >> 3) ^ ((rr >> 1) & 3)) << 4) + (lane & 7) * 2);
+          s += __uint_as_float(uint32_t(v) << 16);
+        }
+        csum[pass] += s;
+        ptx::fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          ptx::tma_store_2d(&hn.map_d, stg, c * 32, j * kRows + q * 32);
+          ptx::bulk_commit();
+        }
+      }
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(hfree);
+    }
+
+    // ---- per-CTA outputs
+    // (a) bias gradient of layer L-1: combine the 4 lane quarters in order
+#pragma unroll
+    for (int pass = 0; pass < 2; ++pass) {
+      const int c = h + 4 * pass;
+      if (c * 32 < 256) red[q * 256 + c * 32 + lane] = csum[pass];
+    }
+    epi_bar();
+    if (q == 0)
+#pragma unroll
+      for (int pass = 0; pass < 2; ++pass) {
+        const int col = (h + 4 * pass) * 32 + lane;
+        if (col < hp) hn.colsum[(long long)cta * hp + col] = ((red[col] + red[256 + col]) + red[512 + col]) + red[768 + col];
+      }
+    epi_bar();
+    // (b) head weight gradient slab: TMEM rows = hp index, columns = head outputs
+    ptx::mbar_wait_sleep(fin, 0);
+    ptx::tc_fence_after();
+    if (h < 2 && h * 128 < hp) {
+      uint32_t r[32];
+      ptx::tmem_ld_32x32b_x32(tmem + kTmemAcc3 + h * 32 + (static_cast<uint32_t>(q * 32) << 16), r);
+      ptx::tmem_ld_wait();
+      const int k = h * 128 + row;
+      if (k < hp)
+        for (int o = 0; o < nout; ++o)
+          hn.dw_slab[((long long)cta * nout + o) * hp + k] = (it > 0) ? __uint_as_float(r[o]) : 0.f;
+    }
+    // (c) head-bias / log-std gradients and loss statistics (warps with h == 0 hold them)
+    const int stride = head_partial_stride(a.A);
+    if (h == 0) {
+      auto put = [&](int col, float x) {
+        x = warp_sum(x);
+        if (lane == 0) red[q * 128 + col] = x;
+      };
+      for (int col = 0; col < stride; ++col) {  // zero the record first (fields of the other net)
+        if (lane == 0) red[q * 128 + col] = 0.f;
+      }
+      __syncwarp();
+      if (net == 0) {
+#pragma unroll
+        for (int i = 0; i < MAXA; ++i)
+          if (i < a.A) {
+            put(i, sg[i]);
+            put(a.A + 1 + i, sl[i]);
+          }
+        put(2 * a.A + 1, st[0]);
+        put(2 * a.A + 3, st[2]);
+        put(2 * a.A + 4, st[3]);
+      } else {
+        put(a.A, sg[0]);
+        put(2 * a.A + 2, st[1]);
+      }
+    }
+    epi_bar();
+    if (h == 0 && q == 0)
+      for (int col = lane; col < stride; col += 32)
+        a.part[(long long)blockIdx.x * stride + col] =
+            ((red[col] + red[128 + col]) + red[256 + col]) + red[384 + col];
+    if (lane == 0) ptx::bulk_wait<0>();
+  }
+
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) ptx::tmem_dealloc(tmem, 512);
+}
+
+}  // namespace
+
+bool head_fusable(int hp, int A) { return hp <= 256 && A <= 31 && A >= 1; }
+
+int head_fused_grid(int Bm, int sms) {
+  const int tiles = (Bm + kRows - 1) / kRows;
+  const int per_net = std::max(1, std::min(tiles, sms / 2));
+  return 2 * per_net;
+}
+
+void launch_head_fused(const HeadFusedArgs& a, int grid, cudaStream_t s) {
+  auto go = [&](auto kern) {
+    static bool configured[4] = {};
+    (void)configured;
+    GMI_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
+    launch_pdl(kern, dim3(grid), dim3(kThreads), kSmem, s, a);
+  };
+  if (a.A <= 8)
+    go(head_fused_kernel<8>);
+  else if (a.A <= 16)
+    go(head_fused_kernel<16>);
+  else
+    go(head_fused_kernel<31>);
+}
+
+}  // namespace gmi::ppo

@@ -24,6 +24,7 @@
 #include <cstring>
 
 #include "../cuda/rng.cuh"
+#include "../cuda/head_fused.cuh"
 #include "../cuda/rollout.cuh"
 #include "errors.hpp"
 #include "gmi_exec.hpp"
@@ -143,6 +144,9 @@ struct Trainer::Gmi {
   bool fused_roll = false;
   ppo::RolloutArgs roll_args{};
   bool fused_bias[GMI_MAX_HIDDEN] = {};  // bias gradient summed in the producing DACT GEMM
+  bool fused_head = false;
+  int head_grid = 0;
+  ppo::HeadFusedArgs head_args{};
 };
 
 // ------------------------------------------------------------------ construction
@@ -307,9 +311,13 @@ void Trainer::init_params() {
 // ------------------------------------------------------------------ GEMM descriptors
 void Trainer::build_plans() {
   const int L = geo_.L, S_p = geo_.wp[0], A = geo_.A, hp = geo_.wp[L];
+  // Kernel-written scratch (slabs, partial rows). GMI_POISON=1 fills it with NaN bytes so a
+  // read-before-write shows up in the parity tests instead of depending on allocator history.
+  const char* poison = std::getenv("GMI_POISON");
   auto dev = [&](size_t bytes) {
     void* p = nullptr;
     GMI_CUDA_CHECK(cudaMalloc(&p, std::max<size_t>(bytes, 256)));
+    if (poison && poison[0] == '1') GMI_CUDA_CHECK(cudaMemset(p, 0xFF, std::max<size_t>(bytes, 256)));
     allocs_.push_back(p);
     return static_cast<float*>(p);
   };
@@ -367,7 +375,7 @@ void Trainer::build_plans() {
 
       // weight gradient dW_l[out_p][in_p] = sum_rows dPre_l^T in_l (both operands MN-major)
       const int cur = (L - 1 - l) & 1;
-      const int bnw = std::min(256, ((in_p + 63) / 64) * 64);
+      const int bnw = in_p <= 64 ? 64 : in_p <= 128 ? 128 : 256;  // instantiated block widths
       g.bn_dw[l] = bnw;
       int splits = 1, kbps = 1;
       pick_splits(out_p, in_p, bnw, 2, g.Bm, g.ctas, &splits, &kbps);
@@ -468,7 +476,7 @@ void Trainer::build_plans() {
       g.fused_bias[L - 1] = g.ws_hdx;
     }
     // head weight gradients on the tensor cores: dW_mu = G_pi^T H_L, dw_v = G_v^T H^v_L
-    const int bnh = std::min(256, ((hp + 63) / 64) * 64);
+    const int bnh = hp <= 64 ? 64 : hp <= 128 ? 128 : 256;
     g.bn_head = bnh;
     int hsplits = 1, hkbps = 1;
     pick_splits(A, hp, bnh, 2, g.Bm, g.ctas, &hsplits, &hkbps);
@@ -491,22 +499,63 @@ void Trainer::build_plans() {
     g.dhead.num_problems = 2;
     g.dhead.splits = hsplits;
     g.flop_head = 2.0 * (A + 1) * double(geo_.width[L]) * g.Bm;
+
+    // fused head (forward + loss + head input / weight gradients + bias sums of layer L-1)
+    const char* head_unfused = std::getenv("GMI_HEAD_UNFUSED");
+    g.fused_head = ppo::head_fusable(hp, A) && !(head_unfused && head_unfused[0] == '1');
+    int head_parts = ppo::head_loss_blocks(g.Bm), hslab_parts = hsplits;
+    if (g.fused_head) {
+      g.head_grid = ppo::head_fused_grid(g.Bm, g.ctas);
+      const int per_net = g.head_grid / 2;
+      ppo::HeadFusedArgs& h = g.head_args;
+      for (int n = 0; n < 2; ++n) {
+        ppo::HeadNet& hn = h.net[n];
+        hn.n_out = head_rows[n];
+        hn.nh = hn.n_out <= 16 ? 16 : 32;
+        hn.map_h = tma_kmajor(g.H[n][L - 1], hp, g.Bm, hp, kGemmBlockM);
+        hn.map_wk = tma_kmajor(shadow_ + geo_.net[n][L].w, hp, hn.n_out, hp, hn.nh);
+        hn.map_wm = tma_mnmajor(shadow_ + geo_.net[n][L].w, hp, hn.n_out, hp);
+        hn.map_d = make_tma_out_bf16(g.D[n][0], hp, g.Bm, hp);
+        hn.bias = params_ + geo_.net[n][L].b;
+        hn.colsum = g.colsum[n][L - 1];
+        g.head_slab[n] = dev((size_t)per_net * hn.n_out * hp * 4);
+        hn.dw_slab = g.head_slab[n];
+      }
+      h.log_std = params_ + geo_.log_std;
+      h.act = g.act_sh;
+      h.oldlp = g.oldlp_sh;
+      h.adv = g.adv_sh;
+      h.ret = g.ret_sh;
+      g.head_part = dev((size_t)g.head_grid * ppo::head_partial_stride(A) * 4);  // one record per CTA
+      h.part = g.head_part;
+      h.Bm = g.Bm;
+      h.A = A;
+      h.hp = hp;
+      h.clip = cfg_.clip;
+      h.vf_coef = cfg_.vf_coef;
+      h.ent_coef = cfg_.ent_coef;
+      g.fused_bias[L - 1] = true;
+      head_parts = g.head_grid;
+      hslab_parts = per_net;
+    }
+
     // gradient assembly segments (fixed-order sums of slabs / partials into the flat grad)
-    const int hb = ppo::head_loss_blocks(g.Bm), cb = ppo::colsum_blocks(g.Bm);
+    const int cb = ppo::colsum_blocks(g.Bm);
     const int hs = ppo::head_partial_stride(A);
     for (int n = 0; n < 2; ++n)
       for (int l = 0; l < L; ++l) {
         const Tensor& t = geo_.net[n][l];
         g.segs.push_back({g.grad + t.w, g.slab[n][l], (long long)t.out_p * t.in_p, t.out_p * t.in_p, g.dw[l].splits});
-        const int parts = g.fused_bias[l] ? gemm_ws_grid(g.Bm, 2, g.ctas) / 2 : cb;
+        int parts = cb;
+        if (g.fused_bias[l]) parts = (l == L - 1 && g.fused_head) ? g.head_grid / 2 : gemm_ws_grid(g.Bm, 2, g.ctas) / 2;
         g.segs.push_back({g.grad + t.b, g.colsum[n][l], t.out_p, t.out_p, parts});
       }
-    g.segs.push_back({g.grad + geo_.net[0][L].w, g.head_slab[0], (long long)A * hp, A * hp, hsplits});
-    g.segs.push_back({g.grad + geo_.net[1][L].w, g.head_slab[1], hp, hp, hsplits});
-    g.segs.push_back({g.grad + geo_.net[0][L].b, g.head_part, hs, A, hb});
-    g.segs.push_back({g.grad + geo_.net[1][L].b, g.head_part + A, hs, 1, hb});
-    g.segs.push_back({g.grad + geo_.log_std, g.head_part + A + 1, hs, A, hb});
-    if (g.local == 0) g.segs.push_back({stats_dev_, g.head_part + 2 * A + 1, hs, 4, hb});
+    g.segs.push_back({g.grad + geo_.net[0][L].w, g.head_slab[0], (long long)A * hp, A * hp, hslab_parts});
+    g.segs.push_back({g.grad + geo_.net[1][L].w, g.head_slab[1], hp, hp, hslab_parts});
+    g.segs.push_back({g.grad + geo_.net[0][L].b, g.head_part, hs, A, head_parts});
+    g.segs.push_back({g.grad + geo_.net[1][L].b, g.head_part + A, hs, 1, head_parts});
+    g.segs.push_back({g.grad + geo_.log_std, g.head_part + A + 1, hs, A, head_parts});
+    if (g.local == 0) g.segs.push_back({stats_dev_, g.head_part + 2 * A + 1, hs, 4, head_parts});
 
     // fused rollout (one persistent kernel per rollout) when the policy MLP fits on chip
     const char* unfused = std::getenv("GMI_ROLLOUT_UNFUSED");
@@ -702,8 +751,14 @@ void Trainer::train_minibatch(Gmi& g, int k) {
     gemm(g, GMI_PH_FWD_GEMM, P, g.bn_fwd[l], 0, 0, EPI_BIAS_ELU, g.flop_fwd[l], g.ws_fwd[l]);
   }
   const double hflop = 2.0 * (A + 1) * geo_.width[L] * g.Bm;
-  gemm(g, GMI_PH_HEAD_FWD, g.head_train, 64, 0, 0, EPI_F32, hflop);
-  ppo::HeadLossArgs h{};
+  if (g.fused_head) {  // head forward + loss + head input/weight grads + bias sums, one launch
+    ppo::HeadFusedArgs h = g.head_args;
+    h.row0 = (long long)k * g.Bm;
+    timed(g.s, GMI_PH_HEAD_LOSS, 3.0 * hflop, 0.0, [&] { ppo::launch_head_fused(h, g.head_grid, g.s); });
+    ++launches_;
+  } else {
+    gemm(g, GMI_PH_HEAD_FWD, g.head_train, 64, 0, 0, EPI_F32, hflop);
+    ppo::HeadLossArgs h{};
   h.mu = g.outh[0];
   h.v = g.outh[1];
   h.b_mu = params_ + geo_.net[0][L].b;
@@ -722,10 +777,11 @@ void Trainer::train_minibatch(Gmi& g, int k) {
   h.clip = cfg_.clip;
   h.vf_coef = cfg_.vf_coef;
   h.ent_coef = cfg_.ent_coef;
-  timed(g.s, GMI_PH_HEAD_LOSS, 0.0, double(g.Bm) * (10.0 * A + 18.0), [&] { ppo::launch_head_loss(h, g.s); });
-  ++launches_;
-  gemm(g, GMI_PH_HEAD_DX, g.head_dx, g.bn_hdx, 0, 1, EPI_DACT, hflop, g.ws_hdx);
-  gemm(g, GMI_PH_HEAD_DW, g.dhead, g.bn_head, 1, 1, EPI_F32, g.flop_head);
+    timed(g.s, GMI_PH_HEAD_LOSS, 0.0, double(g.Bm) * (10.0 * A + 18.0), [&] { ppo::launch_head_loss(h, g.s); });
+    ++launches_;
+    gemm(g, GMI_PH_HEAD_DX, g.head_dx, g.bn_hdx, 0, 1, EPI_DACT, hflop, g.ws_hdx);
+    gemm(g, GMI_PH_HEAD_DW, g.dhead, g.bn_head, 1, 1, EPI_F32, g.flop_head);
+  }
   for (int l = L - 1; l >= 0; --l) {
     GemmParams P = g.dw[l];
     if (l == 0) P.prob[0].b_row0 = P.prob[1].b_row0 = k * g.Bm;
@@ -954,6 +1010,10 @@ long long Trainer::get(const std::string& what, int gi, void* dst) {
   if (what == "ep_step") return copy(g.ep_step, N, 4);
   if (what == "ep_len") return copy(g.ep_len, N, 4);
   if (what == "ep_count") return copy(g.ep_count, N, 4);
+  if (what == "head_part") {  // per-block head-gradient / loss partial records (debug)
+    const int parts = g.fused_head ? g.head_grid : ppo::head_loss_blocks(g.Bm);
+    return copy(g.head_part, (long long)parts * ppo::head_partial_stride(geo_.A), 4);
+  }
   if (what == "rollout_trace") {  // GMI_ROLLOUT_TRACE=1: globaltimer stamps of CTA 0 (int64)
     if (!g.roll_args.trace) invalid("rollout trace not enabled (GMI_ROLLOUT_TRACE=1)");
     return copy(g.roll_args.trace, T * 16, 8);

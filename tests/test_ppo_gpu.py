@@ -140,6 +140,37 @@ def test_fused_rollout_matches_per_layer_path(cuda, monkeypatch, dims):
             np.testing.assert_allclose(fused.get(f), plain.get(f), rtol=1e-5, atol=1e-5)
 
 
+@pytest.mark.parametrize("dims", [(12, 3, [64, 64]), (60, 8, [256, 256, 256]), (40, 20, [96, 160])])
+def test_fused_head_matches_per_kernel_path(cuda, monkeypatch, dims):
+    """cuda/head_fused.cu (head forward + loss + head input / weight gradients + bias sums in
+    one kernel) vs the head GEMMs + loss kernel path on the same minibatch. The per-row loss
+    and every bf16 rounding point are shared; only fp32 accumulation orders differ."""
+    from paper_2206_08482_b200.ppo import PpoConfig, Trainer
+    S, A, hidden = dims
+    cfg = dict(obs_dim=S, act_dim=A, hidden=hidden, num_envs=200)
+    fused = Trainer(PpoConfig(**cfg))
+    monkeypatch.setenv("GMI_HEAD_UNFUSED", "1")
+    plain = Trainer(PpoConfig(**cfg))
+    B = 200 * 32 // 4
+    rng = np.random.default_rng(S + A)
+    X = rng.uniform(-1, 1, (B, S)).astype(np.float32)
+    act = rng.standard_normal((B, A)).astype(np.float32)
+    oldlp = (rng.standard_normal(B) - 3).astype(np.float32)
+    adv = rng.standard_normal(B).astype(np.float32)
+    ret = rng.standard_normal(B).astype(np.float32)
+    g1 = fused.minibatch_grad(X, act, oldlp, adv, ret)
+    g2 = plain.minibatch_grad(X, act, oldlp, adv, ret)
+    lay = param_layout(S, A, hidden)
+    for key, t in lay.items():
+        if not isinstance(key, tuple):
+            continue
+        for part, n in (("w", t["out_p"] * t["in_p"]), ("b", t["out_p"])):
+            a, b = g1[t[part]:t[part] + n], g2[t[part]:t[part] + n]
+            assert np.linalg.norm(a - b) <= 1e-4 * (np.linalg.norm(b) + 1e-12), (key, part)
+    ls = slice(lay["log_std"], lay["log_std"] + A)
+    np.testing.assert_allclose(g1[ls], g2[ls], rtol=1e-4, atol=1e-7)
+
+
 def test_bench_workload_runs(cuda):
     """BASELINE config 2: AT, 4096 envs, 3x256, 1 GMI."""
     from paper_2206_08482_b200.ppo import PpoConfig, Trainer
