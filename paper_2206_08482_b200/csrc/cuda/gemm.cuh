@@ -83,13 +83,16 @@ struct GemmSmem {
   static_assert(kBytes <= 232448, "shared memory budget");
 };
 
-template <int BN, int A_MN, int B_MN, int EPI, int WS>
-__global__ void __launch_bounds__(gemm_threads(EPI), 1) gemm_tcgen05_kernel(const __grid_constant__ GemmParams P) {
+// CS = 1 (EPI_F32 with MN-major A only): 4 extra warps sum the A stages over K (bias gradient).
+template <int BN, int A_MN, int B_MN, int EPI, int WS, int CS = 0>
+__global__ void __launch_bounds__(gemm_threads(EPI) + 128 * CS, 1)
+    gemm_tcgen05_kernel(const __grid_constant__ GemmParams P) {
   using L = GemmSmem<BN, EPI, WS>;
   constexpr int S = L::kStages;
   constexpr int kEpiWarps = L::kEpiWarps;
   constexpr uint32_t kIdesc = ptx::umma_idesc_bf16(kGemmBlockM, BN, A_MN, B_MN);
   static_assert(BN % 64 == 0 && BN <= 256, "BN must be 64, 128 or 256");
+  static_assert(!CS || (EPI == EPI_F32 && A_MN && !WS), "column sums: split-K weight gradient only");
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -114,7 +117,7 @@ __global__ void __launch_bounds__(gemm_threads(EPI), 1) gemm_tcgen05_kernel(cons
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       ptx::mbar_init(&full_bar[s], 1);
-      ptx::mbar_init(&empty_bar[s], 1);
+      ptx::mbar_init(&empty_bar[s], 1 + 4 * CS);  // MMA commit (+ 4 column-sum warps)
     }
     for (int b = 0; b < 2; ++b) {
       ptx::mbar_init(&tfull_bar[b], 1);
@@ -233,7 +236,7 @@ __global__ void __launch_bounds__(gemm_threads(EPI), 1) gemm_tcgen05_kernel(cons
         ptx::mma_commit(&tfull_bar[buf]);
       }
     }
-  } else {
+  } else if (warp < 2 + kEpiWarps) {
     // ---------------- epilogue warps: TMEM lane quarter q, every W-th 32-column chunk
     constexpr int W = kEpiWarps / 4;  // warps per lane quarter
     const int e = warp - 2;
@@ -243,13 +246,6 @@ __global__ void __launch_bounds__(gemm_threads(EPI), 1) gemm_tcgen05_kernel(cons
     uint8_t* stage_base = staging + e * L::kStagingBufs * L::kStaging;
     int sbuf = 0;
     int lt = 0;
-    // Fused bias gradient (EPI_DACT, weight-stationary: this CTA always sees the same problem
-    // and columns): per-lane running column sums of the bf16 output over all of its tiles.
-    constexpr bool kColsum = EPI == EPI_DACT && WS;
-    constexpr int kMyChunks = (kChunks + W - 1) / W;
-    float csum[kMyChunks];
-#pragma unroll
-    for (int i = 0; i < kMyChunks; ++i) csum[i] = 0.f;
     for (int tile = blockIdx.x; tile < ntile_total; tile += gridDim.x, ++lt) {
       int prob, split, m0, n0, kb0, nkb;
       decode(tile, prob, split, m0, n0, kb0, nkb);
@@ -325,21 +321,6 @@ __global__ void __launch_bounds__(gemm_threads(EPI), 1) gemm_tcgen05_kernel(cons
           for (int j = 0; j < 4; ++j)
             *reinterpret_cast<uint4*>(st + lane * 64 + ((j ^ ((lane >> 1) & 3)) << 4)) =
                 make_uint4(packed[4 * j], packed[4 * j + 1], packed[4 * j + 2], packed[4 * j + 3]);
-          if constexpr (kColsum) {
-            if (pr.colsum) {  // lane = column: sum the staged 32 rows in row order
-              __syncwarp();
-              float s = 0.f;
-#pragma unroll
-              for (int rr = 0; rr < 32; ++rr) {
-                const uint16_t v = *reinterpret_cast<const uint16_t*>(
-                    st + rr * 64 + ((((lane >> 3) ^ ((rr >> 1) & 3))) << 4) + (lane & 7) * 2);
-                s += __uint_as_float(uint32_t(v) << 16);
-              }
-#pragma unroll
-              for (int i = 0; i < kMyChunks; ++i)
-                if (i == (c - h) / W) csum[i] += s;
-            }
-          }
         }
         ptx::fence_proxy_async_smem();
         __syncwarp();
@@ -356,28 +337,37 @@ __global__ void __launch_bounds__(gemm_threads(EPI), 1) gemm_tcgen05_kernel(cons
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(&tempty_bar[buf]);
     }
-    if constexpr (kColsum) {
-      const GemmProblem& pr = P.prob[blockIdx.x % P.num_problems];
-      if (pr.colsum) {  // combine the 4 lane quarters in order; one row per CTA
-        float* red = reinterpret_cast<float*>(smem);  // operand stages are idle by now
-#pragma unroll
-        for (int i = 0; i < kMyChunks; ++i) {
-          const int c = h + i * W;
-          if (c < kChunks) red[q * BN + c * 32 + lane] = csum[i];
-        }
-        asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");
-        if (q == 0) {
-          float* dst = pr.colsum + (long long)(blockIdx.x / P.num_problems) * pr.N;
-#pragma unroll
-          for (int i = 0; i < kMyChunks; ++i) {
-            const int col = (h + i * W) * 32 + lane;
-            if (col < pr.N && col < BN)
-              dst[col] = ((red[col] + red[BN + col]) + red[2 * BN + col]) + red[3 * BN + col];
+    if (lane == 0) ptx::bulk_wait<0>();
+  } else if constexpr (CS) {
+    // ---------------- column-sum warps (split-K weight gradient, A = dPre MN-major): while the
+    // MMA consumes each A stage, sum its 64 K-rows for the tile's 128 M-columns (the layer's
+    // bias gradient = column sums of dPre), then co-release the stage. CTAs with n0 == 0 write
+    // one fp32 row per (split, m-tile): colsum[split * M + m].
+    const int c = (warp - 2 - kEpiWarps) * 32 + lane;  // 0..127
+    const int box = c >> 6, cc = c & 63;
+    int it = 0;
+    for (int tile = blockIdx.x; tile < ntile_total; tile += gridDim.x) {
+      int prob, split, m0, n0, kb0, nkb;
+      decode(tile, prob, split, m0, n0, kb0, nkb);
+      const GemmProblem& pr = P.prob[prob];
+      const bool on = pr.colsum != nullptr && n0 == 0;
+      float s = 0.f;
+      for (int i = 0; i < nkb; ++i, ++it) {
+        const int st = it % S;
+        ptx::mbar_wait(&full_bar[st], (it / S) & 1);
+        if (on) {
+          const uint8_t* sa = smem + st * L::kStage + box * 8192 + (cc & 7) * 2;
+#pragma unroll 8
+          for (int r = 0; r < kGemmBlockK; ++r) {
+            const uint16_t v = *reinterpret_cast<const uint16_t*>(sa + r * 128 + ((((cc >> 3) ^ (r & 7))) << 4));
+            s += __uint_as_float(uint32_t(v) << 16);
           }
         }
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&empty_bar[st]);
       }
+      if (on && m0 + c < pr.M) pr.colsum[(long long)split * pr.M + m0 + c] = s;
     }
-    if (lane == 0) ptx::bulk_wait<0>();
   }
 
   ptx::tc_fence_before();

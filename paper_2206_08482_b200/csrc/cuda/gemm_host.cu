@@ -102,21 +102,27 @@ int gemm_choose_bn(int M, int N, int problems, int splits, int sms) {
 
 namespace {
 
-template <int BN, int AMN, int BMN, int EPI, int WS = 0>
+template <int BN, int AMN, int BMN, int EPI, int WS = 0, int CS = 0>
 void launch_t(const GemmParams& P, int ctas, cudaStream_t s) {
   constexpr int smem = GemmSmem<BN, EPI, WS>::kBytes;
-  auto kern = gemm_tcgen05_kernel<BN, AMN, BMN, EPI, WS>;
+  auto kern = gemm_tcgen05_kernel<BN, AMN, BMN, EPI, WS, CS>;
   static bool configured = false;  // per instantiation
   if (!configured) {
     GMI_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     configured = true;
   }
-  launch_pdl(kern, dim3(ctas), dim3(gemm_threads(EPI)), smem, s, P);
+  launch_pdl(kern, dim3(ctas), dim3(gemm_threads(EPI) + 128 * CS), smem, s, P);
 }
 
 template <int BN>
 void launch_bn(const GemmParams& P, int a_mn, int b_mn, int epi, int ctas, cudaStream_t s, int ws) {
   const int key = a_mn * 100 + b_mn * 10 + epi;
+  bool cs = false;
+  for (int i = 0; i < P.num_problems; ++i) cs = cs || P.prob[i].colsum != nullptr;
+  if (cs) {  // split-K weight gradient with fused bias-gradient column sums
+    if (key != 1 * 100 + 1 * 10 + EPI_F32 || ws) invalid("column sums need the MN-major weight-gradient GEMM");
+    return launch_t<BN, 1, 1, EPI_F32, 0, 1>(P, ctas, s);
+  }
   if (ws) {
     switch (key) {
       case 0 * 100 + 0 * 10 + EPI_BIAS_ELU: return launch_t<BN, 0, 0, EPI_BIAS_ELU, 1>(P, ctas, s);
@@ -163,9 +169,6 @@ void gemm_launch(const GemmParams& P, int bn, int a_mn, int b_mn, int epi, cudaS
     if (P.splits != 1 || P.prob[0].N > bn || P.prob[0].K > kGemmMaxKbWS * kGemmBlockK)
       invalid("weight-stationary GEMM needs splits == 1, N <= block_n, K <= 256");
     ctas = gemm_ws_grid(P.prob[0].M, P.num_problems, max_ctas > 0 ? max_ctas : sms);
-  } else {
-    for (int i = 0; i < P.num_problems; ++i)
-      if (P.prob[i].colsum) invalid("fused column sums need the weight-stationary GEMM");
   }
   switch (bn) {
     case 64: return launch_bn<64>(P, a_mn, b_mn, epi, ctas, s, ws);

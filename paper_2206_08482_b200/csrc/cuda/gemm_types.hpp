@@ -24,8 +24,8 @@ struct alignas(64) GemmProblem {
   const float* bias;
   const __nv_bfloat16* aux;
   int64_t ld_aux;
-  // EPI_DACT + weight-stationary: per-CTA column sums of the bf16 output (the bias gradient
-  // of the layer), one fp32 row of N per CTA serving this problem (CTA order), or null.
+  // Split-K weight gradient (EPI_F32, MN-major A = dPre): column sums of A over this split's
+  // K range (the layer's bias gradient), fp32 [splits][M], or null.
   float* colsum;
   int M, N, K;
   int kb_per_split;

@@ -272,14 +272,16 @@ __global__ void __launch_bounds__(kThreads, 1) head_fused_kernel(const __grid_co
           *reinterpret_cast<uint4*>(stg + lane * 64 + ((u ^ ((lane >> 1) & 3)) << 4)) =
               make_uint4(packed[4 * u], packed[4 * u + 1], packed[4 * u + 2], packed[4 * u + 3]);
         __syncwarp();
-        float s = 0.f;  // lane = column: the 32 staged rows in row order
+        if (hn.colsum) {
+          float s = 0.f;  // lane = column: the 32 staged rows in row order
 #pragma unroll
-        for (int rr = 0; rr < 32; ++rr) {
-          const uint16_t v =
-              *reinterpret_cast<const uint16_t*>(stg + rr * 64 + (((lane >> 3) ^ ((rr >> 1) & 3)) << 4) + (lane & 7) * 2);
-          s += __uint_as_float(uint32_t(v) << 16);
+          for (int rr = 0; rr < 32; ++rr) {
+            const uint16_t v = *reinterpret_cast<const uint16_t*>(stg + rr * 64 +
+                                                                 (((lane >> 3) ^ ((rr >> 1) & 3)) << 4) + (lane & 7) * 2);
+            s += __uint_as_float(uint32_t(v) << 16);
+          }
+          csum[pass] += s;
         }
-        csum[pass] += s;
         ptx::fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
@@ -293,20 +295,23 @@ __global__ void __launch_bounds__(kThreads, 1) head_fused_kernel(const __grid_co
     }
 
     // ---- per-CTA outputs
-    // (a) bias gradient of layer L-1: combine the 4 lane quarters in order
-#pragma unroll
-    for (int pass = 0; pass < 2; ++pass) {
-      const int c = h + 4 * pass;
-      if (c * 32 < 256) red[q * 256 + c * 32 + lane] = csum[pass];
-    }
-    epi_bar();
-    if (q == 0)
+    // (a) optional bias gradient of layer L-1: combine the 4 lane quarters in order
+    if (hn.colsum) {
 #pragma unroll
       for (int pass = 0; pass < 2; ++pass) {
-        const int col = (h + 4 * pass) * 32 + lane;
-        if (col < hp) hn.colsum[(long long)cta * hp + col] = ((red[col] + red[256 + col]) + red[512 + col]) + red[768 + col];
+        const int c = h + 4 * pass;
+        if (c * 32 < 256) red[q * 256 + c * 32 + lane] = csum[pass];
       }
-    epi_bar();
+      epi_bar();
+      if (q == 0)
+#pragma unroll
+        for (int pass = 0; pass < 2; ++pass) {
+          const int col = (h + 4 * pass) * 32 + lane;
+          if (col < hp)
+            hn.colsum[(long long)cta * hp + col] = ((red[col] + red[256 + col]) + red[512 + col]) + red[768 + col];
+        }
+      epi_bar();
+    }
     // (b) head weight gradient slab: TMEM rows = hp index, columns = head outputs
     ptx::mbar_wait_sleep(fin, 0);
     ptx::tc_fence_after();

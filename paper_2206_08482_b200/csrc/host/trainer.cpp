@@ -143,7 +143,7 @@ struct Trainer::Gmi {
   std::vector<ppo::Segment> segs;
   bool fused_roll = false;
   ppo::RolloutArgs roll_args{};
-  bool fused_bias[GMI_MAX_HIDDEN] = {};  // bias gradient summed in the producing DACT GEMM
+  bool fused_bias[GMI_MAX_HIDDEN] = {};  // bias gradient summed inside the layer's dW GEMM
   bool fused_head = false;
   int head_grid = 0;
   ppo::HeadFusedArgs head_args{};
@@ -382,11 +382,12 @@ void Trainer::build_plans() {
       g.dw[l] = GemmParams{};
       for (int n = 0; n < 2; ++n) {
         g.slab[n][l] = dev((size_t)splits * out_p * in_p * 4);
-        g.colsum[n][l] = dev((size_t)ppo::colsum_blocks(g.Bm) * out_p * 4);
+        g.colsum[n][l] = dev((size_t)std::max(ppo::colsum_blocks(g.Bm), splits) * out_p * 4);
         GemmProblem p{};
         p.map_a = tma_mnmajor(g.D[n][cur], out_p, g.Bm, out_p);
         p.map_b = l == 0 ? tma_mnmajor(g.X_sh, S_p, g.B, S_p) : tma_mnmajor(g.H[n][l - 1], in_p, g.Bm, in_p);
         p.map_out = make_tma_out_f32(g.slab[n][l], in_p, out_p, splits, in_p, (uint64_t)out_p * in_p);
+        p.colsum = g.colsum[n][l];  // bias gradient of layer l: column sums of dPre_l per split
         p.M = out_p;
         p.N = in_p;
         p.K = g.Bm;
@@ -395,6 +396,7 @@ void Trainer::build_plans() {
       }
       g.dw[l].num_problems = 2;
       g.dw[l].splits = splits;
+      g.fused_bias[l] = true;
       g.flop_dw[l] = 2.0 * real * g.Bm;
 
       // input gradient dPre_{l-1} = (dPre_l W_l) * elu'(H_{l-1}); W_l read MN-major
@@ -410,7 +412,6 @@ void Trainer::build_plans() {
           p.map_out = make_tma_out_bf16(g.D[n][cur ^ 1], in_p, g.Bm, in_p);
           p.aux = g.H[n][l - 1];
           p.ld_aux = in_p;
-          p.colsum = g.ws_dx[l] ? g.colsum[n][l - 1] : nullptr;  // bias gradient of layer l-1
           p.M = g.Bm;
           p.N = in_p;
           p.K = out_p;
@@ -419,7 +420,6 @@ void Trainer::build_plans() {
         }
         g.dx[l].num_problems = 2;
         g.dx[l].splits = 1;
-        g.fused_bias[l - 1] = g.ws_dx[l];
         g.flop_dx[l] = 2.0 * real * g.Bm;
       }
     }
@@ -464,7 +464,6 @@ void Trainer::build_plans() {
         p.map_out = make_tma_out_bf16(g.D[n][0], hp, g.Bm, hp);
         p.aux = g.H[n][L - 1];
         p.ld_aux = hp;
-        p.colsum = g.ws_hdx ? g.colsum[n][L - 1] : nullptr;  // bias gradient of layer L-1
         p.M = g.Bm;
         p.N = hp;
         p.K = ppo::kHeadG;
@@ -473,7 +472,6 @@ void Trainer::build_plans() {
       }
       g.head_dx.num_problems = 2;
       g.head_dx.splits = 1;
-      g.fused_bias[L - 1] = g.ws_hdx;
     }
     // head weight gradients on the tensor cores: dW_mu = G_pi^T H_L, dw_v = G_v^T H^v_L
     const int bnh = hp <= 64 ? 64 : hp <= 128 ? 128 : 256;
@@ -517,7 +515,7 @@ void Trainer::build_plans() {
         hn.map_wm = tma_mnmajor(shadow_ + geo_.net[n][L].w, hp, hn.n_out, hp);
         hn.map_d = make_tma_out_bf16(g.D[n][0], hp, g.Bm, hp);
         hn.bias = params_ + geo_.net[n][L].b;
-        hn.colsum = g.colsum[n][L - 1];
+        hn.colsum = nullptr;  // layer L-1 bias: column sums inside its dW GEMM
         g.head_slab[n] = dev((size_t)per_net * hn.n_out * hp * 4);
         hn.dw_slab = g.head_slab[n];
       }
@@ -534,7 +532,6 @@ void Trainer::build_plans() {
       h.clip = cfg_.clip;
       h.vf_coef = cfg_.vf_coef;
       h.ent_coef = cfg_.ent_coef;
-      g.fused_bias[L - 1] = true;
       head_parts = g.head_grid;
       hslab_parts = per_net;
     }
@@ -546,8 +543,7 @@ void Trainer::build_plans() {
       for (int l = 0; l < L; ++l) {
         const Tensor& t = geo_.net[n][l];
         g.segs.push_back({g.grad + t.w, g.slab[n][l], (long long)t.out_p * t.in_p, t.out_p * t.in_p, g.dw[l].splits});
-        int parts = cb;
-        if (g.fused_bias[l]) parts = (l == L - 1 && g.fused_head) ? g.head_grid / 2 : gemm_ws_grid(g.Bm, 2, g.ctas) / 2;
+        const int parts = g.fused_bias[l] ? g.dw[l].splits : cb;
         g.segs.push_back({g.grad + t.b, g.colsum[n][l], t.out_p, t.out_p, parts});
       }
     g.segs.push_back({g.grad + geo_.net[0][L].w, g.head_slab[0], (long long)A * hp, A * hp, hslab_parts});
