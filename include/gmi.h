@@ -185,6 +185,16 @@ GMI_API int gmi_build_plan(int tpl, const gmi_topology_t* topo, int gmis_per_gpu
 typedef int (*gmi_probe_fn)(void* user, const char* bench, int gmis_per_gpu, int num_env,
                             int* runnable, double* top, double* mem);
 
+/* Measured profiler (B200): the real PPO iteration of `bench`'s catalog MLP on `device` with
+ * `gmis_per_gpu` GMIs (backend 0 streams, 1 green contexts) of `num_env` envs each, timed over
+ * `iters` graph-replayed iterations. top = per-GMI env-steps/s, mem = per-GMI device GB;
+ * shapes that cannot be built report runnable = 0 (search.hpp:32-37 semantics). */
+GMI_API int gmi_gpu_profile(const char* bench, int gmis_per_gpu, int num_env, int device, int backend,
+                            int iters, int* runnable, double* top, double* mem);
+/* gmi_probe_fn adapter over gmi_gpu_profile; user -> int[3] {device, backend, iters}. */
+GMI_API int gmi_gpu_probe(void* user, const char* bench, int gmis_per_gpu, int num_env, int* runnable,
+                          double* top, double* mem);
+
 typedef struct {
   const int* num_env_grid;
   int grid_len;

@@ -695,6 +695,26 @@ class RecordedTraceProfiler final : public Profiler {
   std::shared_ptr<void> h_;
 };
 
+/// B200 extension: the on-device Profiler the reference's explore() was written for
+/// (search.hpp:32-37) -- runs the real PPO iteration with gmis_per_gpu GMIs (green contexts
+/// by default) of num_env envs each and reports per-GMI env-steps/s and device GB.
+class GpuProfiler final : public Profiler {
+ public:
+  explicit GpuProfiler(int device = 0, int backend = 1, int iters = 3)
+      : device_(device), backend_(backend), iters_(iters) {}
+  ProfileResult profile(const std::string& bench, int gmis_per_gpu, int num_env) const override {
+    int ok = 0;
+    ProfileResult r;
+    detail::check(gmi_gpu_profile(bench.c_str(), gmis_per_gpu, num_env, device_, backend_, iters_, &ok, &r.top,
+                                  &r.mem));
+    r.runnable = ok != 0;
+    return r;
+  }
+
+ private:
+  int device_, backend_, iters_;
+};
+
 struct VisitedPoint {
   int gmis_per_gpu = 0;
   int num_env = 0;

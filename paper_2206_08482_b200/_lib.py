@@ -169,6 +169,8 @@ PROTOTYPES: dict[str, tuple] = {
     "gmi_trace_profiler_load": (ci, [C.c_char_p, P(vp)]),
     "gmi_trace_profiler_profile": (ci, [vp, C.c_char_p, ci, ci, c_int_p, c_double_p, c_double_p]),
     "gmi_trace_profiler_free": (None, [vp]),
+    "gmi_gpu_profile": (ci, [C.c_char_p, ci, ci, ci, ci, ci, c_int_p, c_double_p, c_double_p]),
+    "gmi_gpu_probe": (ci, [vp, C.c_char_p, ci, ci, c_int_p, c_double_p, c_double_p]),
     "gmi_pipeline_config_defaults": (None, [P(PipelineConfigT)]),
     "gmi_simulate_pipeline": (ci, [P(WorkloadT), P(PlanT), P(TopologyT), P(PipelineConfigT), cd,
                                    P(vp), P(PipelineMetricsT)]),

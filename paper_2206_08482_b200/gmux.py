@@ -665,6 +665,23 @@ class RecordedTraceProfiler(Profiler):
 
 
 @dataclass
+class GpuProfiler(Profiler):
+    """B200 measured profiler: runs the real PPO iteration of the benchmark's catalog MLP
+    with `gmis_per_gpu` GMIs x `num_env` envs on `device` (gmi_gpu_profile) and reports
+    per-GMI env-steps/s and per-GMI device GB -- the on-device Profiler::profile the
+    reference leaves to a synthetic model (search.hpp:32-37, 100-132)."""
+    device: int = 0
+    backend: int = 1  # 1 = SM-partitioned green contexts, 0 = streams
+    iters: int = 3
+
+    def profile(self, bench, gmis_per_gpu, num_env):
+        ok, top, mem = C.c_int(), C.c_double(), C.c_double()
+        L.check(_lib().gmi_gpu_profile(bench.encode(), gmis_per_gpu, num_env, self.device, self.backend,
+                                       self.iters, C.byref(ok), C.byref(top), C.byref(mem)))
+        return ProfileResult(bool(ok.value), top.value, mem.value)
+
+
+@dataclass
 class VisitedPoint:
     gmis_per_gpu: int
     num_env: int
