@@ -34,11 +34,11 @@ constexpr int kRows = 128;
 constexpr int kEpiWarps = 16;
 constexpr int kThreads = 64 + 32 * kEpiWarps;
 constexpr uint32_t kChunk = kRows * 128;  // [128 rows][64 bf16], SW128
-constexpr uint32_t kOffH = 0;              // H_L tile, 4 K-chunks
-constexpr uint32_t kOffG = 4 * kChunk;     // G tile [128][64] bf16 (cols >= n_out stay 0)
+constexpr uint32_t kOffH = 0;              // 2 x H_L tile (double-buffered), 4 K-chunks each
+constexpr uint32_t kOffG = 8 * kChunk;     // G tile [128][64] bf16 (cols >= n_out stay 0)
 constexpr uint32_t kOffWK = kOffG + kChunk;  // W_head K-major, per K-chunk [32 rows][128 B]
-constexpr uint32_t kOffWM = kOffWK + 4 * 4096;  // W_head MN-major, 64x64 boxes
-constexpr uint32_t kOffStg = kOffWM + 4 * 8192;  // epilogue staging, 2 KB per warp
+constexpr uint32_t kOffWM = kOffWK + 4 * 4096;  // W_head MN-major, [32 K-rows][64 cols] boxes
+constexpr uint32_t kOffStg = kOffWM + 4 * 4096;  // epilogue staging, 2 KB per warp
 constexpr uint32_t kOffRed = kOffStg + kEpiWarps * 2048;  // 4 x 256 fp32
 constexpr uint32_t kOffBar = kOffRed + 4 * 256 * 4;
 constexpr uint32_t kSmem = kOffBar + 256 + 1024;
@@ -57,13 +57,14 @@ __global__ void __launch_bounds__(kThreads, 1) head_fused_kernel(const __grid_co
   float* red = reinterpret_cast<float*>(smem + kOffRed);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kOffBar);
   uint64_t* wbar = bars;
-  uint64_t* hfull = bars + 1;
-  uint64_t* hfree = bars + 2;
-  uint64_t* acc1_full = bars + 3;
-  uint64_t* g_ready = bars + 4;
-  uint64_t* acc2_full = bars + 5;
-  uint64_t* fin = bars + 6;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 7);
+  uint64_t* hfull = bars + 1;  // [2]
+  uint64_t* hfree = bars + 3;  // [2]
+  uint64_t* acc1_full = bars + 5;
+  uint64_t* g_ready = bars + 6;
+  uint64_t* acc2_full = bars + 7;
+  uint64_t* acc2_free = bars + 8;
+  uint64_t* fin = bars + 9;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 10);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int net = blockIdx.x & 1;
@@ -74,11 +75,14 @@ __global__ void __launch_bounds__(kThreads, 1) head_fused_kernel(const __grid_co
 
   if (threadIdx.x == 0) {
     ptx::mbar_init(wbar, 1);
-    ptx::mbar_init(hfull, 1);
-    ptx::mbar_init(hfree, kEpiWarps + 1);
+    for (int b = 0; b < 2; ++b) {
+      ptx::mbar_init(&hfull[b], 1);
+      ptx::mbar_init(&hfree[b], kEpiWarps + 1);  // epilogue (elu' reads) + MMA3 commit
+    }
     ptx::mbar_init(acc1_full, 1);
     ptx::mbar_init(g_ready, 4);
     ptx::mbar_init(acc2_full, 1);
+    ptx::mbar_init(acc2_free, kEpiWarps);
     ptx::mbar_init(fin, 1);
     ptx::fence_mbar_init();
     ptx::tma_prefetch_desc(&hn.map_h);
@@ -101,16 +105,18 @@ __global__ void __launch_bounds__(kThreads, 1) head_fused_kernel(const __grid_co
   if (warp == 0) {
     // ------------------------------------------------ TMA producer
     if (lane == 0) {
-      ptx::mbar_arrive_expect_tx(wbar, uint32_t(nk) * (uint32_t(NH) * 128u + 8192u));
+      ptx::mbar_arrive_expect_tx(wbar, uint32_t(nk) * (uint32_t(NH) * 128u + 4096u));
       for (int kc = 0; kc < nk; ++kc) {
         ptx::tma_load_2d(sWK + kc * 4096, &hn.map_wk, wbar, kc * 64, 0);
-        ptx::tma_load_2d(sWM + kc * 8192, &hn.map_wm, wbar, kc * 64, 0);
+        ptx::tma_load_2d(sWM + kc * 4096, &hn.map_wm, wbar, kc * 64, 0);
       }
       int it = 0;
       for (int j = cta; j < mtiles; j += ctas, ++it) {
-        if (it > 0) ptx::mbar_wait_sleep(hfree, (it - 1) & 1);
-        ptx::mbar_arrive_expect_tx(hfull, uint32_t(nk) * kChunk);
-        for (int kc = 0; kc < nk; ++kc) ptx::tma_load_2d(sH + kc * kChunk, &hn.map_h, hfull, kc * 64, j * kRows);
+        const int b = it & 1;
+        if (it >= 2) ptx::mbar_wait_sleep(&hfree[b], ((it >> 1) - 1) & 1);
+        ptx::mbar_arrive_expect_tx(&hfull[b], uint32_t(nk) * kChunk);
+        for (int kc = 0; kc < nk; ++kc)
+          ptx::tma_load_2d(sH + (b * 4 + kc) * kChunk, &hn.map_h, &hfull[b], kc * 64, j * kRows);
       }
     }
   } else if (warp == 1) {
@@ -120,11 +126,13 @@ __global__ void __launch_bounds__(kThreads, 1) head_fused_kernel(const __grid_co
       const uint32_t idesc1 = ptx::umma_idesc_bf16(kRows, uint32_t(NH), 0, 0);
       const uint32_t idesc2 = ptx::umma_idesc_bf16(kRows, uint32_t((hp + 15) / 16 * 16), 0, 1);
       const uint32_t idesc3 = ptx::umma_idesc_bf16(kRows, uint32_t(NH), 1, 1);
-      const uint32_t h0 = ptx::smem_u32(sH), g0 = ptx::smem_u32(sG);
+      const uint32_t g0 = ptx::smem_u32(sG);
       const uint32_t wk0 = ptx::smem_u32(sWK), wm0 = ptx::smem_u32(sWM);
       int it = 0;
       for (int j = cta; j < mtiles; j += ctas, ++it) {
-        ptx::mbar_wait(hfull, it & 1);
+        const int b = it & 1;
+        const uint32_t h0 = ptx::smem_u32(sH + b * 4 * kChunk);
+        ptx::mbar_wait(&hfull[b], (it >> 1) & 1);
         ptx::tc_fence_after();
         // MMA1: [128 x NH] = H . W_head^T (K = hp)
         for (int kc = 0; kc < nk; ++kc) {
@@ -136,11 +144,12 @@ __global__ void __launch_bounds__(kThreads, 1) head_fused_kernel(const __grid_co
         }
         ptx::mma_commit(acc1_full);
         ptx::mbar_wait(g_ready, it & 1);
+        if (it > 0) ptx::mbar_wait(acc2_free, (it - 1) & 1);  // previous tile's elu' epilogue drained acc2
         ptx::tc_fence_after();
         // MMA2: [128 x hp] = G . W_head (K = NH; W_head read MN-major)
         for (int k = 0; k < NH / 16; ++k)
           ptx::mma_bf16(tmem + kTmemAcc2, ptx::umma_desc_sw128(g0 + k * 32, 16, 1024),
-                        ptx::umma_desc_sw128(wm0 + k * 2048, 8192, 1024), idesc2, k > 0 ? 1u : 0u);
+                        ptx::umma_desc_sw128(wm0 + k * 2048, 4096, 1024), idesc2, k > 0 ? 1u : 0u);
         ptx::mma_commit(acc2_full);
         // MMA3: dW_head^T[hp x NH] += H^T . G (K = tile rows; both operands MN-major views)
         for (int half = 0; half * 128 < hp; ++half)
@@ -149,7 +158,7 @@ __global__ void __launch_bounds__(kThreads, 1) head_fused_kernel(const __grid_co
                           ptx::umma_desc_sw128(h0 + 2 * half * kChunk + k * 2048, kChunk, 1024),
                           ptx::umma_desc_sw128(g0 + k * 2048, 8192, 1024), idesc3,
                           (it > 0 || k > 0) ? 1u : 0u);
-        ptx::mma_commit(hfree);
+        ptx::mma_commit(&hfree[b]);
       }
       ptx::mma_commit(fin);
     }
@@ -170,7 +179,23 @@ __global__ void __launch_bounds__(kThreads, 1) head_fused_kernel(const __grid_co
       const int grow = j * kRows + row;
       const bool valid = grow < a.Bm;
       if (h == 0) {
-        // ---- per-row loss (thread = row): TMEM lane quarter q
+        // ---- per-row loss (thread = row): TMEM lane quarter q. The row's stored action, old
+        // log-prob, advantage and return are fetched before the accumulator wait so their
+        // latency overlaps the head MMA.
+        const long long rr = a.row0 + grow;
+        float act_r[MAXA];
+        float oldlp = 0.f, adv = 0.f, ret = 0.f;
+        if (valid) {
+          if (net == 0) {
+#pragma unroll
+            for (int i = 0; i < MAXA; ++i)
+              if (i < nout) act_r[i] = a.act[rr * nout + i];
+            oldlp = a.oldlp[rr];
+            adv = a.adv[rr];
+          } else {
+            ret = a.ret[rr];
+          }
+        }
         ptx::mbar_wait_sleep(acc1_full, it & 1);
         ptx::tc_fence_after();
         uint32_t r[32];
@@ -187,7 +212,6 @@ __global__ void __launch_bounds__(kThreads, 1) head_fused_kernel(const __grid_co
 #pragma unroll
           for (int i = 0; i < MAXA; ++i) gmu[i] = 0.f;
           if (valid) {
-            const long long rr = a.row0 + grow;
             float mu[MAXA], z[MAXA], sig[MAXA], ls[MAXA];
             float lp = 0.f;
 #pragma unroll
@@ -196,10 +220,9 @@ __global__ void __launch_bounds__(kThreads, 1) head_fused_kernel(const __grid_co
                 mu[i] = __uint_as_float(r[i]) + hn.bias[i];
                 ls[i] = a.log_std[i];
                 sig[i] = expf(ls[i]);
-                z[i] = (a.act[rr * A + i] - mu[i]) / sig[i];
+                z[i] = (act_r[i] - mu[i]) / sig[i];
                 lp += -0.5f * z[i] * z[i] - ls[i] - kLog2PiHalf;
               }
-            const float oldlp = a.oldlp[rr], adv = a.adv[rr];
             const float ratio = expf(lp - oldlp);
             const float s1 = ratio * adv;
             const float rc = fminf(fmaxf(ratio, 1.f - a.clip), 1.f + a.clip);
@@ -223,9 +246,8 @@ __global__ void __launch_bounds__(kThreads, 1) head_fused_kernel(const __grid_co
         } else {
           float gv = 0.f;
           if (valid) {
-            const long long rr = a.row0 + grow;
             const float v = __uint_as_float(r[0]) + hn.bias[0];
-            const float verr = v - a.ret[rr];
+            const float verr = v - ret;
             gv = a.vf_coef * verr * invB;
             sg[0] += gv;
             st[1] += 0.5f * a.vf_coef * verr * verr;
@@ -248,7 +270,7 @@ __global__ void __launch_bounds__(kThreads, 1) head_fused_kernel(const __grid_co
         uint32_t r[32];
         ptx::tmem_ld_32x32b_x32(tmem + kTmemAcc2 + (static_cast<uint32_t>(q * 32) << 16) + c * 32, r);
         // H_L row `row`, columns 32c..32c+31: 4 x 16 B from the swizzled operand tile
-        const uint8_t* hrow = sH + (c >> 1) * kChunk + row * 128;
+        const uint8_t* hrow = sH + ((it & 1) * 4 + (c >> 1)) * kChunk + row * 128;
         uint4 hv[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u)
@@ -291,7 +313,10 @@ __global__ void __launch_bounds__(kThreads, 1) head_fused_kernel(const __grid_co
       }
       ptx::tc_fence_before();
       __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(hfree);
+      if (lane == 0) {
+        ptx::mbar_arrive(acc2_free);
+        ptx::mbar_arrive(&hfree[it & 1]);
+      }
     }
 
     // ---- per-CTA outputs

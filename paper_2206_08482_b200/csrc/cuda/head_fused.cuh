@@ -11,7 +11,7 @@ namespace gmi::ppo {
 struct HeadNet {
   CUtensorMap map_h;   // H_L [Bm][hp] bf16, box {64, 128}, SW128
   CUtensorMap map_wk;  // head weights [n_out][hp] K-major, box {64, nh}, SW128 (rows >= n_out zero)
-  CUtensorMap map_wm;  // same weights viewed [K = n_out rows][N = hp], box {64, 64}, SW128
+  CUtensorMap map_wm;  // same weights viewed [K = n_out rows][N = hp], box {64, 32}, SW128
   CUtensorMap map_d;   // dPre_{L-1} out [Bm][hp] bf16, box {32, 32}, SW64
   const float* bias;   // head bias [n_out]
   float* colsum;       // [ctas per net][hp]  bias gradient of layer L-1

@@ -512,7 +512,7 @@ void Trainer::build_plans() {
         hn.nh = hn.n_out <= 16 ? 16 : 32;
         hn.map_h = tma_kmajor(g.H[n][L - 1], hp, g.Bm, hp, kGemmBlockM);
         hn.map_wk = tma_kmajor(shadow_ + geo_.net[n][L].w, hp, hn.n_out, hp, hn.nh);
-        hn.map_wm = tma_mnmajor(shadow_ + geo_.net[n][L].w, hp, hn.n_out, hp);
+        hn.map_wm = make_tma_2d_bf16(shadow_ + geo_.net[n][L].w, hp, hn.n_out, hp, 64, 32);  // [32 K][64 N]
         hn.map_d = make_tma_out_bf16(g.D[n][0], hp, g.Bm, hp);
         hn.bias = params_ + geo_.net[n][L].b;
         hn.colsum = nullptr;  // layer L-1 bias: column sums inside its dW GEMM
