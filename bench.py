@@ -114,6 +114,16 @@ def measured_peaks():
         return 1400.0, 6650.0, "fallback (B200_PROFILING.md)"
 
 
+def gemm_traffic():
+    """dram__bytes_read.sum + dram__bytes_write.sum per gemm_tcgen05_kernel launch, from the
+    committed ncu --set full capture (profiles/traffic.json); None when absent."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            return json.load(f)["gemm_tcgen05_kernel"]["dram_bytes_per_launch"]
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 GEMM_PHASES = ("roll_gemm", "roll_head", "val_gemm", "val_head", "fwd_gemm", "head_fwd", "head_dx", "head_dw",
                "dw_gemm", "dx_gemm")
 
@@ -292,7 +302,9 @@ def main():
                        "cuda_graph": bool(cfg.use_graph)},
             "roofline": {"bound": "tensor", "kernel": "gemm_tcgen05_kernel (every MLP GEMM of GMI 0, all phases)",
                          "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
-                         "frac": achieved / peak_tf, "traffic": None, "peak_source": peak_src,
+                         "frac": achieved / peak_tf, "traffic": gemm_traffic(),
+                         "traffic_unit": "DRAM bytes per launch (ncu, profiles/traffic.json)",
+                         "peak_source": peak_src,
                          "gemm_share_of_step": gemm_ms / iter_ms_instr if iter_ms_instr else None,
                          "instrumented_ms_per_step": iter_ms_instr},
             "phases": phase_table(prof, iter_ms_instr, peak_tf, peak_gbs),
