@@ -70,7 +70,7 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
 template <int BN, int EPI, int WS>
 struct GemmSmem {
   static constexpr int kEpiWarps = gemm_epi_warps(EPI);
-  static constexpr int kStages = WS ? 3 : (BN == 256 ? 3 : 4);
+  static constexpr int kStages = WS ? 4 : (BN == 256 ? 3 : 4);
   static constexpr uint32_t kA = kGemmBlockM * kGemmBlockK * 2;  // 16 KB
   static constexpr uint32_t kB = BN * kGemmBlockK * 2;           // one k-block of B
   static constexpr uint32_t kStage = WS ? kA : kA + kB;
@@ -176,11 +176,6 @@ __global__ void __launch_bounds__(gemm_threads(EPI) + 128 * CS, 1)
           ptx::tma_load_2d(sb, &pr.map_b, bar, k0, n0 + pr.b_row0);
         }
       };
-      if constexpr (WS) {  // this CTA's problem: whole B once
-        const GemmProblem& pr = P.prob[blockIdx.x % P.num_problems];
-        ptx::mbar_arrive_expect_tx(bres_bar, nkb_total * L::kB);
-        for (int j = 0; j < nkb_total; ++j) load_b(pr, b_res + j * L::kB, bres_bar, 0, j * kGemmBlockK);
-      }
       int it = 0;
       for (int tile = blockIdx.x; tile < ntile_total; tile += gridDim.x) {
         int prob, split, m0, n0, kb0, nkb;
@@ -191,7 +186,11 @@ __global__ void __launch_bounds__(gemm_threads(EPI) + 128 * CS, 1)
           if (it >= S) ptx::mbar_wait(&empty_bar[s], ((it / S) - 1) & 1);
           uint8_t* sa = smem + s * L::kStage;
           const int k0 = (kb0 + i) * kGemmBlockK;
-          ptx::mbar_arrive_expect_tx(&full_bar[s], L::kStage);
+          // WS: the CTA's first tile also brings the resident B k-block i on the same barrier,
+          // so the first MMAs start after one k-block instead of after the whole weight tile.
+          const bool first_ws = WS && it < nkb_total;
+          ptx::mbar_arrive_expect_tx(&full_bar[s], L::kStage + (first_ws ? L::kB : 0u));
+          if (first_ws) load_b(pr, b_res + i * L::kB, &full_bar[s], 0, k0);
           if constexpr (A_MN) {
 #pragma unroll
             for (int j = 0; j < kGemmBlockM / 64; ++j)
@@ -207,7 +206,6 @@ __global__ void __launch_bounds__(gemm_threads(EPI) + 128 * CS, 1)
     // ---------------- MMA issuer (one lane), double-buffered TMEM accumulators
     if (lane == 0) {
       int it = 0, lt = 0;
-      if constexpr (WS) ptx::mbar_wait(bres_bar, 0);
       for (int tile = blockIdx.x; tile < ntile_total; tile += gridDim.x, ++lt) {
         int prob, split, m0, n0, kb0, nkb;
         decode(tile, prob, split, m0, n0, kb0, nkb);

@@ -401,7 +401,9 @@ void Trainer::build_plans() {
 
       // input gradient dPre_{l-1} = (dPre_l W_l) * elu'(H_{l-1}); W_l read MN-major
       if (l > 0) {
-        const int ws_dx = gemm_ws_bn(g.Bm, in_p, out_p, 2, g.ctas);
+        // input gradients stream W with the dPre tiles: measured faster than weight-stationary here
+        // (the elu' operand already doubles the activation traffic; WS has one staging buffer)
+        const int ws_dx = std::getenv("GMI_DX_WS") ? gemm_ws_bn(g.Bm, in_p, out_p, 2, g.ctas) : 0;
         g.ws_dx[l] = ws_dx > 0;
         g.bn_dx[l] = ws_dx > 0 ? ws_dx : gemm_choose_bn(g.Bm, in_p, 2, 1, g.ctas);
         g.dx[l] = GemmParams{};
