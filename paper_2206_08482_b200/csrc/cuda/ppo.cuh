@@ -81,6 +81,20 @@ struct Segment {  // dst[i] = sum_{p < nparts} src[p * stride + i]  (fixed order
   long long stride;
   int len;
   int nparts;
+  long long param_off = -1;  // >= 0: dst[i] is the gradient of parameter param_off + i (fused Adam)
+};
+
+// Adam applied by the gradient-assembly kernel right after an element's gradient is summed
+// (single GMI, single GPU: no cross-GMI fold or all-reduce sits in between).
+struct SegAdam {
+  float* p;
+  float* m;
+  float* v;
+  __nv_bfloat16* shadow;
+  const float* bc;  // [2*steps] bias corrections
+  const Control* ctl;
+  int step_in_iter;
+  float lr, b1, b2, eps, inv_n;
 };
 
 struct AdamArgs {
@@ -115,7 +129,7 @@ int head_loss_blocks(int B);
 void launch_colsum(const __nv_bfloat16* const* D, const int* widths, float* const* partial,
                    int nproblems, int rows, cudaStream_t s);
 int colsum_blocks(int rows);
-void launch_segments(const Segment* segs, int nsegs, cudaStream_t s);
+void launch_segments(const Segment* segs, int nsegs, cudaStream_t s, const SegAdam* adam = nullptr);
 void launch_adam(const AdamArgs& a, cudaStream_t s);
 
 }  // namespace gmi::ppo

@@ -149,6 +149,8 @@ struct SegmentTable {
   Segment s[kMaxSegments];
   int first_block[kMaxSegments + 1];  // prefix of blocks per segment
   int nseg;
+  int has_adam;
+  SegAdam adam;
 };
 __global__ void __launch_bounds__(256) segments_kernel(const __grid_constant__ SegmentTable t) {
   __shared__ float4 acc_s[8][32];
@@ -213,6 +215,30 @@ __global__ void __launch_bounds__(256) segments_kernel(const __grid_constant__ S
       const float o[4] = {s.x, s.y, s.z, s.w};
       for (int c = 0; c < 4 && i0 + c < sg.len; ++c) sg.dst[i0 + c] = o[c];
     }
+    if (t.has_adam) acc_s[0][lane] = s;  // hand the block's 128 sums to 128 Adam threads
+  }
+  if (t.has_adam && sg.param_off >= 0) {  // fused Adam, same arithmetic as adam_kernel
+    __syncthreads();
+    const int e = threadIdx.x;  // element of this block
+    const int ie = (blockIdx.x - t.first_block[si]) * kSegElems + e;
+    if (e < kSegElems && ie < sg.len) {
+      const SegAdam& a = t.adam;
+      const long long st = a.ctl->adam_step0 + a.step_in_iter;
+      const float bc1 = a.bc[2 * st], bc2 = a.bc[2 * st + 1];
+      const float ob1 = __fsub_rn(1.0f, a.b1), ob2 = __fsub_rn(1.0f, a.b2);
+      const float4 s4 = acc_s[0][e >> 2];
+      const float gs = (e & 3) == 0 ? s4.x : (e & 3) == 1 ? s4.y : (e & 3) == 2 ? s4.z : s4.w;
+      const long long i = sg.param_off + ie;
+      const float g = __fmul_rn(gs, a.inv_n);
+      const float m = __fadd_rn(__fmul_rn(a.b1, a.m[i]), __fmul_rn(ob1, g));
+      const float v = __fadd_rn(__fmul_rn(a.b2, a.v[i]), __fmul_rn(__fmul_rn(ob2, g), g));
+      a.m[i] = m;
+      a.v[i] = v;
+      const float mh = __fdiv_rn(m, bc1), vh = __fdiv_rn(v, bc2);
+      const float p = __fsub_rn(a.p[i], __fmul_rn(a.lr, __fdiv_rn(mh, __fadd_rn(__fsqrt_rn(vh), a.eps))));
+      a.p[i] = p;
+      a.shadow[i] = __float2bfloat16_rn(p);
+    }
   }
 }
 
@@ -248,11 +274,13 @@ void launch_colsum(const __nv_bfloat16* const* D, const int* widths, float* cons
   launch_pdl(colsum_kernel, dim3(colsum_blocks(rows), np), dim3(256), 0, s, a, rows);
 }
 
-void launch_segments(const Segment* segs, int n, cudaStream_t s) {
+void launch_segments(const Segment* segs, int n, cudaStream_t s, const SegAdam* adam) {
   for (int base = 0; base < n; base += kMaxSegments) {
     SegmentTable t{};
     const int m = std::min(kMaxSegments, n - base);
     t.nseg = m;
+    t.has_adam = adam != nullptr;
+    if (adam) t.adam = *adam;
     t.first_block[0] = 0;
     for (int i = 0; i < m; ++i) {
       t.s[i] = segs[base + i];

@@ -59,7 +59,7 @@ class Trainer {
   void record_iteration();  // the launch sequence of one iteration (eager or under capture)
   void rollout(Gmi& g);
   void values(Gmi& g);
-  void train_minibatch(Gmi& g, int k);
+  void train_minibatch(Gmi& g, int k, int adam_step = -1);  // adam_step >= 0: fused Adam
   void reduce_and_step(int k);
   void gemm(Gmi& g, int phase, const GemmParams& P, int bn, int amn, int bmn, int epi, double flop, int ws = 0);
   // Runs f (which enqueues work on s); with cfg.instrument and s = GMI 0's stream or the
