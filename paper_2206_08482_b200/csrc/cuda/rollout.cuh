@@ -38,5 +38,9 @@ struct RolloutArgs {
 // Whether the fused rollout supports this MLP (hidden widths <= 256, <= 4 layers, S_p <= 256, A <= 31).
 bool rollout_fusable(int L, const int* widths_p, int S_p, int A);
 void launch_rollout(const RolloutArgs& a, cudaStream_t s);
+// Cluster variant (rollout_cluster.cu): returns the CTAs per 128-env tile (0 = not applicable).
+// map_w[l] must then be built with 64-row boxes (hidden slices) and map_w[L] with 16-row boxes.
+int rollout_cluster_size(int L, const int* widths_p, int S_p, int A, int N);
+void launch_rollout_cluster(const RolloutArgs& a, int C, cudaStream_t s);
 
 }  // namespace gmi::ppo

@@ -38,6 +38,8 @@ GmiResources::GmiResources(int device, int count, int backend, int sm_per_gmi) :
       cudaStream_t s;
       GMI_CUDA_CHECK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
       streams_.push_back(s);
+      GMI_CUDA_CHECK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+      aux_.push_back(s);
       sms_.push_back(0);
     }
     return;
@@ -80,12 +82,15 @@ GmiResources::GmiResources(int device, int count, int backend, int sm_per_gmi) :
     cu_check(cuGreenCtxStreamCreate_(&s, g, CU_STREAM_NON_BLOCKING, 0), "cuGreenCtxStreamCreate");
     green_.push_back(g);
     streams_.push_back(reinterpret_cast<cudaStream_t>(s));
+    cu_check(cuGreenCtxStreamCreate_(&s, g, CU_STREAM_NON_BLOCKING, 0), "cuGreenCtxStreamCreate");
+    aux_.push_back(reinterpret_cast<cudaStream_t>(s));
     sms_.push_back(int(groups[i].sm.smCount));
   }
 }
 
 GmiResources::~GmiResources() {
   for (auto s : streams_) cudaStreamDestroy(s);
+  for (auto s : aux_) cudaStreamDestroy(s);
   if (!green_.empty()) {
     using Destroy = CUresult (*)(CUgreenCtx);
     void* p = nullptr;

@@ -12,12 +12,15 @@ class GmiResources {
   GmiResources(int device, int count, int backend, int sm_per_gmi);
   ~GmiResources();
   cudaStream_t stream(int i) const { return streams_[i]; }
+  // second stream of the same GMI (same SM partition): independent branches of the
+  // iteration (e.g. weight- and input-gradient GEMMs of a layer) run on it concurrently
+  cudaStream_t aux_stream(int i) const { return aux_[i]; }
   int sm_count(int i) const { return sms_[i]; }
   int backend() const { return backend_; }
 
  private:
   int backend_;
-  std::vector<cudaStream_t> streams_;
+  std::vector<cudaStream_t> streams_, aux_;
   std::vector<void*> green_;
   std::vector<int> sms_;
 };

@@ -114,6 +114,8 @@ struct Trainer::Gmi {
   int local = 0, gid = 0, env0 = 0, N = 0, B = 0, Bm = 0, Mrows = 0, ctas = 0;
   cudaStream_t s = nullptr;
   cudaEvent_t ev_done = nullptr;
+  cudaStream_t s2 = nullptr;  // second stream of the GMI (backward branch parallelism)
+  cudaEvent_t ev_fork = nullptr, ev_d[GMI_MAX_HIDDEN] = {};
   float* x = nullptr;
   int *ep_step = nullptr, *ep_len = nullptr, *ep_count = nullptr;
   __nv_bfloat16* X_roll = nullptr;
@@ -124,7 +126,7 @@ struct Trainer::Gmi {
   __nv_bfloat16* X_sh = nullptr;
   float *act_sh = nullptr, *oldlp_sh = nullptr, *adv_sh = nullptr, *ret_sh = nullptr;
   __nv_bfloat16* H[2][GMI_MAX_HIDDEN] = {};
-  __nv_bfloat16* D[2][2] = {};
+  __nv_bfloat16* D[2][GMI_MAX_HIDDEN] = {};  // dPre_l per layer (bf16 [Bm][w_p])
   __nv_bfloat16 *Gpi = nullptr, *Gv = nullptr;
   float* outh[2] = {};  // [Mrows][64] fp32 head outputs: mu (policy), v in column 0 (value)
   float* slab[2][GMI_MAX_HIDDEN] = {};
@@ -142,6 +144,7 @@ struct Trainer::Gmi {
          flop_dx[GMI_MAX_HIDDEN] = {}, flop_head = 0;
   std::vector<ppo::Segment> segs;
   bool fused_roll = false;
+  int roll_cluster = 0;  // > 0: cluster rollout with this many CTAs per 128-env tile
   ppo::RolloutArgs roll_args{};
   bool fused_bias[GMI_MAX_HIDDEN] = {};  // bias gradient summed inside the layer's dW GEMM
   bool fused_head = false;
@@ -160,6 +163,12 @@ Trainer::Trainer(const gmi_ppo_config_t& cfg, const void* nccl_id) : cfg_(cfg) {
   if (geo_.S > 256) invalid("obs_dim > 256 unsupported");
   if (geo_.wp[geo_.L] > ppo::kMaxHeadIn) invalid("last hidden width > 512 unsupported");
   T_ = cfg.horizon;
+  {
+    const char* par = std::getenv("GMI_BWD_PAR");  // "0" disables backward branch parallelism
+    bwd_par_ = !(par && par[0] == '0');
+    const char* share = std::getenv("GMI_BWD_DX_SHARE");  // percent of the GMI's SMs for dx
+    if (share) bwd_dx_share_ = std::max(10, std::min(90, std::atoi(share)));
+  }
   K_ = cfg.minibatches;
   n_local_ = cfg.gmis_per_gpu;
   n_total_ = cfg.num_gpus * cfg.gmis_per_gpu;
@@ -182,8 +191,11 @@ Trainer::Trainer(const gmi_ppo_config_t& cfg, const void* nccl_id) : cfg_(cfg) {
     if (g->Bm % 64 != 0) invalid("minibatch rows per GMI must be a multiple of 64 (use envs per GMI % 8 == 0)");
     g->Mrows = std::max(g->Bm, g->N);
     g->s = exec_->stream(i);
+    g->s2 = exec_->aux_stream(i);
     g->ctas = exec_->sm_count(i) > 0 ? exec_->sm_count(i) : sms;
     GMI_CUDA_CHECK(cudaEventCreateWithFlags(&g->ev_done, cudaEventDisableTiming));
+    GMI_CUDA_CHECK(cudaEventCreateWithFlags(&g->ev_fork, cudaEventDisableTiming));
+    for (auto& e : g->ev_d) GMI_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     gmis_.push_back(std::move(g));
   }
   alloc();
@@ -214,7 +226,11 @@ Trainer::~Trainer() {
     cudaEventDestroy(m.a);
     cudaEventDestroy(m.b);
   }
-  for (auto& g : gmis_) cudaEventDestroy(g->ev_done);
+  for (auto& g : gmis_) {
+    cudaEventDestroy(g->ev_done);
+    cudaEventDestroy(g->ev_fork);
+    for (auto e : g->ev_d) cudaEventDestroy(e);
+  }
   if (ev_adam_) cudaEventDestroy(ev_adam_);
   if (ev_start_) cudaEventDestroy(ev_start_);
   if (upd_) cudaStreamDestroy(upd_);
@@ -274,7 +290,7 @@ void Trainer::alloc() {
     g.ret_sh = static_cast<float*>(dev(B * 4));
     for (int n = 0; n < 2; ++n) {
       for (int l = 0; l < L; ++l) g.H[n][l] = static_cast<__nv_bfloat16*>(dev((long long)g.Mrows * geo_.wp[l + 1] * 2));
-      for (int j = 0; j < 2; ++j) g.D[n][j] = static_cast<__nv_bfloat16*>(dev((long long)g.Bm * maxw * 2));
+      for (int l = 0; l < L; ++l) g.D[n][l] = static_cast<__nv_bfloat16*>(dev((long long)g.Bm * maxw * 2));
     }
     g.Gpi = static_cast<__nv_bfloat16*>(dev((long long)g.Bm * ppo::kHeadG * 2));
     g.Gv = static_cast<__nv_bfloat16*>(dev((long long)g.Bm * ppo::kHeadG * 2));
@@ -374,7 +390,6 @@ void Trainer::build_plans() {
       g.flop_fwd[l] = 2.0 * real * g.Bm;
 
       // weight gradient dW_l[out_p][in_p] = sum_rows dPre_l^T in_l (both operands MN-major)
-      const int cur = (L - 1 - l) & 1;
       const int bnw = in_p <= 64 ? 64 : in_p <= 128 ? 128 : 256;  // instantiated block widths
       g.bn_dw[l] = bnw;
       int splits = 1, kbps = 1;
@@ -384,7 +399,7 @@ void Trainer::build_plans() {
         g.slab[n][l] = dev((size_t)splits * out_p * in_p * 4);
         g.colsum[n][l] = dev((size_t)std::max(ppo::colsum_blocks(g.Bm), splits) * out_p * 4);
         GemmProblem p{};
-        p.map_a = tma_mnmajor(g.D[n][cur], out_p, g.Bm, out_p);
+        p.map_a = tma_mnmajor(g.D[n][l], out_p, g.Bm, out_p);
         p.map_b = l == 0 ? tma_mnmajor(g.X_sh, S_p, g.B, S_p) : tma_mnmajor(g.H[n][l - 1], in_p, g.Bm, in_p);
         p.map_out = make_tma_out_f32(g.slab[n][l], in_p, out_p, splits, in_p, (uint64_t)out_p * in_p);
         p.colsum = g.colsum[n][l];  // bias gradient of layer l: column sums of dPre_l per split
@@ -409,9 +424,9 @@ void Trainer::build_plans() {
         g.dx[l] = GemmParams{};
         for (int n = 0; n < 2; ++n) {
           GemmProblem p{};
-          p.map_a = tma_kmajor(g.D[n][cur], out_p, g.Bm, out_p, kGemmBlockM);
+          p.map_a = tma_kmajor(g.D[n][l], out_p, g.Bm, out_p, kGemmBlockM);
           p.map_b = tma_mnmajor(shadow_ + geo_.net[n][l].w, in_p, out_p, in_p);
-          p.map_out = make_tma_out_bf16(g.D[n][cur ^ 1], in_p, g.Bm, in_p);
+          p.map_out = make_tma_out_bf16(g.D[n][l - 1], in_p, g.Bm, in_p);
           p.aux = g.H[n][l - 1];
           p.ld_aux = in_p;
           p.M = g.Bm;
@@ -463,7 +478,7 @@ void Trainer::build_plans() {
         GemmProblem p{};
         p.map_a = tma_kmajor(G[n], ppo::kHeadG, g.Bm, ppo::kHeadG, kGemmBlockM);
         p.map_b = tma_mnmajor(shadow_ + geo_.net[n][L].w, hp, head_rows[n], hp);
-        p.map_out = make_tma_out_bf16(g.D[n][0], hp, g.Bm, hp);
+        p.map_out = make_tma_out_bf16(g.D[n][L - 1], hp, g.Bm, hp);
         p.aux = g.H[n][L - 1];
         p.ld_aux = hp;
         p.M = g.Bm;
@@ -515,7 +530,7 @@ void Trainer::build_plans() {
         hn.map_h = tma_kmajor(g.H[n][L - 1], hp, g.Bm, hp, kGemmBlockM);
         hn.map_wk = tma_kmajor(shadow_ + geo_.net[n][L].w, hp, hn.n_out, hp, hn.nh);
         hn.map_wm = make_tma_2d_bf16(shadow_ + geo_.net[n][L].w, hp, hn.n_out, hp, 64, 32);  // [32 K][64 N]
-        hn.map_d = make_tma_out_bf16(g.D[n][0], hp, g.Bm, hp);
+        hn.map_d = make_tma_out_bf16(g.D[n][L - 1], hp, g.Bm, hp);
         hn.bias = params_ + geo_.net[n][L].b;
         hn.colsum = nullptr;  // layer L-1 bias: column sums inside its dW GEMM
         g.head_slab[n] = dev((size_t)per_net * hn.n_out * hp * 4);
@@ -572,6 +587,16 @@ void Trainer::build_plans() {
       }
       const int head_n = A <= 16 ? 16 : 32;
       r.map_w[L] = tma_kmajor(shadow_ + geo_.net[0][L].w, hp, A, hp, head_n);
+      // cluster variant: 64-row weight slices per CTA, 16-row head (rollout_cluster.cu)
+      const char* nocl = std::getenv("GMI_ROLLOUT_NOCLUSTER");
+      g.roll_cluster = (nocl && nocl[0] == '1') ? 0 : ppo::rollout_cluster_size(L, geo_.wp.data(), S_p, A, g.N);
+      if (g.roll_cluster) {
+        for (int l = 0; l < L; ++l) {
+          const Tensor& t = geo_.net[0][l];
+          r.map_w[l] = tma_kmajor(shadow_ + t.w, t.in_p, t.out_p, t.in_p, 64);
+        }
+        r.map_w[L] = tma_kmajor(shadow_ + geo_.net[0][L].w, hp, A, hp, 16);
+      }
       r.bias[L] = params_ + geo_.net[0][L].b;
       r.in_p[L] = hp;
       r.out_n[L] = head_n;
@@ -603,7 +628,7 @@ void Trainer::build_plans() {
 // ------------------------------------------------------------------ launch helpers
 template <class F>
 void Trainer::timed(cudaStream_t s, int phase, double flop, double bytes, F&& f) {
-  const bool on = cfg_.instrument && (s == upd_ || s == gmis_[0]->s);
+  const bool on = cfg_.instrument && (s == upd_ || s == gmis_[0]->s || s == gmis_[0]->s2);
   if (!on) {
     f();
     return;
@@ -626,8 +651,10 @@ void Trainer::timed(cudaStream_t s, int phase, double flop, double bytes, F&& f)
   m.bytes = bytes;
 }
 
-void Trainer::gemm(Gmi& g, int phase, const GemmParams& P, int bn, int amn, int bmn, int epi, double flop, int ws) {
-  timed(g.s, phase, flop, 0.0, [&] { gemm_launch(P, bn, amn, bmn, epi, g.s, g.ctas, ws); });
+void Trainer::gemm(Gmi& g, int phase, const GemmParams& P, int bn, int amn, int bmn, int epi, double flop, int ws,
+                   cudaStream_t stream, int ctas) {
+  cudaStream_t st = stream ? stream : g.s;
+  timed(st, phase, flop, 0.0, [&] { gemm_launch(P, bn, amn, bmn, epi, st, ctas > 0 ? ctas : g.ctas, ws); });
   ++launches_;
 }
 
@@ -684,7 +711,12 @@ void Trainer::rollout(Gmi& g) {
   if (g.fused_roll) {  // whole rollout in one persistent kernel (cuda/rollout.cu)
     double flop = 2.0 * geo_.A * geo_.width[L] * g.N;
     for (int l = 0; l < L; ++l) flop += g.flop_roll[l];
-    timed(g.s, GMI_PH_ROLL_GEMM, flop * T_, 0.0, [&] { ppo::launch_rollout(g.roll_args, g.s); });
+    timed(g.s, GMI_PH_ROLL_GEMM, flop * T_, 0.0, [&] {
+      if (g.roll_cluster)
+        ppo::launch_rollout_cluster(g.roll_args, g.roll_cluster, g.s);
+      else
+        ppo::launch_rollout(g.roll_args, g.s);
+    });
     ++launches_;
     return;
   }
@@ -782,13 +814,33 @@ void Trainer::train_minibatch(Gmi& g, int k, int adam_step) {
     gemm(g, GMI_PH_HEAD_DX, g.head_dx, g.bn_hdx, 0, 1, EPI_DACT, hflop, g.ws_hdx);
     gemm(g, GMI_PH_HEAD_DW, g.dhead, g.bn_head, 1, 1, EPI_F32, g.flop_head);
   }
-  for (int l = L - 1; l >= 0; --l) {
+  // Backward branch parallelism: the input-gradient chain dx(L-1) -> ... -> dx(1) runs on the
+  // GMI's second stream while the weight-gradient GEMMs dW(l) follow on the main stream as soon
+  // as their dPre_l is ready (per-layer dPre buffers, so there is no write-after-read hazard).
+  // Each branch gets its own share of the GMI's SMs (GMI_BWD_SPLIT=dx_ctas,dw_ctas to tune).
+  bool par = bwd_par_;
+  for (int l = 0; l < L; ++l) par = par && g.fused_bias[l];
+  if (par && L > 1) {
+    const int dx_ctas = std::max(1, g.ctas * bwd_dx_share_ / 100), dw_ctas = std::max(1, g.ctas - dx_ctas);
+    GMI_CUDA_CHECK(cudaEventRecord(g.ev_fork, g.s));
+    GMI_CUDA_CHECK(cudaStreamWaitEvent(g.s2, g.ev_fork, 0));
+    for (int l = L - 1; l >= 1; --l) {
+      gemm(g, GMI_PH_DX_GEMM, g.dx[l], g.bn_dx[l], 0, 1, EPI_DACT, g.flop_dx[l], g.ws_dx[l], g.s2, dx_ctas);
+      GMI_CUDA_CHECK(cudaEventRecord(g.ev_d[l - 1], g.s2));
+    }
+    for (int l = L - 1; l >= 0; --l) {
+      if (l < L - 1) GMI_CUDA_CHECK(cudaStreamWaitEvent(g.s, g.ev_d[l], 0));
+      GemmParams P = g.dw[l];
+      if (l == 0) P.prob[0].b_row0 = P.prob[1].b_row0 = k * g.Bm;
+      gemm(g, GMI_PH_DW_GEMM, P, g.bn_dw[l], 1, 1, EPI_F32, g.flop_dw[l], 0, g.s, dw_ctas);
+    }
+  }
+  for (int l = L - 1; l >= 0 && !(par && L > 1); --l) {
     GemmParams P = g.dw[l];
     if (l == 0) P.prob[0].b_row0 = P.prob[1].b_row0 = k * g.Bm;
     gemm(g, GMI_PH_DW_GEMM, P, g.bn_dw[l], 1, 1, EPI_F32, g.flop_dw[l]);
     if (!g.fused_bias[l]) {  // else summed by the DACT GEMM that produced dPre_l
-      const int cur = (L - 1 - l) & 1;
-      const __nv_bfloat16* Ds[2] = {g.D[0][cur], g.D[1][cur]};
+      const __nv_bfloat16* Ds[2] = {g.D[0][l], g.D[1][l]};
       const int widths[2] = {geo_.wp[l + 1], geo_.wp[l + 1]};
       float* outs[2] = {g.colsum[0][l], g.colsum[1][l]};
       timed(g.s, GMI_PH_COLSUM, 0.0, 2.0 * 2.0 * g.Bm * geo_.wp[l + 1],

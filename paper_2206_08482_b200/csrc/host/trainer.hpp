@@ -61,7 +61,8 @@ class Trainer {
   void values(Gmi& g);
   void train_minibatch(Gmi& g, int k, int adam_step = -1);  // adam_step >= 0: fused Adam
   void reduce_and_step(int k);
-  void gemm(Gmi& g, int phase, const GemmParams& P, int bn, int amn, int bmn, int epi, double flop, int ws = 0);
+  void gemm(Gmi& g, int phase, const GemmParams& P, int bn, int amn, int bmn, int epi, double flop, int ws = 0,
+            cudaStream_t stream = nullptr, int ctas = 0);
   // Runs f (which enqueues work on s); with cfg.instrument and s = GMI 0's stream or the
   // update stream, brackets it with CUDA events booked to `phase` (+ algorithmic flop/bytes).
   template <class F>
@@ -86,6 +87,8 @@ class Trainer {
   cudaEvent_t ev_adam_ = nullptr;
   cudaEvent_t ev_start_ = nullptr;
   void* nccl_ = nullptr;
+  bool bwd_par_ = true;    // dx chain || dW GEMMs on two streams of the GMI
+  int bwd_dx_share_ = 50;  // percent of the GMI's SMs given to the dx branch
   int iteration_ = 0;      // iterations enqueued so far
   long long adam_steps_ = 0;
   int launches_ = 0;       // kernels in one iteration
