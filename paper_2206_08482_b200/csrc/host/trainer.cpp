@@ -164,8 +164,10 @@ Trainer::Trainer(const gmi_ppo_config_t& cfg, const void* nccl_id) : cfg_(cfg) {
   if (geo_.wp[geo_.L] > ppo::kMaxHeadIn) invalid("last hidden width > 512 unsupported");
   T_ = cfg.horizon;
   {
-    const char* par = std::getenv("GMI_BWD_PAR");  // "0" disables backward branch parallelism
-    bwd_par_ = !(par && par[0] == '0');
+    // backward branch parallelism (GMI_BWD_PAR=1): measured neutral on B200 (the branches share
+    // the same L2/HBM bandwidth), so it is opt-in
+    const char* par = std::getenv("GMI_BWD_PAR");
+    bwd_par_ = par && par[0] == '1';
     const char* share = std::getenv("GMI_BWD_DX_SHARE");  // percent of the GMI's SMs for dx
     if (share) bwd_dx_share_ = std::max(10, std::min(90, std::atoi(share)));
   }

@@ -87,7 +87,7 @@ class Trainer {
   cudaEvent_t ev_adam_ = nullptr;
   cudaEvent_t ev_start_ = nullptr;
   void* nccl_ = nullptr;
-  bool bwd_par_ = true;    // dx chain || dW GEMMs on two streams of the GMI
+  bool bwd_par_ = false;   // dx chain || dW GEMMs on two streams of the GMI
   int bwd_dx_share_ = 50;  // percent of the GMI's SMs given to the dx branch
   int iteration_ = 0;      // iterations enqueued so far
   long long adam_steps_ = 0;
