@@ -35,6 +35,19 @@ struct RolloutArgs {
   unsigned long long* trace;  // optional [T][16] globaltimer stamps of CTA 0 (development aid)
 };
 
+// Fused value pass (value_mlp.cu): V[r] = value_net(X_roll row r) for rows [0, rows).
+struct ValueArgs {
+  CUtensorMap map_obs;               // X_roll {S_p, rows}, box {64, 128}
+  CUtensorMap map_w[kRollMaxL + 1];  // value-net weights, box {64, out_n}; [L] = value head (16 rows)
+  const float* bias[kRollMaxL + 1];
+  int in_p[kRollMaxL + 1];
+  int out_n[kRollMaxL + 1];  // hidden out_p; head 16
+  int L;
+  long long rows;
+  float* V;
+};
+void launch_value_mlp(const ValueArgs& a, int max_ctas, cudaStream_t s);
+
 // Whether the fused rollout supports this MLP (hidden widths <= 256, <= 4 layers, S_p <= 256, A <= 31).
 bool rollout_fusable(int L, const int* widths_p, int S_p, int A);
 void launch_rollout(const RolloutArgs& a, cudaStream_t s);

@@ -145,6 +145,8 @@ struct Trainer::Gmi {
   std::vector<ppo::Segment> segs;
   bool fused_roll = false;
   int roll_cluster = 0;  // > 0: cluster rollout with this many CTAs per 128-env tile
+  bool fused_val = false;
+  ppo::ValueArgs val_args{};
   ppo::RolloutArgs roll_args{};
   bool fused_bias[GMI_MAX_HIDDEN] = {};  // bias gradient summed inside the layer's dW GEMM
   bool fused_head = false;
@@ -574,6 +576,28 @@ void Trainer::build_plans() {
     for (auto& sg : g.segs)  // parameter segments may carry the fused Adam update
       sg.param_off = (sg.dst >= g.grad && sg.dst < g.grad + geo_.P) ? (long long)(sg.dst - g.grad) : -1;
 
+    // fused value pass (value MLP on chip over all (T+1) x N observations)
+    const char* vunf = std::getenv("GMI_VALUE_UNFUSED");
+    g.fused_val = ppo::rollout_fusable(L, geo_.wp.data(), S_p, A) && !(vunf && vunf[0] == '1');
+    if (g.fused_val) {
+      ppo::ValueArgs& v = g.val_args;
+      v.map_obs = tma_kmajor(g.X_roll, S_p, (long long)(T_ + 1) * g.N, S_p, kGemmBlockM);
+      for (int l = 0; l < L; ++l) {
+        const Tensor& t = geo_.net[1][l];
+        v.map_w[l] = tma_kmajor(shadow_ + t.w, t.in_p, t.out_p, t.in_p, t.out_p);
+        v.bias[l] = params_ + t.b;
+        v.in_p[l] = t.in_p;
+        v.out_n[l] = t.out_p;
+      }
+      v.map_w[L] = tma_kmajor(shadow_ + geo_.net[1][L].w, hp, 1, hp, 16);
+      v.bias[L] = params_ + geo_.net[1][L].b;
+      v.in_p[L] = hp;
+      v.out_n[L] = 16;
+      v.L = L;
+      v.rows = (long long)(T_ + 1) * g.N;
+      v.V = g.V;
+    }
+
     // fused rollout (one persistent kernel per rollout) when the policy MLP fits on chip
     const char* unfused = std::getenv("GMI_ROLLOUT_UNFUSED");
     g.fused_roll = ppo::rollout_fusable(L, geo_.wp.data(), S_p, A) && !(unfused && unfused[0] == '1');
@@ -754,7 +778,13 @@ void Trainer::values(Gmi& g) {
   const int L = geo_.L;
   const long long rows = (long long)(T_ + 1) * g.N;
   const Tensor& head = geo_.net[1][L];
-  for (long long c0 = 0; c0 < rows; c0 += g.Mrows) {
+  if (g.fused_val) {  // the whole value MLP on chip, one persistent launch (cuda/value_mlp.cu)
+    double flop = 2.0 * geo_.width[L] * rows;
+    for (int l = 0; l < L; ++l) flop += g.flop_roll[l] * double(rows) / g.N;
+    timed(g.s, GMI_PH_VAL_GEMM, flop, 0.0, [&] { ppo::launch_value_mlp(g.val_args, g.ctas, g.s); });
+    ++launches_;
+  }
+  for (long long c0 = 0; c0 < rows && !g.fused_val; c0 += g.Mrows) {
     const int m = int(std::min<long long>(g.Mrows, rows - c0));
     for (int l = 0; l < L; ++l) {
       GemmParams P = g.fwd_val[l];

@@ -130,11 +130,12 @@ def test_fused_rollout_matches_per_layer_path(cuda, monkeypatch, dims):
     cfg = dict(obs_dim=S, act_dim=A, hidden=hidden, num_envs=200)
     fused = Trainer(PpoConfig(**cfg))
     monkeypatch.setenv("GMI_ROLLOUT_UNFUSED", "1")
+    monkeypatch.setenv("GMI_VALUE_UNFUSED", "1")
     plain = Trainer(PpoConfig(**cfg))
     for _ in range(2):  # second rollout starts from carried-over state (done resets inside)
         fused.rollout()
         plain.rollout()
-        for f in ("done", "ep_count", "ep_step", "act", "obs", "x"):
+        for f in ("done", "ep_count", "ep_step", "act", "obs", "x", "val"):
             assert np.array_equal(fused.get(f), plain.get(f)), f
         for f in ("rew", "logp"):
             np.testing.assert_allclose(fused.get(f), plain.get(f), rtol=1e-5, atol=1e-5)
