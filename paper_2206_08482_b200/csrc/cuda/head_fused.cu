@@ -3,12 +3,12 @@
 //   MMA1  head forward        mu | v  = H_L W_head^T           (N = 16 / 32, fp32 in TMEM)
 //   loss  clipped surrogate / value loss per row -> G = dL/dmu | dL/dv (bf16, smem operand)
 //   MMA2  head input grad     acc    = G W_head                (N = hp)
-//   epi   dPre_{L-1} = acc * elu'(H_L) (H_L read from the smem tile) -> bf16 -> TMA store,
-//         plus the column sums of dPre_{L-1} (bias gradient of layer L-1)
+//   epi   dPre_{L-1} = acc * elu'(H_L) (H_L read from the smem tile) -> bf16 -> TMA store
 //   MMA3  head weight grad    dW^T  += H_L^T G                 (accumulated in TMEM over all
 //         tiles of the CTA; one fp32 slab per CTA)
-// so the head forward, the loss, the head input- and weight-gradient GEMMs and a column-sum
-// pass become one launch, and mu / v / G never touch HBM.
+// so the head forward, the loss and the head input- and weight-gradient GEMMs become one
+// launch, and mu / v / G never touch HBM. Column group 0 (4 warps) runs the per-row loss while
+// groups 1-3 run the elu' epilogue of the previous tile.
 //
 // CTA b serves net b % 2 (0 = policy, 1 = value) and its tiles b/2, b/2 + grid/2, ...
 // Warp 0: TMA (head weights once, H tiles), warp 1: tcgen05.mma issuer, warps 2..17:
@@ -41,7 +41,8 @@ constexpr uint32_t kOffWM = kOffWK + 4 * 4096;  // W_head MN-major, [32 K-rows][
 constexpr uint32_t kOffStg = kOffWM + 4 * 4096;  // epilogue staging, 2 KB per warp
 constexpr uint32_t kOffRed = kOffStg + kEpiWarps * 2048;  // 4 x 256 fp32
 constexpr uint32_t kOffBar = kOffRed + 4 * 256 * 4;
-constexpr uint32_t kSmem = kOffBar + 256 + 1024;
+constexpr uint32_t kSmem = kOffBar + 512 + 1024;  // barriers + per-action constants
+constexpr int kElu = 12;  // warps on the elu' epilogue (column groups 1..3); group 0 runs the loss
 constexpr uint32_t kTmemAcc1 = 0, kTmemAcc3 = 64, kTmemAcc2 = 256;
 
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory"); }
@@ -77,12 +78,12 @@ __global__ void __launch_bounds__(kThreads, 1) head_fused_kernel(const __grid_co
     ptx::mbar_init(wbar, 1);
     for (int b = 0; b < 2; ++b) {
       ptx::mbar_init(&hfull[b], 1);
-      ptx::mbar_init(&hfree[b], kEpiWarps + 1);  // epilogue (elu' reads) + MMA3 commit
+      ptx::mbar_init(&hfree[b], kElu + 1);  // elu' epilogue reads + MMA3 commit
     }
     ptx::mbar_init(acc1_full, 1);
     ptx::mbar_init(g_ready, 4);
     ptx::mbar_init(acc2_full, 1);
-    ptx::mbar_init(acc2_free, kEpiWarps);
+    ptx::mbar_init(acc2_free, kElu);
     ptx::mbar_init(fin, 1);
     ptx::fence_mbar_init();
     ptx::tma_prefetch_desc(&hn.map_h);
@@ -169,11 +170,18 @@ __global__ void __launch_bounds__(kThreads, 1) head_fused_kernel(const __grid_co
     const int row = q * 32 + lane;
     const float invB = 1.0f / float(a.Bm);
     uint8_t* stg = smem + kOffStg + (warp - 2) * 2048;
+    // per-action constants of the loss, once per CTA: log_std and exp(log_std)
+    float* cst = reinterpret_cast<float*>(smem + kOffBar + 128);
+    if (threadIdx.x - 64 < a.A) {
+      const float ls = a.log_std[threadIdx.x - 64];
+      cst[threadIdx.x - 64] = ls;
+      cst[32 + threadIdx.x - 64] = expf(ls);
+    }
+    epi_bar();
     float sg[MAXA], sl[MAXA];  // running db_head / dlog_std of this thread's rows
 #pragma unroll
     for (int i = 0; i < MAXA; ++i) sg[i] = sl[i] = 0.f;
     float st[4] = {0.f, 0.f, 0.f, 0.f};
-    float csum[2] = {0.f, 0.f};
     int it = 0;
     for (int j = cta; j < mtiles; j += ctas, ++it) {
       const int grow = j * kRows + row;
@@ -218,8 +226,8 @@ __global__ void __launch_bounds__(kThreads, 1) head_fused_kernel(const __grid_co
             for (int i = 0; i < MAXA; ++i)
               if (i < A) {
                 mu[i] = __uint_as_float(r[i]) + hn.bias[i];
-                ls[i] = a.log_std[i];
-                sig[i] = expf(ls[i]);
+                ls[i] = cst[i];
+                sig[i] = cst[32 + i];
                 z[i] = (act_r[i] - mu[i]) / sig[i];
                 lp += -0.5f * z[i] * z[i] - ls[i] - kLog2PiHalf;
               }
@@ -260,12 +268,14 @@ __global__ void __launch_bounds__(kThreads, 1) head_fused_kernel(const __grid_co
         if (lane == 0) ptx::mbar_arrive(g_ready);
       }
 
-      // ---- dPre_{L-1} = (G W_head) * elu'(H_L): 32-column chunks c = h, h + 4
+      // ---- dPre_{L-1} = (G W_head) * elu'(H_L) on column groups 1..3 (chunks c = h-1, h+2, h+5),
+      // so group 0 can already run the next tile's loss
+      if (h == 0) continue;
       ptx::mbar_wait_sleep(acc2_full, it & 1);
       ptx::tc_fence_after();
 #pragma unroll 1
-      for (int pass = 0; pass < 2; ++pass) {
-        const int c = h + 4 * pass;
+      for (int pass = 0; pass < 3; ++pass) {
+        const int c = (h - 1) + 3 * pass;
         if (c * 32 >= hp) break;
         uint32_t r[32];
         ptx::tmem_ld_32x32b_x32(tmem + kTmemAcc2 + (static_cast<uint32_t>(q * 32) << 16) + c * 32, r);
@@ -293,17 +303,6 @@ __global__ void __launch_bounds__(kThreads, 1) head_fused_kernel(const __grid_co
         for (int u = 0; u < 4; ++u)
           *reinterpret_cast<uint4*>(stg + lane * 64 + ((u ^ ((lane >> 1) & 3)) << 4)) =
               make_uint4(packed[4 * u], packed[4 * u + 1], packed[4 * u + 2], packed[4 * u + 3]);
-        __syncwarp();
-        if (hn.colsum) {
-          float s = 0.f;  // lane = column: the 32 staged rows in row order
-#pragma unroll
-          for (int rr = 0; rr < 32; ++rr) {
-            const uint16_t v = *reinterpret_cast<const uint16_t*>(stg + rr * 64 +
-                                                                 (((lane >> 3) ^ ((rr >> 1) & 3)) << 4) + (lane & 7) * 2);
-            s += __uint_as_float(uint32_t(v) << 16);
-          }
-          csum[pass] += s;
-        }
         ptx::fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
@@ -320,23 +319,6 @@ __global__ void __launch_bounds__(kThreads, 1) head_fused_kernel(const __grid_co
     }
 
     // ---- per-CTA outputs
-    // (a) optional bias gradient of layer L-1: combine the 4 lane quarters in order
-    if (hn.colsum) {
-#pragma unroll
-      for (int pass = 0; pass < 2; ++pass) {
-        const int c = h + 4 * pass;
-        if (c * 32 < 256) red[q * 256 + c * 32 + lane] = csum[pass];
-      }
-      epi_bar();
-      if (q == 0)
-#pragma unroll
-        for (int pass = 0; pass < 2; ++pass) {
-          const int col = (h + 4 * pass) * 32 + lane;
-          if (col < hp)
-            hn.colsum[(long long)cta * hp + col] = ((red[col] + red[256 + col]) + red[512 + col]) + red[768 + col];
-        }
-      epi_bar();
-    }
     // (b) head weight gradient slab: TMEM rows = hp index, columns = head outputs
     ptx::mbar_wait_sleep(fin, 0);
     ptx::tc_fence_after();

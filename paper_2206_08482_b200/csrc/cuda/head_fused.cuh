@@ -14,7 +14,6 @@ struct HeadNet {
   CUtensorMap map_wm;  // same weights viewed [K = n_out rows][N = hp], box {64, 32}, SW128
   CUtensorMap map_d;   // dPre_{L-1} out [Bm][hp] bf16, box {32, 32}, SW64
   const float* bias;   // head bias [n_out]
-  float* colsum;       // [ctas per net][hp]  bias gradient of layer L-1
   float* dw_slab;      // [ctas per net][n_out][hp]  head weight gradient
   int n_out;           // A (policy) or 1 (value)
   int nh;              // MMA N of the head: 16 or 32

@@ -536,7 +536,6 @@ void Trainer::build_plans() {
         hn.map_wm = make_tma_2d_bf16(shadow_ + geo_.net[n][L].w, hp, hn.n_out, hp, 64, 32);  // [32 K][64 N]
         hn.map_d = make_tma_out_bf16(g.D[n][L - 1], hp, g.Bm, hp);
         hn.bias = params_ + geo_.net[n][L].b;
-        hn.colsum = nullptr;  // layer L-1 bias: column sums inside its dW GEMM
         g.head_slab[n] = dev((size_t)per_net * hn.n_out * hp * 4);
         hn.dw_slab = g.head_slab[n];
       }
