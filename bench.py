@@ -39,7 +39,10 @@ def parse():
     p.add_argument("--config", default=os.path.join(ROOT, "configs", "at_4096env_3x256.cfg"))
     p.add_argument("--gmis", type=int, default=0, help="override GMIs per GPU")
     p.add_argument("--envs", type=int, default=0, help="override envs per GPU")
-    p.add_argument("--backend", type=int, default=0, help="0 streams, 1 green contexts")
+    p.add_argument("--backend", type=int, default=None, help="0 streams, 1 green contexts (default: config)")
+    p.add_argument("--decoupled", type=int, default=None,
+                   help="1: serving GMI + trainer GMI per GPU with an experience channel (BASELINE config 4)")
+    p.add_argument("--serving-sms", type=int, default=0, help="SMs of the serving GMI (decoupled mode)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-sample-envs", type=int, default=64)
     return p.parse_args()
@@ -208,7 +211,15 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     cfg.num_gpus, cfg.rank, cfg.device = world, rank, local
     cfg.num_envs = envs_per_gpu * world
-    cfg.gmi_backend = args.backend
+    if args.decoupled is not None:
+        cfg.decoupled = args.decoupled
+        if cfg.decoupled:
+            cfg.gmis_per_gpu = 1
+            cfg.gmi_backend = 1
+    if args.serving_sms:
+        cfg.serving_sms = args.serving_sms
+    if args.backend is not None:
+        cfg.gmi_backend = args.backend
     cfg.instrument = 0  # timed loop runs the plain graph; a separate pass below is instrumented
     nid = None
     if world > 1:
@@ -285,17 +296,21 @@ def main():
             cv, cores, sample = cpu_iteration_sample(cfg, args.cpu_sample_envs, 1, 0)
             cpu = {"value": cv, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample}
         ws = working_set_mb(cfg, envs_per_gpu)
+        layout = (f"{cfg.gmis_per_gpu} GMI(s) per B200 (BASELINE configs[1])" if not cfg.decoupled else
+                  f"decoupled: 1 serving GMI ({cfg.serving_sms or 16} SMs, simulator+agent) + 1 trainer GMI "
+                  f"per B200, device experience channel, one-iteration policy lag (BASELINE configs[3])")
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": max(3, args.warmup), "ms_per_step": ms_max / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {"workload": f"AT-like locomotion, {envs_per_gpu} envs/GPU, "
                                    f"{'x'.join(map(str, cfg.hidden))} actor-critic MLP, "
-                                   f"{cfg.gmis_per_gpu} GMI(s) per B200 (BASELINE configs[1])",
+                                   f"{layout}",
                        "config_file": os.path.relpath(args.config, ROOT), "envs_per_gpu": envs_per_gpu,
                        "obs_dim": cfg.obs_dim, "act_dim": cfg.act_dim, "hidden": cfg.hidden,
                        "horizon": cfg.horizon, "epochs": cfg.epochs, "minibatches": cfg.minibatches,
-                       "gmis_per_gpu": cfg.gmis_per_gpu, "gmi_backend": ["streams", "green_ctx"][args.backend],
+                       "gmis_per_gpu": cfg.gmis_per_gpu + (1 if cfg.decoupled else 0),
+                       "gmi_backend": ["streams", "green_ctx"][cfg.gmi_backend], "decoupled": bool(cfg.decoupled),
                        "parallelism": f"dp{world * cfg.gmis_per_gpu} ({world} GPU x {cfg.gmis_per_gpu} GMI)",
                        "env_steps_per_step": steps_total // args.steps,
                        "l2": f"no flush: per-iteration working set ~{ws:.0f} MB > 126 MB L2",

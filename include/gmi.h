@@ -352,6 +352,15 @@ typedef struct {
   int sm_per_gmi;             /* green-context SMs per GMI (multiple of 8; 0 = even split) */
   int use_graph;              /* capture the update phase in a CUDA graph */
   int instrument;             /* time GEMM launches with CUDA events (roofline) */
+  /* Decoupled (asynchronous) mode, BASELINE config 4 / PAPER.md:378-407: per GPU one serving
+   * GMI (simulator + agent, roles of mapping.hpp:243) on `serving_sms` SMs streams experience
+   * through a device channel to the trainer GMI on the remaining SMs. Iteration i trains on the
+   * experience the serving GMI generated with the weights of iteration i-1 while it generates
+   * iteration i+1's experience with the weights of iteration i (one-iteration policy lag; the
+   * behaviour log-probs are recorded, so the clipped ratio stays exact). gmis_per_gpu counts
+   * trainer GMIs and must be 1. */
+  int decoupled;
+  int serving_sms;            /* green-context SMs of the serving GMI (multiple of 8; 0 = 16) */
 } gmi_ppo_config_t;
 
 typedef struct {

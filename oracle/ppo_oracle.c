@@ -122,6 +122,7 @@ typedef struct {
   long long P; /* padded flat length */
   int n_gmi;
   int iteration;
+  int primed; /* decoupled mode: rollout 0 done */
   long long adam_step;
   float *params, *adam_m, *adam_v, *grad_sum;
   /* per GMI */
@@ -602,9 +603,22 @@ void ppo_oracle_free(void* h) {
 
 static float* g_mean_std; /* scratch for rollout -> update hand-off */
 
-int ppo_oracle_rollout(void* h) {
-  oracle_t* o = (oracle_t*)h;
-  g_exact = o->c.exact_fp32;
+/* Env stepping of every GMI with the current parameters (obs slot 0 carries the last
+ * observation of the previous rollout after the first one). */
+static void rollout_all(oracle_t* o) {
+  float* wbf = (float*)malloc(sizeof(float) * o->P);
+  make_bf16_weights(o, wbf);
+  for (int c = 0; c < o->n_gmi; ++c) {
+    struct gmi* g = &o->g[c];
+    const long long N = g->nenv, S = o->c.obs_dim, T = o->c.horizon;
+    if (o->iteration > 0) memmove(g->obs, g->obs + T * N * S, sizeof(float) * N * S);
+    rollout_gmi(o, c, wbf);
+  }
+  free(wbf);
+}
+
+/* Values of all T+1 observation slots with the current parameters, GAE, advantage moments. */
+static void values_gae_all(oracle_t* o) {
   float* wbf = (float*)malloc(sizeof(float) * o->P);
   make_bf16_weights(o, wbf);
   double rsum = 0;
@@ -613,10 +627,7 @@ int ppo_oracle_rollout(void* h) {
   g_mean_std = (float*)calloc((size_t)(2 * o->n_gmi), sizeof(float));
   for (int c = 0; c < o->n_gmi; ++c) {
     struct gmi* g = &o->g[c];
-    const long long N = g->nenv, S = o->c.obs_dim, T = o->c.horizon;
-    /* first observation slot is the carried-over state */
-    if (o->iteration > 0) memmove(g->obs, g->obs + T * N * S, sizeof(float) * N * S);
-    rollout_gmi(o, c, wbf);
+    const long long N = g->nenv, T = o->c.horizon;
     values_gmi(o, c, wbf);
     gae_gmi(o, c, &g_mean_std[2 * c], &g_mean_std[2 * c + 1]);
     for (long long i = 0; i < T * N; ++i) rsum += g->rew[i];
@@ -625,12 +636,18 @@ int ppo_oracle_rollout(void* h) {
   o->last.mean_reward = rsum / (double)(rn ? rn : 1);
   o->last.env_steps = rn;
   free(wbf);
+}
+
+int ppo_oracle_rollout(void* h) {
+  oracle_t* o = (oracle_t*)h;
+  g_exact = o->c.exact_fp32;
+  rollout_all(o);
+  values_gae_all(o);
   return 0;
 }
 
-int ppo_oracle_iteration(void* h, ppo_stats_t* out) {
-  oracle_t* o = (oracle_t*)h;
-  ppo_oracle_rollout(h);
+/* E epochs x K minibatch updates on the GMIs' current experience; iteration += 1. */
+static void train_all(oracle_t* o) {
   const int S = o->c.obs_dim, A = o->c.act_dim, T = o->c.horizon, L = o->L;
   float* wbf = (float*)malloc(sizeof(float) * o->P);
   mb_t* mbs = (mb_t*)calloc((size_t)o->n_gmi, sizeof(mb_t));
@@ -678,9 +695,42 @@ int ppo_oracle_iteration(void* h, ppo_stats_t* out) {
   free(Bm);
   free(wbf);
   o->iteration += 1;
+}
+
+int ppo_oracle_iteration(void* h, ppo_stats_t* out) {
+  oracle_t* o = (oracle_t*)h;
+  ppo_oracle_rollout(h);
+  train_all(o);
   if (out) *out = o->last;
   return 0;
 }
+
+/* Decoupled mode (device: gmi_ppo_config_t.decoupled): iteration i trains on rollout i, which
+ * the serving GMI produced with theta_{i-1} (rollout 0: theta_0), while rollout i+1 is
+ * produced with theta_i. Values/GAE use the trainer's theta_i. Rollout r keys its action
+ * noise with r (= the iteration counter when it runs here). */
+int ppo_oracle_iteration_decoupled(void* h, ppo_stats_t* out) {
+  oracle_t* o = (oracle_t*)h;
+  g_exact = o->c.exact_fp32;
+  if (!o->primed) {
+    rollout_all(o);
+    o->primed = 1;
+  }
+  float* snap = (float*)malloc(sizeof(float) * o->P);
+  memcpy(snap, o->params, sizeof(float) * o->P);
+  values_gae_all(o);
+  train_all(o);
+  const ppo_stats_t trained = o->last;
+  float* cur = o->params;
+  o->params = snap;
+  rollout_all(o);
+  o->params = cur;
+  free(snap);
+  o->last = trained;
+  if (out) *out = o->last;
+  return 0;
+}
+
 
 static void mb_alloc(const oracle_t* o, mb_t* m, int Bm) {
   const int S = o->c.obs_dim, A = o->c.act_dim;

@@ -43,6 +43,9 @@ typedef struct {
 void* ppo_oracle_create(const ppo_cfg_t* cfg);
 void ppo_oracle_free(void* h);
 int ppo_oracle_iteration(void* h, ppo_stats_t* out);
+/* Decoupled (asynchronous serving/trainer) iteration, one-iteration policy lag; see
+ * ppo_oracle.c. Do not mix with ppo_oracle_iteration on one handle. */
+int ppo_oracle_iteration_decoupled(void* h, ppo_stats_t* out);
 /* Runs only the rollout + GAE part of the next iteration (no update). */
 int ppo_oracle_rollout(void* h);
 

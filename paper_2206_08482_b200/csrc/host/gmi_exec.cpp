@@ -34,28 +34,60 @@ void cu_check(CUresult r, const char* what) {
 GmiResources::GmiResources(int device, int count, int backend, int sm_per_gmi) : backend_(backend) {
   GMI_CUDA_CHECK(cudaSetDevice(device));
   if (backend == 0) {
-    for (int i = 0; i < count; ++i) {
-      cudaStream_t s;
-      GMI_CUDA_CHECK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-      streams_.push_back(s);
-      GMI_CUDA_CHECK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-      aux_.push_back(s);
-      sms_.push_back(0);
-    }
+    for (int i = 0; i < count; ++i) add_stream_pair(nullptr, 0);
     return;
   }
+  int total = 0;
+  GMI_CUDA_CHECK(cudaDeviceGetAttribute(&total, cudaDevAttrMultiProcessorCount, device));
+  const int per = sm_per_gmi > 0 ? sm_per_gmi : (total / count) / 8 * 8;
+  make_green(device, std::vector<int>(count, per));
+}
+
+GmiResources::GmiResources(int device, const std::vector<int>& sms, int backend) : backend_(backend) {
+  GMI_CUDA_CHECK(cudaSetDevice(device));
+  if (backend == 0) {
+    for (size_t i = 0; i < sms.size(); ++i) add_stream_pair(nullptr, 0);
+    return;
+  }
+  make_green(device, sms);
+}
+
+void GmiResources::add_stream_pair(void* green, int sms) {
+  if (!green) {
+    cudaStream_t s;
+    GMI_CUDA_CHECK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    streams_.push_back(s);
+    GMI_CUDA_CHECK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    aux_.push_back(s);
+    sms_.push_back(sms);
+    return;
+  }
+  using StreamCreate = CUresult (*)(CUstream*, CUgreenCtx, unsigned, int);
+  static auto cuGreenCtxStreamCreate_ = driver_fn<StreamCreate>("cuGreenCtxStreamCreate");
+  CUstream s;
+  cu_check(cuGreenCtxStreamCreate_(&s, static_cast<CUgreenCtx>(green), CU_STREAM_NON_BLOCKING, 0),
+           "cuGreenCtxStreamCreate");
+  streams_.push_back(reinterpret_cast<cudaStream_t>(s));
+  cu_check(cuGreenCtxStreamCreate_(&s, static_cast<CUgreenCtx>(green), CU_STREAM_NON_BLOCKING, 0),
+           "cuGreenCtxStreamCreate");
+  aux_.push_back(reinterpret_cast<cudaStream_t>(s));
+  sms_.push_back(sms);
+}
+
+// One SM group per GMI, carved off the device's SM resource in order
+// (cuDevSmResourceSplitByCount with a single group of the requested size, then the remainder
+// is split again); an entry of 0 takes whatever the other GMIs left over.
+void GmiResources::make_green(int device, const std::vector<int>& sms) {
   using GetDev = CUresult (*)(CUdevice*, int);
   using GetRes = CUresult (*)(CUdevice, CUdevResource*, CUdevResourceType);
   using Split = CUresult (*)(CUdevResource*, unsigned*, const CUdevResource*, CUdevResource*, unsigned, unsigned);
   using GenDesc = CUresult (*)(CUdevResourceDesc*, CUdevResource*, unsigned);
   using Create = CUresult (*)(CUgreenCtx*, CUdevResourceDesc, CUdevice, unsigned);
-  using StreamCreate = CUresult (*)(CUstream*, CUgreenCtx, unsigned, int);
   auto cuDeviceGet_ = driver_fn<GetDev>("cuDeviceGet");
   auto cuDeviceGetDevResource_ = driver_fn<GetRes>("cuDeviceGetDevResource");
   auto cuDevSmResourceSplitByCount_ = driver_fn<Split>("cuDevSmResourceSplitByCount");
   auto cuDevResourceGenerateDesc_ = driver_fn<GenDesc>("cuDevResourceGenerateDesc");
   auto cuGreenCtxCreate_ = driver_fn<Create>("cuGreenCtxCreate");
-  auto cuGreenCtxStreamCreate_ = driver_fn<StreamCreate>("cuGreenCtxStreamCreate");
 
   GMI_CUDA_CHECK(cudaFree(nullptr));  // make the primary context current first
   CUdevice dev;
@@ -63,28 +95,35 @@ GmiResources::GmiResources(int device, int count, int backend, int sm_per_gmi) :
   CUdevResource all{};
   cu_check(cuDeviceGetDevResource_(dev, &all, CU_DEV_RESOURCE_TYPE_SM), "cuDeviceGetDevResource");
   const int total = int(all.sm.smCount);
-  int per = sm_per_gmi > 0 ? sm_per_gmi : (total / count) / 8 * 8;
-  if (per < 8 || per % 8 != 0 || per * count > total)
-    fail(GMI_ERR_INVALID, "green-context split infeasible: " + std::to_string(count) + " GMIs x " +
-                              std::to_string(per) + " SMs on a " + std::to_string(total) + "-SM GPU");
-  std::vector<CUdevResource> groups(count);
-  unsigned n = unsigned(count);
-  CUdevResource rest{};
-  cu_check(cuDevSmResourceSplitByCount_(groups.data(), &n, &all, &rest, 0, unsigned(per)),
-           "cuDevSmResourceSplitByCount");
-  if (int(n) < count) fail(GMI_ERR_INVALID, "green-context split produced too few groups");
-  for (int i = 0; i < count; ++i) {
+  int fixed = 0, zeros = 0;
+  for (int s : sms) {
+    if (s == 0) ++zeros;
+    else if (s < 8 || s % 8 != 0) fail(GMI_ERR_INVALID, "green-context GMI sizes must be multiples of 8 SMs (>= 8)");
+    fixed += s;
+  }
+  if (zeros > 1 || fixed > total || (zeros == 1 && total - fixed < 8))
+    fail(GMI_ERR_INVALID, "green-context split infeasible: " + std::to_string(sms.size()) + " GMIs, " +
+                              std::to_string(fixed) + " fixed SMs on a " + std::to_string(total) + "-SM GPU");
+  std::vector<CUdevResource> res(sms.size());
+  CUdevResource cur = all;
+  for (size_t i = 0; i < sms.size(); ++i) {
+    if (sms[i] == 0) continue;
+    unsigned n = 1;
+    CUdevResource rest{};
+    cu_check(cuDevSmResourceSplitByCount_(&res[i], &n, &cur, &rest, 0, unsigned(sms[i])),
+             "cuDevSmResourceSplitByCount");
+    if (n < 1) fail(GMI_ERR_INVALID, "green-context split produced no group");
+    cur = rest;
+  }
+  for (size_t i = 0; i < sms.size(); ++i)
+    if (sms[i] == 0) res[i] = cur;
+  for (size_t i = 0; i < sms.size(); ++i) {
     CUdevResourceDesc desc;
-    cu_check(cuDevResourceGenerateDesc_(&desc, &groups[i], 1), "cuDevResourceGenerateDesc");
+    cu_check(cuDevResourceGenerateDesc_(&desc, &res[i], 1), "cuDevResourceGenerateDesc");
     CUgreenCtx g;
     cu_check(cuGreenCtxCreate_(&g, desc, dev, CU_GREEN_CTX_DEFAULT_STREAM), "cuGreenCtxCreate");
-    CUstream s;
-    cu_check(cuGreenCtxStreamCreate_(&s, g, CU_STREAM_NON_BLOCKING, 0), "cuGreenCtxStreamCreate");
     green_.push_back(g);
-    streams_.push_back(reinterpret_cast<cudaStream_t>(s));
-    cu_check(cuGreenCtxStreamCreate_(&s, g, CU_STREAM_NON_BLOCKING, 0), "cuGreenCtxStreamCreate");
-    aux_.push_back(reinterpret_cast<cudaStream_t>(s));
-    sms_.push_back(int(groups[i].sm.smCount));
+    add_stream_pair(g, int(res[i].sm.smCount));
   }
 }
 

@@ -10,6 +10,9 @@ class GmiResources {
  public:
   // backend 0: streams; 1: green contexts with sm_per_gmi SMs each (0 = even split).
   GmiResources(int device, int count, int backend, int sm_per_gmi);
+  // backend 1 with explicit per-GMI SM counts (multiples of 8); one entry may be 0 = the
+  // SMs left over by the others (e.g. {16, 0}: a 16-SM serving GMI + a 132-SM trainer GMI).
+  GmiResources(int device, const std::vector<int>& sms, int backend);
   ~GmiResources();
   cudaStream_t stream(int i) const { return streams_[i]; }
   // second stream of the same GMI (same SM partition): independent branches of the
@@ -19,6 +22,8 @@ class GmiResources {
   int backend() const { return backend_; }
 
  private:
+  void make_green(int device, const std::vector<int>& sms);
+  void add_stream_pair(void* green, int sms);
   int backend_;
   std::vector<cudaStream_t> streams_, aux_;
   std::vector<void*> green_;

@@ -121,6 +121,11 @@ struct Trainer::Gmi {
   __nv_bfloat16* X_roll = nullptr;
   float *act = nullptr, *logp = nullptr, *rew = nullptr, *V = nullptr, *adv = nullptr, *ret = nullptr;
   uint8_t* done = nullptr;
+  // decoupled mode: the experience channel the serving GMI writes (same layouts as X_roll,
+  // act, logp, rew, done); the trainer migrates it into the buffers above at slot start
+  __nv_bfloat16* ch_X = nullptr;
+  float *ch_act = nullptr, *ch_logp = nullptr, *ch_rew = nullptr;
+  uint8_t* ch_done = nullptr;
   double* gae_part = nullptr;
   float* adv_stats = nullptr;  // mean, std, mean reward
   __nv_bfloat16* X_sh = nullptr;
@@ -178,7 +183,19 @@ Trainer::Trainer(const gmi_ppo_config_t& cfg, const void* nccl_id) : cfg_(cfg) {
   n_total_ = cfg.num_gpus * cfg.gmis_per_gpu;
   if (cfg.num_envs < n_total_) invalid("fewer environments than GMIs");
   GMI_CUDA_CHECK(cudaSetDevice(cfg.device));
-  exec_ = std::make_unique<GmiResources>(cfg.device, n_local_, cfg.gmi_backend, cfg.sm_per_gmi);
+  decoupled_ = cfg.decoupled != 0;
+  if (decoupled_) {
+    // GMI 2r: simulator + agent (serving), GMI 2r+1: trainer (mapping.hpp:243-249 roles)
+    if (n_local_ != 1) invalid("decoupled mode runs one trainer GMI per GPU (gmis_per_gpu = 1)");
+    const int serving = cfg.serving_sms > 0 ? cfg.serving_sms : 16;
+    exec_ = std::make_unique<GmiResources>(cfg.device, std::vector<int>{serving, 0}, cfg.gmi_backend);
+    serve_s_ = exec_->stream(0);
+    GMI_CUDA_CHECK(cudaEventCreateWithFlags(&ev_copied_, cudaEventDisableTiming));
+    GMI_CUDA_CHECK(cudaEventCreateWithFlags(&ev_rolled_, cudaEventDisableTiming));
+  } else {
+    exec_ = std::make_unique<GmiResources>(cfg.device, n_local_, cfg.gmi_backend, cfg.sm_per_gmi);
+  }
+  const int tix = decoupled_ ? 1 : 0;  // execution-resource index of the first trainer GMI
   GMI_CUDA_CHECK(cudaStreamCreateWithFlags(&upd_, cudaStreamNonBlocking));
   GMI_CUDA_CHECK(cudaEventCreateWithFlags(&ev_adam_, cudaEventDisableTiming));
   GMI_CUDA_CHECK(cudaEventCreateWithFlags(&ev_start_, cudaEventDisableTiming));
@@ -194,9 +211,9 @@ Trainer::Trainer(const gmi_ppo_config_t& cfg, const void* nccl_id) : cfg_(cfg) {
     g->Bm = g->B / K_;
     if (g->Bm % 64 != 0) invalid("minibatch rows per GMI must be a multiple of 64 (use envs per GMI % 8 == 0)");
     g->Mrows = std::max(g->Bm, g->N);
-    g->s = exec_->stream(i);
-    g->s2 = exec_->aux_stream(i);
-    g->ctas = exec_->sm_count(i) > 0 ? exec_->sm_count(i) : sms;
+    g->s = exec_->stream(tix + i);
+    g->s2 = exec_->aux_stream(tix + i);
+    g->ctas = exec_->sm_count(tix + i) > 0 ? exec_->sm_count(tix + i) : sms;
     GMI_CUDA_CHECK(cudaEventCreateWithFlags(&g->ev_done, cudaEventDisableTiming));
     GMI_CUDA_CHECK(cudaEventCreateWithFlags(&g->ev_fork, cudaEventDisableTiming));
     for (auto& e : g->ev_d) GMI_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -205,6 +222,8 @@ Trainer::Trainer(const gmi_ppo_config_t& cfg, const void* nccl_id) : cfg_(cfg) {
   alloc();
   init_params();
   build_plans();
+  if (decoupled_ && !gmis_[0]->fused_roll)
+    invalid("decoupled mode needs the fused rollout (hidden widths <= 256, <= 4 layers)");
   ensure_bias_table(1 << 20);
   if (cfg.num_gpus > 1) {
     if (!nccl_id) invalid("nccl_id required when num_gpus > 1");
@@ -216,7 +235,7 @@ Trainer::Trainer(const gmi_ppo_config_t& cfg, const void* nccl_id) : cfg_(cfg) {
   }
   for (auto& g : gmis_) {
     ppo::EnvParams ep{g->N, geo_.S, geo_.A, geo_.wp[0], g->env0, T_, cfg_.seed};
-    ppo::launch_env_init(ep, g->x, g->ep_step, g->ep_len, g->ep_count, g->X_roll, g->s);
+    ppo::launch_env_init(ep, g->x, g->ep_step, g->ep_len, g->ep_count, decoupled_ ? g->ch_X : g->X_roll, g->s);
   }
   GMI_CUDA_CHECK(cudaEventRecord(ev_adam_, upd_));
   GMI_CUDA_CHECK(cudaDeviceSynchronize());
@@ -235,6 +254,8 @@ Trainer::~Trainer() {
     cudaEventDestroy(g->ev_fork);
     for (auto e : g->ev_d) cudaEventDestroy(e);
   }
+  if (ev_copied_) cudaEventDestroy(ev_copied_);
+  if (ev_rolled_) cudaEventDestroy(ev_rolled_);
   if (ev_adam_) cudaEventDestroy(ev_adam_);
   if (ev_start_) cudaEventDestroy(ev_start_);
   if (upd_) cudaStreamDestroy(upd_);
@@ -266,6 +287,11 @@ void Trainer::alloc() {
   GMI_CUDA_CHECK(cudaMallocHost(&stats_host_, 8 * 4));
   std::memset(ctl_host_, 0, sizeof(ppo::Control));
   std::memset(stats_host_, 0, 8 * 4);
+  if (decoupled_) {
+    params_roll_ = static_cast<float*>(dev(P * 4));
+    shadow_roll_ = static_cast<__nv_bfloat16*>(dev(P * 2));
+    ctl_roll_ = static_cast<ppo::Control*>(dev(sizeof(ppo::Control)));
+  }
 
   const int S_p = geo_.wp[0], A = geo_.A, L = geo_.L;
   int maxw = 0;
@@ -282,6 +308,13 @@ void Trainer::alloc() {
     g.logp = static_cast<float*>(dev(T * N * 4));
     g.rew = static_cast<float*>(dev(T * N * 4));
     g.done = static_cast<uint8_t*>(dev(T * N));
+    if (decoupled_) {
+      g.ch_X = static_cast<__nv_bfloat16*>(dev((T + 1) * N * S_p * 2));
+      g.ch_act = static_cast<float*>(dev(T * N * A * 4));
+      g.ch_logp = static_cast<float*>(dev(T * N * 4));
+      g.ch_rew = static_cast<float*>(dev(T * N * 4));
+      g.ch_done = static_cast<uint8_t*>(dev(T * N));
+    }
     g.V = static_cast<float*>(dev((T + 1) * N * 4));
     g.adv = static_cast<float*>(dev(T * N * 4));
     g.ret = static_cast<float*>(dev(T * N * 4));
@@ -602,30 +635,38 @@ void Trainer::build_plans() {
     g.fused_roll = ppo::rollout_fusable(L, geo_.wp.data(), S_p, A) && !(unfused && unfused[0] == '1');
     if (g.fused_roll) {
       ppo::RolloutArgs& r = g.roll_args;
-      r.map_obs = tma_kmajor(g.X_roll, S_p, g.N, S_p, kGemmBlockM);
+      // decoupled mode: the serving GMI acts with the policy snapshot and writes the channel
+      __nv_bfloat16* wsrc = decoupled_ ? shadow_roll_ : shadow_;
+      float* psrc = decoupled_ ? params_roll_ : params_;
+      __nv_bfloat16* Xr = decoupled_ ? g.ch_X : g.X_roll;
+      r.map_obs = tma_kmajor(Xr, S_p, g.N, S_p, kGemmBlockM);
       for (int l = 0; l < L; ++l) {
         const Tensor& t = geo_.net[0][l];
-        r.map_w[l] = tma_kmajor(shadow_ + t.w, t.in_p, t.out_p, t.in_p, t.out_p);
-        r.bias[l] = params_ + t.b;
+        r.map_w[l] = tma_kmajor(wsrc + t.w, t.in_p, t.out_p, t.in_p, t.out_p);
+        r.bias[l] = psrc + t.b;
         r.in_p[l] = t.in_p;
         r.out_n[l] = t.out_p;
       }
       const int head_n = A <= 16 ? 16 : 32;
-      r.map_w[L] = tma_kmajor(shadow_ + geo_.net[0][L].w, hp, A, hp, head_n);
+      r.map_w[L] = tma_kmajor(wsrc + geo_.net[0][L].w, hp, A, hp, head_n);
       // cluster variant: 64-row weight slices per CTA, 16-row head (rollout_cluster.cu)
       const char* nocl = std::getenv("GMI_ROLLOUT_NOCLUSTER");
       g.roll_cluster = (nocl && nocl[0] == '1') ? 0 : ppo::rollout_cluster_size(L, geo_.wp.data(), S_p, A, g.N);
+      // a small serving partition runs the rollout in waves: one CTA per env tile then beats
+      // 4-CTA clusters (measured on B200: 1.9 vs 4.3 ms for 4096 envs on 16 SMs)
+      if (decoupled_ && exec_->sm_count(0) > 0 && g.roll_cluster * (g.N / kGemmBlockM) > exec_->sm_count(0))
+        g.roll_cluster = 0;
       if (g.roll_cluster) {
         for (int l = 0; l < L; ++l) {
           const Tensor& t = geo_.net[0][l];
-          r.map_w[l] = tma_kmajor(shadow_ + t.w, t.in_p, t.out_p, t.in_p, 64);
+          r.map_w[l] = tma_kmajor(wsrc + t.w, t.in_p, t.out_p, t.in_p, 64);
         }
-        r.map_w[L] = tma_kmajor(shadow_ + geo_.net[0][L].w, hp, A, hp, 16);
+        r.map_w[L] = tma_kmajor(wsrc + geo_.net[0][L].w, hp, A, hp, 16);
       }
-      r.bias[L] = params_ + geo_.net[0][L].b;
+      r.bias[L] = psrc + geo_.net[0][L].b;
       r.in_p[L] = hp;
       r.out_n[L] = head_n;
-      r.log_std = params_ + geo_.log_std;
+      r.log_std = psrc + geo_.log_std;
       r.L = L;
       r.A = A;
       r.S = geo_.S;
@@ -638,12 +679,12 @@ void Trainer::build_plans() {
       r.ep_step = g.ep_step;
       r.ep_len = g.ep_len;
       r.ep_count = g.ep_count;
-      r.X_roll = g.X_roll;
-      r.act = g.act;
-      r.logp = g.logp;
-      r.rew = g.rew;
-      r.done = g.done;
-      r.ctl = ctl_dev_;
+      r.X_roll = Xr;
+      r.act = decoupled_ ? g.ch_act : g.act;
+      r.logp = decoupled_ ? g.ch_logp : g.logp;
+      r.rew = decoupled_ ? g.ch_rew : g.rew;
+      r.done = decoupled_ ? g.ch_done : g.done;
+      r.ctl = decoupled_ ? ctl_roll_ : ctl_dev_;
       const char* trace = std::getenv("GMI_ROLLOUT_TRACE");
       if (trace && trace[0] == '1') r.trace = reinterpret_cast<unsigned long long*>(dev((size_t)T_ * 16 * 8));
     }
@@ -940,7 +981,26 @@ void Trainer::reduce_and_step(int step_in_iter) {
   GMI_CUDA_CHECK(cudaEventRecord(ev_adam_, upd_));
 }
 
+// Decoupled mode: the serving GMI (its own SM partition) steps every env T times with the
+// policy snapshot and writes the experience channel; rollouts after the first continue from
+// the last observation of the previous one. Its control block counts rollouts (noise keys).
+void Trainer::serve_rollout(Gmi& g) {
+  const int S_p = geo_.wp[0];
+  if (rollouts_ > 0)
+    GMI_CUDA_CHECK(cudaMemcpyAsync(g.ch_X, g.ch_X + (long long)T_ * g.N * S_p, (size_t)g.N * S_p * 2,
+                                   cudaMemcpyDeviceToDevice, serve_s_));
+  if (g.roll_cluster)
+    ppo::launch_rollout_cluster(g.roll_args, g.roll_cluster, serve_s_);
+  else
+    ppo::launch_rollout(g.roll_args, serve_s_);
+  ppo::launch_control_advance(ctl_roll_, 0, serve_s_);
+  GMI_CUDA_CHECK(cudaEventRecord(ev_rolled_, serve_s_));
+  launches_ += 2;
+  ++rollouts_;
+}
+
 void Trainer::enqueue_rollout() {
+  if (decoupled_) invalid("gmi_ppo_rollout: the serving GMI rolls out inside each decoupled iteration");
   write_control();
   GMI_CUDA_CHECK(cudaEventRecord(ev_start_, upd_));
   for (auto& g : gmis_) {
@@ -957,10 +1017,30 @@ void Trainer::record_iteration() {
   launches_ = 0;
   marks_used_ = 0;
   GMI_CUDA_CHECK(cudaEventRecord(ev_start_, upd_));
-  for (auto& g : gmis_) {
-    GMI_CUDA_CHECK(cudaStreamWaitEvent(g->s, ev_start_, 0));
-    rollout(*g);
-    values(*g);
+  if (decoupled_) {
+    // migrate the channel's experience (rollout i) into the trainer's buffers, then let the
+    // serving GMI produce rollout i+1 with the snapshot theta_i while this slot trains
+    Gmi& g = *gmis_[0];
+    const long long TN = (long long)T_ * g.N;
+    const int S_p = geo_.wp[0], A = geo_.A;
+    GMI_CUDA_CHECK(cudaStreamWaitEvent(g.s, ev_start_, 0));
+    timed(g.s, GMI_PH_OTHER, 0.0, 2.0 * (TN + g.N) * S_p * 2 + 2.0 * TN * (4.0 * A + 9.0), [&] {
+      GMI_CUDA_CHECK(cudaMemcpyAsync(g.X_roll, g.ch_X, (size_t)(TN + g.N) * S_p * 2, cudaMemcpyDeviceToDevice, g.s));
+      GMI_CUDA_CHECK(cudaMemcpyAsync(g.act, g.ch_act, (size_t)TN * A * 4, cudaMemcpyDeviceToDevice, g.s));
+      GMI_CUDA_CHECK(cudaMemcpyAsync(g.logp, g.ch_logp, (size_t)TN * 4, cudaMemcpyDeviceToDevice, g.s));
+      GMI_CUDA_CHECK(cudaMemcpyAsync(g.rew, g.ch_rew, (size_t)TN * 4, cudaMemcpyDeviceToDevice, g.s));
+      GMI_CUDA_CHECK(cudaMemcpyAsync(g.done, g.ch_done, (size_t)TN, cudaMemcpyDeviceToDevice, g.s));
+    });
+    GMI_CUDA_CHECK(cudaEventRecord(ev_copied_, g.s));
+    GMI_CUDA_CHECK(cudaStreamWaitEvent(serve_s_, ev_copied_, 0));
+    serve_rollout(g);
+    values(g);
+  } else {
+    for (auto& g : gmis_) {
+      GMI_CUDA_CHECK(cudaStreamWaitEvent(g->s, ev_start_, 0));
+      rollout(*g);
+      values(*g);
+    }
   }
   int step = 0;
   // One GMI on one GPU: Adam can run inside the gradient-assembly kernel (GMI_ADAM_FUSED=1).
@@ -993,6 +1073,11 @@ void Trainer::record_iteration() {
     }
   }
   for (auto& g : gmis_) GMI_CUDA_CHECK(cudaStreamWaitEvent(upd_, g->ev_done, 0));
+  if (decoupled_) {  // rollout i+1 is done with the snapshot: refresh it to theta_{i+1}
+    GMI_CUDA_CHECK(cudaStreamWaitEvent(upd_, ev_rolled_, 0));
+    GMI_CUDA_CHECK(cudaMemcpyAsync(params_roll_, params_, (size_t)geo_.P * 4, cudaMemcpyDeviceToDevice, upd_));
+    GMI_CUDA_CHECK(cudaMemcpyAsync(shadow_roll_, shadow_, (size_t)geo_.P * 2, cudaMemcpyDeviceToDevice, upd_));
+  }
   timed(upd_, GMI_PH_OTHER, 0.0, 0.0, [&] {
     GMI_CUDA_CHECK(cudaMemcpyAsync(stats_dev_ + 4, gmis_[0]->adv_stats, 3 * 4, cudaMemcpyDeviceToDevice, upd_));
     GMI_CUDA_CHECK(cudaMemcpyAsync(stats_host_, stats_dev_, 8 * 4, cudaMemcpyDeviceToHost, upd_));
@@ -1004,6 +1089,15 @@ void Trainer::record_iteration() {
 void Trainer::enqueue_iteration(bool host_control) {
   ensure_bias_table(adam_steps_ + (long long)cfg_.epochs * K_ + 1);
   if (host_control || iteration_ == 0) write_control();
+  if (decoupled_ && rollouts_ == 0) {  // prologue: rollout 0 with theta_0 (not overlapped)
+    GMI_CUDA_CHECK(cudaMemcpyAsync(params_roll_, params_, (size_t)geo_.P * 4, cudaMemcpyDeviceToDevice, upd_));
+    GMI_CUDA_CHECK(cudaMemcpyAsync(shadow_roll_, shadow_, (size_t)geo_.P * 2, cudaMemcpyDeviceToDevice, upd_));
+    GMI_CUDA_CHECK(cudaMemsetAsync(ctl_roll_, 0, sizeof(ppo::Control), upd_));
+    GMI_CUDA_CHECK(cudaEventRecord(ev_start_, upd_));
+    GMI_CUDA_CHECK(cudaStreamWaitEvent(serve_s_, ev_start_, 0));
+    serve_rollout(*gmis_[0]);
+    GMI_CUDA_CHECK(cudaStreamWaitEvent(upd_, ev_rolled_, 0));
+  }
   if (cfg_.use_graph && iteration_ > 0) {
     if (!graph_) {
       GMI_CUDA_CHECK(cudaStreamSynchronize(upd_));
@@ -1033,6 +1127,7 @@ void Trainer::enqueue_iteration(bool host_control) {
 void Trainer::synchronize(gmi_ppo_stats_t* st) {
   GMI_CUDA_CHECK(cudaStreamSynchronize(upd_));
   for (auto& g : gmis_) GMI_CUDA_CHECK(cudaStreamSynchronize(g->s));
+  if (serve_s_) GMI_CUDA_CHECK(cudaStreamSynchronize(serve_s_));
   gmi_ppo_phase_t gemm{};
   if (cfg_.instrument) {
     std::memset(phases_, 0, sizeof(phases_));
@@ -1102,13 +1197,16 @@ long long Trainer::get(const std::string& what, int gi, void* dst) {
   const long long N = g.N, T = T_, S = geo_.S, A = geo_.A;
   if (what == "grad") return copy(g.grad, P, 4);
   if (what == "x") return copy(g.x, N * S, 4);
-  if (what == "act") return copy(g.act, T * N * A, 4);
-  if (what == "logp") return copy(g.logp, T * N, 4);
-  if (what == "rew") return copy(g.rew, T * N, 4);
+  // decoupled mode: act/logp/rew/done/obs are the latest rollout (the experience channel, one
+  // rollout ahead of the trainer); val/adv/ret belong to the rollout trained last
+  const bool ch = decoupled_;
+  if (what == "act") return copy(ch ? g.ch_act : g.act, T * N * A, 4);
+  if (what == "logp") return copy(ch ? g.ch_logp : g.logp, T * N, 4);
+  if (what == "rew") return copy(ch ? g.ch_rew : g.rew, T * N, 4);
   if (what == "val") return copy(g.V, (T + 1) * N, 4);
   if (what == "adv") return copy(g.adv, T * N, 4);
   if (what == "ret") return copy(g.ret, T * N, 4);
-  if (what == "done") return copy(g.done, T * N, 1);
+  if (what == "done") return copy(ch ? g.ch_done : g.done, T * N, 1);
   if (what == "ep_step") return copy(g.ep_step, N, 4);
   if (what == "ep_len") return copy(g.ep_len, N, 4);
   if (what == "ep_count") return copy(g.ep_count, N, 4);
@@ -1125,7 +1223,7 @@ long long Trainer::get(const std::string& what, int gi, void* dst) {
     if (dst) {
       const int S_p = geo_.wp[0];
       std::vector<uint16_t> raw((size_t)(T + 1) * N * S_p);
-      GMI_CUDA_CHECK(cudaMemcpy(raw.data(), g.X_roll, raw.size() * 2, cudaMemcpyDeviceToHost));
+      GMI_CUDA_CHECK(cudaMemcpy(raw.data(), ch ? g.ch_X : g.X_roll, raw.size() * 2, cudaMemcpyDeviceToHost));
       float* o = static_cast<float*>(dst);
       for (long long r = 0; r < (T + 1) * N; ++r)
         for (long long i = 0; i < S; ++i) o[r * S + i] = bf16_float(raw[(size_t)(r * S_p + i)]);

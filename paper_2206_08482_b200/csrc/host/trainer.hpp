@@ -57,6 +57,7 @@ class Trainer {
   void ensure_bias_table(long long steps);
   void write_control();
   void record_iteration();  // the launch sequence of one iteration (eager or under capture)
+  void serve_rollout(Gmi& g);  // decoupled mode: the serving GMI's rollout into the channel
   void rollout(Gmi& g);
   void values(Gmi& g);
   void train_minibatch(Gmi& g, int k, int adam_step = -1);  // adam_step >= 0: fused Adam
@@ -87,6 +88,15 @@ class Trainer {
   cudaEvent_t ev_adam_ = nullptr;
   cudaEvent_t ev_start_ = nullptr;
   void* nccl_ = nullptr;
+  // decoupled mode (cfg.decoupled): serving GMI stream, experience-channel events, the policy
+  // snapshot the serving GMI acts with, and its own control block (rollout index)
+  bool decoupled_ = false;
+  cudaStream_t serve_s_ = nullptr;
+  cudaEvent_t ev_copied_ = nullptr, ev_rolled_ = nullptr;
+  float* params_roll_ = nullptr;
+  __nv_bfloat16* shadow_roll_ = nullptr;
+  ppo::Control* ctl_roll_ = nullptr;
+  long long rollouts_ = 0;  // serving-GMI rollouts enqueued so far
   bool bwd_par_ = false;   // dx chain || dW GEMMs on two streams of the GMI
   int bwd_dx_share_ = 50;  // percent of the GMI's SMs given to the dx branch
   int iteration_ = 0;      // iterations enqueued so far

@@ -26,7 +26,7 @@ class PpoConfigT(C.Structure):
                 ("ent_coef", C.c_float), ("seed", C.c_ulonglong), ("num_gpus", C.c_int),
                 ("gmis_per_gpu", C.c_int), ("rank", C.c_int), ("device", C.c_int),
                 ("gmi_backend", C.c_int), ("sm_per_gmi", C.c_int), ("use_graph", C.c_int),
-                ("instrument", C.c_int)]
+                ("instrument", C.c_int), ("decoupled", C.c_int), ("serving_sms", C.c_int)]
 
 
 PPO_PHASES = 20  # GMI_PPO_PHASES
@@ -95,6 +95,8 @@ class PpoConfig:
     sm_per_gmi: int = 0
     use_graph: int = 1
     instrument: int = 0
+    decoupled: int = 0
+    serving_sms: int = 0
 
     def to_c(self) -> PpoConfigT:
         c = PpoConfigT()
@@ -133,7 +135,12 @@ class PpoConfig:
                         horizon=int(cfg.get("ppo", "horizon") or w.steps_per_train),
                         epochs=int(cfg.get("ppo", "epochs") or 4),
                         minibatches=int(cfg.get("ppo", "minibatches") or 4),
-                        gmis_per_gpu=model.gmis_per_gpu, num_gpus=max(1, len(topo.gpus)))
+                        gmis_per_gpu=model.gmis_per_gpu, num_gpus=max(1, len(topo.gpus)),
+                        decoupled=int(cfg.get("ppo", "decoupled") or 0),
+                        serving_sms=int(cfg.get("ppo", "serving_sms") or 0))
+        if out.decoupled:  # [model] gmis_per_gpu counts all GMIs; the trainer side is one per GPU
+            out.gmis_per_gpu = 1
+            out.gmi_backend = int(cfg.get("ppo", "gmi_backend") or 1)
         for k, v in kw.items():
             setattr(out, k, v)
         return out

@@ -115,6 +115,7 @@ def ppo_lib():
             "ppo_oracle_free": (None, [vp]),
             "ppo_oracle_iteration": (C.c_int, [vp, C.POINTER(PpoStats)]),
             "ppo_oracle_rollout": (C.c_int, [vp]),
+            "ppo_oracle_iteration_decoupled": (C.c_int, [vp, C.POINTER(PpoStats)]),
             "ppo_oracle_minibatch": (C.c_int, [vp, C.c_int, fp, fp, fp, fp, fp, C.c_int, fp,
                                                C.POINTER(C.c_double)]),
             "ppo_oracle_adam": (C.c_int, [vp, fp]),
@@ -184,6 +185,11 @@ class PpoOracle:
 
     def rollout(self):
         ppo_lib().ppo_oracle_rollout(self.h)
+
+    def iteration_decoupled(self):
+        s = PpoStats()
+        ppo_lib().ppo_oracle_iteration_decoupled(self.h, C.byref(s))
+        return s
 
     def width(self, layer):
         return ppo_lib().ppo_oracle_width(self.h, layer)

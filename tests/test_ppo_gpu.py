@@ -183,3 +183,31 @@ def test_bench_workload_runs(cuda):
     assert np.isfinite([s.policy_loss, s.value_loss, s.approx_kl, s.mean_reward]).all()
     assert s.gemm_launches > 0 and s.kernel_launches > s.gemm_launches
     assert np.isfinite(t.get("params")).all()
+
+
+@pytest.mark.parametrize("backend", [0, 1])
+def test_decoupled_mode_matches_oracle(cuda, backend):
+    """Decoupled mode (BASELINE config 4 on one GPU): a serving GMI (16-SM green context, or a
+    plain stream) rolls out into the experience channel with the policy snapshot while the
+    trainer GMI trains on the previous rollout. Three iterations (the first eager, then CUDA
+    graph replays) against the oracle's lagged schedule; same tolerances as the synchronous
+    iteration, reset masks bit-exact."""
+    dev, orc = _pair(**SMALL, decoupled=1, gmi_backend=backend)
+    for it in range(3):
+        s = dev.iteration()
+        o = orc.iteration_decoupled()
+        assert s.env_steps == SMALL["num_envs"] * 32
+        tol = (2e-3, 5e-5) if it == 0 else (4e-3, 1e-4)
+        _close(f"params[{it}]", dev.get("params"), orc.get("params"), *tol)
+        # reset masks of the latest rollout (the channel, one ahead of the trainer): bit-exact
+        assert np.array_equal(dev.get("done"), orc.get("done")), it
+        _close(f"rew[{it}]", dev.get("rew"), orc.get("rew"), 5e-2, 5e-4)
+        assert abs(s.mean_reward - o.mean_reward) < 1e-3
+
+
+def test_decoupled_bench_shape_matches_oracle(cuda):
+    dev, orc = _pair(60, 8, [256, 256, 256], 128, decoupled=1, gmi_backend=1)
+    for it in range(2):
+        dev.iteration()
+        orc.iteration_decoupled()
+        _close(f"params[{it}]", dev.get("params"), orc.get("params"), 4e-3, 1e-4)

@@ -200,3 +200,35 @@ def test_full_iteration_runs_and_learns_something():
     assert s.env_steps == 64 * 32
     assert np.isfinite([s.policy_loss, s.value_loss, s.approx_kl]).all()
     assert not np.array_equal(o.get("params"), p0)
+
+
+def test_decoupled_first_iteration_equals_synchronous():
+    """Decoupled mode (serving GMI + trainer GMI, one-iteration policy lag): iteration 0 trains
+    on rollout 0, produced with theta_0 exactly as in the synchronous iteration, so the
+    parameters after it are bit-identical; from iteration 1 on the experience is one policy
+    version behind and the trajectories diverge."""
+    sync = PpoOracle(make_cfg(12, 3, [32, 32], 64))
+    dec = PpoOracle(make_cfg(12, 3, [32, 32], 64))
+    s0 = sync.iteration()
+    d0 = dec.iteration_decoupled()
+    assert np.array_equal(sync.get("params").view(np.uint32), dec.get("params").view(np.uint32))
+    assert s0.mean_reward == d0.mean_reward and d0.env_steps == 64 * 32
+    sync.iteration()
+    dec.iteration_decoupled()
+    assert not np.array_equal(sync.get("params"), dec.get("params"))
+
+
+def test_decoupled_rollout_uses_the_lagged_policy():
+    """Rollout i+1 is produced with theta_i: replaying it with a synchronous handle whose
+    parameters are set to theta_i (and whose env state is rollout i's) reproduces it."""
+    dec = PpoOracle(make_cfg(12, 3, [32], 64))
+    dec.iteration_decoupled()        # trains rollout 0 -> theta_1; produces rollout 1 with theta_0
+    # a synchronous handle at iteration 1 (env state after rollout 0) whose parameters are
+    # reset to theta_0 produces the same rollout 1
+    ref2 = PpoOracle(make_cfg(12, 3, [32], 64))
+    theta0 = ref2.get("params").copy()
+    ref2.iteration()                 # env state after rollout 0, iteration counter 1
+    ref2.set("params", theta0)
+    ref2.rollout()                   # rollout 1 with theta_0
+    for what in ("rew", "act", "logp", "done"):
+        assert np.array_equal(dec.get(what), ref2.get(what)), what
