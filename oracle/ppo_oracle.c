@@ -705,32 +705,37 @@ int ppo_oracle_iteration(void* h, ppo_stats_t* out) {
   return 0;
 }
 
-/* Decoupled mode (device: gmi_ppo_config_t.decoupled): iteration i trains on rollout i, which
- * the serving GMI produced with theta_{i-1} (rollout 0: theta_0), while rollout i+1 is
- * produced with theta_i. Values/GAE use the trainer's theta_i. Rollout r keys its action
- * noise with r (= the iteration counter when it runs here). */
+/* Decoupled mode (device: gmi_ppo_config_t.decoupled): the serving GMI produces rollout i+1
+ * -- env steps, critic values of its T+1 observation slots and GAE -- with a snapshot of
+ * theta_i, while the trainer runs the epochs of iteration i on rollout i (produced with
+ * theta_{i-1}; rollout 0 with theta_0). Rollout r keys its action noise with r (= the
+ * iteration counter when it runs here). Reported stats: losses of iteration i's update and
+ * the mean reward of rollout i. */
 int ppo_oracle_iteration_decoupled(void* h, ppo_stats_t* out) {
   oracle_t* o = (oracle_t*)h;
   g_exact = o->c.exact_fp32;
   if (!o->primed) {
     rollout_all(o);
+    values_gae_all(o);
     o->primed = 1;
   }
   float* snap = (float*)malloc(sizeof(float) * o->P);
   memcpy(snap, o->params, sizeof(float) * o->P);
-  values_gae_all(o);
   train_all(o);
   const ppo_stats_t trained = o->last;
   float* cur = o->params;
   o->params = snap;
   rollout_all(o);
+  values_gae_all(o);
   o->params = cur;
   free(snap);
+  if (out) *out = trained;
+  /* o->last keeps rollout i+1's reward statistics for the next call's report */
+  const double next_reward = o->last.mean_reward;
   o->last = trained;
-  if (out) *out = o->last;
+  o->last.mean_reward = next_reward;
   return 0;
 }
-
 
 static void mb_alloc(const oracle_t* o, mb_t* m, int Bm) {
   const int S = o->c.obs_dim, A = o->c.act_dim;

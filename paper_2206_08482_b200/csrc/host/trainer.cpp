@@ -126,6 +126,9 @@ struct Trainer::Gmi {
   __nv_bfloat16* ch_X = nullptr;
   float *ch_act = nullptr, *ch_logp = nullptr, *ch_rew = nullptr;
   uint8_t* ch_done = nullptr;
+  float *ch_V = nullptr, *ch_adv = nullptr, *ch_ret = nullptr, *ch_adv_stats = nullptr;
+  double* ch_gae_part = nullptr;
+  ppo::ValueArgs ch_val_args{};  // value pass of the serving GMI (snapshot weights, channel obs)
   double* gae_part = nullptr;
   float* adv_stats = nullptr;  // mean, std, mean reward
   __nv_bfloat16* X_sh = nullptr;
@@ -222,8 +225,8 @@ Trainer::Trainer(const gmi_ppo_config_t& cfg, const void* nccl_id) : cfg_(cfg) {
   alloc();
   init_params();
   build_plans();
-  if (decoupled_ && !gmis_[0]->fused_roll)
-    invalid("decoupled mode needs the fused rollout (hidden widths <= 256, <= 4 layers)");
+  if (decoupled_ && !(gmis_[0]->fused_roll && gmis_[0]->fused_val))
+    invalid("decoupled mode needs the fused rollout and value pass (hidden widths <= 256, <= 4 layers)");
   ensure_bias_table(1 << 20);
   if (cfg.num_gpus > 1) {
     if (!nccl_id) invalid("nccl_id required when num_gpus > 1");
@@ -314,6 +317,11 @@ void Trainer::alloc() {
       g.ch_logp = static_cast<float*>(dev(T * N * 4));
       g.ch_rew = static_cast<float*>(dev(T * N * 4));
       g.ch_done = static_cast<uint8_t*>(dev(T * N));
+      g.ch_V = static_cast<float*>(dev((T + 1) * N * 4));
+      g.ch_adv = static_cast<float*>(dev(T * N * 4));
+      g.ch_ret = static_cast<float*>(dev(T * N * 4));
+      g.ch_adv_stats = static_cast<float*>(dev(4 * 4));
+      g.ch_gae_part = static_cast<double*>(dev(ppo::gae_blocks(g.N) * 3 * 8));
     }
     g.V = static_cast<float*>(dev((T + 1) * N * 4));
     g.adv = static_cast<float*>(dev(T * N * 4));
@@ -628,6 +636,19 @@ void Trainer::build_plans() {
       v.L = L;
       v.rows = (long long)(T_ + 1) * g.N;
       v.V = g.V;
+      if (decoupled_) {  // the serving GMI's copy: snapshot weights over the channel's observations
+        ppo::ValueArgs& c = g.ch_val_args;
+        c = v;
+        c.map_obs = tma_kmajor(g.ch_X, S_p, (long long)(T_ + 1) * g.N, S_p, kGemmBlockM);
+        for (int l = 0; l < L; ++l) {
+          const Tensor& t = geo_.net[1][l];
+          c.map_w[l] = tma_kmajor(shadow_roll_ + t.w, t.in_p, t.out_p, t.in_p, t.out_p);
+          c.bias[l] = params_roll_ + t.b;
+        }
+        c.map_w[L] = tma_kmajor(shadow_roll_ + geo_.net[1][L].w, hp, 1, hp, 16);
+        c.bias[L] = params_roll_ + geo_.net[1][L].b;
+        c.V = g.ch_V;
+      }
     }
 
     // fused rollout (one persistent kernel per rollout) when the policy MLP fits on chip
@@ -982,8 +1003,9 @@ void Trainer::reduce_and_step(int step_in_iter) {
 }
 
 // Decoupled mode: the serving GMI (its own SM partition) steps every env T times with the
-// policy snapshot and writes the experience channel; rollouts after the first continue from
-// the last observation of the previous one. Its control block counts rollouts (noise keys).
+// policy snapshot, evaluates the critic on the T+1 observation slots and runs GAE, writing the
+// experience channel; rollouts after the first continue from the last observation of the
+// previous one. Its control block counts rollouts (noise keys).
 void Trainer::serve_rollout(Gmi& g) {
   const int S_p = geo_.wp[0];
   if (rollouts_ > 0)
@@ -993,9 +1015,16 @@ void Trainer::serve_rollout(Gmi& g) {
     ppo::launch_rollout_cluster(g.roll_args, g.roll_cluster, serve_s_);
   else
     ppo::launch_rollout(g.roll_args, serve_s_);
+  // values of all T+1 observation slots with the same snapshot, then GAE: the channel carries
+  // ready advantages / returns, so the trainer starts straight at the epoch shuffle
+  const int sms = exec_->sm_count(0) > 0 ? exec_->sm_count(0) : device_sm_count();
+  ppo::launch_value_mlp(g.ch_val_args, sms, serve_s_);
+  ppo::launch_gae(g.ch_rew, g.ch_done, g.ch_V, g.ch_adv, g.ch_ret, g.ch_gae_part, g.N, T_, cfg_.gamma, cfg_.lam,
+                  serve_s_);
+  ppo::launch_adv_stats(g.ch_gae_part, ppo::gae_blocks(g.N), (long long)T_ * g.N, g.ch_adv_stats, serve_s_);
   ppo::launch_control_advance(ctl_roll_, 0, serve_s_);
   GMI_CUDA_CHECK(cudaEventRecord(ev_rolled_, serve_s_));
-  launches_ += 2;
+  launches_ += 5;
   ++rollouts_;
 }
 
@@ -1024,17 +1053,20 @@ void Trainer::record_iteration() {
     const long long TN = (long long)T_ * g.N;
     const int S_p = geo_.wp[0], A = geo_.A;
     GMI_CUDA_CHECK(cudaStreamWaitEvent(g.s, ev_start_, 0));
-    timed(g.s, GMI_PH_OTHER, 0.0, 2.0 * (TN + g.N) * S_p * 2 + 2.0 * TN * (4.0 * A + 9.0), [&] {
-      GMI_CUDA_CHECK(cudaMemcpyAsync(g.X_roll, g.ch_X, (size_t)(TN + g.N) * S_p * 2, cudaMemcpyDeviceToDevice, g.s));
-      GMI_CUDA_CHECK(cudaMemcpyAsync(g.act, g.ch_act, (size_t)TN * A * 4, cudaMemcpyDeviceToDevice, g.s));
-      GMI_CUDA_CHECK(cudaMemcpyAsync(g.logp, g.ch_logp, (size_t)TN * 4, cudaMemcpyDeviceToDevice, g.s));
-      GMI_CUDA_CHECK(cudaMemcpyAsync(g.rew, g.ch_rew, (size_t)TN * 4, cudaMemcpyDeviceToDevice, g.s));
-      GMI_CUDA_CHECK(cudaMemcpyAsync(g.done, g.ch_done, (size_t)TN, cudaMemcpyDeviceToDevice, g.s));
+    timed(g.s, GMI_PH_OTHER, 0.0, 2.0 * ((TN + g.N) * S_p * 2 + TN * (4.0 * A + 12.0) + 16.0), [&] {
+      auto mig = [&](void* dst, const void* src, size_t bytes) {
+        GMI_CUDA_CHECK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, g.s));
+      };
+      mig(g.X_roll, g.ch_X, (size_t)(TN + g.N) * S_p * 2);
+      mig(g.act, g.ch_act, (size_t)TN * A * 4);
+      mig(g.logp, g.ch_logp, (size_t)TN * 4);
+      mig(g.adv, g.ch_adv, (size_t)TN * 4);
+      mig(g.ret, g.ch_ret, (size_t)TN * 4);
+      mig(g.adv_stats, g.ch_adv_stats, 16);
     });
     GMI_CUDA_CHECK(cudaEventRecord(ev_copied_, g.s));
     GMI_CUDA_CHECK(cudaStreamWaitEvent(serve_s_, ev_copied_, 0));
     serve_rollout(g);
-    values(g);
   } else {
     for (auto& g : gmis_) {
       GMI_CUDA_CHECK(cudaStreamWaitEvent(g->s, ev_start_, 0));
@@ -1197,15 +1229,15 @@ long long Trainer::get(const std::string& what, int gi, void* dst) {
   const long long N = g.N, T = T_, S = geo_.S, A = geo_.A;
   if (what == "grad") return copy(g.grad, P, 4);
   if (what == "x") return copy(g.x, N * S, 4);
-  // decoupled mode: act/logp/rew/done/obs are the latest rollout (the experience channel, one
-  // rollout ahead of the trainer); val/adv/ret belong to the rollout trained last
+  // decoupled mode: rollout fields (act/logp/rew/done/obs/val/adv/ret) are the latest rollout
+  // in the experience channel, one rollout ahead of the trainer
   const bool ch = decoupled_;
   if (what == "act") return copy(ch ? g.ch_act : g.act, T * N * A, 4);
   if (what == "logp") return copy(ch ? g.ch_logp : g.logp, T * N, 4);
   if (what == "rew") return copy(ch ? g.ch_rew : g.rew, T * N, 4);
-  if (what == "val") return copy(g.V, (T + 1) * N, 4);
-  if (what == "adv") return copy(g.adv, T * N, 4);
-  if (what == "ret") return copy(g.ret, T * N, 4);
+  if (what == "val") return copy(ch ? g.ch_V : g.V, (T + 1) * N, 4);
+  if (what == "adv") return copy(ch ? g.ch_adv : g.adv, T * N, 4);
+  if (what == "ret") return copy(ch ? g.ch_ret : g.ret, T * N, 4);
   if (what == "done") return copy(ch ? g.ch_done : g.done, T * N, 1);
   if (what == "ep_step") return copy(g.ep_step, N, 4);
   if (what == "ep_len") return copy(g.ep_len, N, 4);

@@ -188,8 +188,8 @@ def test_bench_workload_runs(cuda):
 @pytest.mark.parametrize("backend", [0, 1])
 def test_decoupled_mode_matches_oracle(cuda, backend):
     """Decoupled mode (BASELINE config 4 on one GPU): a serving GMI (16-SM green context, or a
-    plain stream) rolls out into the experience channel with the policy snapshot while the
-    trainer GMI trains on the previous rollout. Three iterations (the first eager, then CUDA
+    plain stream) rolls out, evaluates the critic and runs GAE into the experience channel with
+    the policy snapshot while the trainer GMI trains on the previous rollout. Three iterations (the first eager, then CUDA
     graph replays) against the oracle's lagged schedule; same tolerances as the synchronous
     iteration, reset masks bit-exact."""
     dev, orc = _pair(**SMALL, decoupled=1, gmi_backend=backend)
@@ -202,6 +202,7 @@ def test_decoupled_mode_matches_oracle(cuda, backend):
         # reset masks of the latest rollout (the channel, one ahead of the trainer): bit-exact
         assert np.array_equal(dev.get("done"), orc.get("done")), it
         _close(f"rew[{it}]", dev.get("rew"), orc.get("rew"), 5e-2, 5e-4)
+        _close(f"adv[{it}]", dev.get("adv"), orc.get("adv"), 5e-2, 5e-4)  # serving-side critic + GAE
         assert abs(s.mean_reward - o.mean_reward) < 1e-3
 
 
