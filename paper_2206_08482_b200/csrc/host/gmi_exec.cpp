@@ -127,7 +127,21 @@ void GmiResources::make_green(int device, const std::vector<int>& sms) {
   }
 }
 
+cudaStream_t GmiResources::extra_stream(int i) {
+  const size_t n = streams_.size();
+  add_stream_pair(green_.empty() ? nullptr : green_.at(i), sms_.at(i));
+  cudaStream_t s = streams_.back();
+  // keep the per-GMI vectors indexed by GMI: the new pair lives past the GMIs
+  extra_.push_back(streams_.back());
+  extra_.push_back(aux_.back());
+  streams_.resize(n);
+  aux_.resize(n);
+  sms_.resize(n);
+  return s;
+}
+
 GmiResources::~GmiResources() {
+  for (auto s : extra_) cudaStreamDestroy(s);
   for (auto s : streams_) cudaStreamDestroy(s);
   for (auto s : aux_) cudaStreamDestroy(s);
   if (!green_.empty()) {

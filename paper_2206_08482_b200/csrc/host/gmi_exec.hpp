@@ -19,13 +19,15 @@ class GmiResources {
   // iteration (e.g. weight- and input-gradient GEMMs of a layer) run on it concurrently
   cudaStream_t aux_stream(int i) const { return aux_[i]; }
   int sm_count(int i) const { return sms_[i]; }
+  // one more stream in GMI i's partition, owned by this object (e.g. the trainer's update stream)
+  cudaStream_t extra_stream(int i);
   int backend() const { return backend_; }
 
  private:
   void make_green(int device, const std::vector<int>& sms);
   void add_stream_pair(void* green, int sms);
   int backend_;
-  std::vector<cudaStream_t> streams_, aux_;
+  std::vector<cudaStream_t> streams_, aux_, extra_;
   std::vector<void*> green_;
   std::vector<int> sms_;
 };

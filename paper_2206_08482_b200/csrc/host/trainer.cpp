@@ -199,7 +199,10 @@ Trainer::Trainer(const gmi_ppo_config_t& cfg, const void* nccl_id) : cfg_(cfg) {
     exec_ = std::make_unique<GmiResources>(cfg.device, n_local_, cfg.gmi_backend, cfg.sm_per_gmi);
   }
   const int tix = decoupled_ ? 1 : 0;  // execution-resource index of the first trainer GMI
-  GMI_CUDA_CHECK(cudaStreamCreateWithFlags(&upd_, cudaStreamNonBlocking));
+  if (decoupled_)  // the trainer's update stream (fold, Adam, snapshot) stays inside its partition
+    upd_ = exec_->extra_stream(1);
+  else
+    GMI_CUDA_CHECK(cudaStreamCreateWithFlags(&upd_, cudaStreamNonBlocking));
   GMI_CUDA_CHECK(cudaEventCreateWithFlags(&ev_adam_, cudaEventDisableTiming));
   GMI_CUDA_CHECK(cudaEventCreateWithFlags(&ev_start_, cudaEventDisableTiming));
   const int sms = device_sm_count();
@@ -261,7 +264,7 @@ Trainer::~Trainer() {
   if (ev_rolled_) cudaEventDestroy(ev_rolled_);
   if (ev_adam_) cudaEventDestroy(ev_adam_);
   if (ev_start_) cudaEventDestroy(ev_start_);
-  if (upd_) cudaStreamDestroy(upd_);
+  if (upd_ && !decoupled_) cudaStreamDestroy(upd_);
   for (void* p : allocs_) cudaFree(p);
   if (ctl_host_) cudaFreeHost(ctl_host_);
   if (stats_host_) cudaFreeHost(stats_host_);
