@@ -105,18 +105,28 @@ void GmiResources::make_green(int device, const std::vector<int>& sms) {
     fail(GMI_ERR_INVALID, "green-context split infeasible: " + std::to_string(sms.size()) + " GMIs, " +
                               std::to_string(fixed) + " fixed SMs on a " + std::to_string(total) + "-SM GPU");
   std::vector<CUdevResource> res(sms.size());
-  CUdevResource cur = all;
-  for (size_t i = 0; i < sms.size(); ++i) {
-    if (sms[i] == 0) continue;
-    unsigned n = 1;
+  bool equal = zeros == 0;
+  for (int s : sms) equal = equal && s == sms[0];
+  if (equal) {  // one split call: the driver places the equal groups itself
+    unsigned n = unsigned(sms.size());
     CUdevResource rest{};
-    cu_check(cuDevSmResourceSplitByCount_(&res[i], &n, &cur, &rest, 0, unsigned(sms[i])),
+    cu_check(cuDevSmResourceSplitByCount_(res.data(), &n, &all, &rest, 0, unsigned(sms[0])),
              "cuDevSmResourceSplitByCount");
-    if (n < 1) fail(GMI_ERR_INVALID, "green-context split produced no group");
-    cur = rest;
+    if (n < sms.size()) fail(GMI_ERR_INVALID, "green-context split produced too few groups");
+  } else {
+    CUdevResource cur = all;
+    for (size_t i = 0; i < sms.size(); ++i) {
+      if (sms[i] == 0) continue;
+      unsigned n = 1;
+      CUdevResource rest{};
+      cu_check(cuDevSmResourceSplitByCount_(&res[i], &n, &cur, &rest, 0, unsigned(sms[i])),
+               "cuDevSmResourceSplitByCount");
+      if (n < 1) fail(GMI_ERR_INVALID, "green-context split produced no group");
+      cur = rest;
+    }
+    for (size_t i = 0; i < sms.size(); ++i)
+      if (sms[i] == 0) res[i] = cur;
   }
-  for (size_t i = 0; i < sms.size(); ++i)
-    if (sms[i] == 0) res[i] = cur;
   for (size_t i = 0; i < sms.size(); ++i) {
     CUdevResourceDesc desc;
     cu_check(cuDevResourceGenerateDesc_(&desc, &res[i], 1), "cuDevResourceGenerateDesc");

@@ -25,6 +25,7 @@
 
 #include "../cuda/rng.cuh"
 #include "../cuda/head_fused.cuh"
+#include "../cuda/train_fwd.cuh"
 #include "../cuda/rollout.cuh"
 #include "errors.hpp"
 #include "gmi_exec.hpp"
@@ -160,6 +161,8 @@ struct Trainer::Gmi {
   bool fused_head = false;
   int head_grid = 0;
   ppo::HeadFusedArgs head_args{};
+  bool fused_fwd = false;  // hidden forward + head step in one launch (train_fwd.cu)
+  ppo::TrainFwdArgs fwd_args{};
 };
 
 // ------------------------------------------------------------------ construction
@@ -598,6 +601,51 @@ void Trainer::build_plans() {
       h.ent_coef = cfg_.ent_coef;
       head_parts = g.head_grid;
       hslab_parts = per_net;
+      // whole training forward + head step on chip (same per-CTA records as the head kernel).
+      // Opt-in (GMI_TRAIN_FWD=1): bit-identical, but with one tile in flight per CTA its MMA ->
+      // epilogue chain is serial and it measured slower on B200 than the per-layer GEMMs plus
+      // the fused head kernel, which overlap through PDL (3.65 vs 3.37 ms per iteration).
+      const char* fwd_on = std::getenv("GMI_TRAIN_FWD");
+      g.fused_fwd = ppo::train_fwd_fusable(L, geo_.wp.data(), S_p, A) && fwd_on && fwd_on[0] == '1';
+      if (g.fused_fwd) {
+        ppo::TrainFwdArgs& f = g.fwd_args;
+        f.map_x = tma_kmajor(g.X_sh, S_p, (long long)g.B, S_p, kGemmBlockM);
+        for (int n = 0; n < 2; ++n) {
+          ppo::TrainFwdNet& fn = f.net[n];
+          for (int l = 0; l < L; ++l) {
+            const Tensor& t = geo_.net[n][l];
+            fn.map_w[l] = tma_kmajor(shadow_ + t.w, t.in_p, t.out_p, t.in_p, t.out_p);
+            fn.bias[l] = params_ + t.b;
+            fn.in_p[l] = t.in_p;
+            fn.out_n[l] = t.out_p;
+            if (l < L - 1) fn.map_h[l] = tma_kmajor(g.H[n][l], t.out_p, g.Bm, t.out_p, 32);
+          }
+          const ppo::HeadNet& hn = h.net[n];
+          fn.n_out = hn.n_out;
+          fn.nh = hn.nh;
+          fn.map_w[L] = tma_kmajor(shadow_ + geo_.net[n][L].w, hp, hn.n_out, hp, hn.nh);
+          fn.map_wm = make_tma_2d_bf16(shadow_ + geo_.net[n][L].w, hp, hn.n_out, hp, 64, 32);
+          fn.map_d = tma_kmajor(g.D[n][L - 1], hp, g.Bm, hp, 32);
+          fn.bias[L] = params_ + geo_.net[n][L].b;
+          fn.in_p[L] = hp;
+          fn.out_n[L] = hn.nh;
+          fn.dw_slab = hn.dw_slab;
+        }
+        f.log_std = h.log_std;
+        f.act = h.act;
+        f.oldlp = h.oldlp;
+        f.adv = h.adv;
+        f.ret = h.ret;
+        f.part = h.part;
+        f.Bm = g.Bm;
+        f.A = A;
+        f.L = L;
+        f.hp = hp;
+        f.S_p = S_p;
+        f.clip = cfg_.clip;
+        f.vf_coef = cfg_.vf_coef;
+        f.ent_coef = cfg_.ent_coef;
+      }
     }
 
     // gradient assembly segments (fixed-order sums of slabs / partials into the flat grad)
@@ -873,13 +921,22 @@ void Trainer::values(Gmi& g) {
 
 void Trainer::train_minibatch(Gmi& g, int k, int adam_step) {
   const int L = geo_.L, A = geo_.A;
-  for (int l = 0; l < L; ++l) {
+  if (g.fused_fwd) {  // hidden forward (both nets) + head step, one launch
+    ppo::TrainFwdArgs f = g.fwd_args;
+    f.row0 = (long long)k * g.Bm;
+    double flop = 3.0 * 2.0 * (A + 1) * geo_.width[L] * g.Bm;
+    for (int l = 0; l < L; ++l) flop += g.flop_fwd[l];
+    timed(g.s, GMI_PH_FWD_GEMM, flop, 0.0, [&] { ppo::launch_train_fwd(f, g.head_grid, g.s); });
+    ++launches_;
+  }
+  for (int l = 0; l < L && !g.fused_fwd; ++l) {
     GemmParams P = g.fwd_train[l];
     if (l == 0) P.prob[0].a_row0 = P.prob[1].a_row0 = k * g.Bm;
     gemm(g, GMI_PH_FWD_GEMM, P, g.bn_fwd[l], 0, 0, EPI_BIAS_ELU, g.flop_fwd[l], g.ws_fwd[l]);
   }
   const double hflop = 2.0 * (A + 1) * geo_.width[L] * g.Bm;
-  if (g.fused_head) {  // head forward + loss + head input/weight grads + bias sums, one launch
+  if (g.fused_fwd) {
+  } else if (g.fused_head) {  // head forward + loss + head input/weight grads + bias sums, one launch
     ppo::HeadFusedArgs h = g.head_args;
     h.row0 = (long long)k * g.Bm;
     timed(g.s, GMI_PH_HEAD_LOSS, 3.0 * hflop, 0.0, [&] { ppo::launch_head_fused(h, g.head_grid, g.s); });
@@ -1245,6 +1302,19 @@ long long Trainer::get(const std::string& what, int gi, void* dst) {
   if (what == "ep_step") return copy(g.ep_step, N, 4);
   if (what == "ep_len") return copy(g.ep_len, N, 4);
   if (what == "ep_count") return copy(g.ep_count, N, 4);
+  if (what.size() == 3 && (what[0] == 'H' || what[0] == 'D')) {  // debug: H<net><layer> / D<net><layer>
+    const int n = what[1] - '0', l = what[2] - '0';
+    if (n < 0 || n > 1 || l < 0 || l >= geo_.L) invalid("bad activation name");
+    const long long w = geo_.wp[l + 1], rows = g.Bm;
+    if (dst) {
+      std::vector<uint16_t> raw((size_t)(rows * w));
+      const void* src = what[0] == 'H' ? (const void*)g.H[n][l] : (const void*)g.D[n][l];
+      GMI_CUDA_CHECK(cudaMemcpy(raw.data(), src, raw.size() * 2, cudaMemcpyDeviceToHost));
+      float* o = static_cast<float*>(dst);
+      for (size_t i = 0; i < raw.size(); ++i) o[i] = bf16_float(raw[i]);
+    }
+    return rows * w;
+  }
   if (what == "head_part") {  // per-block head-gradient / loss partial records (debug)
     const int parts = g.fused_head ? g.head_grid : ppo::head_loss_blocks(g.Bm);
     return copy(g.head_part, (long long)parts * ppo::head_partial_stride(geo_.A), 4);

@@ -141,6 +141,48 @@ def test_fused_rollout_matches_per_layer_path(cuda, monkeypatch, dims):
             np.testing.assert_allclose(fused.get(f), plain.get(f), rtol=1e-5, atol=1e-5)
 
 
+def _grad_pair(monkeypatch, env_first, env_second, dims, envs=200):
+    from paper_2206_08482_b200.ppo import PpoConfig, Trainer
+    S, A, hidden = dims
+    cfg = dict(obs_dim=S, act_dim=A, hidden=hidden, num_envs=envs)
+    if env_first:
+        monkeypatch.setenv(env_first, "1")
+    fused = Trainer(PpoConfig(**cfg))
+    if env_first:
+        monkeypatch.delenv(env_first)
+    if env_second:
+        monkeypatch.setenv(env_second, "1")
+    plain = Trainer(PpoConfig(**cfg))
+    B = envs * 32 // 4
+    rng = np.random.default_rng(S + A)
+    X = rng.uniform(-1, 1, (B, S)).astype(np.float32)
+    act = rng.standard_normal((B, A)).astype(np.float32)
+    oldlp = (rng.standard_normal(B) - 3).astype(np.float32)
+    adv = rng.standard_normal(B).astype(np.float32)
+    ret = rng.standard_normal(B).astype(np.float32)
+    return fused.minibatch_grad(X, act, oldlp, adv, ret), plain.minibatch_grad(X, act, oldlp, adv, ret)
+
+
+@pytest.mark.parametrize("dims", [(60, 8, [256, 256, 256]), (12, 3, [64]), (40, 20, [96, 160, 64]),
+                                  (100, 1, [128, 256, 192])])
+def test_fused_train_forward_matches_per_layer_path(cuda, monkeypatch, dims):
+    """cuda/train_fwd.cu (all hidden layers on chip + the fused head step, one launch per
+    minibatch) vs per-layer forward GEMMs + the fused head kernel. Same operands, MMA K order,
+    bias/ELU and loss code; only the head weight-gradient summation order (per-tile fp32
+    partials in registers vs one TMEM accumulator) differs. 1000 rows: a ragged last tile."""
+    S, A, hidden = dims
+    g1, g2 = _grad_pair(monkeypatch, "GMI_TRAIN_FWD", None, dims, envs=1000)
+    lay = param_layout(S, A, hidden)
+    for key, t in lay.items():
+        if not isinstance(key, tuple):
+            continue
+        for part, n in (("w", t["out_p"] * t["in_p"]), ("b", t["out_p"])):
+            a, b = g1[t[part]:t[part] + n], g2[t[part]:t[part] + n]
+            assert np.linalg.norm(a - b) <= 1e-5 * (np.linalg.norm(b) + 1e-12), (key, part)
+    ls = slice(lay["log_std"], lay["log_std"] + A)
+    np.testing.assert_allclose(g1[ls], g2[ls], rtol=1e-5, atol=1e-7)
+
+
 @pytest.mark.parametrize("dims", [(12, 3, [64, 64]), (60, 8, [256, 256, 256]), (40, 20, [96, 160])])
 def test_fused_head_matches_per_kernel_path(cuda, monkeypatch, dims):
     """cuda/head_fused.cu (head forward + loss + head input / weight gradients + bias sums in
