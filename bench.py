@@ -44,6 +44,8 @@ def parse():
                    help="1: serving GMI + trainer GMI per GPU with an experience channel (BASELINE config 4)")
     p.add_argument("--serving-sms", type=int, default=0, help="SMs of the serving GMI (decoupled mode)")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-multi-gmi", action="store_true",
+                   help="skip the decoupled multi-GMI layout measured beside the single-context one")
     p.add_argument("--cpu-sample-envs", type=int, default=64)
     return p.parse_args()
 
@@ -287,6 +289,13 @@ def main():
     iter_ms_instr = t2.elapsed_time(t3)
     trainer.set_instrument(False)
 
+    multi = None
+    if not cfg.decoupled and not args.no_multi_gmi:
+        trainer.close()
+        multi = time_decoupled(args, cfg, world, rank, barrier)
+        if multi and rank == 0:
+            multi["vs_single_context"] = multi["value"] / value
+
     if rank == 0:
         peak_tf, peak_gbs, peak_src = measured_peaks()
         gemm_ms, gemm_flop = ist.gemm_ms, ist.gemm_flop
@@ -328,11 +337,53 @@ def main():
                     "api": "gmi_ppo_iteration (synchronous C-ABI call per step)"},
             "gpu_launches": launches,
             "clocks": clk,
+            "multi_gmi": multi,
         }
         print(json.dumps(line), flush=True)
-    trainer.close()
+    if multi is None:
+        trainer.close()
     if world > 1:
         dist.destroy_process_group()
+
+
+def time_decoupled(args, cfg, world, rank, barrier):
+    """The same workload in the decoupled multi-GMI layout (BASELINE configs[3] per GPU): a
+    16-SM serving GMI (simulator + agent) streams experience to a 132-SM trainer GMI through the
+    device channel, one-iteration policy lag. Device-timed like the main number, max over ranks."""
+    import copy
+    import torch
+    import torch.distributed as dist
+    from paper_2206_08482_b200.ppo import Trainer, nccl_unique_id
+
+    dc = copy.deepcopy(cfg)
+    dc.decoupled, dc.gmis_per_gpu, dc.gmi_backend = 1, 1, 1
+    dc.serving_sms = args.serving_sms or 16
+    nid = None
+    if world > 1:
+        obj = [nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nid = obj[0]
+    t = Trainer(dc, nid)
+    upd = torch.cuda.ExternalStream(t.stream(-1))
+    for _ in range(max(3, args.warmup)):
+        t.iteration()
+    barrier()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(upd)
+    for _ in range(args.steps):
+        t.iteration_async()
+    b.record(upd)
+    st = t.synchronize()
+    barrier()
+    ms = torch.tensor([a.elapsed_time(b)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    t.close()
+    value = st.env_steps * world * args.steps / (ms.item() / 1e3)
+    return {"layout": f"decoupled: serving GMI ({dc.serving_sms} SMs, simulator+agent) + trainer GMI "
+                      f"(remaining SMs) per B200, device experience channel (configs/at_4096env_decoupled.cfg)",
+            "semantics": "one-iteration policy lag (PAPER.md:378-407); behaviour log-probs recorded",
+            "value": value, "unit": UNIT, "ms_per_step": ms.item() / args.steps}
 
 
 def working_set_mb(cfg, envs):

@@ -265,33 +265,49 @@ __global__ void __launch_bounds__(gemm_threads(EPI) + 128 * CS, 1)
       if constexpr (EPI == EPI_DACT) load_aux(h, hv);
       ptx::mbar_wait(&tfull_bar[buf], (lt >> 1) & 1);
       ptx::tc_fence_after();
-#pragma unroll 1
-      for (int c = h; c < kChunks; c += W) {
+      // 16-column units of chunks c = h, h + W, ...: the TMEM load of the next unit is issued
+      // before this unit's math, and the staging buffer is claimed only after the math, so TMEM
+      // latency and the previous TMA store overlap useful work (the epilogue is latency-bound
+      // at K <= 256); x16 units keep two loads in flight within the register budget.
+      constexpr int kUnits = 2 * ((kChunks + W - 1) / W);
+      const uint32_t trow = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + buf * BN;
+      uint32_t rr[2][16];
+      if (n0 + h * 32 < pr.N) ptx::tmem_ld_32x32b_x16(trow + h * 32, rr[0]);
+#pragma unroll
+      for (int i = 0; i < kUnits; ++i) {
+        const int c = h + (i >> 1) * W, half = i & 1;
         const int col0 = n0 + c * 32;
-        if (col0 >= pr.N) break;  // warp-uniform
-        if constexpr (EPI == EPI_DACT) load_aux(c + W, hn);
-        uint32_t r[32];
-        ptx::tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + buf * BN + c * 32, r);
+        if (c >= kChunks || col0 >= pr.N) break;  // warp-uniform
+        uint32_t(&r)[16] = rr[i & 1];
+        if constexpr (EPI == EPI_DACT) {
+          if (half == 0) load_aux(c + W, hn);
+        }
         ptx::tmem_ld_wait();
+        if (i + 1 < kUnits) {
+          const int cn = h + ((i + 1) >> 1) * W;
+          if (cn < kChunks && n0 + cn * 32 < pr.N) ptx::tmem_ld_32x32b_x16(trow + cn * 32 + ((i + 1) & 1) * 16, rr[(i + 1) & 1]);
+        }
         if (nkb == 0) {
 #pragma unroll
-          for (int j = 0; j < 32; ++j) r[j] = 0u;
+          for (int j = 0; j < 16; ++j) r[j] = 0u;
         }
         uint8_t* st = stage_base + sbuf * L::kStaging;
-        if (lane == 0) ptx::bulk_wait_read<L::kStagingBufs - 1>();  // this staging buffer's last store has read it
-        __syncwarp();
         if constexpr (EPI == EPI_F32) {
+          if (half == 0) {
+            if (lane == 0) ptx::bulk_wait_read<L::kStagingBufs - 1>();  // this staging buffer's last store has read it
+            __syncwarp();
+          }
           // 32 fp32 = 8 x 16 B per row; SWIZZLE_128B: chunk ^= row & 7
 #pragma unroll
-          for (int j = 0; j < 8; ++j)
-            *reinterpret_cast<uint4*>(st + lane * 128 + ((j ^ (lane & 7)) << 4)) =
+          for (int j = 0; j < 4; ++j)
+            *reinterpret_cast<uint4*>(st + lane * 128 + (((half * 4 + j) ^ (lane & 7)) << 4)) =
                 make_uint4(r[4 * j], r[4 * j + 1], r[4 * j + 2], r[4 * j + 3]);
         } else {
-          uint32_t packed[16];
+          uint32_t packed[8];
           if constexpr (EPI == EPI_BIAS_ELU) {
-            const float4* b4 = reinterpret_cast<const float4*>(pr.bias + col0);
+            const float4* b4 = reinterpret_cast<const float4*>(pr.bias + col0 + half * 16);
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
+            for (int j = 0; j < 4; ++j) {
               const float4 b = __ldg(b4 + j);
               const float2 y0 = bias_elu2(make_float2(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1])),
                                           make_float2(b.x, b.y));
@@ -302,8 +318,9 @@ __global__ void __launch_bounds__(gemm_threads(EPI) + 128 * CS, 1)
             }
           } else {  // EPI_DACT
 #pragma unroll
-            for (int qd = 0; qd < 4; ++qd) {
-              const uint32_t hw[4] = {hv[qd].x, hv[qd].y, hv[qd].z, hv[qd].w};
+            for (int qd = 0; qd < 2; ++qd) {
+              const uint4 hq = half ? hv[2 + qd] : hv[qd];
+              const uint32_t hw[4] = {hq.x, hq.y, hq.z, hq.w};
 #pragma unroll
               for (int x = 0; x < 4; ++x) {
                 const int j = qd * 8 + x * 2;
@@ -311,25 +328,33 @@ __global__ void __launch_bounds__(gemm_threads(EPI) + 128 * CS, 1)
                 packed[j / 2] = pack_bf16(d.x, d.y);
               }
             }
+            if (half == 1) {
 #pragma unroll
-            for (int qd = 0; qd < 4; ++qd) hv[qd] = hn[qd];
+              for (int qd = 0; qd < 4; ++qd) hv[qd] = hn[qd];
+            }
+          }
+          if (half == 0) {
+            if (lane == 0) ptx::bulk_wait_read<L::kStagingBufs - 1>();  // this staging buffer's last store has read it
+            __syncwarp();
           }
           // 32 bf16 = 4 x 16 B per row; SWIZZLE_64B: chunk ^= (row >> 1) & 3
 #pragma unroll
-          for (int j = 0; j < 4; ++j)
-            *reinterpret_cast<uint4*>(st + lane * 64 + ((j ^ ((lane >> 1) & 3)) << 4)) =
+          for (int j = 0; j < 2; ++j)
+            *reinterpret_cast<uint4*>(st + lane * 64 + (((half * 2 + j) ^ ((lane >> 1) & 3)) << 4)) =
                 make_uint4(packed[4 * j], packed[4 * j + 1], packed[4 * j + 2], packed[4 * j + 3]);
         }
-        ptx::fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0) {
-          if constexpr (EPI == EPI_F32)
-            ptx::tma_store_3d(&pr.map_out, st, col0, rbase, split);
-          else
-            ptx::tma_store_2d(&pr.map_out, st, col0, rbase + pr.out_row0);
-          ptx::bulk_commit();
+        if (half == 1) {
+          ptx::fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            if constexpr (EPI == EPI_F32)
+              ptx::tma_store_3d(&pr.map_out, st, col0, rbase, split);
+            else
+              ptx::tma_store_2d(&pr.map_out, st, col0, rbase + pr.out_row0);
+            ptx::bulk_commit();
+          }
+          sbuf = (sbuf + 1) % L::kStagingBufs;
         }
-        sbuf = (sbuf + 1) % L::kStagingBufs;
       }
       ptx::tc_fence_before();
       __syncwarp();

@@ -44,6 +44,14 @@ constexpr uint32_t kWStage = 256 * 128;
 constexpr uint32_t kOffBar = 2 * kActBytes + kStages * kWStage;
 constexpr uint32_t kSmem = kOffBar + 512 + 1024;  // barriers + per-action constants + alignment
 
+__device__ __forceinline__ void stamp(unsigned long long* tr, int ti, int k) {
+  if (tr && blockIdx.x == 0 && ti < 4) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    tr[ti * 16 + k] = t;
+  }
+}
+
 __device__ __forceinline__ void pair_bar(int id) { asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory"); }
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory"); }
 
@@ -155,7 +163,10 @@ __global__ void __launch_bounds__(kThreads, 1) train_fwd_kernel(const __grid_con
           const uint32_t in = ptx::smem_u32((l & 1) ? buf1 : buf0);
           const int K = nw.in_p[l];
           const int nk = (K + 63) / 64;
-          if (l == 0) ptx::mbar_wait(obs_full, ti & 1);
+          if (l == 0) {
+            ptx::mbar_wait(obs_full, ti & 1);
+            stamp(a.trace, ti, 11);
+          }
           for (int kc = 0; kc < nk; ++kc, ++it) {
             if (l > 0 && kc == 0) ptx::mbar_wait(act_lo, (ph_lo++) & 1);
             if (l > 0 && kc == 2) ptx::mbar_wait(act_hi, (ph_hi++) & 1);
@@ -177,6 +188,7 @@ __global__ void __launch_bounds__(kThreads, 1) train_fwd_kernel(const __grid_con
         const uint32_t hb = tmem + ((u - 1) & 1) * 256;
         const uint32_t acc2 = tmem + (u & 1) * 256;
         ptx::mbar_wait(g_ready, ti & 1);
+        stamp(a.trace, ti, 12);
         const int s = it % kStages;
         ptx::mbar_wait(&wfull[s], (it / kStages) & 1);
         ptx::tc_fence_after();
@@ -231,8 +243,10 @@ __global__ void __launch_bounds__(kThreads, 1) train_fwd_kernel(const __grid_con
       }
     };
     int accph = 0;
-    for (int j = cta; j < mtiles; j += ctas) {
+    unsigned long long* tr = (warp == 2 && lane == 0) ? a.trace : nullptr;
+    for (int j = cta, ti = 0; j < mtiles; j += ctas, ++ti) {
       const int grow0 = j * kRows + q * 32;  // minibatch row of this warp quarter's first row
+      stamp(tr, ti, 0);
       // ---- hidden layers
       for (int l = 0; l < L; ++l) {
         const uint32_t acc = tmem + (accph & 1) * 256;
@@ -246,6 +260,7 @@ __global__ void __launch_bounds__(kThreads, 1) train_fwd_kernel(const __grid_con
         }
         ptx::mbar_wait_sleep(acc_full, accph & 1);
         ++accph;
+        stamp(tr, ti, 1 + l);
         ptx::tc_fence_after();
         const float* bias = nw.bias[l];
         const int nchunks = nw.out_n[l] / 32;
@@ -282,6 +297,7 @@ __global__ void __launch_bounds__(kThreads, 1) train_fwd_kernel(const __grid_con
           __syncwarp();
           if (lane == 0) ptx::mbar_arrive(pass == 0 ? act_lo : act_hi);
         }
+        stamp(tr, ti, 4 + l);
       }
       // ---- head MMA1 -> per-row loss -> G (column group 0; the other groups go ahead)
       if (h == 0) {
@@ -301,6 +317,7 @@ __global__ void __launch_bounds__(kThreads, 1) train_fwd_kernel(const __grid_con
           }
         }
         ptx::mbar_wait_sleep(acc_full, accph & 1);
+        stamp(tr, ti, 7);
         ptx::tc_fence_after();
         uint32_t r[32];
         ptx::tmem_ld_32x32b_x32(tmem + (accph & 1) * 256 + (static_cast<uint32_t>(q * 32) << 16), r);
@@ -357,6 +374,7 @@ __global__ void __launch_bounds__(kThreads, 1) train_fwd_kernel(const __grid_con
         ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(g_ready);
+        stamp(tr, ti, 8);
       } else {
         // the other groups still observe the head phase: an mbarrier parity wait is only
         // meaningful for the barrier's current or just-completed phase
@@ -368,6 +386,7 @@ __global__ void __launch_bounds__(kThreads, 1) train_fwd_kernel(const __grid_con
       const uint32_t acc2 = tmem + (accph & 1) * 256;
       ptx::mbar_wait_sleep(acc_full, accph & 1);
       ++accph;
+      stamp(tr, ti, 9);
       ptx::tc_fence_after();
       {
         const int half = h >> 1, col = half * 32 + (h & 1) * 16;
@@ -414,6 +433,7 @@ __global__ void __launch_bounds__(kThreads, 1) train_fwd_kernel(const __grid_con
         }
         if ((c >> 1) * 64 < hp) store_box(&nw.map_d, hlb, c >> 1, grow0);
       }
+      stamp(tr, ti, 10);
       ptx::tc_fence_before();
     }
 

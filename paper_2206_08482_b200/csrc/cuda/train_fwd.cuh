@@ -34,6 +34,7 @@ struct alignas(64) TrainFwdArgs {
   long long row0;     // first epoch-copy row of this minibatch
   int Bm, A, L, hp, S_p;
   float clip, vf_coef, ent_coef;
+  unsigned long long* trace;  // optional [4 tiles][16] globaltimer stamps of CTA 0 (development aid)
 };
 
 // Whole forward of one minibatch (hidden layers on chip, H_1..H_{L-1} stored for the backward)

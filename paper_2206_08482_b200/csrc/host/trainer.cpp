@@ -645,6 +645,8 @@ void Trainer::build_plans() {
         f.clip = cfg_.clip;
         f.vf_coef = cfg_.vf_coef;
         f.ent_coef = cfg_.ent_coef;
+        const char* trace = std::getenv("GMI_TRAIN_FWD_TRACE");
+        if (trace && trace[0] == '1') f.trace = reinterpret_cast<unsigned long long*>(dev(64 * 8));
       }
     }
 
@@ -1318,6 +1320,10 @@ long long Trainer::get(const std::string& what, int gi, void* dst) {
   if (what == "head_part") {  // per-block head-gradient / loss partial records (debug)
     const int parts = g.fused_head ? g.head_grid : ppo::head_loss_blocks(g.Bm);
     return copy(g.head_part, (long long)parts * ppo::head_partial_stride(geo_.A), 4);
+  }
+  if (what == "train_fwd_trace") {  // GMI_TRAIN_FWD_TRACE=1: stamps of CTA 0, last minibatch
+    if (!g.fwd_args.trace) invalid("train-forward trace not enabled (GMI_TRAIN_FWD_TRACE=1)");
+    return copy(g.fwd_args.trace, 64, 8);
   }
   if (what == "rollout_trace") {  // GMI_ROLLOUT_TRACE=1: globaltimer stamps of CTA 0 (int64)
     if (!g.roll_args.trace) invalid("rollout trace not enabled (GMI_ROLLOUT_TRACE=1)");
