@@ -67,6 +67,19 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
+// Development trace (tools/gemm_trace.py): compiled in only with `make TRACE=1` (-DGMI_TRACE).
+__device__ __forceinline__ void gemm_stamp(unsigned long long* tr, int lt, int k) {
+#ifdef GMI_TRACE
+  if (tr && blockIdx.x == 0 && lt < 8) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    tr[lt * 16 + k] = t;
+  }
+#else
+  (void)tr, (void)lt, (void)k;
+#endif
+}
+
 template <int BN, int EPI, int WS>
 struct GemmSmem {
   static constexpr int kEpiWarps = gemm_epi_warps(EPI);
@@ -176,11 +189,12 @@ __global__ void __launch_bounds__(gemm_threads(EPI) + 128 * CS, 1)
           ptx::tma_load_2d(sb, &pr.map_b, bar, k0, n0 + pr.b_row0);
         }
       };
-      int it = 0;
-      for (int tile = blockIdx.x; tile < ntile_total; tile += gridDim.x) {
+      int it = 0, plt = 0;
+      for (int tile = blockIdx.x; tile < ntile_total; tile += gridDim.x, ++plt) {
         int prob, split, m0, n0, kb0, nkb;
         decode(tile, prob, split, m0, n0, kb0, nkb);
         const GemmProblem& pr = P.prob[prob];
+        gemm_stamp(P.trace, plt, 7);
         for (int i = 0; i < nkb; ++i, ++it) {
           const int s = it % S;
           if (it >= S) ptx::mbar_wait(&empty_bar[s], ((it / S) - 1) & 1);
@@ -200,6 +214,7 @@ __global__ void __launch_bounds__(gemm_threads(EPI) + 128 * CS, 1)
           }
           if constexpr (!WS) load_b(pr, sa + L::kA, &full_bar[s], n0, k0);
         }
+        gemm_stamp(P.trace, plt, 8);
       }
     }
   } else if (warp == 1) {
@@ -210,12 +225,15 @@ __global__ void __launch_bounds__(gemm_threads(EPI) + 128 * CS, 1)
         int prob, split, m0, n0, kb0, nkb;
         decode(tile, prob, split, m0, n0, kb0, nkb);
         const int buf = lt & 1;
+        gemm_stamp(P.trace, lt, 0);
         if (lt >= 2) ptx::mbar_wait(&tempty_bar[buf], ((lt >> 1) - 1) & 1);
+        gemm_stamp(P.trace, lt, 1);
         ptx::tc_fence_after();
         const uint32_t acc = tmem_base + buf * BN;
         for (int i = 0; i < nkb; ++i, ++it) {
           const int s = it % S;
           ptx::mbar_wait(&full_bar[s], (it / S) & 1);
+          if (i == 0) gemm_stamp(P.trace, lt, 2);
           ptx::tc_fence_after();
           const uint32_t sa = ptx::smem_u32(smem + s * L::kStage);
           const uint32_t sb = WS ? ptx::smem_u32(b_res + i * L::kB) : sa + L::kA;
@@ -232,6 +250,7 @@ __global__ void __launch_bounds__(gemm_threads(EPI) + 128 * CS, 1)
           ptx::mma_commit(&empty_bar[s]);
         }
         ptx::mma_commit(&tfull_bar[buf]);
+        gemm_stamp(P.trace, lt, 3);
       }
     }
   } else if (warp < 2 + kEpiWarps) {
@@ -263,7 +282,9 @@ __global__ void __launch_bounds__(gemm_threads(EPI) + 128 * CS, 1)
         }
       };
       if constexpr (EPI == EPI_DACT) load_aux(h, hv);
+      unsigned long long* etr = (warp == 2 && lane == 0) ? P.trace : nullptr;
       ptx::mbar_wait(&tfull_bar[buf], (lt >> 1) & 1);
+      gemm_stamp(etr, lt, 4);
       ptx::tc_fence_after();
       // 16-column units of chunks c = h, h + W, ...: the TMEM load of the next unit is issued
       // before this unit's math, and the staging buffer is claimed only after the math, so TMEM
@@ -354,11 +375,13 @@ __global__ void __launch_bounds__(gemm_threads(EPI) + 128 * CS, 1)
             ptx::bulk_commit();
           }
           sbuf = (sbuf + 1) % L::kStagingBufs;
+          gemm_stamp(etr, lt, (i >> 1) == 0 ? 5 : 9);
         }
       }
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(&tempty_bar[buf]);
+      gemm_stamp(etr, lt, 6);
     }
     if (lane == 0) ptx::bulk_wait<0>();
   } else if constexpr (CS) {

@@ -39,6 +39,7 @@ struct alignas(64) GemmParams {
   GemmProblem prob[2];
   int num_problems;
   int splits;
+  unsigned long long* trace;  // optional [8 tiles][16] globaltimer stamps of CTA 0 (development aid)
 };
 
 }  // namespace gmi

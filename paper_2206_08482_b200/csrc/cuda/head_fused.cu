@@ -23,6 +23,7 @@
 #include "../host/errors.hpp"
 #include "gemm.cuh"
 #include "head_fused.cuh"
+#include "head_loss.cuh"
 #include "launch.cuh"
 #include "ppo_common.cuh"
 
@@ -170,18 +171,22 @@ __global__ void __launch_bounds__(kThreads, 1) head_fused_kernel(const __grid_co
     const int row = q * 32 + lane;
     const float invB = 1.0f / float(a.Bm);
     uint8_t* stg = smem + kOffStg + (warp - 2) * 2048;
-    // per-action constants of the loss, once per CTA: log_std and exp(log_std)
+    // per-action constants of the loss, once per CTA: log_std, exp(log_std), head bias
     float* cst = reinterpret_cast<float*>(smem + kOffBar + 128);
+    float* lacc = red + q * 128;  // this lane quarter's per-action sums [0, 64) and statistics [64, 68)
     if (threadIdx.x - 64 < a.A) {
       const float ls = a.log_std[threadIdx.x - 64];
       cst[threadIdx.x - 64] = ls;
       cst[32 + threadIdx.x - 64] = expf(ls);
     }
+    if (threadIdx.x - 64 < nout) cst[64 + threadIdx.x - 64] = hn.bias[threadIdx.x - 64];
+    if (h == 0 && lane == 0)
+      for (int i = 0; i < 128; ++i) lacc[i] = 0.f;
     epi_bar();
-    float sg[MAXA], sl[MAXA];  // running db_head / dlog_std of this thread's rows
-#pragma unroll
-    for (int i = 0; i < MAXA; ++i) sg[i] = sl[i] = 0.f;
     float st[4] = {0.f, 0.f, 0.f, 0.f};
+    float sg[kLossRegAcc<MAXA> ? MAXA : 1], sl[kLossRegAcc<MAXA> ? MAXA : 1];  // running per-action sums (A <= 8)
+#pragma unroll
+    for (int i = 0; i < (kLossRegAcc<MAXA> ? MAXA : 1); ++i) sg[i] = sl[i] = 0.f;
     int it = 0;
     for (int j = cta; j < mtiles; j += ctas, ++it) {
       const int grow = j * kRows + row;
@@ -191,13 +196,15 @@ __global__ void __launch_bounds__(kThreads, 1) head_fused_kernel(const __grid_co
         // log-prob, advantage and return are fetched before the accumulator wait so their
         // latency overlaps the head MMA.
         const long long rr = a.row0 + grow;
-        float act_r[MAXA];
+        float act_r[MAXA <= 16 ? MAXA : 1];
         float oldlp = 0.f, adv = 0.f, ret = 0.f;
         if (valid) {
           if (net == 0) {
+            if constexpr (MAXA <= 16) {
 #pragma unroll
-            for (int i = 0; i < MAXA; ++i)
-              if (i < nout) act_r[i] = a.act[rr * nout + i];
+              for (int i = 0; i < MAXA; ++i)
+                if (i < nout) act_r[i] = a.act[rr * nout + i];
+            }
             oldlp = a.oldlp[rr];
             adv = a.adv[rr];
           } else {
@@ -209,59 +216,8 @@ __global__ void __launch_bounds__(kThreads, 1) head_fused_kernel(const __grid_co
         uint32_t r[32];
         ptx::tmem_ld_32x32b_x32(tmem + kTmemAcc1 + (static_cast<uint32_t>(q * 32) << 16), r);
         ptx::tmem_ld_wait();
-        uint8_t* grow_s = sG + row * 128;
-        auto put_g = [&](int col, float v) {  // bf16 into the SW128 G tile
-          *reinterpret_cast<__nv_bfloat16*>(grow_s + ((((col >> 3) ^ (row & 7))) << 4) + (col & 7) * 2) =
-              __float2bfloat16_rn(v);
-        };
-        if (net == 0) {
-          const int A = nout;
-          float gmu[MAXA];
-#pragma unroll
-          for (int i = 0; i < MAXA; ++i) gmu[i] = 0.f;
-          if (valid) {
-            float mu[MAXA], z[MAXA], sig[MAXA], ls[MAXA];
-            float lp = 0.f;
-#pragma unroll
-            for (int i = 0; i < MAXA; ++i)
-              if (i < A) {
-                mu[i] = __uint_as_float(r[i]) + hn.bias[i];
-                ls[i] = cst[i];
-                sig[i] = cst[32 + i];
-                z[i] = (act_r[i] - mu[i]) / sig[i];
-                lp += -0.5f * z[i] * z[i] - ls[i] - kLog2PiHalf;
-              }
-            const float ratio = expf(lp - oldlp);
-            const float s1 = ratio * adv;
-            const float rc = fminf(fmaxf(ratio, 1.f - a.clip), 1.f + a.clip);
-            const float s2 = rc * adv;
-            const bool take1 = s1 <= s2;
-            const float glp = take1 ? -s1 * invB : 0.f;
-#pragma unroll
-            for (int i = 0; i < MAXA; ++i)
-              if (i < A) {
-                gmu[i] = glp * z[i] / sig[i];
-                sg[i] += gmu[i];
-                sl[i] += glp * (z[i] * z[i] - 1.f) - a.ent_coef * invB;
-              }
-            st[0] += -(take1 ? s1 : s2);
-            st[2] += oldlp - lp;
-            st[3] += (ratio < 1.f - a.clip || ratio > 1.f + a.clip) ? 1.f : 0.f;
-          }
-#pragma unroll
-          for (int i = 0; i < MAXA; ++i)
-            if (i < A) put_g(i, gmu[i]);
-        } else {
-          float gv = 0.f;
-          if (valid) {
-            const float v = __uint_as_float(r[0]) + hn.bias[0];
-            const float verr = v - ret;
-            gv = a.vf_coef * verr * invB;
-            sg[0] += gv;
-            st[1] += 0.5f * a.vf_coef * verr * verr;
-          }
-          put_g(0, gv);
-        }
+        head_row_loss<MAXA>(net, r, cst, nout, NH, valid, a.act + rr * nout, act_r, oldlp, adv, ret, a.clip,
+                            a.vf_coef, a.ent_coef, invB, sG + row * 128, row, lacc, st, sg, sl);
         ptx::fence_proxy_async_smem();
         ptx::tc_fence_before();
         __syncwarp();
@@ -331,37 +287,26 @@ __global__ void __launch_bounds__(kThreads, 1) head_fused_kernel(const __grid_co
         for (int o = 0; o < nout; ++o)
           hn.dw_slab[((long long)cta * nout + o) * hp + k] = (it > 0) ? __uint_as_float(r[o]) : 0.f;
     }
-    // (c) head-bias / log-std gradients and loss statistics (warps with h == 0 hold them)
+    // (c) head-bias / log-std gradients and loss statistics: per-quarter records in `red`
     const int stride = head_partial_stride(a.A);
-    if (h == 0) {
-      auto put = [&](int col, float x) {
-        x = warp_sum(x);
-        if (lane == 0) red[q * 128 + col] = x;
-      };
-      for (int col = 0; col < stride; ++col) {  // zero the record first (fields of the other net)
-        if (lane == 0) red[q * 128 + col] = 0.f;
-      }
-      __syncwarp();
-      if (net == 0) {
-#pragma unroll
-        for (int i = 0; i < MAXA; ++i)
-          if (i < a.A) {
-            put(i, sg[i]);
-            put(a.A + 1 + i, sl[i]);
-          }
-        put(2 * a.A + 1, st[0]);
-        put(2 * a.A + 3, st[2]);
-        put(2 * a.A + 4, st[3]);
-      } else {
-        put(a.A, sg[0]);
-        put(2 * a.A + 2, st[1]);
-      }
-    }
+    if (h == 0) head_loss_flush<MAXA>(nout, lacc, st, sg, sl);
     epi_bar();
     if (h == 0 && q == 0)
-      for (int col = lane; col < stride; col += 32)
+      for (int col = lane; col < stride; col += 32) {
+        int src = -1;  // offset inside a quarter record, or -1 for the other net's fields
+        if (net == 0) {
+          if (col < a.A) src = col;
+          else if (col > a.A && col <= 2 * a.A) src = 32 + col - a.A - 1;
+          else if (col == 2 * a.A + 1) src = 64;
+          else if (col == 2 * a.A + 3) src = 66;
+          else if (col == 2 * a.A + 4) src = 67;
+        } else {
+          if (col == a.A) src = 0;
+          else if (col == 2 * a.A + 2) src = 65;
+        }
         a.part[(long long)blockIdx.x * stride + col] =
-            ((red[col] + red[128 + col]) + red[256 + col]) + red[384 + col];
+            src < 0 ? 0.f : ((red[src] + red[128 + src]) + red[256 + src]) + red[384 + src];
+      }
     if (lane == 0) ptx::bulk_wait<0>();
   }
 

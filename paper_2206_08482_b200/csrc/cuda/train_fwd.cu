@@ -28,6 +28,7 @@
 #include "gemm.cuh"
 #include "launch.cuh"
 #include "ppo_common.cuh"
+#include "head_loss.cuh"
 #include "train_fwd.cuh"
 
 namespace gmi::ppo {
@@ -42,14 +43,22 @@ constexpr uint32_t kChunk = kRows * 128;  // [128 rows][64 bf16], SW128
 constexpr uint32_t kActBytes = 4 * kChunk;
 constexpr uint32_t kWStage = 256 * 128;
 constexpr uint32_t kOffBar = 2 * kActBytes + kStages * kWStage;
-constexpr uint32_t kSmem = kOffBar + 512 + 1024;  // barriers + per-action constants + alignment
+constexpr int kQ = 68;                                 // per-quarter loss record: sums [0, 64) + statistics
+constexpr uint32_t kOffLacc = kOffBar + 512;
+constexpr uint32_t kSmem = kOffLacc + 4 * kQ * 4 + 1024;  // barriers + constants + records + alignment
+static_assert(kSmem <= 232448, "shared memory budget");
 
+// Development trace (tools/train_fwd_trace.py): compiled in only with `make TRACE=1`.
 __device__ __forceinline__ void stamp(unsigned long long* tr, int ti, int k) {
+#ifdef GMI_TRACE
   if (tr && blockIdx.x == 0 && ti < 4) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     tr[ti * 16 + k] = t;
   }
+#else
+  (void)tr, (void)ti, (void)k;
+#endif
 }
 
 __device__ __forceinline__ void pair_bar(int id) { asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory"); }
@@ -75,7 +84,8 @@ __global__ void __launch_bounds__(kThreads, 1) train_fwd_kernel(const __grid_con
   uint64_t* dw_drained = obs_full + 6;
   uint64_t* h_stored = obs_full + 7;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(obs_full + 8);
-  float* cst = reinterpret_cast<float*>(smem + kOffBar + 256);  // [32] log_std, [32] exp(log_std)
+  float* cst = reinterpret_cast<float*>(smem + kOffBar + 128);  // log_std, exp(log_std), head bias
+  float* red = reinterpret_cast<float*>(smem + kOffLacc);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int net = blockIdx.x & 1;
@@ -216,16 +226,20 @@ __global__ void __launch_bounds__(kThreads, 1) train_fwd_kernel(const __grid_con
     const bool even = (h & 1) == 0;
     const float invB = 1.0f / float(a.Bm);
     const int et = threadIdx.x - 64;
+    float* lacc = red + q * kQ;  // this lane quarter's per-action sums [0, 64) and statistics [64, 68)
     if (et < a.A) {
       const float ls = a.log_std[et];
       cst[et] = ls;
       cst[32 + et] = expf(ls);
     }
+    if (et < nout) cst[64 + et] = nw.bias[L][et];
+    if (h == 0 && lane == 0)
+      for (int i = 0; i < kQ; ++i) lacc[i] = 0.f;
     epi_bar();
-    float sg[MAXA], sl[MAXA];  // running db_head / dlog_std of this thread's rows (h == 0)
-#pragma unroll
-    for (int i = 0; i < MAXA; ++i) sg[i] = sl[i] = 0.f;
     float st[4] = {0.f, 0.f, 0.f, 0.f};
+    float sg[kLossRegAcc<MAXA> ? MAXA : 1], sl[kLossRegAcc<MAXA> ? MAXA : 1];  // running per-action sums (A <= 8)
+#pragma unroll
+    for (int i = 0; i < (kLossRegAcc<MAXA> ? MAXA : 1); ++i) sg[i] = sl[i] = 0.f;
     float dwacc[16];  // head weight gradient of hidden unit (h >> 1) * 128 + row, outputs (h & 1) * 16 + i
 #pragma unroll
     for (int i = 0; i < 16; ++i) dwacc[i] = 0.f;
@@ -303,13 +317,15 @@ __global__ void __launch_bounds__(kThreads, 1) train_fwd_kernel(const __grid_con
       if (h == 0) {
         const long long rr = a.row0 + j * kRows + row;
         const bool valid = j * kRows + row < a.Bm;
-        float act_r[MAXA];
+        float act_r[MAXA <= 16 ? MAXA : 1];
         float oldlp = 0.f, adv = 0.f, ret = 0.f;
         if (valid) {
           if (net == 0) {
+            if constexpr (MAXA <= 16) {
 #pragma unroll
-            for (int i = 0; i < MAXA; ++i)
-              if (i < nout) act_r[i] = a.act[rr * nout + i];
+              for (int i = 0; i < MAXA; ++i)
+                if (i < nout) act_r[i] = a.act[rr * nout + i];
+            }
             oldlp = a.oldlp[rr];
             adv = a.adv[rr];
           } else {
@@ -322,54 +338,10 @@ __global__ void __launch_bounds__(kThreads, 1) train_fwd_kernel(const __grid_con
         uint32_t r[32];
         ptx::tmem_ld_32x32b_x32(tmem + (accph & 1) * 256 + (static_cast<uint32_t>(q * 32) << 16), r);
         ptx::tmem_ld_wait();
-        float gv[32];
-#pragma unroll
-        for (int i = 0; i < 32; ++i) gv[i] = 0.f;
-        if (net == 0) {
-          if (valid) {
-            float mu[MAXA], z[MAXA], sig[MAXA];
-            float lp = 0.f;
-#pragma unroll
-            for (int i = 0; i < MAXA; ++i)
-              if (i < nout) {
-                mu[i] = __uint_as_float(r[i]) + nw.bias[L][i];
-                sig[i] = cst[32 + i];
-                z[i] = (act_r[i] - mu[i]) / sig[i];
-                lp += -0.5f * z[i] * z[i] - cst[i] - kLog2PiHalf;
-              }
-            const float ratio = expf(lp - oldlp);
-            const float s1 = ratio * adv;
-            const float rc = fminf(fmaxf(ratio, 1.f - a.clip), 1.f + a.clip);
-            const float s2 = rc * adv;
-            const bool take1 = s1 <= s2;
-            const float glp = take1 ? -s1 * invB : 0.f;
-#pragma unroll
-            for (int i = 0; i < MAXA; ++i)
-              if (i < nout) {
-                gv[i] = glp * z[i] / sig[i];
-                sg[i] += gv[i];
-                sl[i] += glp * (z[i] * z[i] - 1.f) - a.ent_coef * invB;
-              }
-            st[0] += -(take1 ? s1 : s2);
-            st[2] += oldlp - lp;
-            st[3] += (ratio < 1.f - a.clip || ratio > 1.f + a.clip) ? 1.f : 0.f;
-          }
-        } else if (valid) {
-          const float v = __uint_as_float(r[0]) + nw.bias[L][0];
-          const float verr = v - ret;
-          gv[0] = a.vf_coef * verr * invB;
-          sg[0] += gv[0];
-          st[1] += 0.5f * a.vf_coef * verr * verr;
-        }
-        // G row (NH bf16, zero beyond n_out) into K-chunk 3 of act_buf0 (SW128). The H_2
-        // stores that read that chunk have completed (h_stored, arrived before layer 2).
-        uint8_t* grow_s = sG + row * 128;
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-          if (u * 8 < NH)
-            *reinterpret_cast<uint4*>(grow_s + ((u ^ (row & 7)) << 4)) =
-                make_uint4(pack_bf16(gv[8 * u], gv[8 * u + 1]), pack_bf16(gv[8 * u + 2], gv[8 * u + 3]),
-                           pack_bf16(gv[8 * u + 4], gv[8 * u + 5]), pack_bf16(gv[8 * u + 6], gv[8 * u + 7]));
+        // G row into K-chunk 3 of act_buf0 (SW128). The H_2 stores that read that chunk have
+        // completed (h_stored, arrived before layer 2).
+        head_row_loss<MAXA>(net, r, cst, nout, NH, valid, a.act + rr * nout, act_r, oldlp, adv, ret, a.clip,
+                            a.vf_coef, a.ent_coef, invB, sG + row * 128, row, lacc, st, sg, sl);
         ptx::fence_proxy_async_smem();
         ptx::tc_fence_before();
         __syncwarp();
@@ -446,38 +418,27 @@ __global__ void __launch_bounds__(kThreads, 1) train_fwd_kernel(const __grid_con
         for (int i = 0; i < 16; ++i)
           if (o0 + i < nout) nw.dw_slab[((long long)cta * nout + o0 + i) * hp + k] = dwacc[i];
     }
-    // (b) head-bias / log-std gradients and loss statistics (warps with h == 0 hold them)
+    // (b) head-bias / log-std gradients and loss statistics: per-quarter records in `red`
     if (lane == 0) ptx::bulk_wait<0>();
-    epi_bar();  // every TMA store has finished: act_buf1 is scratch now
-    float* red = reinterpret_cast<float*>(buf1);
     const int stride = head_partial_stride(a.A);
-    if (h == 0) {
-      auto put = [&](int col, float x) {
-        x = warp_sum(x);
-        if (lane == 0) red[q * 128 + col] = x;
-      };
-      for (int col = 0; col < stride; ++col)
-        if (lane == 0) red[q * 128 + col] = 0.f;
-      __syncwarp();
-      if (net == 0) {
-#pragma unroll
-        for (int i = 0; i < MAXA; ++i)
-          if (i < a.A) {
-            put(i, sg[i]);
-            put(a.A + 1 + i, sl[i]);
-          }
-        put(2 * a.A + 1, st[0]);
-        put(2 * a.A + 3, st[2]);
-        put(2 * a.A + 4, st[3]);
-      } else {
-        put(a.A, sg[0]);
-        put(2 * a.A + 2, st[1]);
-      }
-    }
+    if (h == 0) head_loss_flush<MAXA>(nout, lacc, st, sg, sl);
     epi_bar();
     if (h == 0 && q == 0)
-      for (int col = lane; col < stride; col += 32)
-        a.part[(long long)blockIdx.x * stride + col] = ((red[col] + red[128 + col]) + red[256 + col]) + red[384 + col];
+      for (int col = lane; col < stride; col += 32) {
+        int src = -1;  // offset inside a quarter record, or -1 for the other net's fields
+        if (net == 0) {
+          if (col < a.A) src = col;
+          else if (col > a.A && col <= 2 * a.A) src = 32 + col - a.A - 1;
+          else if (col == 2 * a.A + 1) src = 64;
+          else if (col == 2 * a.A + 3) src = 66;
+          else if (col == 2 * a.A + 4) src = 67;
+        } else {
+          if (col == a.A) src = 0;
+          else if (col == 2 * a.A + 2) src = 65;
+        }
+        a.part[(long long)blockIdx.x * stride + col] =
+            src < 0 ? 0.f : ((red[src] + red[kQ + src]) + red[2 * kQ + src]) + red[3 * kQ + src];
+      }
   }
 
   ptx::tc_fence_before();

@@ -794,6 +794,21 @@ void Trainer::timed(cudaStream_t s, int phase, double flop, double bytes, F&& f)
 void Trainer::gemm(Gmi& g, int phase, const GemmParams& P, int bn, int amn, int bmn, int epi, double flop, int ws,
                    cudaStream_t stream, int ctas) {
   cudaStream_t st = stream ? stream : g.s;
+  // GMI_GEMM_TRACE=<phase id>: globaltimer stamps of CTA 0 for every launch of that phase
+  // (the last one of the iteration wins; read with get("gemm_trace")). Development aid.
+  static const char* tr_env = std::getenv("GMI_GEMM_TRACE");
+  if (tr_env && std::atoi(tr_env) == phase) {
+    if (!gemm_trace_) {
+      GMI_CUDA_CHECK(cudaMalloc(&gemm_trace_, 128 * 8));
+      GMI_CUDA_CHECK(cudaMemset(gemm_trace_, 0, 128 * 8));
+      allocs_.push_back(gemm_trace_);
+    }
+    GemmParams Pt = P;
+    Pt.trace = static_cast<unsigned long long*>(gemm_trace_);
+    timed(st, phase, flop, 0.0, [&] { gemm_launch(Pt, bn, amn, bmn, epi, st, ctas > 0 ? ctas : g.ctas, ws); });
+    ++launches_;
+    return;
+  }
   timed(st, phase, flop, 0.0, [&] { gemm_launch(P, bn, amn, bmn, epi, st, ctas > 0 ? ctas : g.ctas, ws); });
   ++launches_;
 }
@@ -1320,6 +1335,10 @@ long long Trainer::get(const std::string& what, int gi, void* dst) {
   if (what == "head_part") {  // per-block head-gradient / loss partial records (debug)
     const int parts = g.fused_head ? g.head_grid : ppo::head_loss_blocks(g.Bm);
     return copy(g.head_part, (long long)parts * ppo::head_partial_stride(geo_.A), 4);
+  }
+  if (what == "gemm_trace") {
+    if (!gemm_trace_) invalid("GEMM trace not enabled (GMI_GEMM_TRACE=<phase>)");
+    return copy(gemm_trace_, 128, 8);
   }
   if (what == "train_fwd_trace") {  // GMI_TRAIN_FWD_TRACE=1: stamps of CTA 0, last minibatch
     if (!g.fwd_args.trace) invalid("train-forward trace not enabled (GMI_TRAIN_FWD_TRACE=1)");

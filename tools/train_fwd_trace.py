@@ -1,6 +1,6 @@
 #!/usr/bin/env python3
 """Phase timing inside the fused training-forward kernel (CTA 0, globaltimer stamps written
-when GMI_TRAIN_FWD_TRACE=1 and GMI_TRAIN_FWD=1). Development aid."""
+when GMI_TRAIN_FWD_TRACE=1 and GMI_TRAIN_FWD=1). Development aid; needs a trace build: make -C paper_2206_08482_b200/csrc clean all TRACE=1."""
 import os
 import sys
 
