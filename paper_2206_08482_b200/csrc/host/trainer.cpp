@@ -202,7 +202,10 @@ Trainer::Trainer(const gmi_ppo_config_t& cfg, const void* nccl_id) : cfg_(cfg) {
     exec_ = std::make_unique<GmiResources>(cfg.device, n_local_, cfg.gmi_backend, cfg.sm_per_gmi);
   }
   const int tix = decoupled_ ? 1 : 0;  // execution-resource index of the first trainer GMI
-  if (decoupled_)  // the trainer's update stream (fold, Adam, snapshot) stays inside its partition
+  // decoupled, one GPU: the trainer's update stream (Adam, snapshot) stays inside its partition;
+  // with NCCL in the update chain it stays in the primary context the communicator was made in
+  upd_in_gmi_ = decoupled_ && cfg.num_gpus == 1;
+  if (upd_in_gmi_)
     upd_ = exec_->extra_stream(1);
   else
     GMI_CUDA_CHECK(cudaStreamCreateWithFlags(&upd_, cudaStreamNonBlocking));
@@ -267,7 +270,7 @@ Trainer::~Trainer() {
   if (ev_rolled_) cudaEventDestroy(ev_rolled_);
   if (ev_adam_) cudaEventDestroy(ev_adam_);
   if (ev_start_) cudaEventDestroy(ev_start_);
-  if (upd_ && !decoupled_) cudaStreamDestroy(upd_);
+  if (upd_ && !upd_in_gmi_) cudaStreamDestroy(upd_);
   for (void* p : allocs_) cudaFree(p);
   if (ctl_host_) cudaFreeHost(ctl_host_);
   if (stats_host_) cudaFreeHost(stats_host_);

@@ -91,6 +91,7 @@ class Trainer {
   // decoupled mode (cfg.decoupled): serving GMI stream, experience-channel events, the policy
   // snapshot the serving GMI acts with, and its own control block (rollout index)
   bool decoupled_ = false;
+  bool upd_in_gmi_ = false;  // update stream owned by the trainer GMI's green context
   cudaStream_t serve_s_ = nullptr;
   cudaEvent_t ev_copied_ = nullptr, ev_rolled_ = nullptr;
   float* params_roll_ = nullptr;
