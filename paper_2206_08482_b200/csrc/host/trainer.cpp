@@ -204,7 +204,11 @@ Trainer::Trainer(const gmi_ppo_config_t& cfg, const void* nccl_id) : cfg_(cfg) {
   const int tix = decoupled_ ? 1 : 0;  // execution-resource index of the first trainer GMI
   // decoupled, one GPU: the trainer's update stream (Adam, snapshot) stays inside its partition;
   // with NCCL in the update chain it stays in the primary context the communicator was made in
-  upd_in_gmi_ = decoupled_ && cfg.num_gpus == 1;
+  // GMI_FORCE_NCCL=1 (tests): a one-rank communicator on a single GPU, so the NCCL all-reduce
+  // in the captured iteration graph is exercised on one-GPU boxes (identity sum, bit-exact)
+  const char* force = std::getenv("GMI_FORCE_NCCL");
+  const bool force_nccl = cfg.num_gpus == 1 && force && force[0] == '1';
+  upd_in_gmi_ = decoupled_ && cfg.num_gpus == 1 && !force_nccl;
   if (upd_in_gmi_)
     upd_ = exec_->extra_stream(1);
   else
@@ -237,10 +241,14 @@ Trainer::Trainer(const gmi_ppo_config_t& cfg, const void* nccl_id) : cfg_(cfg) {
   if (decoupled_ && !(gmis_[0]->fused_roll && gmis_[0]->fused_val))
     invalid("decoupled mode needs the fused rollout and value pass (hidden widths <= 256, <= 4 layers)");
   ensure_bias_table(1 << 20);
-  if (cfg.num_gpus > 1) {
-    if (!nccl_id) invalid("nccl_id required when num_gpus > 1");
+  if (cfg.num_gpus > 1 || force_nccl) {
     ncclUniqueId id;
-    std::memcpy(&id, nccl_id, sizeof(id));
+    if (force_nccl) {
+      NCCL_CHECK(ncclGetUniqueId(&id));
+    } else {
+      if (!nccl_id) invalid("nccl_id required when num_gpus > 1");
+      std::memcpy(&id, nccl_id, sizeof(id));
+    }
     ncclComm_t comm;
     NCCL_CHECK(ncclCommInitRank(&comm, cfg.num_gpus, id, cfg.rank));
     nccl_ = comm;

@@ -254,3 +254,20 @@ def test_decoupled_bench_shape_matches_oracle(cuda):
         dev.iteration()
         orc.iteration_decoupled()
         _close(f"params[{it}]", dev.get("params"), orc.get("params"), 4e-3, 1e-4)
+
+
+@pytest.mark.parametrize("layout", [dict(gmis_per_gpu=1), dict(gmis_per_gpu=2), dict(decoupled=1, gmi_backend=1)])
+def test_nccl_allreduce_in_iteration_graph(cuda, monkeypatch, layout):
+    """The cross-GPU gradient all-reduce (ncclAllReduce on the update stream, captured in the
+    iteration's CUDA graph) exercised on a one-GPU box through a one-rank communicator
+    (GMI_FORCE_NCCL=1): the sum over one rank is the identity, so three iterations (eager, then
+    graph replays) must leave the parameters bit-identical to the run without NCCL."""
+    from paper_2206_08482_b200.ppo import PpoConfig, Trainer
+    cfg = dict(obs_dim=12, act_dim=3, hidden=[64, 64], num_envs=64, **layout)
+    plain = Trainer(PpoConfig(**cfg))
+    monkeypatch.setenv("GMI_FORCE_NCCL", "1")
+    with_nccl = Trainer(PpoConfig(**cfg))
+    for _ in range(3):
+        plain.iteration()
+        with_nccl.iteration()
+    assert np.array_equal(plain.get("params").view(np.uint32), with_nccl.get("params").view(np.uint32))
