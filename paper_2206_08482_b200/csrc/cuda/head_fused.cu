@@ -33,18 +33,34 @@ namespace {
 
 constexpr int kRows = 128;
 constexpr int kEpiWarps = 16;
-constexpr int kThreads = 64 + 32 * kEpiWarps;
+constexpr int kThreads = 64 + 32 * kEpiWarps + 32;  // TMA, MMA, epilogue warps, MMA3 warp (last)
 constexpr uint32_t kChunk = kRows * 128;  // [128 rows][64 bf16], SW128
 constexpr uint32_t kOffH = 0;              // 2 x H_L tile (double-buffered), 4 K-chunks each
-constexpr uint32_t kOffG = 8 * kChunk;     // G tile [128][64] bf16 (cols >= n_out stay 0)
-constexpr uint32_t kOffWK = kOffG + kChunk;  // W_head K-major, per K-chunk [32 rows][128 B]
+constexpr uint32_t kOffG = 8 * kChunk;     // 2 x G tile [128][64] bf16 (double-buffered, see MMA3)
+constexpr uint32_t kOffWK = kOffG + 2 * kChunk;  // W_head K-major, per K-chunk [32 rows][128 B]
 constexpr uint32_t kOffWM = kOffWK + 4 * 4096;  // W_head MN-major, [32 K-rows][64 cols] boxes
-constexpr uint32_t kOffStg = kOffWM + 4 * 4096;  // epilogue staging, 2 KB per warp
-constexpr uint32_t kOffRed = kOffStg + kEpiWarps * 2048;  // 4 x 256 fp32
+constexpr int kElu = 12;  // warps on the elu' epilogue (column groups 1..3); group 0 runs the loss
+constexpr uint32_t kOffStg = kOffWM + 4 * 4096;  // epilogue staging, 2 KB per elu' warp
+constexpr uint32_t kOffRed = kOffStg + kElu * 2048;  // 4 x 256 fp32
 constexpr uint32_t kOffBar = kOffRed + 4 * 256 * 4;
 constexpr uint32_t kSmem = kOffBar + 512 + 1024;  // barriers + per-action constants
-constexpr int kElu = 12;  // warps on the elu' epilogue (column groups 1..3); group 0 runs the loss
+static_assert(kSmem <= 232448, "shared memory budget");
 constexpr uint32_t kTmemAcc1 = 0, kTmemAcc3 = 64, kTmemAcc2 = 256;
+
+// Development trace (`make TRACE=1`): globaltimer stamps of CTA 0, tiles 0..3, into a buffer
+// set with head_fused_set_trace (tools: get("head_trace")).
+__device__ unsigned long long* g_head_trace = nullptr;
+__device__ __forceinline__ void hstamp(bool on, int it, int k) {
+#ifdef GMI_TRACE
+  if (on && g_head_trace && blockIdx.x == 0 && it < 4) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_head_trace[it * 16 + k] = t;
+  }
+#else
+  (void)on, (void)it, (void)k;
+#endif
+}
 
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory"); }
 
@@ -94,7 +110,7 @@ __global__ void __launch_bounds__(kThreads, 1) head_fused_kernel(const __grid_co
   }
   if (warp == 1) ptx::tmem_alloc(tmem_slot, 512);
   // G tile: columns >= n_out must be zero (they are the K padding of MMA2 / N padding of MMA3)
-  for (int i = threadIdx.x; i < int(kChunk / 16); i += blockDim.x)
+  for (int i = threadIdx.x; i < int(2 * kChunk / 16); i += blockDim.x)
     reinterpret_cast<uint4*>(sG)[i] = make_uint4(0u, 0u, 0u, 0u);
   ptx::fence_proxy_async_smem();
   pdl_trigger();
@@ -127,14 +143,16 @@ __global__ void __launch_bounds__(kThreads, 1) head_fused_kernel(const __grid_co
       ptx::mbar_wait_sleep(wbar, 0);
       const uint32_t idesc1 = ptx::umma_idesc_bf16(kRows, uint32_t(NH), 0, 0);
       const uint32_t idesc2 = ptx::umma_idesc_bf16(kRows, uint32_t((hp + 15) / 16 * 16), 0, 1);
-      const uint32_t idesc3 = ptx::umma_idesc_bf16(kRows, uint32_t(NH), 1, 1);
       const uint32_t g0 = ptx::smem_u32(sG);
       const uint32_t wk0 = ptx::smem_u32(sWK), wm0 = ptx::smem_u32(sWM);
       int it = 0;
       for (int j = cta; j < mtiles; j += ctas, ++it) {
         const int b = it & 1;
         const uint32_t h0 = ptx::smem_u32(sH + b * 4 * kChunk);
+        const uint32_t gt = g0 + b * kChunk;
+        hstamp(true, it, 0);
         ptx::mbar_wait(&hfull[b], (it >> 1) & 1);
+        hstamp(true, it, 1);
         ptx::tc_fence_after();
         // MMA1: [128 x NH] = H . W_head^T (K = hp)
         for (int kc = 0; kc < nk; ++kc) {
@@ -145,22 +163,41 @@ __global__ void __launch_bounds__(kThreads, 1) head_fused_kernel(const __grid_co
                           (kc > 0 || k > 0) ? 1u : 0u);
         }
         ptx::mma_commit(acc1_full);
+        hstamp(true, it, 2);
         ptx::mbar_wait(g_ready, it & 1);
+        hstamp(true, it, 3);
         if (it > 0) ptx::mbar_wait(acc2_free, (it - 1) & 1);  // previous tile's elu' epilogue drained acc2
         ptx::tc_fence_after();
         // MMA2: [128 x hp] = G . W_head (K = NH; W_head read MN-major)
         for (int k = 0; k < NH / 16; ++k)
-          ptx::mma_bf16(tmem + kTmemAcc2, ptx::umma_desc_sw128(g0 + k * 32, 16, 1024),
+          ptx::mma_bf16(tmem + kTmemAcc2, ptx::umma_desc_sw128(gt + k * 32, 16, 1024),
                         ptx::umma_desc_sw128(wm0 + k * 2048, 4096, 1024), idesc2, k > 0 ? 1u : 0u);
         ptx::mma_commit(acc2_full);
-        // MMA3: dW_head^T[hp x NH] += H^T . G (K = tile rows; both operands MN-major views)
+        hstamp(true, it, 4);
+      }
+    }
+  } else if (warp == 2 + kEpiWarps) {
+    // ------------------------------------------------ MMA3 issuer: the head weight gradient
+    // dW_head^T[hp x NH] += H^T . G (K = tile rows; both operands MN-major views), accumulated in
+    // TMEM over the CTA's tiles. A thread of its own: its 16 small-N MMAs take ~1.3 us to issue
+    // and would otherwise delay the next tile's MMA1 / MMA2. G is double-buffered: the loss of
+    // tile t+2 only starts after MMA1(t+2), whose H tile could load only after MMA3(t) freed it.
+    if (lane == 0) {
+      ptx::mbar_wait_sleep(wbar, 0);
+      const uint32_t idesc3 = ptx::umma_idesc_bf16(kRows, uint32_t(NH), 1, 1);
+      const uint32_t g0 = ptx::smem_u32(sG);
+      int it = 0;
+      for (int j = cta; j < mtiles; j += ctas, ++it) {
+        const uint32_t h0 = ptx::smem_u32(sH + (it & 1) * 4 * kChunk);
+        const uint32_t gt = g0 + (it & 1) * kChunk;
+        ptx::mbar_wait_sleep(g_ready, it & 1);  // G(t) written; H(t) landed before MMA1(t)
+        ptx::tc_fence_after();
         for (int half = 0; half * 128 < hp; ++half)
           for (int k = 0; k < kRows / 16; ++k)
             ptx::mma_bf16(tmem + kTmemAcc3 + half * 32,
                           ptx::umma_desc_sw128(h0 + 2 * half * kChunk + k * 2048, kChunk, 1024),
-                          ptx::umma_desc_sw128(g0 + k * 2048, 8192, 1024), idesc3,
-                          (it > 0 || k > 0) ? 1u : 0u);
-        ptx::mma_commit(&hfree[b]);
+                          ptx::umma_desc_sw128(gt + k * 2048, 8192, 1024), idesc3, (it > 0 || k > 0) ? 1u : 0u);
+        ptx::mma_commit(&hfree[it & 1]);
       }
       ptx::mma_commit(fin);
     }
@@ -170,7 +207,7 @@ __global__ void __launch_bounds__(kThreads, 1) head_fused_kernel(const __grid_co
     const int h = (warp - 2) >> 2;
     const int row = q * 32 + lane;
     const float invB = 1.0f / float(a.Bm);
-    uint8_t* stg = smem + kOffStg + (warp - 2) * 2048;
+    uint8_t* stg = smem + kOffStg + (h > 0 ? warp - 6 : 0) * 2048;  // elu' warps only
     // per-action constants of the loss, once per CTA: log_std, exp(log_std), head bias
     float* cst = reinterpret_cast<float*>(smem + kOffBar + 128);
     float* lacc = red + q * 128;  // this lane quarter's per-action sums [0, 64) and statistics [64, 68)
@@ -212,22 +249,25 @@ __global__ void __launch_bounds__(kThreads, 1) head_fused_kernel(const __grid_co
           }
         }
         ptx::mbar_wait_sleep(acc1_full, it & 1);
+        hstamp(warp == 2 && lane == 0, it, 5);
         ptx::tc_fence_after();
         uint32_t r[32];
         ptx::tmem_ld_32x32b_x32(tmem + kTmemAcc1 + (static_cast<uint32_t>(q * 32) << 16), r);
         ptx::tmem_ld_wait();
         head_row_loss<MAXA>(net, r, cst, nout, NH, valid, a.act + rr * nout, act_r, oldlp, adv, ret, a.clip,
-                            a.vf_coef, a.ent_coef, invB, sG + row * 128, row, lacc, st, sg, sl);
+                            a.vf_coef, a.ent_coef, invB, sG + (it & 1) * kChunk + row * 128, row, lacc, st, sg, sl);
         ptx::fence_proxy_async_smem();
         ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(g_ready);
+        hstamp(warp == 2 && lane == 0, it, 6);
       }
 
       // ---- dPre_{L-1} = (G W_head) * elu'(H_L) on column groups 1..3 (chunks c = h-1, h+2, h+5),
       // so group 0 can already run the next tile's loss
       if (h == 0) continue;
       ptx::mbar_wait_sleep(acc2_full, it & 1);
+      hstamp(warp == 6 && lane == 0, it, 7);
       ptx::tc_fence_after();
 #pragma unroll 1
       for (int pass = 0; pass < 3; ++pass) {
@@ -270,6 +310,7 @@ __global__ void __launch_bounds__(kThreads, 1) head_fused_kernel(const __grid_co
       __syncwarp();
       if (lane == 0) {
         ptx::mbar_arrive(acc2_free);
+        hstamp(warp == 6, it, 8);
         ptx::mbar_arrive(&hfree[it & 1]);
       }
     }
@@ -316,6 +357,10 @@ __global__ void __launch_bounds__(kThreads, 1) head_fused_kernel(const __grid_co
 }
 
 }  // namespace
+
+void head_fused_set_trace(unsigned long long* buf) {
+  GMI_CUDA_CHECK(cudaMemcpyToSymbol(g_head_trace, &buf, sizeof(buf)));
+}
 
 bool head_fusable(int hp, int A) { return hp <= 256 && A <= 31 && A >= 1; }
 

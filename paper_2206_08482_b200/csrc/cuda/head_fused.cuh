@@ -35,5 +35,6 @@ struct alignas(64) HeadFusedArgs {
 bool head_fusable(int hp, int A);
 int head_fused_grid(int Bm, int sms);  // even; CTA b serves net b % 2
 void launch_head_fused(const HeadFusedArgs& a, int grid, cudaStream_t s);
+void head_fused_set_trace(unsigned long long* buf);  // development trace (TRACE=1 builds)
 
 }  // namespace gmi::ppo

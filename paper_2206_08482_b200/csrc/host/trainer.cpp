@@ -612,6 +612,11 @@ void Trainer::build_plans() {
       h.ent_coef = cfg_.ent_coef;
       head_parts = g.head_grid;
       hslab_parts = per_net;
+      const char* htr = std::getenv("GMI_HEAD_TRACE");
+      if (htr && htr[0] == '1' && !head_trace_) {
+        head_trace_ = dev(64 * 8);
+        ppo::head_fused_set_trace(static_cast<unsigned long long*>(head_trace_));
+      }
       // whole training forward + head step on chip (same per-CTA records as the head kernel).
       // Opt-in (GMI_TRAIN_FWD=1): bit-identical, but with one tile in flight per CTA its MMA ->
       // epilogue chain is serial and it measured slower on B200 than the per-layer GEMMs plus
@@ -1346,6 +1351,10 @@ long long Trainer::get(const std::string& what, int gi, void* dst) {
   if (what == "head_part") {  // per-block head-gradient / loss partial records (debug)
     const int parts = g.fused_head ? g.head_grid : ppo::head_loss_blocks(g.Bm);
     return copy(g.head_part, (long long)parts * ppo::head_partial_stride(geo_.A), 4);
+  }
+  if (what == "head_trace") {  // GMI_HEAD_TRACE=1 with a TRACE=1 build
+    if (!head_trace_) invalid("head trace not enabled (GMI_HEAD_TRACE=1)");
+    return copy(head_trace_, 64, 8);
   }
   if (what == "gemm_trace") {
     if (!gemm_trace_) invalid("GEMM trace not enabled (GMI_GEMM_TRACE=<phase>)");

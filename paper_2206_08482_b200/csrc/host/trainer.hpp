@@ -99,6 +99,7 @@ class Trainer {
   ppo::Control* ctl_roll_ = nullptr;
   long long rollouts_ = 0;  // serving-GMI rollouts enqueued so far
   void* gemm_trace_ = nullptr;  // GMI_GEMM_TRACE development aid
+  void* head_trace_ = nullptr;  // GMI_HEAD_TRACE development aid
   bool bwd_par_ = false;   // dx chain || dW GEMMs on two streams of the GMI
   int bwd_dx_share_ = 50;  // percent of the GMI's SMs given to the dx branch
   int iteration_ = 0;      // iterations enqueued so far

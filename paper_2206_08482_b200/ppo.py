@@ -167,7 +167,7 @@ class IterationStats:
 
 
 _DT = {"done": np.uint8, "ep_step": np.int32, "ep_len": np.int32, "ep_count": np.int32,
-       "rollout_trace": np.int64, "train_fwd_trace": np.int64, "gemm_trace": np.int64}
+       "rollout_trace": np.int64, "train_fwd_trace": np.int64, "gemm_trace": np.int64, "head_trace": np.int64}
 
 
 class Trainer:
