@@ -45,7 +45,7 @@ constexpr uint32_t kOffRed = kOffStg + kElu * 2048;  // 4 x 256 fp32
 constexpr uint32_t kOffBar = kOffRed + 4 * 256 * 4;
 constexpr uint32_t kSmem = kOffBar + 512 + 1024;  // barriers + per-action constants
 static_assert(kSmem <= 232448, "shared memory budget");
-constexpr uint32_t kTmemAcc1 = 0, kTmemAcc3 = 64, kTmemAcc2 = 256;
+constexpr uint32_t kTmemAcc1 = 0, kTmemAcc3 = 64, kTmemAcc2 = 256;  // acc1: 2 x 32 columns
 
 // Development trace (`make TRACE=1`): globaltimer stamps of CTA 0, tiles 0..3, into a buffer
 // set with head_fused_set_trace (tools: get("head_trace")).
@@ -77,12 +77,12 @@ __global__ void __launch_bounds__(kThreads, 1) head_fused_kernel(const __grid_co
   uint64_t* wbar = bars;
   uint64_t* hfull = bars + 1;  // [2]
   uint64_t* hfree = bars + 3;  // [2]
-  uint64_t* acc1_full = bars + 5;
-  uint64_t* g_ready = bars + 6;
-  uint64_t* acc2_full = bars + 7;
-  uint64_t* acc2_free = bars + 8;
-  uint64_t* fin = bars + 9;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 10);
+  uint64_t* g_ready = bars + 5;
+  uint64_t* acc2_full = bars + 6;
+  uint64_t* acc2_free = bars + 7;
+  uint64_t* fin = bars + 8;
+  uint64_t* acc1_full = bars + 9;  // [2]: double-buffered head output
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 11);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int net = blockIdx.x & 1;
@@ -97,7 +97,8 @@ __global__ void __launch_bounds__(kThreads, 1) head_fused_kernel(const __grid_co
       ptx::mbar_init(&hfull[b], 1);
       ptx::mbar_init(&hfree[b], kElu + 1);  // elu' epilogue reads + MMA3 commit
     }
-    ptx::mbar_init(acc1_full, 1);
+    ptx::mbar_init(&acc1_full[0], 1);
+    ptx::mbar_init(&acc1_full[1], 1);
     ptx::mbar_init(g_ready, 4);
     ptx::mbar_init(acc2_full, 1);
     ptx::mbar_init(acc2_free, kElu);
@@ -145,25 +146,31 @@ __global__ void __launch_bounds__(kThreads, 1) head_fused_kernel(const __grid_co
       const uint32_t idesc2 = ptx::umma_idesc_bf16(kRows, uint32_t((hp + 15) / 16 * 16), 0, 1);
       const uint32_t g0 = ptx::smem_u32(sG);
       const uint32_t wk0 = ptx::smem_u32(sWK), wm0 = ptx::smem_u32(sWM);
-      int it = 0;
-      for (int j = cta; j < mtiles; j += ctas, ++it) {
-        const int b = it & 1;
+      // MMA1 of tile t+1 is issued before waiting for tile t's loss (double-buffered head
+      // output, acc1_full[t & 1]), so the head forward of the next tile overlaps this tile's loss
+      auto mma1 = [&](int t) {
+        const int b = t & 1;
         const uint32_t h0 = ptx::smem_u32(sH + b * 4 * kChunk);
-        const uint32_t gt = g0 + b * kChunk;
-        hstamp(true, it, 0);
-        ptx::mbar_wait(&hfull[b], (it >> 1) & 1);
-        hstamp(true, it, 1);
+        hstamp(true, t, 0);
+        ptx::mbar_wait(&hfull[b], (t >> 1) & 1);
+        hstamp(true, t, 1);
         ptx::tc_fence_after();
         // MMA1: [128 x NH] = H . W_head^T (K = hp)
         for (int kc = 0; kc < nk; ++kc) {
           const int ks = min(4, (hp - kc * 64 + 15) / 16);
           for (int k = 0; k < ks; ++k)
-            ptx::mma_bf16(tmem + kTmemAcc1, ptx::umma_desc_sw128(h0 + kc * kChunk + k * 32, 16, 1024),
+            ptx::mma_bf16(tmem + kTmemAcc1 + b * 32, ptx::umma_desc_sw128(h0 + kc * kChunk + k * 32, 16, 1024),
                           ptx::umma_desc_sw128(wk0 + kc * 4096 + k * 32, 16, 1024), idesc1,
                           (kc > 0 || k > 0) ? 1u : 0u);
         }
-        ptx::mma_commit(acc1_full);
-        hstamp(true, it, 2);
+        ptx::mma_commit(&acc1_full[b]);
+        hstamp(true, t, 2);
+      };
+      const int ntiles = cta < mtiles ? (mtiles - cta + ctas - 1) / ctas : 0;
+      if (ntiles > 0) mma1(0);
+      for (int it = 0; it < ntiles; ++it) {
+        if (it + 1 < ntiles) mma1(it + 1);
+        const uint32_t gt = g0 + (it & 1) * kChunk;
         ptx::mbar_wait(g_ready, it & 1);
         hstamp(true, it, 3);
         if (it > 0) ptx::mbar_wait(acc2_free, (it - 1) & 1);  // previous tile's elu' epilogue drained acc2
@@ -248,11 +255,11 @@ __global__ void __launch_bounds__(kThreads, 1) head_fused_kernel(const __grid_co
             ret = a.ret[rr];
           }
         }
-        ptx::mbar_wait_sleep(acc1_full, it & 1);
+        ptx::mbar_wait_sleep(&acc1_full[it & 1], (it >> 1) & 1);
         hstamp(warp == 2 && lane == 0, it, 5);
         ptx::tc_fence_after();
         uint32_t r[32];
-        ptx::tmem_ld_32x32b_x32(tmem + kTmemAcc1 + (static_cast<uint32_t>(q * 32) << 16), r);
+        ptx::tmem_ld_32x32b_x32(tmem + kTmemAcc1 + (it & 1) * 32 + (static_cast<uint32_t>(q * 32) << 16), r);
         ptx::tmem_ld_wait();
         head_row_loss<MAXA>(net, r, cst, nout, NH, valid, a.act + rr * nout, act_r, oldlp, adv, ret, a.clip,
                             a.vf_coef, a.ent_coef, invB, sG + (it & 1) * kChunk + row * 128, row, lacc, st, sg, sl);
