@@ -43,7 +43,7 @@ constexpr int kElu = 12;  // warps on the elu' epilogue (column groups 1..3); gr
 constexpr uint32_t kOffStg = kOffWM + 4 * 4096;  // epilogue staging, 2 KB per elu' warp
 constexpr uint32_t kOffRed = kOffStg + kElu * 2048;  // 4 x 256 fp32
 constexpr uint32_t kOffBar = kOffRed + 4 * 256 * 4;
-constexpr uint32_t kSmem = kOffBar + 512 + 1024;  // barriers + per-action constants
+constexpr uint32_t kSmem = kOffBar + 768 + 1024;  // barriers + per-action constants (128 floats)
 static_assert(kSmem <= 232448, "shared memory budget");
 constexpr uint32_t kTmemAcc1 = 0, kTmemAcc3 = 64, kTmemAcc2 = 256;  // acc1: 2 x 32 columns
 
@@ -222,6 +222,7 @@ __global__ void __launch_bounds__(kThreads, 1) head_fused_kernel(const __grid_co
       const float ls = a.log_std[threadIdx.x - 64];
       cst[threadIdx.x - 64] = ls;
       cst[32 + threadIdx.x - 64] = expf(ls);
+      cst[96 + threadIdx.x - 64] = 1.0f / expf(ls);
     }
     if (threadIdx.x - 64 < nout) cst[64 + threadIdx.x - 64] = hn.bias[threadIdx.x - 64];
     if (h == 0 && lane == 0)

@@ -18,13 +18,19 @@
 
 namespace gmi::ppo {
 
-// cst (shared): [0, 32) log_std, [32, 64) exp(log_std), [64, 96) head bias of this net.
+// cst (shared): [0, 32) log_std, [32, 64) exp(log_std), [64, 96) head bias of this net,
+// [96, 128) 1 / exp(log_std).
 // lacc (shared, this warp): [i] sum of dL/dmu_i (or dL/dv), [32 + i] sum of dL/dlog_std_i.
 // st: running loss statistics of this thread's rows {policy loss, value loss, kl, clipped}.
 // G row: bf16 dL/dout into the SW128 K-major tile row `grow_s` (16-byte units swizzled by row & 7);
 // columns [n_out, nh) are written as zeros.
 template <int MAXA>
 constexpr bool kLossRegAcc = MAXA <= 8;
+
+__device__ __forceinline__ uint32_t pack2(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
 
 template <int MAXA>
 __device__ __forceinline__ void head_row_loss(int net, const uint32_t (&r)[32], const float* cst, int nout, int nh,
@@ -35,17 +41,20 @@ __device__ __forceinline__ void head_row_loss(int net, const uint32_t (&r)[32], 
                                               float (&sl)[kLossRegAcc<MAXA> ? MAXA : 1]) {
   constexpr bool kPre = MAXA <= 16;  // actions prefetched into registers before the accumulator wait
   const int lane = threadIdx.x & 31;
-#pragma unroll
-  for (int u = 0; u < 4; ++u)
-    if (u * 8 < nh) *reinterpret_cast<uint4*>(grow_s + ((u ^ (row & 7)) << 4)) = make_uint4(0u, 0u, 0u, 0u);
   auto put_g = [&](int col, float v) {
     *reinterpret_cast<__nv_bfloat16*>(grow_s + ((((col >> 3) ^ (row & 7))) << 4) + (col & 7) * 2) =
         __float2bfloat16_rn(v);
   };
-  // z_i = (a_i - mu_i) / sigma_i: with prefetched actions the registers are reused for z
+  auto zero_row = [&](int from_unit) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (u >= from_unit && u * 8 < nh) *reinterpret_cast<uint4*>(grow_s + ((u ^ (row & 7)) << 4)) = make_uint4(0u, 0u, 0u, 0u);
+  };
+  // z_i = (a_i - mu_i) / sigma_i, as a multiply by 1 / sigma_i (cst[96 + i]); with prefetched
+  // actions the registers are reused for z
   auto zval = [&](int i) {
     const float mu = __uint_as_float(r[i]) + cst[64 + i];
-    return ((kPre ? act_r[kPre ? i : 0] : act_row[i]) - mu) / cst[32 + i];
+    return ((kPre ? act_r[kPre ? i : 0] : act_row[i]) - mu) * cst[96 + i];
   };
   if (net == 0) {
     float lp = 0.f;
@@ -68,17 +77,21 @@ __device__ __forceinline__ void head_row_loss(int net, const uint32_t (&r)[32], 
       st[2] += oldlp - lp;
       st[3] += (ratio < 1.f - clip || ratio > 1.f + clip) ? 1.f : 0.f;
     }
+    if constexpr (!kPre) zero_row(0);
+    float gk[kPre ? 16 : 1];  // small action spaces: the G row is packed and stored as 16-byte units
+#pragma unroll
+    for (int i = 0; i < (kPre ? 16 : 1); ++i) gk[i] = 0.f;
 #pragma unroll
     for (int i = 0; i < MAXA; ++i)
       if (i < nout) {
         float g = 0.f, gl = 0.f;
         if (valid) {
-          const float sig = cst[32 + i];
           const float z = kPre ? act_r[kPre ? i : 0] : zval(i);
-          g = glp * z / sig;
+          g = glp * z * cst[96 + i];
           gl = glp * (z * z - 1.f) - ent_coef * invB;
         }
-        put_g(i, g);
+        if constexpr (kPre) gk[i] = g;
+        else put_g(i, g);
         if constexpr (kLossRegAcc<MAXA>) {
           sg[i] += g;
           sl[i] += gl;
@@ -91,7 +104,16 @@ __device__ __forceinline__ void head_row_loss(int net, const uint32_t (&r)[32], 
           }
         }
       }
+    if constexpr (kPre) {
+#pragma unroll
+      for (int u = 0; u < 2; ++u)
+        *reinterpret_cast<uint4*>(grow_s + ((u ^ (row & 7)) << 4)) =
+            make_uint4(pack2(gk[8 * u], gk[8 * u + 1]), pack2(gk[8 * u + 2], gk[8 * u + 3]),
+                       pack2(gk[8 * u + 4], gk[8 * u + 5]), pack2(gk[8 * u + 6], gk[8 * u + 7]));
+      zero_row(2);
+    }
   } else {
+    zero_row(0);
     float g = 0.f;
     if (valid) {
       const float v = __uint_as_float(r[0]) + cst[64];

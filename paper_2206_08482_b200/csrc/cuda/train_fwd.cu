@@ -44,7 +44,7 @@ constexpr uint32_t kActBytes = 4 * kChunk;
 constexpr uint32_t kWStage = 256 * 128;
 constexpr uint32_t kOffBar = 2 * kActBytes + kStages * kWStage;
 constexpr int kQ = 68;                                 // per-quarter loss record: sums [0, 64) + statistics
-constexpr uint32_t kOffLacc = kOffBar + 512;
+constexpr uint32_t kOffLacc = kOffBar + 640;  // after barriers (128 B) + 128 per-action constants
 constexpr uint32_t kSmem = kOffLacc + 4 * kQ * 4 + 1024;  // barriers + constants + records + alignment
 static_assert(kSmem <= 232448, "shared memory budget");
 
@@ -231,6 +231,7 @@ __global__ void __launch_bounds__(kThreads, 1) train_fwd_kernel(const __grid_con
       const float ls = a.log_std[et];
       cst[et] = ls;
       cst[32 + et] = expf(ls);
+      cst[96 + et] = 1.0f / expf(ls);
     }
     if (et < nout) cst[64 + et] = nw.bias[L][et];
     if (h == 0 && lane == 0)
