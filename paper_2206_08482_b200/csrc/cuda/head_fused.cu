@@ -146,8 +146,7 @@ __global__ void __launch_bounds__(kThreads, 1) head_fused_kernel(const __grid_co
       const uint32_t idesc2 = ptx::umma_idesc_bf16(kRows, uint32_t((hp + 15) / 16 * 16), 0, 1);
       const uint32_t g0 = ptx::smem_u32(sG);
       const uint32_t wk0 = ptx::smem_u32(sWK), wm0 = ptx::smem_u32(sWM);
-      // MMA1 of tile t+1 is issued before waiting for tile t's loss (double-buffered head
-      // output, acc1_full[t & 1]), so the head forward of the next tile overlaps this tile's loss
+      // MMA1 of tile t+1 overlaps tile t's loss (double-buffered head output, acc1_full[t & 1])
       auto mma1 = [&](int t) {
         const int b = t & 1;
         const uint32_t h0 = ptx::smem_u32(sH + b * 4 * kChunk);
@@ -167,13 +166,20 @@ __global__ void __launch_bounds__(kThreads, 1) head_fused_kernel(const __grid_co
         hstamp(true, t, 2);
       };
       const int ntiles = cta < mtiles ? (mtiles - cta + ctas - 1) / ctas : 0;
-      if (ntiles > 0) mma1(0);
+      int next1 = 0;  // first tile whose MMA1 is not issued yet
       for (int it = 0; it < ntiles; ++it) {
-        if (it + 1 < ntiles) mma1(it + 1);
+        // MMA2(it) as soon as its G is ready and acc2 is drained; meanwhile MMA1 of the next
+        // tile is issued the moment its H tile lands (acc1 is double-buffered: at most one ahead)
+        while (true) {
+          if (next1 < ntiles && next1 <= it + 1 && ptx::mbar_test(&hfull[next1 & 1], (next1 >> 1) & 1)) {
+            mma1(next1);
+            ++next1;
+          }
+          if (next1 > it && ptx::mbar_test(g_ready, it & 1) && (it == 0 || ptx::mbar_test(acc2_free, (it - 1) & 1)))
+            break;
+        }
         const uint32_t gt = g0 + (it & 1) * kChunk;
-        ptx::mbar_wait(g_ready, it & 1);
         hstamp(true, it, 3);
-        if (it > 0) ptx::mbar_wait(acc2_free, (it - 1) & 1);  // previous tile's elu' epilogue drained acc2
         ptx::tc_fence_after();
         // MMA2: [128 x hp] = G . W_head (K = NH; W_head read MN-major)
         for (int k = 0; k < NH / 16; ++k)
