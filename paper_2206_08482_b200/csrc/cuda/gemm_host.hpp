@@ -30,6 +30,10 @@ void gemm_launch(const GemmParams& P, int bn, int a_mn, int b_mn, int epi, cudaS
 // Weight-stationary choice for a launch: returns the block N (N padded to 64) when every
 // CTA gets at least one tile and the weights fit, else 0 (use the streaming kernel).
 int gemm_ws_bn(int M, int N, int K, int problems, int sms);
+// Weight-gradient GEMM on SM pairs (gemm_pair.cu): M = N = 256, MN-major operands, fp32 slabs.
+bool gemm_pair_applicable(int M, int N, int a_mn, int b_mn, int epi);
+void gemm_pair_launch(const GemmParams& P, int max_ctas, cudaStream_t s);
+int gemm_pair_max_clusters();
 // Grid of a weight-stationary launch (a multiple of `problems`); the fused column-sum
 // output has grid / problems rows per problem.
 int gemm_ws_grid(int M, int problems, int max_ctas);

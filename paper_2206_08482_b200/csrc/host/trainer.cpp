@@ -158,6 +158,7 @@ struct Trainer::Gmi {
   ppo::ValueArgs val_args{};
   ppo::RolloutArgs roll_args{};
   bool fused_bias[GMI_MAX_HIDDEN] = {};  // bias gradient summed inside the layer's dW GEMM
+  bool dw_pair[GMI_MAX_HIDDEN] = {};     // weight gradient on SM pairs (cuda/gemm_pair.cu)
   bool fused_head = false;
   int head_grid = 0;
   ppo::HeadFusedArgs head_args{};
@@ -474,6 +475,18 @@ void Trainer::build_plans() {
       g.dw[l].num_problems = 2;
       g.dw[l].splits = splits;
       g.fused_bias[l] = true;
+      // 256 x 256 layers, opt-in (GMI_DW_PAIR=1): SM-pair kernel (tcgen05 cta_group::2,
+      // cuda/gemm_pair.cu), same slabs. It cuts L2->SM traffic by a third (ncu: 67 vs 100 MB per
+      // launch) but measured slower on B200 (25.9 vs 20.3 us per launch), so it is off by default.
+      const char* pair_on = std::getenv("GMI_DW_PAIR");
+      g.dw_pair[l] = gemm_pair_applicable(out_p, in_p, 1, 1, EPI_F32) && pair_on && pair_on[0] == '1';
+      if (g.dw_pair[l]) {  // one (problem, split) tile per co-resident SM pair: a single wave
+        const int pairs = std::max(2, std::min(gemm_pair_max_clusters(), g.ctas / 2));
+        const int nkb = (g.Bm + kGemmBlockK - 1) / kGemmBlockK;
+        const int per = (nkb + pairs / 2 - 1) / (pairs / 2);
+        for (int n = 0; n < 2; ++n) g.dw[l].prob[n].kb_per_split = per;
+        g.dw[l].splits = (nkb + per - 1) / per;
+      }
       g.flop_dw[l] = 2.0 * real * g.Bm;
 
       // input gradient dPre_{l-1} = (dPre_l W_l) * elu'(H_{l-1}); W_l read MN-major
@@ -1018,13 +1031,23 @@ void Trainer::train_minibatch(Gmi& g, int k, int adam_step) {
       if (l < L - 1) GMI_CUDA_CHECK(cudaStreamWaitEvent(g.s, g.ev_d[l], 0));
       GemmParams P = g.dw[l];
       if (l == 0) P.prob[0].b_row0 = P.prob[1].b_row0 = k * g.Bm;
-      gemm(g, GMI_PH_DW_GEMM, P, g.bn_dw[l], 1, 1, EPI_F32, g.flop_dw[l], 0, g.s, dw_ctas);
+      if (g.dw_pair[l]) {
+        timed(g.s, GMI_PH_DW_GEMM, g.flop_dw[l], 0.0, [&] { gemm_pair_launch(P, dw_ctas, g.s); });
+        ++launches_;
+      } else {
+        gemm(g, GMI_PH_DW_GEMM, P, g.bn_dw[l], 1, 1, EPI_F32, g.flop_dw[l], 0, g.s, dw_ctas);
+      }
     }
   }
   for (int l = L - 1; l >= 0 && !(par && L > 1); --l) {
     GemmParams P = g.dw[l];
     if (l == 0) P.prob[0].b_row0 = P.prob[1].b_row0 = k * g.Bm;
-    gemm(g, GMI_PH_DW_GEMM, P, g.bn_dw[l], 1, 1, EPI_F32, g.flop_dw[l]);
+    if (g.dw_pair[l]) {
+      timed(g.s, GMI_PH_DW_GEMM, g.flop_dw[l], 0.0, [&] { gemm_pair_launch(P, g.ctas, g.s); });
+      ++launches_;
+    } else {
+      gemm(g, GMI_PH_DW_GEMM, P, g.bn_dw[l], 1, 1, EPI_F32, g.flop_dw[l]);
+    }
     if (!g.fused_bias[l]) {  // else summed by the DACT GEMM that produced dPre_l
       const __nv_bfloat16* Ds[2] = {g.D[0][l], g.D[1][l]};
       const int widths[2] = {geo_.wp[l + 1], geo_.wp[l + 1]};

@@ -271,3 +271,19 @@ def test_nccl_allreduce_in_iteration_graph(cuda, monkeypatch, layout):
         plain.iteration()
         with_nccl.iteration()
     assert np.array_equal(plain.get("params").view(np.uint32), with_nccl.get("params").view(np.uint32))
+
+
+@pytest.mark.parametrize("dims", [(60, 8, [256, 256, 256]), (40, 20, [256, 256])])
+def test_pair_weight_gradient_matches_single_cta(cuda, monkeypatch, dims):
+    """cuda/gemm_pair.cu (tcgen05 cta_group::2: two SMs form one M = 256 tile, each loading half of
+    dPre and half of H) vs the single-CTA split-K kernel on the same minibatch: same slabs, same
+    k-block order per output element, so the weight and bias gradients agree to fp32 rounding."""
+    S, A, hidden = dims
+    g1, g2 = _grad_pair(monkeypatch, "GMI_DW_PAIR", None, dims, envs=1000)
+    lay = param_layout(S, A, hidden)
+    for key, t in lay.items():
+        if not isinstance(key, tuple):
+            continue
+        for part, n in (("w", t["out_p"] * t["in_p"]), ("b", t["out_p"])):
+            a, b = g1[t[part]:t[part] + n], g2[t[part]:t[part] + n]
+            assert np.linalg.norm(a - b) <= 1e-6 * (np.linalg.norm(b) + 1e-12), (key, part)
