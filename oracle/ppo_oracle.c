@@ -83,6 +83,14 @@ float ppo_bf16_round(float x) {
   return x;
 }
 
+/* Epoch permutation of GMI `gmi` (global id) at (iteration, epoch): out[j] = sample of row j. */
+int ppo_oracle_perm(unsigned long long seed, int gmi, int iteration, int epoch, uint32_t n, uint32_t* out) {
+  uint32_t keys[4];
+  philox_tag(seed, (uint32_t)gmi, (uint32_t)iteration, (uint32_t)epoch, TAG_PERM, keys);
+  for (uint32_t j = 0; j < n; ++j) out[j] = ppo_perm_index(j, n, keys);
+  return 0;
+}
+
 uint32_t ppo_perm_index(uint32_t j, uint32_t n, const uint32_t keys[4]) {
   if (n <= 1) return 0;
   uint32_t bits = 0;

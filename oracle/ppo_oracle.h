@@ -66,6 +66,7 @@ int ppo_oracle_set(void* h, const char* what, int gmi, const void* src, long lon
 /* Deterministic primitives shared (by restatement) with the device code. */
 void ppo_philox(uint32_t k0, uint32_t k1, const uint32_t ctr[4], uint32_t out[4]);
 uint32_t ppo_perm_index(uint32_t j, uint32_t n, const uint32_t keys[4]);
+int ppo_oracle_perm(unsigned long long seed, int gmi, int iteration, int epoch, uint32_t n, uint32_t* out);
 float ppo_bf16_round(float x);
 
 #ifdef __cplusplus

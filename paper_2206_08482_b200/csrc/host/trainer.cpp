@@ -1345,6 +1345,10 @@ long long Trainer::get(const std::string& what, int gi, void* dst) {
   const long long N = g.N, T = T_, S = geo_.S, A = geo_.A;
   if (what == "grad") return copy(g.grad, P, 4);
   if (what == "x") return copy(g.x, N * S, 4);
+  // epoch copy of the last shuffle (rows permuted by the epoch's bijection)
+  if (what == "oldlp_sh") return copy(g.oldlp_sh, T * N, 4);
+  if (what == "act_sh") return copy(g.act_sh, T * N * A, 4);
+  if (what == "trained_logp") return copy(g.logp, T * N, 4);  // the trainer's rollout copy
   // decoupled mode: rollout fields (act/logp/rew/done/obs/val/adv/ret) are the latest rollout
   // in the experience channel, one rollout ahead of the trainer
   const bool ch = decoupled_;

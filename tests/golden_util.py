@@ -125,6 +125,8 @@ def ppo_lib():
             "ppo_oracle_set": (C.c_int, [vp, C.c_char_p, C.c_int, vp, C.c_longlong]),
             "ppo_philox": (None, [C.c_uint32, C.c_uint32, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]),
             "ppo_perm_index": (C.c_uint32, [C.c_uint32, C.c_uint32, C.POINTER(C.c_uint32)]),
+            "ppo_oracle_perm": (C.c_int, [C.c_ulonglong, C.c_int, C.c_int, C.c_int, C.c_uint32,
+                                          C.POINTER(C.c_uint32)]),
             "ppo_bf16_round": (C.c_float, [C.c_float]),
         }
         for name, (res, args) in sig.items():
@@ -206,6 +208,12 @@ class PpoOracle:
     def adam(self, grad_sum):
         g = np.ascontiguousarray(grad_sum, dtype=np.float32)
         ppo_lib().ppo_oracle_adam(self.h, g.ctypes.data_as(C.POINTER(C.c_float)))
+
+
+def oracle_perm(seed, gmi, iteration, epoch, n):
+    out = np.empty(n, dtype=np.uint32)
+    ppo_lib().ppo_oracle_perm(seed, gmi, iteration, epoch, n, out.ctypes.data_as(C.POINTER(C.c_uint32)))
+    return out
 
 
 def param_layout(obs_dim, act_dim, hidden):

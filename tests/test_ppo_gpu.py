@@ -287,3 +287,21 @@ def test_pair_weight_gradient_matches_single_cta(cuda, monkeypatch, dims):
         for part, n in (("w", t["out_p"] * t["in_p"]), ("b", t["out_p"])):
             a, b = g1[t[part]:t[part] + n], g2[t[part]:t[part] + n]
             assert np.linalg.norm(a - b) <= 1e-6 * (np.linalg.norm(b) + 1e-12), (key, part)
+
+
+@pytest.mark.parametrize("layout", [dict(gmis_per_gpu=1), dict(gmis_per_gpu=2), dict(decoupled=1, gmi_backend=1)])
+def test_minibatch_permutation_indices_are_bit_exact(cuda, layout):
+    """The device epoch shuffle gathers rows by the oracle's permutation (Feistel bijection keyed
+    by (seed, GMI id, iteration, epoch), ppo_oracle.c): after an iteration the last epoch copy
+    holds logp[perm(j)] -- checked bit for bit against the device's own rollout log-probs with
+    the oracle's indices, per GMI (integer contract of the north_star)."""
+    from golden_util import oracle_perm
+    from paper_2206_08482_b200.ppo import PpoConfig, Trainer
+    cfg = PpoConfig(obs_dim=12, act_dim=3, hidden=[64, 64], num_envs=64, **layout)
+    t = Trainer(cfg)
+    for it in range(2):
+        t.iteration()
+        for gmi in range(cfg.gmis_per_gpu):
+            logp = t.get("trained_logp", gmi)
+            perm = oracle_perm(cfg.seed, gmi, it, cfg.epochs - 1, logp.size)
+            assert np.array_equal(t.get("oldlp_sh", gmi).view(np.uint32), logp[perm].view(np.uint32)), (it, gmi)
