@@ -496,6 +496,7 @@ void Trainer::build_plans() {
         const int ws_dx = std::getenv("GMI_DX_WS") ? gemm_ws_bn(g.Bm, in_p, out_p, 2, g.ctas) : 0;
         g.ws_dx[l] = ws_dx > 0;
         g.bn_dx[l] = ws_dx > 0 ? ws_dx : gemm_choose_bn(g.Bm, in_p, 2, 1, g.ctas);
+        if (const char* bn = std::getenv("GMI_DX_BN"); bn && ws_dx == 0) g.bn_dx[l] = std::atoi(bn);  // experiments
         g.dx[l] = GemmParams{};
         for (int n = 0; n < 2; ++n) {
           GemmProblem p{};
