@@ -99,6 +99,11 @@ GMI_API int gmi_reduce_device(int strategy, int num_gpus, const int* counts, con
 GMI_API int gmi_execute_host(int strategy, int num_gpus, const int* counts, const int* ids,
                              const void* const* bufs, size_t len, int dtype, void* result);
 
+/* B200 extension: SMs of the green context that realises an MPS `share` on an sm100 GPU
+ * (whole 8-SM groups of 148 SMs, or of sm_units when > 8). validate_layout flags sm100 shares
+ * below one group and MIG partitions on sm100 (the B200 MIG profile table is not modelled). */
+GMI_API int gmi_green_sms(double share, int sm_units, int* out);
+
 /* ------------------------------------------------------------------ topology
  * topology.hpp:60-252. arch: 70, 80 or 100 (sm100 is a B200 extension).
  * backend: 0 = MPS share (realised as an SM-partitioned green context), 1 = MIG. */

@@ -145,6 +145,7 @@ PROTOTYPES: dict[str, tuple] = {
                                     P(ReductionInfo)]),
     "gmi_reduce_device": (ci, [ci, ci, c_int_p, c_int_p, P(vp), vp, csz, ci, ci, vp]),
     "gmi_validate_layout": (ci, [P(TopologyT), P(ViolationT), ci, c_int_p]),
+    "gmi_green_sms": (ci, [C.c_double, ci, c_int_p]),
     "gmi_select_backend": (ci, [ci, ci, c_int_p]),
     "gmi_path_bandwidth": (ci, [P(TopologyT), ci, ci, c_int_p, c_double_p]),
     "gmi_load_benchmark": (ci, [C.c_char_p, P(WorkloadT)]),

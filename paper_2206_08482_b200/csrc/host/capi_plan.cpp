@@ -225,6 +225,17 @@ GMI_API int gmi_load_benchmark(const char* name, gmi_workload_t* out) {
   return guarded([&] { from_workload(catalog(name ? name : ""), out); });
 }
 
+GMI_API int gmi_green_sms(double share, int sm_units, int* out) {
+  return guarded([&] {
+    if (!out) invalid("null argument");
+    if (!(share > 0 && share <= 1.0)) invalid("share outside (0, 1]");
+    plan::Gpu g;
+    g.arch = plan::Arch::SM100;
+    g.sm_units = sm_units;
+    *out = plan::green_sms(share, g);
+  });
+}
+
 GMI_API int gmi_validate_workload(const gmi_workload_t* w) {
   return guarded([&] { check_workload(to_workload(w)); });
 }

@@ -98,6 +98,14 @@ static const Gpu* gpu_by_id(const Machine& m, int id) {
   return nullptr;
 }
 
+// SMs of the green context realising an MPS share on an sm100 GPU: whole 8-SM groups
+// (cuDevSmResourceSplitByCount granularity, cuda.h:25262) of the physical SM count (148 on
+// B200 unless the config gives sm_units > 8).
+int green_sms(double share, const Gpu& gpu) {
+  const int sms = gpu.sm_units > 8 ? gpu.sm_units : 148;
+  return int(share * sms + 1e-9) / 8 * 8;
+}
+
 std::vector<std::pair<int, std::string>> check_machine(const Machine& m) {
   std::vector<std::pair<int, std::string>> bad;
   auto flag = [&](int gpu, std::string why) { bad.emplace_back(gpu, std::move(why)); };
@@ -137,6 +145,10 @@ std::vector<std::pair<int, std::string>> check_machine(const Machine& m) {
       }
     }
     if (!fields) continue;
+    if (be == Backend::MIG && gpu.arch == Arch::SM100) {  // B200 extension (reference stops at sm80)
+      flag(gid, "MIG profiles not modelled for sm100: use backend=mps (SM-partitioned green contexts)");
+      continue;
+    }
     if (be == Backend::MIG) {
       if (gpu.arch == Arch::SM70) {
         flag(gid, "MIG unavailable on sm70 (only MPS)");
@@ -164,6 +176,10 @@ std::vector<std::pair<int, std::string>> check_machine(const Machine& m) {
       double sum = 0;
       for (const auto* p : parts) sum += p->sm_share;
       if (sum > 1.0 + 1e-9) flag(gid, "MPS shares exceed 1.0");
+      if (gpu.arch == Arch::SM100)  // B200: each share is realised as a green context of 8-SM groups
+        for (const auto* p : parts)
+          if (green_sms(p->sm_share, gpu) < 8)
+            flag(gid, "gmi " + std::to_string(p->gmi_id) + " share below one 8-SM green-context group");
     }
   }
   return bad;

@@ -100,6 +100,7 @@ const MigShape* mig_by_name(const std::string& name);
 
 Machine default_machine(int num_gpus);
 std::vector<std::pair<int, std::string>> check_machine(const Machine& m);  // violations
+int green_sms(double share, const Gpu& gpu);  // sm100: SMs of the green context realising an MPS share
 Backend backend_for(Arch a, bool training);
 Link link_between(const Machine& m, int src_gmi, int dst_gmi, double* bandwidth);
 

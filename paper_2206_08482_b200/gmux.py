@@ -287,6 +287,14 @@ class Topology:
         return t
 
 
+def green_sms(share: float, sm_units: int = 8) -> int:
+    """B200 extension: SMs of the green context realising an MPS `share` on an sm100 GPU
+    (whole 8-SM groups of 148 SMs, or of sm_units when > 8)."""
+    n = C.c_int()
+    L.check(_lib().gmi_green_sms(float(share), int(sm_units), C.byref(n)))
+    return n.value
+
+
 def default_topology(num_gpus: int = 2) -> Topology:
     return Topology([GpuSpec(i) for i in range(num_gpus)])
 

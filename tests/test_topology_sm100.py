@@ -1,0 +1,50 @@
+"""the topology extension for B200 (reference enum stops at sm80,
+topology.hpp:20). MPS shares on an sm100 GPU are realised as SM-partitioned green contexts in
+whole 8-SM groups (cuDevSmResourceSplitByCount granularity, cuda.h:25262); validate_layout
+flags shares below one group and MIG partitions on sm100 (no B200 MIG profile table is
+modelled: MIG mode is disabled on the pool's B200s, `nvidia-smi mig -lgip` lists none). The
+sm70 / sm80 rules stay the reference's (tests/test_planner_golden.py)."""
+import os
+
+from paper_2206_08482_b200 import gmux
+from paper_2206_08482_b200.ppo import PpoConfig
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_green_context_sizes():
+    assert gmux.green_sms(1.0) == 144
+    assert gmux.green_sms(0.125) == 16
+    assert gmux.green_sms(0.875) == 128
+    assert gmux.green_sms(0.25) == 32
+    assert gmux.green_sms(0.05) == 0
+    assert gmux.green_sms(0.5, sm_units=132) == 64
+
+
+def _b200(parts):
+    t = gmux.Topology([gmux.GpuSpec(0, gmux.GpuArch.SM100, 8, 180.0)])
+    t.partitions = parts
+    return t
+
+
+def test_sm100_share_below_one_group_is_a_violation():
+    ok = _b200([gmux.mps_partition(0, 0, 0.125, 22.5), gmux.mps_partition(1, 0, 0.875, 157.5)])
+    assert gmux.validate_layout(ok) == []
+    bad = _b200([gmux.mps_partition(0, 0, 0.05, 9.0), gmux.mps_partition(1, 0, 0.95, 171.0)])
+    v = gmux.validate_layout(bad)
+    assert len(v) == 1 and v[0].gpu_id == 0 and "8-SM green-context group" in v[0].rule
+
+
+def test_sm100_mig_is_a_violation_but_sm80_mig_is_the_reference_rule():
+    v = gmux.validate_layout(_b200([gmux.mig_partition(0, 0, "3g.20gb")]))
+    assert len(v) == 1 and "not modelled for sm100" in v[0].rule
+    a100 = gmux.Topology([gmux.GpuSpec(0, gmux.GpuArch.SM80, 8, 40.0)], [gmux.mig_partition(0, 0, "3g.20gb")])
+    assert gmux.validate_layout(a100) == []
+
+
+def test_decoupled_config_serving_share_matches_green_context():
+    cfg = gmux.load_config(os.path.join(ROOT, "configs", "at_4096env_decoupled.cfg"))
+    topo = gmux.topology_from_config(cfg)
+    share = topo.partitions[0].sm_share
+    assert gmux.green_sms(share) == PpoConfig.from_config_file(
+        os.path.join(ROOT, "configs", "at_4096env_decoupled.cfg")).serving_sms == 16
