@@ -86,6 +86,9 @@ __global__ void __launch_bounds__(kThreads, 1) rollout_cluster_kernel(const __gr
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 4);
   float* ls_s = reinterpret_cast<float*>(bars + 8);  // [16] log_std, [16] exp(log_std)
   float* sig_s = ls_s + 16;
+  // per K-chunk arrival of a hidden layer's all-gathered output ([buffer][chunk = producing CTA]):
+  // the next layer's MMAs on chunk kc start as soon as that slice is here, in the fixed kc order
+  uint64_t* chunk_full = bars + 24;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int L = a.L, T = a.T;
@@ -98,6 +101,7 @@ __global__ void __launch_bounds__(kThreads, 1) rollout_cluster_kernel(const __gr
     ptx::mbar_init(wbar, 1);
     ptx::mbar_init(&act_full[0], 1);
     ptx::mbar_init(&act_full[1], 1);
+    for (int i = 0; i < 2 * C; ++i) ptx::mbar_init(&chunk_full[i], 1);
     ptx::mbar_init(acc_full, 1);
     ptx::fence_mbar_init();
     ptx::tma_prefetch_desc(&a.map_obs);
@@ -128,13 +132,13 @@ __global__ void __launch_bounds__(kThreads, 1) rollout_cluster_kernel(const __gr
     // ------------------------------------------------ MMA issuer
     if (lane == 0) {
       ptx::mbar_wait(wbar, 0);
-      int ph[2] = {0, 0}, acc_ph = 0;
+      int obs_ph = 0, cph[2] = {0, 0}, acc_ph = 0;
       const uint32_t idesc_h = ptx::umma_idesc_bf16(kRows, 64, 0, 0);
       const uint32_t idesc_o = ptx::umma_idesc_bf16(kRows, 16, 0, 0);
       for (int t = 0; t < T; ++t)
         for (int l = 0; l <= L; ++l) {
           const int b = l & 1;
-          ptx::mbar_wait(&act_full[b], (ph[b]++) & 1);
+          if (l == 0) ptx::mbar_wait(&act_full[0], (obs_ph++) & 1);  // observation rows of all 4 CTAs
           ptx::tc_fence_after();
           const bool head = l == L;
           const uint32_t acc = tmem + (head ? 128u : uint32_t(acc_ph++ & 1) * 64u);
@@ -144,12 +148,17 @@ __global__ void __launch_bounds__(kThreads, 1) rollout_cluster_kernel(const __gr
           const int K = a.in_p[l];
           const int nk = (K + 63) / 64;
           for (int kc = 0; kc < nk; ++kc) {
+            if (l > 0) {  // slice kc of the previous layer (local or pushed by CTA kc)
+              ptx::mbar_wait(&chunk_full[b * C + kc], cph[b] & 1);
+              ptx::tc_fence_after();
+            }
             const int ks = min(4, (K - kc * 64 + 15) / 16);
             for (int k = 0; k < ks; ++k)
               ptx::mma_bf16(acc, ptx::umma_desc_sw128(in + kc * kChunk + k * 32, 16, 1024),
                             ptx::umma_desc_sw128(wb + kc * cstride + k * 32, 16, 1024), head ? idesc_o : idesc_h,
                             (kc > 0 || k > 0) ? 1u : 0u);
           }
+          if (l > 0) ++cph[b];
           ptx::mma_commit(acc_full);
         }
     }
@@ -219,15 +228,22 @@ __global__ void __launch_bounds__(kThreads, 1) rollout_cluster_kernel(const __gr
         ptx::tc_fence_before();
         epi_bar();
         trace_at(a, t * 16 + 2 * l + 1);
-        if (tid == 0) {  // push the slice (one 16 KB K-chunk) to the peers, then arm + arrive locally
+        if (tid == 0) {  // push the slice (one 16 KB K-chunk) to the peers' chunk `rank`, arm our
+          // remote chunks and mark our own chunk ready
           const uint32_t src = act_base[nb] + rank * kChunk;
-          const uint32_t bar = ptx::smem_u32(&act_full[nb]);
+          const uint32_t bar = ptx::smem_u32(&chunk_full[nb * C + rank]);
 #pragma unroll
           for (int p = 1; p < C; ++p) {
             const uint32_t peer = uint32_t((rank + p) % C);
             ptx::bulk_s2s(ptx::mapa(src, peer), src, kChunk, ptx::mapa(bar, peer));
           }
-          ptx::mbar_arrive_expect_tx(&act_full[nb], uint32_t(C - 1) * kChunk);
+#pragma unroll
+          for (int kc = 0; kc < C; ++kc) {
+            if (kc == rank)
+              ptx::mbar_arrive(&chunk_full[nb * C + kc]);
+            else
+              ptx::mbar_arrive_expect_tx(&chunk_full[nb * C + kc], kChunk);
+          }
         }
       }
 
