@@ -83,3 +83,16 @@ def test_execute_dropin_matches_reference_cli_example(cuda):
         run = G.execute(s, lay, bufs, G.default_topology(2))
         assert run.result == ref[s.name]["result"]
         assert run.latency == ref[s.name]["latency"]
+
+
+@pytest.mark.parametrize("mpl,algo", [([[0, 1, 2, 3, 4, 5, 6]], 0), ([[0, 1, 2, 3], [4, 5, 6, 7]], 2)])
+def test_fp32_bit_identical_at_shadowhand_size(cuda, mpl, algo):
+    """Largest BASELINE payload: ShadowHand-like 211:512:512:512:256:20 actor-critic, P = 1,535,765
+    parameters (workload.hpp:95-100), folded over 7 GMIs of one GPU (cfg 5, MPR) and a 2 x 4
+    layout (HAR); bit-identical to the ring oracle."""
+    length = 1535765
+    ids = [i for l in mpl for i in l]
+    bufs = [(buffer_values("hash", 23, i, length) - 0.55).astype(np.float32) for i in ids]
+    out, _ = _device_reduce(algo, mpl, bufs)
+    ref = oracle_execute(algo, mpl, bufs)
+    assert np.array_equal(out.view(np.uint32), ref.view(np.uint32))
