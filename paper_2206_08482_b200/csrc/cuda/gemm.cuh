@@ -81,7 +81,7 @@ __device__ __forceinline__ void gemm_stamp(unsigned long long* tr, int lt, int k
 }
 
 #ifndef GMI_WS_STAGES
-#define GMI_WS_STAGES 4
+#define GMI_WS_STAGES 8
 #endif
 #ifndef GMI_WS_STAGING
 #define GMI_WS_STAGING 1
@@ -90,15 +90,18 @@ __device__ __forceinline__ void gemm_stamp(unsigned long long* tr, int lt, int k
 template <int BN, int EPI, int WS>
 struct GemmSmem {
   static constexpr int kEpiWarps = gemm_epi_warps(EPI);
-  // WS: 4 activation stages, single epilogue staging buffer per warp (2 stages + double staging
-  // measured 3% slower on B200: the A ring starves the MMA)
-  static constexpr int kStages = WS ? GMI_WS_STAGES : (BN == 256 ? 3 : 4);
+  // WS: single epilogue staging buffer per warp (2 stages + double staging measured 3% slower
+  // on B200: the A ring starves the MMA)
   static constexpr uint32_t kA = kGemmBlockM * kGemmBlockK * 2;  // 16 KB
   static constexpr uint32_t kB = BN * kGemmBlockK * 2;           // one k-block of B
-  static constexpr uint32_t kStage = WS ? kA : kA + kB;
   static constexpr uint32_t kBRes = WS ? kGemmMaxKbWS * kB : 0;  // resident B (WS)
   static constexpr int kStagingBufs = WS ? GMI_WS_STAGING : 2;
   static constexpr uint32_t kStaging = EPI == 2 ? 4096 : 2048;  // one 32x32 chunk per warp
+  // WS: as many activation stages as fit next to the resident weights, up to two whole tiles
+  // (K <= 256 is 4 k-blocks), so the next tile's rows are in flight while this tile's MMAs run
+  static constexpr int kWsFit = int((232448u - 1280u - kBRes - kEpiWarps * kStagingBufs * kStaging) / kA);
+  static constexpr int kStages = WS ? (kWsFit < GMI_WS_STAGES ? kWsFit : GMI_WS_STAGES) : (BN == 256 ? 3 : 4);
+  static constexpr uint32_t kStage = WS ? kA : kA + kB;
   static constexpr uint32_t kBarOff = kStages * kStage + kBRes + kEpiWarps * kStagingBufs * kStaging;
   static constexpr uint32_t kBytes = kBarOff + 256 + 1024;  // + barriers + alignment slack
   static constexpr uint32_t kTmemCols = 2 * BN < 32 ? 32 : 2 * BN;

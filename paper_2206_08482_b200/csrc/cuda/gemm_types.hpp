@@ -36,7 +36,7 @@ struct alignas(64) GemmProblem {
 
 // All problems of one launch share M, N, K and the split count (grouped GEMM).
 struct alignas(64) GemmParams {
-  GemmProblem prob[2];
+  GemmProblem prob[4];  // grouped problems (e.g. policy / value nets, or their N-halves)
   int num_problems;
   int splits;
   unsigned long long* trace;  // optional [8 tiles][16] globaltimer stamps of CTA 0 (development aid)

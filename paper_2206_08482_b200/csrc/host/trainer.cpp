@@ -159,6 +159,7 @@ struct Trainer::Gmi {
   ppo::RolloutArgs roll_args{};
   bool fused_bias[GMI_MAX_HIDDEN] = {};  // bias gradient summed inside the layer's dW GEMM
   bool dw_pair[GMI_MAX_HIDDEN] = {};     // weight gradient on SM pairs (cuda/gemm_pair.cu)
+  bool dx_halves[GMI_MAX_HIDDEN] = {};   // input gradient as 4 weight-stationary problems (N-halves)
   bool fused_head = false;
   int head_grid = 0;
   ppo::HeadFusedArgs head_args{};
@@ -493,25 +494,33 @@ void Trainer::build_plans() {
       if (l > 0) {
         // input gradients stream W with the dPre tiles: measured faster than weight-stationary here
         // (the elu' operand already doubles the activation traffic; WS has one staging buffer)
-        const int ws_dx = std::getenv("GMI_DX_WS") ? gemm_ws_bn(g.Bm, in_p, out_p, 2, g.ctas) : 0;
+        // Default for 256-wide inputs: weight-stationary over four problems (2 nets x 2 N-halves
+        // of 128 columns): each CTA keeps one 256 x 128 weight half resident and streams only the
+        // dPre tiles, with one 32-column chunk per epilogue warp per tile.
+        const char* dx4_off = std::getenv("GMI_DX_WS4_OFF");
+        g.dx_halves[l] = in_p == 256 && out_p <= 256 && !(dx4_off && dx4_off[0] == '1') &&
+                         gemm_ws_bn(g.Bm, 128, out_p, 4, g.ctas) == 128;
+        const int ws_dx = g.dx_halves[l] ? 128 : std::getenv("GMI_DX_WS") ? gemm_ws_bn(g.Bm, in_p, out_p, 2, g.ctas) : 0;
         g.ws_dx[l] = ws_dx > 0;
         g.bn_dx[l] = ws_dx > 0 ? ws_dx : gemm_choose_bn(g.Bm, in_p, 2, 1, g.ctas);
         if (const char* bn = std::getenv("GMI_DX_BN"); bn && ws_dx == 0) g.bn_dx[l] = std::atoi(bn);  // experiments
         g.dx[l] = GemmParams{};
-        for (int n = 0; n < 2; ++n) {
-          GemmProblem p{};
-          p.map_a = tma_kmajor(g.D[n][l], out_p, g.Bm, out_p, kGemmBlockM);
-          p.map_b = tma_mnmajor(shadow_ + geo_.net[n][l].w, in_p, out_p, in_p);
-          p.map_out = make_tma_out_bf16(g.D[n][l - 1], in_p, g.Bm, in_p);
-          p.aux = g.H[n][l - 1];
-          p.ld_aux = in_p;
-          p.M = g.Bm;
-          p.N = in_p;
-          p.K = out_p;
-          p.kb_per_split = (out_p + kGemmBlockK - 1) / kGemmBlockK;
-          g.dx[l].prob[n] = p;
-        }
-        g.dx[l].num_problems = 2;
+        const int halves = g.dx_halves[l] ? 2 : 1, ncols = in_p / halves;
+        for (int n = 0; n < 2; ++n)
+          for (int hh = 0; hh < halves; ++hh) {
+            GemmProblem p{};
+            p.map_a = tma_kmajor(g.D[n][l], out_p, g.Bm, out_p, kGemmBlockM);
+            p.map_b = tma_mnmajor(shadow_ + geo_.net[n][l].w + hh * ncols, ncols, out_p, in_p);
+            p.map_out = make_tma_out_bf16(g.D[n][l - 1] + hh * ncols, ncols, g.Bm, in_p);
+            p.aux = g.H[n][l - 1] + hh * ncols;
+            p.ld_aux = in_p;
+            p.M = g.Bm;
+            p.N = ncols;
+            p.K = out_p;
+            p.kb_per_split = (out_p + kGemmBlockK - 1) / kGemmBlockK;
+            g.dx[l].prob[n * halves + hh] = p;
+          }
+        g.dx[l].num_problems = 2 * halves;
         g.dx[l].splits = 1;
         g.flop_dx[l] = 2.0 * real * g.Bm;
       }
