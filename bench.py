@@ -143,9 +143,17 @@ def phase_table(prof: dict, iter_ms: float, peak_tf: float, peak_gbs: float) -> 
             continue
         row = {"ms": round(p["ms"], 4), "share": round(p["ms"] / iter_ms, 4) if iter_ms else None,
                "launches": p["launches"]}
+        ridge = peak_tf * 1e12 / (peak_gbs * 1e9)  # flop per byte where the two roofs meet
         if p["flop"] > 0 and p["ms"] > 0:
             tf = p["flop"] / (p["ms"] / 1e3) / 1e12
-            row.update(bound="tensor", achieved_tflops=round(tf, 1), frac=round(tf / peak_tf, 4))
+            row.update(achieved_tflops=round(tf, 1))
+            if p["bytes"] > 0:
+                gbs = p["bytes"] / (p["ms"] / 1e3) / 1e9
+                row.update(achieved_gbs=round(gbs, 1), intensity=round(p["flop"] / p["bytes"], 1))
+            if p["bytes"] > 0 and p["flop"] / p["bytes"] < ridge:
+                row.update(bound="hbm", frac=round(gbs / peak_gbs, 4))
+            else:
+                row.update(bound="tensor", frac=round(tf / peak_tf, 4))
         elif p["bytes"] > 0 and p["ms"] > 0:
             gbs = p["bytes"] / (p["ms"] / 1e3) / 1e9
             row.update(bound="hbm", achieved_gbs=round(gbs, 1), frac=round(gbs / peak_gbs, 4))
@@ -300,8 +308,13 @@ def main():
 
     if rank == 0:
         peak_tf, peak_gbs, peak_src = measured_peaks()
-        gemm_ms, gemm_flop = ist.gemm_ms, ist.gemm_flop
-        achieved = gemm_flop / (gemm_ms / 1e3) / 1e12 if gemm_ms > 0 else 0.0
+        gemm_ms, gemm_flop, gemm_bytes = ist.gemm_ms, ist.gemm_flop, ist.gemm_bytes
+        achieved_tf = gemm_flop / (gemm_ms / 1e3) / 1e12 if gemm_ms > 0 else 0.0
+        achieved_gbs = gemm_bytes / (gemm_ms / 1e3) / 1e9 if gemm_ms > 0 else 0.0
+        # K <= 256 layer GEMMs and split-K weight gradients sit below the ridge point
+        # (peak_tf / peak_gbs flop per byte): the roof that binds them is HBM bandwidth.
+        intensity = gemm_flop / gemm_bytes if gemm_bytes > 0 else float("inf")
+        hbm_bound = intensity < peak_tf * 1e12 / (peak_gbs * 1e9)
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
             cv, cores, sample = cpu_iteration_sample(cfg, args.cpu_sample_envs, 1, 0)
@@ -326,9 +339,17 @@ def main():
                        "env_steps_per_step": steps_total // args.steps,
                        "l2": f"no flush: per-iteration working set ~{ws:.0f} MB > 126 MB L2",
                        "cuda_graph": bool(cfg.use_graph)},
-            "roofline": {"bound": "tensor", "kernel": "gemm_tcgen05_kernel (every MLP GEMM of GMI 0, all phases)",
-                         "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
-                         "frac": achieved / peak_tf, "traffic": gemm_traffic(),
+            "roofline": {"bound": "hbm" if hbm_bound else "tensor",
+                         "kernel": "gemm_tcgen05_kernel (every MLP GEMM of GMI 0, all phases)",
+                         "achieved": achieved_gbs if hbm_bound else achieved_tf,
+                         "peak": peak_gbs if hbm_bound else peak_tf, "unit": "GB/s" if hbm_bound else "TFLOP/s",
+                         "frac": achieved_gbs / peak_gbs if hbm_bound else achieved_tf / peak_tf,
+                         "intensity_flop_per_byte": intensity,
+                         "ridge_flop_per_byte": peak_tf * 1e12 / (peak_gbs * 1e9),
+                         "algorithmic_bytes_per_launch": gemm_bytes / max(1, ist.gemm_launches),
+                         "tensor_view": {"achieved": achieved_tf, "peak": peak_tf, "unit": "TFLOP/s",
+                                         "frac": achieved_tf / peak_tf},
+                         "traffic": gemm_traffic(),
                          "traffic_unit": "DRAM bytes per launch (ncu, profiles/traffic.json)",
                          "peak_source": peak_src,
                          "gemm_share_of_step": gemm_ms / iter_ms_instr if iter_ms_instr else None,

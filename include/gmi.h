@@ -376,6 +376,7 @@ typedef struct {
   double gemm_flop; /* instrument: algorithmic GEMM flops of those launches */
   int gemm_launches;
   int kernel_launches; /* every libgmi kernel launched this iteration (this GPU) */
+  double gemm_bytes;   /* instrument: algorithmic GEMM bytes (operands read + outputs written) */
 } gmi_ppo_stats_t;
 
 GMI_API void gmi_ppo_config_defaults(gmi_ppo_config_t* cfg);

@@ -830,13 +830,29 @@ void Trainer::timed(cudaStream_t s, int phase, double flop, double bytes, F&& f)
   m.bytes = bytes;
 }
 
+// Algorithmic bytes of one grouped GEMM launch: each operand read once, each output written
+// once (bf16 activations / dPre, or fp32 split-K slabs), plus the elu' operand of EPI_DACT.
+static double gemm_bytes(const GemmParams& P, int epi) {
+  double b = 0;
+  for (int i = 0; i < P.num_problems; ++i) {
+    const GemmProblem& p = P.prob[i];
+    b += 2.0 * p.K * (double(p.M) + p.N);
+    b += double(p.M) * p.N * (epi == EPI_F32 ? 4.0 * P.splits : epi == EPI_DACT ? 4.0 : 2.0);
+  }
+  return b;
+}
+
 void Trainer::gemm(Gmi& g, int phase, const GemmParams& P, int bn, int amn, int bmn, int epi, double flop, int ws,
                    cudaStream_t stream, int ctas) {
   cudaStream_t st = stream ? stream : g.s;
   // GMI_GEMM_TRACE=<phase id>: globaltimer stamps of CTA 0 for every launch of that phase
   // (the last one of the iteration wins; read with get("gemm_trace")). Development aid.
+  // GMI_GEMM_TRACE_NTH=<k>: only the k-th recorded launch of the phase (e.g. 0 = the first
+  // minibatch's last layer for the backward phases).
   static const char* tr_env = std::getenv("GMI_GEMM_TRACE");
-  if (tr_env && std::atoi(tr_env) == phase) {
+  static const char* tr_nth = std::getenv("GMI_GEMM_TRACE_NTH");
+  static int tr_calls = 0;
+  if (tr_env && std::atoi(tr_env) == phase && (!tr_nth || tr_calls++ == std::atoi(tr_nth))) {
     if (!gemm_trace_) {
       GMI_CUDA_CHECK(cudaMalloc(&gemm_trace_, 128 * 8));
       GMI_CUDA_CHECK(cudaMemset(gemm_trace_, 0, 128 * 8));
@@ -844,11 +860,11 @@ void Trainer::gemm(Gmi& g, int phase, const GemmParams& P, int bn, int amn, int 
     }
     GemmParams Pt = P;
     Pt.trace = static_cast<unsigned long long*>(gemm_trace_);
-    timed(st, phase, flop, 0.0, [&] { gemm_launch(Pt, bn, amn, bmn, epi, st, ctas > 0 ? ctas : g.ctas, ws); });
+    timed(st, phase, flop, gemm_bytes(P, epi), [&] { gemm_launch(Pt, bn, amn, bmn, epi, st, ctas > 0 ? ctas : g.ctas, ws); });
     ++launches_;
     return;
   }
-  timed(st, phase, flop, 0.0, [&] { gemm_launch(P, bn, amn, bmn, epi, st, ctas > 0 ? ctas : g.ctas, ws); });
+  timed(st, phase, flop, gemm_bytes(P, epi), [&] { gemm_launch(P, bn, amn, bmn, epi, st, ctas > 0 ? ctas : g.ctas, ws); });
   ++launches_;
 }
 
@@ -1300,6 +1316,7 @@ void Trainer::synchronize(gmi_ppo_stats_t* st) {
       if (marks_[i].flop > 0) {
         gemm.ms += ms;
         gemm.flop += marks_[i].flop;
+        gemm.bytes += marks_[i].bytes;
         gemm.launches += 1;
       }
     }
@@ -1319,6 +1336,7 @@ void Trainer::synchronize(gmi_ppo_stats_t* st) {
   st->gemm_ms = gemm.ms;
   st->gemm_flop = gemm.flop;
   st->gemm_launches = gemm.launches;
+  st->gemm_bytes = gemm.bytes;
 }
 
 // ------------------------------------------------------------------ parity hooks

@@ -40,7 +40,7 @@ class PpoStatsT(C.Structure):
     _fields_ = [("policy_loss", C.c_double), ("value_loss", C.c_double), ("approx_kl", C.c_double),
                 ("clip_frac", C.c_double), ("mean_reward", C.c_double), ("env_steps", C.c_longlong),
                 ("gemm_ms", C.c_double), ("gemm_flop", C.c_double), ("gemm_launches", C.c_int),
-                ("kernel_launches", C.c_int)]
+                ("kernel_launches", C.c_int), ("gemm_bytes", C.c_double)]
 
 
 _PROTOS = {
@@ -164,6 +164,7 @@ class IterationStats:
     gemm_flop: float
     gemm_launches: int
     kernel_launches: int
+    gemm_bytes: float = 0.0
 
 
 _DT = {"done": np.uint8, "ep_step": np.int32, "ep_len": np.int32, "ep_count": np.int32,
@@ -192,7 +193,8 @@ class Trainer:
     @staticmethod
     def _stats(s: PpoStatsT) -> IterationStats:
         return IterationStats(s.policy_loss, s.value_loss, s.approx_kl, s.clip_frac, s.mean_reward,
-                              s.env_steps, s.gemm_ms, s.gemm_flop, s.gemm_launches, s.kernel_launches)
+                              s.env_steps, s.gemm_ms, s.gemm_flop, s.gemm_launches, s.kernel_launches,
+                              s.gemm_bytes)
 
     def iteration(self) -> IterationStats:
         s = PpoStatsT()
