@@ -168,25 +168,22 @@ __global__ void __launch_bounds__(256) segments_kernel(const __grid_constant__ S
   if (vec) {
     if (i0 < sg.len) {
       const float* base = sg.src + i0;
-      int p = p0;
-      for (; p + 4 <= p1; p += 4) {
-        float4 v[4];
+      // up to 8 parts in flight per thread (a warp owns ~nparts/8 parts, so usually one round
+      // trip), summed in part order
+      for (int p = p0; p < p1; p += 8) {
+        float4 v[8];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) v[u] = __ldcs(reinterpret_cast<const float4*>(base + (long long)(p + u) * sg.stride));
+        for (int u = 0; u < 8; ++u)
+          if (p + u < p1) v[u] = __ldcs(reinterpret_cast<const float4*>(base + (long long)(p + u) * sg.stride));
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          acc.x += v[u].x;
-          acc.y += v[u].y;
-          acc.z += v[u].z;
-          acc.w += v[u].w;
+        for (int u = 0; u < 8; ++u) {
+          if (p + u < p1) {
+            acc.x += v[u].x;
+            acc.y += v[u].y;
+            acc.z += v[u].z;
+            acc.w += v[u].w;
+          }
         }
-      }
-      for (; p < p1; ++p) {
-        const float4 v = __ldcs(reinterpret_cast<const float4*>(base + (long long)p * sg.stride));
-        acc.x += v.x;
-        acc.y += v.y;
-        acc.z += v.z;
-        acc.w += v.w;
       }
     }
   } else {

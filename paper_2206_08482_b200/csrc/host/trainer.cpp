@@ -160,6 +160,7 @@ struct Trainer::Gmi {
   bool fused_bias[GMI_MAX_HIDDEN] = {};  // bias gradient summed inside the layer's dW GEMM
   bool dw_pair[GMI_MAX_HIDDEN] = {};     // weight gradient on SM pairs (cuda/gemm_pair.cu)
   bool dx_halves[GMI_MAX_HIDDEN] = {};   // input gradient as 4 weight-stationary problems (N-halves)
+  bool dw_grouped = false;               // dW of layers L-1 and L-2 in one launch (dw[L-1], 4 problems)
   bool fused_head = false;
   int head_grid = 0;
   ppo::HeadFusedArgs head_args{};
@@ -689,6 +690,35 @@ void Trainer::build_plans() {
       }
     }
 
+    // Weight gradients of the last two hidden layers in one grouped launch (4 problems: 2 nets x
+    // 2 layers) once dPre of both exist (after dx(L-1)): half the split-K slabs for the same
+    // grid (splits 37 -> 18 at 256 x 256), so half the slab writes and gradient-assembly reads,
+    // and one launch ramp/tail less per minibatch. GMI_DW_GROUP=0 keeps one launch per layer.
+    {
+      const char* grp = std::getenv("GMI_DW_GROUP");
+      const int a = L - 1, b = L - 2;
+      g.dw_grouped = L >= 3 && !(grp && grp[0] == '0') && !bwd_par_ && !g.dw_pair[a] && !g.dw_pair[b] &&
+                     geo_.wp[a + 1] == geo_.wp[a] && geo_.wp[a] == geo_.wp[b];
+      if (g.dw_grouped) {
+        const int out_p = geo_.wp[a + 1], in_p = geo_.wp[a];
+        int splits = 1, kbps = 1;
+        pick_splits(out_p, in_p, g.bn_dw[a], 4, g.Bm, g.ctas, &splits, &kbps);
+        GemmParams P{};
+        for (int j = 0; j < 4; ++j) {
+          const int l = j < 2 ? a : b, n = j & 1;
+          GemmProblem p = g.dw[l].prob[n];
+          p.map_out = make_tma_out_f32(g.slab[n][l], in_p, out_p, splits, in_p, (uint64_t)out_p * in_p);
+          p.kb_per_split = kbps;
+          P.prob[j] = p;
+        }
+        P.num_problems = 4;
+        P.splits = splits;
+        g.dw[a] = P;
+        g.dw[b].splits = splits;
+        g.flop_dw[a] += g.flop_dw[b];
+      }
+    }
+
     // gradient assembly segments (fixed-order sums of slabs / partials into the flat grad)
     const int cb = ppo::colsum_blocks(g.Bm);
     const int hs = ppo::head_partial_stride(A);
@@ -832,11 +862,15 @@ void Trainer::timed(cudaStream_t s, int phase, double flop, double bytes, F&& f)
 
 // Algorithmic bytes of one grouped GEMM launch: each operand read once, each output written
 // once (bf16 activations / dPre, or fp32 split-K slabs), plus the elu' operand of EPI_DACT.
+// Problems that share an operand (the N-halves of one input-gradient GEMM read the same dPre
+// rows) count it once.
 static double gemm_bytes(const GemmParams& P, int epi) {
   double b = 0;
   for (int i = 0; i < P.num_problems; ++i) {
     const GemmProblem& p = P.prob[i];
-    b += 2.0 * p.K * (double(p.M) + p.N);
+    bool a_seen = false;
+    for (int j = 0; j < i; ++j) a_seen |= std::memcmp(&P.prob[j].map_a, &p.map_a, sizeof(CUtensorMap)) == 0;
+    b += 2.0 * p.K * ((a_seen ? 0.0 : double(p.M)) + p.N);
     b += double(p.M) * p.N * (epi == EPI_F32 ? 4.0 * P.splits : epi == EPI_DACT ? 4.0 : 2.0);
   }
   return b;
@@ -1066,13 +1100,17 @@ void Trainer::train_minibatch(Gmi& g, int k, int adam_step) {
     }
   }
   for (int l = L - 1; l >= 0 && !(par && L > 1); --l) {
-    GemmParams P = g.dw[l];
+    // grouped: dW(L-1) waits for dPre(L-2) and runs with dW(L-2) as one launch (plan above)
+    const int lw = g.dw_grouped && l == L - 2 ? L - 1 : l;
+    GemmParams P = g.dw[lw];
     if (l == 0) P.prob[0].b_row0 = P.prob[1].b_row0 = k * g.Bm;
-    if (g.dw_pair[l]) {
+    if (g.dw_grouped && l == L - 1) {
+      // deferred
+    } else if (g.dw_pair[l]) {
       timed(g.s, GMI_PH_DW_GEMM, g.flop_dw[l], 0.0, [&] { gemm_pair_launch(P, g.ctas, g.s); });
       ++launches_;
     } else {
-      gemm(g, GMI_PH_DW_GEMM, P, g.bn_dw[l], 1, 1, EPI_F32, g.flop_dw[l]);
+      gemm(g, GMI_PH_DW_GEMM, P, g.bn_dw[lw], 1, 1, EPI_F32, g.flop_dw[lw]);
     }
     if (!g.fused_bias[l]) {  // else summed by the DACT GEMM that produced dPre_l
       const __nv_bfloat16* Ds[2] = {g.D[0][l], g.D[1][l]};
