@@ -102,10 +102,12 @@ struct GemmSmem {
   static constexpr uint32_t kStaging = EPI == 2 ? 4096 : 2048;  // one 32x32 chunk per warp
   // WS: as many activation stages as fit next to the resident weights, up to two whole tiles
   // (K <= 256 is 4 k-blocks), so the next tile's rows are in flight while this tile's MMAs run
-  static constexpr int kWsFit = int((232448u - 1280u - kBRes - kEpiWarps * kStagingBufs * kStaging) / kA);
+  // WS forward: the CTA's bias row (one problem per CTA, n0 = 0) staged in shared memory once
+  static constexpr uint32_t kBias = (WS && EPI == 0) ? BN * 4 : 0;
+  static constexpr int kWsFit = int((232448u - 1280u - kBias - kBRes - kEpiWarps * kStagingBufs * kStaging) / kA);
   static constexpr int kStages = WS ? (kWsFit < GMI_WS_STAGES ? kWsFit : GMI_WS_STAGES) : (BN == 256 && !kDw4 ? 3 : 4);
   static constexpr uint32_t kStage = WS ? kA : kA + kB;
-  static constexpr uint32_t kBarOff = kStages * kStage + kBRes + kEpiWarps * kStagingBufs * kStaging;
+  static constexpr uint32_t kBarOff = kStages * kStage + kBRes + kEpiWarps * kStagingBufs * kStaging + kBias;
   static constexpr uint32_t kBytes = kBarOff + 256 + 1024;  // + barriers + alignment slack
   static constexpr uint32_t kTmemCols = 2 * BN < 32 ? 32 : 2 * BN;
   static_assert(kBytes <= 232448, "shared memory budget");
@@ -276,6 +278,12 @@ __global__ void __launch_bounds__(gemm_threads(EPI) + 128 * CS, 1)
     const int h = e >> 2;
     constexpr int kChunks = BN / 32;
     uint8_t* stage_base = staging + e * L::kStagingBufs * L::kStaging;
+    float* bias_s = reinterpret_cast<float*>(staging + kEpiWarps * L::kStagingBufs * L::kStaging);
+    if constexpr (L::kBias > 0) {  // WS: this CTA's problem is blockIdx.x % problems for every tile
+      const GemmProblem& pb = P.prob[blockIdx.x % P.num_problems];
+      for (int i = e * 32 + lane; i < BN; i += kEpiWarps * 32) bias_s[i] = i < pb.N ? pb.bias[i] : 0.f;
+      asm volatile("bar.sync 1, %0;" ::"r"(kEpiWarps * 32));
+    }
     int sbuf = 0;
     int lt = 0;
     for (int tile = blockIdx.x; tile < ntile_total; tile += gridDim.x, ++lt) {
@@ -341,10 +349,10 @@ __global__ void __launch_bounds__(gemm_threads(EPI) + 128 * CS, 1)
         } else {
           uint32_t packed[8];
           if constexpr (EPI == EPI_BIAS_ELU) {
-            const float4* b4 = reinterpret_cast<const float4*>(pr.bias + col0 + half * 16);
+            const float4* b4 = reinterpret_cast<const float4*>((L::kBias > 0 ? bias_s : pr.bias) + col0 + half * 16);
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
-              const float4 b = __ldg(b4 + j);
+              const float4 b = L::kBias > 0 ? b4[j] : __ldg(b4 + j);
               const float2 y0 = bias_elu2(make_float2(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1])),
                                           make_float2(b.x, b.y));
               const float2 y1 = bias_elu2(make_float2(__uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3])),
