@@ -120,6 +120,36 @@ def test_rollout_is_layout_invariant_on_device(cuda):
     assert np.array_equal(r1, r2)
 
 
+@pytest.mark.parametrize("env", [None, "GMI_DW_GROUP=0", "GMI_DX_WS4_OFF=1"])
+def test_minibatch_gradient_bench_kernels_match_oracle(cuda, monkeypatch, env):
+    """Minibatch large enough (1200 envs: 9600 rows, 75 M-tiles per net) that the plan picks the
+    bench's kernels: weight-stationary forward GEMMs, the 4-problem weight-stationary input
+    gradient (N-halves), and the grouped weight gradient of layers 2+1 (18 splits); the
+    non-default plans stay covered through their switches."""
+    if env:
+        k, v = env.split("=")
+        monkeypatch.setenv(k, v)
+    S, A, hidden = 60, 8, [256, 256, 256]
+    dev, orc = _pair(S, A, hidden, 1200)
+    B = 1200 * 32 // 4
+    rng = np.random.default_rng(7)
+    X = rng.uniform(-1, 1, (B, S)).astype(np.float32)
+    act = rng.standard_normal((B, A)).astype(np.float32)
+    oldlp = (rng.standard_normal(B) - 3).astype(np.float32)
+    adv = rng.standard_normal(B).astype(np.float32)
+    ret = rng.standard_normal(B).astype(np.float32)
+    g_dev = dev.minibatch_grad(X, act, oldlp, adv, ret)
+    g_orc, _ = orc.minibatch(X, act, oldlp, adv, ret)
+    lay = param_layout(S, A, hidden)
+    for key, t in lay.items():
+        if not isinstance(key, tuple):
+            continue
+        for part, n in (("w", t["out_p"] * t["in_p"]), ("b", t["out_p"])):
+            a, b = g_dev[t[part]:t[part] + n], g_orc[t[part]:t[part] + n]
+            ref = np.linalg.norm(b) + 1e-12
+            assert np.linalg.norm(a - b) <= 2e-2 * ref, (key, part, np.linalg.norm(a - b) / ref)
+
+
 @pytest.mark.parametrize("dims", [(12, 3, [64, 64]), (60, 8, [256, 256, 256]), (40, 20, [96, 160])])
 def test_fused_rollout_matches_per_layer_path(cuda, monkeypatch, dims):
     """cuda/rollout.cu (one persistent kernel) vs the per-layer GEMM + act/env path: the MLP
