@@ -97,7 +97,7 @@ struct GemmSmem {
   static constexpr uint32_t kBRes = WS ? kGemmMaxKbWS * kB : 0;  // resident B (WS)
   // split-K fp32 slabs at BN = 256 (one tile per CTA): a 4th operand stage beats double
   // staging of the once-per-CTA epilogue (weight-gradient phase 0.99 -> 0.96 ms per iteration)
-  static constexpr bool kDw4 = !WS && EPI == 2 && BN == 256;
+  static constexpr bool kDw4 = !WS && EPI == 2;  // every split-K launch: one tile per CTA
   static constexpr int kStagingBufs = WS || kDw4 ? GMI_WS_STAGING : 2;
   static constexpr uint32_t kStaging = EPI == 2 ? 4096 : 2048;  // one 32x32 chunk per warp
   // WS: as many activation stages as fit next to the resident weights, up to two whole tiles
@@ -105,7 +105,12 @@ struct GemmSmem {
   // WS forward: the CTA's bias row (one problem per CTA, n0 = 0) staged in shared memory once
   static constexpr uint32_t kBias = (WS && EPI == 0) ? BN * 4 : 0;
   static constexpr int kWsFit = int((232448u - 1280u - kBias - kBRes - kEpiWarps * kStagingBufs * kStaging) / kA);
-  static constexpr int kStages = WS ? (kWsFit < GMI_WS_STAGES ? kWsFit : GMI_WS_STAGES) : (BN == 256 && !kDw4 ? 3 : 4);
+  // split-K weight gradients: as many operand stages as fit (up to 8) -- the kernel streams a
+  // long K range per CTA and is bound by bytes in flight
+  static constexpr int kDwFit = int((232448u - 1280u - kEpiWarps * kStagingBufs * kStaging) / (kA + kB));
+  static constexpr int kStages = WS     ? (kWsFit < GMI_WS_STAGES ? kWsFit : GMI_WS_STAGES)
+                                 : kDw4 ? (kDwFit < 8 ? kDwFit : 8)
+                                        : (BN == 256 ? 3 : 4);
   static constexpr uint32_t kStage = WS ? kA : kA + kB;
   static constexpr uint32_t kBarOff = kStages * kStage + kBRes + kEpiWarps * kStagingBufs * kStaging + kBias;
   static constexpr uint32_t kBytes = kBarOff + 256 + 1024;  // + barriers + alignment slack
