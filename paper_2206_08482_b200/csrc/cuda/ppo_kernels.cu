@@ -280,18 +280,31 @@ __global__ void __launch_bounds__(256) shuffle_kernel(const __nv_bfloat16* X_rol
                                                       const Control* ctl) {
   pdl_trigger();
   pdl_wait();
+  // Block = 256 rows of the epoch copy: the Feistel permutation index is computed once per row
+  // (shared memory), then the block's threads copy the rows' 16-byte observation chunks (S_p / 8
+  // consecutive threads per row) and the per-row scalars, so no lane does serial work.
+  __shared__ long long src_s[256];
   const int cpr = S_p / 8;  // 16-byte chunks per row
   const long long B = (long long)T * N;
-  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= B * cpr) return;
-  const long long j = idx / cpr;
-  const int c = int(idx % cpr);
-  uint32_t keys[4];
-  rng::draw(seed, uint32_t(gmi_gid), uint32_t(ctl->iteration), uint32_t(epoch), rng::kPerm, keys);
-  const long long src = rng::perm_index(uint32_t(j), uint32_t(B), keys);
-  reinterpret_cast<uint4*>(X_sh + j * S_p)[c] = reinterpret_cast<const uint4*>(X_roll + src * S_p)[c];
-  if (c == 0) {
-    for (int i = 0; i < A; ++i) act_sh[j * A + i] = act[src * A + i];
+  const long long r0 = (long long)blockIdx.x * 256;
+  const int rows = int(B - r0 < 256 ? B - r0 : 256);
+  if (threadIdx.x < rows) {
+    uint32_t keys[4];
+    rng::draw(seed, uint32_t(gmi_gid), uint32_t(ctl->iteration), uint32_t(epoch), rng::kPerm, keys);
+    src_s[threadIdx.x] = rng::perm_index(uint32_t(r0 + threadIdx.x), uint32_t(B), keys);
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < rows * cpr; k += 256) {
+    const int r = k / cpr, c = k - r * cpr;
+    const long long j = r0 + r, src = src_s[r];
+    reinterpret_cast<uint4*>(X_sh + j * S_p)[c] = reinterpret_cast<const uint4*>(X_roll + src * S_p)[c];
+  }
+  for (int k = threadIdx.x; k < rows * A; k += 256) {
+    const int r = k / A, i = k - r * A;
+    act_sh[(r0 + r) * A + i] = act[src_s[r] * A + i];
+  }
+  if (threadIdx.x < rows) {
+    const long long j = r0 + threadIdx.x, src = src_s[threadIdx.x];
     oldlp_sh[j] = logp[src];
     adv_sh[j] = __fdiv_rn(__fsub_rn(adv[src], stats[0]), stats[1]);
     ret_sh[j] = ret[src];
@@ -355,8 +368,8 @@ void launch_shuffle(const __nv_bfloat16* X_roll, const float* act, const float* 
                     const float* ret, const float* adv_stats, __nv_bfloat16* X_sh, float* act_sh, float* oldlp_sh,
                     float* adv_sh, float* ret_sh, int N, int T, int S_p, int A, uint64_t seed, int gmi_gid, int epoch,
                     const Control* ctl, cudaStream_t s) {
-  const long long work = (long long)T * N * (S_p / 8);
-  launch_pdl(shuffle_kernel, dim3(grid_for(work, 256, 1 << 30)), dim3(256), 0, s, X_roll, act, logp, adv, ret,
+  const long long rows = (long long)T * N;
+  launch_pdl(shuffle_kernel, dim3(unsigned((rows + 255) / 256)), dim3(256), 0, s, X_roll, act, logp, adv, ret,
              adv_stats, X_sh, act_sh, oldlp_sh, adv_sh, ret_sh, N, T, S_p, A, seed, gmi_gid, epoch, ctl);
 }
 
