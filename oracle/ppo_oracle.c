@@ -212,25 +212,34 @@ static void env_reset_state(const oracle_t* o, int gid, int ep_count, float* x) 
 /* bf16 hidden forward of one row for net n; h[l] receives layer-l outputs (bf16-rounded).
  * x: bf16-rounded input [S]. Returns pointer to last hidden. */
 static void mlp_hidden(const oracle_t* o, const float* wbf, int n, const float* x, float** h) {
+  /* wbf + P holds every hidden weight block transposed ([in_p][out_p], make_bf16_weights):
+   * the k loop is outermost so the out-neuron accumulators vectorise; each accumulator still
+   * sums its products in ascending k, so the result is the row-major dot product's. */
   const float* in = x;
+  double acc[1024];
   for (int l = 0; l < o->L; ++l) {
     const tensor_t* t = &o->net[n][l];
-    for (int r = 0; r < t->out; ++r) {
-      double acc = 0.0;
-      const float* wr = wbf + t->w + (long long)r * t->in_p;
-      for (int k = 0; k < t->in; ++k) acc += (double)in[k] * (double)wr[k];
-      const float pre = (float)acc + o->params[t->b + r];
+    const int nout = t->out;
+    for (int r = 0; r < nout; ++r) acc[r] = 0.0;
+    for (int k = 0; k < t->in; ++k) {
+      const double xk = (double)in[k];
+      const float* wk = wbf + o->P + t->w + (long long)k * t->out_p;
+      for (int r = 0; r < nout; ++r) acc[r] += xk * (double)wk[r];
+    }
+    for (int r = 0; r < nout; ++r) {
+      const float pre = (float)acc[r] + o->params[t->b + r];
       h[l][r] = R(elu(pre));
     }
     in = h[l];
   }
 }
 
-static float head_out(const oracle_t* o, int n, int a, const float* hl) {
+static float head_out(const oracle_t* o, const float* wbf, int n, int a, const float* hl) {
   const tensor_t* t = &o->net[n][o->L];
   double acc = 0.0;
   /* heads run on the tensor cores: bf16 head weights, fp32 bias added after the GEMM */
-  for (int k = 0; k < t->in; ++k) acc += (double)hl[k] * (double)R(o->params[t->w + (long long)a * t->in_p + k]);
+  const float* wr = wbf + t->w + (long long)a * t->in_p;
+  for (int k = 0; k < t->in; ++k) acc += (double)hl[k] * (double)wr[k];
   return (float)acc + o->params[t->b + a];
 }
 
@@ -245,8 +254,19 @@ static float gauss_logp(const oracle_t* o, const float* act, const float* mu) {
 }
 
 /* ---------------------------------------------------------------- rollout + GAE */
-static void make_bf16_weights(const oracle_t* o, float* wbf) {
+/* wbf[0, P): bf16-rounded parameters; wbf[P, 2P): the hidden weight blocks again, transposed
+ * to [in_p][out_p] at the same offsets (mlp_hidden's k-outer loop). */
+static float* make_bf16_weights(const oracle_t* o) {
+  float* wbf = (float*)calloc((size_t)(2 * o->P), sizeof(float));
   for (long long i = 0; i < o->P; ++i) wbf[i] = R(o->params[i]);
+  for (int n = 0; n < 2; ++n)
+    for (int l = 0; l < o->L; ++l) {
+      const tensor_t* t = &o->net[n][l];
+      for (int r = 0; r < t->out_p; ++r)
+        for (int k = 0; k < t->in_p; ++k)
+          wbf[o->P + t->w + (long long)k * t->out_p + r] = wbf[t->w + (long long)r * t->in_p + k];
+    }
+  return wbf;
 }
 
 static void alloc_rows(const oracle_t* o, float** h) {
@@ -272,7 +292,7 @@ static void rollout_gmi(oracle_t* o, int gi, const float* wbf) {
       for (int t = 0; t < T; ++t) {
         const float* ob = g->obs + ((long long)t * N + e) * S;
         mlp_hidden(o, wbf, 0, ob, h);
-        for (int a = 0; a < A; ++a) mu[a] = head_out(o, 0, a, h[o->L - 1]);
+        for (int a = 0; a < A; ++a) mu[a] = head_out(o, wbf, 0, a, h[o->L - 1]);
         const uint32_t step = (uint32_t)(o->iteration * T + t);
         for (int q = 0; q < A; q += 4) {
           uint32_t r[4];
@@ -329,7 +349,7 @@ static void values_gmi(oracle_t* o, int gi, const float* wbf) {
 #pragma omp for schedule(static)
     for (long long r = 0; r < (long long)(T + 1) * N; ++r) {
       mlp_hidden(o, wbf, 1, g->obs + r * S, h);
-      g->val[r] = head_out(o, 1, 0, h[o->L - 1]);
+      g->val[r] = head_out(o, wbf, 1, 0, h[o->L - 1]);
     }
     free_rows(o, h);
   }
@@ -395,8 +415,8 @@ static void minibatch_grad(oracle_t* o, int gi, mb_t* mb, int Bm, const float* w
     mlp_hidden(o, wbf, 0, x, hp);
     mlp_hidden(o, wbf, 1, x, hv);
     float mu[64];
-    for (int a = 0; a < A; ++a) mu[a] = head_out(o, 0, a, hp[L - 1]);
-    const float v = head_out(o, 1, 0, hv[L - 1]);
+    for (int a = 0; a < A; ++a) mu[a] = head_out(o, wbf, 0, a, hp[L - 1]);
+    const float v = head_out(o, wbf, 1, 0, hv[L - 1]);
     const float* act = mb->act + (long long)r * A;
     const float lp = gauss_logp(o, act, mu);
     const float ratio = expf(lp - mb->oldlp[r]);
@@ -428,9 +448,9 @@ static void minibatch_grad(oracle_t* o, int gi, mb_t* mb, int Bm, const float* w
         double acc = 0.0;
         if (n == 0)
           for (int a = 0; a < A; ++a)
-            acc += (double)R(mb->gmu[(long long)r * A + a]) * (double)R(o->params[th->w + (long long)a * th->in_p + k]);
+            acc += (double)R(mb->gmu[(long long)r * A + a]) * (double)wbf[th->w + (long long)a * th->in_p + k];
         else
-          acc = (double)R(mb->gv[r]) * (double)R(o->params[th->w + k]);
+          acc = (double)R(mb->gv[r]) * (double)wbf[th->w + k];
         d[k] = R((float)acc * elu_grad_from_out(hl[k]));
       }
       /* hidden backward: dPre_{l-1} = (dPre_l W_l) * elu'(H_{l-1}) */
@@ -439,11 +459,14 @@ static void minibatch_grad(oracle_t* o, int gi, mb_t* mb, int Bm, const float* w
         const float* dl = mb->D[n][l] + (long long)r * o->width[l + 1];
         const float* hprev = (n == 0 ? hp : hv)[l - 1];
         float* dp = mb->D[n][l - 1] + (long long)r * o->width[l];
-        for (int k = 0; k < t->in; ++k) {
-          double acc = 0.0;
-          for (int j = 0; j < t->out; ++j) acc += (double)dl[j] * (double)wbf[t->w + (long long)j * t->in_p + k];
-          dp[k] = R((float)acc * elu_grad_from_out(hprev[k]));
+        double acc[1024];
+        for (int k = 0; k < t->in; ++k) acc[k] = 0.0;
+        for (int j = 0; j < t->out; ++j) {  /* per k: ascending j, as the column dot product */
+          const double dj = (double)dl[j];
+          const float* wj = wbf + t->w + (long long)j * t->in_p;
+          for (int k = 0; k < t->in; ++k) acc[k] += dj * (double)wj[k];
         }
+        for (int k = 0; k < t->in; ++k) dp[k] = R((float)acc[k] * elu_grad_from_out(hprev[k]));
       }
     }
   }
@@ -460,18 +483,26 @@ static void minibatch_grad(oracle_t* o, int gi, mb_t* mb, int Bm, const float* w
       const float* in = l == 0 ? mb->X : mb->H[n][l - 1];
       const int in_w = l == 0 ? o->c.obs_dim : o->width[l];
       const float* d = mb->D[n][l];
-#pragma omp parallel for schedule(static)
-      for (int j = 0; j < t->out; ++j) {
-        double db = 0.0;
-        double* acc = (double*)calloc((size_t)t->in, sizeof(double));
+#pragma omp parallel for schedule(dynamic, 1)
+      for (int j0 = 0; j0 < t->out; j0 += 16) {
+        /* 16 output rows per task share each input row; every (j, k) sums over ascending r */
+        const int nj = t->out - j0 < 16 ? t->out - j0 : 16;
+        double db[16] = {0};
+        double* acc = (double*)calloc((size_t)16 * t->in, sizeof(double));
         for (int r = 0; r < Bm; ++r) {
-          const double dj = d[(long long)r * t->out + j];
           const float* row = in + (long long)r * in_w;
-          db += dj;
-          for (int k = 0; k < t->in; ++k) acc[k] += dj * (double)row[k];
+          for (int jj = 0; jj < nj; ++jj) {
+            const double dj = d[(long long)r * t->out + j0 + jj];
+            double* aj = acc + (long long)jj * t->in;
+            db[jj] += dj;
+            for (int k = 0; k < t->in; ++k) aj[k] += dj * (double)row[k];
+          }
         }
-        grad[t->b + j] = (float)db;
-        for (int k = 0; k < t->in; ++k) grad[t->w + (long long)j * t->in_p + k] = (float)acc[k];
+        for (int jj = 0; jj < nj; ++jj) {
+          const int j = j0 + jj;
+          grad[t->b + j] = (float)db[jj];
+          for (int k = 0; k < t->in; ++k) grad[t->w + (long long)j * t->in_p + k] = (float)acc[(long long)jj * t->in + k];
+        }
         free(acc);
       }
     }
@@ -479,18 +510,20 @@ static void minibatch_grad(oracle_t* o, int gi, mb_t* mb, int Bm, const float* w
     const tensor_t* th = &o->net[n][L];
     const float* hl = mb->H[n][L - 1];
     const int hw = o->width[L];
+#pragma omp parallel for schedule(static)
     for (int a = 0; a < th->out; ++a) {
       double db = 0.0;
       for (int r = 0; r < Bm; ++r) db += n == 0 ? mb->gmu[(long long)r * A + a] : mb->gv[r];
       grad[th->b + a] = (float)db;
-#pragma omp parallel for schedule(static)
-      for (int k = 0; k < th->in; ++k) {
-        double acc = 0.0;
-        for (int r = 0; r < Bm; ++r)
-          /* head weight gradients run on the tensor cores with bf16 dL/dmu, dL/dv operands */
-          acc += (double)R(n == 0 ? mb->gmu[(long long)r * A + a] : mb->gv[r]) * (double)hl[(long long)r * hw + k];
-        grad[th->w + (long long)a * th->in_p + k] = (float)acc;
+      double* acc = (double*)calloc((size_t)th->in, sizeof(double));
+      for (int r = 0; r < Bm; ++r) {
+        /* head weight gradients run on the tensor cores with bf16 dL/dmu, dL/dv operands */
+        const double ga = (double)R(n == 0 ? mb->gmu[(long long)r * A + a] : mb->gv[r]);
+        const float* hr = hl + (long long)r * hw;
+        for (int k = 0; k < th->in; ++k) acc[k] += ga * (double)hr[k];
       }
+      for (int k = 0; k < th->in; ++k) grad[th->w + (long long)a * th->in_p + k] = (float)acc[k];
+      free(acc);
     }
   }
   for (int a = 0; a < A; ++a) {
@@ -614,8 +647,7 @@ static float* g_mean_std; /* scratch for rollout -> update hand-off */
 /* Env stepping of every GMI with the current parameters (obs slot 0 carries the last
  * observation of the previous rollout after the first one). */
 static void rollout_all(oracle_t* o) {
-  float* wbf = (float*)malloc(sizeof(float) * o->P);
-  make_bf16_weights(o, wbf);
+  float* wbf = make_bf16_weights(o);
   for (int c = 0; c < o->n_gmi; ++c) {
     struct gmi* g = &o->g[c];
     const long long N = g->nenv, S = o->c.obs_dim, T = o->c.horizon;
@@ -627,8 +659,7 @@ static void rollout_all(oracle_t* o) {
 
 /* Values of all T+1 observation slots with the current parameters, GAE, advantage moments. */
 static void values_gae_all(oracle_t* o) {
-  float* wbf = (float*)malloc(sizeof(float) * o->P);
-  make_bf16_weights(o, wbf);
+  float* wbf = make_bf16_weights(o);
   double rsum = 0;
   long long rn = 0;
   free(g_mean_std);
@@ -657,7 +688,7 @@ int ppo_oracle_rollout(void* h) {
 /* E epochs x K minibatch updates on the GMIs' current experience; iteration += 1. */
 static void train_all(oracle_t* o) {
   const int S = o->c.obs_dim, A = o->c.act_dim, T = o->c.horizon, L = o->L;
-  float* wbf = (float*)malloc(sizeof(float) * o->P);
+  float* wbf = NULL;
   mb_t* mbs = (mb_t*)calloc((size_t)o->n_gmi, sizeof(mb_t));
   int* Bm = (int*)calloc((size_t)o->n_gmi, sizeof(int));
   for (int c = 0; c < o->n_gmi; ++c) {
@@ -670,7 +701,8 @@ static void train_all(oracle_t* o) {
     for (int c = 0; c < o->n_gmi; ++c)
       philox_tag(o->c.seed, (uint32_t)c, (uint32_t)o->iteration, (uint32_t)ep, TAG_PERM, keys[c]);
     for (int k = 0; k < o->c.minibatches; ++k) {
-      make_bf16_weights(o, wbf);
+      free(wbf);
+      wbf = make_bf16_weights(o);
       for (int c = 0; c < o->n_gmi; ++c) {
         struct gmi* g = &o->g[c];
         mb_t* m = &mbs[c];
@@ -783,8 +815,7 @@ int ppo_oracle_minibatch(void* h, int gmi, const float* X, const float* act, con
   memcpy(m.oldlp, oldlp, sizeof(float) * (size_t)B);
   memcpy(m.adv, adv, sizeof(float) * (size_t)B);
   memcpy(m.ret, ret, sizeof(float) * (size_t)B);
-  float* wbf = (float*)malloc(sizeof(float) * o->P);
-  make_bf16_weights(o, wbf);
+  float* wbf = make_bf16_weights(o);
   minibatch_grad(o, gmi, &m, B, wbf, grad);
   if (stats) {
     stats[0] = m.loss_pi;
