@@ -3,7 +3,8 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config configs/at_4096env_3x256.cfg]
     torchrun --nproc-per-node N bench.py --gpus N ...          (N > 1, one rank per GPU)
-    python bench.py --impl reference ...                        (CPU reference arm)
+    python bench.py --gpus N ...        (N > 1: re-executes itself under torch.distributed.run)
+    python bench.py --impl reference ...                        (CPU reference arm, no libgmi)
 
 A step is one PPO iteration of the data-parallel TCG_EX job: every env of every GMI
 advances `horizon` steps (rollout), then `epochs` x `minibatches` PPO updates with the
@@ -46,7 +47,6 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-multi-gmi", action="store_true",
                    help="skip the decoupled multi-GMI layout measured beside the single-context one")
-    p.add_argument("--cpu-sample-envs", type=int, default=64)
     return p.parse_args()
 
 
@@ -111,20 +111,23 @@ class ClockSampler:
 
 
 def measured_peaks():
+    """(burst bf16 TF/s, sustained bf16 TF/s, HBM GB/s, source) from the driver-written
+    MEASURED_PEAKS.json, else the B200_PROFILING.md fallbacks."""
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             j = json.load(f)
-        return j["bf16_tflops_sustained"], j["hbm_gbs"], "measured (MEASURED_PEAKS.json: sustained bf16, HBM copy)"
+        return (j["bf16_tflops"], j["bf16_tflops_sustained"], j["hbm_gbs"],
+                "measured (MEASURED_PEAKS.json):")
     except (OSError, KeyError, ValueError):
-        return 1400.0, 6650.0, "fallback (B200_PROFILING.md)"
+        return 2250.0, 1400.0, 6650.0, "fallback (B200_PROFILING.md):"
 
 
-def gemm_traffic():
-    """dram__bytes_read.sum + dram__bytes_write.sum per gemm_tcgen05_kernel launch, from the
-    committed ncu --set full capture (profiles/traffic.json); None when absent."""
+def gemm_traffic(kind: str):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the `kind` GEMM (fwd / dx / dw)
+    from the committed ncu --set full capture summary (profiles/traffic.json); None when absent."""
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-            return json.load(f)["gemm_tcgen05_kernel"]["dram_bytes_per_launch"]
+            return json.load(f)["kernels"][kind]["dram_bytes_per_launch"]
     except (OSError, KeyError, ValueError):
         return None
 
@@ -161,60 +164,267 @@ def phase_table(prof: dict, iter_ms: float, peak_tf: float, peak_gbs: float) -> 
     return out
 
 
+# ------------------------------------------------------------------ config without libgmi
+# Catalog observation / action widths and default hidden widths (workload.hpp:126-134); the
+# reference arm reads the config file with this plain parser so that it never loads libgmi.
+CATALOG = {"AT": (60, 8, [256, 128, 64]), "AY": (48, 12, [256, 128, 64]), "BB": (24, 3, [256, 128, 64]),
+           "FC": (23, 9, [256, 128, 64]), "HM": (108, 21, [200, 400, 100]), "SH": (211, 20, [512, 512, 512, 256])}
+ENV_NAMES = {"AT": "Ant-like locomotion", "AY": "Anymal-like", "BB": "BallBalance-like", "FC": "FrankaCabinet-like",
+             "HM": "Humanoid-like", "SH": "ShadowHand-like"}
+BASELINE_CONFIG = {"at_512env_2x64.cfg": "configs[0]", "at_4096env_3x256.cfg": "configs[1]",
+                   "hm_8192env_4gmi.cfg": "configs[2]", "at_4096env_decoupled.cfg": "configs[3] (one GPU)",
+                   "decoupled_8gpu.cfg": "configs[3]", "sh_sweep_8gpu.cfg": "configs[4]"}
+
+
+def plain_config(path):
+    """Sections / keys of a proj/configs-schema file (config.hpp:125-154 syntax), no validation."""
+    sec, out = None, {}
+    with open(path) as f:
+        for line in f:
+            line = line.split("#", 1)[0].strip()
+            if not line:
+                continue
+            if line.startswith("["):
+                sec = line.strip("[]").strip()
+                out.setdefault(sec, {})
+            elif "=" in line and sec is not None:
+                k, v = (x.strip() for x in line.split("=", 1))
+                out[sec].setdefault(k, v)
+    return out
+
+
+def workload_of(path, envs_override=0):
+    c = plain_config(path)
+    bench = c.get("workload", {}).get("benchmark", "AT")
+    S, A, hid = CATALOG[bench]
+    ppo = c.get("ppo", {})
+    hidden = [int(h) for h in ppo["hidden"].split(",")] if "hidden" in ppo else hid
+    ngpu = sum(1 for _ in open(path) if _.split("#", 1)[0].strip().startswith("gpu ")
+               or _.split("#", 1)[0].strip().startswith("gpu="))
+    num_envs = int(ppo.get("num_envs", 4096))
+    envs = envs_override or num_envs // max(1, ngpu)
+    return dict(bench=bench, env=ENV_NAMES.get(bench, bench), obs_dim=S, act_dim=A, hidden=hidden,
+                envs_per_gpu=envs, horizon=int(ppo.get("horizon", 32)), epochs=int(ppo.get("epochs", 4)),
+                minibatches=int(ppo.get("minibatches", 4)),
+                gmis_per_gpu=int(c.get("model", {}).get("gmis_per_gpu", 1)),
+                decoupled=int(ppo.get("decoupled", 0)),
+                baseline=BASELINE_CONFIG.get(os.path.basename(path), "custom"), path=path)
+
+
+def workload_label(w, n_gpus, layout):
+    return (f"{w['env']} ({w['bench']}), {w['envs_per_gpu']} envs/GPU x {n_gpus} GPU, "
+            f"{w['obs_dim']}:{':'.join(map(str, w['hidden']))}:{w['act_dim']} actor-critic MLP, {layout} "
+            f"(BASELINE {w['baseline']})")
+
+
 # ------------------------------------------------------------------ CPU leg (oracle port)
-def cpu_iteration_sample(cfg, envs: int, iters: int, warmup: int):
-    """Times the CPU restatement (oracle/ppo_oracle.c, OpenMP, all host threads) on a bounded
-    sample of the same workload: `envs` environments, same MLP / horizon / epochs / minibatches."""
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def cpu_iteration_sample(w, envs: int, iters: int, warmup: int, threads: int = 0, warmup_envs: int = 0):
+    """Times the CPU restatement (oracle/ppo_oracle.c, OpenMP) on `envs` environments of the same
+    workload (same MLP / horizon / epochs / minibatches): `warmup` untimed iterations (at
+    `warmup_envs` envs when given), then `iters` timed ones. Returns env-steps/s and a sample note."""
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     from golden_util import PpoOracle, make_cfg  # test infrastructure: baseline leg only
 
-    threads = os.cpu_count() or 1
-    o = PpoOracle(make_cfg(cfg.obs_dim, cfg.act_dim, cfg.hidden, envs, threads=threads,
-                           horizon=cfg.horizon, epochs=cfg.epochs, minibatches=cfg.minibatches))
-    for _ in range(warmup):
-        o.iteration()
+    threads = threads or os.cpu_count() or 1
+    mk = lambda n: PpoOracle(make_cfg(w["obs_dim"], w["act_dim"], w["hidden"], n, threads=threads,
+                                      horizon=w["horizon"], epochs=w["epochs"], minibatches=w["minibatches"]))
+    if warmup:
+        ow = mk(warmup_envs or envs)
+        for _ in range(warmup):
+            ow.iteration()
+        del ow
+    o = mk(envs)
     t0 = time.perf_counter()
     steps = 0
     for _ in range(iters):
         steps += o.iteration().env_steps
     dt = time.perf_counter() - t0
-    sample = (f"{iters} PPO iteration(s) of the same workload at {envs} envs "
-              f"({steps // max(iters, 1)} env-steps each, {cfg.epochs}x{cfg.minibatches} updates), "
-              f"oracle/ppo_oracle.c with {threads} OpenMP threads")
+    sample = (f"{iters} PPO iteration(s) at {envs} envs ({steps // max(iters, 1)} env-steps each, "
+              f"{w['epochs']}x{w['minibatches']} updates), oracle/ppo_oracle.c, {threads} OpenMP thread(s)")
     return steps / dt, threads, sample
 
 
-def run_reference(args, cfg):
+def reduction_vs_reference():
+    """The reference's own execute() (reduction.hpp:225-334, oracle/_ref/gmux_ref_bench, one host
+    thread as shipped) beside K1 (gmi_reduce_device, fp64, the same fold order, bit-identical
+    results) on the BASELINE layouts at the real gradient lengths."""
+    exe = os.path.join(ROOT, "oracle", "_ref", "gmux_ref_bench")
+    if not os.path.exists(exe):
+        return {"unavailable": "oracle/_ref/gmux_ref_bench not built"}
+    import ctypes as C
+    import torch
+    from paper_2206_08482_b200 import _lib
+    out = []
+    res = subprocess.run([exe, "1"], capture_output=True, text=True, timeout=300)
+    codes = {"MPR": 0, "MRR": 1, "HAR": 2}
+    for line in res.stdout.splitlines():
+        r = json.loads(line)
+        g, t, n = r["g"], r["t"], r["len"]
+        bufs = [torch.full((n,), 1.0 + 0.001 * i, dtype=torch.float64, device="cuda") for i in range(g * t)]
+        dst = torch.empty(n, dtype=torch.float64, device="cuda")
+        ptrs = (C.c_void_p * (g * t))(*[b.data_ptr() for b in bufs])
+        counts, ids = (C.c_int * g)(*([t] * g)), (C.c_int * (g * t))(*range(g * t))
+        st = torch.cuda.current_stream()
+
+        def k1():
+            _lib.call("gmi_reduce_device", codes[r["strategy"]], g, counts, ids, ptrs, C.c_void_p(dst.data_ptr()),
+                      n, 1, 0, C.c_void_p(st.cuda_stream))
+        for _ in range(3):
+            k1()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(st)
+        for _ in range(20):
+            k1()
+        b.record(st)
+        torch.cuda.synchronize()
+        ms = a.elapsed_time(b) / 20
+        out.append({"case": r["case"], "strategy": r["strategy"], "len": n, "ref_execute_s": r["seconds"],
+                    "k1_ms": ms, "speedup": r["seconds"] / (ms / 1e3),
+                    "k1_gbs": (g * t + 1) * 8.0 * n / (ms / 1e3) / 1e9})
+    return {"layouts": out, "note": "reference execute() single host thread (as shipped) vs K1 on one B200, "
+                                    "fp64, all g x t GMI buffers resident on the device"}
+
+
+def run_reference(args):
+    """Reference arm: the CPU path of this workload (the reference has no PPO code, so its CPU
+    restatement oracle/ppo_oracle.c is timed) on all host threads, same config as our arm;
+    every timed step is one full PPO iteration of one GPU's share of envs. No libgmi."""
     world, rank, _ = dist_env()
     if rank != 0:
         return
-    value, threads, sample = cpu_iteration_sample(cfg, args.cpu_sample_envs, args.steps, args.warmup)
-    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+    w = workload_of(args.config, args.envs)
+    if args.gmis:
+        w["gmis_per_gpu"] = args.gmis
+    ngpu = max(1, args.gpus)
+    # warm-up steps touch the code/data paths only (a smaller env count keeps the run within minutes)
+    value, threads, sample = cpu_iteration_sample(w, w["envs_per_gpu"], args.steps, args.warmup,
+                                                  warmup_envs=min(512, w["envs_per_gpu"]))
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ngpu,
             "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": "AT-like locomotion, 3x256 actor-critic MLP (BASELINE configs[1] shapes)",
-                       "num_envs": args.cpu_sample_envs, "note": "reference has no PPO code; oracle port timed"},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
+            "config": bench_config(w, ngpu),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                             "sample": sample + (f"; warm-up iterations at {min(512, w['envs_per_gpu'])} envs"
+                                                 if args.warmup else ""),
+                             "nproc": os.cpu_count(), "cpu_model": cpu_model(),
+                             "note": "the reference (gmux) has no PPO code; its CPU restatement is timed. "
+                                     "Host env-steps/s do not depend on the GPU count, so each step "
+                                     "processes one GPU's envs"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
+def layout_of(w):
+    return (f"{w['gmis_per_gpu']} GMI(s) per GPU" if not w["decoupled"] else
+            "decoupled: serving GMI + trainer GMI per GPU, device experience channel")
+
+
+def bench_config(w, ngpu):
+    """The workload as named by the config file -- identical in both arms (same_config)."""
+    return {"workload": workload_label(w, ngpu, layout_of(w)),
+            "config_file": os.path.relpath(os.path.abspath(w["path"]), ROOT),
+            "benchmark": w["bench"], "envs_per_gpu": w["envs_per_gpu"], "obs_dim": w["obs_dim"],
+            "act_dim": w["act_dim"], "hidden": w["hidden"], "horizon": w["horizon"], "epochs": w["epochs"],
+            "minibatches": w["minibatches"], "gmis_per_gpu": w["gmis_per_gpu"],
+            "parallelism": f"dp{ngpu * w['gmis_per_gpu']} ({ngpu} GPU x {w['gmis_per_gpu']} GMI)",
+            "l2": "no flush: per-iteration working set > 126 MB L2 (run.working_set_mb)"}
+
+
+def relaunch(args):
+    """`python bench.py --gpus N` (N > 1) outside torchrun: re-exec under torch.distributed.run,
+    one rank per GPU on this node, rendezvous on 127.0.0.1."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 # ------------------------------------------------------------------ our arm
+def time_trainer(cfg, steps, warmup, world, barrier, instrument=True):
+    """Device-timed K iterations of one trainer (max over ranks), then one instrumented iteration
+    for the per-unit (per-GMI) busy time. Returns (value, ms_per_step, units, trainer stats)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2206_08482_b200.ppo import Trainer, nccl_unique_id
+
+    nid = None
+    if world > 1:
+        obj = [nccl_unique_id() if cfg.rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nid = obj[0]
+    t = Trainer(cfg, nid)
+    upd = torch.cuda.ExternalStream(t.stream(-1))
+    for _ in range(max(3, warmup)):
+        t.iteration()
+    barrier()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(upd)
+    for _ in range(steps):
+        t.iteration_async()
+    b.record(upd)
+    st = t.synchronize()
+    barrier()
+    ms = torch.tensor([a.elapsed_time(b)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    value = st.env_steps * world * steps / (ms.item() / 1e3)
+    units = None
+    if instrument:
+        t.set_instrument(True)
+        t.iteration()
+        c, d = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        c.record(upd)
+        t.iteration_async()
+        d.record(upd)
+        t.synchronize()
+        it_ms = c.elapsed_time(d)
+        units = unit_report(t.unit_busy(), it_ms, cfg.decoupled)
+    t.close()
+    return value, ms.item() / steps, units
+
+
+def unit_report(busy, it_ms, decoupled):
+    names = (["serving GMI (simulator+agent)", "trainer GMI"] if decoupled else
+             [f"GMI {i}" for i in range(len(busy) - 1)]) + ["update stream (K1 fold + Adam)"]
+    return [{"unit": n, "sms": s, "busy_ms": round(b, 4), "sm_busy_frac": round(b / it_ms, 4) if it_ms else None}
+            for n, (b, s) in zip(names, busy)] + [{"instrumented_iteration_ms": round(it_ms, 4)}]
+
+
 def main():
     args = parse()
-    from paper_2206_08482_b200.ppo import PpoConfig, Trainer, nccl_unique_id
-
-    world, rank, local = dist_env()
-    cfg = PpoConfig.from_config_file(args.config)
-    if args.gmis:
-        cfg.gmis_per_gpu = args.gmis
-    envs_per_gpu = args.envs or cfg.num_envs // max(1, cfg.num_gpus)
     if args.impl == "reference":
-        run_reference(args, cfg)
+        run_reference(args)
         return
+    world, rank, local = dist_env()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch(args))
+    if "WORLD_SIZE" in os.environ and world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
 
     import torch
     import torch.distributed as dist
+    from paper_2206_08482_b200.ppo import PpoConfig, Trainer, nccl_unique_id
+
+    w = workload_of(args.config, args.envs)
+    w["path"] = args.config
+    cfg = PpoConfig.from_config_file(args.config)
+    if args.gmis:
+        cfg.gmis_per_gpu = w["gmis_per_gpu"] = args.gmis
+    envs_per_gpu = w["envs_per_gpu"]
 
     torch.cuda.set_device(local)
     if world > 1:
@@ -284,7 +494,7 @@ def main():
     e2e = steps_total / wall_t.item()
 
     # ---- instrumented pass (not part of the timed numbers): CUDA events around every launch
-    # of GMI 0 and the update stream -> per-phase time, flops and bytes for the rooflines.
+    # -> per-phase time / flops / bytes for the rooflines and per-GMI busy time.
     trainer.set_instrument(True)
     trainer.iteration()
     t2, t3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -292,121 +502,123 @@ def main():
     t2.record(upd)
     trainer.iteration_async()
     t3.record(upd)
-    ist = trainer.synchronize()
+    trainer.synchronize()
     prof = trainer.profile()
     iter_ms_instr = t2.elapsed_time(t3)
+    units = unit_report(trainer.unit_busy(), iter_ms_instr, cfg.decoupled)
     trainer.set_instrument(False)
+    trainer.close()
 
-    multi = None
-    if not cfg.decoupled and not args.no_multi_gmi and world == 1:  # one box, same workload
-        trainer.close()
-        try:
-            multi = time_decoupled(args, cfg, world, rank, barrier)
-            multi["vs_single_context"] = multi["value"] / value
-        except Exception as e:  # noqa: BLE001 -- the headline line must still print
-            multi = {"error": f"{type(e).__name__}: {e}"}
+    extra = {}
+    if world == 1 and not args.no_multi_gmi and not cfg.decoupled:
+        extra = other_layouts(args, cfg, w, value, world, barrier)
 
     if rank == 0:
-        peak_tf, peak_gbs, peak_src = measured_peaks()
-        gemm_ms, gemm_flop, gemm_bytes = ist.gemm_ms, ist.gemm_flop, ist.gemm_bytes
-        achieved_tf = gemm_flop / (gemm_ms / 1e3) / 1e12 if gemm_ms > 0 else 0.0
-        achieved_gbs = gemm_bytes / (gemm_ms / 1e3) / 1e9 if gemm_ms > 0 else 0.0
-        # K <= 256 layer GEMMs and split-K weight gradients sit below the ridge point
-        # (peak_tf / peak_gbs flop per byte): the roof that binds them is HBM bandwidth.
-        intensity = gemm_flop / gemm_bytes if gemm_bytes > 0 else float("inf")
-        hbm_bound = intensity < peak_tf * 1e12 / (peak_gbs * 1e9)
+        peak_burst, peak_sust, peak_gbs, peak_src = measured_peaks()
+        at_max = bool(clk and clk.get("sm_mhz") and clk.get("sm_max_mhz") and clk["sm_mhz"] >= 0.97 * clk["sm_max_mhz"])
+        peak_tf = peak_burst if at_max else peak_sust
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
-            cv, cores, sample = cpu_iteration_sample(cfg, args.cpu_sample_envs, 1, 0)
-            cpu = {"value": cv, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample}
-        ws = working_set_mb(cfg, envs_per_gpu)
-        layout = (f"{cfg.gmis_per_gpu} GMI(s) per B200 (BASELINE configs[1])" if not cfg.decoupled else
-                  f"decoupled: 1 serving GMI ({cfg.serving_sms or 16} SMs, simulator+agent) + 1 trainer GMI "
-                  f"per B200, device experience channel, one-iteration policy lag (BASELINE configs[3])")
+            cv, cores, sample = cpu_iteration_sample(w, envs_per_gpu, 1, 0)
+            c1, _, s1 = cpu_iteration_sample(w, max(64, envs_per_gpu // 16), 1, 0, threads=1)
+            cpu = {"value": cv, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample,
+                   "single_thread": {"value": c1, "sample": s1}, "nproc": os.cpu_count(), "cpu_model": cpu_model(),
+                   "reduction": reduction_vs_reference()}
+        layout = (f"{cfg.gmis_per_gpu} GMI(s) per B200 ({['CUDA streams', 'green contexts'][cfg.gmi_backend]})"
+                  if not cfg.decoupled else
+                  f"decoupled: serving GMI ({cfg.serving_sms or 16} SMs, simulator+agent) + trainer GMI per B200, "
+                  f"device experience channel, one-iteration policy lag")
+        run = {"layout": layout, "gmis_per_gpu": cfg.gmis_per_gpu + (1 if cfg.decoupled else 0),
+               "gmi_backend": ["streams", "green_ctx"][cfg.gmi_backend], "sm_per_gmi": cfg.sm_per_gmi,
+               "decoupled": bool(cfg.decoupled), "env_steps_per_step": steps_total // args.steps,
+               "cuda_graph": bool(cfg.use_graph),
+               "working_set_mb": round(working_set_mb(cfg, envs_per_gpu), 1)}
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": max(3, args.warmup), "ms_per_step": ms_max / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": f"AT-like locomotion, {envs_per_gpu} envs/GPU, "
-                                   f"{'x'.join(map(str, cfg.hidden))} actor-critic MLP, "
-                                   f"{layout}",
-                       "config_file": os.path.relpath(args.config, ROOT), "envs_per_gpu": envs_per_gpu,
-                       "obs_dim": cfg.obs_dim, "act_dim": cfg.act_dim, "hidden": cfg.hidden,
-                       "horizon": cfg.horizon, "epochs": cfg.epochs, "minibatches": cfg.minibatches,
-                       "gmis_per_gpu": cfg.gmis_per_gpu + (1 if cfg.decoupled else 0),
-                       "gmi_backend": ["streams", "green_ctx"][cfg.gmi_backend], "decoupled": bool(cfg.decoupled),
-                       "parallelism": f"dp{world * cfg.gmis_per_gpu} ({world} GPU x {cfg.gmis_per_gpu} GMI)",
-                       "env_steps_per_step": steps_total // args.steps,
-                       "l2": f"no flush: per-iteration working set ~{ws:.0f} MB > 126 MB L2",
-                       "cuda_graph": bool(cfg.use_graph)},
-            "roofline": {"bound": "hbm" if hbm_bound else "tensor",
-                         "kernel": "gemm_tcgen05_kernel (every MLP GEMM of GMI 0, all phases)",
-                         "achieved": achieved_gbs if hbm_bound else achieved_tf,
-                         "peak": peak_gbs if hbm_bound else peak_tf, "unit": "GB/s" if hbm_bound else "TFLOP/s",
-                         "frac": achieved_gbs / peak_gbs if hbm_bound else achieved_tf / peak_tf,
-                         "intensity_flop_per_byte": intensity,
-                         "ridge_flop_per_byte": peak_tf * 1e12 / (peak_gbs * 1e9),
-                         "algorithmic_bytes_per_launch": gemm_bytes / max(1, ist.gemm_launches),
-                         "tensor_view": {"achieved": achieved_tf, "peak": peak_tf, "unit": "TFLOP/s",
-                                         "frac": achieved_tf / peak_tf},
-                         "traffic": gemm_traffic(),
-                         "traffic_unit": "DRAM bytes per launch (ncu, profiles/traffic.json)",
-                         "peak_source": peak_src,
-                         "gemm_share_of_step": gemm_ms / iter_ms_instr if iter_ms_instr else None,
-                         "instrumented_ms_per_step": iter_ms_instr},
+            "config": bench_config(w, world),
+            "run": run,
+            "roofline": roofline(prof, peak_tf, peak_gbs, peak_src, at_max, iter_ms_instr),
             "phases": phase_table(prof, iter_ms_instr, peak_tf, peak_gbs),
+            "gmi_units": units,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": 16, "d2h_bytes_per_step": 32,
                     "api": "gmi_ppo_iteration (synchronous C-ABI call per step)"},
             "gpu_launches": launches,
             "clocks": clk,
-            "multi_gmi": multi,
         }
+        line.update(extra)
         print(json.dumps(line), flush=True)
-    if multi is None:
-        trainer.close()
     if world > 1:
         dist.destroy_process_group()
 
 
-def time_decoupled(args, cfg, world, rank, barrier):
-    """The same workload in the decoupled multi-GMI layout (BASELINE configs[3] per GPU): a
-    16-SM serving GMI (simulator + agent) streams experience to a 132-SM trainer GMI through the
-    device channel, one-iteration policy lag. Device-timed like the main number, max over ranks."""
-    import copy
-    import torch
-    import torch.distributed as dist
-    from paper_2206_08482_b200.ppo import Trainer, nccl_unique_id
+def roofline(prof, peak_tf, peak_gbs, peak_src, at_max, iter_ms):
+    """Dominant kernel: the training-forward GEMM (gemm_tcgen05_kernel, weight-stationary
+    bias+ELU epilogue; the largest single phase of the iteration). Tensor-bound per SURVEY §8d:
+    algorithmic flops (2·M·N·K per problem, real widths) of its launches ÷ their CUDA-event time
+    on the GMI stream, against the burst bf16 peak when the SM clock sat at its maximum."""
+    f = prof.get("fwd_gemm", {})
+    ms, flop = f.get("ms", 0.0), f.get("flop", 0.0)
+    tf = flop / (ms / 1e3) / 1e12 if ms else 0.0
+    fam = {k: prof[k] for k in ("fwd_gemm", "dx_gemm", "dw_gemm") if k in prof}
+    fms = sum(v["ms"] for v in fam.values())
+    ffl = sum(v["flop"] for v in fam.values())
+    fby = sum(v["bytes"] for v in fam.values())
+    n = max(1, f.get("launches", 0))
+    return {"bound": "tensor", "kernel": "gemm_tcgen05_kernel<256,0,0,0,1,0> (training forward, both nets)",
+            "achieved": tf, "peak": peak_tf, "unit": "TFLOP/s", "frac": tf / peak_tf if peak_tf else None,
+            "traffic": gemm_traffic("fwd"), "traffic_unit": "DRAM bytes per launch (ncu --set full, profiles/traffic.json)",
+            "algorithmic_flop_per_launch": flop / n, "algorithmic_bytes_per_launch": f.get("bytes", 0.0) / n,
+            "launches_per_step": f.get("launches", 0), "avg_launch_us": 1e3 * ms / n,
+            "share_of_step": ms / iter_ms if iter_ms else None,
+            "peak_source": peak_src + (" burst (SM clock at max during the timed region)" if at_max else " sustained"),
+            "hbm_view": {"achieved": f.get("bytes", 0.0) / (ms / 1e3) / 1e9 if ms else 0.0, "peak": peak_gbs,
+                         "unit": "GB/s"},
+            "gemm_family": {"kernels": "forward + input-gradient + weight-gradient GEMMs", "ms": fms,
+                            "achieved_tflops": ffl / (fms / 1e3) / 1e12 if fms else 0.0,
+                            "frac": (ffl / (fms / 1e3) / 1e12) / peak_tf if fms else None,
+                            "achieved_gbs": fby / (fms / 1e3) / 1e9 if fms else 0.0}}
 
-    dc = copy.deepcopy(cfg)
-    dc.decoupled, dc.gmis_per_gpu, dc.gmi_backend = 1, 1, 1
-    dc.serving_sms = args.serving_sms or 16
-    nid = None
-    if world > 1:
-        obj = [nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        nid = obj[0]
-    t = Trainer(dc, nid)
-    upd = torch.cuda.ExternalStream(t.stream(-1))
-    for _ in range(max(3, args.warmup)):
-        t.iteration()
-    barrier()
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record(upd)
-    for _ in range(args.steps):
-        t.iteration_async()
-    b.record(upd)
-    st = t.synchronize()
-    barrier()
-    ms = torch.tensor([a.elapsed_time(b)], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
-    t.close()
-    value = st.env_steps * world * args.steps / (ms.item() / 1e3)
-    return {"layout": f"decoupled: serving GMI ({dc.serving_sms} SMs, simulator+agent) + trainer GMI "
-                      f"(remaining SMs) per B200, device experience channel (configs/at_4096env_decoupled.cfg)",
-            "semantics": "one-iteration policy lag (PAPER.md:378-407); behaviour log-probs recorded",
-            "value": value, "unit": UNIT, "ms_per_step": ms.item() / args.steps}
+
+def other_layouts(args, cfg, w, value, world, barrier):
+    """Extra keys, N = 1 only: the decoupled multi-GMI layout of the same workload (BASELINE
+    configs[3] per GPU) and BASELINE configs[2] (HM, 8192 envs, 4 green-context GMIs) beside HM
+    with one GMI on the same box -- the north_star's multi-GMI vs single-context check -- each
+    with per-GMI busy fractions from an instrumented iteration."""
+    import copy
+    out = {}
+    try:
+        dc = copy.deepcopy(cfg)
+        dc.decoupled, dc.gmis_per_gpu, dc.gmi_backend, dc.sm_per_gmi = 1, 1, 1, 0
+        dc.serving_sms = args.serving_sms or 16
+        v, msps, units = time_trainer(dc, args.steps, args.warmup, world, barrier)
+        out["multi_gmi"] = {"layout": f"decoupled: serving GMI ({dc.serving_sms} SMs) + trainer GMI (remaining SMs), "
+                                      "device experience channel (configs/at_4096env_decoupled.cfg)",
+                            "semantics": "one-iteration policy lag (PAPER.md:378-407); behaviour log-probs recorded",
+                            "value": v, "unit": UNIT, "ms_per_step": msps, "vs_single_context": v / value,
+                            "gmi_units": units}
+    except Exception as e:  # noqa: BLE001 -- the headline line must still print
+        out["multi_gmi"] = {"error": f"{type(e).__name__}: {e}"}
+    try:
+        from paper_2206_08482_b200.ppo import PpoConfig
+        hm_path = os.path.join(ROOT, "configs", "hm_8192env_4gmi.cfg")
+        hm = PpoConfig.from_config_file(hm_path)
+        hm.num_gpus, hm.rank, hm.device = 1, 0, cfg.device
+        v4, ms4, u4 = time_trainer(hm, args.steps, args.warmup, world, barrier)
+        one = copy.deepcopy(hm)
+        one.gmis_per_gpu, one.gmi_backend, one.sm_per_gmi = 1, 0, 0
+        v1, ms1, u1 = time_trainer(one, args.steps, args.warmup, world, barrier)
+        hw = workload_of(hm_path)
+        out["config2_hm_4gmi"] = {
+            "workload": workload_label(hw, 1, f"4 GMIs per B200 (green contexts, {hm.sm_per_gmi} SMs each)"),
+            "value": v4, "unit": UNIT, "ms_per_step": ms4, "gmi_units": u4,
+            "single_context": {"value": v1, "ms_per_step": ms1, "gmi_units": u1},
+            "vs_single_context": v4 / v1}
+    except Exception as e:  # noqa: BLE001
+        out["config2_hm_4gmi"] = {"error": f"{type(e).__name__}: {e}"}
+    return out
 
 
 def working_set_mb(cfg, envs):

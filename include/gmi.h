@@ -366,6 +366,15 @@ typedef struct {
    * trainer GMIs and must be 1. */
   int decoupled;
   int serving_sms;            /* green-context SMs of the serving GMI (multiple of 8; 0 = 16) */
+  /* Cross-GPU gradient exchange (num_gpus > 1; HAR leader step, reduction.hpp:287-299):
+   * 0 = ncclAllReduce on the update stream, then Adam on every rank (baseline);
+   * 1 = peer exchange: one fused kernel per update over peer memory (NVLink P2P) that sums the
+   *     ranks' folded gradients in the reference's leader-ring order, runs Adam on this rank's
+   *     shard and writes the new weights into every rank (reduce-scatter -> sharded Adam ->
+   *     all-gather, cuda/exchange.cu). The ranks must be wired before the first iteration with
+   *     gmi_ppo_comm_attach (one process per GPU, CUDA IPC handles) or gmi_ppo_comm_connect (all
+   *     ranks in one process). With num_gpus == 1 the exchange runs over the rank itself. */
+  int comm;
 } gmi_ppo_config_t;
 
 typedef struct {
@@ -390,7 +399,17 @@ GMI_API int gmi_ppo_iteration(void* trainer, gmi_ppo_stats_t* stats);
 /* Asynchronous variant: enqueue one iteration on the trainer's streams, no host sync. */
 GMI_API int gmi_ppo_iteration_async(void* trainer);
 GMI_API int gmi_ppo_synchronize(void* trainer, gmi_ppo_stats_t* stats);
-/* Rollout + values + GAE of the next iteration only (parity checks). */
+/* Peer exchange wiring (cfg.comm = 1). gmi_ppo_comm_handle: the 64-byte CUDA IPC handle of this
+ * rank's exchange window (flags, published gradient, fp32 parameters, bf16 shadow); every rank
+ * gathers all handles in rank order (e.g. torch.distributed all_gather_object) and passes the
+ * num_gpus x 64 bytes to gmi_ppo_comm_attach. gmi_ppo_comm_connect wires n = num_gpus trainers
+ * that live in this process (trainers[r] has rank r; same or peer-capable devices). */
+GMI_API int gmi_ppo_comm_handle(void* trainer, void* out64);
+GMI_API int gmi_ppo_comm_attach(void* trainer, const void* handles);
+GMI_API int gmi_ppo_comm_connect(void* const* trainers, int n);
+/* Rollout + values + GAE of the next iteration only (parity checks). The following
+ * gmi_ppo_iteration trains on this rollout instead of rolling out again; calling the hook
+ * twice without an iteration in between fails with GMI_ERR_INVALID. */
 GMI_API int gmi_ppo_rollout(void* trainer);
 /* One minibatch gradient of local GMI `gmi` on caller rows (host fp32; B = minibatch size). */
 GMI_API int gmi_ppo_minibatch_grad(void* trainer, int gmi, const float* X, const float* act,
@@ -440,6 +459,12 @@ typedef struct {
 } gmi_ppo_phase_t;
 GMI_API const char* gmi_ppo_phase_name(int phase);
 GMI_API int gmi_ppo_profile(void* trainer, gmi_ppo_phase_t* out /* [GMI_PPO_PHASES] */);
+/* Per-GMI busy time of the last instrumented iteration (cfg.instrument = 1): summed CUDA-event
+ * time of every launch on each execution unit, with the unit's SM count (its green-context
+ * partition, or the whole GPU for plain streams). Units: decoupled -> serving GMI, trainer GMI;
+ * otherwise the local GMIs; the last unit is the update / reduction stream. busy_ms / (SMs-
+ * weighted) iteration time = the GMI's stream-level SM utilisation. *count = number of units. */
+GMI_API int gmi_ppo_unit_busy(void* trainer, double* busy_ms, int* sms, int cap, int* count);
 /* Toggle cfg.instrument on a live trainer (re-captures the iteration graph). */
 GMI_API int gmi_ppo_set_instrument(void* trainer, int on);
 

@@ -131,6 +131,7 @@ typedef struct {
   int n_gmi;
   int iteration;
   int primed; /* decoupled mode: rollout 0 done */
+  int pending; /* ppo_oracle_rollout ran the next iteration's rollout; the iteration trains on it */
   long long adam_step;
   float *params, *adam_m, *adam_v, *grad_sum;
   /* per GMI */
@@ -679,9 +680,11 @@ static void values_gae_all(oracle_t* o) {
 
 int ppo_oracle_rollout(void* h) {
   oracle_t* o = (oracle_t*)h;
+  if (o->pending) return -2; /* the next iteration's rollout already ran */
   g_exact = o->c.exact_fp32;
   rollout_all(o);
   values_gae_all(o);
+  o->pending = 1;
   return 0;
 }
 
@@ -739,7 +742,9 @@ static void train_all(oracle_t* o) {
 
 int ppo_oracle_iteration(void* h, ppo_stats_t* out) {
   oracle_t* o = (oracle_t*)h;
-  ppo_oracle_rollout(h);
+  if (!o->pending) ppo_oracle_rollout(h);
+  g_exact = o->c.exact_fp32;
+  o->pending = 0;
   train_all(o);
   if (out) *out = o->last;
   return 0;

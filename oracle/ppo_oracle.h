@@ -46,7 +46,9 @@ int ppo_oracle_iteration(void* h, ppo_stats_t* out);
 /* Decoupled (asynchronous serving/trainer) iteration, one-iteration policy lag; see
  * ppo_oracle.c. Do not mix with ppo_oracle_iteration on one handle. */
 int ppo_oracle_iteration_decoupled(void* h, ppo_stats_t* out);
-/* Runs only the rollout + GAE part of the next iteration (no update). */
+/* Runs only the rollout + GAE part of the next iteration (no update); the following
+ * ppo_oracle_iteration trains on it instead of rolling out again. Returns -2 (and does
+ * nothing) when such a rollout is already pending. */
 int ppo_oracle_rollout(void* h);
 
 /* One minibatch gradient of GMI `gmi` on caller rows with the current parameters:

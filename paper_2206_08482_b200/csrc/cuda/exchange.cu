@@ -1,0 +1,124 @@
+// Cross-GPU gradient exchange fused with Adam over peer memory (the B200 form of the HAR leader
+// all-reduce, reduction.hpp:287-299, followed by the update): reduce-scatter -> sharded Adam ->
+// all-gather in ONE kernel per minibatch update, no NCCL.
+//
+// Every rank (one per GPU, num_gpus ranks) owns an exchange window in its HBM -- flags, the
+// published gradient (its GMIs' K1 fold), the fp32 master parameters and their bf16 shadow --
+// mapped into every peer (CUDA IPC across processes, plain pointers inside one process). Per
+// update s (1-based, replay-safe: derived from the device control block):
+//   1. signal: rank r publishes ready[r] = s (release, system scope) once its fold is final;
+//   2. exchange_adam: every CTA waits for ready[q] >= s of all peers, then for its slice of
+//      rank r's shard [P r/G, P (r+1)/G) sums the G published gradients over NVLink in the
+//      leader-ring fold order of the reference (chunk c of the leader ring starts at member c,
+//      reduction.hpp:164-212; oracle/ppo_oracle.c fold_gradients), runs Adam on the shard (Adam
+//      moments are sharded: each element's m, v live only on its owner) and stores the new
+//      parameter and its bf16 shadow into EVERY rank's window (the all-gather), then bumps every
+//      rank's done counter once (release);
+//   3. wait: one thread spins until its own done counter reaches s * G * C (all C CTAs of all G
+//      ranks finished writing step s into this rank), so the next minibatch reads final weights.
+// No float atomics: every element is summed by exactly one owner in a fixed order, so all ranks
+// hold bit-identical parameters, and the arithmetic of the update is adam_kernel's.
+#include <cuda_bf16.h>
+
+#include "launch.cuh"
+#include "ppo.cuh"
+
+namespace gmi::ppo {
+
+namespace {
+
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ void red_add_release_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("red.release.sys.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ void spin_until(const unsigned long long* p, unsigned long long target) {
+  unsigned ns = 32;
+  while (ld_acquire_sys(p) < target) {
+    __nanosleep(ns);
+    ns = ns < 1024 ? ns * 2 : ns;
+  }
+}
+
+__device__ __forceinline__ long long step_id(const ExchangeArgs& a) {
+  return a.ctl->adam_step0 + a.step_in_iter + 1;  // 1-based, consecutive over the job
+}
+
+__global__ void exchange_signal_kernel(const ExchangeArgs a) {
+  pdl_trigger();
+  pdl_wait();  // the fold that produced pub[rank] has completed (device scope)
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    st_release_sys(a.ready[a.rank], (unsigned long long)step_id(a));
+  }
+}
+
+__global__ void __launch_bounds__(256) exchange_adam_kernel(const ExchangeArgs a) {
+  pdl_trigger();
+  pdl_wait();
+  const long long s = step_id(a);
+  if (threadIdx.x < a.G) spin_until(a.ready[threadIdx.x], (unsigned long long)s);
+  __syncthreads();
+  const long long st = s - 1;  // completed updates before this one (bias-correction index)
+  const float bc1 = a.bc[2 * st], bc2 = a.bc[2 * st + 1];
+  const float ob1 = __fsub_rn(1.0f, a.b1), ob2 = __fsub_rn(1.0f, a.b2);
+  // this CTA's contiguous slice of the shard
+  const long long len = a.hi - a.lo;
+  const long long c0 = a.lo + len * blockIdx.x / gridDim.x, c1 = a.lo + len * (blockIdx.x + 1) / gridDim.x;
+  for (long long i = c0 + threadIdx.x; i < c1; i += blockDim.x) {
+    // leader-ring fold: chunk cg = the ring chunk holding element i, fold starts at member cg
+    const int cg = int(((i + 1) * a.G + a.P - 1) / a.P) - 1;
+    float acc = 0.f;
+    for (int j = 0; j < a.G; ++j) {
+      int q = cg + j;
+      q -= q >= a.G ? a.G : 0;
+      const float x = a.pub[q][i];
+      acc = j == 0 ? x : __fadd_rn(x, acc);
+    }
+    const float g = __fmul_rn(acc, a.inv_n);
+    const float m = __fadd_rn(__fmul_rn(a.b1, a.m[i]), __fmul_rn(ob1, g));
+    const float v = __fadd_rn(__fmul_rn(a.b2, a.v[i]), __fmul_rn(__fmul_rn(ob2, g), g));
+    a.m[i] = m;
+    a.v[i] = v;
+    const float mh = __fdiv_rn(m, bc1), vh = __fdiv_rn(v, bc2);
+    const float p = __fsub_rn(a.params[a.rank][i], __fmul_rn(a.lr, __fdiv_rn(mh, __fadd_rn(__fsqrt_rn(vh), a.eps))));
+    const __nv_bfloat16 sh = __float2bfloat16_rn(p);
+    for (int q = 0; q < a.G; ++q) {  // all-gather: the owner writes every replica
+      a.params[q][i] = p;
+      a.shadow[q][i] = sh;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < a.G) {
+    __threadfence_system();
+    red_add_release_sys(a.done[threadIdx.x], 1ull);
+  }
+}
+
+__global__ void exchange_wait_kernel(const ExchangeArgs a) {
+  pdl_trigger();
+  pdl_wait();
+  if (threadIdx.x == 0) spin_until(a.done[a.rank], (unsigned long long)step_id(a) * (unsigned long long)(a.G * a.ctas));
+  __syncthreads();
+}
+
+}  // namespace
+
+void launch_exchange_adam(const ExchangeArgs& a, cudaStream_t s) {
+  if (a.G < 1 || a.G > kMaxRanks) invalid("exchange: 1..8 ranks");
+  if (a.ctas < 1) invalid("exchange: ctas must be >= 1");
+  launch_pdl(exchange_signal_kernel, dim3(1), dim3(32), 0, s, a);
+  launch_pdl(exchange_adam_kernel, dim3(a.ctas), dim3(256), 0, s, a);
+  launch_pdl(exchange_wait_kernel, dim3(1), dim3(32), 0, s, a);
+}
+
+}  // namespace gmi::ppo

@@ -97,6 +97,25 @@ struct SegAdam {
   float lr, b1, b2, eps, inv_n;
 };
 
+// Cross-GPU exchange + sharded Adam over peer memory (cuda/exchange.cu).
+constexpr int kMaxRanks = 8;
+struct ExchangeArgs {
+  const float* pub[kMaxRanks];           // each rank's published (K1-folded) gradient
+  float* params[kMaxRanks];              // each rank's fp32 master parameters
+  __nv_bfloat16* shadow[kMaxRanks];      // each rank's bf16 shadow
+  unsigned long long* ready[kMaxRanks];  // each rank's "gradient of step s published" flag
+  unsigned long long* done[kMaxRanks];   // each rank's "step s written into me" counter
+  int G, rank, ctas;
+  long long P, lo, hi;  // flat length; this rank's shard [lo, hi)
+  float* m;             // Adam moments (only the shard is used)
+  float* v;
+  const float* bc;
+  const Control* ctl;
+  int step_in_iter;
+  float lr, b1, b2, eps, inv_n;
+};
+void launch_exchange_adam(const ExchangeArgs& a, cudaStream_t s);
+
 struct AdamArgs {
   float* p;
   float* m;

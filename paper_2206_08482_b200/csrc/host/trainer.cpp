@@ -169,7 +169,20 @@ struct Trainer::Gmi {
 };
 
 // ------------------------------------------------------------------ construction
+// Everything the constructor acquires is released by release(), which is idempotent over
+// partially built state, so a constructor that throws midway (OOM, infeasible green-context
+// split, NCCL failure) leaks nothing (a GpuProfiler probe sweep keeps creating trainers).
 Trainer::Trainer(const gmi_ppo_config_t& cfg, const void* nccl_id) : cfg_(cfg) {
+  try {
+    init(nccl_id);
+  } catch (...) {
+    release();
+    throw;
+  }
+}
+
+void Trainer::init(const void* nccl_id) {
+  const gmi_ppo_config_t& cfg = cfg_;
   geo_ = Geometry::make(cfg);
   if (cfg.horizon < 1 || cfg.horizon > 32) invalid("horizon must be in [1, 32]");
   if (cfg.epochs < 1 || cfg.minibatches < 1) invalid("epochs and minibatches must be >= 1");
@@ -210,7 +223,10 @@ Trainer::Trainer(const gmi_ppo_config_t& cfg, const void* nccl_id) : cfg_(cfg) {
   // GMI_FORCE_NCCL=1 (tests): a one-rank communicator on a single GPU, so the NCCL all-reduce
   // in the captured iteration graph is exercised on one-GPU boxes (identity sum, bit-exact)
   const char* force = std::getenv("GMI_FORCE_NCCL");
-  const bool force_nccl = cfg.num_gpus == 1 && force && force[0] == '1';
+  xchg_ = cfg.comm == 1;
+  if (cfg.comm != 0 && cfg.comm != 1) invalid("comm must be 0 (NCCL) or 1 (peer exchange)");
+  if (xchg_ && cfg.num_gpus > ppo::kMaxRanks) invalid("peer exchange supports up to 8 GPUs per job");
+  const bool force_nccl = !xchg_ && cfg.num_gpus == 1 && force && force[0] == '1';
   upd_in_gmi_ = decoupled_ && cfg.num_gpus == 1 && !force_nccl;
   if (upd_in_gmi_)
     upd_ = exec_->extra_stream(1);
@@ -233,10 +249,11 @@ Trainer::Trainer(const gmi_ppo_config_t& cfg, const void* nccl_id) : cfg_(cfg) {
     g->s = exec_->stream(tix + i);
     g->s2 = exec_->aux_stream(tix + i);
     g->ctas = exec_->sm_count(tix + i) > 0 ? exec_->sm_count(tix + i) : sms;
-    GMI_CUDA_CHECK(cudaEventCreateWithFlags(&g->ev_done, cudaEventDisableTiming));
-    GMI_CUDA_CHECK(cudaEventCreateWithFlags(&g->ev_fork, cudaEventDisableTiming));
-    for (auto& e : g->ev_d) GMI_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    gmis_.push_back(std::move(g));
+    gmis_.push_back(std::move(g));  // owned before its events exist (release() on failure)
+    Gmi& gm = *gmis_.back();
+    GMI_CUDA_CHECK(cudaEventCreateWithFlags(&gm.ev_done, cudaEventDisableTiming));
+    GMI_CUDA_CHECK(cudaEventCreateWithFlags(&gm.ev_fork, cudaEventDisableTiming));
+    for (auto& e : gm.ev_d) GMI_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
   alloc();
   init_params();
@@ -244,7 +261,19 @@ Trainer::Trainer(const gmi_ppo_config_t& cfg, const void* nccl_id) : cfg_(cfg) {
   if (decoupled_ && !(gmis_[0]->fused_roll && gmis_[0]->fused_val))
     invalid("decoupled mode needs the fused rollout and value pass (hidden widths <= 256, <= 4 layers)");
   ensure_bias_table(1 << 20);
-  if (cfg.num_gpus > 1 || force_nccl) {
+  if (xchg_) {
+    xa_.G = cfg.num_gpus;
+    xa_.rank = cfg.rank;
+    xa_.P = geo_.P;
+    xa_.lo = geo_.P * cfg.rank / cfg.num_gpus;
+    xa_.hi = geo_.P * (cfg.rank + 1) / cfg.num_gpus;
+    // same on every rank (the done counter target is steps x G x ctas)
+    xa_.ctas = int(std::max<long long>(1, std::min<long long>(148, (geo_.P / cfg.num_gpus + 2047) / 2048)));
+    if (cfg.num_gpus == 1) {  // one rank: the exchange runs over the rank itself
+      Trainer* self = this;
+      comm_connect(&self, 1);
+    }
+  } else if (cfg.num_gpus > 1 || force_nccl) {
     ncclUniqueId id;
     if (force_nccl) {
       NCCL_CHECK(ncclGetUniqueId(&id));
@@ -264,27 +293,41 @@ Trainer::Trainer(const gmi_ppo_config_t& cfg, const void* nccl_id) : cfg_(cfg) {
   GMI_CUDA_CHECK(cudaDeviceSynchronize());
 }
 
-Trainer::~Trainer() {
+Trainer::~Trainer() { release(); }
+
+void Trainer::release() noexcept {
   cudaDeviceSynchronize();
   if (graph_) cudaGraphExecDestroy(graph_);
+  graph_ = nullptr;
   if (nccl_) ncclCommDestroy(static_cast<ncclComm_t>(nccl_));
+  nccl_ = nullptr;
+  for (void* p : ipc_opened_) cudaIpcCloseMemHandle(p);
+  ipc_opened_.clear();
   for (auto& m : marks_) {
     cudaEventDestroy(m.a);
     cudaEventDestroy(m.b);
   }
+  marks_.clear();
   for (auto& g : gmis_) {
-    cudaEventDestroy(g->ev_done);
-    cudaEventDestroy(g->ev_fork);
-    for (auto e : g->ev_d) cudaEventDestroy(e);
+    if (g->ev_done) cudaEventDestroy(g->ev_done);
+    if (g->ev_fork) cudaEventDestroy(g->ev_fork);
+    for (auto e : g->ev_d)
+      if (e) cudaEventDestroy(e);
   }
+  gmis_.clear();
   if (ev_copied_) cudaEventDestroy(ev_copied_);
   if (ev_rolled_) cudaEventDestroy(ev_rolled_);
   if (ev_adam_) cudaEventDestroy(ev_adam_);
   if (ev_start_) cudaEventDestroy(ev_start_);
+  ev_copied_ = ev_rolled_ = ev_adam_ = ev_start_ = nullptr;
   if (upd_ && !upd_in_gmi_) cudaStreamDestroy(upd_);
+  upd_ = nullptr;
   for (void* p : allocs_) cudaFree(p);
+  allocs_.clear();
   if (ctl_host_) cudaFreeHost(ctl_host_);
   if (stats_host_) cudaFreeHost(stats_host_);
+  ctl_host_ = nullptr;
+  stats_host_ = nullptr;
   exec_.reset();
 }
 
@@ -299,11 +342,20 @@ void Trainer::alloc() {
     return p;
   };
   const long long P = geo_.P;
-  params_ = static_cast<float*>(dev(P * 4));
+  if (xchg_) {  // exchange window: [flags 256 B | pub P fp32 | params P fp32 | shadow P bf16]
+    win_off_params_ = 256 + (size_t)P * 4;
+    win_off_shadow_ = win_off_params_ + (size_t)P * 4;
+    win_ = static_cast<char*>(dev(win_off_shadow_ + (size_t)P * 2));
+    grad_sum_ = reinterpret_cast<float*>(win_ + 256);
+    params_ = reinterpret_cast<float*>(win_ + win_off_params_);
+    shadow_ = reinterpret_cast<__nv_bfloat16*>(win_ + win_off_shadow_);
+  } else {
+    params_ = static_cast<float*>(dev(P * 4));
+    grad_sum_ = static_cast<float*>(dev(P * 4));
+    shadow_ = static_cast<__nv_bfloat16*>(dev(P * 2));
+  }
   m_ = static_cast<float*>(dev(P * 4));
   v_ = static_cast<float*>(dev(P * 4));
-  grad_sum_ = static_cast<float*>(dev(P * 4));
-  shadow_ = static_cast<__nv_bfloat16*>(dev(P * 2));
   ctl_dev_ = static_cast<ppo::Control*>(dev(sizeof(ppo::Control)));
   stats_dev_ = static_cast<float*>(dev(8 * 4));
   GMI_CUDA_CHECK(cudaMallocHost(&ctl_host_, sizeof(ppo::Control)));
@@ -360,7 +412,8 @@ void Trainer::alloc() {
     g.Gpi = static_cast<__nv_bfloat16*>(dev((long long)g.Bm * ppo::kHeadG * 2));
     g.Gv = static_cast<__nv_bfloat16*>(dev((long long)g.Bm * ppo::kHeadG * 2));
     for (int n = 0; n < 2; ++n) g.outh[n] = static_cast<float*>(dev((long long)g.Mrows * ppo::kHeadG * 4));
-    g.grad = static_cast<float*>(dev(P * 4));
+    // peer exchange with one GMI: its assembled gradient is the published one (no K1 fold)
+    g.grad = xchg_ && n_local_ == 1 ? grad_sum_ : static_cast<float*>(dev(P * 4));
     g.head_part = static_cast<float*>(dev((long long)ppo::head_loss_blocks(g.Bm) * ppo::head_partial_stride(A) * 4));
   }
 }
@@ -835,10 +888,32 @@ void Trainer::build_plans() {
 }
 
 // ------------------------------------------------------------------ launch helpers
+int Trainer::unit_of(cudaStream_t s) const {
+  if (s == upd_) return decoupled_ ? 2 : n_local_;
+  if (decoupled_ && s == serve_s_) return 0;
+  for (const auto& g : gmis_)
+    if (s == g->s || s == g->s2) return decoupled_ ? 1 : g->local;
+  return -1;
+}
+
+int Trainer::busy_units(double* busy_ms, int* sms, int cap) const {
+  const int n = decoupled_ ? 3 : n_local_ + 1;
+  for (int i = 0; i < n && i < cap; ++i) {
+    if (busy_ms) busy_ms[i] = i < int(unit_busy_ms_.size()) ? unit_busy_ms_[i] : 0.0;
+    if (sms) {
+      const bool upd = i == n - 1;
+      // GMI i is execution resource i (decoupled: 0 serving, 1 trainer)
+      sms[i] = upd ? (upd_in_gmi_ ? exec_->sm_count(1) : 0) : exec_->sm_count(i);
+      if (sms[i] <= 0) sms[i] = device_sm_count();
+    }
+  }
+  return n;
+}
+
 template <class F>
 void Trainer::timed(cudaStream_t s, int phase, double flop, double bytes, F&& f) {
-  const bool on = cfg_.instrument && (s == upd_ || s == gmis_[0]->s || s == gmis_[0]->s2);
-  if (!on) {
+  const int unit = cfg_.instrument ? unit_of(s) : -1;
+  if (unit < 0) {
     f();
     return;
   }
@@ -856,6 +931,8 @@ void Trainer::timed(cudaStream_t s, int phase, double flop, double bytes, F&& f)
   f();
   GMI_CUDA_CHECK(cudaEventRecordWithFlags(m.b, s, flags));
   m.phase = phase;
+  m.unit = unit;
+  m.in_phases = s == upd_ || s == gmis_[0]->s || s == gmis_[0]->s2;
   m.flop = flop;
   m.bytes = bytes;
 }
@@ -1154,6 +1231,26 @@ void Trainer::reduce_and_step(int step_in_iter) {
     ++launches_;
     src = grad_sum_;
   }
+  if (xchg_) {  // fused reduce-scatter -> sharded Adam -> all-gather over peer memory
+    ppo::ExchangeArgs a = xa_;
+    a.m = m_;
+    a.v = v_;
+    a.bc = bc_;
+    a.ctl = ctl_dev_;
+    a.step_in_iter = step_in_iter;
+    a.lr = cfg_.lr;
+    a.b1 = cfg_.beta1;
+    a.b2 = cfg_.beta2;
+    a.eps = cfg_.adam_eps;
+    a.inv_n = 1.0f / float(n_total_);
+    // per rank and update: G x 4 B read per shard element, 6 B written per element per replica
+    const double shard = double(xa_.hi - xa_.lo);
+    timed(upd_, GMI_PH_ALLREDUCE, 0.0, shard * (4.0 * cfg_.num_gpus + 16.0 + 6.0 * cfg_.num_gpus),
+          [&] { ppo::launch_exchange_adam(a, upd_); });
+    launches_ += 3;
+    GMI_CUDA_CHECK(cudaEventRecord(ev_adam_, upd_));
+    return;
+  }
   if (nccl_) {
     const double bus = 2.0 * (cfg_.num_gpus - 1) / cfg_.num_gpus * 4.0 * geo_.P;
     timed(upd_, GMI_PH_ALLREDUCE, 0.0, bus, [&] {
@@ -1189,27 +1286,39 @@ void Trainer::reduce_and_step(int step_in_iter) {
 void Trainer::serve_rollout(Gmi& g) {
   const int S_p = geo_.wp[0];
   if (rollouts_ > 0)
-    GMI_CUDA_CHECK(cudaMemcpyAsync(g.ch_X, g.ch_X + (long long)T_ * g.N * S_p, (size_t)g.N * S_p * 2,
-                                   cudaMemcpyDeviceToDevice, serve_s_));
-  if (g.roll_cluster)
-    ppo::launch_rollout_cluster(g.roll_args, g.roll_cluster, serve_s_);
-  else
-    ppo::launch_rollout(g.roll_args, serve_s_);
+    timed(serve_s_, GMI_PH_OTHER, 0.0, 4.0 * g.N * S_p, [&] {
+      GMI_CUDA_CHECK(cudaMemcpyAsync(g.ch_X, g.ch_X + (long long)T_ * g.N * S_p, (size_t)g.N * S_p * 2,
+                                     cudaMemcpyDeviceToDevice, serve_s_));
+    });
+  timed(serve_s_, GMI_PH_ROLL_GEMM, 0.0, 0.0, [&] {
+    if (g.roll_cluster)
+      ppo::launch_rollout_cluster(g.roll_args, g.roll_cluster, serve_s_);
+    else
+      ppo::launch_rollout(g.roll_args, serve_s_);
+  });
   // values of all T+1 observation slots with the same snapshot, then GAE: the channel carries
   // ready advantages / returns, so the trainer starts straight at the epoch shuffle
   const int sms = exec_->sm_count(0) > 0 ? exec_->sm_count(0) : device_sm_count();
-  ppo::launch_value_mlp(g.ch_val_args, sms, serve_s_);
-  ppo::launch_gae(g.ch_rew, g.ch_done, g.ch_V, g.ch_adv, g.ch_ret, g.ch_gae_part, g.N, T_, cfg_.gamma, cfg_.lam,
-                  serve_s_);
-  ppo::launch_adv_stats(g.ch_gae_part, ppo::gae_blocks(g.N), (long long)T_ * g.N, g.ch_adv_stats, serve_s_);
-  ppo::launch_control_advance(ctl_roll_, 0, serve_s_);
+  timed(serve_s_, GMI_PH_VAL_GEMM, 0.0, 0.0, [&] { ppo::launch_value_mlp(g.ch_val_args, sms, serve_s_); });
+  timed(serve_s_, GMI_PH_GAE, 0.0, 0.0, [&] {
+    ppo::launch_gae(g.ch_rew, g.ch_done, g.ch_V, g.ch_adv, g.ch_ret, g.ch_gae_part, g.N, T_, cfg_.gamma, cfg_.lam,
+                    serve_s_);
+    ppo::launch_adv_stats(g.ch_gae_part, ppo::gae_blocks(g.N), (long long)T_ * g.N, g.ch_adv_stats, serve_s_);
+    ppo::launch_control_advance(ctl_roll_, 0, serve_s_);
+  });
   GMI_CUDA_CHECK(cudaEventRecord(ev_rolled_, serve_s_));
   launches_ += 5;
   ++rollouts_;
 }
 
+// Parity hook: the next iteration's rollout + values + GAE only. The following iteration trains
+// on this rollout instead of rolling out again (so the env never steps twice from one
+// observation slot and noise keys are never reused); a second hook before it is rejected.
 void Trainer::enqueue_rollout() {
   if (decoupled_) invalid("gmi_ppo_rollout: the serving GMI rolls out inside each decoupled iteration");
+  if (rollout_pending_) invalid("gmi_ppo_rollout: a rollout is already pending; run gmi_ppo_iteration to train on it");
+  GMI_CUDA_CHECK(cudaSetDevice(cfg_.device));
+  rollout_pending_ = true;
   write_control();
   GMI_CUDA_CHECK(cudaEventRecord(ev_start_, upd_));
   for (auto& g : gmis_) {
@@ -1222,11 +1331,13 @@ void Trainer::enqueue_rollout() {
 }
 
 // Every kernel / copy / collective of one iteration, on the GMI streams and upd_.
-void Trainer::record_iteration() {
+void Trainer::record_iteration(bool with_rollout) {
   launches_ = 0;
   marks_used_ = 0;
   GMI_CUDA_CHECK(cudaEventRecord(ev_start_, upd_));
-  if (decoupled_) {
+  if (!with_rollout) {  // trains on the rollout a gmi_ppo_rollout hook produced
+    for (auto& g : gmis_) GMI_CUDA_CHECK(cudaStreamWaitEvent(g->s, ev_start_, 0));
+  } else if (decoupled_) {
     // migrate the channel's experience (rollout i) into the trainer's buffers, then let the
     // serving GMI produce rollout i+1 with the snapshot theta_i while this slot trains
     Gmi& g = *gmis_[0];
@@ -1259,7 +1370,7 @@ void Trainer::record_iteration() {
   // Measured slightly slower than the separate Adam launch on B200 (3.62 vs 3.60 ms per
   // iteration), so the separate kernel stays the default.
   const char* adam_fused = std::getenv("GMI_ADAM_FUSED");
-  const bool fused_adam = n_local_ == 1 && !nccl_ && adam_fused && adam_fused[0] == '1';
+  const bool fused_adam = n_local_ == 1 && !nccl_ && !xchg_ && adam_fused && adam_fused[0] == '1';
   for (int e = 0; e < cfg_.epochs; ++e) {
     for (auto& g : gmis_) {
       if (step > 0 && !fused_adam) GMI_CUDA_CHECK(cudaStreamWaitEvent(g->s, ev_adam_, 0));
@@ -1298,7 +1409,71 @@ void Trainer::record_iteration() {
   ++launches_;
 }
 
+void Trainer::comm_handle(void* out64) const {
+  if (!xchg_) invalid("gmi_ppo_comm_handle: the trainer was not created with comm = 1");
+  cudaIpcMemHandle_t h;
+  GMI_CUDA_CHECK(cudaIpcGetMemHandle(&h, win_));
+  static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+  std::memcpy(out64, &h, sizeof(h));
+}
+
+void Trainer::comm_attach(const void* handles) {
+  if (!xchg_) invalid("gmi_ppo_comm_attach: the trainer was not created with comm = 1");
+  if (connected_) invalid("gmi_ppo_comm_attach: already wired");
+  GMI_CUDA_CHECK(cudaSetDevice(cfg_.device));
+  const char* hb = static_cast<const char*>(handles);
+  for (int q = 0; q < cfg_.num_gpus; ++q) {
+    char* base = win_;
+    if (q != cfg_.rank) {
+      cudaIpcMemHandle_t h;
+      std::memcpy(&h, hb + 64 * q, 64);
+      void* p = nullptr;
+      GMI_CUDA_CHECK(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+      ipc_opened_.push_back(p);
+      base = static_cast<char*>(p);
+    }
+    xa_.ready[q] = reinterpret_cast<unsigned long long*>(base);
+    xa_.done[q] = reinterpret_cast<unsigned long long*>(base + 128);
+    xa_.pub[q] = reinterpret_cast<const float*>(base + 256);
+    xa_.params[q] = reinterpret_cast<float*>(base + win_off_params_);
+    xa_.shadow[q] = reinterpret_cast<__nv_bfloat16*>(base + win_off_shadow_);
+  }
+  connected_ = true;
+}
+
+void Trainer::comm_connect(Trainer* const* t, int n) {
+  if (n < 1 || n > ppo::kMaxRanks) invalid("gmi_ppo_comm_connect: 1..8 trainers");
+  for (int r = 0; r < n; ++r) {
+    if (!t[r] || !t[r]->xchg_) invalid("gmi_ppo_comm_connect: every trainer needs comm = 1");
+    if (t[r]->cfg_.rank != r || t[r]->cfg_.num_gpus != n || t[r]->geo_.P != t[0]->geo_.P)
+      invalid("gmi_ppo_comm_connect: trainers[r] must be rank r of one num_gpus = n job");
+    if (t[r]->connected_) invalid("gmi_ppo_comm_connect: already wired");
+  }
+  for (int r = 0; r < n; ++r) {
+    Trainer& me = *t[r];
+    GMI_CUDA_CHECK(cudaSetDevice(me.cfg_.device));
+    for (int q = 0; q < n; ++q) {
+      const Trainer& peer = *t[q];
+      if (peer.cfg_.device != me.cfg_.device) {
+        const cudaError_t e = cudaDeviceEnablePeerAccess(peer.cfg_.device, 0);
+        if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+        else GMI_CUDA_CHECK(e);
+      }
+      me.xa_.ready[q] = reinterpret_cast<unsigned long long*>(peer.win_);
+      me.xa_.done[q] = reinterpret_cast<unsigned long long*>(peer.win_ + 128);
+      me.xa_.pub[q] = peer.grad_sum_;
+      me.xa_.params[q] = peer.params_;
+      me.xa_.shadow[q] = peer.shadow_;
+    }
+    me.connected_ = true;
+  }
+  GMI_CUDA_CHECK(cudaSetDevice(t[n - 1]->cfg_.device));
+}
+
 void Trainer::enqueue_iteration(bool host_control) {
+  if (xchg_ && !connected_)
+    invalid("peer exchange not wired: call gmi_ppo_comm_attach / gmi_ppo_comm_connect before iterating");
+  GMI_CUDA_CHECK(cudaSetDevice(cfg_.device));
   ensure_bias_table(adam_steps_ + (long long)cfg_.epochs * K_ + 1);
   if (host_control || iteration_ == 0) write_control();
   if (decoupled_ && rollouts_ == 0) {  // prologue: rollout 0 with theta_0 (not overlapped)
@@ -1310,14 +1485,17 @@ void Trainer::enqueue_iteration(bool host_control) {
     serve_rollout(*gmis_[0]);
     GMI_CUDA_CHECK(cudaStreamWaitEvent(upd_, ev_rolled_, 0));
   }
-  if (cfg_.use_graph && iteration_ > 0) {
+  if (rollout_pending_) {  // after the rollout hook: the update phases only, eagerly
+    rollout_pending_ = false;
+    record_iteration(false);
+  } else if (cfg_.use_graph && iteration_ > 0) {
     if (!graph_) {
       GMI_CUDA_CHECK(cudaStreamSynchronize(upd_));
       cudaGraph_t gr;
       GMI_CUDA_CHECK(cudaStreamBeginCapture(upd_, cudaStreamCaptureModeThreadLocal));
       capturing_ = true;
       try {
-        record_iteration();
+        record_iteration(true);
       } catch (...) {
         cudaStreamEndCapture(upd_, &gr);
         capturing_ = false;
@@ -1330,7 +1508,7 @@ void Trainer::enqueue_iteration(bool host_control) {
     }
     GMI_CUDA_CHECK(cudaGraphLaunch(graph_, upd_));
   } else {
-    record_iteration();
+    record_iteration(true);
   }
   iteration_ += 1;
   adam_steps_ += (long long)cfg_.epochs * K_;
@@ -1343,9 +1521,12 @@ void Trainer::synchronize(gmi_ppo_stats_t* st) {
   gmi_ppo_phase_t gemm{};
   if (cfg_.instrument) {
     std::memset(phases_, 0, sizeof(phases_));
+    unit_busy_ms_.assign(decoupled_ ? 3 : n_local_ + 1, 0.0);
     for (int i = 0; i < marks_used_; ++i) {
       float ms = 0;
       GMI_CUDA_CHECK(cudaEventElapsedTime(&ms, marks_[i].a, marks_[i].b));
+      unit_busy_ms_.at(marks_[i].unit) += ms;
+      if (!marks_[i].in_phases) continue;
       gmi_ppo_phase_t& ph = phases_[marks_[i].phase];
       ph.ms += ms;
       ph.flop += marks_[i].flop;
@@ -1563,6 +1744,29 @@ GMI_API int gmi_ppo_synchronize(void* t, gmi_ppo_stats_t* st) {
   return gmi::guarded([&] { static_cast<gmi::Trainer*>(t)->synchronize(st); });
 }
 
+GMI_API int gmi_ppo_comm_handle(void* t, void* out64) {
+  return gmi::guarded([&] {
+    if (!t || !out64) gmi::invalid("null argument");
+    static_cast<gmi::Trainer*>(t)->comm_handle(out64);
+  });
+}
+
+GMI_API int gmi_ppo_comm_attach(void* t, const void* handles) {
+  return gmi::guarded([&] {
+    if (!t || !handles) gmi::invalid("null argument");
+    static_cast<gmi::Trainer*>(t)->comm_attach(handles);
+  });
+}
+
+GMI_API int gmi_ppo_comm_connect(void* const* trainers, int n) {
+  return gmi::guarded([&] {
+    if (!trainers) gmi::invalid("null argument");
+    std::vector<gmi::Trainer*> v(n > 0 ? n : 0);
+    for (int i = 0; i < n; ++i) v[i] = static_cast<gmi::Trainer*>(trainers[i]);
+    gmi::Trainer::comm_connect(v.data(), n);
+  });
+}
+
 GMI_API int gmi_ppo_rollout(void* t) {
   return gmi::guarded([&] {
     auto* tr = static_cast<gmi::Trainer*>(t);
@@ -1611,6 +1815,13 @@ GMI_API int gmi_ppo_profile(void* t, gmi_ppo_phase_t* out) {
   return gmi::guarded([&] {
     if (!out) gmi::invalid("null output");
     std::memcpy(out, static_cast<gmi::Trainer*>(t)->phases(), sizeof(gmi_ppo_phase_t) * GMI_PPO_PHASES);
+  });
+}
+
+GMI_API int gmi_ppo_unit_busy(void* t, double* busy_ms, int* sms, int cap, int* count) {
+  return gmi::guarded([&] {
+    const int n = static_cast<gmi::Trainer*>(t)->busy_units(busy_ms, sms, cap);
+    if (count) *count = n;
   });
 }
 

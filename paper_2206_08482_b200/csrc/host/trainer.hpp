@@ -51,12 +51,14 @@ class Trainer {
  private:
   struct Gmi;
 
+  void init(const void* nccl_id);
+  void release() noexcept;
   void alloc();
   void init_params();
   void build_plans();
   void ensure_bias_table(long long steps);
   void write_control();
-  void record_iteration();  // the launch sequence of one iteration (eager or under capture)
+  void record_iteration(bool with_rollout);  // one iteration's launches (eager or under capture)
   void serve_rollout(Gmi& g);  // decoupled mode: the serving GMI's rollout into the channel
   void rollout(Gmi& g);
   void values(Gmi& g);
@@ -98,11 +100,20 @@ class Trainer {
   __nv_bfloat16* shadow_roll_ = nullptr;
   ppo::Control* ctl_roll_ = nullptr;
   long long rollouts_ = 0;  // serving-GMI rollouts enqueued so far
+  // peer exchange (cfg.comm = 1, cuda/exchange.cu): this rank's window [flags | pub | params |
+  // shadow] (IPC-exportable cudaMalloc), the peer-pointer table, and IPC mappings opened
+  bool xchg_ = false;
+  bool connected_ = false;
+  char* win_ = nullptr;
+  size_t win_off_params_ = 0, win_off_shadow_ = 0;
+  ppo::ExchangeArgs xa_{};
+  std::vector<void*> ipc_opened_;
   void* gemm_trace_ = nullptr;  // GMI_GEMM_TRACE development aid
   void* head_trace_ = nullptr;  // GMI_HEAD_TRACE development aid
   bool bwd_par_ = false;   // dx chain || dW GEMMs on two streams of the GMI
   int bwd_dx_share_ = 50;  // percent of the GMI's SMs given to the dx branch
   int iteration_ = 0;      // iterations enqueued so far
+  bool rollout_pending_ = false;  // gmi_ppo_rollout produced the next iteration's rollout
   long long adam_steps_ = 0;
   int launches_ = 0;       // kernels in one iteration
   bool capturing_ = false;
@@ -111,14 +122,25 @@ class Trainer {
   struct Mark {
     cudaEvent_t a = nullptr, b = nullptr;
     int phase = 0;
+    int unit = 0;         // execution unit (busy_units order) the launch ran on
+    bool in_phases = false;  // GMI 0 / update stream: booked to phases_
     double flop = 0, bytes = 0;
   };
   std::vector<Mark> marks_;
   int marks_used_ = 0;
   gmi_ppo_phase_t phases_[GMI_PPO_PHASES] = {};
+  std::vector<double> unit_busy_ms_;  // per execution unit, last instrumented iteration
+  int unit_of(cudaStream_t s) const;  // -1: not instrumented
 
  public:
   const gmi_ppo_phase_t* phases() const { return phases_; }
+  // peer exchange wiring (gmi_ppo_comm_*)
+  void comm_handle(void* out64) const;
+  void comm_attach(const void* handles);
+  static void comm_connect(Trainer* const* trainers, int n);
+  // Execution units in report order: decoupled -> [serving GMI, trainer GMI], else the local
+  // GMIs; then the update stream. busy = summed kernel time of the unit's instrumented launches.
+  int busy_units(double* busy_ms, int* sms, int cap) const;
   void set_instrument(int on);
 };
 

@@ -26,7 +26,8 @@ class PpoConfigT(C.Structure):
                 ("ent_coef", C.c_float), ("seed", C.c_ulonglong), ("num_gpus", C.c_int),
                 ("gmis_per_gpu", C.c_int), ("rank", C.c_int), ("device", C.c_int),
                 ("gmi_backend", C.c_int), ("sm_per_gmi", C.c_int), ("use_graph", C.c_int),
-                ("instrument", C.c_int), ("decoupled", C.c_int), ("serving_sms", C.c_int)]
+                ("instrument", C.c_int), ("decoupled", C.c_int), ("serving_sms", C.c_int),
+                ("comm", C.c_int)]
 
 
 PPO_PHASES = 20  # GMI_PPO_PHASES
@@ -52,6 +53,9 @@ _PROTOS = {
     "gmi_ppo_iteration_async": (C.c_int, [C.c_void_p]),
     "gmi_ppo_synchronize": (C.c_int, [C.c_void_p, C.POINTER(PpoStatsT)]),
     "gmi_ppo_rollout": (C.c_int, [C.c_void_p]),
+    "gmi_ppo_comm_handle": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "gmi_ppo_comm_attach": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "gmi_ppo_comm_connect": (C.c_int, [C.POINTER(C.c_void_p), C.c_int]),
     "gmi_ppo_minibatch_grad": (C.c_int, [C.c_void_p, C.c_int] + [C.POINTER(C.c_float)] * 5 +
                                [C.c_int, C.POINTER(C.c_float)]),
     "gmi_ppo_get": (C.c_int, [C.c_void_p, C.c_char_p, C.c_int, C.c_void_p, C.POINTER(C.c_longlong)]),
@@ -61,6 +65,8 @@ _PROTOS = {
     "gmi_ppo_phase_name": (C.c_char_p, [C.c_int]),
     "gmi_ppo_profile": (C.c_int, [C.c_void_p, C.c_void_p]),
     "gmi_ppo_set_instrument": (C.c_int, [C.c_void_p, C.c_int]),
+    "gmi_ppo_unit_busy": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_int), C.c_int,
+                                    C.POINTER(C.c_int)]),
 }
 L.PROTOTYPES.update(_PROTOS)
 if L._lib is not None:  # library already loaded: bind the late prototypes
@@ -97,6 +103,7 @@ class PpoConfig:
     instrument: int = 0
     decoupled: int = 0
     serving_sms: int = 0
+    comm: int = 0  # num_gpus > 1: 0 NCCL all-reduce, 1 peer exchange (fused reduce-scatter/Adam/all-gather)
 
     def to_c(self) -> PpoConfigT:
         c = PpoConfigT()
@@ -138,9 +145,29 @@ class PpoConfig:
                         gmis_per_gpu=model.gmis_per_gpu, num_gpus=max(1, len(topo.gpus)),
                         decoupled=int(cfg.get("ppo", "decoupled") or 0),
                         serving_sms=int(cfg.get("ppo", "serving_sms") or 0))
+        backend = cfg.get("ppo", "gmi_backend")
         if out.decoupled:  # [model] gmis_per_gpu counts all GMIs; the trainer side is one per GPU
             out.gmis_per_gpu = 1
-            out.gmi_backend = int(cfg.get("ppo", "gmi_backend") or 1)
+            out.gmi_backend = int(backend or 1)
+        else:
+            # The topology's MPS partitions of the first GPU are the GMIs (topology.hpp:72-88): on
+            # B200 each share is realised as a green context of whole 8-SM groups (gmi_green_sms).
+            first = min((g.id for g in topo.gpus), default=0)
+            parts = [p for p in topo.partitions if p.gpu_id == first]
+            partitioned = any(p.backend == gmux.Backend.MPS and p.sm_share < 1.0 for p in parts)
+            out.gmi_backend = int(backend) if backend is not None else (1 if partitioned else 0)
+            if out.gmi_backend == 1 and parts:
+                if len(parts) != out.gmis_per_gpu:
+                    raise gmux.ConfigError(f"{path}: [model] gmis_per_gpu = {out.gmis_per_gpu} but GPU {first} "
+                                           f"has {len(parts)} gmi partitions")
+                shares = sorted({round(p.sm_share, 9) for p in parts})
+                if len(shares) != 1:
+                    raise gmux.ConfigError(f"{path}: unequal MPS shares {shares} cannot be realised as equal "
+                                           "green-context GMIs")
+                out.sm_per_gmi = gmux.green_sms(shares[0])
+                if out.sm_per_gmi < 8 or out.sm_per_gmi * len(parts) > 148:
+                    raise gmux.ConfigError(f"{path}: share {shares[0]} x {len(parts)} GMIs is not realisable "
+                                           "on a 148-SM B200 in 8-SM groups")
         for k, v in kw.items():
             setattr(out, k, v)
         return out
@@ -212,6 +239,23 @@ class Trainer:
     def rollout(self) -> None:
         L.check(L.lib().gmi_ppo_rollout(self._h))
 
+    def comm_handle(self) -> bytes:
+        """64-byte CUDA IPC handle of this rank's exchange window (cfg.comm = 1)."""
+        buf = (C.c_char * 64)()
+        L.check(L.lib().gmi_ppo_comm_handle(self._h, buf))
+        return bytes(buf)
+
+    def comm_attach(self, handles: list) -> None:
+        """Wire the peer exchange from every rank's comm_handle(), in rank order."""
+        blob = b"".join(handles)
+        L.check(L.lib().gmi_ppo_comm_attach(self._h, C.create_string_buffer(blob, len(blob))))
+
+    @staticmethod
+    def comm_connect(trainers: list) -> None:
+        """Wire the peer exchange of trainers living in this process (trainers[r] = rank r)."""
+        arr = (C.c_void_p * len(trainers))(*[t._h.value for t in trainers])
+        L.check(L.lib().gmi_ppo_comm_connect(arr, len(trainers)))
+
     def stream(self, gmi: int = -1) -> int:
         s = C.c_void_p()
         L.check(L.lib().gmi_ppo_stream(self._h, gmi, C.byref(s)))
@@ -228,6 +272,15 @@ class Trainer:
         return {L.lib().gmi_ppo_phase_name(i).decode(): {"ms": a.ms, "flop": a.flop, "bytes": a.bytes,
                                                         "launches": a.launches}
                 for i, a in enumerate(arr)}
+
+    def unit_busy(self) -> list:
+        """[(busy_ms, sms)] per execution unit of the last instrumented iteration: decoupled ->
+        serving GMI, trainer GMI; else the local GMIs; last = the update stream."""
+        n = C.c_int()
+        L.check(L.lib().gmi_ppo_unit_busy(self._h, None, None, 0, C.byref(n)))
+        busy, sms = (C.c_double * n.value)(), (C.c_int * n.value)()
+        L.check(L.lib().gmi_ppo_unit_busy(self._h, busy, sms, n.value, C.byref(n)))
+        return [(busy[i], sms[i]) for i in range(n.value)]
 
     def get(self, what: str, gmi: int = 0) -> np.ndarray:
         n = C.c_longlong()

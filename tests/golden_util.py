@@ -186,7 +186,8 @@ class PpoOracle:
         return s
 
     def rollout(self):
-        ppo_lib().ppo_oracle_rollout(self.h)
+        if ppo_lib().ppo_oracle_rollout(self.h) != 0:
+            raise RuntimeError("a rollout is already pending: run iteration() to train on it")
 
     def iteration_decoupled(self):
         s = PpoStats()

@@ -101,7 +101,7 @@ def test_bench_reference_arm_under_torchrun():
     env = dict(os.environ)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.join(ROOT, "bench.py"),
-           "--impl", "reference", "--gpus", "2", "--steps", "1", "--warmup", "0", "--cpu-sample-envs", "16"]
+           "--impl", "reference", "--gpus", "2", "--steps", "1", "--warmup", "0", "--envs", "16"]
     r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-2000:]
     lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
@@ -109,3 +109,13 @@ def test_bench_reference_arm_under_torchrun():
     import json
     d = json.loads(lines[0])
     assert d["impl"] == "reference" and d["value"] > 0 and d["cpu_baseline"]["kind"] == "port"
+
+
+def test_bench_reference_arm_never_loads_libgmi():
+    """The reference arm times the CPU path only: neither the package nor libgmi.so is loaded."""
+    code = ("import runpy, sys; sys.argv = ['bench.py', '--impl', 'reference', '--steps', '1', '--warmup', '0', "
+            "'--envs', '16']; runpy.run_path('bench.py', run_name='__main__'); "
+            "assert 'paper_2206_08482_b200' not in sys.modules; "
+            "assert 'libgmi' not in open('/proc/self/maps').read()")
+    r = subprocess.run([sys.executable, "-c", code], cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]

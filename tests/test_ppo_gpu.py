@@ -162,7 +162,11 @@ def test_fused_rollout_matches_per_layer_path(cuda, monkeypatch, dims):
     monkeypatch.setenv("GMI_ROLLOUT_UNFUSED", "1")
     monkeypatch.setenv("GMI_VALUE_UNFUSED", "1")
     plain = Trainer(PpoConfig(**cfg))
-    for _ in range(2):  # second rollout starts from carried-over state (done resets inside)
+    for it in range(2):  # second rollout starts from the carried-over observation slot
+        if it:  # train on the hook's rollout, then give both the same weights
+            fused.iteration()
+            plain.iteration()
+            plain.set("params", fused.get("params"))
         fused.rollout()
         plain.rollout()
         for f in ("done", "ep_count", "ep_step", "act", "obs", "x", "val"):
