@@ -124,9 +124,17 @@ inline const std::vector<MigProfile>& mig_profiles() {
   return p;
 }
 
+// B200 extension: NVIDIA's published 180 GB B200 profiles (compute slices of 7, label memory).
+inline const std::vector<MigProfile>& mig_profiles_sm100() {
+  static const std::vector<MigProfile> p = {{"1g.23gb", 1, 23.0}, {"1g.45gb", 1, 45.0}, {"2g.45gb", 2, 45.0},
+                                            {"3g.90gb", 3, 90.0}, {"4g.90gb", 4, 90.0}, {"7g.180gb", 7, 180.0}};
+  return p;
+}
+
 inline const MigProfile* find_mig_profile(std::string_view name) {
-  for (const auto& p : mig_profiles())
-    if (p.name == name) return &p;
+  for (const auto* tab : {&mig_profiles(), &mig_profiles_sm100()})
+    for (const auto& p : *tab)
+      if (p.name == name) return &p;
   return nullptr;
 }
 

@@ -535,20 +535,26 @@ static void minibatch_grad(oracle_t* o, int gi, mb_t* mb, int Bm, const float* w
   (void)gi;
 }
 
-/* Sum of per-GMI gradients in the fold order of the layout's reduction strategy
- * (one GPU: MPR ring over its GMIs; several GPUs: per-GPU rings then leaders). */
+/* Sum of per-GMI gradients in the fold order of the strategy Alg. 1 selects for the uniform
+ * G x t layout (reduction.hpp:98-106): G <= 1 MPR (one ring over every GMI), t > G HAR
+ * (per-GPU rings, then the leaders' ring, :287-299), else MRR (t rings of one GMI per GPU,
+ * ring r = GMI r of GPUs r, r+1, ... (:127-139), then the ring results summed into a zero
+ * total in ring order, :255-283). Ring folds start at the owner of the element's chunk
+ * (:164-212). */
+static int chunk_of(long long e, long long len, int n) { return (int)(((e + 1) * n + len - 1) / len) - 1; }
+
 static void fold_gradients(oracle_t* o) {
   const int n = o->n_gmi, t = o->c.gmis_per_gpu, G = o->c.num_gpus;
   const long long len = o->P;
   for (long long e = 0; e < len; ++e) {
     if (G <= 1) {
-      const int c = (int)(((e + 1) * n + len - 1) / len) - 1;
+      const int c = chunk_of(e, len, n);
       float acc = o->g[c].grad[e];
       for (int j = 1; j < n; ++j) acc = o->g[(c + j) % n].grad[e] + acc;
       o->grad_sum[e] = acc;
-    } else {
-      const int cl = (int)(((e + 1) * t + len - 1) / len) - 1;
-      const int cg = (int)(((e + 1) * G + len - 1) / len) - 1;
+    } else if (t > G) {
+      const int cl = chunk_of(e, len, t);
+      const int cg = chunk_of(e, len, G);
       float acc = 0.f;
       for (int jg = 0; jg < G; ++jg) {
         const int gpu = (cg + jg) % G;
@@ -557,6 +563,16 @@ static void fold_gradients(oracle_t* o) {
         acc = jg == 0 ? loc : loc + acc;
       }
       o->grad_sum[e] = acc;
+    } else {
+      const int c = chunk_of(e, len, G);
+      float total = 0.f;
+      for (int r = 0; r < t; ++r) {
+        /* ring r member j = GMI r of GPU (r + j) % G */
+        float acc = o->g[((r + c) % G) * t + r].grad[e];
+        for (int j = 1; j < G; ++j) acc = o->g[((r + (c + j) % G) % G) * t + r].grad[e] + acc;
+        total = total + acc;
+      }
+      o->grad_sum[e] = total;
     }
   }
 }

@@ -8,9 +8,11 @@
 // update s (1-based, replay-safe: derived from the device control block):
 //   1. signal: rank r publishes ready[r] = s (release, system scope) once its fold is final;
 //   2. exchange_adam: every CTA waits for ready[q] >= s of all peers, then for its slice of
-//      rank r's shard [P r/G, P (r+1)/G) sums the G published gradients over NVLink in the
-//      leader-ring fold order of the reference (chunk c of the leader ring starts at member c,
-//      reduction.hpp:164-212; oracle/ppo_oracle.c fold_gradients), runs Adam on the shard (Adam
+//      rank r's shard [P r/G, P (r+1)/G) sums the published gradients over NVLink in the fold
+//      order of the strategy Alg. 1 selects for the job layout (reduction.hpp:98-106): HAR =
+//      the leaders' ring over the ranks' K1 folds; MRR = t rings of one GMI per rank, their
+//      results summed into a zero total in ring order (reduction.hpp:255-283); chunk c of every
+//      ring starts at member c (:164-212; oracle/ppo_oracle.c fold_gradients). Runs Adam on the shard (Adam
 //      moments are sharded: each element's m, v live only on its owner) and stores the new
 //      parameter and its bf16 shadow into EVERY rank's window (the all-gather), then bumps every
 //      rank's done counter once (release);
@@ -75,14 +77,27 @@ __global__ void __launch_bounds__(256) exchange_adam_kernel(const ExchangeArgs a
   const long long len = a.hi - a.lo;
   const long long c0 = a.lo + len * blockIdx.x / gridDim.x, c1 = a.lo + len * (blockIdx.x + 1) / gridDim.x;
   for (long long i = c0 + threadIdx.x; i < c1; i += blockDim.x) {
-    // leader-ring fold: chunk cg = the ring chunk holding element i, fold starts at member cg
+    // chunk cg = the ring chunk holding element i; every ring fold starts at member cg
     const int cg = int(((i + 1) * a.G + a.P - 1) / a.P) - 1;
     float acc = 0.f;
-    for (int j = 0; j < a.G; ++j) {
-      int q = cg + j;
-      q -= q >= a.G ? a.G : 0;
-      const float x = a.pub[q][i];
-      acc = j == 0 ? x : __fadd_rn(x, acc);
+    if (!a.mrr) {  // HAR leader ring (or one rank): the ranks' K1 folds in ring order
+      for (int j = 0; j < a.G; ++j) {
+        int q = cg + j;
+        q -= q >= a.G ? a.G : 0;
+        const float x = a.pub[q][i];
+        acc = j == 0 ? x : __fadd_rn(x, acc);
+      }
+    } else {  // MRR: ring r = GMI r of ranks r, r+1, ...; ring results into a zero total in ring order
+      for (int r = 0; r < a.t; ++r) {
+        float ring = 0.f;
+        for (int j = 0; j < a.G; ++j) {
+          int q = r + cg + j;
+          q %= a.G;
+          const float x = a.gpub[q][r][i];
+          ring = j == 0 ? x : __fadd_rn(x, ring);
+        }
+        acc = __fadd_rn(acc, ring);
+      }
     }
     const float g = __fmul_rn(acc, a.inv_n);
     const float m = __fadd_rn(__fmul_rn(a.b1, a.m[i]), __fmul_rn(ob1, g));

@@ -99,8 +99,12 @@ struct SegAdam {
 
 // Cross-GPU exchange + sharded Adam over peer memory (cuda/exchange.cu).
 constexpr int kMaxRanks = 8;
+constexpr int kMaxLocalGmis = 16;
 struct ExchangeArgs {
+  int mrr;                               // 0: leader ring over pub (HAR / one rank), 1: MRR over gpub
+  int t;                                 // GMIs per rank (MRR)
   const float* pub[kMaxRanks];           // each rank's published (K1-folded) gradient
+  const float* gpub[kMaxRanks][kMaxLocalGmis];  // MRR: each rank's per-GMI gradients
   float* params[kMaxRanks];              // each rank's fp32 master parameters
   __nv_bfloat16* shadow[kMaxRanks];      // each rank's bf16 shadow
   unsigned long long* ready[kMaxRanks];  // each rank's "gradient of step s published" flag

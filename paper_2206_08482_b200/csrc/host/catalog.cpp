@@ -74,14 +74,28 @@ const std::vector<MigShape>& mig_table() {
   return t;
 }
 
+// B200 extension of topology.hpp:37-43: the MIG profiles NVIDIA publishes for the 180 GB B200
+// (7 compute slices, 8 memory slices of ~22.5 GB; label sizes). Units count compute slices in
+// the reference's 8-unit model with one unit reserved (topology.hpp:34-35), so the same
+// "7 usable units" rule applies; B200 adds the memory-slice budget (8) that the A100-40GB
+// table never needed (every A100 profile there has memory slices == compute units + 0..1).
+const std::vector<MigShape>& mig_table_sm100() {
+  static const std::vector<MigShape> t = {{"1g.23gb", 1, 23.0}, {"1g.45gb", 1, 45.0}, {"2g.45gb", 2, 45.0},
+                                          {"3g.90gb", 3, 90.0}, {"4g.90gb", 4, 90.0}, {"7g.180gb", 7, 180.0}};
+  return t;
+}
+
+int mig_memory_slices_sm100(double mem_gb) { return int(mem_gb / 22.5 + 0.5); }
+
 const MigShape* mig_by_name(const std::string& name) {
-  for (const auto& s : mig_table())
-    if (name == s.name) return &s;
+  for (const auto* tab : {&mig_table(), &mig_table_sm100()})
+    for (const auto& s : *tab)
+      if (name == s.name) return &s;
   return nullptr;
 }
 
-static const MigShape* mig_by_shape(double share, double mem) {
-  for (const auto& s : mig_table())
+static const MigShape* mig_by_shape(double share, double mem, Arch arch) {
+  for (const auto& s : arch == Arch::SM100 ? mig_table_sm100() : mig_table())
     if (std::abs(share - double(s.units) / 8.0) < 1e-9 && std::abs(mem - s.mem_gb) < 1e-9) return &s;
   return nullptr;
 }
@@ -145,10 +159,6 @@ std::vector<std::pair<int, std::string>> check_machine(const Machine& m) {
       }
     }
     if (!fields) continue;
-    if (be == Backend::MIG && gpu.arch == Arch::SM100) {  // B200 extension (reference stops at sm80)
-      flag(gid, "MIG profiles not modelled for sm100: use backend=mps (SM-partitioned green contexts)");
-      continue;
-    }
     if (be == Backend::MIG) {
       if (gpu.arch == Arch::SM70) {
         flag(gid, "MIG unavailable on sm70 (only MPS)");
@@ -158,20 +168,23 @@ std::vector<std::pair<int, std::string>> check_machine(const Machine& m) {
         flag(gid, "MIG profiles require an 8-unit GPU");
         continue;
       }
-      int units = 0;
+      int units = 0, mem_slices = 0;
       bool shapes = true;
       for (const auto* p : parts) {
-        const MigShape* s = mig_by_shape(p->sm_share, p->mem_gb);
+        const MigShape* s = mig_by_shape(p->sm_share, p->mem_gb, gpu.arch);
         if (!s) {
           flag(gid, "gmi " + std::to_string(p->gmi_id) + " not an allowed MIG profile");
           shapes = false;
           continue;
         }
         units += s->units;
+        mem_slices += mig_memory_slices_sm100(s->mem_gb);
       }
       const int usable = gpu.arch == Arch::SM70 ? gpu.sm_units : gpu.sm_units - 1;
       if (shapes && units > usable)
         flag(gid, "exceeds 7 usable units (" + std::to_string(units) + "/8 allocated)");
+      if (shapes && gpu.arch == Arch::SM100 && mem_slices > 8)
+        flag(gid, "exceeds 8 memory slices (" + std::to_string(mem_slices) + "/8 allocated)");
     } else {
       double sum = 0;
       for (const auto* p : parts) sum += p->sm_share;

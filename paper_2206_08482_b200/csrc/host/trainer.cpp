@@ -262,6 +262,15 @@ void Trainer::init(const void* nccl_id) {
     invalid("decoupled mode needs the fused rollout and value pass (hidden widths <= 256, <= 4 layers)");
   ensure_bias_table(1 << 20);
   if (xchg_) {
+    // Alg. 1 on the job layout (GPU-major ids, t per GPU) decides the cross-GPU fold order
+    plan::Placement job;
+    job.per_gpu.resize(cfg.num_gpus);
+    for (int q = 0, id = 0; q < cfg.num_gpus; ++q)
+      for (int j = 0; j < n_local_; ++j) job.per_gpu[q].push_back(id++);
+    strategy_ = plan::choose_algo(job);
+    if (n_local_ > ppo::kMaxLocalGmis) invalid("peer exchange supports up to 16 GMIs per GPU");
+    xa_.mrr = strategy_ == plan::Algo::MRR ? 1 : 0;
+    xa_.t = n_local_;
     xa_.G = cfg.num_gpus;
     xa_.rank = cfg.rank;
     xa_.P = geo_.P;
@@ -342,8 +351,11 @@ void Trainer::alloc() {
     return p;
   };
   const long long P = geo_.P;
-  if (xchg_) {  // exchange window: [flags 256 B | pub P fp32 | params P fp32 | shadow P bf16]
-    win_off_params_ = 256 + (size_t)P * 4;
+  if (xchg_) {
+    // exchange window: [flags 256 B | fold P fp32 | t GMI gradients P fp32 | params P fp32 |
+    // shadow P bf16]; peers read the fold (HAR) or the GMI gradients (MRR)
+    win_off_gmi_ = 256 + (size_t)P * 4;
+    win_off_params_ = win_off_gmi_ + (size_t)n_local_ * P * 4;
     win_off_shadow_ = win_off_params_ + (size_t)P * 4;
     win_ = static_cast<char*>(dev(win_off_shadow_ + (size_t)P * 2));
     grad_sum_ = reinterpret_cast<float*>(win_ + 256);
@@ -412,8 +424,9 @@ void Trainer::alloc() {
     g.Gpi = static_cast<__nv_bfloat16*>(dev((long long)g.Bm * ppo::kHeadG * 2));
     g.Gv = static_cast<__nv_bfloat16*>(dev((long long)g.Bm * ppo::kHeadG * 2));
     for (int n = 0; n < 2; ++n) g.outh[n] = static_cast<float*>(dev((long long)g.Mrows * ppo::kHeadG * 4));
-    // peer exchange with one GMI: its assembled gradient is the published one (no K1 fold)
-    g.grad = xchg_ && n_local_ == 1 ? grad_sum_ : static_cast<float*>(dev(P * 4));
+    // peer exchange: GMI gradients live in the exchange window (MRR reads them remotely)
+    g.grad = xchg_ ? reinterpret_cast<float*>(win_ + win_off_gmi_ + (size_t)g.local * P * 4)
+                   : static_cast<float*>(dev(P * 4));
     g.head_part = static_cast<float*>(dev((long long)ppo::head_loss_blocks(g.Bm) * ppo::head_partial_stride(A) * 4));
   }
 }
@@ -1217,7 +1230,7 @@ void Trainer::train_minibatch(Gmi& g, int k, int adam_step) {
 void Trainer::reduce_and_step(int step_in_iter) {
   for (auto& g : gmis_) GMI_CUDA_CHECK(cudaStreamWaitEvent(upd_, g->ev_done, 0));
   float* src = gmis_[0]->grad;
-  if (n_local_ > 1) {  // K1: fold the GMIs' gradients in the layout's ring order (one GPU: MPR)
+  if (n_local_ > 1 && !(xchg_ && xa_.mrr)) {  // K1: fold the GPU's GMIs in ring order (MPR / HAR step 1)
     plan::Placement p;
     p.per_gpu.resize(1);
     std::vector<void*> bufs;
@@ -1243,9 +1256,10 @@ void Trainer::reduce_and_step(int step_in_iter) {
     a.b2 = cfg_.beta2;
     a.eps = cfg_.adam_eps;
     a.inv_n = 1.0f / float(n_total_);
-    // per rank and update: G x 4 B read per shard element, 6 B written per element per replica
-    const double shard = double(xa_.hi - xa_.lo);
-    timed(upd_, GMI_PH_ALLREDUCE, 0.0, shard * (4.0 * cfg_.num_gpus + 16.0 + 6.0 * cfg_.num_gpus),
+    // per rank and update and shard element: G (HAR) or G x t (MRR) 4-byte reads, Adam's m / v /
+    // p (16 B), 6 B written per replica
+    const double shard = double(xa_.hi - xa_.lo), reads = cfg_.num_gpus * (xa_.mrr ? n_local_ : 1);
+    timed(upd_, GMI_PH_ALLREDUCE, 0.0, shard * (4.0 * reads + 16.0 + 6.0 * cfg_.num_gpus),
           [&] { ppo::launch_exchange_adam(a, upd_); });
     launches_ += 3;
     GMI_CUDA_CHECK(cudaEventRecord(ev_adam_, upd_));
@@ -1434,7 +1448,9 @@ void Trainer::comm_attach(const void* handles) {
     }
     xa_.ready[q] = reinterpret_cast<unsigned long long*>(base);
     xa_.done[q] = reinterpret_cast<unsigned long long*>(base + 128);
-    xa_.pub[q] = reinterpret_cast<const float*>(base + 256);
+    xa_.pub[q] = reinterpret_cast<const float*>(n_local_ == 1 ? base + win_off_gmi_ : base + 256);
+    for (int j = 0; j < n_local_; ++j)
+      xa_.gpub[q][j] = reinterpret_cast<const float*>(base + win_off_gmi_ + (size_t)j * geo_.P * 4);
     xa_.params[q] = reinterpret_cast<float*>(base + win_off_params_);
     xa_.shadow[q] = reinterpret_cast<__nv_bfloat16*>(base + win_off_shadow_);
   }
@@ -1445,7 +1461,8 @@ void Trainer::comm_connect(Trainer* const* t, int n) {
   if (n < 1 || n > ppo::kMaxRanks) invalid("gmi_ppo_comm_connect: 1..8 trainers");
   for (int r = 0; r < n; ++r) {
     if (!t[r] || !t[r]->xchg_) invalid("gmi_ppo_comm_connect: every trainer needs comm = 1");
-    if (t[r]->cfg_.rank != r || t[r]->cfg_.num_gpus != n || t[r]->geo_.P != t[0]->geo_.P)
+    if (t[r]->cfg_.rank != r || t[r]->cfg_.num_gpus != n || t[r]->geo_.P != t[0]->geo_.P ||
+        t[r]->n_local_ != t[0]->n_local_)
       invalid("gmi_ppo_comm_connect: trainers[r] must be rank r of one num_gpus = n job");
     if (t[r]->connected_) invalid("gmi_ppo_comm_connect: already wired");
   }
@@ -1461,7 +1478,8 @@ void Trainer::comm_connect(Trainer* const* t, int n) {
       }
       me.xa_.ready[q] = reinterpret_cast<unsigned long long*>(peer.win_);
       me.xa_.done[q] = reinterpret_cast<unsigned long long*>(peer.win_ + 128);
-      me.xa_.pub[q] = peer.grad_sum_;
+      me.xa_.pub[q] = peer.n_local_ == 1 ? peer.gmis_[0]->grad : peer.grad_sum_;
+      for (int j = 0; j < peer.n_local_; ++j) me.xa_.gpub[q][j] = peer.gmis_[j]->grad;
       me.xa_.params[q] = peer.params_;
       me.xa_.shadow[q] = peer.shadow_;
     }

@@ -14,6 +14,7 @@
 #include "../cuda/gemm_host.hpp"
 #include "../cuda/ppo.cuh"
 #include "gmi.h"
+#include "planner.hpp"
 
 namespace gmi {
 
@@ -105,7 +106,8 @@ class Trainer {
   bool xchg_ = false;
   bool connected_ = false;
   char* win_ = nullptr;
-  size_t win_off_params_ = 0, win_off_shadow_ = 0;
+  size_t win_off_gmi_ = 0, win_off_params_ = 0, win_off_shadow_ = 0;
+  plan::Algo strategy_ = plan::Algo::MPR;  // Alg. 1 on the job layout (cross-GPU fold order)
   ppo::ExchangeArgs xa_{};
   std::vector<void*> ipc_opened_;
   void* gemm_trace_ = nullptr;  // GMI_GEMM_TRACE development aid

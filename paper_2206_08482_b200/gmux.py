@@ -241,6 +241,10 @@ class TaskMode(enum.IntEnum):
 
 MIG_PROFILES = {"1g.5gb": (1, 5.0), "2g.10gb": (2, 10.0), "3g.20gb": (3, 20.0),
                 "4g.20gb": (4, 20.0), "7g.40gb": (7, 40.0)}
+# B200 (sm100, 180 GB) profiles as NVIDIA publishes them (compute slices of 7, label memory):
+# host/catalog.cpp mig_table_sm100; validate_layout also checks the 8 memory slices.
+MIG_PROFILES.update({"1g.23gb": (1, 23.0), "1g.45gb": (1, 45.0), "2g.45gb": (2, 45.0), "3g.90gb": (3, 90.0),
+                     "4g.90gb": (4, 90.0), "7g.180gb": (7, 180.0)})
 
 
 @dataclass

@@ -1,9 +1,10 @@
 """the topology extension for B200 (reference enum stops at sm80,
 topology.hpp:20). MPS shares on an sm100 GPU are realised as SM-partitioned green contexts in
 whole 8-SM groups (cuDevSmResourceSplitByCount granularity, cuda.h:25262); validate_layout
-flags shares below one group and MIG partitions on sm100 (no B200 MIG profile table is
-modelled: MIG mode is disabled on the pool's B200s, `nvidia-smi mig -lgip` lists none). The
-sm70 / sm80 rules stay the reference's (tests/test_planner_golden.py)."""
+flags shares below one group. MIG partitions on sm100 are checked against NVIDIA's published
+B200 180 GB profile table (MIG mode is disabled on the pool's B200s, so the table cannot be
+probed with `nvidia-smi mig -lgip` there). The sm70 / sm80 rules stay the reference's
+(tests/test_planner_golden.py)."""
 import os
 
 from paper_2206_08482_b200 import gmux
@@ -35,9 +36,21 @@ def test_sm100_share_below_one_group_is_a_violation():
     assert len(v) == 1 and v[0].gpu_id == 0 and "8-SM green-context group" in v[0].rule
 
 
-def test_sm100_mig_is_a_violation_but_sm80_mig_is_the_reference_rule():
+def test_sm100_mig_profiles():
+    """B200 MIG table (NVIDIA's 180 GB profiles): 7 usable compute slices, 8 memory slices;
+    A100 profiles are not B200 profiles; sm80 keeps the reference table."""
+    ok = [gmux.mig_partition(0, 0, "3g.90gb"), gmux.mig_partition(1, 0, "3g.90gb")]
+    assert gmux.validate_layout(_b200(ok)) == []
+    seven = [gmux.mig_partition(i, 0, "1g.23gb") for i in range(7)]
+    assert gmux.validate_layout(_b200(seven)) == []
+    v = gmux.validate_layout(_b200(seven + [gmux.mig_partition(7, 0, "1g.23gb")]))
+    assert len(v) == 1 and "exceeds 7 usable units" in v[0].rule
+    mem = [gmux.mig_partition(0, 0, "4g.90gb"), gmux.mig_partition(1, 0, "1g.45gb"),
+           gmux.mig_partition(2, 0, "1g.45gb"), gmux.mig_partition(3, 0, "1g.23gb")]
+    v = gmux.validate_layout(_b200(mem))
+    assert len(v) == 1 and "exceeds 8 memory slices" in v[0].rule
     v = gmux.validate_layout(_b200([gmux.mig_partition(0, 0, "3g.20gb")]))
-    assert len(v) == 1 and "not modelled for sm100" in v[0].rule
+    assert len(v) == 1 and "not an allowed MIG profile" in v[0].rule
     a100 = gmux.Topology([gmux.GpuSpec(0, gmux.GpuArch.SM80, 8, 40.0)], [gmux.mig_partition(0, 0, "3g.20gb")])
     assert gmux.validate_layout(a100) == []
 
