@@ -399,6 +399,19 @@ GMI_API int gmi_ppo_iteration(void* trainer, gmi_ppo_stats_t* stats);
 /* Asynchronous variant: enqueue one iteration on the trainer's streams, no host sync. */
 GMI_API int gmi_ppo_iteration_async(void* trainer);
 GMI_API int gmi_ppo_synchronize(void* trainer, gmi_ppo_stats_t* stats);
+/* Adaptive GMI manager (search.hpp:32-37): re-split the green-context SM
+ * partitions of a live trainer (gmi_backend = 1). `gpu` is the trainer's rank; sm_counts[t]
+ * gives each GMI's SMs (multiples of 8; decoupled: {serving, trainer}, one entry may be 0 =
+ * the rest). Buffers, parameters and optimizer state stay; streams, GEMM plans and the
+ * iteration graph are rebuilt. t must equal the trainer's GMI count. */
+GMI_API int gmi_resize(void* trainer, int gpu, const int* sm_counts, int t);
+/* Per-role SM-share retuning from measured throughput: for each candidate split
+ * (candidates[c * t .. c * t + t), t = the trainer's GMI count, decoupled: {serving, trainer})
+ * resize, run `iters` timed iterations (after one eager and one capture iteration) and record
+ * env-steps/s in throughput[c]; the trainer is left at the best split (*best). Training
+ * continues through the probe iterations (they are real updates). */
+GMI_API int gmi_ppo_tune_shares(void* trainer, const int* candidates, int ncand, int iters, int* best,
+                                double* throughput);
 /* Peer exchange wiring (cfg.comm = 1). gmi_ppo_comm_handle: the 64-byte CUDA IPC handle of this
  * rank's exchange window (flags, published gradient, fp32 parameters, bf16 shadow); every rank
  * gathers all handles in rank order (e.g. torch.distributed all_gather_object) and passes the

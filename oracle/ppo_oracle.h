@@ -6,9 +6,9 @@
  * This restatement is therefore pinned by (1) the reference's shape contracts (param
  * counts, workload.hpp:95-100), (2) the reference's partition rule for env -> GMI
  * ([N*c/n, N*(c+1)/n), reduction.hpp:164-166) and fold order for the gradient sum
- * (reduction.hpp:170-212), and (3) torch-CPU autograd fixtures for the MLP / loss /
- * Adam pieces (tests/golden/gen_ppo_golden.py). Env dynamics, seeds and PPO
- * hyper-parameters are builder-pinned.
+ * (reduction.hpp:170-212), and (3) torch-CPU autograd / torch.optim.Adam / bf16 rounding
+ * checks of the MLP / loss / Adam pieces, run live in tests/test_ppo_oracle.py. Env
+ * dynamics, seeds and PPO hyper-parameters are builder-pinned.
  */
 #ifndef PPO_ORACLE_H_
 #define PPO_ORACLE_H_

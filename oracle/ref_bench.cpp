@@ -1,7 +1,7 @@
 // TEST INFRASTRUCTURE ONLY — times the reference's own execute() (reduction.hpp:225-334,
 // single-threaded C++ as shipped) on the BASELINE layouts at the real gradient lengths.
-// Compiled in place against /root/reference by oracle/Makefile; used by tests/bench as the
-// CPU baseline of the inter-GMI gradient reduction step. Prints one JSON object per line.
+// Compiled in place against /root/reference by oracle/Makefile; bench.py's cpu_baseline leg
+// (reduction_vs_reference) times it beside K1 on the same layouts. One JSON object per line.
 #include <chrono>
 #include <cstdio>
 #include <string>

@@ -6,8 +6,9 @@
 // published gradient (its GMIs' K1 fold), the fp32 master parameters and their bf16 shadow --
 // mapped into every peer (CUDA IPC across processes, plain pointers inside one process). Per
 // update s (1-based, replay-safe: derived from the device control block):
-//   1. signal: rank r publishes ready[r] = s (release, system scope) once its fold is final;
-//   2. exchange_adam: every CTA waits for ready[q] >= s of all peers, then for its slice of
+//   1. signal: rank r publishes ready[r] = s (release, system scope) once its fold is final,
+//      and one warp waits until every peer's ready[q] >= s;
+//   2. exchange_adam: for its slice of
 //      rank r's shard [P r/G, P (r+1)/G) sums the published gradients over NVLink in the fold
 //      order of the strategy Alg. 1 selects for the job layout (reduction.hpp:98-106): HAR =
 //      the leaders' ring over the ranks' K1 folds; MRR = t rings of one GMI per rank, their
@@ -55,21 +56,26 @@ __device__ __forceinline__ long long step_id(const ExchangeArgs& a) {
   return a.ctl->adam_step0 + a.step_in_iter + 1;  // 1-based, consecutive over the job
 }
 
-__global__ void exchange_signal_kernel(const ExchangeArgs a) {
+// One warp: publish this rank's readiness, then wait for every peer's. The waiting happens
+// here, in a single small CTA, and never in the wide exchange kernel: a spinning CTA holds an
+// SM slot, and ranks that share a GPU (tests, or several ranks per device) must leave room for
+// the peers' persistent GEMMs to finish the gradients being waited for.
+__global__ void __launch_bounds__(32) exchange_signal_kernel(const ExchangeArgs a) {
   pdl_trigger();
   pdl_wait();  // the fold that produced pub[rank] has completed (device scope)
+  const long long s = step_id(a);
   if (threadIdx.x == 0) {
     __threadfence_system();
-    st_release_sys(a.ready[a.rank], (unsigned long long)step_id(a));
+    st_release_sys(a.ready[a.rank], (unsigned long long)s);
   }
+  if (int(threadIdx.x) < a.G) spin_until(a.ready[threadIdx.x], (unsigned long long)s);
+  __syncwarp();
 }
 
 __global__ void __launch_bounds__(256) exchange_adam_kernel(const ExchangeArgs a) {
   pdl_trigger();
-  pdl_wait();
+  pdl_wait();  // exchange_signal_kernel completed: every peer's gradient of this step is published
   const long long s = step_id(a);
-  if (threadIdx.x < a.G) spin_until(a.ready[threadIdx.x], (unsigned long long)s);
-  __syncthreads();
   const long long st = s - 1;  // completed updates before this one (bias-correction index)
   const float bc1 = a.bc[2 * st], bc2 = a.bc[2 * st + 1];
   const float ob1 = __fsub_rn(1.0f, a.b1), ob2 = __fsub_rn(1.0f, a.b2);
@@ -84,7 +90,7 @@ __global__ void __launch_bounds__(256) exchange_adam_kernel(const ExchangeArgs a
       for (int j = 0; j < a.G; ++j) {
         int q = cg + j;
         q -= q >= a.G ? a.G : 0;
-        const float x = a.pub[q][i];
+        const float x = __ldcg(a.pub[q] + i);  // peer memory: L2 of the owner, never a stale L1 line
         acc = j == 0 ? x : __fadd_rn(x, acc);
       }
     } else {  // MRR: ring r = GMI r of ranks r, r+1, ...; ring results into a zero total in ring order
@@ -93,7 +99,7 @@ __global__ void __launch_bounds__(256) exchange_adam_kernel(const ExchangeArgs a
         for (int j = 0; j < a.G; ++j) {
           int q = r + cg + j;
           q %= a.G;
-          const float x = a.gpub[q][r][i];
+          const float x = __ldcg(a.gpub[q][r] + i);
           ring = j == 0 ? x : __fadd_rn(x, ring);
         }
         acc = __fadd_rn(acc, ring);
@@ -113,17 +119,18 @@ __global__ void __launch_bounds__(256) exchange_adam_kernel(const ExchangeArgs a
     }
   }
   __syncthreads();
-  if (threadIdx.x < a.G) {
+  if (int(threadIdx.x) < a.G) {
     __threadfence_system();
     red_add_release_sys(a.done[threadIdx.x], 1ull);
   }
 }
 
-__global__ void exchange_wait_kernel(const ExchangeArgs a) {
+__global__ void __launch_bounds__(32) exchange_wait_kernel(const ExchangeArgs a) {
   pdl_trigger();
   pdl_wait();
-  if (threadIdx.x == 0) spin_until(a.done[a.rank], (unsigned long long)step_id(a) * (unsigned long long)(a.G * a.ctas));
-  __syncthreads();
+  if (threadIdx.x == 0)
+    spin_until(a.done[a.rank], (unsigned long long)step_id(a) * (unsigned long long)(a.G * a.ctas));
+  __syncwarp();
 }
 
 }  // namespace

@@ -1,8 +1,9 @@
 // Experience-channel accounting for the decoupled mode (config 4): agents emit
 // records at the serving cadence, records are grouped k at a time into three channel
 // transfer units, routed to a same-GPU trainer or the least-loaded one, batched and
-// consumed. Reference behaviour: channels.hpp:93-397. The device-side channel ring
-// buffers are in cuda/channels.cu; this module is the host-side accounting model.
+// consumed. Reference behaviour: channels.hpp:93-397. This module is the host-side
+// accounting model; the device-side experience hand-off of the decoupled trainer is in
+// host/trainer.cpp (serve_rollout / record_iteration).
 #include <algorithm>
 #include <cmath>
 #include <optional>

@@ -1,6 +1,6 @@
 // Adaptive GMI manager (Alg. 2): saturation-pruned sweep over (GMIs per GPU,
 // num_env) behind a pluggable probe. Reference behaviour: search.hpp:45-249.
-// The probe is where the measured B200 iteration plugs in (runtime/profiler.cpp).
+// The probe is where the measured B200 iteration plugs in (host/gpu_profiler.cpp).
 #include <cmath>
 #include <fstream>
 #include <limits>

@@ -333,6 +333,8 @@ void Trainer::release() noexcept {
   upd_ = nullptr;
   for (void* p : allocs_) cudaFree(p);
   allocs_.clear();
+  for (void* p : plan_allocs_) cudaFree(p);
+  plan_allocs_.clear();
   if (ctl_host_) cudaFreeHost(ctl_host_);
   if (stats_host_) cudaFreeHost(stats_host_);
   ctl_host_ = nullptr;
@@ -461,15 +463,19 @@ void Trainer::build_plans() {
   // Kernel-written scratch (slabs, partial rows). GMI_POISON=1 fills it with NaN bytes so a
   // read-before-write shows up in the parity tests instead of depending on allocator history.
   const char* poison = std::getenv("GMI_POISON");
+  // plan scratch depends on the GMIs' SM counts: a rebuild (gmi_resize) frees the previous set
+  for (void* p : plan_allocs_) cudaFree(p);
+  plan_allocs_.clear();
   auto dev = [&](size_t bytes) {
     void* p = nullptr;
     GMI_CUDA_CHECK(cudaMalloc(&p, std::max<size_t>(bytes, 256)));
     if (poison && poison[0] == '1') GMI_CUDA_CHECK(cudaMemset(p, 0xFF, std::max<size_t>(bytes, 256)));
-    allocs_.push_back(p);
+    plan_allocs_.push_back(p);
     return static_cast<float*>(p);
   };
   for (auto& gp : gmis_) {
     Gmi& g = *gp;
+    g.segs.clear();
     const long long rollrows = (long long)(T_ + 1) * g.N;
     for (int l = 0; l < L; ++l) {
       const int in_p = geo_.wp[l], out_p = geo_.wp[l + 1];
@@ -1423,6 +1429,36 @@ void Trainer::record_iteration(bool with_rollout) {
   ++launches_;
 }
 
+// gmi_resize: re-split this GPU's green-context partitions on a live trainer. Env state,
+// experience, parameters, optimizer state and the exchange window stay where they are; the
+// streams move to the new partitions and the GEMM plans (split-K / tile choices depend on each
+// GMI's SM count) and the iteration graph are rebuilt. The GMI count is fixed (changing it
+// re-partitions the envs over GMIs, which is a new trainer).
+void Trainer::resize(const int* sms, int n) {
+  if (!exec_ || exec_->backend() != 1)
+    invalid("gmi_resize: SM shares exist only for green-context GMIs (gmi_backend = 1)");
+  const int units = decoupled_ ? 2 : n_local_;
+  if (n != units)
+    invalid("gmi_resize: t = " + std::to_string(n) + " but this GPU runs " + std::to_string(units) +
+            " GMIs (changing the count re-partitions the envs; create a new trainer)");
+  GMI_CUDA_CHECK(cudaSetDevice(cfg_.device));
+  GMI_CUDA_CHECK(cudaDeviceSynchronize());
+  auto fresh = std::make_unique<GmiResources>(cfg_.device, std::vector<int>(sms, sms + n), 1);  // validates
+  if (graph_) GMI_CUDA_CHECK(cudaGraphExecDestroy(graph_));
+  graph_ = nullptr;
+  exec_ = std::move(fresh);  // the old partitions (and their streams) are released here
+  const int tix = decoupled_ ? 1 : 0;
+  if (decoupled_) serve_s_ = exec_->stream(0);
+  if (upd_in_gmi_) upd_ = exec_->extra_stream(1);
+  for (auto& g : gmis_) {
+    g->s = exec_->stream(tix + g->local);
+    g->s2 = exec_->aux_stream(tix + g->local);
+    g->ctas = exec_->sm_count(tix + g->local);
+  }
+  build_plans();
+  GMI_CUDA_CHECK(cudaDeviceSynchronize());
+}
+
 void Trainer::comm_handle(void* out64) const {
   if (!xchg_) invalid("gmi_ppo_comm_handle: the trainer was not created with comm = 1");
   cudaIpcMemHandle_t h;
@@ -1760,6 +1796,55 @@ GMI_API int gmi_ppo_iteration_async(void* t) {
 
 GMI_API int gmi_ppo_synchronize(void* t, gmi_ppo_stats_t* st) {
   return gmi::guarded([&] { static_cast<gmi::Trainer*>(t)->synchronize(st); });
+}
+
+GMI_API int gmi_resize(void* t, int gpu, const int* sm_counts, int n) {
+  return gmi::guarded([&] {
+    if (!t || !sm_counts) gmi::invalid("null argument");
+    auto* tr = static_cast<gmi::Trainer*>(t);
+    if (gpu != tr->rank()) gmi::invalid("gmi_resize: this trainer drives GPU (rank) " + std::to_string(tr->rank()));
+    tr->resize(sm_counts, n);
+  });
+}
+
+GMI_API int gmi_ppo_tune_shares(void* t, const int* candidates, int ncand, int iters, int* best,
+                                double* throughput) {
+  return gmi::guarded([&] {
+    if (!t || !candidates || ncand < 1 || iters < 1) gmi::invalid("gmi_ppo_tune_shares: bad arguments");
+    auto* tr = static_cast<gmi::Trainer*>(t);
+    const int n = tr->units();
+    cudaEvent_t a, b;
+    GMI_CUDA_CHECK(cudaEventCreate(&a));
+    GMI_CUDA_CHECK(cudaEventCreate(&b));
+    int bi = 0;
+    double bv = -1.0;
+    try {
+      for (int c = 0; c < ncand; ++c) {
+        tr->resize(candidates + (size_t)c * n, n);
+        tr->enqueue_iteration(false);  // eager after a resize (rebuilds the graph on the next call)
+        tr->enqueue_iteration(false);  // capture
+        tr->synchronize(nullptr);
+        GMI_CUDA_CHECK(cudaEventRecord(a, tr->stream(-1)));
+        for (int i = 0; i < iters; ++i) tr->enqueue_iteration(false);
+        GMI_CUDA_CHECK(cudaEventRecord(b, tr->stream(-1)));
+        gmi_ppo_stats_t st;
+        tr->synchronize(&st);
+        float ms = 0.f;
+        GMI_CUDA_CHECK(cudaEventElapsedTime(&ms, a, b));
+        const double v = double(st.env_steps) * iters / (double(ms) / 1e3);
+        if (throughput) throughput[c] = v;
+        if (v > bv) bv = v, bi = c;
+      }
+      tr->resize(candidates + (size_t)bi * n, n);
+    } catch (...) {
+      cudaEventDestroy(a);
+      cudaEventDestroy(b);
+      throw;
+    }
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    if (best) *best = bi;
+  });
 }
 
 GMI_API int gmi_ppo_comm_handle(void* t, void* out64) {

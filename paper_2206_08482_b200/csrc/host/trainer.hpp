@@ -78,6 +78,7 @@ class Trainer {
   std::unique_ptr<GmiResources> exec_;
   std::vector<std::unique_ptr<Gmi>> gmis_;
   std::vector<void*> allocs_;
+  std::vector<void*> plan_allocs_;  // GEMM-plan scratch (rebuilt by resize)
 
   // shared per GPU
   float *params_ = nullptr, *m_ = nullptr, *v_ = nullptr, *grad_sum_ = nullptr, *bc_ = nullptr;
@@ -136,6 +137,9 @@ class Trainer {
 
  public:
   const gmi_ppo_phase_t* phases() const { return phases_; }
+  void resize(const int* sms, int n);  // gmi_resize
+  int rank() const { return cfg_.rank; }
+  int units() const { return decoupled_ ? 2 : n_local_; }  // GMIs with an SM partition
   // peer exchange wiring (gmi_ppo_comm_*)
   void comm_handle(void* out64) const;
   void comm_attach(const void* handles);

@@ -54,6 +54,9 @@ _PROTOS = {
     "gmi_ppo_synchronize": (C.c_int, [C.c_void_p, C.POINTER(PpoStatsT)]),
     "gmi_ppo_rollout": (C.c_int, [C.c_void_p]),
     "gmi_ppo_comm_handle": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "gmi_resize": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_int), C.c_int]),
+    "gmi_ppo_tune_shares": (C.c_int, [C.c_void_p, C.POINTER(C.c_int), C.c_int, C.c_int, C.POINTER(C.c_int),
+                                      C.POINTER(C.c_double)]),
     "gmi_ppo_comm_attach": (C.c_int, [C.c_void_p, C.c_void_p]),
     "gmi_ppo_comm_connect": (C.c_int, [C.POINTER(C.c_void_p), C.c_int]),
     "gmi_ppo_minibatch_grad": (C.c_int, [C.c_void_p, C.c_int] + [C.POINTER(C.c_float)] * 5 +
@@ -238,6 +241,21 @@ class Trainer:
 
     def rollout(self) -> None:
         L.check(L.lib().gmi_ppo_rollout(self._h))
+
+    def resize(self, sm_counts: list) -> None:
+        """Re-split this GPU's green-context partitions (gmi_resize); same GMI count."""
+        arr = (C.c_int * len(sm_counts))(*sm_counts)
+        L.check(L.lib().gmi_resize(self._h, self.cfg.rank, arr, len(sm_counts)))
+
+    def tune_shares(self, candidates: list, iters: int = 3):
+        """Measured per-role SM-share retuning (gmi_ppo_tune_shares): returns (best index,
+        env-steps/s per candidate); the trainer is left at the best split."""
+        flat = [x for c in candidates for x in c]
+        arr = (C.c_int * len(flat))(*flat)
+        out = (C.c_double * len(candidates))()
+        best = C.c_int()
+        L.check(L.lib().gmi_ppo_tune_shares(self._h, arr, len(candidates), iters, C.byref(best), out))
+        return best.value, list(out)
 
     def comm_handle(self) -> bytes:
         """64-byte CUDA IPC handle of this rank's exchange window (cfg.comm = 1)."""

@@ -232,3 +232,96 @@ def test_decoupled_rollout_uses_the_lagged_policy():
     ref2.rollout()                   # rollout 1 with theta_0
     for what in ("rew", "act", "logp", "done"):
         assert np.array_equal(dec.get(what), ref2.get(what)), what
+
+
+def _bf(x):
+    return x.to(torch.bfloat16).to(x.dtype)
+
+
+class _RoundFwd(torch.autograd.Function):
+    """bf16 rounding of a forward value (operands the device stores in bf16); identity backward."""
+
+    @staticmethod
+    def forward(ctx, x):
+        return _bf(x)
+
+    @staticmethod
+    def backward(ctx, g):
+        return g
+
+
+class _RoundBwd(torch.autograd.Function):
+    """Identity forward; bf16 rounding of the incoming gradient (head output grads G_pi / G_v)."""
+
+    @staticmethod
+    def forward(ctx, x):
+        return x.clone()
+
+    @staticmethod
+    def backward(ctx, g):
+        return _bf(g)
+
+
+class _EluBf16(torch.autograd.Function):
+    """Hidden activation as the device computes it: H = bf16(elu(pre)); dPre = bf16(dH * elu'(H)),
+    elu'(H) = H > 0 ? 1 : H + 1 (from the stored bf16 output)."""
+
+    @staticmethod
+    def forward(ctx, pre):
+        h = _bf(torch.nn.functional.elu(pre))
+        ctx.save_for_backward(h)
+        return h
+
+    @staticmethod
+    def backward(ctx, g):
+        (h,) = ctx.saved_tensors
+        return _bf(g * torch.where(h > 0, torch.ones_like(h), h + 1))
+
+
+@pytest.mark.parametrize("dims,B", [([12, 64, 32, 3], 96), ([60, 64, 64, 8], 128), ([23, 96, 64, 64, 9], 64)])
+def test_bf16_mode_gradient_matches_torch_with_the_same_rounding_points(dims, B):
+    """The default (bf16) oracle mode -- the GPU checker -- against torch float64 autograd with bf16
+    rounding at exactly the device's storage points: observations, every weight matrix, hidden
+    activations, pre-activation gradients and head output gradients. Measured agreement ~2e-8
+    relative (float vs double accumulation before a rounding point); bound 1e-5."""
+    S, A, hidden = dims[0], dims[-1], dims[1:-1]
+    o = PpoOracle(make_cfg(S, A, hidden, 16, ent_coef=0.01))
+    lay = param_layout(S, A, hidden)
+    flat = o.get("params").astype(np.float64)
+    rng = np.random.default_rng(B + 1)
+    # observations are stored in bf16 (rollout buffer) before they reach the update
+    X = torch.from_numpy(rng.uniform(-1, 1, (B, S)).astype(np.float32)).bfloat16().float().numpy()
+    act = rng.standard_normal((B, A)).astype(np.float32)
+    oldlp = (rng.standard_normal(B) - 5).astype(np.float32)
+    adv = rng.standard_normal(B).astype(np.float32)
+    ret = rng.standard_normal(B).astype(np.float32)
+    grad, stats = o.minibatch(X, act, oldlp, adv, ret)
+
+    nets, log_std = _torch_nets(flat, lay, len(hidden))
+    T = lambda a: torch.tensor(a, dtype=torch.float64)
+
+    def fwd(layers, x):
+        x = _RoundFwd.apply(x)
+        for W, b in layers[:-1]:
+            x = _EluBf16.apply(x @ _RoundFwd.apply(W).T + b)
+        W, b = layers[-1]
+        return _RoundBwd.apply(x @ _RoundFwd.apply(W).T) + b  # bias gradient from the unrounded G
+
+    mu = fwd(nets[0], T(X))
+    v = fwd(nets[1], T(X))[:, 0]
+    dist = torch.distributions.Normal(mu, log_std.exp())
+    lp = dist.log_prob(T(act)).sum(-1)
+    ratio = torch.exp(lp - T(oldlp))
+    s1, s2 = ratio * T(adv), torch.clamp(ratio, 0.8, 1.2) * T(adv)
+    loss = -torch.min(s1, s2).mean() + 0.5 * ((v - T(ret)) ** 2).mean() - 0.01 * dist.entropy().sum(-1).mean()
+    loss.backward()
+    for n in range(2):
+        for l, (W, b) in enumerate(nets[n]):
+            t = lay[(n, l)]
+            gw = grad[t["w"]:t["w"] + t["out_p"] * t["in_p"]].reshape(t["out_p"], t["in_p"])[:t["out"], :t["inp"]]
+            ref = W.grad.numpy()
+            assert np.linalg.norm(gw - ref) <= 1e-5 * np.linalg.norm(ref), (n, l)
+            gb, rb = grad[t["b"]:t["b"] + t["out"]], b.grad.numpy()
+            assert np.linalg.norm(gb - rb) <= 1e-5 * np.linalg.norm(rb) + 1e-9, (n, l, "b")
+    gl = grad[lay["log_std"]:lay["log_std"] + A]
+    np.testing.assert_allclose(gl, log_std.grad.numpy(), rtol=1e-5, atol=1e-7)
