@@ -44,6 +44,8 @@ def parse():
     p.add_argument("--decoupled", type=int, default=None,
                    help="1: serving GMI + trainer GMI per GPU with an experience channel (BASELINE config 4)")
     p.add_argument("--serving-sms", type=int, default=0, help="SMs of the serving GMI (decoupled mode)")
+    p.add_argument("--comm", default="peer", choices=["peer", "nccl"],
+                   help="cross-GPU step (N > 1): fused peer exchange over NVLink (default) or ncclAllReduce")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-multi-gmi", action="store_true",
                    help="skip the decoupled multi-GMI layout measured beside the single-context one")
@@ -359,14 +361,8 @@ def time_trainer(cfg, steps, warmup, world, barrier, instrument=True):
     for the per-unit (per-GMI) busy time. Returns (value, ms_per_step, units, trainer stats)."""
     import torch
     import torch.distributed as dist
-    from paper_2206_08482_b200.ppo import Trainer, nccl_unique_id
 
-    nid = None
-    if world > 1:
-        obj = [nccl_unique_id() if cfg.rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        nid = obj[0]
-    t = Trainer(cfg, nid)
+    t = make_trainer(cfg, world, cfg.rank)
     upd = torch.cuda.ExternalStream(t.stream(-1))
     for _ in range(max(3, warmup)):
         t.iteration()
@@ -397,6 +393,26 @@ def time_trainer(cfg, steps, warmup, world, barrier, instrument=True):
     return value, ms.item() / steps, units
 
 
+def make_trainer(cfg, world, rank):
+    """One rank's trainer. N > 1: the peer exchange is wired over CUDA IPC (every rank's window
+    handle gathered through torch.distributed), or an NCCL communicator with --comm nccl."""
+    import torch.distributed as dist
+    from paper_2206_08482_b200.ppo import Trainer, nccl_unique_id
+
+    if world == 1:
+        return Trainer(cfg)
+    if cfg.comm == 1:
+        t = Trainer(cfg)
+        handles = [None] * world
+        dist.all_gather_object(handles, t.comm_handle())
+        t.comm_attach(handles)
+        dist.barrier()
+        return t
+    obj = [nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    return Trainer(cfg, obj[0])
+
+
 def unit_report(busy, it_ms, decoupled):
     names = (["serving GMI (simulator+agent)", "trainer GMI"] if decoupled else
              [f"GMI {i}" for i in range(len(busy) - 1)]) + ["update stream (K1 fold + Adam)"]
@@ -417,7 +433,7 @@ def main():
 
     import torch
     import torch.distributed as dist
-    from paper_2206_08482_b200.ppo import PpoConfig, Trainer, nccl_unique_id
+    from paper_2206_08482_b200.ppo import PpoConfig
 
     w = workload_of(args.config, args.envs)
     w["path"] = args.config
@@ -441,12 +457,8 @@ def main():
     if args.backend is not None:
         cfg.gmi_backend = args.backend
     cfg.instrument = 0  # timed loop runs the plain graph; a separate pass below is instrumented
-    nid = None
-    if world > 1:
-        obj = [nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        nid = obj[0]
-    trainer = Trainer(cfg, nid)
+    cfg.comm = 1 if args.comm == "peer" else 0
+    trainer = make_trainer(cfg, world, rank)
     upd = torch.cuda.ExternalStream(trainer.stream(-1))
 
     def barrier():
@@ -528,7 +540,9 @@ def main():
                   if not cfg.decoupled else
                   f"decoupled: serving GMI ({cfg.serving_sms or 16} SMs, simulator+agent) + trainer GMI per B200, "
                   f"device experience channel, one-iteration policy lag")
-        run = {"layout": layout, "gmis_per_gpu": cfg.gmis_per_gpu + (1 if cfg.decoupled else 0),
+        run = {"layout": layout, "comm": (["ncclAllReduce", "peer exchange (fused RS + sharded Adam + AG)"]
+                                          [cfg.comm] if world > 1 else "none (one GPU)"),
+               "gmis_per_gpu": cfg.gmis_per_gpu + (1 if cfg.decoupled else 0),
                "gmi_backend": ["streams", "green_ctx"][cfg.gmi_backend], "sm_per_gmi": cfg.sm_per_gmi,
                "decoupled": bool(cfg.decoupled), "env_steps_per_step": steps_total // args.steps,
                "cuda_graph": bool(cfg.use_graph),

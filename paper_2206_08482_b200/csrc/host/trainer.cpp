@@ -1501,6 +1501,14 @@ void Trainer::comm_connect(Trainer* const* t, int n) {
         t[r]->n_local_ != t[0]->n_local_)
       invalid("gmi_ppo_comm_connect: trainers[r] must be rank r of one num_gpus = n job");
     if (t[r]->connected_) invalid("gmi_ppo_comm_connect: already wired");
+    // Ranks of one process must sit on distinct devices: two ranks sharing a device in one
+    // context can have their streams multiplexed onto one hardware queue, where a rank's wait for
+    // its peer would block the peer's own work (ranks sharing a GPU: one process each + IPC).
+    for (int q = 0; q < r && n > 1; ++q)
+      if (t[q]->cfg_.device == t[r]->cfg_.device)
+        invalid("gmi_ppo_comm_connect: ranks " + std::to_string(q) + " and " + std::to_string(r) +
+                " share device " + std::to_string(t[r]->cfg_.device) +
+                "; ranks on one GPU need one process each (gmi_ppo_comm_attach)");
   }
   for (int r = 0; r < n; ++r) {
     Trainer& me = *t[r];

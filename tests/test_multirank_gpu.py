@@ -2,76 +2,113 @@
 the peer exchange (cfg.comm = 1, cuda/exchange.cu: fused reduce-scatter -> sharded Adam ->
 all-gather over peer memory, the HAR leader step of reduction.hpp:287-299).
 
-Every gpurun box has one GPU, so the ranks live in one process on cuda:0 and are wired with
-gmi_ppo_comm_connect (the same kernels, flags and fold order as one process per GPU over
-CUDA IPC; only the pointer source differs). Checks:
+Every gpurun box has one GPU, so the ranks are separate processes on cuda:0 (one CUDA context
+each, time-sliced) wired over CUDA IPC exactly as one process per GPU would be
+(tests/multirank_worker.py: gmi_ppo_comm_handle -> gloo all_gather_object ->
+gmi_ppo_comm_attach). Checks:
   * 2 ranks x 1 GMI == 1 rank x 2 GMIs, bit for bit (same env slices, RNG keys, permutation
     keys; the leader-ring fold of 2 ranks is the MPR fold of 2 GMIs; same Adam arithmetic), and
     both ranks hold bit-identical parameters;
-  * 2 ranks x 2 GMIs against the oracle's 2-GPU layout (leader-ring fold over per-GPU rings):
+  * 2 ranks x 2 GMIs (MRR) and 3 ranks x 4 GMIs (HAR) against the oracle's layouts:
     integer state bit-exact, relative parameter-change error <= 2e-2;
   * the exchange over a single rank is bit-identical to the plain Adam kernel (3 iterations:
     eager, then CUDA-graph replays), for 1 GMI, 2 GMIs and the decoupled layout;
   * an unwired rank (decomposition hooks only): its env slice, reset masks and rollout equal
     the oracle's GMI of that rank, and gmi_ppo_iteration refuses to run.
 """
+import os
+import socket
+import subprocess
+import sys
+
 import numpy as np
 import pytest
 
 from golden_util import PpoOracle, make_cfg
 
-pytestmark = [pytest.mark.gpu, pytest.mark.timeout(300)]
+pytestmark = [pytest.mark.gpu, pytest.mark.timeout(600)]
 
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 SMALL = dict(obs_dim=12, act_dim=3, hidden=[64, 64])
 
 
-def _ranks(n, envs, gmis=1, **kw):
+def _port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _job(tmp_path, world, envs, gmis=1, iters=2):
+    """Runs `world` rank processes on cuda:0 and returns their dumps."""
+    port = _port()
+    procs, outs = [], []
+    for r in range(world):
+        out = str(tmp_path / f"rank{r}.npz")
+        outs.append(out)
+        procs.append(subprocess.Popen([sys.executable, os.path.join(ROOT, "tests", "multirank_worker.py"),
+                                       "--rank", str(r), "--world", str(world), "--port", str(port),
+                                       "--envs", str(envs), "--gmis", str(gmis), "--iters", str(iters),
+                                       "--out", out], cwd=ROOT, stdout=subprocess.PIPE, stderr=subprocess.STDOUT,
+                                      text=True))
+    logs = []
+    try:
+        for p in procs:
+            logs.append(p.communicate(timeout=400)[0])
+    finally:
+        for p in procs:
+            if p.poll() is None:
+                p.kill()
+    for p, log in zip(procs, logs):
+        assert p.returncode == 0, log[-3000:]
+    return [dict(np.load(o)) for o in outs]
+
+
+def test_two_ranks_equal_one_rank_two_gmis(cuda, tmp_path):
     from paper_2206_08482_b200.ppo import PpoConfig, Trainer
-    ts = [Trainer(PpoConfig(**SMALL, num_envs=envs, num_gpus=n, rank=r, gmis_per_gpu=gmis, comm=1, **kw))
-          for r in range(n)]
-    Trainer.comm_connect(ts)
-    return ts
-
-
-def _iterate(ts, iters):
-    for _ in range(iters):
-        for t in ts:
-            t.iteration_async()
-        stats = [t.synchronize() for t in ts]
-    return stats
-
-
-def test_two_ranks_equal_one_rank_two_gmis(cuda):
-    from paper_2206_08482_b200.ppo import PpoConfig, Trainer
-    ranks = _ranks(2, 128)
+    ranks = _job(tmp_path, 2, 128, iters=2)
     one = Trainer(PpoConfig(**SMALL, num_envs=128, gmis_per_gpu=2))
-    _iterate(ranks, 3)
-    for _ in range(3):
+    for _ in range(2):
         one.iteration()
-    p0, p1, p = (x.get("params").view(np.uint32) for x in (ranks[0], ranks[1], one))
-    assert np.array_equal(p0, p1)
-    assert np.array_equal(p0, p)
+    p = one.get("params").view(np.uint32)
+    assert np.array_equal(ranks[0]["params"].view(np.uint32), ranks[1]["params"].view(np.uint32))
+    assert np.array_equal(ranks[0]["params"].view(np.uint32), p)
     for r in range(2):
         for f in ("done", "ep_count", "rew", "act"):
-            assert np.array_equal(ranks[r].get(f), one.get(f, r)), (r, f)
+            assert np.array_equal(ranks[r][f"{f}0"], one.get(f, r)), (r, f)
 
 
-def test_two_ranks_two_gmis_match_oracle(cuda):
-    ranks = _ranks(2, 256, gmis=2)
+def test_two_ranks_two_gmis_match_oracle(cuda, tmp_path):
+    """2 GPUs x 2 GMIs: Alg. 1 selects MRR (t <= g), so the exchange folds two rings of one GMI
+    per rank; the oracle folds the same way."""
+    ranks = _job(tmp_path, 2, 256, gmis=2, iters=1)
     orc = PpoOracle(make_cfg(12, 3, [64, 64], 256, num_gpus=2, gmis_per_gpu=2))
     th0 = orc.get("params").astype(np.float64)
-    assert np.array_equal(ranks[0].get("params").view(np.uint32), orc.get("params").view(np.uint32))
-    _iterate(ranks, 1)
     orc.iteration()
     for r in range(2):
         for c in range(2):
             for f in ("done", "ep_count", "ep_step"):
-                assert np.array_equal(ranks[r].get(f, c), orc.get(f, 2 * r + c)), (r, c, f)
-    assert np.array_equal(ranks[0].get("params").view(np.uint32), ranks[1].get("params").view(np.uint32))
-    d_dev = ranks[0].get("params").astype(np.float64) - th0
+                assert np.array_equal(ranks[r][f"{f}{c}"], orc.get(f, 2 * r + c)), (r, c, f)
+    assert np.array_equal(ranks[0]["params"].view(np.uint32), ranks[1]["params"].view(np.uint32))
+    d_dev = ranks[0]["params"].astype(np.float64) - th0
     d_orc = orc.get("params").astype(np.float64) - th0
     rel = np.linalg.norm(d_dev - d_orc) / np.linalg.norm(d_orc)
     assert rel <= 2e-2, rel
+
+
+def test_three_ranks_har_match_oracle(cuda, tmp_path):
+    """3 GPUs x 4 GMIs: t > g, so Alg. 1 selects HAR -- K1 folds per rank, then the leaders'
+    ring over the three ranks."""
+    ranks = _job(tmp_path, 3, 3 * 4 * 16, gmis=4, iters=1)
+    orc = PpoOracle(make_cfg(12, 3, [64, 64], 3 * 4 * 16, num_gpus=3, gmis_per_gpu=4))
+    th0 = orc.get("params").astype(np.float64)
+    orc.iteration()
+    for r in range(3):
+        assert np.array_equal(ranks[r]["params"].view(np.uint32), ranks[0]["params"].view(np.uint32))
+        for c in range(4):
+            assert np.array_equal(ranks[r][f"done{c}"], orc.get("done", 4 * r + c)), (r, c)
+    d_dev = ranks[0]["params"].astype(np.float64) - th0
+    d_orc = orc.get("params").astype(np.float64) - th0
+    assert np.linalg.norm(d_dev - d_orc) <= 2e-2 * np.linalg.norm(d_orc)
 
 
 @pytest.mark.parametrize("layout", [dict(gmis_per_gpu=1), dict(gmis_per_gpu=2), dict(decoupled=1, gmi_backend=1)])
@@ -100,5 +137,7 @@ def test_unwired_rank_hooks_match_oracle_slice(cuda):
             assert np.array_equal(t.get(f), orc.get(f, r)), (r, f)
         d = np.abs(t.get("rew").astype(np.float64) - orc.get("rew", r))
         assert d.max() <= 2e-2 and d.mean() <= 2e-4
-        with pytest.raises(_lib.GmiError):
+        with pytest.raises((_lib.GmiError, ValueError)):
             t.iteration()
+    with pytest.raises((_lib.GmiError, ValueError)):  # ranks sharing a device need a process each
+        Trainer.comm_connect(ts)
