@@ -19,6 +19,7 @@ def main():
     ap.add_argument("--envs", type=int)
     ap.add_argument("--gmis", type=int, default=1)
     ap.add_argument("--iters", type=int, default=2)
+    ap.add_argument("--decoupled", type=int, default=0)
     ap.add_argument("--out")
     a = ap.parse_args()
     import torch.distributed as dist
@@ -27,7 +28,8 @@ def main():
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(a.port))
     dist.init_process_group("gloo", rank=a.rank, world_size=a.world)
     t = Trainer(PpoConfig(obs_dim=12, act_dim=3, hidden=[64, 64], num_envs=a.envs, num_gpus=a.world, rank=a.rank,
-                          gmis_per_gpu=a.gmis, comm=1, device=0))
+                          gmis_per_gpu=a.gmis, comm=1, device=0, decoupled=a.decoupled,
+                          gmi_backend=1 if a.decoupled else 0))
     handles = [None] * a.world
     dist.all_gather_object(handles, t.comm_handle())
     t.comm_attach(handles)

@@ -38,7 +38,7 @@ def _port():
         return s.getsockname()[1]
 
 
-def _job(tmp_path, world, envs, gmis=1, iters=2):
+def _job(tmp_path, world, envs, gmis=1, iters=2, decoupled=0):
     """Runs `world` rank processes on cuda:0 and returns their dumps."""
     port = _port()
     procs, outs = [], []
@@ -48,6 +48,7 @@ def _job(tmp_path, world, envs, gmis=1, iters=2):
         procs.append(subprocess.Popen([sys.executable, os.path.join(ROOT, "tests", "multirank_worker.py"),
                                        "--rank", str(r), "--world", str(world), "--port", str(port),
                                        "--envs", str(envs), "--gmis", str(gmis), "--iters", str(iters),
+                                       "--decoupled", str(decoupled),
                                        "--out", out], cwd=ROOT, stdout=subprocess.PIPE, stderr=subprocess.STDOUT,
                                       text=True))
     logs = []
@@ -106,6 +107,23 @@ def test_three_ranks_har_match_oracle(cuda, tmp_path):
         assert np.array_equal(ranks[r]["params"].view(np.uint32), ranks[0]["params"].view(np.uint32))
         for c in range(4):
             assert np.array_equal(ranks[r][f"done{c}"], orc.get("done", 4 * r + c)), (r, c)
+    d_dev = ranks[0]["params"].astype(np.float64) - th0
+    d_orc = orc.get("params").astype(np.float64) - th0
+    assert np.linalg.norm(d_dev - d_orc) <= 2e-2 * np.linalg.norm(d_orc)
+
+
+def test_two_ranks_decoupled_match_oracle(cuda, tmp_path):
+    """BASELINE configs[3] shape on 2 GPUs: per GPU a serving GMI (16-SM green context) streams
+    experience to the trainer GMI; the trainer GMIs' gradients cross GPUs through the peer
+    exchange. Two iterations against the oracle's lagged schedule with num_gpus = 2."""
+    ranks = _job(tmp_path, 2, 128, iters=2, decoupled=1)
+    orc = PpoOracle(make_cfg(12, 3, [64, 64], 128, num_gpus=2))
+    th0 = orc.get("params").astype(np.float64)
+    for _ in range(2):
+        orc.iteration_decoupled()
+    assert np.array_equal(ranks[0]["params"].view(np.uint32), ranks[1]["params"].view(np.uint32))
+    for r in range(2):
+        assert np.array_equal(ranks[r]["done0"], orc.get("done", r)), r
     d_dev = ranks[0]["params"].astype(np.float64) - th0
     d_orc = orc.get("params").astype(np.float64) - th0
     assert np.linalg.norm(d_dev - d_orc) <= 2e-2 * np.linalg.norm(d_orc)
