@@ -44,8 +44,9 @@ def parse():
     p.add_argument("--decoupled", type=int, default=None,
                    help="1: serving GMI + trainer GMI per GPU with an experience channel (BASELINE config 4)")
     p.add_argument("--serving-sms", type=int, default=0, help="SMs of the serving GMI (decoupled mode)")
-    p.add_argument("--comm", default="peer", choices=["peer", "nccl"],
-                   help="cross-GPU step (N > 1): fused peer exchange over NVLink (default) or ncclAllReduce")
+    p.add_argument("--comm", default="auto", choices=["auto", "peer", "nccl"],
+                   help="cross-GPU step: auto = peer exchange for N > 1 (none at N = 1); peer = the fused "
+                        "peer exchange even at N = 1 (measures its cost over one rank); nccl = ncclAllReduce")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-multi-gmi", action="store_true",
                    help="skip the decoupled multi-GMI layout measured beside the single-context one")
@@ -457,7 +458,7 @@ def main():
     if args.backend is not None:
         cfg.gmi_backend = args.backend
     cfg.instrument = 0  # timed loop runs the plain graph; a separate pass below is instrumented
-    cfg.comm = 1 if args.comm == "peer" else 0
+    cfg.comm = 1 if args.comm == "peer" or (args.comm == "auto" and world > 1) else 0
     trainer = make_trainer(cfg, world, rank)
     upd = torch.cuda.ExternalStream(trainer.stream(-1))
 
@@ -540,8 +541,8 @@ def main():
                   if not cfg.decoupled else
                   f"decoupled: serving GMI ({cfg.serving_sms or 16} SMs, simulator+agent) + trainer GMI per B200, "
                   f"device experience channel, one-iteration policy lag")
-        run = {"layout": layout, "comm": (["ncclAllReduce", "peer exchange (fused RS + sharded Adam + AG)"]
-                                          [cfg.comm] if world > 1 else "none (one GPU)"),
+        run = {"layout": layout, "comm": (["ncclAllReduce" if world > 1 else "none (one GPU)",
+                                           "peer exchange (fused RS + sharded Adam + AG)"][cfg.comm]),
                "gmis_per_gpu": cfg.gmis_per_gpu + (1 if cfg.decoupled else 0),
                "gmi_backend": ["streams", "green_ctx"][cfg.gmi_backend], "sm_per_gmi": cfg.sm_per_gmi,
                "decoupled": bool(cfg.decoupled), "env_steps_per_step": steps_total // args.steps,

@@ -15,10 +15,10 @@
 //      results summed into a zero total in ring order (reduction.hpp:255-283); chunk c of every
 //      ring starts at member c (:164-212; oracle/ppo_oracle.c fold_gradients). Runs Adam on the shard (Adam
 //      moments are sharded: each element's m, v live only on its owner) and stores the new
-//      parameter and its bf16 shadow into EVERY rank's window (the all-gather), then bumps every
-//      rank's done counter once (release);
-//   3. wait: one thread spins until its own done counter reaches s * G * C (all C CTAs of all G
-//      ranks finished writing step s into this rank), so the next minibatch reads final weights.
+//      parameter and its bf16 shadow into EVERY rank's window (the all-gather), then stores its
+//      (rank, CTA) done flag = s into every rank's window (release; no contended atomics);
+//   3. wait: one CTA spins until all G x C done flags in its own window reached s (every CTA of
+//      every rank finished writing step s into this rank), so the next minibatch reads final weights.
 // No float atomics: every element is summed by exactly one owner in a fixed order, so all ranks
 // hold bit-identical parameters, and the arithmetic of the update is adam_kernel's.
 #include <cuda_bf16.h>
@@ -38,10 +38,6 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long
 
 __device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
   asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-
-__device__ __forceinline__ void red_add_release_sys(unsigned long long* p, unsigned long long v) {
-  asm volatile("red.release.sys.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
 __device__ __forceinline__ void spin_until(const unsigned long long* p, unsigned long long target) {
@@ -64,10 +60,7 @@ __global__ void __launch_bounds__(32) exchange_signal_kernel(const ExchangeArgs 
   pdl_trigger();
   pdl_wait();  // the fold that produced pub[rank] has completed (device scope)
   const long long s = step_id(a);
-  if (threadIdx.x == 0) {
-    __threadfence_system();
-    st_release_sys(a.ready[a.rank], (unsigned long long)s);
-  }
+  if (threadIdx.x == 0) st_release_sys(a.ready[a.rank], (unsigned long long)s);  // release: orders the fold
   if (int(threadIdx.x) < a.G) spin_until(a.ready[threadIdx.x], (unsigned long long)s);
   __syncwarp();
 }
@@ -79,10 +72,9 @@ __global__ void __launch_bounds__(256) exchange_adam_kernel(const ExchangeArgs a
   const long long st = s - 1;  // completed updates before this one (bias-correction index)
   const float bc1 = a.bc[2 * st], bc2 = a.bc[2 * st + 1];
   const float ob1 = __fsub_rn(1.0f, a.b1), ob2 = __fsub_rn(1.0f, a.b2);
-  // this CTA's contiguous slice of the shard
-  const long long len = a.hi - a.lo;
-  const long long c0 = a.lo + len * blockIdx.x / gridDim.x, c1 = a.lo + len * (blockIdx.x + 1) / gridDim.x;
-  for (long long i = c0 + threadIdx.x; i < c1; i += blockDim.x) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+#pragma unroll 4
+  for (long long i = a.lo + (long long)blockIdx.x * blockDim.x + threadIdx.x; i < a.hi; i += stride) {
     // chunk cg = the ring chunk holding element i; every ring fold starts at member cg
     const int cg = int(((i + 1) * a.G + a.P - 1) / a.P) - 1;
     float acc = 0.f;
@@ -118,29 +110,33 @@ __global__ void __launch_bounds__(256) exchange_adam_kernel(const ExchangeArgs a
       a.shadow[q][i] = sh;
     }
   }
-  __syncthreads();
-  if (int(threadIdx.x) < a.G) {
-    __threadfence_system();
-    red_add_release_sys(a.done[threadIdx.x], 1ull);
-  }
+  __syncthreads();  // the CTA's stores happen-before the releases below (bar.sync + release cumulativity)
+  // one flag per (rank, CTA) in every destination's window -- plain release stores, no
+  // contended atomics on one counter
+  if (int(threadIdx.x) < a.G)
+    st_release_sys(a.done[threadIdx.x] + a.rank * kMaxXchgCtas + blockIdx.x, (unsigned long long)s);
 }
 
-__global__ void __launch_bounds__(32) exchange_wait_kernel(const ExchangeArgs a) {
+// One CTA: wait until every (source rank, CTA) flag in this rank's window reached step s.
+__global__ void __launch_bounds__(256) exchange_wait_kernel(const ExchangeArgs a) {
   pdl_trigger();
   pdl_wait();
-  if (threadIdx.x == 0)
-    spin_until(a.done[a.rank], (unsigned long long)step_id(a) * (unsigned long long)(a.G * a.ctas));
-  __syncwarp();
+  const unsigned long long s = (unsigned long long)step_id(a);
+  for (int f = threadIdx.x; f < a.G * a.ctas; f += blockDim.x) {
+    const int q = f / a.ctas, c = f - q * a.ctas;
+    spin_until(a.done[a.rank] + q * kMaxXchgCtas + c, s);
+  }
+  __syncthreads();
 }
 
 }  // namespace
 
 void launch_exchange_adam(const ExchangeArgs& a, cudaStream_t s) {
   if (a.G < 1 || a.G > kMaxRanks) invalid("exchange: 1..8 ranks");
-  if (a.ctas < 1) invalid("exchange: ctas must be >= 1");
+  if (a.ctas < 1 || a.ctas > kMaxXchgCtas) invalid("exchange: 1..148 CTAs");
   launch_pdl(exchange_signal_kernel, dim3(1), dim3(32), 0, s, a);
   launch_pdl(exchange_adam_kernel, dim3(a.ctas), dim3(256), 0, s, a);
-  launch_pdl(exchange_wait_kernel, dim3(1), dim3(32), 0, s, a);
+  launch_pdl(exchange_wait_kernel, dim3(1), dim3(256), 0, s, a);
 }
 
 }  // namespace gmi::ppo

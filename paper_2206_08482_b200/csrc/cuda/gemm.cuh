@@ -118,6 +118,11 @@ struct GemmSmem {
   static_assert(kBytes <= 232448, "shared memory budget");
 };
 
+// Total tiles of a weight-stationary launch (one problem per CTA, splits == 1, N <= BN).
+__device__ __forceinline__ int ntile_total_ws(const GemmParams& P) {
+  return (P.prob[0].M + kGemmBlockM - 1) / kGemmBlockM * P.num_problems;
+}
+
 // CS = 1 (EPI_F32 with MN-major A only): 4 extra warps sum the A stages over K (bias gradient).
 template <int BN, int A_MN, int B_MN, int EPI, int WS, int CS = 0>
 __global__ void __launch_bounds__(gemm_threads(EPI) + 128 * CS, 1)
@@ -130,7 +135,7 @@ __global__ void __launch_bounds__(gemm_threads(EPI) + 128 * CS, 1)
   static_assert(!CS || (EPI == EPI_F32 && A_MN && !WS), "column sums: split-K weight gradient only");
 
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = ptx::align_smem_1024(smem_raw);
   uint8_t* b_res = smem + S * L::kStage;  // WS: resident B, k-block j at j * kB
   uint8_t* staging = b_res + L::kBRes;
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + L::kBarOff);
@@ -143,6 +148,14 @@ __global__ void __launch_bounds__(gemm_threads(EPI) + 128 * CS, 1)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const GemmProblem& p0 = P.prob[0];
+  auto load_b = [&](const GemmProblem& pr, uint8_t* sb, uint64_t* bar, int n0, int k0) {
+    if constexpr (B_MN) {
+#pragma unroll
+      for (int j = 0; j < BN / 64; ++j) ptx::tma_load_2d(sb + j * 8192, &pr.map_b, bar, n0 + 64 * j, k0 + pr.b_row0);
+    } else {
+      ptx::tma_load_2d(sb, &pr.map_b, bar, k0, n0 + pr.b_row0);
+    }
+  };
   const int mtiles = (p0.M + kGemmBlockM - 1) / kGemmBlockM;
   const int ntiles = (p0.N + BN - 1) / BN;
   const int per_prob = P.splits * mtiles * ntiles;
@@ -164,6 +177,16 @@ __global__ void __launch_bounds__(gemm_threads(EPI) + 128 * CS, 1)
       ptx::tma_prefetch_desc(&P.prob[i].map_a);
       ptx::tma_prefetch_desc(&P.prob[i].map_b);
       ptx::tma_prefetch_desc(&P.prob[i].map_out);
+    }
+    if constexpr (WS) {
+      // stable weights: the whole resident B before griddepcontrol.wait (overlaps the tail of
+      // the previous kernel); the CTA's problem is blockIdx.x % problems for every tile
+      if (P.b_stable && int(blockIdx.x) < ntile_total_ws(P)) {
+        const GemmProblem& pb = P.prob[blockIdx.x % P.num_problems];
+        const int nkb = (pb.K + kGemmBlockK - 1) / kGemmBlockK;
+        ptx::mbar_arrive_expect_tx(bres_bar, uint32_t(nkb) * L::kB);
+        for (int i = 0; i < nkb; ++i) load_b(pb, b_res + i * L::kB, bres_bar, 0, i * kGemmBlockK);
+      }
     }
   }
   if (warp == 1) ptx::tmem_alloc(tmem_slot, L::kTmemCols);
@@ -203,14 +226,6 @@ __global__ void __launch_bounds__(gemm_threads(EPI) + 128 * CS, 1)
   if (warp == 0) {
     // ---------------- TMA producer (one lane)
     if (lane == 0) {
-      auto load_b = [&](const GemmProblem& pr, uint8_t* sb, uint64_t* bar, int n0, int k0) {
-        if constexpr (B_MN) {
-#pragma unroll
-          for (int j = 0; j < BN / 64; ++j) ptx::tma_load_2d(sb + j * 8192, &pr.map_b, bar, n0 + 64 * j, k0 + pr.b_row0);
-        } else {
-          ptx::tma_load_2d(sb, &pr.map_b, bar, k0, n0 + pr.b_row0);
-        }
-      };
       int it = 0, plt = 0;
       for (int tile = blockIdx.x; tile < ntile_total; tile += gridDim.x, ++plt) {
         int prob, split, m0, n0, kb0, nkb;
@@ -224,7 +239,7 @@ __global__ void __launch_bounds__(gemm_threads(EPI) + 128 * CS, 1)
           const int k0 = (kb0 + i) * kGemmBlockK;
           // WS: the CTA's first tile also brings the resident B k-block i on the same barrier,
           // so the first MMAs start after one k-block instead of after the whole weight tile.
-          const bool first_ws = WS && it < nkb_total;
+          const bool first_ws = WS && !P.b_stable && it < nkb_total;
           ptx::mbar_arrive_expect_tx(&full_bar[s], L::kStage + (first_ws ? L::kB : 0u));
           if (first_ws) load_b(pr, b_res + i * L::kB, &full_bar[s], 0, k0);
           if constexpr (A_MN) {
@@ -243,6 +258,7 @@ __global__ void __launch_bounds__(gemm_threads(EPI) + 128 * CS, 1)
     // ---------------- MMA issuer (one lane), double-buffered TMEM accumulators
     if (lane == 0) {
       int it = 0, lt = 0;
+      if (WS && P.b_stable && int(blockIdx.x) < ntile_total) ptx::mbar_wait(bres_bar, 0);  // resident B landed
       for (int tile = blockIdx.x; tile < ntile_total; tile += gridDim.x, ++lt) {
         int prob, split, m0, n0, kb0, nkb;
         decode(tile, prob, split, m0, n0, kb0, nkb);

@@ -80,7 +80,7 @@ __device__ __forceinline__ void wait_cluster(uint64_t* bar, uint32_t parity) {
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1)
     gemm_pair_kernel(const __grid_constant__ GemmParams P) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = ptx::align_smem_1024(smem_raw);
   uint8_t* staging = smem + kPS * kPStage;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kPBarOff);
   uint64_t* empty = full + kPS;

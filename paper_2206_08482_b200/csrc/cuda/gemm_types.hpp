@@ -39,6 +39,11 @@ struct alignas(64) GemmParams {
   GemmProblem prob[4];  // grouped problems (e.g. policy / value nets, or their N-halves)
   int num_problems;
   int splits;
+  // Weight-stationary launches: B (the layer's weights) is not written by the preceding
+  // kernel in the stream, so the CTA loads its resident B before griddepcontrol.wait and the
+  // load overlaps the previous kernel's tail (set by the host when no in-stream kernel updates
+  // the weights right before this launch).
+  int b_stable;
   unsigned long long* trace;  // optional [8 tiles][16] globaltimer stamps of CTA 0 (development aid)
 };
 

@@ -67,7 +67,7 @@ __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, %0;" ::"n"
 template <int MAXA>
 __global__ void __launch_bounds__(kThreads, 1) head_fused_kernel(const __grid_constant__ HeadFusedArgs a) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = ptx::align_smem_1024(smem_raw);
   uint8_t* sH = smem + kOffH;
   uint8_t* sG = smem + kOffG;
   uint8_t* sWK = smem + kOffWK;

@@ -100,6 +100,9 @@ struct SegAdam {
 // Cross-GPU exchange + sharded Adam over peer memory (cuda/exchange.cu).
 constexpr int kMaxRanks = 8;
 constexpr int kMaxLocalGmis = 16;
+constexpr int kMaxXchgCtas = 148;       // exchange grid (one CTA per SM at most)
+constexpr int kXchgDoneOff = 1024;      // window: done flags [kMaxRanks][kMaxXchgCtas] u64 from here
+constexpr int kXchgHeader = 16384;      // window header bytes (ready flag + done flags)
 struct ExchangeArgs {
   int mrr;                               // 0: leader ring over pub (HAR / one rank), 1: MRR over gpub
   int t;                                 // GMIs per rank (MRR)
@@ -108,7 +111,7 @@ struct ExchangeArgs {
   float* params[kMaxRanks];              // each rank's fp32 master parameters
   __nv_bfloat16* shadow[kMaxRanks];      // each rank's bf16 shadow
   unsigned long long* ready[kMaxRanks];  // each rank's "gradient of step s published" flag
-  unsigned long long* done[kMaxRanks];   // each rank's "step s written into me" counter
+  unsigned long long* done[kMaxRanks];   // each rank's done flags [source rank][CTA] ("step s written into me")
   int G, rank, ctas;
   long long P, lo, hi;  // flat length; this rank's shard [lo, hi)
   float* m;             // Adam moments (only the shard is used)

@@ -9,6 +9,15 @@
 
 namespace gmi::ptx {
 
+// 1024-byte-aligned view of the dynamic shared memory that keeps the shared address space
+// visible to the compiler (pointer arithmetic on the __shared__ array instead of an integer
+// round trip), so every access through it compiles to LDS / STS rather than generic LD / ST
+// (generic accesses to shared memory take the slower LSU path and long-scoreboard waits).
+__device__ __forceinline__ uint8_t* align_smem_1024(uint8_t* smem_raw) {
+  const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw));
+  return smem_raw + (((a + 1023u) & ~1023u) - a);
+}
+
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }

@@ -67,7 +67,7 @@ __device__ __forceinline__ uint32_t sw128(int row, int col_bf16) {  // byte offs
 template <int MAXB>
 __global__ void __launch_bounds__(kThreads, 1) rollout_kernel(const __grid_constant__ RolloutArgs a) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = ptx::align_smem_1024(smem_raw);
   uint8_t* act_buf0 = smem;
   uint8_t* act_buf1 = smem + kActBytes;
   uint8_t* wring = smem + 2 * kActBytes;

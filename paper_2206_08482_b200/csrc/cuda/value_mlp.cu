@@ -30,7 +30,7 @@ constexpr uint32_t kSmem = 2 * kActBytes + kStages * kWStage + 256 + 1024;
 
 __global__ void __launch_bounds__(kThreads, 1) value_mlp_kernel(const __grid_constant__ ValueArgs a) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = ptx::align_smem_1024(smem_raw);
   uint8_t* act_buf0 = smem;
   uint8_t* act_buf1 = smem + kActBytes;
   uint8_t* wring = smem + 2 * kActBytes;

@@ -277,7 +277,7 @@ void Trainer::init(const void* nccl_id) {
     xa_.lo = geo_.P * cfg.rank / cfg.num_gpus;
     xa_.hi = geo_.P * (cfg.rank + 1) / cfg.num_gpus;
     // same on every rank (the done counter target is steps x G x ctas)
-    xa_.ctas = int(std::max<long long>(1, std::min<long long>(148, (geo_.P / cfg.num_gpus + 2047) / 2048)));
+    xa_.ctas = int(std::max<long long>(1, std::min<long long>(ppo::kMaxXchgCtas, (geo_.P / cfg.num_gpus + 1023) / 1024)));
     if (cfg.num_gpus == 1) {  // one rank: the exchange runs over the rank itself
       Trainer* self = this;
       comm_connect(&self, 1);
@@ -354,13 +354,13 @@ void Trainer::alloc() {
   };
   const long long P = geo_.P;
   if (xchg_) {
-    // exchange window: [flags 256 B | fold P fp32 | t GMI gradients P fp32 | params P fp32 |
+    // exchange window: [flags 16 KB | fold P fp32 | t GMI gradients P fp32 | params P fp32 |
     // shadow P bf16]; peers read the fold (HAR) or the GMI gradients (MRR)
-    win_off_gmi_ = 256 + (size_t)P * 4;
+    win_off_gmi_ = ppo::kXchgHeader + (size_t)P * 4;
     win_off_params_ = win_off_gmi_ + (size_t)n_local_ * P * 4;
     win_off_shadow_ = win_off_params_ + (size_t)P * 4;
     win_ = static_cast<char*>(dev(win_off_shadow_ + (size_t)P * 2));
-    grad_sum_ = reinterpret_cast<float*>(win_ + 256);
+    grad_sum_ = reinterpret_cast<float*>(win_ + ppo::kXchgHeader);
     params_ = reinterpret_cast<float*>(win_ + win_off_params_);
     shadow_ = reinterpret_cast<__nv_bfloat16*>(win_ + win_off_shadow_);
   } else {
@@ -972,9 +972,13 @@ static double gemm_bytes(const GemmParams& P, int epi) {
   return b;
 }
 
-void Trainer::gemm(Gmi& g, int phase, const GemmParams& P, int bn, int amn, int bmn, int epi, double flop, int ws,
+void Trainer::gemm(Gmi& g, int phase, const GemmParams& P0, int bn, int amn, int bmn, int epi, double flop, int ws,
                    cudaStream_t stream, int ctas) {
   cudaStream_t st = stream ? stream : g.s;
+  // weight-stationary B = the layer's weights: only Adam writes them, on the update stream
+  // (ordered by an event) -- unless Adam is fused into this GMI's gradient assembly
+  GemmParams P = P0;
+  P.b_stable = ws && !adam_in_gmi_stream_ ? 1 : 0;
   // GMI_GEMM_TRACE=<phase id>: globaltimer stamps of CTA 0 for every launch of that phase
   // (the last one of the iteration wins; read with get("gemm_trace")). Development aid.
   // GMI_GEMM_TRACE_NTH=<k>: only the k-th recorded launch of the phase (e.g. 0 = the first
@@ -1354,6 +1358,10 @@ void Trainer::enqueue_rollout() {
 void Trainer::record_iteration(bool with_rollout) {
   launches_ = 0;
   marks_used_ = 0;
+  {
+    const char* af = std::getenv("GMI_ADAM_FUSED");  // see the fused_adam note below
+    adam_in_gmi_stream_ = n_local_ == 1 && !nccl_ && !xchg_ && af && af[0] == '1';
+  }
   GMI_CUDA_CHECK(cudaEventRecord(ev_start_, upd_));
   if (!with_rollout) {  // trains on the rollout a gmi_ppo_rollout hook produced
     for (auto& g : gmis_) GMI_CUDA_CHECK(cudaStreamWaitEvent(g->s, ev_start_, 0));
@@ -1483,8 +1491,8 @@ void Trainer::comm_attach(const void* handles) {
       base = static_cast<char*>(p);
     }
     xa_.ready[q] = reinterpret_cast<unsigned long long*>(base);
-    xa_.done[q] = reinterpret_cast<unsigned long long*>(base + 128);
-    xa_.pub[q] = reinterpret_cast<const float*>(n_local_ == 1 ? base + win_off_gmi_ : base + 256);
+    xa_.done[q] = reinterpret_cast<unsigned long long*>(base + ppo::kXchgDoneOff);
+    xa_.pub[q] = reinterpret_cast<const float*>(n_local_ == 1 ? base + win_off_gmi_ : base + ppo::kXchgHeader);
     for (int j = 0; j < n_local_; ++j)
       xa_.gpub[q][j] = reinterpret_cast<const float*>(base + win_off_gmi_ + (size_t)j * geo_.P * 4);
     xa_.params[q] = reinterpret_cast<float*>(base + win_off_params_);
@@ -1521,7 +1529,7 @@ void Trainer::comm_connect(Trainer* const* t, int n) {
         else GMI_CUDA_CHECK(e);
       }
       me.xa_.ready[q] = reinterpret_cast<unsigned long long*>(peer.win_);
-      me.xa_.done[q] = reinterpret_cast<unsigned long long*>(peer.win_ + 128);
+      me.xa_.done[q] = reinterpret_cast<unsigned long long*>(peer.win_ + ppo::kXchgDoneOff);
       me.xa_.pub[q] = peer.n_local_ == 1 ? peer.gmis_[0]->grad : peer.grad_sum_;
       for (int j = 0; j < peer.n_local_; ++j) me.xa_.gpub[q][j] = peer.gmis_[j]->grad;
       me.xa_.params[q] = peer.params_;

@@ -117,6 +117,7 @@ class Trainer {
   int bwd_dx_share_ = 50;  // percent of the GMI's SMs given to the dx branch
   int iteration_ = 0;      // iterations enqueued so far
   bool rollout_pending_ = false;  // gmi_ppo_rollout produced the next iteration's rollout
+  bool adam_in_gmi_stream_ = false;  // GMI_ADAM_FUSED: Adam runs in the GMI stream (no B preload)
   long long adam_steps_ = 0;
   int launches_ = 0;       // kernels in one iteration
   bool capturing_ = false;
