@@ -292,6 +292,19 @@ GMI_API void gmi_pipeline_config_defaults(gmi_pipeline_config_t* c);
 GMI_API int gmi_simulate_pipeline(const gmi_workload_t* w, const gmi_plan_t* plan,
                                   const gmi_topology_t* topo, const gmi_pipeline_config_t* cfg,
                                   double duration, void** handle, gmi_pipeline_metrics_t* out);
+/* The same pipeline on the GPU over real payloads (cuda/channels.cu, K9): every agent GMI (role
+ * mask & AGENT, ascending id) supplies three device channel buffers -- agent_bufs[c * agents + a],
+ * c = 0 state (S bytes per record), 1 action (A), 2 reward (W); records in production order --
+ * and every trainer GMI three receive buffers of trainer_capacity records
+ * (trainer_bufs[c * trainers + t]). compress(k) units, send / arrival clocks, direct vs
+ * least-load routing, delivery, stack / slice batching and PPS / TTOP follow
+ * gmi_simulate_pipeline bit for bit; the delivered records land in the receive buffers in
+ * delivery order (batches are contiguous ranges). The handle answers the gmi_pipeline_*
+ * accessors below. */
+GMI_API int gmi_channel_run(const gmi_workload_t* w, const gmi_plan_t* plan, const gmi_topology_t* topo,
+                            const gmi_pipeline_config_t* cfg, double duration, const void* const* agent_bufs,
+                            int num_agent_bufs, void* const* trainer_bufs, int num_trainer_bufs,
+                            long trainer_capacity, void* stream, void** handle, gmi_pipeline_metrics_t* out);
 GMI_API int gmi_pipeline_trainer_records(void* handle, int* trainers, long* records);
 GMI_API size_t gmi_pipeline_num_batches(void* handle);
 GMI_API int gmi_pipeline_batch(void* handle, size_t i, int* trainer, double* emit_time,

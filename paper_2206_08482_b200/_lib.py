@@ -175,6 +175,8 @@ PROTOTYPES: dict[str, tuple] = {
     "gmi_pipeline_config_defaults": (None, [P(PipelineConfigT)]),
     "gmi_simulate_pipeline": (ci, [P(WorkloadT), P(PlanT), P(TopologyT), P(PipelineConfigT), cd,
                                    P(vp), P(PipelineMetricsT)]),
+    "gmi_channel_run": (ci, [P(WorkloadT), P(PlanT), P(TopologyT), P(PipelineConfigT), cd, P(vp), ci, P(vp), ci,
+                             C.c_long, vp, P(vp), P(PipelineMetricsT)]),
     "gmi_pipeline_trainer_records": (ci, [vp, c_int_p, P(C.c_long)]),
     "gmi_pipeline_num_batches": (csz, [vp]),
     "gmi_pipeline_batch": (ci, [vp, csz, c_int_p, c_double_p, P(csz)]),

@@ -56,7 +56,7 @@ __device__ __forceinline__ long long step_id(const ExchangeArgs& a) {
 // here, in a single small CTA, and never in the wide exchange kernel: a spinning CTA holds an
 // SM slot, and ranks that share a GPU (tests, or several ranks per device) must leave room for
 // the peers' persistent GEMMs to finish the gradients being waited for.
-__global__ void __launch_bounds__(32) exchange_signal_kernel(const ExchangeArgs a) {
+__global__ void __launch_bounds__(32) exchange_signal_kernel(const __grid_constant__ ExchangeArgs a) {
   pdl_trigger();
   pdl_wait();  // the fold that produced pub[rank] has completed (device scope)
   const long long s = step_id(a);
@@ -65,7 +65,7 @@ __global__ void __launch_bounds__(32) exchange_signal_kernel(const ExchangeArgs 
   __syncwarp();
 }
 
-__global__ void __launch_bounds__(256) exchange_adam_kernel(const ExchangeArgs a) {
+__global__ void __launch_bounds__(256) exchange_adam_kernel(const __grid_constant__ ExchangeArgs a) {
   pdl_trigger();
   pdl_wait();  // exchange_signal_kernel completed: every peer's gradient of this step is published
   const long long s = step_id(a);
@@ -75,8 +75,10 @@ __global__ void __launch_bounds__(256) exchange_adam_kernel(const ExchangeArgs a
   const long long stride = (long long)gridDim.x * blockDim.x;
 #pragma unroll 4
   for (long long i = a.lo + (long long)blockIdx.x * blockDim.x + threadIdx.x; i < a.hi; i += stride) {
-    // chunk cg = the ring chunk holding element i; every ring fold starts at member cg
-    const int cg = int(((i + 1) * a.G + a.P - 1) / a.P) - 1;
+    // chunk cg = the ring chunk holding element i (chunk c = [P c / G, P (c + 1) / G),
+    // reduction.hpp:164-166); every ring fold starts at member cg
+    int cg = 0;
+    while (cg + 1 < a.G && i >= a.chunk0[cg + 1]) ++cg;
     float acc = 0.f;
     if (!a.mrr) {  // HAR leader ring (or one rank): the ranks' K1 folds in ring order
       for (int j = 0; j < a.G; ++j) {
@@ -118,7 +120,7 @@ __global__ void __launch_bounds__(256) exchange_adam_kernel(const ExchangeArgs a
 }
 
 // One CTA: wait until every (source rank, CTA) flag in this rank's window reached step s.
-__global__ void __launch_bounds__(256) exchange_wait_kernel(const ExchangeArgs a) {
+__global__ void __launch_bounds__(256) exchange_wait_kernel(const __grid_constant__ ExchangeArgs a) {
   pdl_trigger();
   pdl_wait();
   const unsigned long long s = (unsigned long long)step_id(a);

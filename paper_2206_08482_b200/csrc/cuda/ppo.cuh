@@ -114,6 +114,7 @@ struct ExchangeArgs {
   unsigned long long* done[kMaxRanks];   // each rank's done flags [source rank][CTA] ("step s written into me")
   int G, rank, ctas;
   long long P, lo, hi;  // flat length; this rank's shard [lo, hi)
+  long long chunk0[kMaxRanks];  // ring chunk starts P c / G
   float* m;             // Adam moments (only the shard is used)
   float* v;
   const float* bc;

@@ -400,6 +400,32 @@ GMI_API int gmi_simulate_pipeline(const gmi_workload_t* w, const gmi_plan_t* pla
   });
 }
 
+GMI_API int gmi_channel_run(const gmi_workload_t* w, const gmi_plan_t* plan, const gmi_topology_t* topo,
+                            const gmi_pipeline_config_t* cfg, double duration, const void* const* agent_bufs,
+                            int num_agent_bufs, void* const* trainer_bufs, int num_trainer_bufs,
+                            long trainer_capacity, void* stream, void** handle, gmi_pipeline_metrics_t* out) {
+  return guarded([&] {
+    if (!plan || !agent_bufs || !trainer_bufs || !out) invalid("null argument");
+    Assignment a;
+    a.tpl = to_tpl(plan->template_kind);
+    int k = 0;
+    for (int g = 0; g < plan->num_gpus; ++g) {
+      auto& ids = a.per_gpu[plan->gpu_ids[g]];
+      for (int j = 0; j < plan->counts[g]; ++j, ++k) {
+        ids.push_back(plan->gmi_ids[k]);
+        a.roles[plan->gmi_ids[k]] = plan->role_masks[k];
+      }
+    }
+    std::vector<const void*> ab(agent_bufs, agent_bufs + num_agent_bufs);
+    std::vector<void*> tb(trainer_bufs, trainer_bufs + num_trainer_bufs);
+    auto st = std::make_unique<FlowStats>(run_channels_device(to_workload(w), a, to_machine(topo), to_channels(cfg),
+                                                              duration, ab, tb, trainer_capacity, stream));
+    *out = {st->pps, st->ttop, st->produced, st->delivered, st->units, st->batches, st->bytes, st->busy,
+            st->delivery_span, st->training_span, st->per_trainer.size()};
+    if (handle) *handle = st.release();
+  });
+}
+
 GMI_API int gmi_pipeline_trainer_records(void* h, int* trainers, long* records) {
   return guarded([&] {
     int i = 0;

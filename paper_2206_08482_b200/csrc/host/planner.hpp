@@ -241,6 +241,14 @@ struct FlowStats {
 };
 FlowStats run_channels(const Workload& w, const Assignment& a, const Machine& m,
                        const ChannelConfig& c, double duration);
+// The same pipeline executed on the GPU over real payloads (cuda/channels.cu): agent_buf holds
+// 3 x agents device pointers [channel * agents + agent] (state / action / reward records of each
+// agent in ascending gmi-id order), trainer_buf 3 x trainers receive buffers of
+// trainer_capacity records each; stream = cudaStream_t.
+FlowStats run_channels_device(const Workload& w, const Assignment& a, const Machine& m, const ChannelConfig& c,
+                              double duration, const std::vector<const void*>& agent_buf,
+                              const std::vector<void*>& trainer_buf, long trainer_capacity, void* stream,
+                              std::vector<int>* key_agent_out = nullptr, std::vector<long>* key_seq_out = nullptr);
 
 // ------------------------------------------------------------------ config schema
 struct CfgLine {

@@ -274,6 +274,7 @@ void Trainer::init(const void* nccl_id) {
     xa_.G = cfg.num_gpus;
     xa_.rank = cfg.rank;
     xa_.P = geo_.P;
+    for (int c = 0; c < cfg.num_gpus; ++c) xa_.chunk0[c] = geo_.P * c / cfg.num_gpus;
     xa_.lo = geo_.P * cfg.rank / cfg.num_gpus;
     xa_.hi = geo_.P * (cfg.rank + 1) / cfg.num_gpus;
     // same on every rank (the done counter target is steps x G x ctas)

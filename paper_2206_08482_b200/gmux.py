@@ -809,6 +809,27 @@ def simulate_pipeline(w: DrlWorkload, plan: MappingPlan, topo: Topology, config:
     m = L.PipelineMetricsT()
     L.check(_lib().gmi_simulate_pipeline(C.byref(wc), C.byref(pc), C.byref(tc), C.byref(cc),
                                          float(duration), C.byref(h), C.byref(m)))
+    return _metrics_from_handle(h, m)
+
+
+def run_channels_device(w: DrlWorkload, plan: MappingPlan, topo: Topology, config: PipelineConfig,
+                        duration: float, agent_bufs: list, trainer_bufs: list, trainer_capacity: int,
+                        stream: int = 0) -> PipelineMetrics:
+    """The channel pipeline on the GPU (gmi_channel_run): agent_bufs = device pointers
+    [channel * agents + agent] (state / action / reward, agents in ascending gmi id),
+    trainer_bufs likewise per trainer (receive buffers of trainer_capacity records)."""
+    wc, pc, tc, cc = w._c(), plan._c(), topo._c(), config._c()
+    h = C.c_void_p()
+    m = L.PipelineMetricsT()
+    ab = (C.c_void_p * len(agent_bufs))(*agent_bufs)
+    tb = (C.c_void_p * len(trainer_bufs))(*trainer_bufs)
+    L.check(_lib().gmi_channel_run(C.byref(wc), C.byref(pc), C.byref(tc), C.byref(cc), float(duration), ab,
+                                   len(agent_bufs), tb, len(trainer_bufs), int(trainer_capacity),
+                                   C.c_void_p(stream), C.byref(h), C.byref(m)))
+    return _metrics_from_handle(h, m)
+
+
+def _metrics_from_handle(h, m) -> PipelineMetrics:
     try:
         out = PipelineMetrics(m.pps, m.ttop, m.records_produced, m.records_delivered, m.units_sent,
                               m.batches_emitted, m.bytes_moved, m.transfer_busy_time,

@@ -3,7 +3,7 @@
 dram__bytes_write.sum --clock-control none --csv --log-file X.csv python bench.py ...`) over the
 last iteration (from the last control_advance_kernel launch on): per-kernel total time, share,
 launch count, average time and DRAM bytes per launch. With --traffic, also writes
-profiles/traffic.json (the bench's roofline.traffic: DRAM bytes per gemm_tcgen05_kernel launch).
+profiles/traffic.json (the bench's roofline.traffic: DRAM bytes per launch of each GEMM family).
 
     python tools/launch_summary.py profiles/r1/v19_launches.csv > profiles/r1/v19_launch_summary.txt
 """
@@ -50,16 +50,23 @@ def main():
               f"dram={g['dram'] / g['n'] / 1e6:8.2f}MB {name}")
     print(f"total {total / 1e3:.1f} us {len(it)} launches (one iteration, ncu-serialised, cold caches between kernels)")
     if a.traffic:
-        gem = [d for d in it if d["name"].startswith("void gemm_tcgen05_kernel")]
-        per = sum(d.get("dram__bytes_read.sum", 0.0) + d.get("dram__bytes_write.sum", 0.0) for d in gem) / max(1, len(gem))
+        # per GEMM family (template = <BN, A_MN, B_MN, EPI, WS, CS>): forward = EPI 0 (bias + ELU),
+        # input gradient = EPI 1 (elu' product), weight gradient = EPI 2 (split-K fp32 slabs)
+        fam = {"fwd": ", 0>", "dx": "1, 1, 0>", "dw": "2, 0, 1>"}
+        kernels = {}
+        for key in fam:
+            epi = {"fwd": 0, "dx": 1, "dw": 2}[key]
+            sel = [d for d in it if d["name"].startswith("void gemm_tcgen05_kernel")
+                   and d["name"].split("<")[1].split(",")[3].strip() == str(epi)]
+            byt = sum(d.get("dram__bytes_read.sum", 0.0) + d.get("dram__bytes_write.sum", 0.0) for d in sel)
+            kernels[key] = {"dram_bytes_per_launch": byt / max(1, len(sel)), "launches": len(sel),
+                            "templates": sorted({d["name"].split("(")[0].replace("void ", "") for d in sel})}
         with open(a.traffic, "w") as f:
             json.dump({"source": f"{os.path.relpath(a.csv)} (ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,"
                                  "dram__bytes_write.sum --clock-control none over `python bench.py --steps 2 --warmup 1`;"
-                                 f" the {len(gem)} gemm_tcgen05_kernel launches of the last iteration, caches flushed"
-                                 " between kernels)",
-                       "gemm_tcgen05_kernel": {"dram_bytes_per_launch": per, "launches": len(gem)}}, f, indent=1)
+                                 " the GEMM launches of the last iteration, caches flushed between kernels)",
+                       "kernels": kernels}, f, indent=1)
             f.write("\n")
-
 
 if __name__ == "__main__":
     main()
