@@ -72,44 +72,63 @@ __global__ void __launch_bounds__(256) exchange_adam_kernel(const __grid_constan
   const long long st = s - 1;  // completed updates before this one (bias-correction index)
   const float bc1 = a.bc[2 * st], bc2 = a.bc[2 * st + 1];
   const float ob1 = __fsub_rn(1.0f, a.b1), ob2 = __fsub_rn(1.0f, a.b2);
+  // Each thread owns up to kX elements of the shard per pass (stride = the grid), and issues all
+  // of their loads before any store: the parameter / moment buffers may alias as far as the
+  // compiler knows, so interleaving would serialise one memory round trip per element.
+  constexpr int kX = 8;
   const long long stride = (long long)gridDim.x * blockDim.x;
-#pragma unroll 4
-  for (long long i = a.lo + (long long)blockIdx.x * blockDim.x + threadIdx.x; i < a.hi; i += stride) {
-    // chunk cg = the ring chunk holding element i (chunk c = [P c / G, P (c + 1) / G),
-    // reduction.hpp:164-166); every ring fold starts at member cg
-    int cg = 0;
-    while (cg + 1 < a.G && i >= a.chunk0[cg + 1]) ++cg;
-    float acc = 0.f;
-    if (!a.mrr) {  // HAR leader ring (or one rank): the ranks' K1 folds in ring order
-      for (int j = 0; j < a.G; ++j) {
-        int q = cg + j;
-        q -= q >= a.G ? a.G : 0;
-        const float x = __ldcg(a.pub[q] + i);  // peer memory: L2 of the owner, never a stale L1 line
-        acc = j == 0 ? x : __fadd_rn(x, acc);
-      }
-    } else {  // MRR: ring r = GMI r of ranks r, r+1, ...; ring results into a zero total in ring order
-      for (int r = 0; r < a.t; ++r) {
-        float ring = 0.f;
+  for (long long base = a.lo + (long long)blockIdx.x * blockDim.x + threadIdx.x; base < a.hi; base += kX * stride) {
+    float gsum[kX], m0[kX], v0[kX], p0[kX];
+#pragma unroll
+    for (int u = 0; u < kX; ++u) {
+      const long long i = base + u * stride;
+      gsum[u] = m0[u] = v0[u] = p0[u] = 0.f;
+      if (i >= a.hi) continue;
+      // chunk cg = the ring chunk holding element i (chunk c = [P c / G, P (c + 1) / G),
+      // reduction.hpp:164-166); every ring fold starts at member cg
+      int cg = 0;
+      while (cg + 1 < a.G && i >= a.chunk0[cg + 1]) ++cg;
+      float acc = 0.f;
+      if (!a.mrr) {  // HAR leader ring (or one rank): the ranks' K1 folds in ring order
         for (int j = 0; j < a.G; ++j) {
-          int q = r + cg + j;
-          q %= a.G;
-          const float x = __ldcg(a.gpub[q][r] + i);
-          ring = j == 0 ? x : __fadd_rn(x, ring);
+          int q = cg + j;
+          q -= q >= a.G ? a.G : 0;
+          const float x = __ldcg(a.pub[q] + i);  // peer memory: L2 of the owner, never a stale L1 line
+          acc = j == 0 ? x : __fadd_rn(x, acc);
         }
-        acc = __fadd_rn(acc, ring);
+      } else {  // MRR: ring r = GMI r of ranks r, r+1, ...; ring results into a zero total in ring order
+        for (int r = 0; r < a.t; ++r) {
+          float ring = 0.f;
+          for (int j = 0; j < a.G; ++j) {
+            int q = r + cg + j;
+            q %= a.G;
+            const float x = __ldcg(a.gpub[q][r] + i);
+            ring = j == 0 ? x : __fadd_rn(x, ring);
+          }
+          acc = __fadd_rn(acc, ring);
+        }
       }
+      gsum[u] = acc;
+      m0[u] = a.m[i];
+      v0[u] = a.v[i];
+      p0[u] = a.params[a.rank][i];
     }
-    const float g = __fmul_rn(acc, a.inv_n);
-    const float m = __fadd_rn(__fmul_rn(a.b1, a.m[i]), __fmul_rn(ob1, g));
-    const float v = __fadd_rn(__fmul_rn(a.b2, a.v[i]), __fmul_rn(__fmul_rn(ob2, g), g));
-    a.m[i] = m;
-    a.v[i] = v;
-    const float mh = __fdiv_rn(m, bc1), vh = __fdiv_rn(v, bc2);
-    const float p = __fsub_rn(a.params[a.rank][i], __fmul_rn(a.lr, __fdiv_rn(mh, __fadd_rn(__fsqrt_rn(vh), a.eps))));
-    const __nv_bfloat16 sh = __float2bfloat16_rn(p);
-    for (int q = 0; q < a.G; ++q) {  // all-gather: the owner writes every replica
-      a.params[q][i] = p;
-      a.shadow[q][i] = sh;
+#pragma unroll
+    for (int u = 0; u < kX; ++u) {
+      const long long i = base + u * stride;
+      if (i >= a.hi) continue;
+      const float g = __fmul_rn(gsum[u], a.inv_n);
+      const float m = __fadd_rn(__fmul_rn(a.b1, m0[u]), __fmul_rn(ob1, g));
+      const float v = __fadd_rn(__fmul_rn(a.b2, v0[u]), __fmul_rn(__fmul_rn(ob2, g), g));
+      a.m[i] = m;
+      a.v[i] = v;
+      const float mh = __fdiv_rn(m, bc1), vh = __fdiv_rn(v, bc2);
+      const float p = __fsub_rn(p0[u], __fmul_rn(a.lr, __fdiv_rn(mh, __fadd_rn(__fsqrt_rn(vh), a.eps))));
+      const __nv_bfloat16 sh = __float2bfloat16_rn(p);
+      for (int q = 0; q < a.G; ++q) {  // all-gather: the owner writes every replica
+        a.params[q][i] = p;
+        a.shadow[q][i] = sh;
+      }
     }
   }
   __syncthreads();  // the CTA's stores happen-before the releases below (bar.sync + release cumulativity)

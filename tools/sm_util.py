@@ -87,6 +87,15 @@ def report(csv_path, probe_path):
     if info["decoupled"] and len(ctxs) >= 2:
         # fewest launches = serving GMI; everything else (trainer green ctx + primary ctx) = trainer
         groups = {"serving (simulator+agent)": [ctxs[0]], "trainer": ctxs[1:]}
+    elif info["backend"] and len(ctxs) >= len(gmis) + 1:
+        # green-context GMIs: the context with the fewest launches is the primary context (the
+        # update stream: K1 fold + Adam, booked separately); the others are the GMIs in creation
+        # order (ncu context ids increase with creation)
+        upd = ctxs[0]
+        green = sorted(ctxs[1:], key=lambda k: int(k) if str(k).isdigit() else str(k))
+        groups = {g["gmi"]: [c] for g, c in zip(gmis, green)}
+        gmis = gmis + [{"gmi": "update stream (primary context)", "sms": info["sms"]}]
+        groups["update stream (primary context)"] = [upd]
     else:
         groups = {g["gmi"]: [] for g in gmis}
         groups[gmis[0]["gmi"]] = ctxs
