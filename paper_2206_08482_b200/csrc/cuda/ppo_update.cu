@@ -187,23 +187,11 @@ __global__ void __launch_bounds__(256) segments_kernel(const __grid_constant__ S
       }
     }
   } else {
-    // unaligned rows (per-CTA partial records: many parts, short rows): the same part order,
-    // with 8 parts x 4 columns of loads in flight instead of one dependent load per part
     float a[4] = {0.f, 0.f, 0.f, 0.f};
-    const int nc = i0 < sg.len ? min(4, sg.len - i0) : 0;
-    for (int p = p0; p < p1; p += 8) {
-      float v[8][4];
 #pragma unroll
-      for (int u = 0; u < 8; ++u)
-#pragma unroll
-        for (int c = 0; c < 4; ++c)
-          v[u][c] = (p + u < p1 && c < nc) ? __ldcs(sg.src + (long long)(p + u) * sg.stride + i0 + c) : 0.f;
-#pragma unroll
-      for (int u = 0; u < 8; ++u)
-        if (p + u < p1)
-#pragma unroll
-          for (int c = 0; c < 4; ++c) a[c] += v[u][c];
-    }
+    for (int c = 0; c < 4; ++c)
+      if (i0 + c < sg.len)
+        for (int p = p0; p < p1; ++p) a[c] += sg.src[(long long)p * sg.stride + i0 + c];
     acc = make_float4(a[0], a[1], a[2], a[3]);
   }
   acc_s[warp][lane] = acc;
