@@ -40,9 +40,28 @@ __device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned l
   asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-__device__ __forceinline__ void spin_until(const unsigned long long* p, unsigned long long target) {
+__device__ __forceinline__ unsigned long long ld_acquire_gpu(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void st_release_gpu(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// Flags of a one-rank exchange never leave the GPU: device scope avoids the system-scope
+// memory barrier (ERRBAR) a release.sys costs every CTA.
+__device__ __forceinline__ void flag_store(unsigned long long* p, unsigned long long v, bool sys) {
+  if (sys)
+    st_release_sys(p, v);
+  else
+    st_release_gpu(p, v);
+}
+
+__device__ __forceinline__ void spin_until(const unsigned long long* p, unsigned long long target, bool sys) {
   unsigned ns = 32;
-  while (ld_acquire_sys(p) < target) {
+  while ((sys ? ld_acquire_sys(p) : ld_acquire_gpu(p)) < target) {
     __nanosleep(ns);
     ns = ns < 1024 ? ns * 2 : ns;
   }
@@ -60,11 +79,13 @@ __global__ void __launch_bounds__(32) exchange_signal_kernel(const __grid_consta
   pdl_trigger();
   pdl_wait();  // the fold that produced pub[rank] has completed (device scope)
   const long long s = step_id(a);
-  if (threadIdx.x == 0) st_release_sys(a.ready[a.rank], (unsigned long long)s);  // release: orders the fold
-  if (int(threadIdx.x) < a.G) spin_until(a.ready[threadIdx.x], (unsigned long long)s);
+  const bool sys = a.G > 1;
+  if (threadIdx.x == 0) flag_store(a.ready[a.rank], (unsigned long long)s, sys);  // release: orders the fold
+  if (int(threadIdx.x) < a.G) spin_until(a.ready[threadIdx.x], (unsigned long long)s, sys);
   __syncwarp();
 }
 
+template <int MRR>
 __global__ void __launch_bounds__(256) exchange_adam_kernel(const __grid_constant__ ExchangeArgs a) {
   pdl_trigger();
   pdl_wait();  // exchange_signal_kernel completed: every peer's gradient of this step is published
@@ -72,24 +93,25 @@ __global__ void __launch_bounds__(256) exchange_adam_kernel(const __grid_constan
   const long long st = s - 1;  // completed updates before this one (bias-correction index)
   const float bc1 = a.bc[2 * st], bc2 = a.bc[2 * st + 1];
   const float ob1 = __fsub_rn(1.0f, a.b1), ob2 = __fsub_rn(1.0f, a.b2);
-  // Each thread owns up to kX elements of the shard per pass (stride = the grid), and issues all
-  // of their loads before any store: the parameter / moment buffers may alias as far as the
-  // compiler knows, so interleaving would serialise one memory round trip per element.
-  constexpr int kX = 8;
+  float* __restrict__ mom = a.m;
+  float* __restrict__ vel = a.v;
+  const float* __restrict__ own = a.params[a.rank];
+  // Each thread owns up to kX elements per pass and issues all their loads before any store
+  // (kept small and not unrolled over the ranks: the kernel stays inside the instruction cache).
+  constexpr int kX = 4;
   const long long stride = (long long)gridDim.x * blockDim.x;
   for (long long base = a.lo + (long long)blockIdx.x * blockDim.x + threadIdx.x; base < a.hi; base += kX * stride) {
     float gsum[kX], m0[kX], v0[kX], p0[kX];
 #pragma unroll
     for (int u = 0; u < kX; ++u) {
-      const long long i = base + u * stride;
-      gsum[u] = m0[u] = v0[u] = p0[u] = 0.f;
-      if (i >= a.hi) continue;
+      const long long i = min(base + u * stride, a.hi - 1);  // clamped: duplicates are not stored
       // chunk cg = the ring chunk holding element i (chunk c = [P c / G, P (c + 1) / G),
       // reduction.hpp:164-166); every ring fold starts at member cg
       int cg = 0;
       while (cg + 1 < a.G && i >= a.chunk0[cg + 1]) ++cg;
       float acc = 0.f;
-      if (!a.mrr) {  // HAR leader ring (or one rank): the ranks' K1 folds in ring order
+      if (!MRR) {  // HAR leader ring (or one rank): the ranks' K1 folds in ring order
+#pragma unroll 1
         for (int j = 0; j < a.G; ++j) {
           int q = cg + j;
           q -= q >= a.G ? a.G : 0;
@@ -97,8 +119,10 @@ __global__ void __launch_bounds__(256) exchange_adam_kernel(const __grid_constan
           acc = j == 0 ? x : __fadd_rn(x, acc);
         }
       } else {  // MRR: ring r = GMI r of ranks r, r+1, ...; ring results into a zero total in ring order
+#pragma unroll 1
         for (int r = 0; r < a.t; ++r) {
           float ring = 0.f;
+#pragma unroll 1
           for (int j = 0; j < a.G; ++j) {
             int q = r + cg + j;
             q %= a.G;
@@ -109,22 +133,23 @@ __global__ void __launch_bounds__(256) exchange_adam_kernel(const __grid_constan
         }
       }
       gsum[u] = acc;
-      m0[u] = a.m[i];
-      v0[u] = a.v[i];
-      p0[u] = a.params[a.rank][i];
+      m0[u] = mom[i];
+      v0[u] = vel[i];
+      p0[u] = own[i];
     }
 #pragma unroll
     for (int u = 0; u < kX; ++u) {
       const long long i = base + u * stride;
-      if (i >= a.hi) continue;
+      if (i >= a.hi) break;
       const float g = __fmul_rn(gsum[u], a.inv_n);
       const float m = __fadd_rn(__fmul_rn(a.b1, m0[u]), __fmul_rn(ob1, g));
       const float v = __fadd_rn(__fmul_rn(a.b2, v0[u]), __fmul_rn(__fmul_rn(ob2, g), g));
-      a.m[i] = m;
-      a.v[i] = v;
+      mom[i] = m;
+      vel[i] = v;
       const float mh = __fdiv_rn(m, bc1), vh = __fdiv_rn(v, bc2);
       const float p = __fsub_rn(p0[u], __fmul_rn(a.lr, __fdiv_rn(mh, __fadd_rn(__fsqrt_rn(vh), a.eps))));
       const __nv_bfloat16 sh = __float2bfloat16_rn(p);
+#pragma unroll 1
       for (int q = 0; q < a.G; ++q) {  // all-gather: the owner writes every replica
         a.params[q][i] = p;
         a.shadow[q][i] = sh;
@@ -135,7 +160,7 @@ __global__ void __launch_bounds__(256) exchange_adam_kernel(const __grid_constan
   // one flag per (rank, CTA) in every destination's window -- plain release stores, no
   // contended atomics on one counter
   if (int(threadIdx.x) < a.G)
-    st_release_sys(a.done[threadIdx.x] + a.rank * kMaxXchgCtas + blockIdx.x, (unsigned long long)s);
+    flag_store(a.done[threadIdx.x] + a.rank * kMaxXchgCtas + blockIdx.x, (unsigned long long)s, a.G > 1);
 }
 
 // One CTA: wait until every (source rank, CTA) flag in this rank's window reached step s.
@@ -145,7 +170,7 @@ __global__ void __launch_bounds__(256) exchange_wait_kernel(const __grid_constan
   const unsigned long long s = (unsigned long long)step_id(a);
   for (int f = threadIdx.x; f < a.G * a.ctas; f += blockDim.x) {
     const int q = f / a.ctas, c = f - q * a.ctas;
-    spin_until(a.done[a.rank] + q * kMaxXchgCtas + c, s);
+    spin_until(a.done[a.rank] + q * kMaxXchgCtas + c, s, a.G > 1);
   }
   __syncthreads();
 }
@@ -156,7 +181,10 @@ void launch_exchange_adam(const ExchangeArgs& a, cudaStream_t s) {
   if (a.G < 1 || a.G > kMaxRanks) invalid("exchange: 1..8 ranks");
   if (a.ctas < 1 || a.ctas > kMaxXchgCtas) invalid("exchange: 1..148 CTAs");
   launch_pdl(exchange_signal_kernel, dim3(1), dim3(32), 0, s, a);
-  launch_pdl(exchange_adam_kernel, dim3(a.ctas), dim3(256), 0, s, a);
+  if (a.mrr)
+    launch_pdl(exchange_adam_kernel<1>, dim3(a.ctas), dim3(256), 0, s, a);
+  else
+    launch_pdl(exchange_adam_kernel<0>, dim3(a.ctas), dim3(256), 0, s, a);
   launch_pdl(exchange_wait_kernel, dim3(1), dim3(256), 0, s, a);
 }
 
