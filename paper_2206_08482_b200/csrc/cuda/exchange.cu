@@ -179,7 +179,7 @@ __global__ void __launch_bounds__(256) exchange_wait_kernel(const __grid_constan
 
 void launch_exchange_adam(const ExchangeArgs& a, cudaStream_t s) {
   if (a.G < 1 || a.G > kMaxRanks) invalid("exchange: 1..8 ranks");
-  if (a.ctas < 1 || a.ctas > kMaxXchgCtas) invalid("exchange: 1..148 CTAs");
+  if (a.ctas < 1 || a.ctas > kMaxXchgCtas) invalid("exchange: 1..1184 CTAs");
   launch_pdl(exchange_signal_kernel, dim3(1), dim3(32), 0, s, a);
   if (a.mrr)
     launch_pdl(exchange_adam_kernel<1>, dim3(a.ctas), dim3(256), 0, s, a);

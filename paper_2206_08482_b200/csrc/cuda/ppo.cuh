@@ -100,9 +100,9 @@ struct SegAdam {
 // Cross-GPU exchange + sharded Adam over peer memory (cuda/exchange.cu).
 constexpr int kMaxRanks = 8;
 constexpr int kMaxLocalGmis = 16;
-constexpr int kMaxXchgCtas = 148;       // exchange grid (one CTA per SM at most)
+constexpr int kMaxXchgCtas = 1184;      // exchange grid (8 CTAs per SM at most)
 constexpr int kXchgDoneOff = 1024;      // window: done flags [kMaxRanks][kMaxXchgCtas] u64 from here
-constexpr int kXchgHeader = 16384;      // window header bytes (ready flag + done flags)
+constexpr int kXchgHeader = 1024 + kMaxRanks * kMaxXchgCtas * 8;  // ready flag + done flags (~75 KB)
 struct ExchangeArgs {
   int mrr;                               // 0: leader ring over pub (HAR / one rank), 1: MRR over gpub
   int t;                                 // GMIs per rank (MRR)

@@ -277,7 +277,7 @@ void Trainer::init(const void* nccl_id) {
     for (int c = 0; c < cfg.num_gpus; ++c) xa_.chunk0[c] = geo_.P * c / cfg.num_gpus;
     xa_.lo = geo_.P * cfg.rank / cfg.num_gpus;
     xa_.hi = geo_.P * (cfg.rank + 1) / cfg.num_gpus;
-    // same on every rank (the done counter target is steps x G x ctas)
+    // one pass of 4 elements per thread over the shard (same on every rank: the wait counts G x C flags)
     xa_.ctas = int(std::max<long long>(1, std::min<long long>(ppo::kMaxXchgCtas, (geo_.P / cfg.num_gpus + 1023) / 1024)));
     if (cfg.num_gpus == 1) {  // one rank: the exchange runs over the rank itself
       Trainer* self = this;
