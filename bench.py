@@ -357,9 +357,10 @@ def relaunch(args):
 
 
 # ------------------------------------------------------------------ our arm
-def time_trainer(cfg, steps, warmup, world, barrier, instrument=True):
+def time_trainer(cfg, steps, warmup, world, barrier, instrument=True, tune=None):
     """Device-timed K iterations of one trainer (max over ranks), then one instrumented iteration
-    for the per-unit (per-GMI) busy time. Returns (value, ms_per_step, units, trainer stats)."""
+    for the per-unit (per-GMI) busy time. Returns (value, ms_per_step, units) and, with `tune`
+    (candidate SM splits), the measured split choice of gmi_ppo_tune_shares made first."""
     import torch
     import torch.distributed as dist
 
@@ -367,6 +368,12 @@ def time_trainer(cfg, steps, warmup, world, barrier, instrument=True):
     upd = torch.cuda.ExternalStream(t.stream(-1))
     for _ in range(max(3, warmup)):
         t.iteration()
+    tuning = None
+    if tune:
+        best, tput = t.tune_shares(tune, iters=3)
+        tuning = {"candidates_sms": tune, "env_steps_per_s": tput, "chosen": tune[best]}
+        for _ in range(2):
+            t.iteration()
     barrier()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record(upd)
@@ -391,6 +398,8 @@ def time_trainer(cfg, steps, warmup, world, barrier, instrument=True):
         it_ms = c.elapsed_time(d)
         units = unit_report(t.unit_busy(), it_ms, cfg.decoupled)
     t.close()
+    if tune:
+        return value, ms.item() / steps, units, tuning
     return value, ms.item() / steps, units
 
 
@@ -631,6 +640,16 @@ def other_layouts(args, cfg, w, value, world, barrier):
             "value": v4, "unit": UNIT, "ms_per_step": ms4, "gmi_units": u4,
             "single_context": {"value": v1, "ms_per_step": ms1, "gmi_units": u1},
             "vs_single_context": v4 / v1}
+        # the same HM workload in the decoupled layout; the serving / trainer split is chosen by
+        # the adaptive manager on the live trainer (gmi_ppo_tune_shares over measured candidates)
+        dec = copy.deepcopy(one)
+        dec.decoupled, dec.gmi_backend, dec.serving_sms = 1, 1, 16
+        vd, msd, ud, tuning = time_trainer(dec, args.steps, args.warmup, world, barrier,
+                                           tune=[[8, 0], [16, 0], [24, 0]])
+        out["config2_hm_4gmi"]["decoupled"] = {
+            "layout": "serving GMI (simulator+agent, per-layer rollout + critic on its partition) + trainer GMI, "
+                      "device experience channel, one-iteration policy lag",
+            "value": vd, "ms_per_step": msd, "gmi_units": ud, "vs_single_context": vd / v1, "tuning": tuning}
     except Exception as e:  # noqa: BLE001
         out["config2_hm_4gmi"] = {"error": f"{type(e).__name__}: {e}"}
     return out

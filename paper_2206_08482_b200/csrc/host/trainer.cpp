@@ -165,6 +165,14 @@ struct Trainer::Gmi {
   int head_grid = 0;
   ppo::HeadFusedArgs head_args{};
   bool fused_fwd = false;  // hidden forward + head step in one launch (train_fwd.cu)
+  // decoupled mode, nets too wide for the fused rollout / value kernels: the serving GMI's own
+  // per-layer plans (channel observations, snapshot weights, its own activation buffers)
+  bool srv_layers = false;
+  int srv_ctas = 0;
+  __nv_bfloat16* srv_H[2][GMI_MAX_HIDDEN] = {};
+  float* srv_outh[2] = {};
+  GemmParams srv_fwd_roll[GMI_MAX_HIDDEN], srv_fwd_val[GMI_MAX_HIDDEN], srv_head_roll, srv_head_val;
+  int srv_bn_roll[GMI_MAX_HIDDEN] = {}, srv_bn_val[GMI_MAX_HIDDEN] = {}, srv_ws_val[GMI_MAX_HIDDEN] = {};
   ppo::TrainFwdArgs fwd_args{};
 };
 
@@ -258,8 +266,6 @@ void Trainer::init(const void* nccl_id) {
   alloc();
   init_params();
   build_plans();
-  if (decoupled_ && !(gmis_[0]->fused_roll && gmis_[0]->fused_val))
-    invalid("decoupled mode needs the fused rollout and value pass (hidden widths <= 256, <= 4 layers)");
   ensure_bias_table(1 << 20);
   if (xchg_) {
     // Alg. 1 on the job layout (GPU-major ids, t per GPU) decides the cross-GPU fold order
@@ -904,6 +910,129 @@ void Trainer::build_plans() {
       const char* trace = std::getenv("GMI_ROLLOUT_TRACE");
       if (trace && trace[0] == '1') r.trace = reinterpret_cast<unsigned long long*>(dev((size_t)T_ * 16 * 8));
     }
+    if (decoupled_ && !(g.fused_roll && g.fused_val)) build_serving_plans(g);
+  }
+}
+
+// Decoupled mode with nets the fused rollout / value kernels cannot hold (widths > 256): the
+// serving GMI runs the per-layer path on its own partition -- the same GEMMs as the synchronous
+// rollout, but reading the experience channel's observations and the policy snapshot, and
+// writing its own activation buffers (the trainer GMI's are busy training concurrently).
+void Trainer::build_serving_plans(Gmi& g) {
+  const int L = geo_.L, S_p = geo_.wp[0], A = geo_.A, hp = geo_.wp[L];
+  auto dev = [&](size_t bytes) {
+    void* p = nullptr;
+    GMI_CUDA_CHECK(cudaMalloc(&p, std::max<size_t>(bytes, 256)));
+    GMI_CUDA_CHECK(cudaMemset(p, 0, std::max<size_t>(bytes, 256)));
+    plan_allocs_.push_back(p);
+    return p;
+  };
+  g.srv_layers = true;
+  g.srv_ctas = exec_->sm_count(0) > 0 ? exec_->sm_count(0) : device_sm_count();
+  const long long rollrows = (long long)(T_ + 1) * g.N;
+  for (int n = 0; n < 2; ++n) {
+    for (int l = 0; l < L; ++l)
+      g.srv_H[n][l] = static_cast<__nv_bfloat16*>(dev((size_t)g.Mrows * geo_.wp[l + 1] * 2));
+    g.srv_outh[n] = static_cast<float*>(dev((size_t)g.Mrows * ppo::kHeadG * 4));
+  }
+  for (int l = 0; l < L; ++l) {
+    const int in_p = geo_.wp[l], out_p = geo_.wp[l + 1];
+    auto problem = [&](int n, const CUtensorMap& amap, int M, int bn) {
+      GemmProblem p{};
+      p.map_a = amap;
+      p.map_b = tma_kmajor(shadow_roll_ + geo_.net[n][l].w, in_p, out_p, in_p, bn);
+      p.map_out = make_tma_out_bf16(g.srv_H[n][l], out_p, g.Mrows, out_p);
+      p.bias = params_roll_ + geo_.net[n][l].b;
+      p.M = M;
+      p.N = out_p;
+      p.K = in_p;
+      p.kb_per_split = (in_p + kGemmBlockK - 1) / kGemmBlockK;
+      return p;
+    };
+    g.srv_bn_roll[l] = gemm_choose_bn(g.N, out_p, 1, 1, g.srv_ctas);
+    const CUtensorMap a_roll = l == 0 ? tma_kmajor(g.ch_X, S_p, rollrows, S_p, kGemmBlockM)
+                                      : tma_kmajor(g.srv_H[0][l - 1], in_p, g.Mrows, in_p, kGemmBlockM);
+    g.srv_fwd_roll[l] = GemmParams{};
+    g.srv_fwd_roll[l].prob[0] = problem(0, a_roll, g.N, g.srv_bn_roll[l]);
+    g.srv_fwd_roll[l].num_problems = 1;
+    g.srv_fwd_roll[l].splits = 1;
+    const int ws_val = gemm_ws_bn(g.Mrows, out_p, in_p, 1, g.srv_ctas);
+    g.srv_ws_val[l] = ws_val > 0;
+    g.srv_bn_val[l] = ws_val > 0 ? ws_val : gemm_choose_bn(g.Mrows, out_p, 1, 1, g.srv_ctas);
+    const CUtensorMap a_val = l == 0 ? tma_kmajor(g.ch_X, S_p, rollrows, S_p, kGemmBlockM)
+                                     : tma_kmajor(g.srv_H[1][l - 1], in_p, g.Mrows, in_p, kGemmBlockM);
+    g.srv_fwd_val[l] = GemmParams{};
+    g.srv_fwd_val[l].prob[0] = problem(1, a_val, g.Mrows, g.srv_bn_val[l]);
+    g.srv_fwd_val[l].num_problems = 1;
+    g.srv_fwd_val[l].splits = 1;
+  }
+  const int head_rows[2] = {A, 1};
+  for (int n = 0; n < 2; ++n) {
+    GemmProblem p{};
+    p.map_a = tma_kmajor(g.srv_H[n][L - 1], hp, g.Mrows, hp, kGemmBlockM);
+    p.map_b = tma_kmajor(shadow_roll_ + geo_.net[n][L].w, hp, head_rows[n], hp, 64);
+    p.map_out = make_tma_out_f32(g.srv_outh[n], ppo::kHeadG, g.Mrows, 1, ppo::kHeadG, (uint64_t)g.Mrows * ppo::kHeadG);
+    p.M = n == 0 ? g.N : g.Mrows;
+    p.N = ppo::kHeadG;
+    p.K = hp;
+    p.kb_per_split = (hp + kGemmBlockK - 1) / kGemmBlockK;
+    GemmParams& P = n == 0 ? g.srv_head_roll : g.srv_head_val;
+    P = GemmParams{};
+    P.prob[0] = p;
+    P.num_problems = 1;
+    P.splits = 1;
+  }
+}
+
+// The serving GMI's rollout + values with the per-layer plans above (decoupled, wide nets).
+void Trainer::serve_rollout_layers(Gmi& g) {
+  const int L = geo_.L, S_p = geo_.wp[0], A = geo_.A;
+  const Tensor& phead = geo_.net[0][L];
+  const Tensor& vhead = geo_.net[1][L];
+  const double env_bytes = double(g.N) * (8.0 * A + 8.0 * geo_.S + 2.0 * S_p + 29.0);
+  for (int t = 0; t < T_; ++t) {
+    for (int l = 0; l < L; ++l) {
+      GemmParams P = g.srv_fwd_roll[l];
+      if (l == 0) P.prob[0].a_row0 = t * g.N;
+      gemm(g, GMI_PH_ROLL_GEMM, P, g.srv_bn_roll[l], 0, 0, EPI_BIAS_ELU, g.flop_roll[l], 0, serve_s_, g.srv_ctas);
+    }
+    gemm(g, GMI_PH_ROLL_HEAD, g.srv_head_roll, 64, 0, 0, EPI_F32, 2.0 * A * geo_.width[L] * g.N, 0, serve_s_,
+         g.srv_ctas);
+    ppo::ActEnvArgs a{};
+    a.ep = {g.N, geo_.S, A, S_p, g.env0, T_, cfg_.seed};
+    a.mu = g.srv_outh[0];
+    a.b_mu = params_roll_ + phead.b;
+    a.log_std = params_roll_ + geo_.log_std;
+    a.x = g.x;
+    a.ep_step = g.ep_step;
+    a.ep_len = g.ep_len;
+    a.ep_count = g.ep_count;
+    a.X_next = g.ch_X + (long long)(t + 1) * g.N * S_p;
+    a.act = g.ch_act + (long long)t * g.N * A;
+    a.logp = g.ch_logp + (long long)t * g.N;
+    a.rew = g.ch_rew + (long long)t * g.N;
+    a.done = g.ch_done + (long long)t * g.N;
+    a.t = t;
+    a.ctl = ctl_roll_;
+    timed(serve_s_, GMI_PH_ACT_ENV, 0.0, env_bytes, [&] { ppo::launch_act_env(a, serve_s_); });
+    ++launches_;
+  }
+  const long long rows = (long long)(T_ + 1) * g.N;
+  for (long long c0 = 0; c0 < rows; c0 += g.Mrows) {
+    const int m = int(std::min<long long>(g.Mrows, rows - c0));
+    for (int l = 0; l < L; ++l) {
+      GemmParams P = g.srv_fwd_val[l];
+      P.prob[0].M = m;
+      if (l == 0) P.prob[0].a_row0 = int(c0);
+      gemm(g, GMI_PH_VAL_GEMM, P, g.srv_bn_val[l], 0, 0, EPI_BIAS_ELU, g.flop_roll[l] * double(m) / g.N,
+           g.srv_ws_val[l], serve_s_, g.srv_ctas);
+    }
+    GemmParams Ph = g.srv_head_val;
+    Ph.prob[0].M = m;
+    gemm(g, GMI_PH_VAL_HEAD, Ph, 64, 0, 0, EPI_F32, 2.0 * geo_.width[L] * m, 0, serve_s_, g.srv_ctas);
+    timed(serve_s_, GMI_PH_VAL_HEAD, 0.0, 8.0 * m,
+          [&] { ppo::launch_value_head(g.srv_outh[1], params_roll_ + vhead.b, g.ch_V + c0, m, serve_s_); });
+    ++launches_;
   }
 }
 
@@ -1315,16 +1444,20 @@ void Trainer::serve_rollout(Gmi& g) {
       GMI_CUDA_CHECK(cudaMemcpyAsync(g.ch_X, g.ch_X + (long long)T_ * g.N * S_p, (size_t)g.N * S_p * 2,
                                      cudaMemcpyDeviceToDevice, serve_s_));
     });
-  timed(serve_s_, GMI_PH_ROLL_GEMM, 0.0, 0.0, [&] {
-    if (g.roll_cluster)
-      ppo::launch_rollout_cluster(g.roll_args, g.roll_cluster, serve_s_);
-    else
-      ppo::launch_rollout(g.roll_args, serve_s_);
-  });
-  // values of all T+1 observation slots with the same snapshot, then GAE: the channel carries
-  // ready advantages / returns, so the trainer starts straight at the epoch shuffle
-  const int sms = exec_->sm_count(0) > 0 ? exec_->sm_count(0) : device_sm_count();
-  timed(serve_s_, GMI_PH_VAL_GEMM, 0.0, 0.0, [&] { ppo::launch_value_mlp(g.ch_val_args, sms, serve_s_); });
+  if (g.srv_layers) {  // wide nets: the per-layer path on the serving partition
+    serve_rollout_layers(g);
+  } else {
+    timed(serve_s_, GMI_PH_ROLL_GEMM, 0.0, 0.0, [&] {
+      if (g.roll_cluster)
+        ppo::launch_rollout_cluster(g.roll_args, g.roll_cluster, serve_s_);
+      else
+        ppo::launch_rollout(g.roll_args, serve_s_);
+    });
+    // values of all T+1 observation slots with the same snapshot, then GAE: the channel carries
+    // ready advantages / returns, so the trainer starts straight at the epoch shuffle
+    const int sms = exec_->sm_count(0) > 0 ? exec_->sm_count(0) : device_sm_count();
+    timed(serve_s_, GMI_PH_VAL_GEMM, 0.0, 0.0, [&] { ppo::launch_value_mlp(g.ch_val_args, sms, serve_s_); });
+  }
   timed(serve_s_, GMI_PH_GAE, 0.0, 0.0, [&] {
     ppo::launch_gae(g.ch_rew, g.ch_done, g.ch_V, g.ch_adv, g.ch_ret, g.ch_gae_part, g.N, T_, cfg_.gamma, cfg_.lam,
                     serve_s_);

@@ -61,6 +61,8 @@ class Trainer {
   void write_control();
   void record_iteration(bool with_rollout);  // one iteration's launches (eager or under capture)
   void serve_rollout(Gmi& g);  // decoupled mode: the serving GMI's rollout into the channel
+  void build_serving_plans(Gmi& g);   // decoupled mode, wide nets: per-layer serving plans
+  void serve_rollout_layers(Gmi& g);  // ... and their launches
   void rollout(Gmi& g);
   void values(Gmi& g);
   void train_minibatch(Gmi& g, int k, int adam_step = -1);  // adam_step >= 0: fused Adam

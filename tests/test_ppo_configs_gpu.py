@@ -126,3 +126,22 @@ def test_config4_sh_gmis(cuda, gmis, backend):
     """BASELINE configs[4] shapes: SH 211:512:512:512:256:20 (P = 1,535,765) at 64 envs per GMI,
     2 GMIs (streams) and 7 GMIs (7 x 16-SM green contexts)."""
     _run(211, 20, [512, 512, 512, 256], 64 * gmis, iters=1, gmis_per_gpu=gmis, gmi_backend=backend)
+
+
+@pytest.mark.parametrize("serving_sms", [16, 32])
+def test_decoupled_wide_nets_match_oracle(cuda, serving_sms):
+    """Decoupled layout with HM-width nets (108:200:400:100:21): the serving GMI runs the
+    per-layer rollout / value path on its partition (the fused kernels hold <= 256 widths) with
+    the policy snapshot; two iterations against the oracle's lagged schedule."""
+    S, A, hidden = 108, 21, [200, 400, 100]
+    dev, orc = _make(S, A, hidden, 256, decoupled=1, gmi_backend=1, serving_sms=serving_sms)
+    th0 = orc.get("params").astype(np.float64)
+    for it in range(2):
+        dev.iteration()
+        orc.iteration_decoupled()
+        assert np.array_equal(dev.get("done"), orc.get("done")), it
+        for f in ("rew", "adv"):
+            _close(f"{f}[{it}]", dev.get(f), orc.get(f), *TRAJ[f])
+    d_dev = dev.get("params").astype(np.float64) - th0
+    d_orc = orc.get("params").astype(np.float64) - th0
+    assert _rel(d_dev, d_orc) <= 2e-2, _rel(d_dev, d_orc)
