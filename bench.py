@@ -372,6 +372,7 @@ def time_trainer(cfg, steps, warmup, world, barrier, instrument=True, tune=None)
     if tune:
         best, tput = t.tune_shares(tune, iters=3)
         tuning = {"candidates_sms": tune, "env_steps_per_s": tput, "chosen": tune[best]}
+        upd = torch.cuda.ExternalStream(t.stream(-1))  # a resize moves the update stream
         for _ in range(2):
             t.iteration()
     barrier()

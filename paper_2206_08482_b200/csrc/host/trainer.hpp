@@ -67,6 +67,7 @@ class Trainer {
   void values(Gmi& g);
   void train_minibatch(Gmi& g, int k, int adam_step = -1);  // adam_step >= 0: fused Adam
   void reduce_and_step(int k);
+  void launch_adam_on(cudaStream_t st, const float* grad, int step_in_iter);
   void gemm(Gmi& g, int phase, const GemmParams& P, int bn, int amn, int bmn, int epi, double flop, int ws = 0,
             cudaStream_t stream = nullptr, int ctas = 0);
   // Runs f (which enqueues work on s); with cfg.instrument and s = GMI 0's stream or the

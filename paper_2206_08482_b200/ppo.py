@@ -243,13 +243,16 @@ class Trainer:
         L.check(L.lib().gmi_ppo_rollout(self._h))
 
     def resize(self, sm_counts: list) -> None:
-        """Re-split this GPU's green-context partitions (gmi_resize); same GMI count."""
+        """Re-split this GPU's green-context partitions (gmi_resize); same GMI count. The GMI
+        streams (and, in the one-GPU decoupled layout, the update stream) are recreated in the new
+        partitions: re-read stream() afterwards."""
         arr = (C.c_int * len(sm_counts))(*sm_counts)
         L.check(L.lib().gmi_resize(self._h, self.cfg.rank, arr, len(sm_counts)))
 
     def tune_shares(self, candidates: list, iters: int = 3):
         """Measured per-role SM-share retuning (gmi_ppo_tune_shares): returns (best index,
-        env-steps/s per candidate); the trainer is left at the best split."""
+        env-steps/s per candidate); the trainer is left at the best split (streams recreated, as
+        for resize())."""
         flat = [x for c in candidates for x in c]
         arr = (C.c_int * len(flat))(*flat)
         out = (C.c_double * len(candidates))()
