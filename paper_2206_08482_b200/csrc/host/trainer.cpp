@@ -1498,8 +1498,7 @@ void Trainer::record_iteration(bool with_rollout) {
   marks_used_ = 0;
   {
     const char* af = std::getenv("GMI_ADAM_FUSED");  // see the fused_adam note below
-    const char* as = std::getenv("GMI_ADAM_STREAM");
-    adam_in_gmi_stream_ = n_local_ == 1 && !nccl_ && !xchg_ && ((af && af[0] == '1') || (as && as[0] == '1'));
+    adam_in_gmi_stream_ = n_local_ == 1 && !nccl_ && !xchg_ && af && af[0] == '1';
   }
   GMI_CUDA_CHECK(cudaEventRecord(ev_start_, upd_));
   if (!with_rollout) {  // trains on the rollout a gmi_ppo_rollout hook produced
@@ -1538,14 +1537,9 @@ void Trainer::record_iteration(bool with_rollout) {
   // iteration), so the separate kernel stays the default.
   const char* adam_fused = std::getenv("GMI_ADAM_FUSED");
   const bool fused_adam = n_local_ == 1 && !nccl_ && !xchg_ && adam_fused && adam_fused[0] == '1';
-  // One GMI, no cross-GMI / cross-GPU step: Adam can follow the gradient assembly on the GMI's own
-  // stream (GMI_ADAM_STREAM=1), removing the two cross-stream hops per minibatch.
-  const char* adam_stream_env = std::getenv("GMI_ADAM_STREAM");
-  const bool adam_stream = !fused_adam && n_local_ == 1 && !nccl_ && !xchg_ && adam_stream_env &&
-                           adam_stream_env[0] == '1';
   for (int e = 0; e < cfg_.epochs; ++e) {
     for (auto& g : gmis_) {
-      if (step > 0 && !fused_adam && !adam_stream) GMI_CUDA_CHECK(cudaStreamWaitEvent(g->s, ev_adam_, 0));
+      if (step > 0 && !fused_adam) GMI_CUDA_CHECK(cudaStreamWaitEvent(g->s, ev_adam_, 0));
       timed(g->s, GMI_PH_SHUFFLE, 0.0, 2.0 * g->B * (2.0 * geo_.wp[0] + 4.0 * geo_.A + 12.0), [&] {
         ppo::launch_shuffle(g->X_roll, g->act, g->logp, g->adv, g->ret, g->adv_stats, g->X_sh, g->act_sh,
                             g->oldlp_sh, g->adv_sh, g->ret_sh, g->N, T_, geo_.wp[0], geo_.A, cfg_.seed, g->gid, e,
@@ -1560,17 +1554,11 @@ void Trainer::record_iteration(bool with_rollout) {
           GMI_CUDA_CHECK(cudaEventRecord(g->ev_done, g->s));
           continue;
         }
-        if (adam_stream) {
-          train_minibatch(*g, k);
-          launch_adam_on(g->s, g->grad, step);
-          GMI_CUDA_CHECK(cudaEventRecord(g->ev_done, g->s));
-          continue;
-        }
         if (step > 0) GMI_CUDA_CHECK(cudaStreamWaitEvent(g->s, ev_adam_, 0));
         train_minibatch(*g, k);
         GMI_CUDA_CHECK(cudaEventRecord(g->ev_done, g->s));
       }
-      if (!fused_adam && !adam_stream) reduce_and_step(step);
+      if (!fused_adam) reduce_and_step(step);
     }
   }
   for (auto& g : gmis_) GMI_CUDA_CHECK(cudaStreamWaitEvent(upd_, g->ev_done, 0));
