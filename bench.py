@@ -383,7 +383,8 @@ def time_trainer(cfg, steps, warmup, world, barrier, instrument=True, tune=None)
     b.record(upd)
     st = t.synchronize()
     barrier()
-    ms = torch.tensor([a.elapsed_time(b)], dtype=torch.float64, device="cuda")
+    ms = torch.tensor([a.elapsed_time(b)], dtype=torch.float64,
+                      device="cpu" if os.environ.get("GMI_BENCH_SHARE_GPU") == "1" else "cuda")
     if world > 1:
         dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     value = st.env_steps * world * steps / (ms.item() / 1e3)
@@ -453,9 +454,17 @@ def main():
         cfg.gmis_per_gpu = w["gmis_per_gpu"] = args.gmis
     envs_per_gpu = w["envs_per_gpu"]
 
+    # GMI_BENCH_SHARE_GPU=1 (tests only): every rank on cuda:0, one process each (time-sliced),
+    # host-side collectives on gloo -- exercises the N > 1 path on a one-GPU box
+    share = os.environ.get("GMI_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     cfg.num_gpus, cfg.rank, cfg.device = world, rank, local
     cfg.num_envs = envs_per_gpu * world
     if args.decoupled is not None:
@@ -496,7 +505,7 @@ def main():
     clk = clocks.stop() if rank == 0 else None
     ms = t0.elapsed_time(t1)
     launches = st.kernel_launches * args.steps
-    ms_t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    ms_t = torch.tensor([ms], dtype=torch.float64, device="cpu" if share else "cuda")
     if world > 1:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
     ms_max = ms_t.item()
@@ -511,7 +520,7 @@ def main():
         trainer.iteration()
     barrier()
     wall = time.perf_counter() - w0
-    wall_t = torch.tensor([wall], dtype=torch.float64, device="cuda")
+    wall_t = torch.tensor([wall], dtype=torch.float64, device="cpu" if share else "cuda")
     if world > 1:
         dist.all_reduce(wall_t, op=dist.ReduceOp.MAX)
     e2e = steps_total / wall_t.item()

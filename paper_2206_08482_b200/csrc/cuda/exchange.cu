@@ -85,7 +85,10 @@ __global__ void __launch_bounds__(32) exchange_signal_kernel(const __grid_consta
   __syncwarp();
 }
 
-template <int MRR>
+// FOLD 0: leader ring over the ranks' published folds (HAR, or one rank with one GMI);
+// FOLD 1: MRR rings over per-GMI gradients; FOLD 2: one rank, the K1 fold of its t GMIs in the
+// MPR ring order (reduction.hpp:164-212) fused in front of Adam -- no separate K1 launch.
+template <int FOLD>
 __global__ void __launch_bounds__(256) exchange_adam_kernel(const __grid_constant__ ExchangeArgs a) {
   pdl_trigger();
   pdl_wait();  // exchange_signal_kernel completed: every peer's gradient of this step is published
@@ -110,7 +113,17 @@ __global__ void __launch_bounds__(256) exchange_adam_kernel(const __grid_constan
       int cg = 0;
       while (cg + 1 < a.G && i >= a.chunk0[cg + 1]) ++cg;
       float acc = 0.f;
-      if (!MRR) {  // HAR leader ring (or one rank): the ranks' K1 folds in ring order
+      if constexpr (FOLD == 2) {  // one rank: MPR ring over its t GMI gradients, chunk c starts at member c
+        int c = 0;
+        while (c + 1 < a.t && i >= a.chunk0_t[c + 1]) ++c;
+#pragma unroll 1
+        for (int j = 0; j < a.t; ++j) {
+          int r = c + j;
+          r -= r >= a.t ? a.t : 0;
+          const float x = a.gpub[0][r][i];
+          acc = j == 0 ? x : __fadd_rn(x, acc);
+        }
+      } else if constexpr (FOLD == 0) {  // HAR leader ring (or one rank): the ranks' K1 folds in ring order
 #pragma unroll 1
         for (int j = 0; j < a.G; ++j) {
           int q = cg + j;
@@ -156,6 +169,7 @@ __global__ void __launch_bounds__(256) exchange_adam_kernel(const __grid_constan
       }
     }
   }
+  if (a.G == 1) return;  // one rank: stream order is the only consumer
   __syncthreads();  // the CTA's stores happen-before the releases below (bar.sync + release cumulativity)
   // one flag per (rank, CTA) in every destination's window -- plain release stores, no
   // contended atomics on one counter
@@ -180,6 +194,13 @@ __global__ void __launch_bounds__(256) exchange_wait_kernel(const __grid_constan
 void launch_exchange_adam(const ExchangeArgs& a, cudaStream_t s) {
   if (a.G < 1 || a.G > kMaxRanks) invalid("exchange: 1..8 ranks");
   if (a.ctas < 1 || a.ctas > kMaxXchgCtas) invalid("exchange: 1..1184 CTAs");
+  if (a.G == 1) {  // one rank: no peers to publish to or wait for; the GMI fold is fused in
+    if (a.t > 1)
+      launch_pdl(exchange_adam_kernel<2>, dim3(a.ctas), dim3(256), 0, s, a);
+    else
+      launch_pdl(exchange_adam_kernel<0>, dim3(a.ctas), dim3(256), 0, s, a);
+    return;
+  }
   launch_pdl(exchange_signal_kernel, dim3(1), dim3(32), 0, s, a);
   if (a.mrr)
     launch_pdl(exchange_adam_kernel<1>, dim3(a.ctas), dim3(256), 0, s, a);

@@ -115,6 +115,7 @@ struct ExchangeArgs {
   int G, rank, ctas;
   long long P, lo, hi;  // flat length; this rank's shard [lo, hi)
   long long chunk0[kMaxRanks];  // ring chunk starts P c / G
+  long long chunk0_t[kMaxLocalGmis];  // local ring chunk starts P c / t (fused K1 fold, one rank)
   float* m;             // Adam moments (only the shard is used)
   float* v;
   const float* bc;

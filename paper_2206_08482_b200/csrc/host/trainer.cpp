@@ -281,10 +281,12 @@ void Trainer::init(const void* nccl_id) {
     xa_.rank = cfg.rank;
     xa_.P = geo_.P;
     for (int c = 0; c < cfg.num_gpus; ++c) xa_.chunk0[c] = geo_.P * c / cfg.num_gpus;
+    for (int c = 0; c < n_local_; ++c) xa_.chunk0_t[c] = geo_.P * c / n_local_;
     xa_.lo = geo_.P * cfg.rank / cfg.num_gpus;
     xa_.hi = geo_.P * (cfg.rank + 1) / cfg.num_gpus;
-    // one pass of 4 elements per thread over the shard (same on every rank: the wait counts G x C flags)
-    xa_.ctas = int(std::max<long long>(1, std::min<long long>(ppo::kMaxXchgCtas, (geo_.P / cfg.num_gpus + 1023) / 1024)));
+    // one element per thread while the shard fits 1184 x 256 threads (latency-bound step: the
+    // widest grid wins); same on every rank (the wait counts G x C flags)
+    xa_.ctas = int(std::max<long long>(1, std::min<long long>(ppo::kMaxXchgCtas, (geo_.P / cfg.num_gpus + 255) / 256)));
     if (cfg.num_gpus == 1) {  // one rank: the exchange runs over the rank itself
       Trainer* self = this;
       comm_connect(&self, 1);
@@ -1370,7 +1372,9 @@ void Trainer::train_minibatch(Gmi& g, int k, int adam_step) {
 void Trainer::reduce_and_step(int step_in_iter) {
   for (auto& g : gmis_) GMI_CUDA_CHECK(cudaStreamWaitEvent(upd_, g->ev_done, 0));
   float* src = gmis_[0]->grad;
-  if (n_local_ > 1 && !(xchg_ && xa_.mrr)) {  // K1: fold the GPU's GMIs in ring order (MPR / HAR step 1)
+  // K1: fold the GPU's GMIs in ring order (MPR / HAR step 1) -- inside the exchange kernel for one
+  // rank, read remotely per GMI for MRR
+  if (n_local_ > 1 && !(xchg_ && (xa_.mrr || cfg_.num_gpus == 1))) {
     plan::Placement p;
     p.per_gpu.resize(1);
     std::vector<void*> bufs;
@@ -1399,9 +1403,10 @@ void Trainer::reduce_and_step(int step_in_iter) {
     // per rank and update and shard element: G (HAR) or G x t (MRR) 4-byte reads, Adam's m / v /
     // p (16 B), 6 B written per replica
     const double shard = double(xa_.hi - xa_.lo), reads = cfg_.num_gpus * (xa_.mrr ? n_local_ : 1);
-    timed(upd_, GMI_PH_ALLREDUCE, 0.0, shard * (4.0 * reads + 16.0 + 6.0 * cfg_.num_gpus),
+    timed(upd_, cfg_.num_gpus == 1 ? GMI_PH_ADAM : GMI_PH_ALLREDUCE, 0.0,
+          shard * (4.0 * (cfg_.num_gpus == 1 ? n_local_ : reads) + 16.0 + 6.0 * cfg_.num_gpus),
           [&] { ppo::launch_exchange_adam(a, upd_); });
-    launches_ += 3;
+    launches_ += cfg_.num_gpus == 1 ? 1 : 3;
     GMI_CUDA_CHECK(cudaEventRecord(ev_adam_, upd_));
     return;
   }

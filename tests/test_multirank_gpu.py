@@ -159,3 +159,21 @@ def test_unwired_rank_hooks_match_oracle_slice(cuda):
             t.iteration()
     with pytest.raises((_lib.GmiError, ValueError)):  # ranks sharing a device need a process each
         Trainer.comm_connect(ts)
+
+
+def test_bench_two_ranks_on_one_gpu(cuda):
+    """The driver's N > 1 bench path (torchrun, one rank per GPU, peer exchange wired over CUDA
+    IPC, max-over-ranks timing, one JSON line) run as 2 rank processes sharing cuda:0
+    (GMI_BENCH_SHARE_GPU=1: time-sliced, so the number is not a measurement)."""
+    import json
+    env = dict(os.environ, GMI_BENCH_SHARE_GPU="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
+           "127.0.0.1", "--master-port", str(_port()), os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "2",
+           "--warmup", "3", "--envs", "256", "--no-cpu-baseline", "--no-multi-gmi"]
+    r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=500)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["run"]["comm"].startswith("peer exchange")
+    assert d["config"]["envs_per_gpu"] == 256
