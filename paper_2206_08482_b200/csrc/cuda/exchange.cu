@@ -107,7 +107,9 @@ __global__ void __launch_bounds__(256) exchange_adam_kernel(const __grid_constan
     float gsum[kX], m0[kX], v0[kX], p0[kX];
 #pragma unroll
     for (int u = 0; u < kX; ++u) {
-      const long long i = min(base + u * stride, a.hi - 1);  // clamped: duplicates are not stored
+      const long long i = base + u * stride;
+      gsum[u] = m0[u] = v0[u] = p0[u] = 0.f;
+      if (i >= a.hi) continue;
       // chunk cg = the ring chunk holding element i (chunk c = [P c / G, P (c + 1) / G),
       // reduction.hpp:164-166); every ring fold starts at member cg
       int cg = 0;
