@@ -42,7 +42,8 @@ def parse():
     p.add_argument("--envs", type=int, default=0, help="override envs per GPU")
     p.add_argument("--backend", type=int, default=None, help="0 streams, 1 green contexts (default: config)")
     p.add_argument("--decoupled", type=int, default=None,
-                   help="1: serving GMI + trainer GMI per GPU with an experience channel (BASELINE config 4)")
+                   help="1: serving GMI + trainer GMI per GPU with an experience channel (BASELINE config 4); "
+                        "2: AsyncDecoupled across GPUs (serving GPUs -> trainer GPUs, even --gpus)")
     p.add_argument("--serving-sms", type=int, default=0, help="SMs of the serving GMI (decoupled mode)")
     p.add_argument("--comm", default="auto", choices=["auto", "peer", "nccl"],
                    help="cross-GPU step: auto = peer exchange for N > 1 (none at N = 1); peer = the fused "
@@ -413,6 +414,20 @@ def make_trainer(cfg, world, rank):
 
     if world == 1:
         return Trainer(cfg)
+    if cfg.decoupled == 2:
+        # AsyncDecoupled across GPUs: serving rank s <-> trainer rank world/2 + s over the link
+        # windows; the trainer ranks' own data-parallel job over the peer exchange
+        t = Trainer(cfg)
+        handles = [None] * world
+        dist.all_gather_object(handles, t.link_handle())
+        t.link_attach(handles[(rank + world // 2) % world])
+        serving = rank < world // 2
+        comm = [None] * world
+        dist.all_gather_object(comm, None if serving or world == 2 else t.comm_handle())
+        if not serving and world > 2:
+            t.comm_attach(comm[world // 2:])
+        dist.barrier()
+        return t
     if cfg.comm == 1:
         t = Trainer(cfg)
         handles = [None] * world
@@ -471,7 +486,12 @@ def main():
         cfg.decoupled = args.decoupled
         if cfg.decoupled:
             cfg.gmis_per_gpu = 1
-            cfg.gmi_backend = 1
+            cfg.gmi_backend = 1 if cfg.decoupled == 1 else 0
+    split = cfg.decoupled == 2
+    if split:  # AsyncDecoupled across GPUs: envs live on the serving half (envs_per_gpu each)
+        if world < 2 or world % 2:
+            raise SystemExit("bench.py: --decoupled 2 needs an even --gpus >= 2")
+        cfg.num_envs = envs_per_gpu * (world // 2)
     if args.serving_sms:
         cfg.serving_sms = args.serving_sms
     if args.backend is not None:
@@ -479,7 +499,9 @@ def main():
     cfg.instrument = 0  # timed loop runs the plain graph; a separate pass below is instrumented
     cfg.comm = 1 if args.comm == "peer" or (args.comm == "auto" and world > 1) else 0
     trainer = make_trainer(cfg, world, rank)
-    upd = torch.cuda.ExternalStream(trainer.stream(-1))
+    serving_rank = split and rank < world // 2
+    # the stream the rank's last work of an iteration lands on (a serving rank: its serving stream)
+    upd = torch.cuda.ExternalStream(trainer.stream(-2 if serving_rank else -1))
 
     def barrier():
         torch.cuda.synchronize()
@@ -509,7 +531,10 @@ def main():
     if world > 1:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
     ms_max = ms_t.item()
-    steps_total = st.env_steps * world * args.steps
+    steps_t = torch.tensor([st.env_steps * args.steps], dtype=torch.float64, device="cpu" if share else "cuda")
+    if world > 1:  # decoupled = 2: only the serving ranks count env-steps
+        dist.all_reduce(steps_t, op=dist.ReduceOp.SUM)
+    steps_total = int(steps_t.item())
     value = steps_total / (ms_max / 1e3)
 
     # ---- end to end through the public API: synchronous gmi_ppo_iteration per step, including
@@ -538,7 +563,13 @@ def main():
     prof = trainer.profile()
     iter_ms_instr = t2.elapsed_time(t3)
     units = unit_report(trainer.unit_busy(), iter_ms_instr, cfg.decoupled)
+    if split:  # the roofline / phases / units of the first trainer rank, reported by rank 0
+        got = [None] * world
+        dist.all_gather_object(got, (prof, iter_ms_instr, units))
+        prof, iter_ms_instr, units = got[world // 2]
+        units = [{"unit": "trainer GPU (whole GPU; the serving GPU rolls out concurrently)"}] + units[1:]
     trainer.set_instrument(False)
+    barrier()
     trainer.close()
 
     extra = {}
@@ -558,13 +589,17 @@ def main():
                    "reduction": reduction_vs_reference()}
         layout = (f"{cfg.gmis_per_gpu} GMI(s) per B200 ({['CUDA streams', 'green contexts'][cfg.gmi_backend]})"
                   if not cfg.decoupled else
+                  f"AsyncDecoupled across GPUs: {world // 2} serving B200(s) (simulator+agent) -> {world // 2} trainer "
+                  f"B200(s), experience pulled over NVLink, one-iteration policy lag" if split else
                   f"decoupled: serving GMI ({cfg.serving_sms or 16} SMs, simulator+agent) + trainer GMI per B200, "
                   f"device experience channel, one-iteration policy lag")
         run = {"layout": layout, "comm": (["ncclAllReduce" if world > 1 else "none (one GPU)",
                                            "peer exchange (fused RS + sharded Adam + AG)"][cfg.comm]),
-               "gmis_per_gpu": cfg.gmis_per_gpu + (1 if cfg.decoupled else 0),
+               "gmis_per_gpu": cfg.gmis_per_gpu + (1 if cfg.decoupled == 1 else 0),
                "gmi_backend": ["streams", "green_ctx"][cfg.gmi_backend], "sm_per_gmi": cfg.sm_per_gmi,
-               "decoupled": bool(cfg.decoupled), "env_steps_per_step": steps_total // args.steps,
+               "decoupled": bool(cfg.decoupled),
+               "decoupled_mode": ["off", "per GPU (serving + trainer GMI)", "across GPUs (AsyncDecoupled)"][cfg.decoupled],
+               "env_steps_per_step": steps_total // args.steps,
                "cuda_graph": bool(cfg.use_graph),
                "working_set_mb": round(working_set_mb(cfg, envs_per_gpu), 1)}
         line = {

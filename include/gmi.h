@@ -376,7 +376,16 @@ typedef struct {
    * experience the serving GMI generated with the weights of iteration i-1 while it generates
    * iteration i+1's experience with the weights of iteration i (one-iteration policy lag; the
    * behaviour log-probs are recorded, so the clipped ratio stays exact). gmis_per_gpu counts
-   * trainer GMIs and must be 1. */
+   * trainer GMIs and must be 1.
+   * decoupled = 2: AsyncDecoupled across GPUs (mapping.hpp:265-276; reference data path
+   * channels.hpp:182-191 migrate): num_gpus even; ranks [0, G/2) are serving GPUs (simulator +
+   * agent on the whole GPU), rank G/2 + s is a trainer GPU that trains on serving rank s's envs
+   * (the 1:1 pairing LeastLoadRouter produces for equal units). Same one-iteration lag: the
+   * trainer pulls rollout i from its partner's link window over NVLink, trains, and pushes the
+   * new policy snapshot back; device flags in the windows order the hand-offs. The trainer
+   * ranks form a data-parallel job of G/2 ranks (rank s; comm as below, among trainers only).
+   * Wire each pair with gmi_ppo_link_attach / gmi_ppo_link_connect before the first iteration;
+   * both ranks call gmi_ppo_iteration the same number of times. */
   int decoupled;
   int serving_sms;            /* green-context SMs of the serving GMI (multiple of 8; 0 = 16) */
   /* Cross-GPU gradient exchange (num_gpus > 1; HAR leader step, reduction.hpp:287-299):
@@ -433,6 +442,14 @@ GMI_API int gmi_ppo_tune_shares(void* trainer, const int* candidates, int ncand,
 GMI_API int gmi_ppo_comm_handle(void* trainer, void* out64);
 GMI_API int gmi_ppo_comm_attach(void* trainer, const void* handles);
 GMI_API int gmi_ppo_comm_connect(void* const* trainers, int n);
+/* Experience link of an AsyncDecoupled pair (cfg.decoupled = 2). gmi_ppo_link_handle: the
+ * 64-byte CUDA IPC handle of this rank's link window ([flags | policy snapshot | experience
+ * channel]); pass the partner's to gmi_ppo_link_attach (serving rank s <-> trainer rank
+ * G/2 + s, one process per GPU). gmi_ppo_link_connect wires a pair living in one process
+ * (distinct, peer-capable devices). Iterating an unwired rank fails with GMI_ERR_INVALID. */
+GMI_API int gmi_ppo_link_handle(void* trainer, void* out64);
+GMI_API int gmi_ppo_link_attach(void* trainer, const void* peer64);
+GMI_API int gmi_ppo_link_connect(void* serving, void* trainer);
 /* Rollout + values + GAE of the next iteration only (parity checks). The following
  * gmi_ppo_iteration trains on this rollout instead of rolling out again; calling the hook
  * twice without an iteration in between fails with GMI_ERR_INVALID. */
@@ -447,7 +464,8 @@ GMI_API int gmi_ppo_minibatch_grad(void* trainer, int gmi, const float* X, const
 GMI_API int gmi_ppo_get(void* trainer, const char* what, int gmi, void* dst, long long* n);
 GMI_API int gmi_ppo_set(void* trainer, const char* what, int gmi, const void* src, long long n);
 GMI_API int gmi_ppo_param_count(void* trainer, long long* padded, long long* real);
-/* cudaStream_t of local GMI `gmi` (-1: the update / reduction stream). */
+/* cudaStream_t of local GMI `gmi` (-1: the update / reduction stream; -2: the serving GMI's
+ * stream in decoupled mode, the whole rank's work on a decoupled = 2 serving rank). */
 GMI_API int gmi_ppo_stream(void* trainer, int gmi, void** stream);
 
 /* Per-phase device time of the last completed iteration when cfg.instrument = 1: CUDA

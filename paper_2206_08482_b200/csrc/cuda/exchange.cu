@@ -23,6 +23,7 @@
 // hold bit-identical parameters, and the arithmetic of the update is adam_kernel's.
 #include <cuda_bf16.h>
 
+#include "../host/errors.hpp"
 #include "launch.cuh"
 #include "ppo.cuh"
 
@@ -191,7 +192,48 @@ __global__ void __launch_bounds__(256) exchange_wait_kernel(const __grid_constan
   __syncthreads();
 }
 
+// ------------------------------------------------------------------ cross-GPU experience link
+// AsyncDecoupled across GPUs (cfg.decoupled = 2): one thread waits until the flag(s) in this
+// GPU's link window reach the next target of a device-resident counter (graph-replay safe:
+// target = ++ctr + add), or signals a peer's flag the same way after a system-scope fence
+// (the copies enqueued before it on the stream have completed). A wait that does not complete
+// within 60 s traps, so a dead peer surfaces as a kernel error instead of a hung GPU.
+__global__ void link_wait_kernel(const unsigned long long* f1, const unsigned long long* f2, unsigned long long* ctr,
+                                 unsigned long long add) {
+  if (threadIdx.x != 0) return;
+  const unsigned long long target = *ctr + 1 + add;
+  unsigned long long t0, t1;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  unsigned ns = 64;
+  while (ld_acquire_sys(f1) < target || (f2 != nullptr && ld_acquire_sys(f2) < target)) {
+    __nanosleep(ns);
+    ns = ns < 2048 ? ns * 2 : ns;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+    if (t1 - t0 > 60000000000ull) asm volatile("trap;");
+  }
+  *ctr += 1;
+}
+
+__global__ void link_signal_kernel(unsigned long long* flag, unsigned long long* ctr, unsigned long long add) {
+  if (threadIdx.x != 0) return;
+  const unsigned long long v = *ctr + 1 + add;
+  *ctr += 1;
+  __threadfence_system();
+  st_release_sys(flag, v);
+}
+
 }  // namespace
+
+void launch_link_wait(const unsigned long long* f1, const unsigned long long* f2, unsigned long long* ctr,
+                      unsigned long long add, cudaStream_t s) {
+  link_wait_kernel<<<1, 32, 0, s>>>(f1, f2, ctr, add);
+  GMI_CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_link_signal(unsigned long long* flag, unsigned long long* ctr, unsigned long long add, cudaStream_t s) {
+  link_signal_kernel<<<1, 32, 0, s>>>(flag, ctr, add);
+  GMI_CUDA_CHECK(cudaGetLastError());
+}
 
 void launch_exchange_adam(const ExchangeArgs& a, cudaStream_t s) {
   if (a.G < 1 || a.G > kMaxRanks) invalid("exchange: 1..8 ranks");

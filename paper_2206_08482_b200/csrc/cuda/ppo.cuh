@@ -124,6 +124,11 @@ struct ExchangeArgs {
   float lr, b1, b2, eps, inv_n;
 };
 void launch_exchange_adam(const ExchangeArgs& a, cudaStream_t s);
+// Cross-GPU experience link (AsyncDecoupled, cfg.decoupled = 2; exchange.cu): wait until
+// f1 (and f2 if given) >= ++*ctr + add; signal *flag = ++*ctr + add (system-scope release).
+void launch_link_wait(const unsigned long long* f1, const unsigned long long* f2, unsigned long long* ctr,
+                      unsigned long long add, cudaStream_t s);
+void launch_link_signal(unsigned long long* flag, unsigned long long* ctr, unsigned long long add, cudaStream_t s);
 
 struct AdamArgs {
   float* p;

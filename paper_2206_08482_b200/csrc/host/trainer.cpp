@@ -196,6 +196,19 @@ void Trainer::init(const void* nccl_id) {
   if (cfg.epochs < 1 || cfg.minibatches < 1) invalid("epochs and minibatches must be >= 1");
   if (cfg.num_gpus < 1 || cfg.gmis_per_gpu < 1) invalid("num_gpus and gmis_per_gpu must be >= 1");
   if (cfg.rank < 0 || cfg.rank >= cfg.num_gpus) invalid("rank out of range");
+  if (cfg.decoupled < 0 || cfg.decoupled > 2) invalid("decoupled must be 0, 1 (per GPU) or 2 (across GPUs)");
+  split_ = cfg.decoupled == 2;
+  if (split_) {
+    // AsyncDecoupled (mapping.hpp:265-276): serving GPUs first; 1:1 serving -> trainer pairs
+    if (cfg.num_gpus < 2 || cfg.num_gpus % 2 != 0)
+      invalid("decoupled = 2 (AsyncDecoupled across GPUs) needs an even num_gpus >= 2: ranks [0, G/2) serve, "
+              "rank G/2 + s trains on serving rank s's experience");
+    link_rank_ = cfg.rank;
+    link_gpus_ = cfg.num_gpus;
+    serving_ = cfg.rank < cfg.num_gpus / 2;
+    cfg_.rank = cfg.rank % (cfg.num_gpus / 2);  // the pair's rank in the trainers' data-parallel job
+    cfg_.num_gpus = cfg.num_gpus / 2;
+  }
   if (geo_.A > ppo::kMaxAct) invalid("act_dim > 31 unsupported");
   if (geo_.S > 256) invalid("obs_dim > 256 unsupported");
   if (geo_.wp[geo_.L] > ppo::kMaxHeadIn) invalid("last hidden width > 512 unsupported");
@@ -218,7 +231,8 @@ void Trainer::init(const void* nccl_id) {
     // GMI 2r: simulator + agent (serving), GMI 2r+1: trainer (mapping.hpp:243-249 roles)
     if (n_local_ != 1) invalid("decoupled mode runs one trainer GMI per GPU (gmis_per_gpu = 1)");
     const int serving = cfg.serving_sms > 0 ? cfg.serving_sms : 16;
-    exec_ = std::make_unique<GmiResources>(cfg.device, std::vector<int>{serving, 0}, cfg.gmi_backend);
+    // across GPUs the serving and trainer roles each own a whole GPU (plain streams)
+    exec_ = std::make_unique<GmiResources>(cfg.device, std::vector<int>{serving, 0}, split_ ? 0 : cfg.gmi_backend);
     serve_s_ = exec_->stream(0);
     GMI_CUDA_CHECK(cudaEventCreateWithFlags(&ev_copied_, cudaEventDisableTiming));
     GMI_CUDA_CHECK(cudaEventCreateWithFlags(&ev_rolled_, cudaEventDisableTiming));
@@ -231,11 +245,11 @@ void Trainer::init(const void* nccl_id) {
   // GMI_FORCE_NCCL=1 (tests): a one-rank communicator on a single GPU, so the NCCL all-reduce
   // in the captured iteration graph is exercised on one-GPU boxes (identity sum, bit-exact)
   const char* force = std::getenv("GMI_FORCE_NCCL");
-  xchg_ = cfg.comm == 1;
+  xchg_ = cfg.comm == 1 && !(split_ && serving_);  // serving ranks take no part in the update
   if (cfg.comm != 0 && cfg.comm != 1) invalid("comm must be 0 (NCCL) or 1 (peer exchange)");
   if (xchg_ && cfg.num_gpus > ppo::kMaxRanks) invalid("peer exchange supports up to 8 GPUs per job");
-  const bool force_nccl = !xchg_ && cfg.num_gpus == 1 && force && force[0] == '1';
-  upd_in_gmi_ = decoupled_ && cfg.num_gpus == 1 && !force_nccl;
+  const bool force_nccl = !xchg_ && cfg.num_gpus == 1 && force && force[0] == '1' && !split_;
+  upd_in_gmi_ = decoupled_ && !split_ && cfg.num_gpus == 1 && !force_nccl;
   if (upd_in_gmi_)
     upd_ = exec_->extra_stream(1);
   else
@@ -291,8 +305,8 @@ void Trainer::init(const void* nccl_id) {
       Trainer* self = this;
       comm_connect(&self, 1);
     }
-  } else if (cfg.num_gpus > 1 || force_nccl) {
-    ncclUniqueId id;
+  } else if ((cfg.num_gpus > 1 || force_nccl) && !(split_ && serving_)) {
+    ncclUniqueId id;  // decoupled = 2: an id of the trainer ranks' communicator
     if (force_nccl) {
       NCCL_CHECK(ncclGetUniqueId(&id));
     } else {
@@ -351,7 +365,11 @@ void Trainer::release() noexcept {
   exec_.reset();
 }
 
-cudaStream_t Trainer::stream(int gmi) const { return gmi < 0 ? upd_ : gmis_.at(gmi)->s; }
+// -1: the update stream; -2: the serving GMI's stream (decoupled); else GMI gmi's stream
+cudaStream_t Trainer::stream(int gmi) const {
+  if (gmi == -2) return serve_s_;
+  return gmi < 0 ? upd_ : gmis_.at(gmi)->s;
+}
 
 void Trainer::alloc() {
   auto dev = [&](size_t bytes) {
@@ -385,9 +403,33 @@ void Trainer::alloc() {
   GMI_CUDA_CHECK(cudaMallocHost(&stats_host_, 8 * 4));
   std::memset(ctl_host_, 0, sizeof(ppo::Control));
   std::memset(stats_host_, 0, 8 * 4);
+  if (split_) {
+    // link window, same layout on both ranks: [flags 4 KB: R @0 (trainer's), C @128, S @256
+    // (serving's) | snapshot params P fp32 | shadow P bf16 | channel X | act | logp | adv | ret |
+    // adv_stats] -- the part of the channel the trainer migrates
+    const long long N = gmis_[0]->N, T = T_;
+    size_t off = 4096;
+    auto take = [&](size_t bytes) {
+      const size_t o = off;
+      off = (off + bytes + 255) / 256 * 256;
+      return o;
+    };
+    loff_params_ = take(P * 4);
+    loff_shadow_ = take(P * 2);
+    loff_X_ = take((T + 1) * N * geo_.wp[0] * 2);
+    loff_act_ = take(T * N * geo_.A * 4);
+    loff_logp_ = take(T * N * 4);
+    loff_adv_ = take(T * N * 4);
+    loff_ret_ = take(T * N * 4);
+    loff_stats_ = take(16);
+    lwin_bytes_ = off;
+    lwin_ = static_cast<char*>(dev(lwin_bytes_));
+    lctr_ = static_cast<unsigned long long*>(dev(16 * 8));
+  }
   if (decoupled_) {
-    params_roll_ = static_cast<float*>(dev(P * 4));
-    shadow_roll_ = static_cast<__nv_bfloat16*>(dev(P * 2));
+    params_roll_ = split_ ? reinterpret_cast<float*>(lwin_ + loff_params_) : static_cast<float*>(dev(P * 4));
+    shadow_roll_ = split_ ? reinterpret_cast<__nv_bfloat16*>(lwin_ + loff_shadow_)
+                          : static_cast<__nv_bfloat16*>(dev(P * 2));
     ctl_roll_ = static_cast<ppo::Control*>(dev(sizeof(ppo::Control)));
   }
 
@@ -406,16 +448,25 @@ void Trainer::alloc() {
     g.logp = static_cast<float*>(dev(T * N * 4));
     g.rew = static_cast<float*>(dev(T * N * 4));
     g.done = static_cast<uint8_t*>(dev(T * N));
-    if (decoupled_) {
+    if (decoupled_ && split_) {
+      g.ch_X = reinterpret_cast<__nv_bfloat16*>(lwin_ + loff_X_);
+      g.ch_act = reinterpret_cast<float*>(lwin_ + loff_act_);
+      g.ch_logp = reinterpret_cast<float*>(lwin_ + loff_logp_);
+      g.ch_adv = reinterpret_cast<float*>(lwin_ + loff_adv_);
+      g.ch_ret = reinterpret_cast<float*>(lwin_ + loff_ret_);
+      g.ch_adv_stats = reinterpret_cast<float*>(lwin_ + loff_stats_);
+    } else if (decoupled_) {
       g.ch_X = static_cast<__nv_bfloat16*>(dev((T + 1) * N * S_p * 2));
       g.ch_act = static_cast<float*>(dev(T * N * A * 4));
       g.ch_logp = static_cast<float*>(dev(T * N * 4));
-      g.ch_rew = static_cast<float*>(dev(T * N * 4));
-      g.ch_done = static_cast<uint8_t*>(dev(T * N));
-      g.ch_V = static_cast<float*>(dev((T + 1) * N * 4));
       g.ch_adv = static_cast<float*>(dev(T * N * 4));
       g.ch_ret = static_cast<float*>(dev(T * N * 4));
       g.ch_adv_stats = static_cast<float*>(dev(4 * 4));
+    }
+    if (decoupled_) {
+      g.ch_rew = static_cast<float*>(dev(T * N * 4));
+      g.ch_done = static_cast<uint8_t*>(dev(T * N));
+      g.ch_V = static_cast<float*>(dev((T + 1) * N * 4));
       g.ch_gae_part = static_cast<double*>(dev(ppo::gae_blocks(g.N) * 3 * 8));
     }
     g.V = static_cast<float*>(dev((T + 1) * N * 4));
@@ -1515,20 +1566,29 @@ void Trainer::record_iteration(bool with_rollout) {
     const long long TN = (long long)T_ * g.N;
     const int S_p = geo_.wp[0], A = geo_.A;
     GMI_CUDA_CHECK(cudaStreamWaitEvent(g.s, ev_start_, 0));
+    // across GPUs (decoupled = 2): wait until the partner published rollout i (R >= i + 1), then
+    // pull it over NVLink from the partner's link window
+    if (split_) ppo::launch_link_wait(link_flag(false, 0), nullptr, lctr_ + 2, 0, g.s);
+    auto ch = [&](const void* local, size_t off) -> const void* { return split_ ? lpeer_ + off : local; };
     timed(g.s, GMI_PH_OTHER, 0.0, 2.0 * ((TN + g.N) * S_p * 2 + TN * (4.0 * A + 12.0) + 16.0), [&] {
       auto mig = [&](void* dst, const void* src, size_t bytes) {
         GMI_CUDA_CHECK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, g.s));
       };
-      mig(g.X_roll, g.ch_X, (size_t)(TN + g.N) * S_p * 2);
-      mig(g.act, g.ch_act, (size_t)TN * A * 4);
-      mig(g.logp, g.ch_logp, (size_t)TN * 4);
-      mig(g.adv, g.ch_adv, (size_t)TN * 4);
-      mig(g.ret, g.ch_ret, (size_t)TN * 4);
-      mig(g.adv_stats, g.ch_adv_stats, 16);
+      mig(g.X_roll, ch(g.ch_X, loff_X_), (size_t)(TN + g.N) * S_p * 2);
+      mig(g.act, ch(g.ch_act, loff_act_), (size_t)TN * A * 4);
+      mig(g.logp, ch(g.ch_logp, loff_logp_), (size_t)TN * 4);
+      mig(g.adv, ch(g.ch_adv, loff_adv_), (size_t)TN * 4);
+      mig(g.ret, ch(g.ch_ret, loff_ret_), (size_t)TN * 4);
+      mig(g.adv_stats, ch(g.ch_adv_stats, loff_stats_), 16);
     });
-    GMI_CUDA_CHECK(cudaEventRecord(ev_copied_, g.s));
-    GMI_CUDA_CHECK(cudaStreamWaitEvent(serve_s_, ev_copied_, 0));
-    serve_rollout(g);
+    if (split_) {  // the channel is free again: C = i + 1
+      ppo::launch_link_signal(link_flag(true, 128), lctr_ + 3, 0, g.s);
+      launches_ += 2;
+    } else {
+      GMI_CUDA_CHECK(cudaEventRecord(ev_copied_, g.s));
+      GMI_CUDA_CHECK(cudaStreamWaitEvent(serve_s_, ev_copied_, 0));
+      serve_rollout(g);
+    }
   } else {
     for (auto& g : gmis_) {
       GMI_CUDA_CHECK(cudaStreamWaitEvent(g->s, ev_start_, 0));
@@ -1567,7 +1627,15 @@ void Trainer::record_iteration(bool with_rollout) {
     }
   }
   for (auto& g : gmis_) GMI_CUDA_CHECK(cudaStreamWaitEvent(upd_, g->ev_done, 0));
-  if (decoupled_) {  // rollout i+1 is done with the snapshot: refresh it to theta_{i+1}
+  if (split_) {
+    // the partner's rollout i+1 is done with the snapshot (R >= i + 2): push theta_{i+1} into its
+    // link window over NVLink, then S = i + 2
+    ppo::launch_link_wait(link_flag(false, 0), nullptr, lctr_ + 4, 1, upd_);
+    GMI_CUDA_CHECK(cudaMemcpyAsync(lpeer_ + loff_params_, params_, (size_t)geo_.P * 4, cudaMemcpyDeviceToDevice, upd_));
+    GMI_CUDA_CHECK(cudaMemcpyAsync(lpeer_ + loff_shadow_, shadow_, (size_t)geo_.P * 2, cudaMemcpyDeviceToDevice, upd_));
+    ppo::launch_link_signal(link_flag(true, 256), lctr_ + 5, 1, upd_);
+    launches_ += 2;
+  } else if (decoupled_) {  // rollout i+1 is done with the snapshot: refresh it to theta_{i+1}
     GMI_CUDA_CHECK(cudaStreamWaitEvent(upd_, ev_rolled_, 0));
     GMI_CUDA_CHECK(cudaMemcpyAsync(params_roll_, params_, (size_t)geo_.P * 4, cudaMemcpyDeviceToDevice, upd_));
     GMI_CUDA_CHECK(cudaMemcpyAsync(shadow_roll_, shadow_, (size_t)geo_.P * 2, cudaMemcpyDeviceToDevice, upd_));
@@ -1608,6 +1676,71 @@ void Trainer::resize(const int* sms, int n) {
   }
   build_plans();
   GMI_CUDA_CHECK(cudaDeviceSynchronize());
+}
+
+// AsyncDecoupled across GPUs, serving rank: rollout i+1 once the trainer has pulled rollout i
+// (C >= i + 1) and pushed the snapshot theta_i (S >= i + 1); the first call first rolls out
+// rollout 0 with theta_0 (initialised here from the same seed as the trainer's). Eager launches
+// on the serving stream; every rollout ends with R = rollouts.
+void Trainer::serve_iteration() {
+  Gmi& g = *gmis_[0];
+  launches_ = 0;
+  marks_used_ = 0;
+  if (rollouts_ == 0) {
+    GMI_CUDA_CHECK(cudaMemcpyAsync(params_roll_, params_, (size_t)geo_.P * 4, cudaMemcpyDeviceToDevice, serve_s_));
+    GMI_CUDA_CHECK(cudaMemcpyAsync(shadow_roll_, shadow_, (size_t)geo_.P * 2, cudaMemcpyDeviceToDevice, serve_s_));
+    GMI_CUDA_CHECK(cudaMemsetAsync(ctl_roll_, 0, sizeof(ppo::Control), serve_s_));
+    ppo::launch_link_signal(link_flag(false, 256), lctr_ + 6, 0, serve_s_);  // own S = 1: theta_0 present
+    serve_rollout(g);
+    ppo::launch_link_signal(link_flag(true, 0), lctr_ + 0, 0, serve_s_);
+  }
+  ppo::launch_link_wait(link_flag(false, 128), link_flag(false, 256), lctr_ + 1, 0, serve_s_);
+  serve_rollout(g);
+  ppo::launch_link_signal(link_flag(true, 0), lctr_ + 0, 0, serve_s_);
+  launches_ += 2;
+}
+
+unsigned long long* Trainer::link_flag(bool peer, size_t off) const {
+  return reinterpret_cast<unsigned long long*>((peer ? lpeer_ : lwin_) + off);
+}
+
+void Trainer::link_handle(void* out64) const {
+  if (!split_) invalid("gmi_ppo_link_handle: the trainer was not created with decoupled = 2");
+  cudaIpcMemHandle_t h;
+  GMI_CUDA_CHECK(cudaIpcGetMemHandle(&h, lwin_));
+  std::memcpy(out64, &h, sizeof(h));
+}
+
+void Trainer::link_attach(const void* peer64) {
+  if (!split_) invalid("gmi_ppo_link_attach: the trainer was not created with decoupled = 2");
+  if (linked_) invalid("gmi_ppo_link_attach: already wired");
+  GMI_CUDA_CHECK(cudaSetDevice(cfg_.device));
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, peer64, sizeof(h));
+  void* p = nullptr;
+  GMI_CUDA_CHECK(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+  ipc_opened_.push_back(p);
+  lpeer_ = static_cast<char*>(p);
+  linked_ = true;
+}
+
+void Trainer::link_connect(Trainer* sv, Trainer* tr) {
+  if (!sv || !tr || !sv->split_ || !tr->split_ || !sv->serving_ || tr->serving_)
+    invalid("gmi_ppo_link_connect: (serving rank, trainer rank) of one decoupled = 2 job");
+  if (sv->link_gpus_ != tr->link_gpus_ || tr->link_rank_ != sv->link_rank_ + sv->link_gpus_ / 2 ||
+      sv->lwin_bytes_ != tr->lwin_bytes_)
+    invalid("gmi_ppo_link_connect: the trainer rank must be serving rank + num_gpus / 2 of the same job");
+  if (sv->linked_ || tr->linked_) invalid("gmi_ppo_link_connect: already wired");
+  if (sv->cfg_.device == tr->cfg_.device)
+    invalid("gmi_ppo_link_connect: ranks on one GPU need one process each (gmi_ppo_link_attach)");
+  for (auto [a, b] : {std::pair<Trainer*, Trainer*>{sv, tr}, {tr, sv}}) {
+    GMI_CUDA_CHECK(cudaSetDevice(a->cfg_.device));
+    const cudaError_t e = cudaDeviceEnablePeerAccess(b->cfg_.device, 0);
+    if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+    else GMI_CUDA_CHECK(e);
+    a->lpeer_ = b->lwin_;
+    a->linked_ = true;
+  }
 }
 
 void Trainer::comm_handle(void* out64) const {
@@ -1686,10 +1819,17 @@ void Trainer::comm_connect(Trainer* const* t, int n) {
 void Trainer::enqueue_iteration(bool host_control) {
   if (xchg_ && !connected_)
     invalid("peer exchange not wired: call gmi_ppo_comm_attach / gmi_ppo_comm_connect before iterating");
+  if (split_ && !linked_)
+    invalid("experience link not wired: call gmi_ppo_link_attach / gmi_ppo_link_connect before iterating");
   GMI_CUDA_CHECK(cudaSetDevice(cfg_.device));
+  if (split_ && serving_) {
+    serve_iteration();
+    iteration_ += 1;
+    return;
+  }
   ensure_bias_table(adam_steps_ + (long long)cfg_.epochs * K_ + 1);
   if (host_control || iteration_ == 0) write_control();
-  if (decoupled_ && rollouts_ == 0) {  // prologue: rollout 0 with theta_0 (not overlapped)
+  if (decoupled_ && !split_ && rollouts_ == 0) {  // prologue: rollout 0 with theta_0 (not overlapped)
     GMI_CUDA_CHECK(cudaMemcpyAsync(params_roll_, params_, (size_t)geo_.P * 4, cudaMemcpyDeviceToDevice, upd_));
     GMI_CUDA_CHECK(cudaMemcpyAsync(shadow_roll_, shadow_, (size_t)geo_.P * 2, cudaMemcpyDeviceToDevice, upd_));
     GMI_CUDA_CHECK(cudaMemsetAsync(ctl_roll_, 0, sizeof(ppo::Control), upd_));
@@ -1761,8 +1901,8 @@ void Trainer::synchronize(gmi_ppo_stats_t* st) {
   st->approx_kl = stats_host_[2] / Bm;
   st->clip_frac = stats_host_[3] / Bm;
   st->mean_reward = stats_host_[6];
-  long long steps = 0;
-  for (auto& g : gmis_) steps += (long long)T_ * g->N;
+  long long steps = 0;  // decoupled = 2: counted by the serving ranks only (a job-wide sum stays right)
+  for (auto& g : gmis_) steps += split_ && !serving_ ? 0 : (long long)T_ * g->N;
   st->env_steps = steps;
   st->kernel_launches = launches_;
   st->gemm_ms = gemm.ms;
@@ -1798,11 +1938,14 @@ long long Trainer::get(const std::string& what, int gi, void* dst) {
     return n;
   };
   const long long P = geo_.P;
-  if (what == "params") return copy(params_, P, 4);
+  if (what == "params") return copy(split_ && serving_ ? params_roll_ : params_, P, 4);
   if (what == "adam_m") return copy(m_, P, 4);
   if (what == "adam_v") return copy(v_, P, 4);
   Gmi& g = *gmis_.at(gi);
   const long long N = g.N, T = T_, S = geo_.S, A = geo_.A;
+  if (split_ && !serving_ && (what == "rew" || what == "val" || what == "done" || what == "x" || what == "ep_step" ||
+                              what == "ep_len" || what == "ep_count"))
+    invalid("decoupled = 2: '" + what + "' lives on the serving rank");
   if (what == "grad") return copy(g.grad, P, 4);
   if (what == "x") return copy(g.x, N * S, 4);
   // epoch copy of the last shuffle (rows permuted by the epoch's bijection)
@@ -1811,7 +1954,7 @@ long long Trainer::get(const std::string& what, int gi, void* dst) {
   if (what == "trained_logp") return copy(g.logp, T * N, 4);  // the trainer's rollout copy
   // decoupled mode: rollout fields (act/logp/rew/done/obs/val/adv/ret) are the latest rollout
   // in the experience channel, one rollout ahead of the trainer
-  const bool ch = decoupled_;
+  const bool ch = decoupled_ && !(split_ && !serving_);
   if (what == "act") return copy(ch ? g.ch_act : g.act, T * N * A, 4);
   if (what == "logp") return copy(ch ? g.ch_logp : g.logp, T * N, 4);
   if (what == "rew") return copy(ch ? g.ch_rew : g.rew, T * N, 4);
@@ -2026,6 +2169,26 @@ GMI_API int gmi_ppo_comm_connect(void* const* trainers, int n) {
     std::vector<gmi::Trainer*> v(n > 0 ? n : 0);
     for (int i = 0; i < n; ++i) v[i] = static_cast<gmi::Trainer*>(trainers[i]);
     gmi::Trainer::comm_connect(v.data(), n);
+  });
+}
+
+GMI_API int gmi_ppo_link_handle(void* t, void* out64) {
+  return gmi::guarded([&] {
+    if (!t || !out64) gmi::invalid("null argument");
+    static_cast<gmi::Trainer*>(t)->link_handle(out64);
+  });
+}
+
+GMI_API int gmi_ppo_link_attach(void* t, const void* peer64) {
+  return gmi::guarded([&] {
+    if (!t || !peer64) gmi::invalid("null argument");
+    static_cast<gmi::Trainer*>(t)->link_attach(peer64);
+  });
+}
+
+GMI_API int gmi_ppo_link_connect(void* serving, void* trainer) {
+  return gmi::guarded([&] {
+    gmi::Trainer::link_connect(static_cast<gmi::Trainer*>(serving), static_cast<gmi::Trainer*>(trainer));
   });
 }
 

@@ -105,6 +105,20 @@ class Trainer {
   __nv_bfloat16* shadow_roll_ = nullptr;
   ppo::Control* ctl_roll_ = nullptr;
   long long rollouts_ = 0;  // serving-GMI rollouts enqueued so far
+  // AsyncDecoupled across GPUs (cfg.decoupled = 2, mapping.hpp:265-276): ranks [0, G/2) serve,
+  // rank G/2 + s trains on serving rank s's experience. cfg_ holds the pair's data-parallel
+  // sub-job view (rank s of G/2); link_rank_ / link_gpus_ the job's. Both ranks lay out the same
+  // link window [flags | policy snapshot | experience channel] (IPC-exported): the trainer pulls
+  // the channel from its partner's window and pushes the snapshot back; device flags order it.
+  bool split_ = false, serving_ = false, linked_ = false;
+  int link_rank_ = 0, link_gpus_ = 0;
+  char* lwin_ = nullptr;                  // this rank's link window
+  char* lpeer_ = nullptr;                 // the partner's (mapped)
+  unsigned long long* lctr_ = nullptr;    // device counters of the link's wait / signal sites
+  size_t loff_params_ = 0, loff_shadow_ = 0, loff_X_ = 0, loff_act_ = 0, loff_logp_ = 0, loff_adv_ = 0,
+         loff_ret_ = 0, loff_stats_ = 0, lwin_bytes_ = 0;
+  void serve_iteration();  // serving rank: one rollout per gmi_ppo_iteration
+  unsigned long long* link_flag(bool peer, size_t off) const;
   // peer exchange (cfg.comm = 1, cuda/exchange.cu): this rank's window [flags | pub | params |
   // shadow] (IPC-exportable cudaMalloc), the peer-pointer table, and IPC mappings opened
   bool xchg_ = false;
@@ -142,12 +156,17 @@ class Trainer {
  public:
   const gmi_ppo_phase_t* phases() const { return phases_; }
   void resize(const int* sms, int n);  // gmi_resize
-  int rank() const { return cfg_.rank; }
+  int rank() const { return split_ ? link_rank_ : cfg_.rank; }
   int units() const { return decoupled_ ? 2 : n_local_; }  // GMIs with an SM partition
   // peer exchange wiring (gmi_ppo_comm_*)
   void comm_handle(void* out64) const;
   void comm_attach(const void* handles);
   static void comm_connect(Trainer* const* trainers, int n);
+  // cross-GPU experience link (decoupled = 2): IPC handle of the link window, map the partner's
+  void link_handle(void* out64) const;
+  void link_attach(const void* peer64);
+  static void link_connect(Trainer* serving, Trainer* trainer);  // one process, two devices
+  bool serving() const { return split_ && serving_; }
   // Execution units in report order: decoupled -> [serving GMI, trainer GMI], else the local
   // GMIs; then the update stream. busy = summed kernel time of the unit's instrumented launches.
   int busy_units(double* busy_ms, int* sms, int cap) const;

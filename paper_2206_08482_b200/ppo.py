@@ -59,6 +59,9 @@ _PROTOS = {
                                       C.POINTER(C.c_double)]),
     "gmi_ppo_comm_attach": (C.c_int, [C.c_void_p, C.c_void_p]),
     "gmi_ppo_comm_connect": (C.c_int, [C.POINTER(C.c_void_p), C.c_int]),
+    "gmi_ppo_link_handle": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "gmi_ppo_link_attach": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "gmi_ppo_link_connect": (C.c_int, [C.c_void_p, C.c_void_p]),
     "gmi_ppo_minibatch_grad": (C.c_int, [C.c_void_p, C.c_int] + [C.POINTER(C.c_float)] * 5 +
                                [C.c_int, C.POINTER(C.c_float)]),
     "gmi_ppo_get": (C.c_int, [C.c_void_p, C.c_char_p, C.c_int, C.c_void_p, C.POINTER(C.c_longlong)]),
@@ -276,6 +279,22 @@ class Trainer:
         """Wire the peer exchange of trainers living in this process (trainers[r] = rank r)."""
         arr = (C.c_void_p * len(trainers))(*[t._h.value for t in trainers])
         L.check(L.lib().gmi_ppo_comm_connect(arr, len(trainers)))
+
+    def link_handle(self) -> bytes:
+        """64-byte CUDA IPC handle of this rank's experience-link window (decoupled = 2)."""
+        buf = (C.c_char * 64)()
+        L.check(L.lib().gmi_ppo_link_handle(self._h, buf))
+        return bytes(buf)
+
+    def link_attach(self, peer_handle: bytes) -> None:
+        """Wire the AsyncDecoupled pair from the partner's link_handle() (serving rank s <->
+        trainer rank num_gpus / 2 + s)."""
+        L.check(L.lib().gmi_ppo_link_attach(self._h, C.create_string_buffer(peer_handle, 64)))
+
+    @staticmethod
+    def link_connect(serving: "Trainer", trainer: "Trainer") -> None:
+        """Wire an AsyncDecoupled pair living in this process (distinct devices)."""
+        L.check(L.lib().gmi_ppo_link_connect(serving._h, trainer._h))
 
     def stream(self, gmi: int = -1) -> int:
         s = C.c_void_p()

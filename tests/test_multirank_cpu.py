@@ -119,3 +119,16 @@ def test_bench_reference_arm_never_loads_libgmi():
             "assert 'libgmi' not in open('/proc/self/maps').read()")
     r = subprocess.run([sys.executable, "-c", code], cwd=ROOT, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-2000:]
+
+
+def test_async_decoupled_config_validation():
+    """decoupled = 2 (AsyncDecoupled across GPUs, mapping.hpp:265-276) is validated before any
+    device work: an even num_gpus >= 2 (1:1 serving -> trainer pairs); decoupled in {0, 1, 2}."""
+    from paper_2206_08482_b200 import _lib
+    from paper_2206_08482_b200.ppo import PpoConfig, Trainer
+    base = dict(obs_dim=12, act_dim=3, hidden=[64, 64], num_envs=256)
+    for kw, msg in ((dict(num_gpus=1, decoupled=2), "even num_gpus"),
+                    (dict(num_gpus=3, rank=1, decoupled=2), "even num_gpus"),
+                    (dict(decoupled=3), "decoupled must be")):
+        with pytest.raises((_lib.GmiError, ValueError), match=msg):
+            Trainer(PpoConfig(**base, **kw))

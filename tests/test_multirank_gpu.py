@@ -38,7 +38,7 @@ def _port():
         return s.getsockname()[1]
 
 
-def _job(tmp_path, world, envs, gmis=1, iters=2, decoupled=0):
+def _job(tmp_path, world, envs, gmis=1, iters=2, decoupled=0, split=0, backend=-1):
     """Runs `world` rank processes on cuda:0 and returns their dumps."""
     port = _port()
     procs, outs = [], []
@@ -48,7 +48,8 @@ def _job(tmp_path, world, envs, gmis=1, iters=2, decoupled=0):
         procs.append(subprocess.Popen([sys.executable, os.path.join(ROOT, "tests", "multirank_worker.py"),
                                        "--rank", str(r), "--world", str(world), "--port", str(port),
                                        "--envs", str(envs), "--gmis", str(gmis), "--iters", str(iters),
-                                       "--decoupled", str(decoupled),
+                                       "--decoupled", str(decoupled), "--split", str(split),
+                                       "--backend", str(backend),
                                        "--out", out], cwd=ROOT, stdout=subprocess.PIPE, stderr=subprocess.STDOUT,
                                       text=True))
     logs = []
@@ -177,3 +178,52 @@ def test_bench_two_ranks_on_one_gpu(cuda):
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["value"] > 0 and d["run"]["comm"].startswith("peer exchange")
     assert d["config"]["envs_per_gpu"] == 256
+
+
+def test_bench_async_decoupled_two_ranks_on_one_gpu(cuda):
+    """bench.py --decoupled 2 --gpus 2: serving rank 0 and trainer rank 1 wired over the link
+    windows, env-steps summed over ranks (serving only), rank 0 reports the trainer's phases
+    (GMI_BENCH_SHARE_GPU=1: both ranks on cuda:0, time-sliced, not a measurement)."""
+    import json
+    env = dict(os.environ, GMI_BENCH_SHARE_GPU="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
+           "127.0.0.1", "--master-port", str(_port()), os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "2",
+           "--warmup", "3", "--envs", "256", "--decoupled", "2", "--no-cpu-baseline", "--no-multi-gmi"]
+    r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=500)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["run"]["decoupled_mode"].startswith("across GPUs")
+    assert d["run"]["env_steps_per_step"] == 256 * 32
+    assert d["phases"]["fwd_gemm"]["launches"] > 0  # the trainer rank's profile
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_async_decoupled_across_ranks(cuda, tmp_path, world):
+    """AsyncDecoupled across GPUs (decoupled = 2, mapping.hpp:265-276): serving rank s rolls out
+    env slice s of G/2 on a whole GPU; trainer rank G/2 + s pulls each rollout from the partner's
+    link window, trains (the trainer ranks form a G/2-rank data-parallel job over the peer
+    exchange) and pushes the policy snapshot back -- device flags, one-iteration policy lag.
+    Must equal the colocated decoupled job with G/2 GPUs (decoupled = 1, whole-GPU streams) bit
+    for bit: trainer parameters, every serving rank's snapshot (theta_K after the last push) and
+    latest rollout; env-steps are counted by the serving ranks only."""
+    iters, envs, half = 3, 256, world // 2
+    ranks = _job(tmp_path, world, envs, iters=iters, split=1)
+    if half == 1:
+        from paper_2206_08482_b200.ppo import PpoConfig, Trainer
+        one = Trainer(PpoConfig(**SMALL, num_envs=envs, decoupled=1, gmi_backend=0))
+        for _ in range(iters):
+            one.iteration()
+        ref = [{"params": one.get("params"), **{f"{f}0": one.get(f) for f in ("done", "rew", "act")}}]
+    else:
+        (tmp_path / "ref").mkdir()
+        ref = _job(tmp_path / "ref", half, envs, iters=iters, decoupled=1, backend=0)
+    for s in range(half):
+        sv, tr = ranks[s], ranks[half + s]
+        p = ref[s]["params"].view(np.uint32)
+        assert np.array_equal(tr["params"].view(np.uint32), p), s
+        assert np.array_equal(sv["params"].view(np.uint32), p), s  # snapshot pushed by the trainer
+        for f in ("done", "rew", "act"):
+            assert np.array_equal(sv[f], ref[s][f"{f}0"]), (s, f)  # latest rollout (K + 1 on both)
+        assert list(sv["steps"]) == [envs // half * 32] * iters and list(tr["steps"]) == [0] * iters
