@@ -82,8 +82,10 @@ __global__ void __launch_bounds__(256) act_env_kernel(const ActEnvArgs a) {
     for (int p = 0; p < 2; ++p) {
       const float rad = sqrtf(-2.0f * logf(rng::u01_open0(r[2 * p])));
       const float th = kTwoPi * rng::u01(r[2 * p + 1]);
-      nrm[2 * p] = rad * cosf(th);
-      nrm[2 * p + 1] = rad * sinf(th);
+      float sn, cs;
+      sincosf(th, &sn, &cs);  // same values as cosf / sinf, one range reduction (as rollout.cu)
+      nrm[2 * p] = rad * cs;
+      nrm[2 * p + 1] = rad * sn;
     }
   }
   float got[4];
@@ -103,16 +105,21 @@ __global__ void __launch_bounds__(256) act_env_kernel(const ActEnvArgs a) {
   }
   const float logp = warp_sum(lp_term);
   const float usq = warp_sum(u * u);
+  const float tu = tanhf(u);  // drive of action lane: tanh(clip(a)), once per action
 
-  // dynamics: lane owns dims i = lane + 32 j
+  // dynamics: lane owns dims i = lane + 32 j, driven by action i mod A (kept incrementally:
+  // (i + 32) mod A = i mod A + 32 mod A, minus A on wrap)
   float* xe = a.x + (long long)e * S;
   float xn[kMaxObsPerLane];
   float xsq_part = 0.f;
+  const int step32 = 32 % A;
+  int src = lane % A;
 #pragma unroll
   for (int j = 0; j < kMaxObsPerLane; ++j) {
     const int i = lane + 32 * j;
-    const int src = i < S ? i % A : 0;
-    const float drive = tanhf(__shfl_sync(0xffffffffu, u, src));
+    const float drive = __shfl_sync(0xffffffffu, tu, i < S ? src : 0);
+    src += step32;
+    src -= src >= A ? A : 0;
     if (i < S) {
       const float xi = xe[i];
       const float nb = xe[i + 1 < S ? i + 1 : 0];
