@@ -59,7 +59,7 @@ __global__ void env_init_kernel(EnvParams ep, float* x, int* ep_step, int* ep_le
 // actions, synthetic Ant-like dynamics, reward, integer episode clock / reset, and the
 // next GEMM-ready observation row. Traffic/env: H_L row (2*hp B) + 2*S*4 (state) + 2*S_p
 // (obs) + (A+3)*4 B.
-__global__ void __launch_bounds__(256) act_env_kernel(const ActEnvArgs a) {
+__global__ void __launch_bounds__(256, 8) act_env_kernel(const ActEnvArgs a) {
   pdl_trigger();
   pdl_wait();
   const int lane = threadIdx.x & 31;
