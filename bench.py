@@ -76,19 +76,50 @@ class ClockSampler:
         self.device, self.period = device, period
         self.samples, self.reasons, self.max_mhz = [], set(), None
         self._stop = threading.Event()
+        self._lock = threading.Lock()
         self._thread = None
         self._nvml = None
+        self._h = None
+        self.error = None
+
+    def _nvml_index(self, nv):
+        """NVML index of CUDA device `self.device` (NVML enumerates all GPUs, CUDA only the
+        visible ones): matched by UUID."""
+        try:
+            import torch
+            uuid = str(torch.cuda.get_device_properties(self.device).uuid).lower()
+            for i in range(nv.nvmlDeviceGetCount()):
+                u = nv.nvmlDeviceGetUUID(nv.nvmlDeviceGetHandleByIndex(i))
+                u = (u.decode() if isinstance(u, bytes) else u).lower()
+                if uuid and uuid in u:
+                    return i
+        except Exception:  # noqa: BLE001 - fall back to the CUDA ordinal
+            pass
+        return self.device
+
+    def sample(self):
+        """One SM-clock + throttle-reason sample (callable from the main thread as well: the
+        timed loop polls its end event and samples while the device drains the queue)."""
+        if self._nvml is None:
+            return
+        nv = self._nvml
+        with self._lock:
+            self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+            try:
+                mask = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+            except AttributeError:  # older bindings
+                mask = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self._h)
+            for name, attr in self.REASONS:
+                if mask & getattr(nv, attr, getattr(nv, attr.replace("ClocksEvent", "ClocksThrottle"), 0)):
+                    self.reasons.add(name)
 
     def _run(self):
-        nv = self._nvml
-        h = nv.nvmlDeviceGetHandleByIndex(self.device)
-        self.max_mhz = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
         while not self._stop.is_set():
-            self.samples.append(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
-            mask = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
-            for name, attr in self.REASONS:
-                if mask & getattr(nv, attr, 0):
-                    self.reasons.add(name)
+            try:
+                self.sample()
+            except Exception as e:  # noqa: BLE001 - keep the failure visible in the line
+                self.error = repr(e)
+                return
             time.sleep(self.period)
 
     def start(self):
@@ -96,8 +127,11 @@ class ClockSampler:
         try:
             import pynvml
             pynvml.nvmlInit()
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(self._nvml_index(pynvml))
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
             self._nvml = pynvml
-        except Exception:  # noqa: BLE001 - no NVML: clocks reported as unavailable
+        except Exception as e:  # noqa: BLE001 - no NVML: clocks reported as unavailable
+            self.error = repr(e)
             return
         self._thread = threading.Thread(target=self._run, daemon=True)
         self._thread.start()
@@ -108,7 +142,8 @@ class ClockSampler:
         self._stop.set()
         self._thread.join(timeout=5)
         if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["no samples"], "samples": 0}
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["no samples"], "samples": 0,
+                    "error": self.error}
         loaded = [x for x in self.samples if x > 0.5 * (self.max_mhz or max(self.samples))] or self.samples
         return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": self.max_mhz,
                 "reasons": sorted(self.reasons), "samples": len(self.samples), "source": "nvml"}
@@ -522,6 +557,9 @@ def main():
     for _ in range(args.steps):
         trainer.iteration_async()
     t1.record(upd)
+    while rank == 0 and not t1.query():  # sample clocks while the device drains the timed queue
+        clocks.sample()
+        time.sleep(0.002)
     st = trainer.synchronize()
     barrier()
     clk = clocks.stop() if rank == 0 else None
