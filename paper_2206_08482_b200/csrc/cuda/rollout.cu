@@ -23,6 +23,8 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "../host/errors.hpp"
 #include "gemm.cuh"
 #include "launch.cuh"
@@ -64,22 +66,26 @@ __device__ __forceinline__ uint32_t sw128(int row, int col_bf16) {  // byte offs
 }
 
 // MAXB: 4-dim state blocks per env thread (S <= 16 * MAXB).
-template <int MAXB>
+// WIDE: hidden widths up to 512 (a.plan, rollout.cuh): per-layer tile offsets and TMEM columns,
+// weights in 128-row N parts, input K-chunk pairs released by act_rdy[pair] (up to 4 pairs).
+template <int MAXB, bool WIDE>
 __global__ void __launch_bounds__(kThreads, 1) rollout_kernel(const __grid_constant__ RolloutArgs a) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = ptx::align_smem_1024(smem_raw);
+  const WidePlan& P = a.plan;
   uint8_t* act_buf0 = smem;
   uint8_t* act_buf1 = smem + kActBytes;
-  uint8_t* wring = smem + 2 * kActBytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(wring + kStages * kWStage);
+  uint8_t* wring = WIDE ? smem + P.ring_off : smem + 2 * kActBytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(WIDE ? smem + P.bar_off : wring + kStages * kWStage);
   uint64_t* wfull = bars;
-  uint64_t* wempty = bars + kStages;
-  uint64_t* obs_bar = bars + 2 * kStages;
+  uint64_t* wempty = bars + (WIDE ? 8 : kStages);
+  uint64_t* obs_bar = bars + (WIDE ? 16 : 2 * kStages);
   uint64_t* acc_full = obs_bar + 1;
   uint64_t* act_lo = acc_full + 1;  // next operand tile, K-chunks 0-1 (columns 0..127) written
   uint64_t* act_hi = act_lo + 1;    // K-chunks 2-3 written
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(act_hi + 1);
-  float* ls_s = reinterpret_cast<float*>(bars + 16);  // log_std[32], exp(log_std)[32]
+  uint64_t* act_rdy = act_lo;       // WIDE: [4] K-chunk pairs 0..3 of the next operand tile written
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(act_lo + 4);
+  float* ls_s = reinterpret_cast<float*>(bars + (WIDE ? 32 : 16));  // log_std[32], exp(log_std)[32]
   float* sig_s = ls_s + 32;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -87,14 +93,13 @@ __global__ void __launch_bounds__(kThreads, 1) rollout_kernel(const __grid_const
   const int m0 = blockIdx.x * kRows;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages; ++s) {
+    for (int s = 0; s < (WIDE ? P.nstages : kStages); ++s) {
       ptx::mbar_init(&wfull[s], 1);
       ptx::mbar_init(&wempty[s], 1);
     }
     ptx::mbar_init(obs_bar, 1);
     ptx::mbar_init(acc_full, 1);
-    ptx::mbar_init(act_lo, kEpiWarps);
-    ptx::mbar_init(act_hi, kEpiWarps);
+    for (int p = 0; p < (WIDE ? 4 : 2); ++p) ptx::mbar_init(&act_rdy[p], kEpiWarps);
     ptx::fence_mbar_init();
     ptx::tma_prefetch_desc(&a.map_obs);
     for (int l = 0; l <= L; ++l) ptx::tma_prefetch_desc(&a.map_w[l]);
@@ -115,7 +120,19 @@ __global__ void __launch_bounds__(kThreads, 1) rollout_kernel(const __grid_const
       ptx::mbar_arrive_expect_tx(obs_bar, nobs * kChunk);
       for (int kc = 0; kc < nobs; ++kc) ptx::tma_load_2d(act_buf0 + kc * kChunk, &a.map_obs, obs_bar, kc * 64, m0);
       int it = 0;
-      for (int t = 0; t < T; ++t)
+      for (int t = 0; t < T && WIDE; ++t)
+        for (int l = 0; l <= L; ++l) {  // one [<=128 rows x 64 K] box per (K-chunk, N part)
+          const int nk = (a.in_p[l] + 63) / 64, np = (a.out_n[l] + 127) / 128;
+          const uint32_t bytes = uint32_t(P.wrows[l]) * 128u;
+          for (int kc = 0; kc < nk; ++kc)
+            for (int p = 0; p < np; ++p, ++it) {
+              const int s = it % P.nstages;
+              if (it >= P.nstages) ptx::mbar_wait_sleep(&wempty[s], ((it / P.nstages) - 1) & 1);
+              ptx::mbar_arrive_expect_tx(&wfull[s], bytes);
+              ptx::tma_load_2d(wring + s * kWideStage, &a.map_w[l], &wfull[s], kc * 64, p * 128);
+            }
+        }
+      for (int t = 0; t < T && !WIDE; ++t)
         for (int l = 0; l <= L; ++l) {
           const int nk = (a.in_p[l] + 63) / 64;
           const uint32_t bytes = uint32_t(a.out_n[l]) * 128u;
@@ -129,7 +146,43 @@ __global__ void __launch_bounds__(kThreads, 1) rollout_kernel(const __grid_const
     }
   } else if (warp == 1) {
     // ------------------------------------------------ MMA issuer
-    if (lane == 0) {
+    if (lane == 0 && WIDE) {
+      ptx::mbar_wait_sleep(obs_bar, 0);
+      int it = 0;
+      uint32_t ph[4] = {0u, 0u, 0u, 0u};
+      for (int t = 0; t < T; ++t)
+        for (int l = 0; l <= L; ++l) {
+          const bool first = t == 0 && l == 0;
+          const int K = a.in_p[l], nk = (K + 63) / 64, N = a.out_n[l], np = (N + 127) / 128;
+          const uint32_t in = ptx::smem_u32(smem + P.in_off[l]);
+          const uint32_t acc = tmem + uint32_t(P.tmem[l]);
+          int ready = 0;  // input K-chunk pairs known written
+          if (!first && P.drain[l])  // accumulator overlaps the previous layer's: wait for its whole drain
+            for (; ready < (nk + 1) / 2; ++ready) ptx::mbar_wait(&act_rdy[ready], (ph[ready]++) & 1);
+          for (int kc = 0; kc < nk; ++kc) {
+            if (!first && (kc >> 1) == ready) {
+              ptx::mbar_wait(&act_rdy[ready], (ph[ready]++) & 1);
+              ++ready;
+            }
+            const int ks = min(4, (K - kc * 64 + 15) / 16);
+            for (int p = 0; p < np; ++p, ++it) {
+              const int s = it % P.nstages;
+              ptx::mbar_wait(&wfull[s], (it / P.nstages) & 1);
+              ptx::tc_fence_after();
+              const uint32_t wb = ptx::smem_u32(wring + s * kWideStage);
+              const uint32_t idesc = ptx::umma_idesc_bf16(kRows, uint32_t(min(128, N - p * 128)), 0, 0);
+              for (int k = 0; k < ks; ++k) {
+                const uint64_t ad = ptx::umma_desc_sw128(in + kc * kChunk + k * 32, 16, 1024);
+                const uint64_t bd = ptx::umma_desc_sw128(wb + k * 32, 16, 1024);
+                ptx::mma_bf16(acc + p * 128, ad, bd, idesc, (kc > 0 || k > 0) ? 1u : 0u);
+              }
+              ptx::mma_commit(&wempty[s]);
+            }
+          }
+          ptx::mma_commit(acc_full);
+        }
+    }
+    if (lane == 0 && !WIDE) {
       ptx::mbar_wait_sleep(obs_bar, 0);
       int it = 0, ph_lo = 0, ph_hi = 0, acc_ph = 0;
       for (int t = 0; t < T; ++t)
@@ -194,18 +247,19 @@ __global__ void __launch_bounds__(kThreads, 1) rollout_kernel(const __grid_const
     for (int t = 0; t < T; ++t) {
       // ---- hidden layers: bias + ELU -> bf16 operand tile of the next layer
       for (int l = 0; l < L; ++l) {
-        const uint32_t acc = tmem + (accph & 1) * 256;
+        const uint32_t acc = WIDE ? tmem + uint32_t(P.tmem[l]) : tmem + (accph & 1) * 256;
         ptx::mbar_wait_sleep(acc_full, accph & 1);
         ++accph;
         ptx::tc_fence_after();
         trace_at(a, t * 16 + 2 * l);
-        uint8_t* out = (l & 1) ? act_buf0 : act_buf1;
+        uint8_t* out = WIDE ? smem + P.in_off[l + 1] : (l & 1) ? act_buf0 : act_buf1;
         const float* bias = a.bias[l];
         const int nchunks = a.out_n[l] / 32;
         // pass 0: columns 0..127 (chunks h), then release K-chunks 0-1 to the next layer's MMA;
-        // pass 1: columns 128..255 (chunks h + 4), then release K-chunks 2-3.
+        // pass 1: columns 128..255 (chunks h + 4), then release K-chunks 2-3 (WIDE: up to 4 passes).
+        const int npass = WIDE ? (a.out_n[l] + 127) / 128 : 2;
 #pragma unroll 1
-        for (int pass = 0; pass < 2; ++pass) {
+        for (int pass = 0; pass < npass; ++pass) {
           const int c = h + 4 * pass;
           if (c < nchunks) {
           uint32_t r[32];
@@ -233,18 +287,18 @@ __global__ void __launch_bounds__(kThreads, 1) rollout_kernel(const __grid_const
           ptx::fence_proxy_async_smem();
           ptx::tc_fence_before();
           __syncwarp();
-          if (pass == 1) trace_at(a, t * 16 + 2 * l + 1);
-          if (lane == 0) ptx::mbar_arrive(pass == 0 ? act_lo : act_hi);
+          if (pass == npass - 1) trace_at(a, t * 16 + 2 * l + 1);
+          if (lane == 0) ptx::mbar_arrive(WIDE ? &act_rdy[pass] : pass == 0 ? act_lo : act_hi);
         }
       }
 
       // ---- policy head: mu = acc + b_mu into smem (aliases the head's input tile)
-      const uint32_t hacc = tmem + (accph & 1) * 256;
+      const uint32_t hacc = WIDE ? tmem + uint32_t(P.tmem[L]) : tmem + (accph & 1) * 256;
       ptx::mbar_wait_sleep(acc_full, accph & 1);
       ++accph;
       ptx::tc_fence_after();
       trace_at(a, t * 16 + 10);
-      float* mu_s = reinterpret_cast<float*>((L & 1) ? act_buf1 : act_buf0);
+      float* mu_s = reinterpret_cast<float*>(WIDE ? smem + P.in_off[L] : (L & 1) ? act_buf1 : act_buf0);
       float* u_s = mu_s + kRows * kMuLd;
       if (h == 0) {
         uint32_t r[32];
@@ -373,8 +427,12 @@ __global__ void __launch_bounds__(kThreads, 1) rollout_kernel(const __grid_const
         __syncwarp();
         trace_at(a, t * 16 + 13);
         if (lane == 0) {
-          ptx::mbar_arrive(act_lo);
-          ptx::mbar_arrive(act_hi);
+          if constexpr (WIDE) {
+            for (int p = 0; p < (S_p + 127) / 128; ++p) ptx::mbar_arrive(&act_rdy[p]);
+          } else {
+            ptx::mbar_arrive(act_lo);
+            ptx::mbar_arrive(act_hi);
+          }
         }
       }
     }
@@ -408,23 +466,74 @@ bool rollout_fusable(int L, const int* widths_p, int S_p, int A) {
   return 2 * kRows * kMuLd * 4 <= int(kActBytes);
 }
 
-template <int MAXB>
+bool plan_wide(int L, const int* widths_p, int head_n, bool rollout, WidePlan* out) {
+  if (L < 1 || L > kRollMaxL) return false;
+  WidePlan P{};
+  auto chunks = [](int w) { return (w + 63) / 64; };
+  int main = 0;  // K-chunks of the in-place activation region
+  for (int l = 0; l <= L; ++l) {
+    if (widths_p[l] <= 0 || widths_p[l] > 512 || widths_p[l] % 32) return false;
+    if (l > 0) main = std::max(main, chunks(widths_p[l]));
+  }
+  const int obs = chunks(widths_p[0]);
+  const uint32_t budget = 232448u - 512u - 1024u;  // dynamic smem - barriers - alignment slack
+  if (rollout) {  // obs written in place by the env threads; mu / tanh(u) staging [2][128][kMuLd]
+    main = std::max({main, obs, int((2 * kRows * kMuLd * 4 + kChunk - 1) / kChunk)});
+  } else {  // own observation buffer when 4 ring stages still fit beside it (next tile's load overlaps)
+    P.obs_sep = uint32_t(main + obs) * kChunk + 4 * kWideStage <= budget;
+    if (!P.obs_sep) main = std::max(main, obs);
+  }
+  P.in_off[0] = P.obs_sep ? uint32_t(main) * kChunk : 0u;
+  P.ring_off = uint32_t(main + (P.obs_sep ? obs : 0)) * kChunk;
+  if (P.ring_off + 2 * kWideStage > budget) return false;
+  P.nstages = std::min<int>(8, int((budget - P.ring_off) / kWideStage));
+  P.bar_off = P.ring_off + uint32_t(P.nstages) * kWideStage;
+  P.smem = P.bar_off + 512 + 1024;
+  int prev_lo = 0, prev_hi = 0;
+  for (int l = 0; l <= L; ++l) {
+    const int o = l < L ? widths_p[l + 1] : head_n;
+    P.wrows[l] = std::min(128, o);
+    if (l == 0) {
+      P.tmem[0] = 0;
+    } else if (prev_hi + o <= 512) {  // beside the previous accumulator
+      P.tmem[l] = prev_hi;
+    } else {  // from column 0: overlaps it unless it ends below the previous start
+      P.tmem[l] = 0;
+      P.drain[l] = o > prev_lo;
+    }
+    prev_lo = P.tmem[l];
+    prev_hi = P.tmem[l] + o;
+  }
+  P.wrap = P.tmem[L] < widths_p[1];
+  *out = P;
+  return true;
+}
+
+bool rollout_wide_fusable(int L, const int* widths_p, int S_p, int A, WidePlan* plan) {
+  if (L < 1 || L > kRollMaxL || S_p > 128 || A > 31 || A < 1) return false;
+  return plan_wide(L, widths_p, A <= 16 ? 16 : 32, true, plan);  // obs / mu in the in-place region
+}
+
+template <int MAXB, bool WIDE>
 void launch_t(const RolloutArgs& a, cudaStream_t s) {
   static bool configured = false;
+  const uint32_t smem = WIDE ? a.plan.smem : kSmemBytes;
   if (!configured) {
     GMI_CUDA_CHECK(
-        cudaFuncSetAttribute(rollout_kernel<MAXB>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
+        cudaFuncSetAttribute(rollout_kernel<MAXB, WIDE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448));
     configured = true;
   }
   const int blocks = (a.N + kRows - 1) / kRows;
-  launch_pdl(rollout_kernel<MAXB>, dim3(blocks), dim3(kThreads), kSmemBytes, s, a);
+  launch_pdl(rollout_kernel<MAXB, WIDE>, dim3(blocks), dim3(kThreads), smem, s, a);
 }
 
 void launch_rollout(const RolloutArgs& a, cudaStream_t s) {
-  if (a.S_p <= 64)
-    launch_t<4>(a, s);
+  if (a.wide)
+    launch_t<8, true>(a, s);
+  else if (a.S_p <= 64)
+    launch_t<4, false>(a, s);
   else
-    launch_t<8>(a, s);
+    launch_t<8, false>(a, s);
 }
 
 }  // namespace gmi::ppo

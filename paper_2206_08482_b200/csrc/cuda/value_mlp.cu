@@ -28,38 +28,46 @@ constexpr uint32_t kActBytes = 4 * kChunk;
 constexpr uint32_t kWStage = 256 * 128;
 constexpr uint32_t kSmem = 2 * kActBytes + kStages * kWStage + 256 + 1024;
 
+// WIDE: hidden widths up to 512 with the shared-memory / TMEM plan a.plan (rollout.cuh), as
+// rollout_kernel<.., true>: 128-row weight parts, act_rdy[pair] per K-chunk pair, and hd_free
+// (the head accumulator read) before the next tile's layer 0 when their TMEM columns overlap.
+template <bool WIDE>
 __global__ void __launch_bounds__(kThreads, 1) value_mlp_kernel(const __grid_constant__ ValueArgs a) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = ptx::align_smem_1024(smem_raw);
+  const WidePlan& P = a.plan;
   uint8_t* act_buf0 = smem;
   uint8_t* act_buf1 = smem + kActBytes;
-  uint8_t* wring = smem + 2 * kActBytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(wring + kStages * kWStage);
+  uint8_t* wring = WIDE ? smem + P.ring_off : smem + 2 * kActBytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(WIDE ? smem + P.bar_off : wring + kStages * kWStage);
   uint64_t* wfull = bars;
-  uint64_t* wempty = bars + kStages;
-  uint64_t* obs_full = bars + 2 * kStages;
+  uint64_t* wempty = bars + (WIDE ? 8 : kStages);
+  uint64_t* obs_full = bars + (WIDE ? 16 : 2 * kStages);
   uint64_t* obs_free = obs_full + 1;
   uint64_t* acc_full = obs_free + 1;
   uint64_t* act_lo = acc_full + 1;
   uint64_t* act_hi = act_lo + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(act_hi + 1);
+  uint64_t* act_rdy = act_lo;       // WIDE: [4]
+  uint64_t* hd_free = act_lo + 4;   // WIDE: head accumulator drained
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(act_lo + 5);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int L = a.L;
   const int ntiles = (a.rows + kRows - 1) / kRows;
-  // the last MMA of a tile that reads the observation tile (act_buf0 = even layers)
-  const int last_even = (L % 2 == 0) ? L : L - 1;
+  // the last MMA of a tile that reads the observation tile (act_buf0 = even layers; WIDE: layer 0
+  // from its own buffer, else the head, the last reader of the in-place region)
+  const int last_even = WIDE ? (P.obs_sep ? 0 : L) : (L % 2 == 0) ? L : L - 1;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages; ++s) {
+    for (int s = 0; s < (WIDE ? P.nstages : kStages); ++s) {
       ptx::mbar_init(&wfull[s], 1);
       ptx::mbar_init(&wempty[s], 1);
     }
     ptx::mbar_init(obs_full, 1);
     ptx::mbar_init(obs_free, 1);
     ptx::mbar_init(acc_full, 1);
-    ptx::mbar_init(act_lo, kEpiWarps);
-    ptx::mbar_init(act_hi, kEpiWarps);
+    for (int p = 0; p < (WIDE ? 4 : 2); ++p) ptx::mbar_init(&act_rdy[p], kEpiWarps);
+    ptx::mbar_init(hd_free, kEpiWarps);
     ptx::fence_mbar_init();
     ptx::tma_prefetch_desc(&a.map_obs);
     for (int l = 0; l <= L; ++l) ptx::tma_prefetch_desc(&a.map_w[l]);
@@ -81,8 +89,19 @@ __global__ void __launch_bounds__(kThreads, 1) value_mlp_kernel(const __grid_con
         if (ti > 0) ptx::mbar_wait_sleep(obs_free, (ti - 1) & 1);
         ptx::mbar_arrive_expect_tx(obs_full, nobs * kChunk);
         for (int kc = 0; kc < nobs; ++kc)
-          ptx::tma_load_2d(act_buf0 + kc * kChunk, &a.map_obs, obs_full, kc * 64, j * kRows);
-        for (int l = 0; l <= L; ++l) {
+          ptx::tma_load_2d(smem + (WIDE ? P.in_off[0] : 0u) + kc * kChunk, &a.map_obs, obs_full, kc * 64, j * kRows);
+        for (int l = 0; l <= L && WIDE; ++l) {  // one [<=128 rows x 64 K] box per (K-chunk, N part)
+          const int nk = (a.in_p[l] + 63) / 64, np = (a.out_n[l] + 127) / 128;
+          const uint32_t bytes = uint32_t(P.wrows[l]) * 128u;
+          for (int kc = 0; kc < nk; ++kc)
+            for (int p = 0; p < np; ++p, ++it) {
+              const int s = it % P.nstages;
+              if (it >= P.nstages) ptx::mbar_wait_sleep(&wempty[s], ((it / P.nstages) - 1) & 1);
+              ptx::mbar_arrive_expect_tx(&wfull[s], bytes);
+              ptx::tma_load_2d(wring + s * kWideStage, &a.map_w[l], &wfull[s], kc * 64, p * 128);
+            }
+        }
+        for (int l = 0; l <= L && !WIDE; ++l) {
           const int nk = (a.in_p[l] + 63) / 64;
           const uint32_t bytes = uint32_t(a.out_n[l]) * 128u;
           for (int kc = 0; kc < nk; ++kc, ++it) {
@@ -96,7 +115,44 @@ __global__ void __launch_bounds__(kThreads, 1) value_mlp_kernel(const __grid_con
     }
   } else if (warp == 1) {
     // ------------------------------------------------ MMA issuer
-    if (lane == 0) {
+    if (lane == 0 && WIDE) {
+      int it = 0, ti = 0;
+      uint32_t ph[4] = {0u, 0u, 0u, 0u};
+      for (int j = blockIdx.x; j < ntiles; j += gridDim.x, ++ti)
+        for (int l = 0; l <= L; ++l) {
+          const int K = a.in_p[l], nk = (K + 63) / 64, N = a.out_n[l], np = (N + 127) / 128;
+          const uint32_t in = ptx::smem_u32(smem + P.in_off[l]);
+          const uint32_t acc = tmem + uint32_t(P.tmem[l]);
+          int ready = 0;
+          if (l == 0) {
+            ptx::mbar_wait(obs_full, ti & 1);
+            if (ti > 0 && P.wrap) ptx::mbar_wait(hd_free, (ti - 1) & 1);
+          } else if (P.drain[l]) {
+            for (; ready < (nk + 1) / 2; ++ready) ptx::mbar_wait(&act_rdy[ready], (ph[ready]++) & 1);
+          }
+          for (int kc = 0; kc < nk; ++kc) {
+            if (l > 0 && (kc >> 1) == ready) {
+              ptx::mbar_wait(&act_rdy[ready], (ph[ready]++) & 1);
+              ++ready;
+            }
+            const int ks = min(4, (K - kc * 64 + 15) / 16);
+            for (int p = 0; p < np; ++p, ++it) {
+              const int s = it % P.nstages;
+              ptx::mbar_wait(&wfull[s], (it / P.nstages) & 1);
+              ptx::tc_fence_after();
+              const uint32_t wb = ptx::smem_u32(wring + s * kWideStage);
+              const uint32_t idesc = ptx::umma_idesc_bf16(kRows, uint32_t(min(128, N - p * 128)), 0, 0);
+              for (int k = 0; k < ks; ++k)
+                ptx::mma_bf16(acc + p * 128, ptx::umma_desc_sw128(in + kc * kChunk + k * 32, 16, 1024),
+                              ptx::umma_desc_sw128(wb + k * 32, 16, 1024), idesc, (kc > 0 || k > 0) ? 1u : 0u);
+              ptx::mma_commit(&wempty[s]);
+            }
+          }
+          ptx::mma_commit(acc_full);
+          if (l == last_even) ptx::mma_commit(obs_free);  // the observation tile may be reloaded
+        }
+    }
+    if (lane == 0 && !WIDE) {
       int it = 0, ph_lo = 0, ph_hi = 0, acc_ph = 0, ti = 0;
       for (int j = blockIdx.x; j < ntiles; j += gridDim.x, ++ti)
         for (int l = 0; l <= L; ++l, ++acc_ph) {
@@ -132,15 +188,16 @@ __global__ void __launch_bounds__(kThreads, 1) value_mlp_kernel(const __grid_con
     int accph = 0;
     for (int j = blockIdx.x; j < ntiles; j += gridDim.x) {
       for (int l = 0; l < L; ++l) {
-        const uint32_t acc = tmem + (accph & 1) * 256;
+        const uint32_t acc = WIDE ? tmem + uint32_t(P.tmem[l]) : tmem + (accph & 1) * 256;
         ptx::mbar_wait_sleep(acc_full, accph & 1);
         ++accph;
         ptx::tc_fence_after();
-        uint8_t* out = (l & 1) ? act_buf0 : act_buf1;
+        uint8_t* out = WIDE ? smem + P.in_off[l + 1] : (l & 1) ? act_buf0 : act_buf1;
         const float* bias = a.bias[l];
         const int nchunks = a.out_n[l] / 32;
+        const int npass = WIDE ? (a.out_n[l] + 127) / 128 : 2;
 #pragma unroll 1
-        for (int pass = 0; pass < 2; ++pass) {
+        for (int pass = 0; pass < npass; ++pass) {
           const int c = h + 4 * pass;
           if (c < nchunks) {
             uint32_t r[32];
@@ -168,11 +225,11 @@ __global__ void __launch_bounds__(kThreads, 1) value_mlp_kernel(const __grid_con
           ptx::fence_proxy_async_smem();
           ptx::tc_fence_before();
           __syncwarp();
-          if (lane == 0) ptx::mbar_arrive(pass == 0 ? act_lo : act_hi);
+          if (lane == 0) ptx::mbar_arrive(WIDE ? &act_rdy[pass] : pass == 0 ? act_lo : act_hi);
         }
       }
       // ---- value head: V = acc[:, 0] + b_v
-      const uint32_t hacc = tmem + (accph & 1) * 256;
+      const uint32_t hacc = WIDE ? tmem + uint32_t(P.tmem[L]) : tmem + (accph & 1) * 256;
       ptx::mbar_wait_sleep(acc_full, accph & 1);
       ++accph;
       ptx::tc_fence_after();
@@ -184,6 +241,10 @@ __global__ void __launch_bounds__(kThreads, 1) value_mlp_kernel(const __grid_con
         if (grow < a.rows) a.V[grow] = __uint_as_float(r[0]) + a.bias[L][0];
       }
       ptx::tc_fence_before();
+      if constexpr (WIDE) {
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(hd_free);
+      }
     }
   }
 
@@ -194,14 +255,23 @@ __global__ void __launch_bounds__(kThreads, 1) value_mlp_kernel(const __grid_con
 
 }  // namespace
 
+bool value_wide_fusable(int L, const int* widths_p, WidePlan* plan) {
+  return plan_wide(L, widths_p, 16, false, plan);
+}
+
 void launch_value_mlp(const ValueArgs& a, int max_ctas, cudaStream_t s) {
   static bool configured = false;
   if (!configured) {
-    GMI_CUDA_CHECK(cudaFuncSetAttribute(value_mlp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
+    GMI_CUDA_CHECK(cudaFuncSetAttribute(value_mlp_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
+    GMI_CUDA_CHECK(cudaFuncSetAttribute(value_mlp_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448));
     configured = true;
   }
   const int tiles = (a.rows + kRows - 1) / kRows;
-  launch_pdl(value_mlp_kernel, dim3(std::max(1, std::min(tiles, max_ctas))), dim3(kThreads), kSmem, s, a);
+  const dim3 grid(std::max(1, std::min(tiles, max_ctas)));
+  if (a.wide)
+    launch_pdl(value_mlp_kernel<true>, grid, dim3(kThreads), a.plan.smem, s, a);
+  else
+    launch_pdl(value_mlp_kernel<false>, grid, dim3(kThreads), kSmem, s, a);
 }
 
 }  // namespace gmi::ppo

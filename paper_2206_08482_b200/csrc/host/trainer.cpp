@@ -874,14 +874,22 @@ void Trainer::build_plans() {
       sg.param_off = (sg.dst >= g.grad && sg.dst < g.grad + geo_.P) ? (long long)(sg.dst - g.grad) : -1;
 
     // fused value pass (value MLP on chip over all (T+1) x N observations)
+    // (hidden widths <= 256: value_mlp_kernel<false>; up to 512 when the tiles fit: <true>)
     const char* vunf = std::getenv("GMI_VALUE_UNFUSED");
-    g.fused_val = ppo::rollout_fusable(L, geo_.wp.data(), S_p, A) && !(vunf && vunf[0] == '1');
+    const char* nowide = std::getenv("GMI_NO_WIDE_FUSED");
+    const bool wide_ok = !(nowide && nowide[0] == '1');
+    ppo::WidePlan vplan{};
+    const bool val_narrow = ppo::rollout_fusable(L, geo_.wp.data(), S_p, A);
+    const bool val_wide = !val_narrow && wide_ok && ppo::value_wide_fusable(L, geo_.wp.data(), &vplan);
+    g.fused_val = (val_narrow || val_wide) && !(vunf && vunf[0] == '1');
     if (g.fused_val) {
       ppo::ValueArgs& v = g.val_args;
+      v.wide = val_wide;
+      v.plan = vplan;
       v.map_obs = tma_kmajor(g.X_roll, S_p, (long long)(T_ + 1) * g.N, S_p, kGemmBlockM);
       for (int l = 0; l < L; ++l) {
         const Tensor& t = geo_.net[1][l];
-        v.map_w[l] = tma_kmajor(shadow_ + t.w, t.in_p, t.out_p, t.in_p, t.out_p);
+        v.map_w[l] = tma_kmajor(shadow_ + t.w, t.in_p, t.out_p, t.in_p, val_wide ? vplan.wrows[l] : t.out_p);
         v.bias[l] = params_ + t.b;
         v.in_p[l] = t.in_p;
         v.out_n[l] = t.out_p;
@@ -899,7 +907,7 @@ void Trainer::build_plans() {
         c.map_obs = tma_kmajor(g.ch_X, S_p, (long long)(T_ + 1) * g.N, S_p, kGemmBlockM);
         for (int l = 0; l < L; ++l) {
           const Tensor& t = geo_.net[1][l];
-          c.map_w[l] = tma_kmajor(shadow_roll_ + t.w, t.in_p, t.out_p, t.in_p, t.out_p);
+          c.map_w[l] = tma_kmajor(shadow_roll_ + t.w, t.in_p, t.out_p, t.in_p, val_wide ? vplan.wrows[l] : t.out_p);
           c.bias[l] = params_roll_ + t.b;
         }
         c.map_w[L] = tma_kmajor(shadow_roll_ + geo_.net[1][L].w, hp, 1, hp, 16);
@@ -909,10 +917,16 @@ void Trainer::build_plans() {
     }
 
     // fused rollout (one persistent kernel per rollout) when the policy MLP fits on chip
+    // (hidden widths <= 256: rollout_kernel / the cluster variant; up to 512: rollout_kernel<8, true>)
     const char* unfused = std::getenv("GMI_ROLLOUT_UNFUSED");
-    g.fused_roll = ppo::rollout_fusable(L, geo_.wp.data(), S_p, A) && !(unfused && unfused[0] == '1');
+    ppo::WidePlan rplan{};
+    const bool roll_narrow = ppo::rollout_fusable(L, geo_.wp.data(), S_p, A);
+    const bool roll_wide = !roll_narrow && wide_ok && ppo::rollout_wide_fusable(L, geo_.wp.data(), S_p, A, &rplan);
+    g.fused_roll = (roll_narrow || roll_wide) && !(unfused && unfused[0] == '1');
     if (g.fused_roll) {
       ppo::RolloutArgs& r = g.roll_args;
+      r.wide = roll_wide;
+      r.plan = rplan;
       // decoupled mode: the serving GMI acts with the policy snapshot and writes the channel
       __nv_bfloat16* wsrc = decoupled_ ? shadow_roll_ : shadow_;
       float* psrc = decoupled_ ? params_roll_ : params_;
@@ -920,7 +934,7 @@ void Trainer::build_plans() {
       r.map_obs = tma_kmajor(Xr, S_p, g.N, S_p, kGemmBlockM);
       for (int l = 0; l < L; ++l) {
         const Tensor& t = geo_.net[0][l];
-        r.map_w[l] = tma_kmajor(wsrc + t.w, t.in_p, t.out_p, t.in_p, t.out_p);
+        r.map_w[l] = tma_kmajor(wsrc + t.w, t.in_p, t.out_p, t.in_p, roll_wide ? rplan.wrows[l] : t.out_p);
         r.bias[l] = psrc + t.b;
         r.in_p[l] = t.in_p;
         r.out_n[l] = t.out_p;
@@ -929,7 +943,7 @@ void Trainer::build_plans() {
       r.map_w[L] = tma_kmajor(wsrc + geo_.net[0][L].w, hp, A, hp, head_n);
       // cluster variant: 64-row weight slices per CTA, 16-row head (rollout_cluster.cu)
       const char* nocl = std::getenv("GMI_ROLLOUT_NOCLUSTER");
-      g.roll_cluster = (nocl && nocl[0] == '1') ? 0 : ppo::rollout_cluster_size(L, geo_.wp.data(), S_p, A, g.N);
+      g.roll_cluster = (nocl && nocl[0] == '1') || roll_wide ? 0 : ppo::rollout_cluster_size(L, geo_.wp.data(), S_p, A, g.N);
       // a small serving partition runs the rollout in waves: one CTA per env tile then beats
       // 4-CTA clusters (measured on B200: 1.9 vs 4.3 ms for 4096 envs on 16 SMs)
       if (decoupled_ && exec_->sm_count(0) > 0 && g.roll_cluster * (g.N / kGemmBlockM) > exec_->sm_count(0))

@@ -150,11 +150,15 @@ def test_minibatch_gradient_bench_kernels_match_oracle(cuda, monkeypatch, env):
             assert np.linalg.norm(a - b) <= 2e-2 * ref, (key, part, np.linalg.norm(a - b) / ref)
 
 
-@pytest.mark.parametrize("dims", [(12, 3, [64, 64]), (60, 8, [256, 256, 256]), (40, 20, [96, 160])])
+@pytest.mark.parametrize("dims", [(12, 3, [64, 64]), (60, 8, [256, 256, 256]), (40, 20, [96, 160]),
+                                  (108, 21, [200, 400, 100]), (40, 20, [96, 448, 160, 64])])
 def test_fused_rollout_matches_per_layer_path(cuda, monkeypatch, dims):
     """cuda/rollout.cu (one persistent kernel) vs the per-layer GEMM + act/env path: the MLP
     arithmetic is identical, so integer state, actions and observations agree bit-for-bit;
-    rewards / log-probs differ only in the order of their small reductions."""
+    rewards / log-probs differ only in the order of their small reductions. The last two shapes
+    (HM 108:200:400:100 and a 4-layer net) take the wide variant (rollout_kernel<8, true>,
+    value_mlp_kernel<true>: 128-row weight parts, TMEM accumulators that wait for the previous
+    layer's drain where they overlap)."""
     from paper_2206_08482_b200.ppo import PpoConfig, Trainer
     S, A, hidden = dims
     cfg = dict(obs_dim=S, act_dim=A, hidden=hidden, num_envs=200)
@@ -173,6 +177,8 @@ def test_fused_rollout_matches_per_layer_path(cuda, monkeypatch, dims):
             assert np.array_equal(fused.get(f), plain.get(f)), f
         for f in ("rew", "logp"):
             np.testing.assert_allclose(fused.get(f), plain.get(f), rtol=1e-5, atol=1e-5)
+    # the fused path really ran: one rollout + one value launch instead of T x (L + 2) + ...
+    assert fused.synchronize().kernel_launches < plain.synchronize().kernel_launches
 
 
 def _grad_pair(monkeypatch, env_first, env_second, dims, envs=200):

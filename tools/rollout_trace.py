@@ -13,10 +13,15 @@ from paper_2206_08482_b200.ppo import PpoConfig, Trainer  # noqa: E402
 
 
 def main():
-    cfg = PpoConfig.from_config_file(os.path.join(os.path.dirname(__file__), "..", "configs", "at_4096env_3x256.cfg"))
+    path = sys.argv[1] if len(sys.argv) > 1 else os.path.join(os.path.dirname(__file__), "..", "configs",
+                                                               "at_4096env_3x256.cfg")
+    cfg = PpoConfig.from_config_file(path)
+    cfg.gmis_per_gpu, cfg.gmi_backend, cfg.sm_per_gmi = 1, 0, 0  # one GMI on the whole GPU
     t = Trainer(cfg)
-    for _ in range(3):
+    for _ in range(3):  # the hook's rollout is consumed by the next iteration
         t.rollout()
+        t.iteration()
+    t.rollout()
     tr = t.get("rollout_trace").view(np.int64).reshape(cfg.horizon, 16).astype(np.float64)
     L = len(cfg.hidden)
     names, cols = [], []
