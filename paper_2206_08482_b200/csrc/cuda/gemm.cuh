@@ -143,7 +143,11 @@ __global__ void __launch_bounds__(gemm_threads(EPI) + 128 * CS, 1)
   uint64_t* tfull_bar = empty_bar + S;   // [2] accumulator ready
   uint64_t* tempty_bar = tfull_bar + 2;  // [2] accumulator drained
   uint64_t* bres_bar = tempty_bar + 2;   // WS: resident B landed
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bres_bar + 1);
+  uint64_t* bfree_bar = bres_bar + 1;    // chained WS: every MMA on the resident B done
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bfree_bar + 1);
+  // chained WS: per epilogue warp, how many of the CTA's tiles (in processing order, all
+  // layers) have their H stores complete in global memory
+  volatile int* stored_s = reinterpret_cast<volatile int*>(tmem_slot + 1);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -156,6 +160,8 @@ __global__ void __launch_bounds__(gemm_threads(EPI) + 128 * CS, 1)
       ptx::tma_load_2d(sb, &pr.map_b, bar, k0, n0 + pr.b_row0);
     }
   };
+  // chained layers (WS forward only): layer c's problems are prob[c * num_problems + i]
+  const int nchain = (WS && EPI == EPI_BIAS_ELU && P.chain > 1) ? P.chain : 1;
   const int mtiles = (p0.M + kGemmBlockM - 1) / kGemmBlockM;
   const int ntiles = (p0.N + BN - 1) / BN;
   const int per_prob = P.splits * mtiles * ntiles;
@@ -172,8 +178,10 @@ __global__ void __launch_bounds__(gemm_threads(EPI) + 128 * CS, 1)
       ptx::mbar_init(&tempty_bar[b], kEpiWarps);
     }
     ptx::mbar_init(bres_bar, 1);
+    ptx::mbar_init(bfree_bar, 1);
+    for (int e = 0; e < kEpiWarps; ++e) stored_s[e] = 0;
     ptx::fence_mbar_init();
-    for (int i = 0; i < P.num_problems; ++i) {
+    for (int i = 0; i < P.num_problems * nchain; ++i) {
       ptx::tma_prefetch_desc(&P.prob[i].map_a);
       ptx::tma_prefetch_desc(&P.prob[i].map_b);
       ptx::tma_prefetch_desc(&P.prob[i].map_out);
@@ -227,10 +235,24 @@ __global__ void __launch_bounds__(gemm_threads(EPI) + 128 * CS, 1)
     // ---------------- TMA producer (one lane)
     if (lane == 0) {
       int it = 0, plt = 0;
-      for (int tile = blockIdx.x; tile < ntile_total; tile += gridDim.x, ++plt) {
+      const int ntl = (ntile_total - int(blockIdx.x) + int(gridDim.x) - 1) / int(gridDim.x);  // tiles per layer
+      for (int ci = 0; ci < nchain; ++ci) {
+      const int pb0 = ci * P.num_problems;
+      int lt = 0;
+      for (int tile = blockIdx.x; tile < ntile_total; tile += gridDim.x, ++plt, ++lt) {
         int prob, split, m0, n0, kb0, nkb;
         decode(tile, prob, split, m0, n0, kb0, nkb);
-        const GemmProblem& pr = P.prob[prob];
+        const GemmProblem& pr = P.prob[pb0 + prob];
+        if (nchain > 1) {
+          nkb = (pr.K + kGemmBlockK - 1) / kGemmBlockK;
+          if (ci > 0) {  // this row tile's layer ci-1 output (stored by this CTA) is in global memory
+            const int need = (ci - 1) * ntl + lt + 1;
+            for (int e = 0; e < kEpiWarps; ++e)
+              while (stored_s[e] < need) __nanosleep(64);
+            __threadfence_block();
+            ptx::fence_proxy_async_global();
+          }
+        }
         gemm_stamp(P.trace, plt, 7);
         for (int i = 0; i < nkb; ++i, ++it) {
           const int s = it % S;
@@ -239,7 +261,7 @@ __global__ void __launch_bounds__(gemm_threads(EPI) + 128 * CS, 1)
           const int k0 = (kb0 + i) * kGemmBlockK;
           // WS: the CTA's first tile also brings the resident B k-block i on the same barrier,
           // so the first MMAs start after one k-block instead of after the whole weight tile.
-          const bool first_ws = WS && !P.b_stable && it < nkb_total;
+          const bool first_ws = WS && !P.b_stable && ci == 0 && it < nkb;
           ptx::mbar_arrive_expect_tx(&full_bar[s], L::kStage + (first_ws ? L::kB : 0u));
           if (first_ws) load_b(pr, b_res + i * L::kB, &full_bar[s], 0, k0);
           if constexpr (A_MN) {
@@ -251,17 +273,29 @@ __global__ void __launch_bounds__(gemm_threads(EPI) + 128 * CS, 1)
           }
           if constexpr (!WS) load_b(pr, sa + L::kA, &full_bar[s], n0, k0);
         }
+        if (ci > 0 && lt == 0) {  // the layer's resident weights, once every MMA on the previous ones is
+          // done (after the first tile's activation loads, which only need free ring stages)
+          ptx::mbar_wait(bfree_bar, (ci - 1) & 1);
+          const GemmProblem& pb = P.prob[pb0 + blockIdx.x % P.num_problems];
+          const int nkbb = (pb.K + kGemmBlockK - 1) / kGemmBlockK;
+          ptx::mbar_arrive_expect_tx(bres_bar, uint32_t(nkbb) * L::kB);
+          for (int i = 0; i < nkbb; ++i) load_b(pb, b_res + i * L::kB, bres_bar, 0, i * kGemmBlockK);
+        }
         gemm_stamp(P.trace, plt, 8);
+      }
       }
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer (one lane), double-buffered TMEM accumulators
     if (lane == 0) {
-      int it = 0, lt = 0;
-      if (WS && P.b_stable && int(blockIdx.x) < ntile_total) ptx::mbar_wait(bres_bar, 0);  // resident B landed
+      int it = 0, lt = 0, bph = 0;
+      if (WS && P.b_stable && int(blockIdx.x) < ntile_total) ptx::mbar_wait(bres_bar, (bph++) & 1);  // resident B landed
+      for (int ci = 0; ci < nchain; ++ci) {
+      if (ci > 0 && int(blockIdx.x) < ntile_total) ptx::mbar_wait(bres_bar, (bph++) & 1);  // next layer's B landed
       for (int tile = blockIdx.x; tile < ntile_total; tile += gridDim.x, ++lt) {
         int prob, split, m0, n0, kb0, nkb;
         decode(tile, prob, split, m0, n0, kb0, nkb);
+        if (nchain > 1) nkb = (P.prob[ci * P.num_problems + prob].K + kGemmBlockK - 1) / kGemmBlockK;
         const int buf = lt & 1;
         gemm_stamp(P.trace, lt, 0);
         if (lt >= 2) ptx::mbar_wait(&tempty_bar[buf], ((lt >> 1) - 1) & 1);
@@ -290,6 +324,8 @@ __global__ void __launch_bounds__(gemm_threads(EPI) + 128 * CS, 1)
         ptx::mma_commit(&tfull_bar[buf]);
         gemm_stamp(P.trace, lt, 3);
       }
+      if (ci + 1 < nchain) ptx::mma_commit(bfree_bar);  // the resident B may be replaced
+      }
     }
   } else if (warp < 2 + kEpiWarps) {
     // ---------------- epilogue warps: TMEM lane quarter q, every W-th 32-column chunk
@@ -300,17 +336,22 @@ __global__ void __launch_bounds__(gemm_threads(EPI) + 128 * CS, 1)
     constexpr int kChunks = BN / 32;
     uint8_t* stage_base = staging + e * L::kStagingBufs * L::kStaging;
     float* bias_s = reinterpret_cast<float*>(staging + kEpiWarps * L::kStagingBufs * L::kStaging);
+    int sbuf = 0;
+    int lt = 0;
+    const int ntl = (ntile_total - int(blockIdx.x) + int(gridDim.x) - 1) / int(gridDim.x);  // tiles per layer
+    for (int ci = 0; ci < nchain; ++ci) {
+    const int pb0 = ci * P.num_problems;
     if constexpr (L::kBias > 0) {  // WS: this CTA's problem is blockIdx.x % problems for every tile
-      const GemmProblem& pb = P.prob[blockIdx.x % P.num_problems];
+      const GemmProblem& pb = P.prob[pb0 + blockIdx.x % P.num_problems];
+      if (ci > 0) asm volatile("bar.sync 1, %0;" ::"r"(kEpiWarps * 32));  // layer ci-1's bias reads done
       for (int i = e * 32 + lane; i < BN; i += kEpiWarps * 32) bias_s[i] = i < pb.N ? pb.bias[i] : 0.f;
       asm volatile("bar.sync 1, %0;" ::"r"(kEpiWarps * 32));
     }
-    int sbuf = 0;
-    int lt = 0;
-    for (int tile = blockIdx.x; tile < ntile_total; tile += gridDim.x, ++lt) {
+    for (int tile = blockIdx.x, tl = 0; tile < ntile_total; tile += gridDim.x, ++lt, ++tl) {
       int prob, split, m0, n0, kb0, nkb;
       decode(tile, prob, split, m0, n0, kb0, nkb);
-      const GemmProblem& pr = P.prob[prob];
+      const GemmProblem& pr = P.prob[pb0 + prob];
+      if (nchain > 1) nkb = (pr.K + kGemmBlockK - 1) / kGemmBlockK;
       const int buf = lt & 1;
       const int rbase = m0 + q * 32;
       const int row = rbase + lane;
@@ -426,6 +467,20 @@ __global__ void __launch_bounds__(gemm_threads(EPI) + 128 * CS, 1)
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(&tempty_bar[buf]);
       gemm_stamp(etr, lt, 6);
+      if (nchain > 1 && ci + 1 < nchain && lane == 0) {
+        // publish store completion for the next layer's producer: the previous tile's stores
+        // (all but this tile's kUnits / 2 groups) without waiting, and everything at the layer's end
+        if (tl + 1 == ntl) {
+          ptx::bulk_wait<0>();
+          __threadfence_block();
+          stored_s[e] = lt + 1;
+        } else {
+          ptx::bulk_wait<kUnits / 2>();
+          __threadfence_block();
+          stored_s[e] = lt;
+        }
+      }
+    }
     }
     if (lane == 0) ptx::bulk_wait<0>();
   } else if constexpr (CS) {

@@ -170,6 +170,13 @@ void gemm_launch(const GemmParams& P, int bn, int a_mn, int b_mn, int epi, cudaS
       invalid("weight-stationary GEMM needs splits == 1, N <= block_n, K <= 256");
     ctas = gemm_ws_grid(P.prob[0].M, P.num_problems, max_ctas > 0 ? max_ctas : sms);
   }
+  if (P.chain > 1) {  // chained forward layers: one grid shape for all of them
+    if (!ws || epi != EPI_BIAS_ELU || P.chain * P.num_problems > kGemmMaxProblems)
+      invalid("chained GEMM: weight-stationary forward layers only, at most 8 problems in all");
+    for (int i = 0; i < P.chain * P.num_problems; ++i)
+      if (P.prob[i].M != P.prob[0].M || P.prob[i].N != bn || P.prob[i].K > kGemmMaxKbWS * kGemmBlockK)
+        invalid("chained GEMM layers must share M and have N == block_n, K <= 256");
+  }
   switch (bn) {
     case 64: return launch_bn<64>(P, a_mn, b_mn, epi, ctas, s, ws);
     case 128: return launch_bn<128>(P, a_mn, b_mn, epi, ctas, s, ws);

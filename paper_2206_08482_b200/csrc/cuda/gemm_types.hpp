@@ -35,8 +35,12 @@ struct alignas(64) GemmProblem {
 };
 
 // All problems of one launch share M, N, K and the split count (grouped GEMM).
+constexpr int kGemmMaxProblems = 8;
+
 struct alignas(64) GemmParams {
-  GemmProblem prob[4];  // grouped problems (e.g. policy / value nets, or their N-halves)
+  // grouped problems (e.g. policy / value nets, or their N-halves); chained launches hold
+  // layer c's problems at prob[c * num_problems + i]
+  GemmProblem prob[kGemmMaxProblems];
   int num_problems;
   int splits;
   // Weight-stationary launches: B (the layer's weights) is not written by the preceding
@@ -44,6 +48,12 @@ struct alignas(64) GemmParams {
   // load overlaps the previous kernel's tail (set by the host when no in-stream kernel updates
   // the weights right before this launch).
   int b_stable;
+  // Chained weight-stationary forward (EPI_BIAS_ELU): `chain` consecutive hidden layers in one
+  // launch. Every CTA keeps its row tiles for all layers (layer c+1's tile m reads the H tile m
+  // this CTA stored for layer c), so there is no cross-CTA dependency between the layers: a CTA
+  // swaps in the next layer's resident weights as soon as its MMAs of the layer are done and
+  // goes on, instead of a kernel boundary (launch, prologue, pipeline fill, wave tail) per layer.
+  int chain;
   unsigned long long* trace;  // optional [8 tiles][16] globaltimer stamps of CTA 0 (development aid)
 };
 

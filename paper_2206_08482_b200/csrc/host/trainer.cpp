@@ -165,6 +165,8 @@ struct Trainer::Gmi {
   int head_grid = 0;
   ppo::HeadFusedArgs head_args{};
   bool fused_fwd = false;  // hidden forward + head step in one launch (train_fwd.cu)
+  GemmParams fwd_chain{};  // all hidden forward layers (both nets) chained in one launch
+  bool chain_fwd = false;
   // decoupled mode, nets too wide for the fused rollout / value kernels: the serving GMI's own
   // per-layer plans (channel observations, snapshot weights, its own activation buffers)
   bool srv_layers = false;
@@ -780,6 +782,20 @@ void Trainer::build_plans() {
       // Opt-in (GMI_TRAIN_FWD=1): bit-identical, but with one tile in flight per CTA its MMA ->
       // epilogue chain is serial and it measured slower on B200 than the per-layer GEMMs plus
       // the fused head kernel, which overlap through PDL (3.65 vs 3.37 ms per iteration).
+      // chained training forward (gemm.cuh, GemmParams::chain): every hidden layer weight-stationary
+      // with the same full-width block N, so each CTA carries its row tiles through all layers
+      const char* nochain = std::getenv("GMI_FWD_CHAIN");
+      g.chain_fwd = !(nochain && nochain[0] == '0') && 2 * L <= kGemmMaxProblems;
+      for (int l = 0; l < L; ++l)
+        g.chain_fwd = g.chain_fwd && g.ws_fwd[l] && g.bn_fwd[l] == g.bn_fwd[0] && geo_.wp[l + 1] == g.bn_fwd[0];
+      if (g.chain_fwd) {
+        g.fwd_chain = GemmParams{};
+        for (int l = 0; l < L; ++l)
+          for (int n = 0; n < 2; ++n) g.fwd_chain.prob[2 * l + n] = g.fwd_train[l].prob[n];
+        g.fwd_chain.num_problems = 2;
+        g.fwd_chain.splits = 1;
+        g.fwd_chain.chain = L;
+      }
       const char* fwd_on = std::getenv("GMI_TRAIN_FWD");
       g.fused_fwd = ppo::train_fwd_fusable(L, geo_.wp.data(), S_p, A) && fwd_on && fwd_on[0] == '1';
       if (g.fused_fwd) {
@@ -1162,7 +1178,7 @@ void Trainer::timed(cudaStream_t s, int phase, double flop, double bytes, F&& f)
 // rows) count it once.
 static double gemm_bytes(const GemmParams& P, int epi) {
   double b = 0;
-  for (int i = 0; i < P.num_problems; ++i) {
+  for (int i = 0; i < P.num_problems * std::max(1, P.chain); ++i) {
     const GemmProblem& p = P.prob[i];
     bool a_seen = false;
     for (int j = 0; j < i; ++j) a_seen |= std::memcmp(&P.prob[j].map_a, &p.map_a, sizeof(CUtensorMap)) == 0;
@@ -1335,7 +1351,14 @@ void Trainer::train_minibatch(Gmi& g, int k, int adam_step) {
     timed(g.s, GMI_PH_FWD_GEMM, flop, 0.0, [&] { ppo::launch_train_fwd(f, g.head_grid, g.s); });
     ++launches_;
   }
-  for (int l = 0; l < L && !g.fused_fwd; ++l) {
+  if (g.chain_fwd && !g.fused_fwd) {  // all hidden layers of both nets in one launch
+    GemmParams P = g.fwd_chain;
+    P.prob[0].a_row0 = P.prob[1].a_row0 = k * g.Bm;
+    double flop = 0;
+    for (int l = 0; l < L; ++l) flop += g.flop_fwd[l];
+    gemm(g, GMI_PH_FWD_GEMM, P, g.bn_fwd[0], 0, 0, EPI_BIAS_ELU, flop, 1);
+  }
+  for (int l = 0; l < L && !g.fused_fwd && !g.chain_fwd; ++l) {
     GemmParams P = g.fwd_train[l];
     if (l == 0) P.prob[0].a_row0 = P.prob[1].a_row0 = k * g.Bm;
     gemm(g, GMI_PH_FWD_GEMM, P, g.bn_fwd[l], 0, 0, EPI_BIAS_ELU, g.flop_fwd[l], g.ws_fwd[l]);

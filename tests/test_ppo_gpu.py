@@ -361,3 +361,20 @@ def test_adam_fused_into_gradient_assembly_is_bit_identical(cuda, monkeypatch):
         monkeypatch.setenv("GMI_ADAM_FUSED", "1")
         fused.iteration()
     assert np.array_equal(plain.get("params").view(np.uint32), fused.get("params").view(np.uint32))
+
+
+@pytest.mark.parametrize("envs", [1536, 4096])
+def test_chained_forward_is_bit_identical(cuda, monkeypatch, envs):
+    """GemmParams::chain (all hidden forward layers of both nets in one weight-stationary launch,
+    each CTA carrying its row tiles through the layers) vs one launch per layer (GMI_FWD_CHAIN=0):
+    same tiles, same MMA K order, same epilogue, so two iterations leave bit-identical parameters.
+    1536 envs gives CTAs with one and with two row tiles per layer, 4096 the bench's three / four."""
+    from paper_2206_08482_b200.ppo import PpoConfig, Trainer
+    cfg = dict(obs_dim=60, act_dim=8, hidden=[256, 256, 256], num_envs=envs)
+    chained = Trainer(PpoConfig(**cfg))
+    monkeypatch.setenv("GMI_FWD_CHAIN", "0")
+    plain = Trainer(PpoConfig(**cfg))
+    for _ in range(2):
+        a, b = chained.iteration(), plain.iteration()
+        assert a.kernel_launches < b.kernel_launches  # the chained launch really ran
+    assert np.array_equal(chained.get("params").view(np.uint32), plain.get("params").view(np.uint32))
