@@ -86,6 +86,9 @@ __device__ __forceinline__ void gemm_stamp(unsigned long long* tr, int lt, int k
 #ifndef GMI_WS_STAGING
 #define GMI_WS_STAGING 1
 #endif
+#ifndef GMI_DX_AUX_BUFS
+#define GMI_DX_AUX_BUFS 2
+#endif
 
 template <int BN, int EPI, int WS>
 struct GemmSmem {
@@ -104,16 +107,23 @@ struct GemmSmem {
   // (K <= 256 is 4 k-blocks), so the next tile's rows are in flight while this tile's MMAs run
   // WS forward: the CTA's bias row (one problem per CTA, n0 = 0) staged in shared memory once
   static constexpr uint32_t kBias = (WS && EPI == 0) ? BN * 4 : 0;
-  static constexpr int kWsFit = int((232448u - 1280u - kBias - kBRes - kEpiWarps * kStagingBufs * kStaging) / kA);
+  // WS input gradient: the elu' operand (H rows of the tile) staged by TMA, double-buffered
+  // [buf][BN / 64 boxes][128 rows][64 cols] SW128, instead of per-thread global loads in the epilogue
+  // (BN <= 128: at BN = 256 the resident weights leave no room; the global-load path is kept)
+  static constexpr int kAuxBufs = (WS && EPI == 1 && BN <= 128) ? GMI_DX_AUX_BUFS : 0;
+  static constexpr uint32_t kAuxBox = kGemmBlockM * 128;  // 128 rows x 64 bf16 columns
+  static constexpr uint32_t kAux = kAuxBufs * (BN / 64) * kAuxBox;
+  static constexpr int kWsFit = int((232448u - 1536u - kBias - kAux - kBRes - kEpiWarps * kStagingBufs * kStaging) / kA);
   // split-K weight gradients: as many operand stages as fit (up to 8) -- the kernel streams a
   // long K range per CTA and is bound by bytes in flight
-  static constexpr int kDwFit = int((232448u - 1280u - kEpiWarps * kStagingBufs * kStaging) / (kA + kB));
+  static constexpr int kDwFit = int((232448u - 1536u - kEpiWarps * kStagingBufs * kStaging) / (kA + kB));
   static constexpr int kStages = WS     ? (kWsFit < GMI_WS_STAGES ? kWsFit : GMI_WS_STAGES)
                                  : kDw4 ? (kDwFit < 8 ? kDwFit : 8)
                                         : (BN == 256 ? 3 : 4);
   static constexpr uint32_t kStage = WS ? kA : kA + kB;
-  static constexpr uint32_t kBarOff = kStages * kStage + kBRes + kEpiWarps * kStagingBufs * kStaging + kBias;
-  static constexpr uint32_t kBytes = kBarOff + 256 + 1024;  // + barriers + alignment slack
+  static constexpr uint32_t kAuxOff = kStages * kStage + kBRes;  // 1024-aligned (SW128 boxes)
+  static constexpr uint32_t kBarOff = kAuxOff + kAux + kEpiWarps * kStagingBufs * kStaging + kBias;
+  static constexpr uint32_t kBytes = kBarOff + 512 + 1024;  // + barriers + alignment slack
   static constexpr uint32_t kTmemCols = 2 * BN < 32 ? 32 : 2 * BN;
   static_assert(kBytes <= 232448, "shared memory budget");
 };
@@ -137,7 +147,8 @@ __global__ void __launch_bounds__(gemm_threads(EPI) + 128 * CS, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = ptx::align_smem_1024(smem_raw);
   uint8_t* b_res = smem + S * L::kStage;  // WS: resident B, k-block j at j * kB
-  uint8_t* staging = b_res + L::kBRes;
+  uint8_t* aux_s = smem + L::kAuxOff;     // WS input gradient: staged elu' operand
+  uint8_t* staging = aux_s + L::kAux;
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + L::kBarOff);
   uint64_t* empty_bar = full_bar + S;
   uint64_t* tfull_bar = empty_bar + S;   // [2] accumulator ready
@@ -148,6 +159,8 @@ __global__ void __launch_bounds__(gemm_threads(EPI) + 128 * CS, 1)
   // chained WS: per epilogue warp, how many of the CTA's tiles (in processing order, all
   // layers) have their H stores complete in global memory
   volatile int* stored_s = reinterpret_cast<volatile int*>(tmem_slot + 1);
+  uint64_t* auxf_bar = reinterpret_cast<uint64_t*>(smem + L::kBarOff + 256);  // [kAuxBufs] aux landed
+  uint64_t* auxe_bar = auxf_bar + 2;                                          // [kAuxBufs] aux consumed
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -179,12 +192,17 @@ __global__ void __launch_bounds__(gemm_threads(EPI) + 128 * CS, 1)
     }
     ptx::mbar_init(bres_bar, 1);
     ptx::mbar_init(bfree_bar, 1);
+    for (int b = 0; b < L::kAuxBufs; ++b) {
+      ptx::mbar_init(&auxf_bar[b], 1);
+      ptx::mbar_init(&auxe_bar[b], kEpiWarps);
+    }
     for (int e = 0; e < kEpiWarps; ++e) stored_s[e] = 0;
     ptx::fence_mbar_init();
     for (int i = 0; i < P.num_problems * nchain; ++i) {
       ptx::tma_prefetch_desc(&P.prob[i].map_a);
       ptx::tma_prefetch_desc(&P.prob[i].map_b);
       ptx::tma_prefetch_desc(&P.prob[i].map_out);
+      if constexpr (L::kAuxBufs > 0) ptx::tma_prefetch_desc(&P.prob[i].map_aux);
     }
     if constexpr (WS) {
       // stable weights: the whole resident B before griddepcontrol.wait (overlaps the tail of
@@ -272,6 +290,14 @@ __global__ void __launch_bounds__(gemm_threads(EPI) + 128 * CS, 1)
             ptx::tma_load_2d(sa, &pr.map_a, &full_bar[s], k0, m0 + pr.a_row0);
           }
           if constexpr (!WS) load_b(pr, sa + L::kA, &full_bar[s], n0, k0);
+        }
+        if constexpr (L::kAuxBufs > 0) {  // the tile's elu' operand rows, into the aux ring
+          const int ab = plt % L::kAuxBufs;
+          if (plt >= L::kAuxBufs) ptx::mbar_wait(&auxe_bar[ab], ((plt / L::kAuxBufs) - 1) & 1);
+          ptx::mbar_arrive_expect_tx(&auxf_bar[ab], (BN / 64) * L::kAuxBox);
+#pragma unroll
+          for (int j = 0; j < BN / 64; ++j)
+            ptx::tma_load_2d(aux_s + (ab * (BN / 64) + j) * L::kAuxBox, &pr.map_aux, &auxf_bar[ab], n0 + 64 * j, m0);
         }
         if (ci > 0 && lt == 0) {  // the layer's resident weights, once every MMA on the previous ones is
           // done (after the first tile's activation loads, which only need free ring stages)
@@ -366,11 +392,19 @@ __global__ void __launch_bounds__(gemm_threads(EPI) + 128 * CS, 1)
           for (int qd = 0; qd < 4; ++qd) dst[qd] = hp[qd];
         }
       };
-      if constexpr (EPI == EPI_DACT) load_aux(h, hv);
+      if constexpr (EPI == EPI_DACT && L::kAuxBufs == 0) load_aux(h, hv);
+      // staged elu' operand: this thread's row of chunk c (32 columns = 4 x 16 B, SW128 box c / 2)
+      auto lds_aux = [&](int c, uint4(&dst)[4]) {
+        const uint8_t* box = aux_s + ((lt % (L::kAuxBufs > 0 ? L::kAuxBufs : 1)) * (BN / 64) + (c >> 1)) * L::kAuxBox;
+#pragma unroll
+        for (int qd = 0; qd < 4; ++qd)
+          dst[qd] = *reinterpret_cast<const uint4*>(box + (q * 32 + lane) * 128 + ((((c & 1) * 4 + qd) ^ (lane & 7)) << 4));
+      };
       unsigned long long* etr = (warp == 2 && lane == 0) ? P.trace : nullptr;
       ptx::mbar_wait(&tfull_bar[buf], (lt >> 1) & 1);
       gemm_stamp(etr, lt, 4);
       ptx::tc_fence_after();
+      if constexpr (L::kAuxBufs > 0) ptx::mbar_wait(&auxf_bar[lt % L::kAuxBufs], (lt / L::kAuxBufs) & 1);
       // 16-column units of chunks c = h, h + W, ...: the TMEM load of the next unit is issued
       // before this unit's math, and the staging buffer is claimed only after the math, so TMEM
       // latency and the previous TMA store overlap useful work (the epilogue is latency-bound
@@ -385,8 +419,11 @@ __global__ void __launch_bounds__(gemm_threads(EPI) + 128 * CS, 1)
         const int col0 = n0 + c * 32;
         if (c >= kChunks || col0 >= pr.N) break;  // warp-uniform
         uint32_t(&r)[16] = rr[i & 1];
-        if constexpr (EPI == EPI_DACT) {
+        if constexpr (EPI == EPI_DACT && L::kAuxBufs == 0) {
           if (half == 0) load_aux(c + W, hn);
+        }
+        if constexpr (EPI == EPI_DACT && L::kAuxBufs > 0) {
+          if (half == 0) lds_aux(c, hv);
         }
         ptx::tmem_ld_wait();
         if (i + 1 < kUnits) {
@@ -434,7 +471,7 @@ __global__ void __launch_bounds__(gemm_threads(EPI) + 128 * CS, 1)
                 packed[j / 2] = pack_bf16(d.x, d.y);
               }
             }
-            if (half == 1) {
+            if (half == 1 && L::kAuxBufs == 0) {
 #pragma unroll
               for (int qd = 0; qd < 4; ++qd) hv[qd] = hn[qd];
             }
@@ -465,7 +502,10 @@ __global__ void __launch_bounds__(gemm_threads(EPI) + 128 * CS, 1)
       }
       ptx::tc_fence_before();
       __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&tempty_bar[buf]);
+      if (lane == 0) {
+        ptx::mbar_arrive(&tempty_bar[buf]);
+        if constexpr (L::kAuxBufs > 0) ptx::mbar_arrive(&auxe_bar[lt % L::kAuxBufs]);
+      }
       gemm_stamp(etr, lt, 6);
       if (nchain > 1 && ci + 1 < nchain && lane == 0) {
         // publish store completion for the next layer's producer: the previous tile's stores

@@ -76,6 +76,10 @@ CUtensorMap tma_kmajor(const void* p, int cols, long long rows, long long ld, in
   return make_tma_2d_bf16(p, uint64_t(cols), uint64_t(rows), uint64_t(ld), kGemmBlockK, uint32_t(box_rows));
 }
 
+CUtensorMap tma_aux(const void* p, int cols, long long rows, long long ld) {
+  return make_tma_2d_bf16(p, uint64_t(cols), uint64_t(rows), uint64_t(ld), 64, kGemmBlockM);
+}
+
 CUtensorMap tma_mnmajor(const void* p, int cols, long long rows, long long ld) {
   return make_tma_2d_bf16(p, uint64_t(cols), uint64_t(rows), uint64_t(ld), 64, 64);
 }
@@ -210,6 +214,7 @@ extern "C" GMI_API int gmi_dev_gemm(int a_mn, int b_mn, int epi, int M, int N, i
     p.bias = bias;
     p.aux = static_cast<const __nv_bfloat16*>(aux);
     p.ld_aux = ld_aux;
+    if (aux && epi == gmi::EPI_DACT && weight_stationary) p.map_aux = gmi::tma_aux(aux, N, M, ld_aux);
     P.num_problems = 1;
     P.splits = splits;
     gmi::gemm_launch(P, bn, a_mn, b_mn, epi, static_cast<cudaStream_t>(stream), 0, weight_stationary);

@@ -22,6 +22,8 @@ CUtensorMap make_tma_out_f32(const void* base, uint64_t cols, uint64_t rows, uin
 // K-major operand map for A (box rows = 128) or B (box rows = bn); MN-major map (box 64 x 64).
 CUtensorMap tma_kmajor(const void* p, int cols, long long rows, long long ld, int box_rows);
 CUtensorMap tma_mnmajor(const void* p, int cols, long long rows, long long ld);
+// elu' operand of a weight-stationary input-gradient GEMM: bf16 [rows x cols], box 64 x 128, SW128.
+CUtensorMap tma_aux(const void* p, int cols, long long rows, long long ld);
 
 // Launches the persistent kernel with min(tiles, max_ctas) CTAs (max_ctas 0 = SM count).
 // ws = 1: weight-stationary mode (requires N <= bn, K <= 256, splits == 1).

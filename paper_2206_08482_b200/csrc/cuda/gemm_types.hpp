@@ -21,6 +21,7 @@ struct alignas(64) GemmProblem {
   CUtensorMap map_a;
   CUtensorMap map_b;
   CUtensorMap map_out;  // bf16 2-D {N, rows} box {32,32} SW64, or fp32 3-D {N, M, splits} box {32,32,1} SW128
+  CUtensorMap map_aux;  // weight-stationary EPI_DACT: the elu' operand (aux) {N, rows}, box {64, 128} SW128
   const float* bias;
   const __nv_bfloat16* aux;
   int64_t ld_aux;

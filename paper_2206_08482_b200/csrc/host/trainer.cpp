@@ -652,6 +652,7 @@ void Trainer::build_plans() {
             p.map_out = make_tma_out_bf16(g.D[n][l - 1] + hh * ncols, ncols, g.Bm, in_p);
             p.aux = g.H[n][l - 1] + hh * ncols;
             p.ld_aux = in_p;
+            p.map_aux = tma_aux(p.aux, ncols, g.Bm, in_p);
             p.M = g.Bm;
             p.N = ncols;
             p.K = out_p;
@@ -704,6 +705,7 @@ void Trainer::build_plans() {
         p.map_out = make_tma_out_bf16(g.D[n][L - 1], hp, g.Bm, hp);
         p.aux = g.H[n][L - 1];
         p.ld_aux = hp;
+        p.map_aux = tma_aux(p.aux, hp, g.Bm, hp);
         p.M = g.Bm;
         p.N = hp;
         p.K = ppo::kHeadG;
