@@ -138,11 +138,16 @@ __global__ void __launch_bounds__(256) colsum_kernel(const ColsumArgs a, int row
 }
 
 // ------------------------------------------------------------------ gradient assembly
-// dst[i] = sum_p src[p*stride + i]. Block = 128 consecutive elements (one float4 per lane) x
-// 8 warps; warp w sums the contiguous part range [w*np/8, (w+1)*np/8) in part order with 4
-// loads in flight, then the 8 warp sums are added in warp order (deterministic, and the same
-// fixed order for every launch). Segments whose length / stride / pointers are not 16-byte
-// multiples take the scalar lane path with the same order.
+// dst[i] = sum_p src[p*stride + i]. Block = 128 consecutive elements x 256 threads, summed in a
+// fixed order (deterministic, the same for every launch):
+//  * vector path (length / stride / pointers 16-byte multiples): one float4 per lane, warp w sums
+//    the contiguous part range [w*np/8, (w+1)*np/8) in part order with 4 loads in flight, then the
+//    8 warp sums are added in warp order;
+//  * lane path (short or unaligned segments: head-bias, log-std and loss-statistic partials, with
+//    up to one part per CTA of the head kernel): the block's threads are (group g, element e) with
+//    G = 256 / pow2(len) groups; group g sums parts g, g + G, g + 2G, ... (4 loads in flight), then
+//    the groups are added in group order. Every part load of the block is in flight at once, where
+//    a thread per element walking all parts serially took a dependent round trip per part.
 constexpr int kMaxSegments = 64;
 constexpr int kSegElems = 128;
 struct SegmentTable {
@@ -152,31 +157,36 @@ struct SegmentTable {
   int has_adam;
   SegAdam adam;
 };
-__global__ void __launch_bounds__(256) segments_kernel(const __grid_constant__ SegmentTable t) {
+// kAdam: the fused-Adam variant (its state registers are kept out of the plain kernel, whose
+// occupancy sets how many part loads are in flight per SM: 5 blocks x 256 threads at 48 registers,
+// no spills; the unsplit kernel ran 3 blocks per SM at 68 registers, 5.3 waves).
+template <bool kAdam>
+__global__ void __launch_bounds__(256, 5) segments_kernel(const __grid_constant__ SegmentTable t) {
   __shared__ float4 acc_s[8][32];
+  __shared__ float red_s[256];
+  __shared__ float sum_s[kSegElems];  // the block's summed elements (fused Adam)
   pdl_trigger();
   pdl_wait();
   int si = 0;
   while (si + 1 < t.nseg && (int)blockIdx.x >= t.first_block[si + 1]) ++si;
   const Segment& sg = t.s[si];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int i0 = (blockIdx.x - t.first_block[si]) * kSegElems + lane * 4;
-  const int p0 = warp * sg.nparts / 8, p1 = (warp + 1) * sg.nparts / 8;
+  const int base = (blockIdx.x - t.first_block[si]) * kSegElems;
   const bool vec = ((sg.len | (int)(sg.stride & 3)) & 3) == 0 &&
                    ((reinterpret_cast<uintptr_t>(sg.src) | reinterpret_cast<uintptr_t>(sg.dst)) & 15) == 0;
-  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
   if (vec) {
+    const int i0 = base + lane * 4;
+    const int p0 = warp * sg.nparts / 8, p1 = (warp + 1) * sg.nparts / 8;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
     if (i0 < sg.len) {
-      const float* base = sg.src + i0;
-      // up to 8 parts in flight per thread (a warp owns ~nparts/8 parts, so usually one round
-      // trip), summed in part order
-      for (int p = p0; p < p1; p += 8) {
-        float4 v[8];
+      const float* src = sg.src + i0;
+      for (int p = p0; p < p1; p += 4) {
+        float4 v[4];
 #pragma unroll
-        for (int u = 0; u < 8; ++u)
-          if (p + u < p1) v[u] = __ldcs(reinterpret_cast<const float4*>(base + (long long)(p + u) * sg.stride));
+        for (int u = 0; u < 4; ++u)
+          if (p + u < p1) v[u] = __ldcs(reinterpret_cast<const float4*>(src + (long long)(p + u) * sg.stride));
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
+        for (int u = 0; u < 4; ++u) {
           if (p + u < p1) {
             acc.x += v[u].x;
             acc.y += v[u].y;
@@ -186,45 +196,59 @@ __global__ void __launch_bounds__(256) segments_kernel(const __grid_constant__ S
         }
       }
     }
-  } else {
-    float a[4] = {0.f, 0.f, 0.f, 0.f};
+    acc_s[warp][lane] = acc;
+    __syncthreads();
+    if (warp == 0 && i0 < sg.len) {
+      float4 s = acc_s[0][lane];
 #pragma unroll
-    for (int c = 0; c < 4; ++c)
-      if (i0 + c < sg.len)
-        for (int p = p0; p < p1; ++p) a[c] += sg.src[(long long)p * sg.stride + i0 + c];
-    acc = make_float4(a[0], a[1], a[2], a[3]);
-  }
-  acc_s[warp][lane] = acc;
-  __syncthreads();
-  if (warp == 0 && i0 < sg.len) {
-    float4 s = acc_s[0][lane];
-#pragma unroll
-    for (int w = 1; w < 8; ++w) {
-      const float4 v = acc_s[w][lane];
-      s.x += v.x;
-      s.y += v.y;
-      s.z += v.z;
-      s.w += v.w;
-    }
-    if (vec) {
+      for (int w = 1; w < 8; ++w) {
+        const float4 v = acc_s[w][lane];
+        s.x += v.x;
+        s.y += v.y;
+        s.z += v.z;
+        s.w += v.w;
+      }
       *reinterpret_cast<float4*>(sg.dst + i0) = s;
-    } else {
-      const float o[4] = {s.x, s.y, s.z, s.w};
-      for (int c = 0; c < 4 && i0 + c < sg.len; ++c) sg.dst[i0 + c] = o[c];
+      *reinterpret_cast<float4*>(sum_s + lane * 4) = s;
     }
-    if (t.has_adam) acc_s[0][lane] = s;  // hand the block's 128 sums to 128 Adam threads
+  } else {
+    const int E = min(kSegElems, sg.len - base);
+    int ep = 1;
+    while (ep < E) ep <<= 1;
+    const int G = 256 / ep;
+    const int e = threadIdx.x & (ep - 1), g = threadIdx.x / ep;
+    float acc = 0.f;
+    if (e < E) {
+      const float* src = sg.src + base + e;
+      for (int p = g; p < sg.nparts; p += 4 * G) {
+        float v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (p + u * G < sg.nparts) v[u] = __ldcs(src + (long long)(p + u * G) * sg.stride);
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (p + u * G < sg.nparts) acc += v[u];
+      }
+    }
+    red_s[threadIdx.x] = acc;
+    __syncthreads();
+    if (int(threadIdx.x) < E) {
+      float s = red_s[threadIdx.x];
+      for (int gg = 1; gg < G; ++gg) s += red_s[gg * ep + threadIdx.x];
+      sg.dst[base + threadIdx.x] = s;
+      sum_s[threadIdx.x] = s;
+    }
   }
-  if (t.has_adam && sg.param_off >= 0) {  // fused Adam, same arithmetic as adam_kernel
+  if (kAdam && sg.param_off >= 0) {  // fused Adam, same arithmetic as adam_kernel
     __syncthreads();
     const int e = threadIdx.x;  // element of this block
-    const int ie = (blockIdx.x - t.first_block[si]) * kSegElems + e;
+    const int ie = base + e;
     if (e < kSegElems && ie < sg.len) {
       const SegAdam& a = t.adam;
       const long long st = a.ctl->adam_step0 + a.step_in_iter;
       const float bc1 = a.bc[2 * st], bc2 = a.bc[2 * st + 1];
       const float ob1 = __fsub_rn(1.0f, a.b1), ob2 = __fsub_rn(1.0f, a.b2);
-      const float4 s4 = acc_s[0][e >> 2];
-      const float gs = (e & 3) == 0 ? s4.x : (e & 3) == 1 ? s4.y : (e & 3) == 2 ? s4.z : s4.w;
+      const float gs = sum_s[e];
       const long long i = sg.param_off + ie;
       const float g = __fmul_rn(gs, a.inv_n);
       const float m = __fadd_rn(__fmul_rn(a.b1, a.m[i]), __fmul_rn(ob1, g));
@@ -283,7 +307,10 @@ void launch_segments(const Segment* segs, int n, cudaStream_t s, const SegAdam* 
       t.s[i] = segs[base + i];
       t.first_block[i + 1] = t.first_block[i] + (std::max(1, t.s[i].len) + kSegElems - 1) / kSegElems;
     }
-    launch_pdl(segments_kernel, dim3(t.first_block[m]), dim3(256), 0, s, t);
+    if (t.has_adam)
+      launch_pdl(segments_kernel<true>, dim3(t.first_block[m]), dim3(256), 0, s, t);
+    else
+      launch_pdl(segments_kernel<false>, dim3(t.first_block[m]), dim3(256), 0, s, t);
   }
 }
 
