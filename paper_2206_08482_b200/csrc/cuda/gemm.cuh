@@ -11,7 +11,8 @@
 // [rows x K]) or MN-major (row-major [K x rows]); MN-major lets the weight-gradient GEMM
 // (dW = dPre^T H, reduction over minibatch rows) read activations in place.
 //
-// Weight-stationary mode (WS = 1; N <= BN, K <= 256, no split-K): each CTA serves one
+// Weight-stationary mode (WS = 1: N <= BN, K <= 256; WS = 2: N <= BN <= 128, K <= 512; no
+// split-K): each CTA serves one
 // problem (CTA index mod problems), loads that problem's whole B operand (the layer's
 // weights, <= 128 KB) into shared memory once and then streams only the A tiles
 // (activations / dPre rows). This removes the per-tile weight re-reads that made the
@@ -97,7 +98,7 @@ struct GemmSmem {
   // on B200: the A ring starves the MMA)
   static constexpr uint32_t kA = kGemmBlockM * kGemmBlockK * 2;  // 16 KB
   static constexpr uint32_t kB = BN * kGemmBlockK * 2;           // one k-block of B
-  static constexpr uint32_t kBRes = WS ? kGemmMaxKbWS * kB : 0;  // resident B (WS)
+  static constexpr uint32_t kBRes = WS ? gemm_ws_kb(WS) * kB : 0;  // resident B (WS)
   // split-K fp32 slabs at BN = 256 (one tile per CTA): a 4th operand stage beats double
   // staging of the once-per-CTA epilogue (weight-gradient phase 0.99 -> 0.96 ms per iteration)
   static constexpr bool kDw4 = !WS && EPI == 2;  // every split-K launch: one tile per CTA
@@ -110,7 +111,8 @@ struct GemmSmem {
   // WS input gradient: the elu' operand (H rows of the tile) staged by TMA, double-buffered
   // [buf][BN / 64 boxes][128 rows][64 cols] SW128, instead of per-thread global loads in the epilogue
   // (BN <= 128: at BN = 256 the resident weights leave no room; the global-load path is kept)
-  static constexpr int kAuxBufs = (WS && EPI == 1 && BN <= 128) ? GMI_DX_AUX_BUFS : 0;
+  // (WS = 2: the 128 KB of resident weights leave no room either)
+  static constexpr int kAuxBufs = (WS == 1 && EPI == 1 && BN <= 128) ? GMI_DX_AUX_BUFS : 0;
   static constexpr uint32_t kAuxBox = kGemmBlockM * 128;  // 128 rows x 64 bf16 columns
   static constexpr uint32_t kAux = kAuxBufs * (BN / 64) * kAuxBox;
   static constexpr int kWsFit = int((232448u - 1536u - kBias - kAux - kBRes - kEpiWarps * kStagingBufs * kStaging) / kA);

@@ -127,6 +127,16 @@ void launch_bn(const GemmParams& P, int a_mn, int b_mn, int epi, int ctas, cudaS
     if (key != 1 * 100 + 1 * 10 + EPI_F32 || ws) invalid("column sums need the MN-major weight-gradient GEMM");
     return launch_t<BN, 1, 1, EPI_F32, 0, 1>(P, ctas, s);
   }
+  if (ws == 2) {  // K <= 512 resident: block N <= 128 only (shared-memory budget)
+    if constexpr (BN <= 128) {
+      switch (key) {
+        case 0 * 100 + 0 * 10 + EPI_BIAS_ELU: return launch_t<BN, 0, 0, EPI_BIAS_ELU, 2>(P, ctas, s);
+        case 0 * 100 + 1 * 10 + EPI_DACT: return launch_t<BN, 0, 1, EPI_DACT, 2>(P, ctas, s);
+        default: invalid("weight-stationary GEMM supports the forward and input-gradient epilogues only");
+      }
+    }
+    invalid("weight-stationary GEMM with K > 256 needs block N <= 128");
+  }
   if (ws) {
     switch (key) {
       case 0 * 100 + 0 * 10 + EPI_BIAS_ELU: return launch_t<BN, 0, 0, EPI_BIAS_ELU, 1>(P, ctas, s);
@@ -155,6 +165,14 @@ int gemm_ws_bn(int M, int N, int K, int problems, int sms) {
   return bn;
 }
 
+int gemm_ws_wide(int M, int N, int K, int nets, int sms, int* parts) {
+  const int np = (N + 127) / 128;
+  if (K > gemm_ws_kb(2) * kGemmBlockK || nets * np > kGemmMaxProblems) return 0;
+  if (((M + kGemmBlockM - 1) / kGemmBlockM) * nets * np < sms) return 0;
+  *parts = np;
+  return K <= kGemmMaxKbWS * kGemmBlockK ? 1 : 2;
+}
+
 int gemm_ws_grid(int M, int problems, int max_ctas) {
   const int tiles = ((M + kGemmBlockM - 1) / kGemmBlockM) * problems;
   const int ctas = std::max(1, std::min(tiles, max_ctas > 0 ? max_ctas : device_sm_count()));
@@ -164,18 +182,21 @@ int gemm_ws_grid(int M, int problems, int max_ctas) {
 void gemm_launch(const GemmParams& P, int bn, int a_mn, int b_mn, int epi, cudaStream_t s, int max_ctas, int ws) {
   static int sms = 0;
   if (!sms) sms = device_sm_count();
+  // weight-stationary problems (one per CTA) may differ in N (<= block N): a layer split into
+  // 128-column parts has a narrower last part
   for (int i = 1; i < P.num_problems; ++i)
-    if (P.prob[i].M != P.prob[0].M || P.prob[i].N != P.prob[0].N || P.prob[i].K != P.prob[0].K)
+    if (P.prob[i].M != P.prob[0].M || (ws ? P.prob[i].N > bn : P.prob[i].N != P.prob[0].N) ||
+        P.prob[i].K != P.prob[0].K)
       invalid("grouped GEMM problems must share M, N, K");
   const int tiles = gemm_tiles(P.prob[0].M, P.prob[0].N, bn, P.num_problems, P.splits);
   int ctas = std::max(1, std::min(tiles, max_ctas > 0 ? max_ctas : sms));
   if (ws) {
-    if (P.splits != 1 || P.prob[0].N > bn || P.prob[0].K > kGemmMaxKbWS * kGemmBlockK)
-      invalid("weight-stationary GEMM needs splits == 1, N <= block_n, K <= 256");
+    if (ws < 0 || ws > 2 || P.splits != 1 || P.prob[0].N > bn || P.prob[0].K > gemm_ws_kb(ws) * kGemmBlockK)
+      invalid("weight-stationary GEMM needs splits == 1, N <= block_n, K <= 256 (ws = 1) / 512 (ws = 2)");
     ctas = gemm_ws_grid(P.prob[0].M, P.num_problems, max_ctas > 0 ? max_ctas : sms);
   }
   if (P.chain > 1) {  // chained forward layers: one grid shape for all of them
-    if (!ws || epi != EPI_BIAS_ELU || P.chain * P.num_problems > kGemmMaxProblems)
+    if (ws != 1 || epi != EPI_BIAS_ELU || P.chain * P.num_problems > kGemmMaxProblems)
       invalid("chained GEMM: weight-stationary forward layers only, at most 8 problems in all");
     for (int i = 0; i < P.chain * P.num_problems; ++i)
       if (P.prob[i].M != P.prob[0].M || P.prob[i].N != bn || P.prob[i].K > kGemmMaxKbWS * kGemmBlockK)

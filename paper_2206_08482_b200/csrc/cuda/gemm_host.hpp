@@ -26,12 +26,17 @@ CUtensorMap tma_mnmajor(const void* p, int cols, long long rows, long long ld);
 CUtensorMap tma_aux(const void* p, int cols, long long rows, long long ld);
 
 // Launches the persistent kernel with min(tiles, max_ctas) CTAs (max_ctas 0 = SM count).
-// ws = 1: weight-stationary mode (requires N <= bn, K <= 256, splits == 1).
+// ws = 1 / 2: weight-stationary mode (requires N <= bn, K <= 256 / 512 (bn <= 128), splits == 1).
 void gemm_launch(const GemmParams& P, int bn, int a_mn, int b_mn, int epi, cudaStream_t s, int max_ctas = 0,
                  int ws = 0);
 // Weight-stationary choice for a launch: returns the block N (N padded to 64) when every
 // CTA gets at least one tile and the weights fit, else 0 (use the streaming kernel).
 int gemm_ws_bn(int M, int N, int K, int problems, int sms);
+// Wide weight-stationary plan for a layer too wide for gemm_ws_bn (N > 256 or K > 256): N split
+// into 128-column parts, one problem per (net, part), block N = 128. Returns the ws mode (1: K <=
+// 256, 2: K <= 512) and the part count, or 0 when the weights do not fit, the problems exceed a
+// launch, or some CTA would get no tile.
+int gemm_ws_wide(int M, int N, int K, int nets, int sms, int* parts);
 // Weight-gradient GEMM on SM pairs (gemm_pair.cu): M = N = 256, MN-major operands, fp32 slabs.
 bool gemm_pair_applicable(int M, int N, int a_mn, int b_mn, int epi);
 void gemm_pair_launch(const GemmParams& P, int max_ctas, cudaStream_t s);

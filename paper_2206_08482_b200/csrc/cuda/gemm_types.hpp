@@ -13,6 +13,10 @@ enum GemmEpi : int { EPI_BIAS_ELU = 0, EPI_DACT = 1, EPI_F32 = 2 };
 constexpr int kGemmBlockM = 128;
 constexpr int kGemmBlockK = 64;  // one 128-byte swizzle atom of bf16
 constexpr int kGemmMaxKbWS = 4;  // weight-stationary mode: K <= 256
+// Resident k-blocks of B per weight-stationary mode: ws = 1 keeps K <= 256 (every block N);
+// ws = 2 keeps K <= 512 for block N <= 128 (the wide HM / SH layers, split into 128-column
+// problems): 8 x 16 KB of resident weights at N = 128.
+constexpr int gemm_ws_kb(int ws) { return ws == 2 ? 8 : kGemmMaxKbWS; }
 // Epilogue warps: 16 for the bf16 (elementwise-heavy) epilogues, 8 for fp32 slabs.
 constexpr int gemm_epi_warps(int epi) { return epi == 2 ? 8 : 16; }
 constexpr int gemm_threads(int epi) { return 64 + 32 * gemm_epi_warps(epi); }  // TMA, MMA, epilogue

@@ -65,6 +65,14 @@ float bf16_float(uint16_t b) {
     if (_r != ncclSuccess) ::gmi::fail(GMI_ERR_NCCL, std::string(#expr) + ": " + ncclGetErrorString(_r)); \
   } while (0)
 
+// Wide weight-stationary families on by default (bit mask, see build_plans). Measured on B200
+// (profiles/r2/SUMMARY.md, r2h): input gradients with K <= 256 resident per 128-column part win
+// (HM 8192 envs 35.0 -> 37.3 M env-steps/s, dx 2.03 -> 1.58 ms; SH 14.1 -> 14.3 M); the K <= 512
+// variants (4 operand stages next to 128 KB of weights, N = 128 MMAs) lose to the streaming
+// kernel (SH forward 2.37 -> 2.83 ms, dx 2.27 -> 2.72 ms), and forward parts at K <= 256 are
+// neutral (HM -1 %, SH +1 %), so only bit 2 is on.
+constexpr int kWideDefault = 0x4;
+
 // Splits of the weight-gradient GEMM: enough k-slabs to give ~one tile per SM.
 void pick_splits(int M, int N, int bn, int problems, int rows, int sms, int* splits, int* kbps) {
   const int base = gemm_tiles(M, N, bn, problems, 1);
@@ -538,6 +546,11 @@ void Trainer::build_plans() {
   for (auto& gp : gmis_) {
     Gmi& g = *gp;
     g.segs.clear();
+    // wide weight-stationary layers (128-column parts), per GEMM family and resident K:
+    // bit 0 forward K <= 256, bit 1 forward K <= 512, bit 2 input gradient K <= 256, bit 3 input
+    // gradient K <= 512 (GMI_WS_WIDE overrides, for measurements)
+    int wide_mask = kWideDefault;
+    if (const char* e = std::getenv("GMI_WS_WIDE")) wide_mask = std::atoi(e);
     const long long rollrows = (long long)(T_ + 1) * g.N;
     for (int l = 0; l < L; ++l) {
       const int in_p = geo_.wp[l], out_p = geo_.wp[l + 1];
@@ -578,15 +591,36 @@ void Trainer::build_plans() {
       g.fwd_val[l].splits = 1;
       // training forward: both nets grouped over the minibatch rows of the epoch copy
       const int ws_fwd = gemm_ws_bn(g.Bm, out_p, in_p, 2, g.ctas);
-      g.ws_fwd[l] = ws_fwd > 0;
-      g.bn_fwd[l] = ws_fwd > 0 ? ws_fwd : gemm_choose_bn(g.Bm, out_p, 2, 1, g.ctas);
+      // layers too wide for that (HM 400 / SH 512 widths): weight-stationary over 128-column
+      // parts of the output, one problem per (net, part), the part's weights resident (K <= 512)
+      int fparts = 1;
+      int ws_fwide = ws_fwd > 0 ? 0 : gemm_ws_wide(g.Bm, out_p, in_p, 2, g.ctas, &fparts);
+      if (ws_fwide && !(wide_mask >> (ws_fwide - 1) & 1)) ws_fwide = 0, fparts = 1;
+      g.ws_fwd[l] = ws_fwd > 0 ? 1 : ws_fwide;
+      g.bn_fwd[l] = ws_fwd > 0 ? ws_fwd : ws_fwide ? 128 : gemm_choose_bn(g.Bm, out_p, 2, 1, g.ctas);
       g.fwd_train[l] = GemmParams{};
       for (int n = 0; n < 2; ++n) {
         const CUtensorMap a = l == 0 ? tma_kmajor(g.X_sh, S_p, g.B, S_p, kGemmBlockM)
                                      : tma_kmajor(g.H[n][l - 1], in_p, g.Mrows, in_p, kGemmBlockM);
-        g.fwd_train[l].prob[n] = fwd_problem(n, a, g.Bm, g.bn_fwd[l]);
+        if (!ws_fwide) {
+          g.fwd_train[l].prob[n] = fwd_problem(n, a, g.Bm, g.bn_fwd[l]);
+          continue;
+        }
+        for (int j = 0; j < fparts; ++j) {
+          const int c0 = 128 * j, nc = std::min(128, out_p - c0);
+          GemmProblem p{};
+          p.map_a = a;
+          p.map_b = tma_kmajor(shadow_ + geo_.net[n][l].w + (long long)c0 * in_p, in_p, nc, in_p, 128);
+          p.map_out = make_tma_out_bf16(g.H[n][l] + c0, nc, g.Mrows, out_p);
+          p.bias = params_ + geo_.net[n][l].b + c0;
+          p.M = g.Bm;
+          p.N = nc;
+          p.K = in_p;
+          p.kb_per_split = (in_p + kGemmBlockK - 1) / kGemmBlockK;
+          g.fwd_train[l].prob[n * fparts + j] = p;
+        }
       }
-      g.fwd_train[l].num_problems = 2;
+      g.fwd_train[l].num_problems = 2 * fparts;
       g.fwd_train[l].splits = 1;
       g.flop_roll[l] = real * g.N;
       g.flop_fwd[l] = 2.0 * real * g.Bm;
@@ -595,7 +629,9 @@ void Trainer::build_plans() {
       const int bnw = in_p <= 64 ? 64 : in_p <= 128 ? 128 : 256;  // instantiated block widths
       g.bn_dw[l] = bnw;
       int splits = 1, kbps = 1;
-      pick_splits(out_p, in_p, bnw, 2, g.Bm, g.ctas, &splits, &kbps);
+      // backward branch parallelism: the dW launches get the SMs the dx branch leaves
+      const int dw_sms = bwd_par_ ? std::max(1, g.ctas - std::max(1, g.ctas * bwd_dx_share_ / 100)) : g.ctas;
+      pick_splits(out_p, in_p, bnw, 2, g.Bm, dw_sms, &splits, &kbps);
       g.dw[l] = GemmParams{};
       for (int n = 0; n < 2; ++n) {
         g.slab[n][l] = dev((size_t)splits * out_p * in_p * 4);
@@ -638,19 +674,25 @@ void Trainer::build_plans() {
         const char* dx4_off = std::getenv("GMI_DX_WS4_OFF");
         g.dx_halves[l] = in_p == 256 && out_p <= 256 && !(dx4_off && dx4_off[0] == '1') &&
                          gemm_ws_bn(g.Bm, 128, out_p, 4, g.ctas) == 128;
-        const int ws_dx = g.dx_halves[l] ? 128 : std::getenv("GMI_DX_WS") ? gemm_ws_bn(g.Bm, in_p, out_p, 2, g.ctas) : 0;
-        g.ws_dx[l] = ws_dx > 0;
+        int ws_dx = g.dx_halves[l] ? 128 : std::getenv("GMI_DX_WS") ? gemm_ws_bn(g.Bm, in_p, out_p, 2, g.ctas) : 0;
+        // wide layers (in_p or out_p > 256): weight-stationary over 128-column parts of dPre_{l-1}
+        int halves = g.dx_halves[l] ? 2 : 1;
+        int ws_dxwide = ws_dx > 0 || (in_p <= 256 && out_p <= 256) ? 0 : gemm_ws_wide(g.Bm, in_p, out_p, 2, g.ctas, &halves);
+        if (ws_dxwide && !(wide_mask >> (ws_dxwide + 1) & 1)) ws_dxwide = 0, halves = 1;
+        if (ws_dxwide) ws_dx = 128;
+        g.ws_dx[l] = ws_dxwide ? ws_dxwide : ws_dx > 0 ? 1 : 0;
         g.bn_dx[l] = ws_dx > 0 ? ws_dx : gemm_choose_bn(g.Bm, in_p, 2, 1, g.ctas);
         if (const char* bn = std::getenv("GMI_DX_BN"); bn && ws_dx == 0) g.bn_dx[l] = std::atoi(bn);  // experiments
         g.dx[l] = GemmParams{};
-        const int halves = g.dx_halves[l] ? 2 : 1, ncols = in_p / halves;
+        const int ncols_full = ws_dxwide ? 128 : in_p / halves;
         for (int n = 0; n < 2; ++n)
           for (int hh = 0; hh < halves; ++hh) {
+            const int c0 = hh * ncols_full, ncols = std::min(ncols_full, in_p - c0);
             GemmProblem p{};
             p.map_a = tma_kmajor(g.D[n][l], out_p, g.Bm, out_p, kGemmBlockM);
-            p.map_b = tma_mnmajor(shadow_ + geo_.net[n][l].w + hh * ncols, ncols, out_p, in_p);
-            p.map_out = make_tma_out_bf16(g.D[n][l - 1] + hh * ncols, ncols, g.Bm, in_p);
-            p.aux = g.H[n][l - 1] + hh * ncols;
+            p.map_b = tma_mnmajor(shadow_ + geo_.net[n][l].w + c0, ncols, out_p, in_p);
+            p.map_out = make_tma_out_bf16(g.D[n][l - 1] + c0, ncols, g.Bm, in_p);
+            p.aux = g.H[n][l - 1] + c0;
             p.ld_aux = in_p;
             p.map_aux = tma_aux(p.aux, ncols, g.Bm, in_p);
             p.M = g.Bm;
@@ -789,7 +831,7 @@ void Trainer::build_plans() {
       const char* nochain = std::getenv("GMI_FWD_CHAIN");
       g.chain_fwd = !(nochain && nochain[0] == '0') && 2 * L <= kGemmMaxProblems;
       for (int l = 0; l < L; ++l)
-        g.chain_fwd = g.chain_fwd && g.ws_fwd[l] && g.bn_fwd[l] == g.bn_fwd[0] && geo_.wp[l + 1] == g.bn_fwd[0];
+        g.chain_fwd = g.chain_fwd && g.ws_fwd[l] == 1 && g.bn_fwd[l] == g.bn_fwd[0] && geo_.wp[l + 1] == g.bn_fwd[0];
       if (g.chain_fwd) {
         g.fwd_chain = GemmParams{};
         for (int l = 0; l < L; ++l)
@@ -1196,7 +1238,8 @@ void Trainer::gemm(Gmi& g, int phase, const GemmParams& P0, int bn, int amn, int
   // weight-stationary B = the layer's weights: only Adam writes them, on the update stream
   // (ordered by an event) -- unless Adam is fused into this GMI's gradient assembly
   GemmParams P = P0;
-  P.b_stable = ws && !adam_in_gmi_stream_ ? 1 : 0;
+  static const char* no_bs = std::getenv("GMI_NO_BSTABLE");  // experiment: no early weight loads
+  P.b_stable = ws && !adam_in_gmi_stream_ && !(no_bs && no_bs[0] == '1') ? 1 : 0;
   // GMI_GEMM_TRACE=<phase id>: globaltimer stamps of CTA 0 for every launch of that phase
   // (the last one of the iteration wins; read with get("gemm_trace")). Development aid.
   // GMI_GEMM_TRACE_NTH=<k>: only the k-th recorded launch of the phase (e.g. 0 = the first
@@ -1362,7 +1405,8 @@ void Trainer::train_minibatch(Gmi& g, int k, int adam_step) {
   }
   for (int l = 0; l < L && !g.fused_fwd && !g.chain_fwd; ++l) {
     GemmParams P = g.fwd_train[l];
-    if (l == 0) P.prob[0].a_row0 = P.prob[1].a_row0 = k * g.Bm;
+    if (l == 0)
+      for (int i = 0; i < P.num_problems; ++i) P.prob[i].a_row0 = k * g.Bm;
     gemm(g, GMI_PH_FWD_GEMM, P, g.bn_fwd[l], 0, 0, EPI_BIAS_ELU, g.flop_fwd[l], g.ws_fwd[l]);
   }
   const double hflop = 2.0 * (A + 1) * geo_.width[L] * g.Bm;

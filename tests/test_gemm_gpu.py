@@ -32,7 +32,9 @@ def _elu(x):
 
 @pytest.mark.parametrize("M,N,K,ldk,ws", [(128, 64, 64, 64, 0), (300, 256, 60, 64, 0), (1024, 128, 256, 256, 0),
                                           (4096, 256, 192, 192, 0), (384, 512, 128, 128, 0),
-                                          (40000, 256, 256, 256, 1), (20000, 224, 64, 64, 1), (300, 128, 192, 192, 1)])
+                                          (40000, 256, 256, 256, 1), (20000, 224, 64, 64, 1), (300, 128, 192, 192, 1),
+                                          # ws = 2: K <= 512 resident (one 128-column part of a wide layer)
+                                          (20000, 128, 448, 448, 2), (5000, 96, 512, 512, 2), (300, 64, 320, 320, 2)])
 def test_forward_bias_elu(cuda, M, N, K, ldk, ws):
     import torch
     g = torch.Generator(device="cpu").manual_seed(M * 7 + N)
@@ -63,7 +65,8 @@ def test_f32_split_k(cuda, splits):
     assert torch.allclose(got, ref, rtol=1e-4, atol=1e-4), (got - ref).abs().max().item()
 
 
-@pytest.mark.parametrize("M,Nl,Kl,ws", [(512, 256, 192, 0), (33000, 256, 256, 1), (20000, 64, 224, 1)])
+@pytest.mark.parametrize("M,Nl,Kl,ws", [(512, 256, 192, 0), (33000, 256, 256, 1), (20000, 64, 224, 1),
+                                        (20000, 416, 128, 2), (9000, 512, 96, 2)])
 def test_dgrad_mn_major_weights(cuda, M, Nl, Kl, ws):
     """dH = (dPre @ W) * elu'(H): B operand is the [N_l x K_l] weight read MN-major."""
     import torch

@@ -128,6 +128,13 @@ def test_config4_sh_gmis(cuda, gmis, backend):
     _run(211, 20, [512, 512, 512, 256], 64 * gmis, iters=1, gmis_per_gpu=gmis, gmi_backend=backend)
 
 
+def test_config4_sh_wide_weight_stationary(cuda):
+    """SH widths at 1024 envs on one GMI: enough minibatch rows for every CTA to get a tile, so
+    the 512-wide input gradient with K = 256 (dPre_3 -> dH_2) takes the wide weight-stationary
+    GEMM (128-column parts of dPre_2, the part's weights resident)."""
+    _run(211, 20, [512, 512, 512, 256], 1024, iters=1)
+
+
 @pytest.mark.parametrize("serving_sms", [16, 32])
 def test_decoupled_wide_nets_match_oracle(cuda, serving_sms):
     """Decoupled layout with HM-width nets (108:200:400:100:21): the serving GMI runs the
