@@ -63,6 +63,8 @@ __device__ __forceinline__ void hstamp(bool on, int it, int k) {
 }
 
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory"); }
+// the four loss warps (column group 0: warps 2..5)
+__device__ __forceinline__ void loss_bar() { asm volatile("bar.sync 2, 128;" ::: "memory"); }
 
 template <int MAXA>
 __global__ void __launch_bounds__(kThreads, 1) head_fused_kernel(const __grid_constant__ HeadFusedArgs a) {
@@ -77,7 +79,9 @@ __global__ void __launch_bounds__(kThreads, 1) head_fused_kernel(const __grid_co
   uint64_t* wbar = bars;
   uint64_t* hfull = bars + 1;  // [2]
   uint64_t* hfree = bars + 3;  // [2]
-  uint64_t* g_ready = bars + 5;
+  // G(t) published: one barrier per G buffer (t & 1), so a barrier's phase advances once per two
+  // tiles and a waiter can never miss a phase (the loss of tile t+2 needs MMA3(t) first)
+  uint64_t* g_ready2[2] = {bars + 5, bars + 12};
   uint64_t* acc2_full = bars + 6;
   uint64_t* acc2_free = bars + 7;
   uint64_t* fin = bars + 8;
@@ -99,7 +103,8 @@ __global__ void __launch_bounds__(kThreads, 1) head_fused_kernel(const __grid_co
     }
     ptx::mbar_init(&acc1_full[0], 1);
     ptx::mbar_init(&acc1_full[1], 1);
-    ptx::mbar_init(g_ready, 4);
+    ptx::mbar_init(g_ready2[0], 1);  // one arrival per tile, after all four loss warps (see below)
+    ptx::mbar_init(g_ready2[1], 1);
     ptx::mbar_init(acc2_full, 1);
     ptx::mbar_init(acc2_free, kElu);
     ptx::mbar_init(fin, 1);
@@ -175,7 +180,7 @@ __global__ void __launch_bounds__(kThreads, 1) head_fused_kernel(const __grid_co
             mma1(next1);
             ++next1;
           }
-          if (next1 > it && ptx::mbar_test(g_ready, it & 1) && (it == 0 || ptx::mbar_test(acc2_free, (it - 1) & 1)))
+          if (next1 > it && ptx::mbar_test(g_ready2[it & 1], (it >> 1) & 1) && (it == 0 || ptx::mbar_test(acc2_free, (it - 1) & 1)))
             break;
         }
         const uint32_t gt = g0 + (it & 1) * kChunk;
@@ -203,7 +208,7 @@ __global__ void __launch_bounds__(kThreads, 1) head_fused_kernel(const __grid_co
       for (int j = cta; j < mtiles; j += ctas, ++it) {
         const uint32_t h0 = ptx::smem_u32(sH + (it & 1) * 4 * kChunk);
         const uint32_t gt = g0 + (it & 1) * kChunk;
-        ptx::mbar_wait_sleep(g_ready, it & 1);  // G(t) written; H(t) landed before MMA1(t)
+        ptx::mbar_wait_sleep(g_ready2[it & 1], (it >> 1) & 1);  // G(t) written; H(t) landed before MMA1(t)
         ptx::tc_fence_after();
         for (int half = 0; half * 128 < hp; ++half)
           for (int k = 0; k < kRows / 16; ++k)
@@ -272,8 +277,13 @@ __global__ void __launch_bounds__(kThreads, 1) head_fused_kernel(const __grid_co
                             a.vf_coef, a.ent_coef, invB, sG + (it & 1) * kChunk + row * 128, row, lacc, st, sg, sl);
         ptx::fence_proxy_async_smem();
         ptx::tc_fence_before();
-        __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(g_ready);
+        // All four loss warps finish tile `it` before G(it) is published. With one arrival per
+        // warp on a count-4 barrier, a warp that ran ahead could arrive for tile it+1 (its
+        // accumulator is double-buffered and MMA1(it+1) may already be done) and complete tile
+        // it's phase while a slower warp's G rows were still unwritten (MMA2 / MMA3 then read
+        // them stale: nondeterministic gradients, ~1 run in 10 at the bench shape).
+        loss_bar();
+        if (warp == 2 && lane == 0) ptx::mbar_arrive(g_ready2[it & 1]);
         hstamp(warp == 2 && lane == 0, it, 6);
       }
 

@@ -109,6 +109,26 @@ def test_iterations_are_deterministic(cuda):
     assert np.array_equal(runs[0].view(np.uint32), runs[1].view(np.uint32))
 
 
+@pytest.mark.parametrize("chain", ["1", "0"])
+def test_repeated_runs_are_bit_identical_at_bench_shape(cuda, monkeypatch, chain):
+    """Eight fresh trainers at the bench shape (AT 3x256, 4096 envs), two iterations each, end
+    bit-identical. Regression for a lapping race in the fused head kernel (a loss warp running a
+    tile ahead completed the count-4 G-ready barrier while a slower warp's G rows were unwritten):
+    ~1 run in 6 differed (tools/determinism_stress.py, profiles/r2/SUMMARY.md)."""
+    from paper_2206_08482_b200.ppo import PpoConfig, Trainer
+    monkeypatch.setenv("GMI_FWD_CHAIN", chain)
+    ref = None
+    for _ in range(8):
+        t = Trainer(PpoConfig(obs_dim=60, act_dim=8, hidden=[256, 256, 256], num_envs=4096))
+        t.iteration()
+        t.iteration()
+        p = t.get("params").view(np.uint32).copy()
+        del t
+        if ref is None:
+            ref = p
+        assert np.array_equal(p, ref)
+
+
 def test_rollout_is_layout_invariant_on_device(cuda):
     from paper_2206_08482_b200.ppo import PpoConfig, Trainer
     one = Trainer(PpoConfig(obs_dim=12, act_dim=3, hidden=[64, 64], num_envs=64))
