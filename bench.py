@@ -728,9 +728,9 @@ def other_layouts(args, cfg, w, value, world, barrier):
         dec = copy.deepcopy(one)
         dec.decoupled, dec.gmi_backend, dec.serving_sms = 1, 1, 16
         vd, msd, ud, tuning = time_trainer(dec, args.steps, args.warmup, world, barrier,
-                                           tune=[[8, 0], [16, 0], [24, 0]])
+                                           tune=[[16, 0], [24, 0], [32, 0], [40, 0]])
         out["config2_hm_4gmi"]["decoupled"] = {
-            "layout": "serving GMI (simulator+agent, per-layer rollout + critic on its partition) + trainer GMI, "
+            "layout": "serving GMI (simulator+agent: fused wide rollout + critic + GAE on its partition) + trainer GMI, "
                       "device experience channel, one-iteration policy lag",
             "value": vd, "ms_per_step": msd, "gmi_units": ud, "vs_single_context": vd / v1, "tuning": tuning}
     except Exception as e:  # noqa: BLE001

@@ -184,8 +184,11 @@ void gemm_launch(const GemmParams& P, int bn, int a_mn, int b_mn, int epi, cudaS
   if (!sms) sms = device_sm_count();
   // weight-stationary problems (one per CTA) may differ in N (<= block N): a layer split into
   // 128-column parts has a narrower last part
+  // (also split-K groups whose problems each fit one block N: the tile schedule is then the
+  // same for all of them, e.g. every layer's weight gradient in one launch)
+  const bool one_ntile = P.prob[0].N <= bn;
   for (int i = 1; i < P.num_problems; ++i)
-    if (P.prob[i].M != P.prob[0].M || (ws ? P.prob[i].N > bn : P.prob[i].N != P.prob[0].N) ||
+    if (P.prob[i].M != P.prob[0].M || (ws || one_ntile ? P.prob[i].N > bn : P.prob[i].N != P.prob[0].N) ||
         P.prob[i].K != P.prob[0].K)
       invalid("grouped GEMM problems must share M, N, K");
   const int tiles = gemm_tiles(P.prob[0].M, P.prob[0].N, bn, P.num_problems, P.splits);

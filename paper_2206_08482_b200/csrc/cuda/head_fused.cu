@@ -10,13 +10,16 @@
 // launch, and mu / v / G never touch HBM. Column group 0 (4 warps) runs the per-row loss while
 // groups 1-3 run the elu' epilogue of the previous tile.
 //
-// CTA b serves net b % 2 (0 = policy, 1 = value) and its tiles b/2, b/2 + grid/2, ...
+// CTAs [0, npol) serve the policy net (0), the rest the value net (1); CTA c of a net takes that
+// net's tiles c, c + ctas, ...
 // Warp 0: TMA (head weights once, H tiles), warp 1: tcgen05.mma issuer, warps 2..17:
 // epilogue (warps with column group 0 also run the per-row loss). Per-CTA partial outputs
 // (weight-grad slab, bias-grad row, head-bias / log-std grads and loss statistics) are summed
 // in a fixed order by the gradient-assembly kernel, so results are deterministic.
 // Numerics follow head_loss_kernel / oracle/ppo_oracle.c.
 #include <cuda.h>
+#include <algorithm>
+#include <cstdlib>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -89,8 +92,9 @@ __global__ void __launch_bounds__(kThreads, 1) head_fused_kernel(const __grid_co
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 11);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int net = blockIdx.x & 1;
-  const int cta = blockIdx.x >> 1, ctas = gridDim.x >> 1;
+  const int net = int(blockIdx.x) < a.npol ? 0 : 1;
+  const int cta = net ? int(blockIdx.x) - a.npol : int(blockIdx.x);
+  const int ctas = net ? int(gridDim.x) - a.npol : a.npol;
   const HeadNet& hn = a.net[net];
   const int hp = a.hp, nk = (hp + 63) / 64, NH = hn.nh, nout = hn.n_out;
   const int mtiles = (a.Bm + kRows - 1) / kRows;
@@ -394,7 +398,22 @@ int head_fused_grid(int Bm, int sms) {
   return 2 * per_net;
 }
 
+int head_fused_npol(int grid, int A) {
+  if (const char* e = std::getenv("GMI_HEAD_NPOL")) {  // measurement override
+    const int n = std::atoi(e);
+    if (n > 0 && n < grid) return n;
+  }
+  // CTAs in proportion to the per-tile cost: a policy tile (A log-probs, ratio, clip, per-action
+  // gradients) costs r value tiles, r measured on B200 from the policy-CTA sweeps of
+  // profiles/r2/SUMMARY.md (AT, A = 8: best split 80 / 68, r ~ 1.2; HM, A = 21: 110-120 / 38-28,
+  // r ~ 3), interpolated linearly in A
+  const double r = std::max(1.0, 1.2 + (3.0 - 1.2) / 13.0 * (A - 8));
+  const int n = int(grid * r / (1.0 + r) + 0.5);
+  return std::max(1, std::min(grid - 1, n));
+}
+
 void launch_head_fused(const HeadFusedArgs& a, int grid, cudaStream_t s) {
+  if (a.npol < 1 || a.npol >= grid) invalid("head kernel: policy CTA count out of range");
   auto go = [&](auto kern) {
     static bool configured[4] = {};
     (void)configured;

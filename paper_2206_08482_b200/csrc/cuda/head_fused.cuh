@@ -29,11 +29,14 @@ struct alignas(64) HeadFusedArgs {
   float* part;         // [grid][head_partial_stride(A)]: db_mu, db_v, dlog_std, 4 loss statistics
   long long row0;      // first epoch-copy row of this minibatch
   int Bm, A, hp;
+  int npol;            // CTAs [0, npol) serve the policy net, [npol, grid) the value net
   float clip, vf_coef, ent_coef;
 };
 
 bool head_fusable(int hp, int A);
-int head_fused_grid(int Bm, int sms);  // even; CTA b serves net b % 2
+int head_fused_grid(int Bm, int sms);
+// Policy CTAs of a head grid, in proportion to the per-tile loss cost (GMI_HEAD_NPOL overrides).
+int head_fused_npol(int grid, int A);
 void launch_head_fused(const HeadFusedArgs& a, int grid, cudaStream_t s);
 void head_fused_set_trace(unsigned long long* buf);  // development trace (TRACE=1 builds)
 

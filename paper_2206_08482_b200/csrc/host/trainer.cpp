@@ -149,6 +149,7 @@ struct Trainer::Gmi {
   float* slab[2][GMI_MAX_HIDDEN] = {};
   float* colsum[2][GMI_MAX_HIDDEN] = {};
   float* head_slab[2] = {};
+  int head_slab_parts[2] = {};  // fused head: per-net CTA count (value net in [1])
   float* head_part = nullptr;
   float* grad = nullptr;
   GemmParams fwd_roll[GMI_MAX_HIDDEN], fwd_val[GMI_MAX_HIDDEN], fwd_train[GMI_MAX_HIDDEN];
@@ -169,6 +170,7 @@ struct Trainer::Gmi {
   bool dw_pair[GMI_MAX_HIDDEN] = {};     // weight gradient on SM pairs (cuda/gemm_pair.cu)
   bool dx_halves[GMI_MAX_HIDDEN] = {};   // input gradient as 4 weight-stationary problems (N-halves)
   bool dw_grouped = false;               // dW of layers L-1 and L-2 in one launch (dw[L-1], 4 problems)
+  bool dw_all = false;                   // dW of every layer in one launch (dw[L-1], 2L problems)
   bool fused_head = false;
   int head_grid = 0;
   ppo::HeadFusedArgs head_args{};
@@ -788,8 +790,12 @@ void Trainer::build_plans() {
     int head_parts = ppo::head_loss_blocks(g.Bm), hslab_parts = hsplits;
     if (g.fused_head) {
       g.head_grid = ppo::head_fused_grid(g.Bm, g.ctas);
-      const int per_net = g.head_grid / 2;
       ppo::HeadFusedArgs& h = g.head_args;
+      // the opt-in fused training forward maps nets as CTA b -> net b % 2: even split there
+      const char* tf = std::getenv("GMI_TRAIN_FWD");
+      h.npol = tf && tf[0] == '1' ? g.head_grid / 2 : ppo::head_fused_npol(g.head_grid, A);
+      const int net_ctas[2] = {h.npol, g.head_grid - h.npol};
+      const int per_net = std::max(net_ctas[0], net_ctas[1]);
       for (int n = 0; n < 2; ++n) {
         ppo::HeadNet& hn = h.net[n];
         hn.n_out = head_rows[n];
@@ -816,7 +822,8 @@ void Trainer::build_plans() {
       h.vf_coef = cfg_.vf_coef;
       h.ent_coef = cfg_.ent_coef;
       head_parts = g.head_grid;
-      hslab_parts = per_net;
+      hslab_parts = net_ctas[0];
+      g.head_slab_parts[1] = net_ctas[1];
       const char* htr = std::getenv("GMI_HEAD_TRACE");
       if (htr && htr[0] == '1' && !head_trace_) {
         head_trace_ = dev(64 * 8);
@@ -912,6 +919,40 @@ void Trainer::build_plans() {
         g.dw[b].splits = splits;
         g.flop_dw[a] += g.flop_dw[b];
       }
+      // Every layer in one launch (GMI_DW_ALL=0 keeps the pair above + a layer-0 launch): when
+      // all hidden widths are equal (same M) and every input fits one block N, the first layer's
+      // problems (N = S_p, narrower) join the group after the last input gradient; their B tiles
+      // are zero-filled past S_p by TMA. One launch ramp / tail and one split-K slab set less per
+      // minibatch (AT: splits 18 + 37 -> 12 for 2 x 3 problems).
+      const char* all_env = std::getenv("GMI_DW_ALL");
+      bool all = g.dw_grouped && L >= 2 && 2 * L <= kGemmMaxProblems && !(all_env && all_env[0] == '0');
+      for (int l = 0; l < L && all; ++l)
+        all = geo_.wp[l + 1] == geo_.wp[L] && geo_.wp[l] <= g.bn_dw[a] && !g.dw_pair[l] && g.fused_bias[l];
+      g.dw_all = all;
+      if (all) {
+        const int out_p = geo_.wp[L];
+        int splits = 1, kbps = 1;
+        pick_splits(out_p, g.bn_dw[a], g.bn_dw[a], 2 * L, g.Bm, g.ctas, &splits, &kbps);
+        GemmParams P{};
+        for (int l = L - 1, j = 0; l >= 0; --l)
+          for (int n = 0; n < 2; ++n, ++j) {
+            const int in_p = geo_.wp[l];
+            // the per-layer problem as planned above (grouped layers: from the pair launch)
+            GemmProblem p = g.dw_grouped && (l == a || l == b) ? g.dw[a].prob[(l == a ? 0 : 2) + n] : g.dw[l].prob[n];
+            p.map_out = make_tma_out_f32(g.slab[n][l], in_p, out_p, splits, in_p, (uint64_t)out_p * in_p);
+            p.kb_per_split = kbps;
+            P.prob[j] = p;
+          }
+        P.num_problems = 2 * L;
+        P.splits = splits;
+        double flop = 0;
+        for (int l = 0; l < L; ++l) {
+          if (!(g.dw_grouped && l == b)) flop += g.flop_dw[l];
+          g.dw[l].splits = splits;
+        }
+        g.dw[a] = P;
+        g.flop_dw[a] = flop;
+      }
     }
 
     // gradient assembly segments (fixed-order sums of slabs / partials into the flat grad)
@@ -925,7 +966,8 @@ void Trainer::build_plans() {
         g.segs.push_back({g.grad + t.b, g.colsum[n][l], t.out_p, t.out_p, parts});
       }
     g.segs.push_back({g.grad + geo_.net[0][L].w, g.head_slab[0], (long long)A * hp, A * hp, hslab_parts});
-    g.segs.push_back({g.grad + geo_.net[1][L].w, g.head_slab[1], hp, hp, hslab_parts});
+    g.segs.push_back({g.grad + geo_.net[1][L].w, g.head_slab[1], hp, hp,
+                      g.fused_head ? g.head_slab_parts[1] : hslab_parts});
     g.segs.push_back({g.grad + geo_.net[0][L].b, g.head_part, hs, A, head_parts});
     g.segs.push_back({g.grad + geo_.net[1][L].b, g.head_part + A, hs, 1, head_parts});
     g.segs.push_back({g.grad + geo_.log_std, g.head_part + A + 1, hs, A, head_parts});
@@ -1468,7 +1510,14 @@ void Trainer::train_minibatch(Gmi& g, int k, int adam_step) {
       }
     }
   }
-  for (int l = L - 1; l >= 0 && !(par && L > 1); --l) {
+  if (g.dw_all && !(par && L > 1)) {  // every input gradient, then every layer's dW in one launch
+    for (int l = L - 1; l >= 1; --l)
+      gemm(g, GMI_PH_DX_GEMM, g.dx[l], g.bn_dx[l], 0, 1, EPI_DACT, g.flop_dx[l], g.ws_dx[l]);
+    GemmParams P = g.dw[L - 1];
+    P.prob[2 * L - 2].b_row0 = P.prob[2 * L - 1].b_row0 = k * g.Bm;  // layer 0 reads X of this minibatch
+    gemm(g, GMI_PH_DW_GEMM, P, g.bn_dw[L - 1], 1, 1, EPI_F32, g.flop_dw[L - 1]);
+  }
+  for (int l = L - 1; l >= 0 && !(par && L > 1) && !g.dw_all; --l) {
     // grouped: dW(L-1) waits for dPre(L-2) and runs with dW(L-2) as one launch (plan above)
     const int lw = g.dw_grouped && l == L - 2 ? L - 1 : l;
     GemmParams P = g.dw[lw];
