@@ -661,28 +661,58 @@ def main():
         dist.destroy_process_group()
 
 
+GEMM_FAMILY = {"fwd_gemm": ("fwd", "gemm_tcgen05_kernel<256,0,0,0,1,0> (training forward, all hidden layers of both "
+                                   "nets chained in one launch)"),
+               "dx_gemm": ("dx", "gemm_tcgen05_kernel<128,0,1,1,1,0> (input gradients, elu' fused, weight-stationary "
+                                 "128-column parts)"),
+               "dw_gemm": ("dw", "gemm_tcgen05_kernel<256,1,1,2,0,1> (split-K weight gradients of every layer, bias "
+                                 "column sums fused)")}
+
+
 def roofline(prof, peak_tf, peak_gbs, peak_src, at_max, iter_ms):
-    """Dominant kernel: the training-forward GEMM (gemm_tcgen05_kernel, weight-stationary
-    bias+ELU epilogue; the largest single phase of the iteration). Tensor-bound per SURVEY §8d:
-    algorithmic flops (2·M·N·K per problem, real widths) of its launches ÷ their CUDA-event time
-    on the GMI stream, against the burst bf16 peak when the SM clock sat at its maximum."""
-    f = prof.get("fwd_gemm", {})
-    ms, flop = f.get("ms", 0.0), f.get("flop", 0.0)
-    tf = flop / (ms / 1e3) / 1e12 if ms else 0.0
-    fam = {k: prof[k] for k in ("fwd_gemm", "dx_gemm", "dw_gemm") if k in prof}
+    """Dominant kernel = the GEMM family (training forward / input gradient / weight gradient,
+    one template each) with the largest measured time in the instrumented iteration (CUDA events
+    around each launch on the GMI stream). Its bound follows from its arithmetic intensity
+    against the ridge point (peak bf16 TF/s / peak HBM GB/s): algorithmic bytes (every operand
+    read once, outputs written once: gemm_bytes() in host/trainer.cpp) / time for HBM-bound,
+    algorithmic flops (2 M N K at the real widths) / time for tensor-bound, against the burst
+    peaks when the SM clock sat at its maximum. The tensor view of the same kernel and the
+    training-forward GEMM's numbers are kept beside it."""
+    fam = {k: prof[k] for k in GEMM_FAMILY if k in prof and prof[k].get("ms", 0) > 0}
+    if not fam:
+        return None
+    dom = max(fam, key=lambda k: fam[k]["ms"])
+    d = fam[dom]
+    ms, flop, byt = d["ms"], d["flop"], d["bytes"]
+    n = max(1, d.get("launches", 0))
+    tf = flop / (ms / 1e3) / 1e12
+    gbs = byt / (ms / 1e3) / 1e9 if byt else 0.0
+    ridge = peak_tf * 1e12 / (peak_gbs * 1e9)
+    hbm = byt > 0 and flop / byt < ridge
     fms = sum(v["ms"] for v in fam.values())
     ffl = sum(v["flop"] for v in fam.values())
     fby = sum(v["bytes"] for v in fam.values())
-    n = max(1, f.get("launches", 0))
-    return {"bound": "tensor", "kernel": "gemm_tcgen05_kernel<256,0,0,0,1,0> (training forward, both nets)",
-            "achieved": tf, "peak": peak_tf, "unit": "TFLOP/s", "frac": tf / peak_tf if peak_tf else None,
-            "traffic": gemm_traffic("fwd"), "traffic_unit": "DRAM bytes per launch (ncu --set full, profiles/traffic.json)",
-            "algorithmic_flop_per_launch": flop / n, "algorithmic_bytes_per_launch": f.get("bytes", 0.0) / n,
-            "launches_per_step": f.get("launches", 0), "avg_launch_us": 1e3 * ms / n,
+    f = prof.get("fwd_gemm", {})
+    fwd = None
+    if f.get("ms"):
+        ftf = f["flop"] / (f["ms"] / 1e3) / 1e12
+        fwd = {"kernel": GEMM_FAMILY["fwd_gemm"][1], "achieved_tflops": ftf,
+               "frac_tensor": ftf / peak_tf if peak_tf else None,
+               "achieved_gbs": f["bytes"] / (f["ms"] / 1e3) / 1e9 if f.get("bytes") else 0.0,
+               "launches_per_step": f.get("launches", 0), "traffic": gemm_traffic("fwd")}
+    return {"bound": "hbm" if hbm else "tensor", "kernel": GEMM_FAMILY[dom][1],
+            "achieved": gbs if hbm else tf, "peak": peak_gbs if hbm else peak_tf,
+            "unit": "GB/s" if hbm else "TFLOP/s",
+            "frac": (gbs / peak_gbs if hbm else tf / peak_tf) if (peak_gbs if hbm else peak_tf) else None,
+            "traffic": gemm_traffic(GEMM_FAMILY[dom][0]),
+            "traffic_unit": "DRAM bytes per launch (ncu launch list, profiles/traffic.json)",
+            "algorithmic_flop_per_launch": flop / n, "algorithmic_bytes_per_launch": byt / n,
+            "intensity_flop_per_byte": flop / byt if byt else None, "ridge_flop_per_byte": ridge,
+            "launches_per_step": d.get("launches", 0), "avg_launch_us": 1e3 * ms / n,
             "share_of_step": ms / iter_ms if iter_ms else None,
             "peak_source": peak_src + (" burst (SM clock at max during the timed region)" if at_max else " sustained"),
-            "hbm_view": {"achieved": f.get("bytes", 0.0) / (ms / 1e3) / 1e9 if ms else 0.0, "peak": peak_gbs,
-                         "unit": "GB/s"},
+            "tensor_view": {"achieved": tf, "peak": peak_tf, "unit": "TFLOP/s", "frac": tf / peak_tf if peak_tf else None},
+            "training_forward": fwd,
             "gemm_family": {"kernels": "forward + input-gradient + weight-gradient GEMMs", "ms": fms,
                             "achieved_tflops": ffl / (fms / 1e3) / 1e12 if fms else 0.0,
                             "frac": (ffl / (fms / 1e3) / 1e12) / peak_tf if fms else None,
