@@ -301,14 +301,45 @@ __global__ void __launch_bounds__(256) shuffle_kernel(const __nv_bfloat16* X_rol
     src_s[threadIdx.x] = rng::perm_index(uint32_t(r0 + threadIdx.x), uint32_t(B), keys);
   }
   __syncthreads();
-  for (int k = threadIdx.x; k < rows * cpr; k += 256) {
-    const int r = k / cpr, c = k - r * cpr;
-    const long long j = r0 + r, src = src_s[r];
-    reinterpret_cast<uint4*>(X_sh + j * S_p)[c] = reinterpret_cast<const uint4*>(X_roll + src * S_p)[c];
+  // 8 gathered loads in flight per thread before their stores (the stores could alias the loads
+  // as far as the compiler knows, so a load -> store loop would run one round trip per chunk)
+  for (int k0 = threadIdx.x; k0 < rows * cpr; k0 += 8 * 256) {
+    uint4 v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int k = k0 + u * 256;
+      if (k < rows * cpr) {
+        const int r = k / cpr, c = k - r * cpr;
+        v[u] = reinterpret_cast<const uint4*>(X_roll + src_s[r] * S_p)[c];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int k = k0 + u * 256;
+      if (k < rows * cpr) {
+        const int r = k / cpr, c = k - r * cpr;
+        reinterpret_cast<uint4*>(X_sh + (r0 + r) * S_p)[c] = v[u];
+      }
+    }
   }
-  for (int k = threadIdx.x; k < rows * A; k += 256) {
-    const int r = k / A, i = k - r * A;
-    act_sh[(r0 + r) * A + i] = act[src_s[r] * A + i];
+  for (int k0 = threadIdx.x; k0 < rows * A; k0 += 8 * 256) {
+    float v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int k = k0 + u * 256;
+      if (k < rows * A) {
+        const int r = k / A, i = k - r * A;
+        v[u] = act[src_s[r] * A + i];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int k = k0 + u * 256;
+      if (k < rows * A) {
+        const int r = k / A, i = k - r * A;
+        act_sh[(r0 + r) * A + i] = v[u];
+      }
+    }
   }
   if (threadIdx.x < rows) {
     const long long j = r0 + threadIdx.x, src = src_s[threadIdx.x];
