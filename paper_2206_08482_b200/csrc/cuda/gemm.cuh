@@ -180,7 +180,7 @@ __global__ void __launch_bounds__(gemm_threads(EPI) + 128 * CS, 1)
   const int mtiles = (p0.M + kGemmBlockM - 1) / kGemmBlockM;
   const int ntiles = (p0.N + BN - 1) / BN;
   const int per_prob = P.splits * mtiles * ntiles;
-  const int ntile_total = per_prob * P.num_problems;
+  const int ntile_total = P.hetero ? P.tile0[P.num_problems] : per_prob * P.num_problems;
   const int nkb_total = (p0.K + kGemmBlockK - 1) / kGemmBlockK;
 
   if (threadIdx.x == 0) {
@@ -239,13 +239,26 @@ __global__ void __launch_bounds__(gemm_threads(EPI) + 128 * CS, 1)
       nkb = nkb_total;
       return;
     }
-    prob = fdiv(tile, per_prob, r_per_prob);
-    int r = tile - prob * per_prob;
-    split = fdiv(r, mn_tiles, r_mn);
-    r -= split * mn_tiles;
-    const int mt = fdiv(r, ntiles, r_n);
-    m0 = mt * kGemmBlockM;
-    n0 = (r - mt * ntiles) * BN;
+    if (P.hetero) {  // problem-own tile counts: find the problem, then split / m / n inside it
+      prob = 0;
+      while (prob + 1 < P.num_problems && tile >= P.tile0[prob + 1]) ++prob;
+      const GemmProblem& pp = P.prob[prob];
+      const int nt = (pp.N + BN - 1) / BN, mn = ((pp.M + kGemmBlockM - 1) / kGemmBlockM) * nt;
+      int r = tile - P.tile0[prob];
+      split = r / mn;
+      r -= split * mn;
+      const int mt = r / nt;
+      m0 = mt * kGemmBlockM;
+      n0 = (r - mt * nt) * BN;
+    } else {
+      prob = fdiv(tile, per_prob, r_per_prob);
+      int r = tile - prob * per_prob;
+      split = fdiv(r, mn_tiles, r_mn);
+      r -= split * mn_tiles;
+      const int mt = fdiv(r, ntiles, r_n);
+      m0 = mt * kGemmBlockM;
+      n0 = (r - mt * ntiles) * BN;
+    }
     kb0 = split * P.prob[prob].kb_per_split;
     const int kb1 = min(nkb_total, kb0 + P.prob[prob].kb_per_split);
     nkb = kb1 > kb0 ? kb1 - kb0 : 0;

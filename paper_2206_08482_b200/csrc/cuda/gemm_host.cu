@@ -187,11 +187,24 @@ void gemm_launch(const GemmParams& P, int bn, int a_mn, int b_mn, int epi, cudaS
   // (also split-K groups whose problems each fit one block N: the tile schedule is then the
   // same for all of them, e.g. every layer's weight gradient in one launch)
   const bool one_ntile = P.prob[0].N <= bn;
-  for (int i = 1; i < P.num_problems; ++i)
-    if (P.prob[i].M != P.prob[0].M || (ws || one_ntile ? P.prob[i].N > bn : P.prob[i].N != P.prob[0].N) ||
-        P.prob[i].K != P.prob[0].K)
-      invalid("grouped GEMM problems must share M, N, K");
-  const int tiles = gemm_tiles(P.prob[0].M, P.prob[0].N, bn, P.num_problems, P.splits);
+  int tiles = 0;
+  GemmParams Q;  // heterogeneous groups: P with the per-problem tile offsets filled in
+  if (P.hetero) {  // own M, N per problem (split-K weight gradients of layers of different widths)
+    if (ws || P.chain > 1) invalid("heterogeneous GEMM groups are split-K launches");
+    Q = P;
+    Q.tile0[0] = 0;
+    for (int i = 0; i < P.num_problems; ++i) {
+      if (P.prob[i].K != P.prob[0].K) invalid("grouped GEMM problems must share K");
+      Q.tile0[i + 1] = Q.tile0[i] + gemm_tiles(P.prob[i].M, P.prob[i].N, bn, 1, P.splits);
+    }
+    tiles = Q.tile0[P.num_problems];
+  } else {
+    for (int i = 1; i < P.num_problems; ++i)
+      if (P.prob[i].M != P.prob[0].M || (ws || one_ntile ? P.prob[i].N > bn : P.prob[i].N != P.prob[0].N) ||
+          P.prob[i].K != P.prob[0].K)
+        invalid("grouped GEMM problems must share M, N, K");
+    tiles = gemm_tiles(P.prob[0].M, P.prob[0].N, bn, P.num_problems, P.splits);
+  }
   int ctas = std::max(1, std::min(tiles, max_ctas > 0 ? max_ctas : sms));
   if (ws) {
     if (ws < 0 || ws > 2 || P.splits != 1 || P.prob[0].N > bn || P.prob[0].K > gemm_ws_kb(ws) * kGemmBlockK)
@@ -205,10 +218,11 @@ void gemm_launch(const GemmParams& P, int bn, int a_mn, int b_mn, int epi, cudaS
       if (P.prob[i].M != P.prob[0].M || P.prob[i].N != bn || P.prob[i].K > kGemmMaxKbWS * kGemmBlockK)
         invalid("chained GEMM layers must share M and have N == block_n, K <= 256");
   }
+  const GemmParams& PL = P.hetero ? Q : P;
   switch (bn) {
-    case 64: return launch_bn<64>(P, a_mn, b_mn, epi, ctas, s, ws);
-    case 128: return launch_bn<128>(P, a_mn, b_mn, epi, ctas, s, ws);
-    case 256: return launch_bn<256>(P, a_mn, b_mn, epi, ctas, s, ws);
+    case 64: return launch_bn<64>(PL, a_mn, b_mn, epi, ctas, s, ws);
+    case 128: return launch_bn<128>(PL, a_mn, b_mn, epi, ctas, s, ws);
+    case 256: return launch_bn<256>(PL, a_mn, b_mn, epi, ctas, s, ws);
     default: invalid("GEMM block_n must be 64, 128 or 256");
   }
 }

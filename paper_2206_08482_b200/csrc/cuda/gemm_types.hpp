@@ -59,6 +59,11 @@ struct alignas(64) GemmParams {
   // swaps in the next layer's resident weights as soon as its MMAs of the layer are done and
   // goes on, instead of a kernel boundary (launch, prologue, pipeline fill, wave tail) per layer.
   int chain;
+  // Heterogeneous split-K group (non-weight-stationary only): problems with their own M and N
+  // (sharing K and the split count); problem p owns tiles [tile0[p], tile0[p+1]) of the launch,
+  // laid out split-major inside it. Set by gemm_launch when `hetero` is 1.
+  int hetero;
+  int tile0[kGemmMaxProblems + 1];
   unsigned long long* trace;  // optional [8 tiles][16] globaltimer stamps of CTA 0 (development aid)
 };
 

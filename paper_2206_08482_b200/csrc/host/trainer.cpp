@@ -954,6 +954,43 @@ void Trainer::build_plans() {
         g.flop_dw[a] = flop;
       }
     }
+    // Layers of different widths (HM 200-400-100, SH 512-512-512-256): every layer's weight
+    // gradient still in one launch after the last input gradient, as a heterogeneous split-K
+    // group (each problem its own M x N tiles of block N 256, one split count for all), instead
+    // of one launch per layer (GMI_DW_HETERO=0 keeps those).
+    if (!g.dw_all && L >= 2 && 2 * L <= kGemmMaxProblems && !bwd_par_) {
+      const char* he = std::getenv("GMI_DW_HETERO");
+      bool het = !(he && he[0] == '0');
+      for (int l = 0; l < L && het; ++l) het = !g.dw_pair[l] && g.fused_bias[l];
+      if (het) {
+        constexpr int bn = 256;
+        int base = 0;
+        for (int l = 0; l < L; ++l) base += 2 * gemm_tiles(geo_.wp[l + 1], geo_.wp[l], bn, 1, 1);
+        const int nkb = (g.Bm + kGemmBlockK - 1) / kGemmBlockK;
+        const int s0 = std::max(1, std::min(nkb, g.ctas / std::max(1, base)));
+        const int kbps = (nkb + s0 - 1) / s0, splits = (nkb + kbps - 1) / kbps;
+        GemmParams P{};
+        double flop = 0;
+        for (int l = L - 1, j = 0; l >= 0; --l) {
+          const int in_p = geo_.wp[l], out_p = geo_.wp[l + 1];
+          for (int n = 0; n < 2; ++n, ++j) {
+            GemmProblem p = g.dw[l].prob[n];
+            p.map_out = make_tma_out_f32(g.slab[n][l], in_p, out_p, splits, in_p, (uint64_t)out_p * in_p);
+            p.kb_per_split = kbps;
+            P.prob[j] = p;
+          }
+          flop += g.flop_dw[l];
+          g.dw[l].splits = splits;
+        }
+        P.num_problems = 2 * L;
+        P.splits = splits;
+        P.hetero = 1;
+        g.dw[L - 1] = P;
+        g.flop_dw[L - 1] = flop;
+        g.bn_dw[L - 1] = bn;
+        g.dw_all = true;  // same schedule: every dx first, then this launch
+      }
+    }
 
     // gradient assembly segments (fixed-order sums of slabs / partials into the flat grad)
     const int cb = ppo::colsum_blocks(g.Bm);
