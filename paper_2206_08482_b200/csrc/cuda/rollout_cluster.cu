@@ -181,6 +181,7 @@ __global__ void __launch_bounds__(kThreads, 1) rollout_cluster_kernel(const __gr
       const int i = blk * 4 + j;
       xs[j] = owns && i < S ? a.x[(long long)env * S + i] : 0.f;
     }
+    const float rA = 1.0f / float(A);  // action index of a state dim: i % A via an fp32 reciprocal
     int st = 0, len = 1, cnt = 0;
     if (valid) {
       st = a.ep_step[env];
@@ -308,7 +309,7 @@ __global__ void __launch_bounds__(kThreads, 1) rollout_cluster_kernel(const __gr
         const int i = blk * 4 + j;
         if (owns && i < S) {
           const float nbv = i + 1 >= S ? x0 : j < 3 ? xs[j + 1] : nx;
-          const float drive = u_s[el * kMuLd + i % A];
+          const float drive = u_s[el * kMuLd + (i - A * fdiv(i, A, rA))];
           const float inner = __fadd_rn(__fsub_rn(drive, __fmul_rn(kDamp, xs[j])), __fmul_rn(kCouple, env_sin(nbv)));
           xn[j] = __fadd_rn(xs[j], __fmul_rn(kDt, inner));
           xsq_part = __fadd_rn(xsq_part, __fmul_rn(xn[j], xn[j]));
