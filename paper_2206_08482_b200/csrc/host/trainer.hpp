@@ -135,6 +135,11 @@ class Trainer {
   int iteration_ = 0;      // iterations enqueued so far
   bool rollout_pending_ = false;  // gmi_ppo_rollout produced the next iteration's rollout
   bool adam_in_gmi_stream_ = false;  // GMI_ADAM_FUSED: Adam runs in the GMI stream (no B preload)
+  // One GMI on one GPU (GMI_ADAM_INLINE=0 disables): Adam launched in the GMI stream right after the gradient
+  // assembly (no cross-stream event hops per minibatch); only the first weight-stationary launch
+  // after it (the next minibatch's forward) gives up its early weight load
+  bool adam_inline_ = false;
+  bool no_b_preload_once_ = false;
   long long adam_steps_ = 0;
   int launches_ = 0;       // kernels in one iteration
   bool capturing_ = false;
