@@ -150,6 +150,28 @@ __global__ void __launch_bounds__(256) colsum_kernel(const ColsumArgs a, int row
 //    a thread per element walking all parts serially took a dependent round trip per part.
 constexpr int kMaxSegments = 64;
 constexpr int kSegElems = 128;
+// quad path: 16-byte-aligned segments with at most kQuadParts parts (the split-K weight and
+// bias-gradient slabs): thread = 4 consecutive elements, all parts loaded before they are summed
+// in part order in registers (one round trip, no cross-warp reduction), 1024 elements per block
+constexpr int kQuadParts = 16;
+constexpr int kQuadElems = 1024;
+__host__ __device__ inline bool seg_quad(const Segment& sg) {
+  return sg.nparts <= kQuadParts && ((sg.len | (int)(sg.stride & 3)) & 3) == 0 &&
+         ((reinterpret_cast<uintptr_t>(sg.src) | reinterpret_cast<uintptr_t>(sg.dst)) & 15) == 0;
+}
+// Adam on one element, same arithmetic as adam_kernel (bit-identical)
+__device__ __forceinline__ void adam_elem(const SegAdam& a, long long i, float gs, float bc1, float bc2) {
+  const float ob1 = __fsub_rn(1.0f, a.b1), ob2 = __fsub_rn(1.0f, a.b2);
+  const float g = __fmul_rn(gs, a.inv_n);
+  const float m = __fadd_rn(__fmul_rn(a.b1, a.m[i]), __fmul_rn(ob1, g));
+  const float v = __fadd_rn(__fmul_rn(a.b2, a.v[i]), __fmul_rn(__fmul_rn(ob2, g), g));
+  a.m[i] = m;
+  a.v[i] = v;
+  const float mh = __fdiv_rn(m, bc1), vh = __fdiv_rn(v, bc2);
+  const float p = __fsub_rn(a.p[i], __fmul_rn(a.lr, __fdiv_rn(mh, __fadd_rn(__fsqrt_rn(vh), a.eps))));
+  a.p[i] = p;
+  a.shadow[i] = __float2bfloat16_rn(p);
+}
 struct SegmentTable {
   Segment s[kMaxSegments];
   int first_block[kMaxSegments + 1];  // prefix of blocks per segment
@@ -157,11 +179,10 @@ struct SegmentTable {
   int has_adam;
   SegAdam adam;
 };
-// kAdam: the fused-Adam variant (its state registers are kept out of the plain kernel, whose
-// occupancy sets how many part loads are in flight per SM: 5 blocks x 256 threads at 48 registers,
-// no spills; the unsplit kernel ran 3 blocks per SM at 68 registers, 5.3 waves).
+// kAdam: the fused-Adam variant. 4 blocks x 256 threads per SM at 64 registers (no spills with
+// the quad path's 8 float4 loads in flight; at 48 registers it spills).
 template <bool kAdam>
-__global__ void __launch_bounds__(256, 5) segments_kernel(const __grid_constant__ SegmentTable t) {
+__global__ void __launch_bounds__(256, 4) segments_kernel(const __grid_constant__ SegmentTable t) {
   __shared__ float4 acc_s[8][32];
   __shared__ float red_s[256];
   __shared__ float sum_s[kSegElems];  // the block's summed elements (fused Adam)
@@ -170,6 +191,40 @@ __global__ void __launch_bounds__(256, 5) segments_kernel(const __grid_constant_
   int si = 0;
   while (si + 1 < t.nseg && (int)blockIdx.x >= t.first_block[si + 1]) ++si;
   const Segment& sg = t.s[si];
+  if (seg_quad(sg)) {
+    const int i0 = (blockIdx.x - t.first_block[si]) * kQuadElems + threadIdx.x * 4;
+    if (i0 >= sg.len) return;
+    const float* src = sg.src + i0;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int p0 = 0; p0 < kQuadParts; p0 += 8) {  // 8 parts in flight per round trip
+      if (p0 >= sg.nparts) break;
+      float4 v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (p0 + u < sg.nparts) v[u] = __ldcs(reinterpret_cast<const float4*>(src + (long long)(p0 + u) * sg.stride));
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (p0 + u < sg.nparts) {
+          acc.x += v[u].x;
+          acc.y += v[u].y;
+          acc.z += v[u].z;
+          acc.w += v[u].w;
+        }
+    }
+    *reinterpret_cast<float4*>(sg.dst + i0) = acc;
+    if (kAdam && sg.param_off >= 0) {
+      const SegAdam& a = t.adam;
+      const long long st = a.ctl->adam_step0 + a.step_in_iter;
+      const float bc1 = a.bc[2 * st], bc2 = a.bc[2 * st + 1];
+      const long long i = sg.param_off + i0;
+      adam_elem(a, i, acc.x, bc1, bc2);
+      adam_elem(a, i + 1, acc.y, bc1, bc2);
+      adam_elem(a, i + 2, acc.z, bc1, bc2);
+      adam_elem(a, i + 3, acc.w, bc1, bc2);
+    }
+    return;
+  }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int base = (blockIdx.x - t.first_block[si]) * kSegElems;
   const bool vec = ((sg.len | (int)(sg.stride & 3)) & 3) == 0 &&
@@ -246,19 +301,7 @@ __global__ void __launch_bounds__(256, 5) segments_kernel(const __grid_constant_
     if (e < kSegElems && ie < sg.len) {
       const SegAdam& a = t.adam;
       const long long st = a.ctl->adam_step0 + a.step_in_iter;
-      const float bc1 = a.bc[2 * st], bc2 = a.bc[2 * st + 1];
-      const float ob1 = __fsub_rn(1.0f, a.b1), ob2 = __fsub_rn(1.0f, a.b2);
-      const float gs = sum_s[e];
-      const long long i = sg.param_off + ie;
-      const float g = __fmul_rn(gs, a.inv_n);
-      const float m = __fadd_rn(__fmul_rn(a.b1, a.m[i]), __fmul_rn(ob1, g));
-      const float v = __fadd_rn(__fmul_rn(a.b2, a.v[i]), __fmul_rn(__fmul_rn(ob2, g), g));
-      a.m[i] = m;
-      a.v[i] = v;
-      const float mh = __fdiv_rn(m, bc1), vh = __fdiv_rn(v, bc2);
-      const float p = __fsub_rn(a.p[i], __fmul_rn(a.lr, __fdiv_rn(mh, __fadd_rn(__fsqrt_rn(vh), a.eps))));
-      a.p[i] = p;
-      a.shadow[i] = __float2bfloat16_rn(p);
+      adam_elem(a, sg.param_off + ie, sum_s[e], a.bc[2 * st], a.bc[2 * st + 1]);
     }
   }
 }
@@ -305,7 +348,8 @@ void launch_segments(const Segment* segs, int n, cudaStream_t s, const SegAdam* 
     t.first_block[0] = 0;
     for (int i = 0; i < m; ++i) {
       t.s[i] = segs[base + i];
-      t.first_block[i + 1] = t.first_block[i] + (std::max(1, t.s[i].len) + kSegElems - 1) / kSegElems;
+      const int per = seg_quad(t.s[i]) ? kQuadElems : kSegElems;
+      t.first_block[i + 1] = t.first_block[i] + (std::max(1, t.s[i].len) + per - 1) / per;
     }
     if (t.has_adam)
       launch_pdl(segments_kernel<true>, dim3(t.first_block[m]), dim3(256), 0, s, t);

@@ -1730,7 +1730,8 @@ void Trainer::record_iteration(bool with_rollout) {
     adam_in_gmi_stream_ = n_local_ == 1 && !nccl_ && !xchg_ && af && af[0] == '1';
     const char* ai = std::getenv("GMI_ADAM_INLINE");
     // measured on B200: 48.3 -> 49.2 M env-steps/s at the bench shape (two cross-stream event hops
-    // per minibatch gone; the forward chain after Adam loads its weights after griddepcontrol.wait)
+    // per minibatch gone; the forward chain after Adam loads its weights after griddepcontrol.wait).
+    // Not in the decoupled layout: there it measured slower (52.7 vs 54-55 M env-steps/s).
     adam_inline_ = n_local_ == 1 && !nccl_ && !xchg_ && !adam_in_gmi_stream_ && !decoupled_ && !(ai && ai[0] == '0');
   }
   GMI_CUDA_CHECK(cudaEventRecord(ev_start_, upd_));
@@ -1796,10 +1797,10 @@ void Trainer::record_iteration(bool with_rollout) {
           GMI_CUDA_CHECK(cudaEventRecord(g->ev_done, g->s));
           continue;
         }
-        if (adam_inline_) {  // Adam of the previous step is the in-stream predecessor
+        if (adam_inline_) {  // Adam of the previous step is the in-stream predecessor; this
+          // step's Adam runs inside the gradient assembly (each element updated as it is summed)
           no_b_preload_once_ = step > 0;
-          train_minibatch(*g, k);
-          launch_adam_on(g->s, g->grad, step);
+          train_minibatch(*g, k, step);
           GMI_CUDA_CHECK(cudaEventRecord(g->ev_done, g->s));
           continue;
         }

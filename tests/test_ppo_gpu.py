@@ -367,18 +367,25 @@ def test_minibatch_permutation_indices_are_bit_exact(cuda, layout):
             assert np.array_equal(t.get("oldlp_sh", gmi).view(np.uint32), logp[perm].view(np.uint32)), (it, gmi)
 
 
-def test_adam_fused_into_gradient_assembly_is_bit_identical(cuda, monkeypatch):
-    """GMI_ADAM_FUSED=1 (one GMI, one GPU): Adam runs inside the gradient-assembly kernel on the
-    GMI stream instead of a separate launch on the update stream -- same arithmetic, so three
-    iterations (eager, then graph replays) leave bit-identical parameters."""
+@pytest.mark.parametrize("fused_env", [None, ("GMI_ADAM_FUSED", "1")])
+@pytest.mark.parametrize("dims", [(60, 8, [256, 256, 256]), (108, 21, [200, 400, 100])])
+def test_adam_fused_into_gradient_assembly_is_bit_identical(cuda, monkeypatch, fused_env, dims):
+    """One GMI on one GPU: Adam inside the gradient-assembly kernel on the GMI stream (the default
+    inline mode, or GMI_ADAM_FUSED=1) vs a separate Adam launch on the update stream
+    (GMI_ADAM_INLINE=0) -- same arithmetic per element (quad and block paths of the assembly), so
+    three iterations (eager, then graph replays) leave bit-identical parameters."""
     from paper_2206_08482_b200.ppo import PpoConfig, Trainer
-    cfg = dict(obs_dim=60, act_dim=8, hidden=[256, 256, 256], num_envs=256)
+    S, A, hidden = dims
+    cfg = dict(obs_dim=S, act_dim=A, hidden=hidden, num_envs=256)
     plain = Trainer(PpoConfig(**cfg))
     fused = Trainer(PpoConfig(**cfg))
-    for _ in range(3):  # the switch is read when an iteration is recorded (eager, then capture)
+    for _ in range(3):  # the switches are read when an iteration is recorded (eager, then capture)
         monkeypatch.delenv("GMI_ADAM_FUSED", raising=False)
+        monkeypatch.setenv("GMI_ADAM_INLINE", "0")
         plain.iteration()
-        monkeypatch.setenv("GMI_ADAM_FUSED", "1")
+        monkeypatch.delenv("GMI_ADAM_INLINE", raising=False)
+        if fused_env:
+            monkeypatch.setenv(*fused_env)
         fused.iteration()
     assert np.array_equal(plain.get("params").view(np.uint32), fused.get("params").view(np.uint32))
 
