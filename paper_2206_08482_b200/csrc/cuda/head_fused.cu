@@ -256,11 +256,11 @@ __global__ void __launch_bounds__(kThreads, 1) head_fused_kernel(const __grid_co
         // log-prob, advantage and return are fetched before the accumulator wait so their
         // latency overlaps the head MMA.
         const long long rr = a.row0 + grow;
-        float act_r[MAXA <= 16 ? MAXA : 1];
+        float act_r[kActRegs<MAXA>];
         float oldlp = 0.f, adv = 0.f, ret = 0.f;
         if (valid) {
           if (net == 0) {
-            if constexpr (MAXA <= 16) {
+            if constexpr (kLossPre<MAXA>) {
 #pragma unroll
               for (int i = 0; i < MAXA; ++i)
                 if (i < nout) act_r[i] = a.act[rr * nout + i];
@@ -424,6 +424,8 @@ void launch_head_fused(const HeadFusedArgs& a, int grid, cudaStream_t s) {
     go(head_fused_kernel<8>);
   else if (a.A <= 16)
     go(head_fused_kernel<16>);
+  else if (a.A <= 24)
+    go(head_fused_kernel<24>);
   else
     go(head_fused_kernel<31>);
 }

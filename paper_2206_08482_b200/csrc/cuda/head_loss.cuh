@@ -26,6 +26,12 @@ namespace gmi::ppo {
 // columns [n_out, nh) are written as zeros.
 template <int MAXA>
 constexpr bool kLossRegAcc = MAXA <= 8;
+// actions prefetched into registers before the accumulator wait (one round trip for the row's
+// actions instead of a dependent load per action between the G stores): A <= 24
+template <int MAXA>
+constexpr bool kLossPre = MAXA <= 24;
+template <int MAXA>
+constexpr int kActRegs = kLossPre<MAXA> ? MAXA : 1;
 
 __device__ __forceinline__ uint32_t pack2(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
@@ -34,12 +40,13 @@ __device__ __forceinline__ uint32_t pack2(float lo, float hi) {
 
 template <int MAXA>
 __device__ __forceinline__ void head_row_loss(int net, const uint32_t (&r)[32], const float* cst, int nout, int nh,
-                                              bool valid, const float* act_row, float (&act_r)[MAXA <= 16 ? MAXA : 1],
+                                              bool valid, const float* act_row, float (&act_r)[kActRegs<MAXA>],
                                               float oldlp, float adv, float ret, float clip, float vf_coef,
                                               float ent_coef, float invB, uint8_t* grow_s, int row, float* lacc,
                                               float (&st)[4], float (&sg)[kLossRegAcc<MAXA> ? MAXA : 1],
                                               float (&sl)[kLossRegAcc<MAXA> ? MAXA : 1]) {
-  constexpr bool kPre = MAXA <= 16;  // actions prefetched into registers before the accumulator wait
+  constexpr bool kPre = kLossPre<MAXA>;  // actions prefetched into registers before the accumulator wait
+  constexpr int kGk = kPre ? (MAXA + 7) / 8 * 8 : 1;  // packed G row: 16-byte units of 8 bf16
   const int lane = threadIdx.x & 31;
   auto put_g = [&](int col, float v) {
     *reinterpret_cast<__nv_bfloat16*>(grow_s + ((((col >> 3) ^ (row & 7))) << 4) + (col & 7) * 2) =
@@ -78,9 +85,9 @@ __device__ __forceinline__ void head_row_loss(int net, const uint32_t (&r)[32], 
       st[3] += (ratio < 1.f - clip || ratio > 1.f + clip) ? 1.f : 0.f;
     }
     if constexpr (!kPre) zero_row(0);
-    float gk[kPre ? 16 : 1];  // small action spaces: the G row is packed and stored as 16-byte units
+    float gk[kGk];  // small action spaces: the G row is packed and stored as 16-byte units
 #pragma unroll
-    for (int i = 0; i < (kPre ? 16 : 1); ++i) gk[i] = 0.f;
+    for (int i = 0; i < kGk; ++i) gk[i] = 0.f;
 #pragma unroll
     for (int i = 0; i < MAXA; ++i)
       if (i < nout) {
@@ -95,7 +102,7 @@ __device__ __forceinline__ void head_row_loss(int net, const uint32_t (&r)[32], 
         if constexpr (kLossRegAcc<MAXA>) {
           sg[i] += g;
           sl[i] += gl;
-        } else {
+        } else if constexpr (!kPre) {
           g = warp_sum(g);
           gl = warp_sum(gl);
           if (lane == 0) {
@@ -105,12 +112,36 @@ __device__ __forceinline__ void head_row_loss(int net, const uint32_t (&r)[32], 
         }
       }
     if constexpr (kPre) {
+      constexpr int kUnits = kGk / 8 < 2 ? 2 : kGk / 8;  // >= the 16 columns of the smallest head
+      auto gv = [&](int k) { return k < kGk ? gk[k] : 0.f; };
 #pragma unroll
-      for (int u = 0; u < 2; ++u)
+      for (int u = 0; u < kUnits; ++u)
         *reinterpret_cast<uint4*>(grow_s + ((u ^ (row & 7)) << 4)) =
-            make_uint4(pack2(gk[8 * u], gk[8 * u + 1]), pack2(gk[8 * u + 2], gk[8 * u + 3]),
-                       pack2(gk[8 * u + 4], gk[8 * u + 5]), pack2(gk[8 * u + 6], gk[8 * u + 7]));
-      zero_row(2);
+            make_uint4(pack2(gv(8 * u), gv(8 * u + 1)), pack2(gv(8 * u + 2), gv(8 * u + 3)),
+                       pack2(gv(8 * u + 4), gv(8 * u + 5)), pack2(gv(8 * u + 6), gv(8 * u + 7)));
+      zero_row(kUnits);
+      if constexpr (!kLossRegAcc<MAXA>) {
+        // per-action sums over the warp's rows (head-bias and log-std gradients), 8 actions at a
+        // time: 8 independent reductions per shuffle step (butterfly over lanes 16 / 8, then
+        // recursive halving) leave action c * 8 + l's sum on lane l, which adds it to the record
+        // -- instead of a dependent 5-shuffle chain and a serial shared-memory update per action
+#pragma unroll
+        for (int c = 0; c < (MAXA + 7) / 8; ++c) {
+          float v[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) v[u] = c * 8 + u < nout ? gk[(c * 8 + u) % kGk] : 0.f;
+          float sum = warp_reduce_transpose<8>(v);
+          if (lane < 8 && c * 8 + lane < nout) lacc[c * 8 + lane] += sum;
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int i = c * 8 + u;
+            const float z = act_r[i % kActRegs<MAXA>];
+            v[u] = i < nout ? (valid ? glp * (z * z - 1.f) - ent_coef * invB : 0.f) : 0.f;
+          }
+          sum = warp_reduce_transpose<8>(v);
+          if (lane < 8 && c * 8 + lane < nout) lacc[32 + c * 8 + lane] += sum;
+        }
+      }
     }
   } else {
     zero_row(0);

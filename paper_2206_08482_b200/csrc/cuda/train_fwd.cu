@@ -318,11 +318,11 @@ __global__ void __launch_bounds__(kThreads, 1) train_fwd_kernel(const __grid_con
       if (h == 0) {
         const long long rr = a.row0 + j * kRows + row;
         const bool valid = j * kRows + row < a.Bm;
-        float act_r[MAXA <= 16 ? MAXA : 1];
+        float act_r[kActRegs<MAXA>];
         float oldlp = 0.f, adv = 0.f, ret = 0.f;
         if (valid) {
           if (net == 0) {
-            if constexpr (MAXA <= 16) {
+            if constexpr (kLossPre<MAXA>) {
 #pragma unroll
               for (int i = 0; i < MAXA; ++i)
                 if (i < nout) act_r[i] = a.act[rr * nout + i];

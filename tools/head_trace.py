@@ -16,7 +16,10 @@ NAMES = {0: "mma: wait H", 1: "H landed", 2: "mma1 committed", 3: "G ready (mma)
 
 
 def main():
-    cfg = PpoConfig.from_config_file(os.path.join(os.path.dirname(__file__), "..", "configs", "at_4096env_3x256.cfg"))
+    path = sys.argv[1] if len(sys.argv) > 1 else os.path.join(os.path.dirname(__file__), "..", "configs",
+                                                               "at_4096env_3x256.cfg")
+    cfg = PpoConfig.from_config_file(path)
+    cfg.gmis_per_gpu, cfg.gmi_backend, cfg.sm_per_gmi = 1, 0, 0  # one GMI on the whole GPU
     t = Trainer(cfg)
     for _ in range(3):
         t.iteration()
