@@ -1730,9 +1730,9 @@ void Trainer::record_iteration(bool with_rollout) {
     adam_in_gmi_stream_ = n_local_ == 1 && !nccl_ && !xchg_ && af && af[0] == '1';
     const char* ai = std::getenv("GMI_ADAM_INLINE");
     // measured on B200: 48.3 -> 49.2 M env-steps/s at the bench shape (two cross-stream event hops
-    // per minibatch gone; the forward chain after Adam loads its weights after griddepcontrol.wait).
-    // Not in the decoupled layout: there it measured slower (52.7 vs 54-55 M env-steps/s).
-    adam_inline_ = n_local_ == 1 && !nccl_ && !xchg_ && !adam_in_gmi_stream_ && !decoupled_ && !(ai && ai[0] == '0');
+    // per minibatch gone; the forward chain after Adam loads its weights after griddepcontrol.wait);
+    // decoupled trainer: 52.7 -> 53.7 M (three paired runs on one box, r3k).
+    adam_inline_ = n_local_ == 1 && !nccl_ && !xchg_ && !adam_in_gmi_stream_ && !(ai && ai[0] == '0');
   }
   GMI_CUDA_CHECK(cudaEventRecord(ev_start_, upd_));
   if (!with_rollout) {  // trains on the rollout a gmi_ppo_rollout hook produced
