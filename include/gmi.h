@@ -92,6 +92,18 @@ GMI_API int gmi_reduce_device(int strategy, int num_gpus, const int* counts, con
                               void* const* bufs, void* out, size_t len, int dtype, int broadcast,
                               void* stream);
 
+/* The SURVEY §8b allreduce over one layout's GMIs (replaces execute(), reduction.hpp:225-334,
+ * for device-resident gradients): the GMIs' buffers are summed in the reference's fold order for
+ * `strategy` (the order of gmi_reduce_device) and the total is written back into EVERY buffer (in
+ * place, like a collective). streams: one cudaStream_t per GMI in flattened layout order, or NULL
+ * (all on the default stream); the reduction runs on streams[0] once every GMI stream has reached
+ * the call, and every GMI stream continues only after it. run (may be NULL): the reference's
+ * modelled latency and broadcast latency for len 8-byte elements over b1 / b2 bytes/s (execute()'s
+ * accounting, reduction.hpp:304-329; trace_len = its trace length). */
+GMI_API int gmi_allreduce(int strategy, int num_gpus, const int* counts, const int* ids, void* const* dev_bufs,
+                          size_t len, int dtype, void* const* streams, double b1, double b2,
+                          gmi_reduction_info_t* run);
+
 /* execute() with HOST buffers (the reference's calling convention, reduction.hpp:225):
  * bufs[i] (len elements of dtype) belongs to the i-th id of the flattened layout; the call
  * stages them into device memory, runs gmi_reduce_device and copies the result back to
@@ -101,7 +113,7 @@ GMI_API int gmi_execute_host(int strategy, int num_gpus, const int* counts, cons
 
 /* B200 extension: SMs of the green context that realises an MPS `share` on an sm100 GPU
  * (whole 8-SM groups of 148 SMs, or of sm_units when > 8). validate_layout flags sm100 shares
- * below one group and MIG partitions on sm100 (the B200 MIG profile table is not modelled). */
+ * below one group and checks sm100 MIG partitions against the B200 profile table. */
 GMI_API int gmi_green_sms(double share, int sm_units, int* out);
 
 /* ------------------------------------------------------------------ topology

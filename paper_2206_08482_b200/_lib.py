@@ -144,6 +144,7 @@ PROTOTYPES: dict[str, tuple] = {
     "gmi_reduction_schedule": (ci, [ci, ci, c_int_p, c_int_p, csz, cd, cd, cd, P(TraceEvent), csz,
                                     P(ReductionInfo)]),
     "gmi_reduce_device": (ci, [ci, ci, c_int_p, c_int_p, P(vp), vp, csz, ci, ci, vp]),
+    "gmi_allreduce": (ci, [ci, ci, c_int_p, c_int_p, P(vp), csz, ci, P(vp), cd, cd, P(ReductionInfo)]),
     "gmi_validate_layout": (ci, [P(TopologyT), P(ViolationT), ci, c_int_p]),
     "gmi_green_sms": (ci, [C.c_double, ci, c_int_p]),
     "gmi_select_backend": (ci, [ci, ci, c_int_p]),

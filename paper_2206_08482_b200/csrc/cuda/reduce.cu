@@ -191,3 +191,60 @@ extern "C" GMI_API int gmi_reduce_device(int strategy, int num_gpus, const int* 
                        static_cast<cudaStream_t>(stream));
   });
 }
+
+extern "C" GMI_API int gmi_allreduce(int strategy, int num_gpus, const int* counts, const int* ids,
+                                     void* const* dev_bufs, size_t len, int dtype, void* const* streams, double b1,
+                                     double b2, gmi_reduction_info_t* run) {
+  return gmi::guarded([&] {
+    if (strategy < 0 || strategy > 2) gmi::invalid("unknown strategy");
+    if (dtype != GMI_F32 && dtype != GMI_F64) gmi::invalid("dtype must be GMI_F32 or GMI_F64");
+    if (!dev_bufs) gmi::invalid("null buffer list");
+    gmi::plan::Placement p;
+    if (num_gpus < 0) gmi::invalid("num_gpus must be >= 0");
+    p.per_gpu.resize(num_gpus);
+    int k = 0;
+    for (int g = 0; g < num_gpus; ++g) {
+      p.per_gpu[g].assign(ids + k, ids + k + counts[g]);
+      k += counts[g];
+    }
+    p.check();
+    const size_t n = p.flat().size();
+    if (run) {  // the reference's accounting of the same call (fp64 bytes, as execute() counts them)
+      const int rc = gmi_reduction_schedule(strategy, num_gpus, counts, ids, len, 8.0, b1, b2, nullptr, 0, run);
+      if (rc != 0) gmi::fail(rc, gmi_last_error());
+    }
+    cudaStream_t s0 = streams ? static_cast<cudaStream_t>(streams[0]) : nullptr;
+    // every GMI stream reaches the call before the fold reads its buffer ...
+    std::vector<cudaEvent_t> evs;
+    auto event = [&] {
+      cudaEvent_t e = nullptr;
+      GMI_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      evs.push_back(e);
+      return e;
+    };
+    try {
+      for (size_t i = 1; streams && i < n; ++i) {
+        cudaStream_t si = static_cast<cudaStream_t>(streams[i]);
+        if (si == s0) continue;
+        cudaEvent_t e = event();
+        GMI_CUDA_CHECK(cudaEventRecord(e, si));
+        GMI_CUDA_CHECK(cudaStreamWaitEvent(s0, e, 0));
+      }
+      // ... the fold writes the total into every buffer (the first one is also the output: the
+      // kernel is elementwise, each element read from every buffer before it is written) ...
+      gmi::reduce_device(gmi::plan::Algo(strategy), p, dev_bufs, dev_bufs[0], len, dtype, true, s0);
+      // ... and every GMI stream continues after it
+      if (streams && n > 1) {
+        cudaEvent_t done = event();
+        GMI_CUDA_CHECK(cudaEventRecord(done, s0));
+        for (size_t i = 1; i < n; ++i)
+          if (static_cast<cudaStream_t>(streams[i]) != s0)
+            GMI_CUDA_CHECK(cudaStreamWaitEvent(static_cast<cudaStream_t>(streams[i]), done, 0));
+      }
+    } catch (...) {
+      for (cudaEvent_t e : evs) cudaEventDestroy(e);
+      throw;
+    }
+    for (cudaEvent_t e : evs) cudaEventDestroy(e);  // released once the recorded work completes
+  });
+}

@@ -96,3 +96,42 @@ def test_fp32_bit_identical_at_shadowhand_size(cuda, mpl, algo):
     out, _ = _device_reduce(algo, mpl, bufs)
     ref = oracle_execute(algo, mpl, bufs)
     assert np.array_equal(out.view(np.uint32), ref.view(np.uint32))
+
+
+@pytest.mark.parametrize("mpl,algo", [([[0, 1, 2], [3, 4, 5]], 2), ([[0, 1], [2, 3], [4, 5]], 1),
+                                      ([[0, 1, 2, 3]], 0)])
+def test_allreduce_in_place_on_gmi_streams(cuda, mpl, algo):
+    """gmi_allreduce: every GMI buffer ends with the total, bit-identical to the
+    reference's execute() fold (fp64), with one CUDA stream per GMI ordered around the call
+    (each GMI stream writes its buffer just before the call; the next kernel on every stream
+    sees the total), and the run info equals the reference's modelled latencies."""
+    import torch
+    from paper_2206_08482_b200 import _lib
+
+    ids = [i for l in mpl for i in l]
+    n = 50_000
+    host = [buffer_values("hash", 29, i, n) for i in ids]
+    ref = oracle_execute(algo, mpl, host)
+    streams = [torch.cuda.Stream() for _ in ids]
+    dev = []
+    for h, st in zip(host, streams):
+        with torch.cuda.stream(st):  # the producer of each GMI's gradient runs on its own stream
+            t = torch.empty(n, dtype=torch.float64, device="cuda")
+            t.copy_(torch.from_numpy(h), non_blocking=False)
+            dev.append(t)
+    counts, cids = layout_arrays(mpl)
+    ptrs = (C.c_void_p * len(dev))(*[t.data_ptr() for t in dev])
+    sp = (C.c_void_p * len(streams))(*[st.cuda_stream for st in streams])
+    run = _lib.ReductionInfo()
+    _lib.call("gmi_allreduce", algo, len(mpl), (C.c_int * len(counts))(*counts), (C.c_int * len(cids))(*cids),
+              ptrs, n, 1, sp, 25e9, 12.5e9, C.byref(run))
+    outs = []
+    for t, st in zip(dev, streams):
+        with torch.cuda.stream(st):  # consumers on the GMI streams (no device-wide sync first)
+            outs.append((t * 1.0).cpu().numpy())
+    for o in outs:
+        assert np.array_equal(o.view(np.uint64), ref.view(np.uint64))
+    info = _lib.ReductionInfo()
+    _lib.call("gmi_reduction_schedule", algo, len(mpl), (C.c_int * len(counts))(*counts),
+              (C.c_int * len(cids))(*cids), n, 8.0, 25e9, 12.5e9, None, 0, C.byref(info))
+    assert (run.latency, run.broadcast_latency, run.trace_len) == (info.latency, info.broadcast_latency, info.trace_len)
